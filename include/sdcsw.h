@@ -1,0 +1,135 @@
+/*
+ * sdcsw.h - C ABI of libsdcsw.so, the B200 (sm_100a) hot path of parallel
+ * spectral deferred corrections (dSDC, MIN-SR-FLEX, IMEX) applied to rotating
+ * shallow water on the sphere in a spherical-harmonic discretisation.
+ *
+ * Plain C types only: device buffers are raw pointers the caller owns
+ * (e.g. torch.Tensor.data_ptr()), streams are cudaStream_t passed as void*.
+ * Every entry point returns an sdcsw_status and never throws; the message of
+ * the last failure on the calling thread is sdcsw_last_error().
+ *
+ * State layout (fixed): complex128 interleaved (re, im); one state is three
+ * fields (Phi', zeta, delta) of C = (T+1)(T+2)/2 coefficients each, triangular
+ * m-major: idx(m, n) = m (T+1) - m (m-1)/2 + (n - m).  A batch of nb states is
+ * nb consecutive states (stride 3 C complex).
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to the parsdc reference package, pkg/src/parsdc/).
+ */
+#ifndef SDCSW_H
+#define SDCSW_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SDCSW_OK = 0,
+  SDCSW_ERR_PARAM = 1,    /* -> ParameterError (errors.py:4) */
+  SDCSW_ERR_CUDA = 2,     /* launch / allocation failure -> DeviceError */
+  SDCSW_ERR_STATE = 3,    /* call on a destroyed or mismatched handle */
+  SDCSW_ERR_DIVERGED = 4  /* non-finite state -> DivergenceError (integrators.py:544-548) */
+} sdcsw_status;
+
+typedef struct sdcsw_plan sdcsw_plan;
+typedef struct sdcsw_stepper sdcsw_stepper;
+
+typedef struct {
+  int trunc;      /* spectral truncation T */
+  int nlat;       /* Gaussian latitudes (even) */
+  int nlon;       /* longitudes, 2^k or 3*2^k, >= 2T+2 */
+  int max_batch;  /* largest nb any call on this plan will use */
+  double radius;  /* a */
+  double omega;   /* rotation rate */
+  double phibar;  /* mean geopotential g*H */
+} sdcsw_config;
+
+/* Host-built constants uploaded once; the plan owns the device copies and the
+ * transform workspaces.  Tables are parity-sorted, padded rows:
+ * ptab/htab [rows][nlat/2], rowoff [T+2], n_even [T+1] (padded even-row count
+ * per m), row_n [rows] (degree n of each row, -1 = padding), lam [C]
+ * (n(n+1)/a^2), mu_north/w_north [nlat/2] (northern Gaussian nodes/weights,
+ * pole first).  Replaces the problem construction of the planar template
+ * (problems/swe.py:77-138) for the spherical problem the reference scopes out. */
+int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_north,
+                      const double* w_north, const double* ptab, const double* htab,
+                      const int* rowoff, const int* n_even, const int* row_n,
+                      const double* lam, sdcsw_plan** out);
+int sdcsw_plan_destroy(sdcsw_plan* plan);
+
+/* fe[b] = f_E(u[b]) for b < nb.  Replaces SplitProblem.f_expl (core.py:102-104)
+ * and the planar _f_expl (problems/swe.py:174-196). */
+int sdcsw_f_expl(sdcsw_plan* plan, const double* u, double* fe, int nb, void* stream);
+
+/* fi[b] = f_I(u[b]) = (-phibar delta, 0, lam Phi').  Replaces
+ * SplitProblem.f_impl (core.py:106-108) / problems/swe.py:157-163. */
+int sdcsw_f_impl(sdcsw_plan* plan, const double* u, double* fi, int nb, void* stream);
+
+/* u[b] solves u - alpha_b f_I(u) = beta[b]; coef is HOST memory [nb][3] =
+ * (alpha, alpha*phibar, alpha*alpha*phibar).  alpha == 0 copies beta.
+ * Replaces SplitProblem.implicit_solve (core.py:110-114) /
+ * problems/swe.py:165-172. */
+int sdcsw_implicit_solve(sdcsw_plan* plan, const double* coef, const double* beta, double* u,
+                         int nb, void* stream);
+
+/* Phase one + solve of one diagonal sweep for nodes [node_lo, node_lo+count):
+ *   F_j = fe_j + fi_j;  beta_m = u0 + sum_j w[m][j] F_j - wd[m] fi_m;
+ *   u_m = solve(alpha_m, beta_m);  fi_out_m = f_I(u_m).
+ * node_coef is HOST memory [M][M + 4] = (w[m][0..M-1], wd[m], alpha_m,
+ * alpha_m*phibar, alpha_m^2*phibar) with w = dt*q, wd = dt*d_m.  fe/fi are
+ * [M][3C] with element stride fe_stride/fi_stride states (0 = every node
+ * aliases the step-start slot, as after initialize_sweep, core.py:165-174);
+ * first != 0 means fi_j = f_I(u0) computed inline (fi ignored).  u_out and
+ * fi_out hold `count` states.  Replaces diagonal_sweep phase one plus the
+ * solve/f_I half of _refresh_node (integrators.py:233-288); f_E of u_out is a
+ * separate sdcsw_f_expl call.  Bit-identical to the reference arithmetic. */
+int sdcsw_sweep_nodes(sdcsw_plan* plan, int n_nodes, int node_lo, int count,
+                      const double* node_coef, const double* u0, const double* fe,
+                      long long fe_stride, const double* fi, long long fi_stride, int first,
+                      double* u_out, double* fi_out, void* stream);
+
+/* Closing last-node solve of a diagonal step (integrators.py:291-311):
+ *   beta = u0 + sum_j (w[j] fe_j + w[j] fi_j) - wd fi_last ; u_out = solve.
+ * final_coef is HOST memory [M + 4] = (w[0..M-1], wd, alpha, alpha*phibar,
+ * alpha^2*phibar).  u_out may alias u0. */
+int sdcsw_final_node(sdcsw_plan* plan, int n_nodes, const double* final_coef, const double* u0,
+                     const double* fe, long long fe_stride, const double* fi, long long fi_stride,
+                     int first, double* u_out, void* stream);
+
+/* Device-resident stepper owning all sweep storage and a CUDA graph of one
+ * step.  mode 0 = diagonal SDC (dsdc_step, integrators.py:347-381),
+ * mode 1 = serial SDC (sdc_step_serial, integrators.py:317-344).
+ * coef is HOST memory:
+ *   mode 0: [K-1][M][M+4] sweep node_coef blocks, then [M+4] final_coef;
+ *   mode 1: [M][M] w = dt*q, then [M] explicit correction weights dt*ew,
+ *           [M] implicit correction weights dt*dtau, [M][3] solve coefs. */
+int sdcsw_stepper_create(sdcsw_plan* plan, int mode, int n_nodes, int n_sweeps,
+                         const double* coef, int n_coef, sdcsw_stepper** out);
+int sdcsw_stepper_destroy(sdcsw_stepper* st);
+
+/* Advance the device state u (one state, in place) by n_steps steps on
+ * stream.  use_graph != 0 replays a captured CUDA graph per step.  The
+ * per-step finiteness check of integrate (integrators.py:538-548,
+ * core.py:42-50) runs on the device; read it with sdcsw_stepper_diverged. */
+int sdcsw_stepper_run(sdcsw_stepper* st, double* u, int n_steps, int use_graph, void* stream);
+
+/* First one-based step index (counted since the last reset) whose state was
+ * non-finite, or 0.  Synchronises the stepper's stream. */
+int sdcsw_stepper_diverged(sdcsw_stepper* st, int* step_index);
+int sdcsw_stepper_reset(sdcsw_stepper* st, void* stream);
+
+/* Number of kernels one step launches (for the bench's gpu_launches). */
+int sdcsw_stepper_launches_per_step(sdcsw_stepper* st, int* n);
+
+/* Any non-finite entry among n doubles -> *flag = 1 (device int).
+ * Replaces check_finite (core.py:42-50) without a host round trip. */
+int sdcsw_check_finite(const double* x, long long n, int* flag, void* stream);
+
+const char* sdcsw_last_error(void);
+int sdcsw_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SDCSW_H */

@@ -1,0 +1,121 @@
+"""ctypes binding of ``libsdcsw.so`` (declared in ``include/sdcsw.h``).
+
+The product path has no CPU fallback: if the library is missing or no CUDA
+device is visible, :func:`lib` raises :class:`DeviceError` immediately.
+"""
+
+import ctypes
+import os
+
+from .errors import DeviceError, DivergenceError, ParameterError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsdcsw.so")
+
+SDCSW_OK, SDCSW_ERR_PARAM, SDCSW_ERR_CUDA, SDCSW_ERR_STATE, SDCSW_ERR_DIVERGED = range(5)
+
+EXPORTS = (
+    "sdcsw_plan_create",
+    "sdcsw_plan_destroy",
+    "sdcsw_f_expl",
+    "sdcsw_f_impl",
+    "sdcsw_implicit_solve",
+    "sdcsw_sweep_nodes",
+    "sdcsw_final_node",
+    "sdcsw_stepper_create",
+    "sdcsw_stepper_destroy",
+    "sdcsw_stepper_run",
+    "sdcsw_stepper_diverged",
+    "sdcsw_stepper_reset",
+    "sdcsw_stepper_launches_per_step",
+    "sdcsw_check_finite",
+    "sdcsw_last_error",
+    "sdcsw_version",
+)
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("trunc", ctypes.c_int),
+        ("nlat", ctypes.c_int),
+        ("nlon", ctypes.c_int),
+        ("max_batch", ctypes.c_int),
+        ("radius", ctypes.c_double),
+        ("omega", ctypes.c_double),
+        ("phibar", ctypes.c_double),
+    ]
+
+
+_LIB = None
+_p = ctypes.c_void_p
+_i = ctypes.c_int
+_ll = ctypes.c_longlong
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int)
+
+_SIGS = {
+    "sdcsw_plan_create": [_i, ctypes.POINTER(Config), _dp, _dp, _dp, _dp, _ip, _ip, _ip, _dp,
+                          ctypes.POINTER(_p)],
+    "sdcsw_plan_destroy": [_p],
+    "sdcsw_f_expl": [_p, _p, _p, _i, _p],
+    "sdcsw_f_impl": [_p, _p, _p, _i, _p],
+    "sdcsw_implicit_solve": [_p, _dp, _p, _p, _i, _p],
+    "sdcsw_sweep_nodes": [_p, _i, _i, _i, _dp, _p, _p, _ll, _p, _ll, _i, _p, _p, _p],
+    "sdcsw_final_node": [_p, _i, _dp, _p, _p, _ll, _p, _ll, _i, _p, _p],
+    "sdcsw_stepper_create": [_p, _i, _i, _i, _dp, _i, ctypes.POINTER(_p)],
+    "sdcsw_stepper_destroy": [_p],
+    "sdcsw_stepper_run": [_p, _p, _i, _i, _p],
+    "sdcsw_stepper_diverged": [_p, _ip],
+    "sdcsw_stepper_reset": [_p, _p],
+    "sdcsw_stepper_launches_per_step": [_p, _ip],
+    "sdcsw_check_finite": [_p, _ll, _p, _p],
+    "sdcsw_last_error": [],
+    "sdcsw_version": [],
+}
+
+
+def load(path=LIB_PATH):
+    """Load the library and bind every exported symbol (no GPU needed)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise DeviceError(
+            f"{path} is not built; run `python -m paper_2403_20135_b200.build` "
+            "(the CUDA path has no CPU fallback)"
+        )
+    lib_ = ctypes.CDLL(path)
+    for name, args in _SIGS.items():
+        fn = getattr(lib_, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_char_p if name == "sdcsw_last_error" else ctypes.c_int
+    _LIB = lib_
+    return lib_
+
+
+def lib():
+    """The library, after checking that a CUDA device is usable."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device visible: the sdcsw path runs only on a B200 (sm_100a)")
+    return load()
+
+
+def check(status, what="sdcsw"):
+    if status == SDCSW_OK:
+        return
+    msg = (_LIB.sdcsw_last_error() or b"").decode() if _LIB is not None else ""
+    if status == SDCSW_ERR_PARAM:
+        raise ParameterError(f"{what}: {msg}")
+    if status == SDCSW_ERR_DIVERGED:
+        raise DivergenceError(f"{what}: {msg}", step_index=-1)
+    raise DeviceError(f"{what}: {msg}", code=status)
+
+
+def dptr(arr):
+    """ctypes double* of a C-contiguous float64 numpy array."""
+    return arr.ctypes.data_as(_dp)
+
+
+def iptr(arr):
+    return arr.ctypes.data_as(_ip)

@@ -1,0 +1,102 @@
+// Internal declarations shared by the libsdcsw.so translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+
+#include "../../include/sdcsw.h"
+
+namespace sdcsw {
+
+// Warp tile of the Legendre GEMMs: two m8 row tiles (16 rows) per warp.
+constexpr int kRowsPerWarp = 16;
+// Rows of the synthesis K-loop staged in shared memory per chunk.
+constexpr int kSynthChunk = 32;
+// Latitudes of the analysis K-loop staged per chunk.
+constexpr int kAnalChunk = 32;
+// Parity-sorted table rows are padded to a multiple of this (an m8 tile is
+// then always of a single parity class).
+constexpr int kRowPad = 8;
+
+// Analysis data slots written by the ring kernel per (batch, pair, m):
+// P-data: X_phi, X_zeta, X_delta, X_ke; H-data: Y_phi, Y_zeta, Y_delta.
+enum { kXPhi = 0, kXZeta, kXDelta, kXKe, kYPhi, kYZeta, kYDelta, kNumSlots };
+
+struct FftPlan {
+  int n;           // nlon
+  int nstages;     // number of radix passes
+  int radix[16];   // radices in application order
+};
+
+struct Plan {
+  int device;
+  int T, nlat, nlon, J, C, L;  // L = T+1 (Fourier modes kept)
+  int max_batch;
+  int rows;                    // packed table rows
+  double radius, omega, phibar;
+  // device constants
+  double* ptab;     // [rows][J]
+  double* htab;     // [rows][J]
+  int* rowoff;      // [T+2]
+  int* n_even;      // [T+1]
+  int* row_n;       // [rows]
+  int* moff;        // [T+2] triangular offsets
+  double* lam;      // [C]
+  double* inv_nn;   // [C] 1/(n(n+1)), 0 for n = 0
+  double* mu;       // [J] northern nodes
+  double* wsyn;     // [J] 2 pi w_j / (a (1 - mu_j^2))
+  double* wke;      // [J] 2 pi w_j
+  double2* twiddle; // [nlon] exp(-2 pi i k / nlon)
+  int* anal_work;   // [n_anal_work] (m << 16 | row block)
+  int n_anal_work;
+  int synth_warps, anal_warps;
+  FftPlan fft;
+  // workspaces
+  double2* fsyn;    // [max_batch][J][L][4][2]
+  double2* gan;     // [max_batch][J][L][kNumSlots][2]
+  double* coef_dev; // small per-call coefficient staging [kCoefCap]
+  int ring_threads;
+  size_t ring_smem;
+};
+constexpr int kCoefCap = 4096;
+
+// error plumbing
+void set_error(const std::string& msg);
+int cuda_status(cudaError_t e, const char* where);
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_synthesis(const Plan& p, const double2* u, int nb, cudaStream_t s,
+                             int* step_counter);
+cudaError_t launch_ring(const Plan& p, int nb, cudaStream_t s);
+cudaError_t launch_analysis(const Plan& p, double2* fe, int nb, cudaStream_t s);
+cudaError_t launch_f_impl(const Plan& p, const double2* u, double2* fi, int nb, cudaStream_t s);
+// coefficient pointers below are HOST memory; values travel as kernel parameters
+cudaError_t launch_solve(const Plan& p, const double* coef_host, const double2* beta, double2* u,
+                         int nb, cudaStream_t s);
+cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, const double* coef_host,
+                               const double2* u0, const double2* fe, long long fe_stride,
+                               const double2* fi, long long fi_stride, int first, double2* u_out,
+                               double2* fi_out, cudaStream_t s);
+cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, const double2* u0,
+                              const double2* fe, long long fe_stride, const double2* fi,
+                              long long fi_stride, int first, double2* u_out, int* diverged,
+                              const int* step_counter, cudaStream_t s);
+cudaError_t launch_serial_quad(const Plan& p, int M, const double* w_host, const double2* u0,
+                               const double2* fe, long long fe_stride, const double2* fi,
+                               long long fi_stride, int first, double2* quad, cudaStream_t s);
+cudaError_t launch_serial_node(const Plan& p, int M, int m, const double* coef_host,
+                               const double2* quad, const double2* corr, const double2* u0,
+                               const double2* fi_old, int first, double2* u_out, double2* u_out2,
+                               double2* fi_new, int* diverged, const int* step_counter,
+                               cudaStream_t s);
+cudaError_t launch_serial_update(const Plan& p, int m, double we, double wi, double2* corr,
+                                 const double2* fe_new, const double2* fe_old,
+                                 const double2* fi_new, const double2* fi_old, const double2* u0,
+                                 int first, cudaStream_t s);
+cudaError_t launch_check_finite(const double* x, long long n, int* flag, cudaStream_t s);
+
+// f_E = synthesis -> ring -> analysis
+cudaError_t f_expl(const Plan& p, const double2* u, double2* fe, int nb, cudaStream_t s,
+                   int* step_counter);
+
+}  // namespace sdcsw

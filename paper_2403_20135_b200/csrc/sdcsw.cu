@@ -1,0 +1,481 @@
+// C ABI of libsdcsw.so (declared in include/sdcsw.h): plan lifecycle, the
+// problem operations, the fused sweep operations and the device-resident
+// stepper that replays one captured CUDA graph per time step.
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace sdcsw {
+
+static thread_local std::string g_error;
+
+void set_error(const std::string& msg) { g_error = msg; }
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return SDCSW_OK;
+  set_error(std::string(where) + ": " + cudaGetErrorString(e));
+  return SDCSW_ERR_CUDA;
+}
+
+cudaError_t configure_ring(size_t smem);
+
+cudaError_t f_expl(const Plan& p, const double2* u, double2* fe, int nb, cudaStream_t s,
+                   int* step_counter) {
+  cudaError_t e = launch_synthesis(p, u, nb, s, step_counter);
+  if (e != cudaSuccess) return e;
+  e = launch_ring(p, nb, s);
+  if (e != cudaSuccess) return e;
+  return launch_analysis(p, fe, nb, s);
+}
+
+template <typename T>
+static cudaError_t upload(T** dst, const T* src, size_t n, size_t pad = 0) {
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), (n + pad) * sizeof(T));
+  if (e != cudaSuccess) return e;
+  if (pad) cudaMemset(*dst + n, 0, pad * sizeof(T));
+  if (n) e = cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+}  // namespace sdcsw
+
+using namespace sdcsw;
+
+struct sdcsw_plan {
+  Plan p;
+  bool alive;
+};
+
+struct sdcsw_stepper {
+  sdcsw_plan* plan;
+  int mode, M, K;
+  std::vector<double> coef;
+  double2* buf;  // all sweep storage in one allocation
+  size_t S;      // one state, in double2
+  double2 *fe0, *fe, *fi, *ustage, *quad, *corr, *feB, *fiB;
+  int* flags;    // [0] first diverged step (INT_MAX = none), [1] step counter
+  cudaStream_t cap;
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  double* graph_u;
+  int launches;
+};
+
+extern "C" {
+
+const char* sdcsw_last_error(void) { return g_error.c_str(); }
+int sdcsw_version(void) { return 1; }
+
+int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_north,
+                      const double* w_north, const double* ptab, const double* htab,
+                      const int* rowoff, const int* n_even, const int* row_n, const double* lam,
+                      sdcsw_plan** out) {
+  if (!cfg || !out || !mu_north || !w_north || !ptab || !htab || !rowoff || !n_even || !row_n ||
+      !lam) {
+    set_error("sdcsw_plan_create: null argument");
+    return SDCSW_ERR_PARAM;
+  }
+  const int T = cfg->trunc, nlat = cfg->nlat, nlon = cfg->nlon;
+  if (T < 1 || nlat % 2 || nlat < T + 1 || (nlat / 2) % 16 || nlon < 2 * T + 2 ||
+      cfg->max_batch < 1 || T > 4000) {
+    set_error("sdcsw_plan_create: unsupported size (need nlat/2 % 16 == 0, nlon >= 2T+2)");
+    return SDCSW_ERR_PARAM;
+  }
+  int k = nlon;
+  while (k % 2 == 0) k /= 2;
+  if (k != 1 && k != 3) {
+    set_error("sdcsw_plan_create: nlon must be 2^k or 3*2^k");
+    return SDCSW_ERR_PARAM;
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+  sdcsw_plan* h = new (std::nothrow) sdcsw_plan();
+  if (!h) {
+    set_error("out of host memory");
+    return SDCSW_ERR_PARAM;
+  }
+  std::memset(&h->p, 0, sizeof(Plan));
+  Plan& p = h->p;
+  p.device = device;
+  p.T = T; p.nlat = nlat; p.nlon = nlon; p.J = nlat / 2; p.L = T + 1;
+  p.C = (T + 1) * (T + 2) / 2;
+  p.max_batch = cfg->max_batch;
+  p.radius = cfg->radius; p.omega = cfg->omega; p.phibar = cfg->phibar;
+  p.rows = rowoff[T + 1];
+  const int J = p.J, C = p.C;
+
+  std::vector<int> moff(T + 2);
+  for (int m = 0; m <= T + 1; ++m) moff[m] = m * (T + 1) - m * (m - 1) / 2;
+  std::vector<double> inv_nn(C), wsyn(J), wke(J);
+  for (int m = 0; m <= T; ++m)
+    for (int n = m; n <= T; ++n) inv_nn[moff[m] + n - m] = n == 0 ? 0.0 : 1.0 / (double(n) * (n + 1.0));
+  const double twopi = 6.283185307179586476925286766559;
+  for (int j = 0; j < J; ++j) {
+    const double mu = mu_north[j];
+    wsyn[j] = twopi * w_north[j] / (p.radius * ((1.0 - mu) * (1.0 + mu)));
+    wke[j] = twopi * w_north[j];
+  }
+  std::vector<double2> tw(nlon);
+  for (int i = 0; i < nlon; ++i) {
+    const long double a = -2.0L * 3.14159265358979323846264338327950288L * (long double)i / nlon;
+    tw[i] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  // FFT radices: 4s, then a 2 if needed, then the 3
+  FftPlan fp;
+  std::memset(&fp, 0, sizeof(fp));
+  fp.n = nlon;
+  int rem = nlon, ns = 0;
+  bool three = rem % 3 == 0;
+  if (three) rem /= 3;
+  while (rem % 4 == 0) { fp.radix[ns++] = 4; rem /= 4; }
+  if (rem == 2) { fp.radix[ns++] = 2; rem = 1; }
+  if (three) fp.radix[ns++] = 3;
+  fp.nstages = ns;
+  p.fft = fp;
+  // analysis work list
+  std::vector<int> work;
+  p.anal_warps = 4;
+  for (int m = 0; m <= T; ++m) {
+    const int rows = rowoff[m + 1] - rowoff[m];
+    const int per = kRowsPerWarp * p.anal_warps;
+    for (int rb = 0; rb * per < rows; ++rb) work.push_back((m << 16) | rb);
+  }
+  p.n_anal_work = (int)work.size();
+  const int jt = J / kRowsPerWarp;
+  p.synth_warps = jt % 4 == 0 ? 4 : (jt % 3 == 0 ? 3 : (jt % 2 == 0 ? 2 : 1));
+  p.ring_threads = 256;
+  p.ring_smem = (size_t)nlon * (2 * sizeof(double2) + 8 * sizeof(double));
+
+  const size_t tab = (size_t)p.rows * J;
+  if ((e = upload(&p.ptab, ptab, tab, (size_t)16 * J)) != cudaSuccess ||
+      (e = upload(&p.htab, htab, tab, (size_t)16 * J)) != cudaSuccess ||
+      (e = upload(&p.rowoff, rowoff, (size_t)T + 2)) != cudaSuccess ||
+      (e = upload(&p.n_even, n_even, (size_t)T + 1)) != cudaSuccess ||
+      (e = upload(&p.row_n, row_n, (size_t)p.rows, 16)) != cudaSuccess ||
+      (e = upload(&p.moff, moff.data(), moff.size())) != cudaSuccess ||
+      (e = upload(&p.lam, lam, (size_t)C)) != cudaSuccess ||
+      (e = upload(&p.inv_nn, inv_nn.data(), inv_nn.size())) != cudaSuccess ||
+      (e = upload(&p.mu, mu_north, (size_t)J)) != cudaSuccess ||
+      (e = upload(&p.wsyn, wsyn.data(), wsyn.size())) != cudaSuccess ||
+      (e = upload(&p.wke, wke.data(), wke.size())) != cudaSuccess ||
+      (e = upload(&p.twiddle, tw.data(), tw.size())) != cudaSuccess ||
+      (e = upload(&p.anal_work, work.data(), work.size())) != cudaSuccess ||
+      (e = cudaMalloc(&p.fsyn, (size_t)p.max_batch * J * p.L * 8 * sizeof(double2))) != cudaSuccess ||
+      (e = cudaMalloc(&p.gan, (size_t)p.max_batch * J * p.L * kNumSlots * 2 * sizeof(double2))) !=
+          cudaSuccess ||
+      (e = cudaMalloc(&p.coef_dev, kCoefCap * sizeof(double))) != cudaSuccess ||
+      (e = configure_ring(p.ring_smem)) != cudaSuccess ||
+      (e = cudaDeviceSynchronize()) != cudaSuccess) {
+    int st = cuda_status(e, "sdcsw_plan_create");
+    void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
+                    p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+    delete h;
+    return st;
+  }
+  h->alive = true;
+  *out = h;
+  return SDCSW_OK;
+}
+
+int sdcsw_plan_destroy(sdcsw_plan* h) {
+  if (!h || !h->alive) {
+    set_error("sdcsw_plan_destroy: invalid handle");
+    return SDCSW_ERR_STATE;
+  }
+  cudaSetDevice(h->p.device);
+  cudaDeviceSynchronize();
+  Plan& p = h->p;
+  void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
+                  p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  h->alive = false;
+  delete h;
+  return SDCSW_OK;
+}
+
+static int check_plan(sdcsw_plan* h, int nb, const char* where) {
+  if (!h || !h->alive) {
+    set_error(std::string(where) + ": invalid plan handle");
+    return SDCSW_ERR_STATE;
+  }
+  if (nb < 0 || nb > h->p.max_batch) {
+    set_error(std::string(where) + ": batch exceeds plan max_batch");
+    return SDCSW_ERR_PARAM;
+  }
+  return SDCSW_OK;
+}
+
+int sdcsw_f_expl(sdcsw_plan* h, const double* u, double* fe, int nb, void* stream) {
+  int st = check_plan(h, nb, "sdcsw_f_expl");
+  if (st) return st;
+  if (nb == 0) return SDCSW_OK;
+  return cuda_status(f_expl(h->p, (const double2*)u, (double2*)fe, nb, (cudaStream_t)stream, nullptr),
+                     "sdcsw_f_expl");
+}
+
+int sdcsw_f_impl(sdcsw_plan* h, const double* u, double* fi, int nb, void* stream) {
+  int st = check_plan(h, 1, "sdcsw_f_impl");
+  if (st) return st;
+  if (nb < 0) return SDCSW_ERR_PARAM;
+  if (nb == 0) return SDCSW_OK;
+  return cuda_status(launch_f_impl(h->p, (const double2*)u, (double2*)fi, nb, (cudaStream_t)stream),
+                     "sdcsw_f_impl");
+}
+
+int sdcsw_implicit_solve(sdcsw_plan* h, const double* coef, const double* beta, double* u, int nb,
+                         void* stream) {
+  int st = check_plan(h, 1, "sdcsw_implicit_solve");
+  if (st) return st;
+  if (nb < 0 || !coef) return SDCSW_ERR_PARAM;
+  if (nb == 0) return SDCSW_OK;
+  return cuda_status(launch_solve(h->p, coef, (const double2*)beta, (double2*)u, nb,
+                                  (cudaStream_t)stream),
+                     "sdcsw_implicit_solve");
+}
+
+int sdcsw_sweep_nodes(sdcsw_plan* h, int n_nodes, int node_lo, int count, const double* node_coef,
+                      const double* u0, const double* fe, long long fe_stride, const double* fi,
+                      long long fi_stride, int first, double* u_out, double* fi_out, void* stream) {
+  int st = check_plan(h, 1, "sdcsw_sweep_nodes");
+  if (st) return st;
+  if (n_nodes < 1 || n_nodes > 16 || node_lo < 0 || count < 0 || node_lo + count > n_nodes ||
+      !node_coef) {
+    set_error("sdcsw_sweep_nodes: bad node range");
+    return SDCSW_ERR_PARAM;
+  }
+  if (count == 0) return SDCSW_OK;
+  return cuda_status(launch_sweep_nodes(h->p, n_nodes, node_lo, count, node_coef,
+                                        (const double2*)u0, (const double2*)fe, fe_stride,
+                                        (const double2*)fi, fi_stride, first, (double2*)u_out,
+                                        (double2*)fi_out, (cudaStream_t)stream),
+                     "sdcsw_sweep_nodes");
+}
+
+int sdcsw_final_node(sdcsw_plan* h, int n_nodes, const double* final_coef, const double* u0,
+                     const double* fe, long long fe_stride, const double* fi, long long fi_stride,
+                     int first, double* u_out, void* stream) {
+  int st = check_plan(h, 1, "sdcsw_final_node");
+  if (st) return st;
+  if (n_nodes < 1 || n_nodes > 16 || !final_coef) return SDCSW_ERR_PARAM;
+  return cuda_status(launch_final_node(h->p, n_nodes, final_coef, (const double2*)u0,
+                                       (const double2*)fe, fe_stride, (const double2*)fi, fi_stride,
+                                       first, (double2*)u_out, nullptr, nullptr,
+                                       (cudaStream_t)stream),
+                     "sdcsw_final_node");
+}
+
+int sdcsw_check_finite(const double* x, long long n, int* flag, void* stream) {
+  if (n < 0 || !flag) return SDCSW_ERR_PARAM;
+  if (n == 0) return SDCSW_OK;
+  return cuda_status(launch_check_finite(x, n, flag, (cudaStream_t)stream), "sdcsw_check_finite");
+}
+
+// ---------------------------------------------------------------------------
+// stepper
+// ---------------------------------------------------------------------------
+static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
+  const Plan& p = st->plan->p;
+  const int M = st->M, K = st->K;
+  const size_t S = st->S;
+  int* diverged = st->flags;
+  int* counter = st->flags + 1;
+  cudaError_t e = f_expl(p, u, st->fe0, 1, s, counter);
+  if (e != cudaSuccess) return e;
+  if (st->mode == 0) {
+    const int cstride = M * (M + 4);
+    for (int k = 1; k < K; ++k) {
+      const bool first = k == 1;
+      e = launch_sweep_nodes(p, M, 0, M, st->coef.data() + (size_t)(k - 1) * cstride, u,
+                             first ? st->fe0 : st->fe, first ? 0 : 1, st->fi, first ? 0 : 1,
+                             first, st->ustage, st->fi, s);
+      if (e != cudaSuccess) return e;
+      e = f_expl(p, st->ustage, st->fe, M, s, nullptr);
+      if (e != cudaSuccess) return e;
+    }
+    const bool first = K == 1;
+    return launch_final_node(p, M, st->coef.data() + (size_t)(K - 1) * cstride, u,
+                             first ? st->fe0 : st->fe, first ? 0 : 1, st->fi, first ? 0 : 1,
+                             first, u, diverged, counter, s);
+  }
+  // serial SDC: old/new tendency buffers alternate between sweeps
+  const double* W = st->coef.data();
+  const double* we = W + M * M;
+  const double* wi = we + M;
+  const double* sc = wi + M;
+  double2* old_fe = st->fe0;
+  double2* old_fi = st->fi;
+  long long old_stride = 0;
+  int first = 1;
+  for (int k = 1; k <= K; ++k) {
+    double2* nfe = (k % 2) ? st->fe : st->feB;
+    double2* nfi = (k % 2) ? st->fi : st->fiB;
+    e = launch_serial_quad(p, M, W, u, old_fe, old_stride, old_fi, old_stride, first, st->quad, s);
+    if (e != cudaSuccess) return e;
+    for (int m = 0; m < M; ++m) {
+      const bool last = (k == K && m == M - 1);
+      e = launch_serial_node(p, M, m, sc + 3 * m, st->quad + m * S, st->corr, u,
+                             old_fi + old_stride * m * S, first, st->ustage, last ? u : nullptr,
+                             nfi + m * S, last ? diverged : nullptr, last ? counter : nullptr, s);
+      if (e != cudaSuccess) return e;
+      e = f_expl(p, st->ustage, nfe + m * S, 1, s, nullptr);
+      if (e != cudaSuccess) return e;
+      if (m + 1 < M) {
+        e = launch_serial_update(p, m, we[m], wi[m], st->corr, nfe + m * S,
+                                 old_fe + old_stride * m * S, nfi + m * S,
+                                 old_fi + old_stride * m * S, u, first, s);
+        if (e != cudaSuccess) return e;
+      }
+    }
+    old_fe = nfe;
+    old_fi = nfi;
+    old_stride = 1;
+    first = 0;
+  }
+  return cudaSuccess;
+}
+
+int sdcsw_stepper_create(sdcsw_plan* h, int mode, int n_nodes, int n_sweeps, const double* coef,
+                         int n_coef, sdcsw_stepper** out) {
+  int st = check_plan(h, 1, "sdcsw_stepper_create");
+  if (st) return st;
+  const int M = n_nodes, K = n_sweeps;
+  if ((mode != 0 && mode != 1) || M < 1 || M > 16 || K < 1 || !coef || !out) {
+    set_error("sdcsw_stepper_create: bad mode / node / sweep count");
+    return SDCSW_ERR_PARAM;
+  }
+  const int want = mode == 0 ? K * M * (M + 4) : M * M + 2 * M + 3 * M;
+  const int need = mode == 0 ? (K - 1) * M * (M + 4) + (M + 4) : want;
+  if (n_coef < need) {
+    set_error("sdcsw_stepper_create: coefficient array too short");
+    return SDCSW_ERR_PARAM;
+  }
+  if (mode == 0 && M > h->p.max_batch) {
+    set_error("sdcsw_stepper_create: plan max_batch < node count");
+    return SDCSW_ERR_PARAM;
+  }
+  sdcsw_stepper* s = new (std::nothrow) sdcsw_stepper();
+  if (!s) return SDCSW_ERR_PARAM;
+  s->plan = h; s->mode = mode; s->M = M; s->K = K;
+  s->coef.assign(coef, coef + need);
+  if (mode == 0) {
+    // pad: final block stored at index K-1
+    s->coef.resize((size_t)K * M * (M + 4), 0.0);
+    const size_t fin = (size_t)(K - 1) * M * (M + 4);
+    std::vector<double> tail(coef + (size_t)(K - 1) * M * (M + 4), coef + need);
+    for (size_t q = 0; q < tail.size(); ++q) s->coef[fin + q] = tail[q];
+  }
+  const Plan& p = h->p;
+  s->S = (size_t)3 * p.C;
+  const size_t nstates = 1 + 3 * (size_t)M + (mode == 1 ? (size_t)3 * M + 1 : 0);
+  cudaError_t e = cudaSetDevice(p.device);
+  if (e == cudaSuccess) e = cudaMalloc(&s->buf, nstates * s->S * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc(&s->flags, 2 * sizeof(int));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    if (s->buf) cudaFree(s->buf);
+    if (s->flags) cudaFree(s->flags);
+    delete s;
+    return cuda_status(e, "sdcsw_stepper_create");
+  }
+  cudaMemset(s->buf, 0, nstates * s->S * sizeof(double2));
+  double2* q = s->buf;
+  s->fe0 = q; q += s->S;
+  s->fe = q; q += M * s->S;
+  s->fi = q; q += M * s->S;
+  s->ustage = q; q += M * s->S;
+  if (mode == 1) {
+    s->quad = q; q += M * s->S;
+    s->feB = q; q += M * s->S;
+    s->fiB = q; q += M * s->S;
+    s->corr = q; q += s->S;
+  }
+  const int init[2] = {INT_MAX, 0};
+  cudaMemcpy(s->flags, init, sizeof(init), cudaMemcpyHostToDevice);
+  s->launches = mode == 0 ? 4 * K : 3 + K * 5 * M;
+  *out = s;
+  return SDCSW_OK;
+}
+
+int sdcsw_stepper_destroy(sdcsw_stepper* s) {
+  if (!s) return SDCSW_ERR_STATE;
+  cudaSetDevice(s->plan->p.device);
+  cudaDeviceSynchronize();
+  if (s->exec) cudaGraphExecDestroy(s->exec);
+  if (s->graph) cudaGraphDestroy(s->graph);
+  cudaStreamDestroy(s->cap);
+  cudaFree(s->buf);
+  cudaFree(s->flags);
+  delete s;
+  return SDCSW_OK;
+}
+
+int sdcsw_stepper_reset(sdcsw_stepper* s, void* stream) {
+  if (!s) return SDCSW_ERR_STATE;
+  const int init[2] = {INT_MAX, 0};
+  return cuda_status(cudaMemcpyAsync(s->flags, init, sizeof(init), cudaMemcpyHostToDevice,
+                                     (cudaStream_t)stream),
+                     "sdcsw_stepper_reset");
+}
+
+int sdcsw_stepper_launches_per_step(sdcsw_stepper* s, int* n) {
+  if (!s || !n) return SDCSW_ERR_STATE;
+  *n = s->launches;
+  return SDCSW_OK;
+}
+
+int sdcsw_stepper_run(sdcsw_stepper* s, double* u, int n_steps, int use_graph, void* stream) {
+  if (!s || !u) {
+    set_error("sdcsw_stepper_run: invalid handle or state");
+    return SDCSW_ERR_STATE;
+  }
+  if (n_steps < 0) return SDCSW_ERR_PARAM;
+  cudaStream_t cs = (cudaStream_t)stream;
+  cudaError_t e = cudaSetDevice(s->plan->p.device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+  if (!use_graph) {
+    for (int i = 0; i < n_steps; ++i) {
+      e = enqueue_step(s, (double2*)u, cs);
+      if (e != cudaSuccess) return cuda_status(e, "sdcsw_stepper_run");
+    }
+    return SDCSW_OK;
+  }
+  if (!s->exec || s->graph_u != u) {
+    if (s->exec) { cudaGraphExecDestroy(s->exec); s->exec = nullptr; }
+    if (s->graph) { cudaGraphDestroy(s->graph); s->graph = nullptr; }
+    e = cudaStreamBeginCapture(s->cap, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_status(e, "cudaStreamBeginCapture");
+    cudaError_t le = enqueue_step(s, (double2*)u, s->cap);
+    e = cudaStreamEndCapture(s->cap, &s->graph);
+    if (le != cudaSuccess) return cuda_status(le, "capture step");
+    if (e != cudaSuccess) return cuda_status(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&s->exec, s->graph, 0);
+    if (e != cudaSuccess) return cuda_status(e, "cudaGraphInstantiate");
+    s->graph_u = u;
+  }
+  for (int i = 0; i < n_steps; ++i) {
+    e = cudaGraphLaunch(s->exec, cs);
+    if (e != cudaSuccess) return cuda_status(e, "cudaGraphLaunch");
+  }
+  return SDCSW_OK;
+}
+
+int sdcsw_stepper_diverged(sdcsw_stepper* s, int* step_index) {
+  if (!s || !step_index) return SDCSW_ERR_STATE;
+  int v[2];
+  cudaSetDevice(s->plan->p.device);
+  cudaDeviceSynchronize();
+  cudaError_t e = cudaMemcpy(v, s->flags, sizeof(v), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_status(e, "sdcsw_stepper_diverged");
+  *step_index = v[0] == INT_MAX ? 0 : v[0];
+  return SDCSW_OK;
+}
+
+}  // extern "C"
