@@ -121,6 +121,20 @@ int sdcsw_stepper_reset(sdcsw_stepper* st, void* stream);
 /* Number of kernels one step launches (for the bench's gpu_launches). */
 int sdcsw_stepper_launches_per_step(sdcsw_stepper* st, int* n);
 
+/* One stage of f_E on the plan's internal workspaces, for per-kernel timing
+ * and stage-level parity tests: stage 0 = Legendre synthesis (u -> Fourier
+ * workspace), 1 = ring FFT + products (Fourier -> analysis workspace),
+ * 2 = Legendre analysis (analysis workspace -> out).  `in`/`out` are
+ * ignored where the stage reads/writes a workspace.  sdcsw_f_expl is the
+ * three stages back to back. */
+int sdcsw_transform_stage(sdcsw_plan* plan, int stage, const double* in, double* out, int nb,
+                          void* stream);
+
+/* Device pointers and sizes of the internal workspaces: which 0 = Fourier
+ * coefficients [max_batch][nlat/2][T+1][4 (U,V,zeta,Phi)][2 (N,S)] complex,
+ * which 1 = analysis data [max_batch][nlat/2][T+1][7][2 (N+S, N-S)] complex. */
+int sdcsw_workspace(sdcsw_plan* plan, int which, void** ptr, long long* bytes);
+
 /* Any non-finite entry among n doubles -> *flag = 1 (device int).
  * Replaces check_finite (core.py:42-50) without a host round trip. */
 int sdcsw_check_finite(const double* x, long long n, int* flag, void* stream);

@@ -28,6 +28,8 @@ EXPORTS = (
     "sdcsw_stepper_reset",
     "sdcsw_stepper_launches_per_step",
     "sdcsw_check_finite",
+    "sdcsw_transform_stage",
+    "sdcsw_workspace",
     "sdcsw_last_error",
     "sdcsw_version",
 )
@@ -68,6 +70,8 @@ _SIGS = {
     "sdcsw_stepper_reset": [_p, _p],
     "sdcsw_stepper_launches_per_step": [_p, _ip],
     "sdcsw_check_finite": [_p, _ll, _p, _p],
+    "sdcsw_transform_stage": [_p, _i, _p, _p, _i, _p],
+    "sdcsw_workspace": [_p, _i, ctypes.POINTER(_p), ctypes.POINTER(_ll)],
     "sdcsw_last_error": [],
     "sdcsw_version": [],
 }

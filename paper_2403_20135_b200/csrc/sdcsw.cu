@@ -272,6 +272,32 @@ int sdcsw_final_node(sdcsw_plan* h, int n_nodes, const double* final_coef, const
                      "sdcsw_final_node");
 }
 
+int sdcsw_transform_stage(sdcsw_plan* h, int stage, const double* in, double* out, int nb,
+                          void* stream) {
+  int st = check_plan(h, nb, "sdcsw_transform_stage");
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  switch (stage) {
+    case 0: e = launch_synthesis(h->p, (const double2*)in, nb, s, nullptr); break;
+    case 1: e = launch_ring(h->p, nb, s); break;
+    case 2: e = launch_analysis(h->p, (double2*)out, nb, s); break;
+    default: set_error("sdcsw_transform_stage: stage must be 0, 1 or 2"); return SDCSW_ERR_PARAM;
+  }
+  return cuda_status(e, "sdcsw_transform_stage");
+}
+
+int sdcsw_workspace(sdcsw_plan* h, int which, void** ptr, long long* bytes) {
+  int st = check_plan(h, 1, "sdcsw_workspace");
+  if (st) return st;
+  if (!ptr || !bytes || which < 0 || which > 1) return SDCSW_ERR_PARAM;
+  const Plan& p = h->p;
+  const long long per = (long long)p.max_batch * p.J * p.L * 2 * sizeof(double2);
+  *ptr = which == 0 ? (void*)p.fsyn : (void*)p.gan;
+  *bytes = which == 0 ? per * 4 : per * kNumSlots;
+  return SDCSW_OK;
+}
+
 int sdcsw_check_finite(const double* x, long long n, int* flag, void* stream) {
   if (n < 0 || !flag) return SDCSW_ERR_PARAM;
   if (n == 0) return SDCSW_OK;
