@@ -80,7 +80,8 @@ int sdcsw_implicit_solve(sdcsw_plan* plan, const double* coef, const double* bet
  * [M][3C] with element stride fe_stride/fi_stride states (0 = every node
  * aliases the step-start slot, as after initialize_sweep, core.py:165-174);
  * first != 0 means fi_j = f_I(u0) computed inline (fi ignored).  u_out and
- * fi_out hold `count` states.  Replaces diagonal_sweep phase one plus the
+ * fi_out hold `count` states; neither may alias u0, fe or fi (nodes are
+ * updated concurrently).  Replaces diagonal_sweep phase one plus the
  * solve/f_I half of _refresh_node (integrators.py:233-288); f_E of u_out is a
  * separate sdcsw_f_expl call.  Bit-identical to the reference arithmetic. */
 int sdcsw_sweep_nodes(sdcsw_plan* plan, int n_nodes, int node_lo, int count,
@@ -132,7 +133,7 @@ int sdcsw_transform_stage(sdcsw_plan* plan, int stage, const double* in, double*
 
 /* Device pointers and sizes of the internal workspaces: which 0 = Fourier
  * coefficients [max_batch][nlat/2][T+1][4 (U,V,zeta,Phi)][2 (N,S)] complex,
- * which 1 = analysis data [max_batch][nlat/2][T+1][7][2 (N+S, N-S)] complex. */
+ * which 1 = analysis data [max_batch][T+1][nlat/2][2 (N+S, N-S)][7] complex. */
 int sdcsw_workspace(sdcsw_plan* plan, int which, void** ptr, long long* bytes);
 
 /* Any non-finite entry among n doubles -> *flag = 1 (device int).

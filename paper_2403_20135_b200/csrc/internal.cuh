@@ -49,11 +49,11 @@ struct Plan {
   double2* twiddle; // [nlon] exp(-2 pi i k / nlon)
   int* anal_work;   // [n_anal_work] (m << 16 | row block)
   int n_anal_work;
-  int synth_warps, anal_warps;
+  int synth_wj, anal_wj;  // row tiles per CTA (the other warps split K)
   FftPlan fft;
   // workspaces
   double2* fsyn;    // [max_batch][J][L][4][2]
-  double2* gan;     // [max_batch][J][L][kNumSlots][2]
+  double2* gan;     // [max_batch][L][J][2 (S,A)][kNumSlots]  (GEMM-ready for the analysis)
   double* coef_dev; // small per-call coefficient staging [kCoefCap]
   int ring_threads;
   size_t ring_smem;

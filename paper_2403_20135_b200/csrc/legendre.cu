@@ -25,30 +25,40 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// Both GEMMs: a CTA of kWarps warps = WJ output row tiles (16 rows each) x
+// WK K-splits (WJ * WK = kWarps, chosen per plan: many K-splits for small
+// truncations so enough warps are in flight, many row tiles for large ones
+// so the B operand is reused through L1).  A fragments (tables) and B
+// fragments (coefficients / analysis data) are loaded straight from global
+// memory; the K loop has no shared-memory staging and no barriers, and is
+// unrolled so its loads are issued ahead of the DMMAs.  CTAs are launched
+// m-major, so all CTAs of one wavenumber run together and its B slice stays
+// in L2.  Partial sums of the K-splits are reduced in shared memory in a
+// fixed order (deterministic).
+constexpr int kWarps = 4;
+
 // ---------------------------------------------------------------------------
 // synthesis: u [nb][3][C] -> fsyn [nb][J][L][4 (U,V,zeta,Phi)][2 (N,S)]
-// grid (T+1, J / (16 warps), ceil(nb / NB)), block 32*warps
+// grid (J / (16 WJ), T+1, ceil(nb/NB)), block 32*kWarps
+// P columns: (U,V) of all b (4 NB), then (zeta,Phi) of all b; H columns: (U,V).
 // ---------------------------------------------------------------------------
 template <int NB>
-__global__ void __launch_bounds__(128) k_synthesis(
+__global__ void __launch_bounds__(32 * kWarps) k_synthesis(
     const double2* __restrict__ u, int nb, int T, int J, int C, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, const int* __restrict__ row_n, const int* __restrict__ moff,
     const double* __restrict__ inv_nn, double radius, double2* __restrict__ fsyn,
-    int* step_counter) {
-  constexpr int PC = 8 * NB;        // P columns: (U,V) of all b, then (zeta,Phi) of all b
-  constexpr int TH = (NB + 1) / 2;  // H tiles (U,V columns only)
-  constexpr int HC = 8 * TH;
-  constexpr int PS = PC + 4;        // strides = 4 or 12 (mod 16): conflict-free B fragments
-  constexpr int HS = HC + 4;
-  __shared__ double xp[kSynthChunk * PS];
-  __shared__ double xh[kSynthChunk * HS];
+    int* step_counter, int WJ) {
+  constexpr int TH = (NB + 1) / 2;  // H tiles
+  constexpr int NACC = 2 * NB * 4;  // doubles per lane (E and O, re and im)
+  __shared__ double red[kWarps * 32 * NACC];
 
-  const int m = blockIdx.x;
-  const int warps = blockDim.x >> 5;
+  const int m = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int j0 = (blockIdx.y * warps + warp) * kRowsPerWarp;
+  const int WK = kWarps / WJ;
+  const int jt = warp % WJ, ks = warp / WJ;
+  const int j0 = (blockIdx.x * WJ + jt) * kRowsPerWarp;
   const int b0 = blockIdx.z * NB;
   const int L = T + 1;
   if (step_counter != nullptr && (blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0)
@@ -62,77 +72,97 @@ __global__ void __launch_bounds__(128) k_synthesis(
   const double* H = htab + (size_t)r0m * J + j0 + g;
   const double dm = (double)m;
 
+  // this lane's B columns: P tile c holds column 8c + g
+  int pb[NB], pf[NB], pr[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    const int col = 8 * c + g;
+    if (col < 4 * NB) { pb[c] = col >> 2; pf[c] = (col & 3) >> 1; }      // 0 = U, 1 = V
+    else { pb[c] = (col - 4 * NB) >> 2; pf[c] = 2 + (((col - 4 * NB) & 3) >> 1); }  // zeta, Phi
+    pr[c] = col & 1;
+  }
+  const double2* ub[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    const int bb = b0 + pb[c] < nb ? b0 + pb[c] : -1;
+    ub[c] = bb >= 0 ? u + (size_t)bb * 3 * C + mo - m : nullptr;
+  }
+
   double accE[2][NB][2], accO[2][NB][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int c = 0; c < NB; ++c) accE[a][c][0] = accE[a][c][1] = accO[a][c][0] = accO[a][c][1] = 0.0;
 
-  for (int c0 = 0; c0 < rows; c0 += kSynthChunk) {
-    const int nr = min(kSynthChunk, rows - c0);
-    __syncthreads();
-    // stage X (P data) and Y (H data) for rows [c0, c0+nr), batch columns
-    for (int it = threadIdx.x; it < kSynthChunk * 2 * TH; it += blockDim.x) {
-      const int rr = it / (2 * TH), b = it % (2 * TH);
-      double2 uu = {0, 0}, vv = {0, 0}, zz = {0, 0}, pp = {0, 0}, uh = {0, 0}, vh = {0, 0};
-      const int n = rr < nr ? row_n[r0m + c0 + rr] : -1;
-      if (n >= 0 && b < NB && b0 + b < nb) {
-        const int idx = mo + n - m;
-        const double2* s = u + (size_t)(b0 + b) * 3 * C;
-        const double2 phi = s[idx], zeta = s[C + idx], delta = s[2 * C + idx];
-        const double il = inv_nn[idx];
-        const double sm = dm * radius * il;  // i m chi / a = -i m a il delta
-        const double sa = radius * il;
-        uu = make_double2(sm * delta.y, -sm * delta.x);
-        vv = make_double2(sm * zeta.y, -sm * zeta.x);
-        zz = zeta;
-        pp = phi;
-        uh = make_double2(sa * zeta.x, sa * zeta.y);     // -psi / a
-        vh = make_double2(-sa * delta.x, -sa * delta.y);  // chi / a
-      }
-      double* rp = xp + rr * PS;
-      double* rh = xh + rr * HS;
-      if (b < NB) {
-        rp[4 * b + 0] = uu.x; rp[4 * b + 1] = uu.y; rp[4 * b + 2] = vv.x; rp[4 * b + 3] = vv.y;
-        rp[4 * NB + 4 * b + 0] = zz.x; rp[4 * NB + 4 * b + 1] = zz.y;
-        rp[4 * NB + 4 * b + 2] = pp.x; rp[4 * NB + 4 * b + 3] = pp.y;
-      }
-      rh[4 * b + 0] = uh.x; rh[4 * b + 1] = uh.y; rh[4 * b + 2] = vh.x; rh[4 * b + 3] = vh.y;
-    }
-    __syncthreads();
-    if (j0 < J) {
-      const int nsteps = nr >> 2;
-      for (int s = 0; s < nsteps; ++s) {
-        const int r = c0 + 4 * s;
-        const size_t off = (size_t)(r + t) * J;
-        double aP[2], aH[2];
-        aP[0] = __ldg(P + off);
-        aP[1] = __ldg(P + off + 8);
-        aH[0] = __ldg(H + off);
-        aH[1] = __ldg(H + off + 8);
-        double bP[NB], bH[TH];
+  const int nsteps = rows >> 2;
+#pragma unroll 4
+  for (int s = ks; s < nsteps; s += WK) {
+    const int r = 4 * s;
+    const size_t off = (size_t)(r + t) * J;
+    const double aP0 = __ldg(P + off), aP1 = __ldg(P + off + 8);
+    const double aH0 = __ldg(H + off), aH1 = __ldg(H + off + 8);
+    const int n = __ldg(row_n + r0m + r + t);
+    double bP[NB], bH[TH];
 #pragma unroll
-        for (int c = 0; c < NB; ++c) bP[c] = xp[(4 * s + t) * PS + 8 * c + g];
-#pragma unroll
-        for (int c = 0; c < TH; ++c) bH[c] = xh[(4 * s + t) * HS + 8 * c + g];
-        if (r < le) {
-#pragma unroll
-          for (int a = 0; a < 2; ++a) {
-#pragma unroll
-            for (int c = 0; c < NB; ++c) dmma(accE[a][c], aP[a], bP[c]);
-#pragma unroll
-            for (int c = 0; c < TH; ++c) dmma(accO[a][c], aH[a], bH[c]);
-          }
+    for (int c = 0; c < NB; ++c) {
+      double x = 0.0, y = 0.0;
+      if (n >= 0 && ub[c] != nullptr) {
+        const double il = __ldg(inv_nn + mo + n - m);
+        const double2* s3 = ub[c] + n;
+        const int f = pf[c];
+        if (f == 0) {  // U: P part i m chi / a = -i m a il delta ; H part -psi/a = a il zeta
+          const double2 d = s3[2 * C];
+          const double sm = dm * radius * il;
+          x = pr[c] ? -sm * d.x : sm * d.y;
+          if (c < TH) { const double2 z = s3[C]; y = radius * il * (pr[c] ? z.y : z.x); }
+        } else if (f == 1) {  // V: P part i m psi / a ; H part chi / a = -a il delta
+          const double2 z = s3[C];
+          const double sm = dm * radius * il;
+          x = pr[c] ? -sm * z.x : sm * z.y;
+          if (c < TH) { const double2 d = s3[2 * C]; y = -radius * il * (pr[c] ? d.y : d.x); }
         } else {
-#pragma unroll
-          for (int a = 0; a < 2; ++a) {
-#pragma unroll
-            for (int c = 0; c < NB; ++c) dmma(accO[a][c], aP[a], bP[c]);
-#pragma unroll
-            for (int c = 0; c < TH; ++c) dmma(accE[a][c], aH[a], bH[c]);
-          }
+          const double2 v = f == 2 ? s3[C] : s3[0];
+          x = pr[c] ? v.y : v.x;
         }
       }
+      bP[c] = x;
+      if (c < TH) bH[c] = y;
+    }
+    if (r < le) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) { dmma(accE[0][c], aP0, bP[c]); dmma(accE[1][c], aP1, bP[c]); }
+#pragma unroll
+      for (int c = 0; c < TH; ++c) { dmma(accO[0][c], aH0, bH[c]); dmma(accO[1][c], aH1, bH[c]); }
+    } else {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) { dmma(accO[0][c], aP0, bP[c]); dmma(accO[1][c], aP1, bP[c]); }
+#pragma unroll
+      for (int c = 0; c < TH; ++c) { dmma(accE[0][c], aH0, bH[c]); dmma(accE[1][c], aH1, bH[c]); }
+    }
+  }
+  // fixed-order reduction over the K-splits of each row tile
+  if (WK > 1) {
+    double* d = red + (warp * 32 + lane) * NACC;
+    int q = 0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        d[q++] = accE[a][c][0]; d[q++] = accE[a][c][1];
+        d[q++] = accO[a][c][0]; d[q++] = accO[a][c][1];
+      }
+    __syncthreads();
+    if (ks != 0) return;
+    for (int w = 1; w < WK; ++w) {
+      const double* e = red + ((w * WJ + jt) * 32 + lane) * NACC;
+      int qq = 0;
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          accE[a][c][0] += e[qq++]; accE[a][c][1] += e[qq++];
+          accO[a][c][0] += e[qq++]; accO[a][c][1] += e[qq++];
+        }
     }
   }
   if (j0 >= J) return;
@@ -143,10 +173,10 @@ __global__ void __launch_bounds__(128) k_synthesis(
     int b, f;
     if (col < 4 * NB) {
       b = col >> 2;
-      f = (col & 3) >> 1;  // 0 = U, 1 = V
+      f = (col & 3) >> 1;
     } else {
       b = (col - 4 * NB) >> 2;
-      f = 2 + (((col - 4 * NB) & 3) >> 1);  // 2 = zeta, 3 = Phi
+      f = 2 + (((col - 4 * NB) & 3) >> 1);
     }
     if (b0 + b >= nb) continue;
 #pragma unroll
@@ -160,41 +190,65 @@ __global__ void __launch_bounds__(128) k_synthesis(
 }
 
 // ---------------------------------------------------------------------------
-// analysis: gan [nb][J][L][7][2 (S,A)] -> fe [nb][3][C]
-// grid (n_work, ceil(nb / NB)), block 32*warps; work = (m << 16) | row block
+// analysis: gan [nb][L][J][2 (S,A)][7] complex -> fe [nb][3][C]
+// grid (n_work, ceil(nb / NB)), block 32*kWarps; work = (m << 16) | block of
+// WJ 16-row tiles (m-major order)
+// P columns: (phi, zeta, delta) of all b (6 NB), then ke of all b; H: first 6 NB.
 // ---------------------------------------------------------------------------
 template <int NB>
-__global__ void __launch_bounds__(128) k_analysis(
+__global__ void __launch_bounds__(32 * kWarps) k_analysis(
     const double2* __restrict__ gan, int nb, int T, int J, int C, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, const int* __restrict__ row_n, const int* __restrict__ moff,
-    const double* __restrict__ lam, const int* __restrict__ work, double2* __restrict__ fe) {
-  constexpr int PC = 8 * NB;        // (phi, zeta, delta) of all b, then ke of all b
-  constexpr int HU = 6 * NB;        // H columns actually used
+    const double* __restrict__ lam, const int* __restrict__ work, double2* __restrict__ fe,
+    int WJ) {
+  constexpr int HU = 6 * NB;
   constexpr int TH = (HU + 7) / 8;
-  constexpr int HC = 8 * TH;
-  constexpr int PS = PC + 4;
-  constexpr int HS = HC + 4;
+  constexpr int PC = 8 * NB;
   constexpr int OS = PC + 1;
-  __shared__ double dp[2][kAnalChunk * PS];
-  __shared__ double dh[2][kAnalChunk * HS];
-  static_assert(4 * kRowsPerWarp * OS <= 2 * kAnalChunk * PS, "output tile aliases dp");
+  constexpr int NACC = 2 * NB * 2;
+  constexpr int RED = kWarps * 32 * NACC;
+  constexpr int OUT = kWarps * kRowsPerWarp * OS;
+  __shared__ double red[RED > OUT ? RED : OUT];
 
   const int wk = work[blockIdx.x];
   const int m = wk >> 16, rb = wk & 0xffff;
-  const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
+  const int WK = kWarps / WJ;
+  const int rt = warp % WJ, ks = warp / WJ;
   const int b0 = blockIdx.y * NB;
   const int L = T + 1;
   const int r0m = rowoff[m];
   const int rows = rowoff[m + 1] - r0m;
   const int le = n_even[m];
-  const int rw = (rb * warps + warp) * kRowsPerWarp;
-  const bool active = rw < rows;
+  const int rw = (rb * WJ + rt) * kRowsPerWarp;
+  const bool live = rw < rows;
   const bool ev0 = rw < le, ev1 = rw + 8 < le;
   const double* P = ptab + (size_t)(r0m + rw + g) * J + t;
   const double* H = htab + (size_t)(r0m + rw + g) * J + t;
+
+  // this lane's B columns (one per tile): data element offsets within a (b, m, j) record
+  // record = [fold 0 (S): 7 complex][fold 1 (A): 7 complex] = 28 doubles
+  const double* gb = reinterpret_cast<const double*>(gan);
+  long long pbase[NB], hbase[TH];
+  int pel[NB], hel[TH];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    const int col = 8 * c + g;
+    int b, slot;
+    if (col < HU) { b = col / 6; slot = kXPhi + (col % 6) / 2; }
+    else { b = (col - HU) >> 1; slot = kXKe; }
+    pbase[c] = b0 + b < nb ? (((long long)(b0 + b) * L + m) * J) * 28 : -1;
+    pel[c] = slot * 2 + (col & 1);
+  }
+#pragma unroll
+  for (int c = 0; c < TH; ++c) {
+    const int col = 8 * c + g;
+    const int b = col / 6;
+    hbase[c] = (col < HU && b0 + b < nb) ? (((long long)(b0 + b) * L + m) * J) * 28 : -1;
+    hel[c] = (kYPhi + (col % 6) / 2) * 2 + (col & 1);
+  }
 
   double acc[2][NB][2];
 #pragma unroll
@@ -202,68 +256,58 @@ __global__ void __launch_bounds__(128) k_analysis(
 #pragma unroll
     for (int c = 0; c < NB; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
 
-  for (int jc = 0; jc < J; jc += kAnalChunk) {
-    const int nj = min(kAnalChunk, J - jc);
-    __syncthreads();
-    for (int it = threadIdx.x; it < kAnalChunk * NB; it += blockDim.x) {
-      const int jj = it / NB, b = it % NB;
-      double2 v[kNumSlots][2];
-      if (jj < nj && b0 + b < nb) {
-        const double2* src = gan + (((size_t)(b0 + b) * J + jc + jj) * L + m) * (kNumSlots * 2);
+  if (live) {
+    const int nsteps = J >> 2;
+#pragma unroll 4
+    for (int s = ks; s < nsteps; s += WK) {
+      const int k = 4 * s;
+      const double aP0 = __ldg(P + k), aP1 = __ldg(P + k + 8 * (size_t)J);
+      const double aH0 = __ldg(H + k), aH1 = __ldg(H + k + 8 * (size_t)J);
+      const long long jrec = (long long)(k + t) * 28;
 #pragma unroll
-        for (int q = 0; q < kNumSlots * 2; ++q) v[q >> 1][q & 1] = src[q];
-      } else {
-#pragma unroll
-        for (int q = 0; q < kNumSlots * 2; ++q) v[q >> 1][q & 1] = make_double2(0.0, 0.0);
+      for (int c = 0; c < NB; ++c) {
+        double bs = 0.0, ba = 0.0;
+        if (pbase[c] >= 0) {
+          bs = __ldg(gb + pbase[c] + jrec + pel[c]);
+          ba = __ldg(gb + pbase[c] + jrec + 14 + pel[c]);
+        }
+        dmma(acc[0][c], aP0, ev0 ? bs : ba);
+        dmma(acc[1][c], aP1, ev1 ? bs : ba);
       }
 #pragma unroll
-      for (int f = 0; f < 2; ++f) {
-        double* rp = dp[f] + jj * PS;
-        double* rh = dh[f] + jj * HS;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          rp[6 * b + 2 * q] = v[kXPhi + q][f].x;
-          rp[6 * b + 2 * q + 1] = v[kXPhi + q][f].y;
-          rh[6 * b + 2 * q] = v[kYPhi + q][f].x;
-          rh[6 * b + 2 * q + 1] = v[kYPhi + q][f].y;
+      for (int c = 0; c < TH; ++c) {
+        double bs = 0.0, ba = 0.0;
+        if (hbase[c] >= 0) {
+          bs = __ldg(gb + hbase[c] + jrec + hel[c]);
+          ba = __ldg(gb + hbase[c] + jrec + 14 + hel[c]);
         }
-        rp[6 * NB + 2 * b] = v[kXKe][f].x;
-        rp[6 * NB + 2 * b + 1] = v[kXKe][f].y;
-        if (b == 0)
-          for (int q = HU; q < HC; ++q) rh[q] = 0.0;
-      }
-    }
-    __syncthreads();
-    if (active) {
-      const int nsteps = nj >> 2;
-      for (int s = 0; s < nsteps; ++s) {
-        const int k = jc + 4 * s;
-        double aP[2], aH[2];
-        aP[0] = __ldg(P + k);
-        aP[1] = __ldg(P + k + 8 * (size_t)J);
-        aH[0] = __ldg(H + k);
-        aH[1] = __ldg(H + k + 8 * (size_t)J);
-        const int sr = (4 * s + t);
-#pragma unroll
-        for (int c = 0; c < NB; ++c) {
-          const double bs = dp[0][sr * PS + 8 * c + g];
-          const double ba = dp[1][sr * PS + 8 * c + g];
-          dmma(acc[0][c], aP[0], ev0 ? bs : ba);
-          dmma(acc[1][c], aP[1], ev1 ? bs : ba);
-        }
-#pragma unroll
-        for (int c = 0; c < TH; ++c) {
-          const double bs = dh[0][sr * HS + 8 * c + g];
-          const double ba = dh[1][sr * HS + 8 * c + g];
-          dmma(acc[0][c], aH[0], ev0 ? ba : bs);
-          dmma(acc[1][c], aH[1], ev1 ? ba : bs);
-        }
+        dmma(acc[0][c], aH0, ev0 ? ba : bs);
+        dmma(acc[1][c], aH1, ev1 ? ba : bs);
       }
     }
   }
-  __syncthreads();  // the output tiles alias dp
-  if (!active) return;
-  double* o = &dp[0][0] + warp * kRowsPerWarp * OS;
+  if (WK > 1) {
+    double* d = red + (warp * 32 + lane) * NACC;
+    int q = 0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < NB; ++c) { d[q++] = acc[a][c][0]; d[q++] = acc[a][c][1]; }
+    __syncthreads();
+    if (ks == 0) {
+      for (int w = 1; w < WK; ++w) {
+        const double* e = red + ((w * WJ + rt) * 32 + lane) * NACC;
+        int qq = 0;
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int c = 0; c < NB; ++c) { acc[a][c][0] += e[qq++]; acc[a][c][1] += e[qq++]; }
+      }
+    }
+    __syncthreads();
+  }
+  if (ks != 0 || !live) return;
+  double* o = red + rt * kRowsPerWarp * OS;
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -293,36 +337,40 @@ __global__ void __launch_bounds__(128) k_analysis(
   }
 }
 
-static int pick_nb(int nb) { return nb <= 1 ? 1 : (nb == 2 ? 2 : 4); }
+static int pick_nb(int nb) { return nb <= 6 ? nb : 4; }
+
+#define SDCSW_NB_LIST(X) X(1) X(2) X(3) X(4) X(5) X(6)
 
 cudaError_t launch_synthesis(const Plan& p, const double2* u, int nb, cudaStream_t s,
                              int* step_counter) {
   const int NB = pick_nb(nb);
-  dim3 grid(p.T + 1, p.J / (kRowsPerWarp * p.synth_warps), (nb + NB - 1) / NB);
-  dim3 block(32 * p.synth_warps);
-#define SDCSW_SYN(NBV)                                                                         \
-  k_synthesis<NBV><<<grid, block, 0, s>>>(u, nb, p.T, p.J, p.C, p.ptab, p.htab, p.rowoff,      \
-                                          p.n_even, p.row_n, p.moff, p.inv_nn, p.radius, p.fsyn, \
-                                          step_counter)
-  if (NB == 1) SDCSW_SYN(1);
-  else if (NB == 2) SDCSW_SYN(2);
-  else SDCSW_SYN(4);
+  const int WJ = p.synth_wj;
+  dim3 grid(p.J / (kRowsPerWarp * WJ), p.T + 1, (nb + NB - 1) / NB);
+#define SDCSW_SYN(NBV)                                                                           \
+  if (NB == NBV) {                                                                               \
+    k_synthesis<NBV><<<grid, 32 * kWarps, 0, s>>>(u, nb, p.T, p.J, p.C, p.ptab, p.htab,          \
+                                                  p.rowoff, p.n_even, p.row_n, p.moff, p.inv_nn, \
+                                                  p.radius, p.fsyn, step_counter, WJ);           \
+    return cudaGetLastError();                                                                   \
+  }
+  SDCSW_NB_LIST(SDCSW_SYN)
 #undef SDCSW_SYN
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_analysis(const Plan& p, double2* fe, int nb, cudaStream_t s) {
   const int NB = pick_nb(nb);
   dim3 grid(p.n_anal_work, (nb + NB - 1) / NB);
-  dim3 block(32 * p.anal_warps);
-#define SDCSW_ANA(NBV)                                                                         \
-  k_analysis<NBV><<<grid, block, 0, s>>>(p.gan, nb, p.T, p.J, p.C, p.ptab, p.htab, p.rowoff,   \
-                                         p.n_even, p.row_n, p.moff, p.lam, p.anal_work, fe)
-  if (NB == 1) SDCSW_ANA(1);
-  else if (NB == 2) SDCSW_ANA(2);
-  else SDCSW_ANA(4);
+#define SDCSW_ANA(NBV)                                                                          \
+  if (NB == NBV) {                                                                              \
+    k_analysis<NBV><<<grid, 32 * kWarps, 0, s>>>(p.gan, nb, p.T, p.J, p.C, p.ptab, p.htab,      \
+                                                 p.rowoff, p.n_even, p.row_n, p.moff, p.lam,    \
+                                                 p.anal_work, fe, p.anal_wj);                   \
+    return cudaGetLastError();                                                                  \
+  }
+  SDCSW_NB_LIST(SDCSW_ANA)
 #undef SDCSW_ANA
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace sdcsw

@@ -23,47 +23,53 @@ struct NodeArgs {
   double v[16 * 20];
 };
 
-__device__ __forceinline__ double2 add2(double2 a, double2 b) {
-  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
-}
-__device__ __forceinline__ double2 sub2(double2 a, double2 b) {
-  return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
-}
-__device__ __forceinline__ double2 scale2(double w, double2 a) {
-  return make_double2(__dmul_rn(w, a.x), __dmul_rn(w, a.y));
-}
-// acc += w * x   (numpy: acc += (python float) * array)
-__device__ __forceinline__ double2 axpy2(double2 acc, double w, double2 x) {
-  return add2(acc, scale2(w, x));
-}
-// acc -= w * x
-__device__ __forceinline__ double2 axmy2(double2 acc, double w, double2 x) {
-  return sub2(acc, scale2(w, x));
-}
-
+// A thread owns one real component (re or im) of one coefficient index across
+// the three fields; the solve and f_I are component-wise (all coefficients are
+// real), so this is bit-identical to the complex formulation and doubles the
+// parallelism.  Element e in [0, 2C) of field f lives at double offset f*2C + e.
 struct Tri {
-  double2 phi, zeta, delta;
+  double phi, zeta, delta;
 };
 
-__device__ __forceinline__ Tri load_tri(const double2* __restrict__ s, int C, int i) {
+__device__ __forceinline__ Tri load_tri(const double* __restrict__ s, int C2, int e) {
   Tri t;
-  t.phi = s[i];
-  t.zeta = s[C + i];
-  t.delta = s[2 * C + i];
+  t.phi = s[e];
+  t.zeta = s[C2 + e];
+  t.delta = s[2 * C2 + e];
   return t;
 }
-__device__ __forceinline__ void store_tri(double2* __restrict__ s, int C, int i, const Tri& t) {
-  s[i] = t.phi;
-  s[C + i] = t.zeta;
-  s[2 * C + i] = t.delta;
+__device__ __forceinline__ void store_tri(double* __restrict__ s, int C2, int e, const Tri& t) {
+  s[e] = t.phi;
+  s[C2 + e] = t.zeta;
+  s[2 * C2 + e] = t.delta;
+}
+__device__ __forceinline__ double axpy1(double acc, double w, double x) {
+  return __dadd_rn(acc, __dmul_rn(w, x));
+}
+__device__ __forceinline__ double axmy1(double acc, double w, double x) {
+  return __dsub_rn(acc, __dmul_rn(w, x));
+}
+__device__ __forceinline__ Tri axpy_tri(Tri a, double w, const Tri& x) {
+  a.phi = axpy1(a.phi, w, x.phi);
+  a.zeta = axpy1(a.zeta, w, x.zeta);
+  a.delta = axpy1(a.delta, w, x.delta);
+  return a;
+}
+__device__ __forceinline__ Tri axmy_tri(Tri a, double w, const Tri& x) {
+  a.phi = axmy1(a.phi, w, x.phi);
+  a.zeta = axmy1(a.zeta, w, x.zeta);
+  a.delta = axmy1(a.delta, w, x.delta);
+  return a;
+}
+__device__ __forceinline__ Tri add_tri(const Tri& a, const Tri& b) {
+  return Tri{__dadd_rn(a.phi, b.phi), __dadd_rn(a.zeta, b.zeta), __dadd_rn(a.delta, b.delta)};
+}
+__device__ __forceinline__ Tri sub_tri(const Tri& a, const Tri& b) {
+  return Tri{__dsub_rn(a.phi, b.phi), __dsub_rn(a.zeta, b.zeta), __dsub_rn(a.delta, b.delta)};
 }
 // f_I(u) = (-phibar delta, 0, lam phi)
 __device__ __forceinline__ Tri f_impl_tri(const Tri& u, double phibar, double lam) {
-  Tri r;
-  r.phi = scale2(-phibar, u.delta);
-  r.zeta = make_double2(0.0, 0.0);
-  r.delta = scale2(lam, u.phi);
-  return r;
+  return Tri{__dmul_rn(-phibar, u.delta), 0.0, __dmul_rn(lam, u.phi)};
 }
 // u - alpha f_I(u) = beta:  phi = (b_phi - a_phi b_delta) * inv,
 // inv = 1 / (1 + a2_phi lam), zeta = b_zeta, delta = b_delta + (alpha lam) phi
@@ -71,213 +77,163 @@ __device__ __forceinline__ Tri solve_tri(const Tri& b, double alpha, double a_ph
                                          double lam) {
   const double inv = __ddiv_rn(1.0, __dadd_rn(1.0, __dmul_rn(a2_phi, lam)));
   Tri u;
-  u.phi = scale2(inv, axmy2(b.phi, a_phi, b.delta));
+  u.phi = __dmul_rn(axmy1(b.phi, a_phi, b.delta), inv);
   u.zeta = b.zeta;
-  u.delta = axpy2(b.delta, __dmul_rn(alpha, lam), u.phi);
+  u.delta = axpy1(b.delta, __dmul_rn(alpha, lam), u.phi);
   return u;
 }
 __device__ __forceinline__ bool finite_tri(const Tri& t) {
-  return isfinite(t.phi.x) && isfinite(t.phi.y) && isfinite(t.zeta.x) && isfinite(t.zeta.y) &&
-         isfinite(t.delta.x) && isfinite(t.delta.y);
+  return isfinite(t.phi) && isfinite(t.zeta) && isfinite(t.delta);
 }
 
 // ---------------------------------------------------------------------------
-// diagonal sweep, nodes [lo, lo+count)
+// diagonal sweep, nodes [lo, lo+count): grid (ceil(2C/256), count)
 // coef layout per node m: w[0..M-1], wd, alpha, a_phi, a2_phi  (stride M+4)
 // ---------------------------------------------------------------------------
-template <int MAXM>
 __global__ void __launch_bounds__(256) k_sweep_nodes(
-    int C, int M, int lo, int count, NodeArgs cf, const double2* __restrict__ u0,
-    const double2* __restrict__ fe, long long fe_stride, const double2* __restrict__ fi,
+    int C2, int M, int lo, NodeArgs cf, const double* __restrict__ u0,
+    const double* __restrict__ fe, long long fe_stride, const double* __restrict__ fi,
     long long fi_stride, int first, double phibar, const double* __restrict__ lamv,
-    double2* __restrict__ u_out, double2* __restrict__ fi_out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= C) return;
-  const double lam = lamv[i];
-  const Tri a0 = load_tri(u0, C, i);
-  Tri F[MAXM], FI[MAXM];
+    double* __restrict__ u_out, double* fi_out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= C2) return;
+  const int q = blockIdx.y, m = lo + q;
+  const double lam = lamv[e >> 1];
+  const Tri a0 = load_tri(u0, C2, e);
   const Tri fi0 = f_impl_tri(a0, phibar, lam);
-#pragma unroll
-  for (int j = 0; j < MAXM; ++j) {
-    if (j < M) {
-      const Tri e = load_tri(fe + (size_t)j * fe_stride, C, i);
-      FI[j] = first ? fi0 : load_tri(fi + (size_t)j * fi_stride, C, i);
-      F[j].phi = add2(e.phi, FI[j].phi);
-      F[j].zeta = add2(e.zeta, FI[j].zeta);
-      F[j].delta = add2(e.delta, FI[j].delta);
-    }
+  const double* c = cf.v + m * (M + 4);
+  Tri b = a0, fim = fi0;
+  for (int j = 0; j < M; ++j) {
+    const Tri ej = load_tri(fe + j * fe_stride, C2, e);
+    const Tri ij = first ? fi0 : load_tri(fi + j * fi_stride, C2, e);
+    b = axpy_tri(b, c[j], add_tri(ej, ij));
+    if (j == m) fim = ij;
   }
-  for (int q = 0; q < count; ++q) {
-    const int m = lo + q;
-    const double* c = cf.v + m * (M + 4);
-    Tri b = a0;
-#pragma unroll
-    for (int j = 0; j < MAXM; ++j) {
-      if (j < M) {
-        b.phi = axpy2(b.phi, c[j], F[j].phi);
-        b.zeta = axpy2(b.zeta, c[j], F[j].zeta);
-        b.delta = axpy2(b.delta, c[j], F[j].delta);
-      }
-    }
-    Tri fim;
-#pragma unroll
-    for (int j = 0; j < MAXM; ++j)
-      if (j == m) fim = FI[j];
-    b.phi = axmy2(b.phi, c[M], fim.phi);
-    b.zeta = axmy2(b.zeta, c[M], fim.zeta);
-    b.delta = axmy2(b.delta, c[M], fim.delta);
-    const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
-    store_tri(u_out + (size_t)q * 3 * C, C, i, u);
-    store_tri(fi_out + (size_t)q * 3 * C, C, i, f_impl_tri(u, phibar, lam));
-  }
+  b = axmy_tri(b, c[M], fim);
+  const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
+  store_tri(u_out + (size_t)q * 3 * C2, C2, e, u);
+  store_tri(fi_out + (size_t)q * 3 * C2, C2, e, f_impl_tri(u, phibar, lam));
 }
 
 // ---------------------------------------------------------------------------
 // closing last-node solve; coef: w[0..M-1], wd, alpha, a_phi, a2_phi
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_final_node(
-    int C, int M, NodeArgs cf, const double2* __restrict__ u0, const double2* __restrict__ fe,
-    long long fe_stride, const double2* __restrict__ fi, long long fi_stride, int first,
-    double phibar, const double* __restrict__ lamv, double2* u_out, int* diverged,
+    int C2, int M, NodeArgs cf, const double* __restrict__ u0, const double* __restrict__ fe,
+    long long fe_stride, const double* __restrict__ fi, long long fi_stride, int first,
+    double phibar, const double* __restrict__ lamv, double* u_out, int* diverged,
     const int* step_counter) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= C) return;
-  const double lam = lamv[i];
-  const Tri a0 = load_tri(u0, C, i);
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= C2) return;
+  const double lam = lamv[e >> 1];
+  const Tri a0 = load_tri(u0, C2, e);
   const Tri fi0 = f_impl_tri(a0, phibar, lam);
   const double* c = cf.v;
   Tri b = a0, fil = fi0;
   for (int j = 0; j < M; ++j) {
-    const Tri e = load_tri(fe + (size_t)j * fe_stride, C, i);
-    const Tri f = first ? fi0 : load_tri(fi + (size_t)j * fi_stride, C, i);
-    const double w = c[j];
-    b.phi = axpy2(axpy2(b.phi, w, e.phi), w, f.phi);
-    b.zeta = axpy2(axpy2(b.zeta, w, e.zeta), w, f.zeta);
-    b.delta = axpy2(axpy2(b.delta, w, e.delta), w, f.delta);
-    if (j == M - 1) fil = f;
+    const Tri ej = load_tri(fe + j * fe_stride, C2, e);
+    const Tri ij = first ? fi0 : load_tri(fi + j * fi_stride, C2, e);
+    b = axpy_tri(axpy_tri(b, c[j], ej), c[j], ij);
+    if (j == M - 1) fil = ij;
   }
-  b.phi = axmy2(b.phi, c[M], fil.phi);
-  b.zeta = axmy2(b.zeta, c[M], fil.zeta);
-  b.delta = axmy2(b.delta, c[M], fil.delta);
+  b = axmy_tri(b, c[M], fil);
   const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
-  store_tri(u_out, C, i, u);
+  store_tri(u_out, C2, e, u);
   if (diverged != nullptr && !finite_tri(u)) atomicMin(diverged, step_counter ? *step_counter : 1);
 }
 
 // ---------------------------------------------------------------------------
 // serial sweep pieces
 // ---------------------------------------------------------------------------
-// quad_m = u0 + sum_j (w_mj fe_j + w_mj fi_j)  for all m   (integrators.py:198-205)
+// quad_m = u0 + sum_j (w_mj fe_j + w_mj fi_j), grid (ceil(2C/256), M)  (integrators.py:198-205)
 __global__ void __launch_bounds__(256) k_serial_quad(
-    int C, int M, NodeArgs cf, const double2* __restrict__ u0, const double2* __restrict__ fe,
-    long long fe_stride, const double2* __restrict__ fi, long long fi_stride, int first,
-    double phibar, const double* __restrict__ lamv, double2* __restrict__ quad) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= C) return;
-  const double lam = lamv[i];
-  const Tri a0 = load_tri(u0, C, i);
+    int C2, int M, NodeArgs cf, const double* __restrict__ u0, const double* __restrict__ fe,
+    long long fe_stride, const double* __restrict__ fi, long long fi_stride, int first,
+    double phibar, const double* __restrict__ lamv, double* __restrict__ quad) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= C2) return;
+  const int m = blockIdx.y;
+  const double lam = lamv[e >> 1];
+  const Tri a0 = load_tri(u0, C2, e);
   const Tri fi0 = f_impl_tri(a0, phibar, lam);
-  for (int m = 0; m < M; ++m) {
-    Tri b = a0;
-    for (int j = 0; j < M; ++j) {
-      const Tri e = load_tri(fe + (size_t)j * fe_stride, C, i);
-      const Tri f = first ? fi0 : load_tri(fi + (size_t)j * fi_stride, C, i);
-      const double w = cf.v[m * M + j];
-      b.phi = axpy2(axpy2(b.phi, w, e.phi), w, f.phi);
-      b.zeta = axpy2(axpy2(b.zeta, w, e.zeta), w, f.zeta);
-      b.delta = axpy2(axpy2(b.delta, w, e.delta), w, f.delta);
-    }
-    store_tri(quad + (size_t)m * 3 * C, C, i, b);
+  Tri b = a0;
+  for (int j = 0; j < M; ++j) {
+    const Tri ej = load_tri(fe + j * fe_stride, C2, e);
+    const Tri ij = first ? fi0 : load_tri(fi + j * fi_stride, C2, e);
+    const double w = cf.v[m * M + j];
+    b = axpy_tri(axpy_tri(b, w, ej), w, ij);
   }
+  store_tri(quad + (size_t)m * 3 * C2, C2, e, b);
 }
 
 // node m of a serial sweep: beta = quad_m (+ corr) - alpha fi_m; u = solve;
-// fi_new = f_I(u).  coef = alpha, a_phi, a2_phi.
+// fi_new = f_I(u).
 __global__ void __launch_bounds__(256) k_serial_node(
-    int C, double alpha, double a_phi, double a2_phi, int use_corr,
-    const double2* __restrict__ quad, const double2* __restrict__ corr,
-    const double2* __restrict__ u0, const double2* __restrict__ fi_old, int first, double phibar,
-    const double* __restrict__ lamv, double2* __restrict__ u_out, double2* u_out2,
-    double2* __restrict__ fi_new, int* diverged, const int* step_counter) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= C) return;
-  const double lam = lamv[i];
-  Tri b = load_tri(quad, C, i);
-  if (use_corr) {
-    const Tri c = load_tri(corr, C, i);
-    b.phi = add2(b.phi, c.phi);
-    b.zeta = add2(b.zeta, c.zeta);
-    b.delta = add2(b.delta, c.delta);
-  }
-  const Tri fo = first ? f_impl_tri(load_tri(u0, C, i), phibar, lam) : load_tri(fi_old, C, i);
-  b.phi = axmy2(b.phi, alpha, fo.phi);
-  b.zeta = axmy2(b.zeta, alpha, fo.zeta);
-  b.delta = axmy2(b.delta, alpha, fo.delta);
+    int C2, double alpha, double a_phi, double a2_phi, int use_corr,
+    const double* __restrict__ quad, const double* __restrict__ corr,
+    const double* __restrict__ u0, const double* __restrict__ fi_old, int first, double phibar,
+    const double* __restrict__ lamv, double* __restrict__ u_out, double* u_out2,
+    double* __restrict__ fi_new, int* diverged, const int* step_counter) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= C2) return;
+  const double lam = lamv[e >> 1];
+  Tri b = load_tri(quad, C2, e);
+  if (use_corr) b = add_tri(b, load_tri(corr, C2, e));
+  const Tri fo = first ? f_impl_tri(load_tri(u0, C2, e), phibar, lam) : load_tri(fi_old, C2, e);
+  b = axmy_tri(b, alpha, fo);
   const Tri u = solve_tri(b, alpha, a_phi, a2_phi, lam);
-  store_tri(u_out, C, i, u);
-  store_tri(fi_new, C, i, f_impl_tri(u, phibar, lam));
+  store_tri(u_out, C2, e, u);
+  store_tri(fi_new, C2, e, f_impl_tri(u, phibar, lam));
   if (u_out2 != nullptr) {
-    store_tri(u_out2, C, i, u);
-    if (diverged != nullptr && !finite_tri(u))
-      atomicMin(diverged, step_counter ? *step_counter : 1);
+    store_tri(u_out2, C2, e, u);
+    if (diverged != nullptr && !finite_tri(u)) atomicMin(diverged, step_counter ? *step_counter : 1);
   }
 }
 
 // corr (+)= we (fe_new - fe_old) ; corr += wi (fi_new - fi_old)   (integrators.py:225-227)
 __global__ void __launch_bounds__(256) k_serial_update(
-    int C, double we, double wi, int use_corr, double2* __restrict__ corr,
-    const double2* __restrict__ fe_new, const double2* __restrict__ fe_old,
-    const double2* __restrict__ fi_new, const double2* __restrict__ fi_old,
-    const double2* __restrict__ u0, int first, double phibar, const double* __restrict__ lamv) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= C) return;
-  const double lam = lamv[i];
-  const Tri en = load_tri(fe_new, C, i), eo = load_tri(fe_old, C, i);
-  const Tri fn = load_tri(fi_new, C, i);
-  const Tri fo = first ? f_impl_tri(load_tri(u0, C, i), phibar, lam) : load_tri(fi_old, C, i);
+    int C2, double we, double wi, int use_corr, double* __restrict__ corr,
+    const double* __restrict__ fe_new, const double* __restrict__ fe_old,
+    const double* __restrict__ fi_new, const double* __restrict__ fi_old,
+    const double* __restrict__ u0, int first, double phibar, const double* __restrict__ lamv) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= C2) return;
+  const double lam = lamv[e >> 1];
+  const Tri en = load_tri(fe_new, C2, e), eo = load_tri(fe_old, C2, e);
+  const Tri fn = load_tri(fi_new, C2, e);
+  const Tri fo = first ? f_impl_tri(load_tri(u0, C2, e), phibar, lam) : load_tri(fi_old, C2, e);
+  const Tri de = sub_tri(en, eo), di = sub_tri(fn, fo);
   Tri c;
   if (use_corr) {
-    c = load_tri(corr, C, i);
-    c.phi = axpy2(c.phi, we, sub2(en.phi, eo.phi));
-    c.zeta = axpy2(c.zeta, we, sub2(en.zeta, eo.zeta));
-    c.delta = axpy2(c.delta, we, sub2(en.delta, eo.delta));
-  } else {  // correction starts at zero: 0 + x == x
-    c.phi = scale2(we, sub2(en.phi, eo.phi));
-    c.zeta = scale2(we, sub2(en.zeta, eo.zeta));
-    c.delta = scale2(we, sub2(en.delta, eo.delta));
+    c = axpy_tri(load_tri(corr, C2, e), we, de);
+  } else {  // the correction starts at zero: 0 + x == x
+    c = Tri{__dmul_rn(we, de.phi), __dmul_rn(we, de.zeta), __dmul_rn(we, de.delta)};
   }
-  c.phi = axpy2(c.phi, wi, sub2(fn.phi, fo.phi));
-  c.zeta = axpy2(c.zeta, wi, sub2(fn.zeta, fo.zeta));
-  c.delta = axpy2(c.delta, wi, sub2(fn.delta, fo.delta));
-  store_tri(corr, C, i, c);
+  store_tri(corr, C2, e, axpy_tri(c, wi, di));
 }
 
 // ---------------------------------------------------------------------------
 // problem operations
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_f_impl(int C, int nb, const double2* __restrict__ u,
-                                                double2* __restrict__ fi, double phibar,
+__global__ void __launch_bounds__(256) k_f_impl(int C2, const double* __restrict__ u,
+                                                double* __restrict__ fi, double phibar,
                                                 const double* __restrict__ lamv) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= C) return;
-  const double lam = lamv[i];
-  for (int b = 0; b < nb; ++b)
-    store_tri(fi + (size_t)b * 3 * C, C, i, f_impl_tri(load_tri(u + (size_t)b * 3 * C, C, i), phibar, lam));
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= C2) return;
+  const size_t b = blockIdx.y;
+  store_tri(fi + b * 3 * C2, C2, e, f_impl_tri(load_tri(u + b * 3 * C2, C2, e), phibar, lamv[e >> 1]));
 }
 
-__global__ void __launch_bounds__(256) k_solve(int C, int nb, NodeArgs cf,
-                                               const double2* __restrict__ beta,
-                                               double2* __restrict__ u,
+__global__ void __launch_bounds__(256) k_solve(int C2, NodeArgs cf, const double* __restrict__ beta,
+                                               double* __restrict__ u,
                                                const double* __restrict__ lamv) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= C) return;
-  const double lam = lamv[i];
-  for (int b = 0; b < nb; ++b) {
-    const Tri bt = load_tri(beta + (size_t)b * 3 * C, C, i);
-    const double alpha = cf.v[3 * b];
-    const Tri r = alpha == 0.0 ? bt : solve_tri(bt, alpha, cf.v[3 * b + 1], cf.v[3 * b + 2], lam);
-    store_tri(u + (size_t)b * 3 * C, C, i, r);
-  }
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= C2) return;
+  const int b = blockIdx.y;
+  const Tri bt = load_tri(beta + (size_t)b * 3 * C2, C2, e);
+  const double alpha = cf.v[3 * b];
+  const Tri r = alpha == 0.0 ? bt : solve_tri(bt, alpha, cf.v[3 * b + 1], cf.v[3 * b + 2], lamv[e >> 1]);
+  store_tri(u + (size_t)b * 3 * C2, C2, e, r);
 }
 
 __global__ void k_check_finite(const double* __restrict__ x, long long n, int* flag) {
@@ -289,7 +245,7 @@ __global__ void k_check_finite(const double* __restrict__ x, long long n, int* f
 }
 
 // ---------------------------------------------------------------------------
-static inline dim3 grid_for(int C) { return dim3((C + 255) / 256); }
+static inline dim3 grid_for(int C, int y = 1) { return dim3((2 * C + 255) / 256, y); }
 
 static NodeArgs pack(const double* v, int n) {
   NodeArgs a;
@@ -297,19 +253,22 @@ static NodeArgs pack(const double* v, int n) {
   return a;
 }
 
+#define D(x) reinterpret_cast<const double*>(x)
+#define W(x) reinterpret_cast<double*>(x)
+
 cudaError_t launch_f_impl(const Plan& p, const double2* u, double2* fi, int nb, cudaStream_t s) {
-  k_f_impl<<<grid_for(p.C), 256, 0, s>>>(p.C, nb, u, fi, p.phibar, p.lam);
+  k_f_impl<<<grid_for(p.C, nb), 256, 0, s>>>(2 * p.C, D(u), W(fi), p.phibar, p.lam);
   return cudaGetLastError();
 }
 
 cudaError_t launch_solve(const Plan& p, const double* coef_host, const double2* beta, double2* u,
                          int nb, cudaStream_t s) {
-  // coefficients travel by value; batches above 106 states are split
+  // coefficients travel by value; batches above 100 states are split
   for (int b0 = 0; b0 < nb; b0 += 100) {
     const int n = nb - b0 < 100 ? nb - b0 : 100;
-    k_solve<<<grid_for(p.C), 256, 0, s>>>(p.C, n, pack(coef_host + 3 * b0, 3 * n),
-                                          beta + (size_t)b0 * 3 * p.C, u + (size_t)b0 * 3 * p.C,
-                                          p.lam);
+    k_solve<<<grid_for(p.C, n), 256, 0, s>>>(2 * p.C, pack(coef_host + 3 * b0, 3 * n),
+                                              D(beta + (size_t)b0 * 3 * p.C),
+                                              W(u + (size_t)b0 * 3 * p.C), p.lam);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -320,17 +279,11 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                const double2* u0, const double2* fe, long long fe_stride,
                                const double2* fi, long long fi_stride, int first, double2* u_out,
                                double2* fi_out, cudaStream_t s) {
-  NodeArgs cf = pack(coef_host, M * (M + 4));
-  const long long fes = fe_stride * 3 * p.C, fis = fi_stride * 3 * p.C;
-  if (M <= 4)
-    k_sweep_nodes<4><<<grid_for(p.C), 256, 0, s>>>(p.C, M, node_lo, count, cf, u0, fe, fes, fi, fis,
-                                                   first, p.phibar, p.lam, u_out, fi_out);
-  else if (M <= 8)
-    k_sweep_nodes<8><<<grid_for(p.C), 256, 0, s>>>(p.C, M, node_lo, count, cf, u0, fe, fes, fi, fis,
-                                                   first, p.phibar, p.lam, u_out, fi_out);
-  else
-    k_sweep_nodes<16><<<grid_for(p.C), 256, 0, s>>>(p.C, M, node_lo, count, cf, u0, fe, fes, fi,
-                                                    fis, first, p.phibar, p.lam, u_out, fi_out);
+  const long long S2 = 6LL * p.C;  // doubles per state
+  k_sweep_nodes<<<grid_for(p.C, count), 256, 0, s>>>(2 * p.C, M, node_lo, pack(coef_host, M * (M + 4)),
+                                                     D(u0), D(fe), fe_stride * S2, D(fi),
+                                                     fi_stride * S2, first, p.phibar, p.lam,
+                                                     W(u_out), W(fi_out));
   return cudaGetLastError();
 }
 
@@ -338,18 +291,20 @@ cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, con
                               const double2* fe, long long fe_stride, const double2* fi,
                               long long fi_stride, int first, double2* u_out, int* diverged,
                               const int* step_counter, cudaStream_t s) {
-  k_final_node<<<grid_for(p.C), 256, 0, s>>>(p.C, M, pack(coef_host, M + 4), u0, fe,
-                                             fe_stride * 3 * p.C, fi, fi_stride * 3 * p.C, first,
-                                             p.phibar, p.lam, u_out, diverged, step_counter);
+  const long long S2 = 6LL * p.C;
+  k_final_node<<<grid_for(p.C), 256, 0, s>>>(2 * p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
+                                             fe_stride * S2, D(fi), fi_stride * S2, first, p.phibar,
+                                             p.lam, W(u_out), diverged, step_counter);
   return cudaGetLastError();
 }
 
 cudaError_t launch_serial_quad(const Plan& p, int M, const double* w_host, const double2* u0,
                                const double2* fe, long long fe_stride, const double2* fi,
                                long long fi_stride, int first, double2* quad, cudaStream_t s) {
-  k_serial_quad<<<grid_for(p.C), 256, 0, s>>>(p.C, M, pack(w_host, M * M), u0, fe,
-                                              fe_stride * 3 * p.C, fi, fi_stride * 3 * p.C, first,
-                                              p.phibar, p.lam, quad);
+  const long long S2 = 6LL * p.C;
+  k_serial_quad<<<grid_for(p.C, M), 256, 0, s>>>(2 * p.C, M, pack(w_host, M * M), D(u0), D(fe),
+                                                 fe_stride * S2, D(fi), fi_stride * S2, first,
+                                                 p.phibar, p.lam, W(quad));
   return cudaGetLastError();
 }
 
@@ -359,9 +314,10 @@ cudaError_t launch_serial_node(const Plan& p, int M, int m, const double* coef_h
                                double2* fi_new, int* diverged, const int* step_counter,
                                cudaStream_t s) {
   (void)M;
-  k_serial_node<<<grid_for(p.C), 256, 0, s>>>(p.C, coef_host[0], coef_host[1], coef_host[2], m > 0,
-                                              quad, corr, u0, fi_old, first, p.phibar, p.lam, u_out,
-                                              u_out2, fi_new, diverged, step_counter);
+  k_serial_node<<<grid_for(p.C), 256, 0, s>>>(2 * p.C, coef_host[0], coef_host[1], coef_host[2],
+                                              m > 0, D(quad), D(corr), D(u0), D(fi_old), first,
+                                              p.phibar, p.lam, W(u_out), W(u_out2), W(fi_new),
+                                              diverged, step_counter);
   return cudaGetLastError();
 }
 
@@ -369,8 +325,9 @@ cudaError_t launch_serial_update(const Plan& p, int m, double we, double wi, dou
                                  const double2* fe_new, const double2* fe_old,
                                  const double2* fi_new, const double2* fi_old, const double2* u0,
                                  int first, cudaStream_t s) {
-  k_serial_update<<<grid_for(p.C), 256, 0, s>>>(p.C, we, wi, m > 0, corr, fe_new, fe_old, fi_new,
-                                                fi_old, u0, first, p.phibar, p.lam);
+  k_serial_update<<<grid_for(p.C), 256, 0, s>>>(2 * p.C, we, wi, m > 0, W(corr), D(fe_new),
+                                                D(fe_old), D(fi_new), D(fi_old), D(u0), first,
+                                                p.phibar, p.lam);
   return cudaGetLastError();
 }
 

@@ -6,12 +6,15 @@
 // restatement (A=eta U, B=eta V, C=Phi' U, D=Phi' V,
 // E=(U^2+V^2)/(2(1-mu^2))).
 //
-// FFT: mixed-radix (4, 2, 3) Stockham autosort over nlon = 2^k or 3*2^k
-// complex points; two real rings (north, south) are packed into one complex
-// transform (z = x_N + i x_S), so 4 inverse + 5 forward complex FFTs of length
-// nlon per ring pair.  Output per (b, pair, m <= T): the seven analysis data
-// slots, pre-weighted, pre-multiplied by i m where the analysis needs it and
-// folded into symmetric (N+S) / antisymmetric (N-S) parts.
+// FFT: mixed-radix (8, 4, 3) Stockham autosort over nlon = 3*2^k complex
+// points (kernel templated on nlon: 96 ... 1536), in place: every pass reads all butterfly inputs of all the
+// concurrent transforms into registers, synchronises, then writes.  The two
+// real rings of a pair are packed into one complex transform (z = x_N + i x_S),
+// and the 4 inverse / 5 forward transforms of a pair run as ONE multi-FFT each,
+// so a pair costs 2 * (#radix passes) barrier phases instead of 9x that.
+// Output per (b, pair, m <= T): the seven analysis data slots, pre-weighted,
+// pre-multiplied by i m where the analysis needs it and folded into symmetric
+// (N+S) / antisymmetric (N-S) parts.
 #include "internal.cuh"
 
 namespace sdcsw {
@@ -19,190 +22,258 @@ namespace sdcsw {
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
-
-// in-place-ish Stockham: ping-pong between x and y; returns the buffer holding
-// the result.  Ends with __syncthreads().
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// multiply by -i (forward) or +i (inverse)
 template <bool INV>
-__device__ double2* fft_stockham(double2* x, double2* y, const FftPlan& fp,
-                                 const double2* __restrict__ tw) {
-  const int N = fp.n;
-  int p = 1;
-  for (int st = 0; st < fp.nstages; ++st) {
-    const int R = fp.radix[st];
-    const int NR = N / R;
-    const int ts = N / (R * p);
-    for (int i = threadIdx.x; i < NR; i += blockDim.x) {
-      const int k = i % p;
-      const int jo = (i - k) * R + k;
-      if (R == 4) {
-        double2 u0 = x[i], u1 = x[i + NR], u2 = x[i + 2 * NR], u3 = x[i + 3 * NR];
-        if (k) {
-          double2 w1 = __ldg(tw + k * ts), w2 = __ldg(tw + 2 * k * ts), w3 = __ldg(tw + 3 * k * ts);
-          if (INV) { w1.y = -w1.y; w2.y = -w2.y; w3.y = -w3.y; }
-          u1 = cmul(u1, w1); u2 = cmul(u2, w2); u3 = cmul(u3, w3);
-        }
-        const double2 a0 = make_double2(u0.x + u2.x, u0.y + u2.y);
-        const double2 a1 = make_double2(u0.x - u2.x, u0.y - u2.y);
-        const double2 a2 = make_double2(u1.x + u3.x, u1.y + u3.y);
-        const double2 a3 = make_double2(u1.x - u3.x, u1.y - u3.y);
-        // forward: y1 = a1 - i a3, y3 = a1 + i a3 ; inverse swaps
-        const double2 ia3 = INV ? make_double2(-a3.y, a3.x) : make_double2(a3.y, -a3.x);
-        y[jo] = make_double2(a0.x + a2.x, a0.y + a2.y);
-        y[jo + p] = make_double2(a1.x + ia3.x, a1.y + ia3.y);
-        y[jo + 2 * p] = make_double2(a0.x - a2.x, a0.y - a2.y);
-        y[jo + 3 * p] = make_double2(a1.x - ia3.x, a1.y - ia3.y);
-      } else if (R == 2) {
-        double2 u0 = x[i], u1 = x[i + NR];
-        if (k) {
-          double2 w1 = __ldg(tw + k * ts);
-          if (INV) w1.y = -w1.y;
-          u1 = cmul(u1, w1);
-        }
-        y[jo] = make_double2(u0.x + u1.x, u0.y + u1.y);
-        y[jo + p] = make_double2(u0.x - u1.x, u0.y - u1.y);
-      } else {  // R == 3
-        double2 u0 = x[i], u1 = x[i + NR], u2 = x[i + 2 * NR];
-        if (k) {
-          double2 w1 = __ldg(tw + k * ts), w2 = __ldg(tw + 2 * k * ts);
-          if (INV) { w1.y = -w1.y; w2.y = -w2.y; }
-          u1 = cmul(u1, w1); u2 = cmul(u2, w2);
-        }
-        const double s3 = 0.86602540378443864676;  // sqrt(3)/2
-        const double2 t1 = make_double2(u1.x + u2.x, u1.y + u2.y);
-        const double2 t2 = make_double2(u0.x - 0.5 * t1.x, u0.y - 0.5 * t1.y);
-        const double2 d = make_double2(u1.x - u2.x, u1.y - u2.y);
-        // forward: y1 = t2 - i s d, y2 = t2 + i s d ; inverse swaps
-        const double2 isd = INV ? make_double2(-s3 * d.y, s3 * d.x) : make_double2(s3 * d.y, -s3 * d.x);
-        y[jo] = make_double2(u0.x + t1.x, u0.y + t1.y);
-        y[jo + p] = make_double2(t2.x + isd.x, t2.y + isd.y);
-        y[jo + 2 * p] = make_double2(t2.x - isd.x, t2.y - isd.y);
-      }
-    }
-    __syncthreads();
-    double2* tmp = x; x = y; y = tmp;
-    p *= R;
-  }
-  return x;
+__device__ __forceinline__ double2 rot(double2 a) {
+  return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
 }
 
-__global__ void __launch_bounds__(256) k_ring(const double2* __restrict__ fsyn,
-                                              double2* __restrict__ gan, int J, int T,
-                                              const double* __restrict__ mu,
-                                              const double* __restrict__ wsyn,
-                                              const double* __restrict__ wke,
-                                              const double2* __restrict__ tw, FftPlan fp,
-                                              double two_omega) {
+template <bool INV>
+__device__ __forceinline__ void dft4(double2& a0, double2& a1, double2& a2, double2& a3) {
+  const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2);
+  const double2 s13 = cadd(a1, a3), d13 = rot<INV>(csub(a1, a3));
+  a0 = cadd(s02, s13);
+  a2 = csub(s02, s13);
+  a1 = cadd(d02, d13);
+  a3 = csub(d02, d13);
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void dft(double2 (&u)[R]) {
+  if constexpr (R == 2) {
+    const double2 a = u[0], b = u[1];
+    u[0] = cadd(a, b);
+    u[1] = csub(a, b);
+  } else if constexpr (R == 3) {
+    const double s3 = 0.86602540378443864676;  // sqrt(3)/2
+    const double2 t1 = cadd(u[1], u[2]);
+    const double2 t2 = make_double2(u[0].x - 0.5 * t1.x, u[0].y - 0.5 * t1.y);
+    const double2 d = csub(u[1], u[2]);
+    const double2 isd = rot<INV>(make_double2(s3 * d.x, s3 * d.y));  // -i s d (fwd)
+    u[0] = cadd(u[0], t1);
+    u[1] = cadd(t2, isd);
+    u[2] = csub(t2, isd);
+  } else if constexpr (R == 4) {
+    dft4<INV>(u[0], u[1], u[2], u[3]);
+  } else {  // R == 8: a_r = u_r + u_{r+4}, b_r = (u_r - u_{r+4}) w8^r, y_2q = DFT4(a), y_2q+1 = DFT4(b)
+    const double h = 0.70710678118654752440;
+    double2 a[4], b[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      a[r] = cadd(u[r], u[r + 4]);
+      b[r] = csub(u[r], u[r + 4]);
+    }
+    // w8 = (1 - i)/sqrt2 (fwd), w8^2 = -i, w8^3 = (-1 - i)/sqrt2
+    b[1] = INV ? make_double2(h * (b[1].x - b[1].y), h * (b[1].x + b[1].y))
+               : make_double2(h * (b[1].x + b[1].y), h * (b[1].y - b[1].x));
+    b[2] = rot<INV>(b[2]);
+    b[3] = INV ? make_double2(-h * (b[3].x + b[3].y), h * (b[3].x - b[3].y))
+               : make_double2(h * (b[3].y - b[3].x), -h * (b[3].x + b[3].y));
+    dft4<INV>(a[0], a[1], a[2], a[3]);
+    dft4<INV>(b[0], b[1], b[2], b[3]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      u[2 * q] = a[q];
+      u[2 * q + 1] = b[q];
+    }
+  }
+}
+
+// Compile-time radix plan for nlon = 3 * 2^k: as many radix-8 passes as
+// possible, then radix 4, then the radix-3 pass (p is a power of two before it).
+constexpr int pow2_of(int n) { return n % 3 == 0 ? n / 3 : n; }
+constexpr int log2i(int n) { return n <= 1 ? 0 : 1 + log2i(n / 2); }
+constexpr int n8_of(int n) {
+  return log2i(pow2_of(n)) % 3 == 1 ? log2i(pow2_of(n)) / 3 - 1 : log2i(pow2_of(n)) / 3;
+}
+constexpr int n4_of(int n) {
+  return log2i(pow2_of(n)) % 3 == 1 ? 2 : (log2i(pow2_of(n)) % 3 == 2 ? 1 : 0);
+}
+constexpr int nstages_of(int n) { return n8_of(n) + n4_of(n) + (n % 3 == 0 ? 1 : 0); }
+constexpr int radix_of(int n, int s) { return s < n8_of(n) ? 8 : (s < n8_of(n) + n4_of(n) ? 4 : 3); }
+
+// One in-place Stockham pass (radix R, sub-length P) over NF concurrent
+// transforms of length N stored at Z[f * N]; all index arithmetic is by
+// compile-time constants.  tw[k] = exp(-2 pi i k / N) in shared memory.
+template <int N, int R, int P, bool INV, int NF, int THREADS>
+__device__ __forceinline__ void pass(double2* Z, const double2* tw) {
+  constexpr int NR = N / R;
+  constexpr int ITEMS = NF * NR;
+  constexpr int TS = N / (R * P);
+  constexpr int MAXIT = (ITEMS + THREADS - 1) / THREADS;
+  double2 v[MAXIT][R];
+#pragma unroll
+  for (int q = 0; q < MAXIT; ++q) {
+    const int it = threadIdx.x + q * THREADS;
+    if (ITEMS % THREADS == 0 || it < ITEMS) {
+      const int f = it / NR, i = it - f * NR;
+      const double2* X = Z + f * N;
+      const int k = i % P;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[q][r] = X[i + r * NR];
+      if (P > 1 && k) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          double2 w = tw[r * k * TS];
+          if (INV) w.y = -w.y;
+          v[q][r] = cmul(v[q][r], w);
+        }
+      }
+      dft<R, INV>(v[q]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < MAXIT; ++q) {
+    const int it = threadIdx.x + q * THREADS;
+    if (ITEMS % THREADS == 0 || it < ITEMS) {
+      const int f = it / NR, i = it - f * NR;
+      double2* X = Z + f * N;
+      const int k = i % P;
+      const int jo = (i - k) * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) X[jo + r * P] = v[q][r];
+    }
+  }
+  __syncthreads();
+}
+
+template <int N, int S, int P, bool INV, int NF, int THREADS>
+__device__ __forceinline__ void passes(double2* Z, const double2* tw) {
+  if constexpr (S < nstages_of(N)) {
+    constexpr int R = radix_of(N, S);
+    pass<N, R, P, INV, NF, THREADS>(Z, tw);
+    passes<N, S + 1, P * R, INV, NF, THREADS>(Z, tw);
+  }
+}
+
+template <int N, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_ring(const double2* __restrict__ fsyn,
+                                                  double2* __restrict__ gan, int J, int T,
+                                                  const double* __restrict__ mu,
+                                                  const double* __restrict__ wsyn,
+                                                  const double* __restrict__ wke,
+                                                  const double2* __restrict__ twg,
+                                                  double two_omega) {
   extern __shared__ double2 sm2[];
-  const int N = fp.n;
   const int L = T + 1;
-  double2* buf0 = sm2;
-  double2* buf1 = sm2 + N;
-  double* grid = reinterpret_cast<double*>(sm2 + 2 * N);  // [4 fields][2 rings][N]
+  double2* Z = sm2;            // [5][N]
+  double2* tw = sm2 + 5 * N;   // [N]
   const int j = blockIdx.x, b = blockIdx.y;
   const double2* F = fsyn + ((size_t)b * J + j) * L * 8;
 
-  // ---- inverse transforms: U, V, zeta, Phi (north + i south) ----
-  for (int f = 0; f < 4; ++f) {
-    for (int k = threadIdx.x; k < N; k += blockDim.x) {
-      double2 z = make_double2(0.0, 0.0);
-      if (k <= T) {
-        double2 xn = F[(k * 4 + f) * 2], xs = F[(k * 4 + f) * 2 + 1];
-        if (k == 0) xn.y = xs.y = 0.0;
-        z = make_double2(xn.x - xs.y, xn.y + xs.x);  // X + i Y
-      } else if (k >= N - T) {
-        const int m = N - k;
-        const double2 xn = F[(m * 4 + f) * 2], xs = F[(m * 4 + f) * 2 + 1];
-        z = make_double2(xn.x + xs.y, xs.x - xn.y);  // conj(X) + i conj(Y)
-      }
-      buf0[k] = z;
+  for (int k = threadIdx.x; k < N; k += THREADS) tw[k] = twg[k];
+  // spectra of U, V, zeta, Phi:  Z_m = X_m + i Y_m,  Z_{N-m} = conj(X_m) + i conj(Y_m)
+  for (int idx = threadIdx.x; idx < 4 * N; idx += THREADS) {
+    const int k = idx >> 2, f = idx & 3;
+    double2 z = make_double2(0.0, 0.0);
+    if (k <= T) {
+      double2 xn = F[(k * 4 + f) * 2], xs = F[(k * 4 + f) * 2 + 1];
+      if (k == 0) xn.y = xs.y = 0.0;
+      z = make_double2(xn.x - xs.y, xn.y + xs.x);
+    } else if (k >= N - T) {
+      const int m = N - k;
+      const double2 xn = F[(m * 4 + f) * 2], xs = F[(m * 4 + f) * 2 + 1];
+      z = make_double2(xn.x + xs.y, xs.x - xn.y);
     }
-    __syncthreads();
-    const double2* res = fft_stockham<true>(buf0, buf1, fp, tw);
-    for (int k = threadIdx.x; k < N; k += blockDim.x) {
-      const double2 z = res[k];
-      grid[(2 * f) * N + k] = z.x;
-      grid[(2 * f + 1) * N + k] = z.y;
-    }
-    __syncthreads();
+    Z[f * N + k] = z;
   }
+  __syncthreads();
+  passes<N, 0, 1, true, 4, THREADS>(Z, tw);
 
-  // ---- products and forward transforms ----
+  // products on the grid: re = north ring, im = south ring
   const double muj = mu[j];
   const double cor_n = two_omega * muj, cor_s = -two_omega * muj;
   const double ke_scale = 0.5 / ((1.0 - muj) * (1.0 + muj));
+  for (int k = threadIdx.x; k < N; k += THREADS) {
+    const double2 U = Z[k], V = Z[N + k], Zt = Z[2 * N + k], Ph = Z[3 * N + k];
+    const double en = Zt.x + cor_n, es = Zt.y + cor_s;
+    Z[k] = make_double2(en * U.x, es * U.y);                      // A = eta U
+    Z[N + k] = make_double2(en * V.x, es * V.y);                  // B = eta V
+    Z[2 * N + k] = make_double2(Ph.x * U.x, Ph.y * U.y);          // C = Phi U
+    Z[3 * N + k] = make_double2(Ph.x * V.x, Ph.y * V.y);          // D = Phi V
+    Z[4 * N + k] = make_double2((U.x * U.x + V.x * V.x) * ke_scale,
+                                (U.y * U.y + V.y * V.y) * ke_scale);  // kinetic energy
+  }
+  __syncthreads();
+  passes<N, 0, 1, false, 5, THREADS>(Z, tw);
+
   const double ws = wsyn[j], wk = wke[j];
-  const double invn = 1.0 / (double)N;
-  double2* out = gan + ((size_t)b * J + j) * L * (kNumSlots * 2);
-  for (int o = 0; o < 5; ++o) {
-    for (int k = threadIdx.x; k < N; k += blockDim.x) {
-      double v[2];
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const double U = grid[(0 + s) * N + k], V = grid[(2 + s) * N + k];
-        const double Z = grid[(4 + s) * N + k], Ph = grid[(6 + s) * N + k];
-        const double eta = Z + (s ? cor_s : cor_n);
-        switch (o) {
-          case 0: v[s] = eta * U; break;
-          case 1: v[s] = eta * V; break;
-          case 2: v[s] = Ph * U; break;
-          case 3: v[s] = Ph * V; break;
-          default: v[s] = (U * U + V * V) * ke_scale; break;
-        }
-      }
-      buf0[k] = make_double2(v[0], v[1]);
+  const double h = 0.5 / (double)N;
+  // analysis layout: [b][m][j][fold][slot]
+  double2* out = gan + ((size_t)b * L * J + j) * (kNumSlots * 2);
+  for (int idx = threadIdx.x; idx < 5 * L; idx += THREADS) {
+    const int m = idx / 5, o = idx - 5 * m;
+    const double2 zm = Z[o * N + m], zc = Z[o * N + (m == 0 ? 0 : N - m)];
+    // X = FFT(north)/N, Y = FFT(south)/N; S = X + Y, A = X - Y
+    const double2 X = make_double2(h * (zm.x + zc.x), h * (zm.y - zc.y));
+    const double2 Y = make_double2(h * (zm.y + zc.y), -h * (zm.x - zc.x));
+    const double2 S = cadd(X, Y), A = csub(X, Y);
+    const double dm = (double)m;
+    double2* dst = out + (size_t)m * J * (kNumSlots * 2);
+    switch (o) {
+      case 0:  // A = eta U:  X_zeta = -(i m A) ws,  Y_delta = A ws
+        dst[0 * kNumSlots + kXZeta] = make_double2(dm * S.y * ws, -dm * S.x * ws);
+        dst[1 * kNumSlots + kXZeta] = make_double2(dm * A.y * ws, -dm * A.x * ws);
+        dst[0 * kNumSlots + kYDelta] = make_double2(S.x * ws, S.y * ws);
+        dst[1 * kNumSlots + kYDelta] = make_double2(A.x * ws, A.y * ws);
+        break;
+      case 1:  // B = eta V:  X_delta = (i m B) ws,  Y_zeta = B ws
+        dst[0 * kNumSlots + kXDelta] = make_double2(-dm * S.y * ws, dm * S.x * ws);
+        dst[1 * kNumSlots + kXDelta] = make_double2(-dm * A.y * ws, dm * A.x * ws);
+        dst[0 * kNumSlots + kYZeta] = make_double2(S.x * ws, S.y * ws);
+        dst[1 * kNumSlots + kYZeta] = make_double2(A.x * ws, A.y * ws);
+        break;
+      case 2:  // C = Phi U:  X_phi = -(i m C) ws
+        dst[0 * kNumSlots + kXPhi] = make_double2(dm * S.y * ws, -dm * S.x * ws);
+        dst[1 * kNumSlots + kXPhi] = make_double2(dm * A.y * ws, -dm * A.x * ws);
+        break;
+      case 3:  // D = Phi V:  Y_phi = D ws
+        dst[0 * kNumSlots + kYPhi] = make_double2(S.x * ws, S.y * ws);
+        dst[1 * kNumSlots + kYPhi] = make_double2(A.x * ws, A.y * ws);
+        break;
+      default:  // kinetic energy: X_ke = E wk
+        dst[0 * kNumSlots + kXKe] = make_double2(S.x * wk, S.y * wk);
+        dst[1 * kNumSlots + kXKe] = make_double2(A.x * wk, A.y * wk);
+        break;
     }
-    __syncthreads();
-    const double2* res = fft_stockham<false>(buf0, buf1, fp, tw);
-    for (int m = threadIdx.x; m <= T; m += blockDim.x) {
-      const double2 zm = res[m], zc = res[m == 0 ? 0 : N - m];
-      // X = FFT(north)/N, Y = FFT(south)/N
-      const double2 X = make_double2(0.5 * (zm.x + zc.x) * invn, 0.5 * (zm.y - zc.y) * invn);
-      const double2 Y = make_double2(0.5 * (zm.y + zc.y) * invn, -0.5 * (zm.x - zc.x) * invn);
-      const double2 S = make_double2(X.x + Y.x, X.y + Y.y);   // symmetric fold
-      const double2 A = make_double2(X.x - Y.x, X.y - Y.y);   // antisymmetric fold
-      const double dm = (double)m;
-      double2* dst = out + (size_t)m * (kNumSlots * 2);
-      // i m z = (-m z.y, m z.x)
-      switch (o) {
-        case 0:  // A = eta U:  X_zeta = -(i m A) ws,  Y_delta = A ws
-          dst[kXZeta * 2 + 0] = make_double2(dm * S.y * ws, -dm * S.x * ws);
-          dst[kXZeta * 2 + 1] = make_double2(dm * A.y * ws, -dm * A.x * ws);
-          dst[kYDelta * 2 + 0] = make_double2(S.x * ws, S.y * ws);
-          dst[kYDelta * 2 + 1] = make_double2(A.x * ws, A.y * ws);
-          break;
-        case 1:  // B = eta V:  X_delta = (i m B) ws,  Y_zeta = B ws
-          dst[kXDelta * 2 + 0] = make_double2(-dm * S.y * ws, dm * S.x * ws);
-          dst[kXDelta * 2 + 1] = make_double2(-dm * A.y * ws, dm * A.x * ws);
-          dst[kYZeta * 2 + 0] = make_double2(S.x * ws, S.y * ws);
-          dst[kYZeta * 2 + 1] = make_double2(A.x * ws, A.y * ws);
-          break;
-        case 2:  // C = Phi U:  X_phi = -(i m C) ws
-          dst[kXPhi * 2 + 0] = make_double2(dm * S.y * ws, -dm * S.x * ws);
-          dst[kXPhi * 2 + 1] = make_double2(dm * A.y * ws, -dm * A.x * ws);
-          break;
-        case 3:  // D = Phi V:  Y_phi = D ws
-          dst[kYPhi * 2 + 0] = make_double2(S.x * ws, S.y * ws);
-          dst[kYPhi * 2 + 1] = make_double2(A.x * ws, A.y * ws);
-          break;
-        default:  // kinetic energy: X_ke = E wk
-          dst[kXKe * 2 + 0] = make_double2(S.x * wk, S.y * wk);
-          dst[kXKe * 2 + 1] = make_double2(A.x * wk, A.y * wk);
-          break;
-      }
-    }
-    __syncthreads();
   }
 }
 
-cudaError_t configure_ring(size_t smem) {
-  return cudaFuncSetAttribute(k_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#define SDCSW_RING_SIZES(X) X(96, 256) X(192, 256) X(384, 256) X(768, 256) X(1536, 512)
+
+bool ring_supported(int nlon) {
+#define SDCSW_RING_OK(NV, TV) if (nlon == NV) return true;
+  SDCSW_RING_SIZES(SDCSW_RING_OK)
+#undef SDCSW_RING_OK
+  return false;
 }
+
+cudaError_t configure_ring(size_t smem) {
+  cudaError_t e = cudaSuccess;
+#define SDCSW_RING_CFG(NV, TV)                                                                     \
+  if (e == cudaSuccess)                                                                            \
+    e = cudaFuncSetAttribute(k_ring<NV, TV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  SDCSW_RING_SIZES(SDCSW_RING_CFG)
+#undef SDCSW_RING_CFG
+  return e;
+}
+
+size_t ring_smem_bytes(int nlon) { return (size_t)nlon * 6 * sizeof(double2); }
 
 cudaError_t launch_ring(const Plan& p, int nb, cudaStream_t s) {
   dim3 grid(p.J, nb);
-  k_ring<<<grid, p.ring_threads, p.ring_smem, s>>>(p.fsyn, p.gan, p.J, p.T, p.mu, p.wsyn, p.wke,
-                                                   p.twiddle, p.fft, 2.0 * p.omega);
-  return cudaGetLastError();
+#define SDCSW_RING_LAUNCH(NV, TV)                                                                  \
+  if (p.nlon == NV) {                                                                              \
+    k_ring<NV, TV><<<grid, TV, p.ring_smem, s>>>(p.fsyn, p.gan, p.J, p.T, p.mu, p.wsyn, p.wke,      \
+                                                 p.twiddle, 2.0 * p.omega);                        \
+    return cudaGetLastError();                                                                     \
+  }
+  SDCSW_RING_SIZES(SDCSW_RING_LAUNCH)
+#undef SDCSW_RING_LAUNCH
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace sdcsw

@@ -23,6 +23,8 @@ int cuda_status(cudaError_t e, const char* where) {
 }
 
 cudaError_t configure_ring(size_t smem);
+size_t ring_smem_bytes(int nlon);
+bool ring_supported(int nlon);
 
 cudaError_t f_expl(const Plan& p, const double2* u, double2* fe, int nb, cudaStream_t s,
                    int* step_counter) {
@@ -81,15 +83,13 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
     return SDCSW_ERR_PARAM;
   }
   const int T = cfg->trunc, nlat = cfg->nlat, nlon = cfg->nlon;
-  if (T < 1 || nlat % 2 || nlat < T + 1 || (nlat / 2) % 16 || nlon < 2 * T + 2 ||
+  if (T < 1 || nlat % 2 || nlat < T + 1 || (nlat / 2) % 16 || nlon < 2 * T + 2 || nlon > 1536 ||
       cfg->max_batch < 1 || T > 4000) {
-    set_error("sdcsw_plan_create: unsupported size (need nlat/2 % 16 == 0, nlon >= 2T+2)");
+    set_error("sdcsw_plan_create: unsupported size (need nlat/2 % 16 == 0, 2T+2 <= nlon <= 1536)");
     return SDCSW_ERR_PARAM;
   }
-  int k = nlon;
-  while (k % 2 == 0) k /= 2;
-  if (k != 1 && k != 3) {
-    set_error("sdcsw_plan_create: nlon must be 2^k or 3*2^k");
+  if (!ring_supported(nlon)) {
+    set_error("sdcsw_plan_create: nlon must be one of 96, 192, 384, 768, 1536 (3*2^k)");
     return SDCSW_ERR_PARAM;
   }
   cudaError_t e = cudaSetDevice(device);
@@ -129,27 +129,40 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   FftPlan fp;
   std::memset(&fp, 0, sizeof(fp));
   fp.n = nlon;
-  int rem = nlon, ns = 0;
+  int rem = nlon, ns = 0, k2 = 0;
   bool three = rem % 3 == 0;
   if (three) rem /= 3;
-  while (rem % 4 == 0) { fp.radix[ns++] = 4; rem /= 4; }
-  if (rem == 2) { fp.radix[ns++] = 2; rem = 1; }
+  while (rem > 1) { rem /= 2; ++k2; }
+  // 2^k2 = 8^a 4^b (2 if k2 == 1): fewest passes
+  int n8 = k2 / 3, n4 = 0, n2 = 0;
+  if (k2 % 3 == 1) { if (n8 > 0) { n8 -= 1; n4 = 2; } else { n2 = 1; } }
+  if (n2) {
+    set_error("sdcsw_plan_create: nlon too small (radix-2 pass not supported)");
+    delete h;
+    return SDCSW_ERR_PARAM;
+  }
+  if (k2 % 3 == 2) n4 = 1;
+  for (int q = 0; q < n8; ++q) fp.radix[ns++] = 8;
+  for (int q = 0; q < n4; ++q) fp.radix[ns++] = 4;
+  for (int q = 0; q < n2; ++q) fp.radix[ns++] = 2;
   if (three) fp.radix[ns++] = 3;
   fp.nstages = ns;
   p.fft = fp;
   // analysis work list
   std::vector<int> work;
-  p.anal_warps = 4;
+  // row tiles per CTA: small truncations split K over the 4 warps (more warps
+  // in flight), large ones give each warp its own row tile (B reuse via L1)
+  p.anal_wj = T < 200 ? 1 : (T < 400 ? 2 : 4);
+  p.synth_wj = T < 200 ? 1 : (T < 400 ? 2 : 4);
+  while ((J / kRowsPerWarp) % p.synth_wj) p.synth_wj /= 2;
   for (int m = 0; m <= T; ++m) {
     const int rows = rowoff[m + 1] - rowoff[m];
-    const int per = kRowsPerWarp * p.anal_warps;
+    const int per = kRowsPerWarp * p.anal_wj;
     for (int rb = 0; rb * per < rows; ++rb) work.push_back((m << 16) | rb);
   }
   p.n_anal_work = (int)work.size();
-  const int jt = J / kRowsPerWarp;
-  p.synth_warps = jt % 4 == 0 ? 4 : (jt % 3 == 0 ? 3 : (jt % 2 == 0 ? 2 : 1));
   p.ring_threads = 256;
-  p.ring_smem = (size_t)nlon * (2 * sizeof(double2) + 8 * sizeof(double));
+  p.ring_smem = ring_smem_bytes(nlon);
 
   const size_t tab = (size_t)p.rows * J;
   if ((e = upload(&p.ptab, ptab, tab, (size_t)16 * J)) != cudaSuccess ||
@@ -294,7 +307,7 @@ int sdcsw_workspace(sdcsw_plan* h, int which, void** ptr, long long* bytes) {
   const Plan& p = h->p;
   const long long per = (long long)p.max_batch * p.J * p.L * 2 * sizeof(double2);
   *ptr = which == 0 ? (void*)p.fsyn : (void*)p.gan;
-  *bytes = which == 0 ? per * 4 : per * kNumSlots;
+  *bytes = which == 0 ? per * 4 : per * kNumSlots;  // see sdcsw.h for the layouts
   return SDCSW_OK;
 }
 
@@ -316,19 +329,24 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
   cudaError_t e = f_expl(p, u, st->fe0, 1, s, counter);
   if (e != cudaSuccess) return e;
   if (st->mode == 0) {
+    // fi alternates between two buffers: every node reads all fi_j while
+    // writing its own fi_m, so the update cannot be in place
     const int cstride = M * (M + 4);
+    double2* fi_cur = st->fi;
     for (int k = 1; k < K; ++k) {
       const bool first = k == 1;
+      double2* fi_new = (k % 2) ? st->fi : st->fiB;
       e = launch_sweep_nodes(p, M, 0, M, st->coef.data() + (size_t)(k - 1) * cstride, u,
-                             first ? st->fe0 : st->fe, first ? 0 : 1, st->fi, first ? 0 : 1,
-                             first, st->ustage, st->fi, s);
+                             first ? st->fe0 : st->fe, first ? 0 : 1, fi_cur, first ? 0 : 1,
+                             first, st->ustage, fi_new, s);
       if (e != cudaSuccess) return e;
       e = f_expl(p, st->ustage, st->fe, M, s, nullptr);
       if (e != cudaSuccess) return e;
+      fi_cur = fi_new;
     }
     const bool first = K == 1;
     return launch_final_node(p, M, st->coef.data() + (size_t)(K - 1) * cstride, u,
-                             first ? st->fe0 : st->fe, first ? 0 : 1, st->fi, first ? 0 : 1,
+                             first ? st->fe0 : st->fe, first ? 0 : 1, fi_cur, first ? 0 : 1,
                              first, u, diverged, counter, s);
   }
   // serial SDC: old/new tendency buffers alternate between sweeps
@@ -400,7 +418,7 @@ int sdcsw_stepper_create(sdcsw_plan* h, int mode, int n_nodes, int n_sweeps, con
   }
   const Plan& p = h->p;
   s->S = (size_t)3 * p.C;
-  const size_t nstates = 1 + 3 * (size_t)M + (mode == 1 ? (size_t)3 * M + 1 : 0);
+  const size_t nstates = 1 + 4 * (size_t)M + (mode == 1 ? (size_t)2 * M + 1 : 0);
   cudaError_t e = cudaSetDevice(p.device);
   if (e == cudaSuccess) e = cudaMalloc(&s->buf, nstates * s->S * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc(&s->flags, 2 * sizeof(int));
@@ -417,10 +435,10 @@ int sdcsw_stepper_create(sdcsw_plan* h, int mode, int n_nodes, int n_sweeps, con
   s->fe = q; q += M * s->S;
   s->fi = q; q += M * s->S;
   s->ustage = q; q += M * s->S;
+  s->fiB = q; q += M * s->S;
   if (mode == 1) {
     s->quad = q; q += M * s->S;
     s->feB = q; q += M * s->S;
-    s->fiB = q; q += M * s->S;
     s->corr = q; q += s->S;
   }
   const int init[2] = {INT_MAX, 0};
