@@ -160,3 +160,28 @@ def march(problem, u_init, dt, n_steps, step_fn, checkpoint_interval=None, name=
                 times.append(step * dt)
                 states.append(state.copy())
     return times, states
+
+
+class DahlquistOracle:
+    """u' = lambda_I u + lambda_E u with closed-form solve (ref problems/dahlquist.py:9-53)."""
+
+    def __init__(self, lambda_impl, lambda_expl):
+        from paper_2403_20135_b200.core import WorkCounters
+
+        self.lambda_impl = complex(lambda_impl)
+        self.lambda_expl = complex(lambda_expl)
+        self.counters = WorkCounters()
+
+    def f_expl(self, state):
+        self.counters.tally_f_expl()
+        return self.lambda_expl * state
+
+    def f_impl(self, state):
+        self.counters.tally_f_impl()
+        return self.lambda_impl * state
+
+    def implicit_solve(self, alpha, beta, guess=None):
+        if alpha == 0.0:
+            return beta.copy()
+        self.counters.tally_solve()
+        return beta / (1.0 - alpha * self.lambda_impl)

@@ -1,0 +1,236 @@
+"""GPU kernel-level parity through the C ABI: bit-exact node arithmetic,
+deterministic and batch-invariant transforms, device divergence detection,
+larger truncations."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import sdc as osdc
+from oracle.sphere_swe import SphericalShallowWaterOracle, relative_l2
+from paper_2403_20135_b200 import (
+    CollocationTable,
+    DiagonalSdcStepper,
+    SdcConfig,
+    SerialSdcStepper,
+    SweepMode,
+    integrate,
+    random_initial_state,
+)
+from paper_2403_20135_b200.errors import DivergenceError
+
+pytestmark = pytest.mark.gpu
+
+_P = {}
+
+
+def gpu(trunc, max_batch=8):
+    key = (trunc, max_batch)
+    if key not in _P:
+        from paper_2403_20135_b200.problem import SphericalShallowWater
+
+        _P[key] = SphericalShallowWater(trunc, max_batch=max_batch)
+    return _P[key]
+
+
+def oracle_for(p, same_tables=False):
+    key = ("oracle", p.trunc, same_tables)
+    if key not in _P:
+        g = p.grid
+        tables = None
+        if same_tables:
+            from paper_2403_20135_b200.sphere import gaussian_latitudes, legendre_tables
+
+            mu, w = gaussian_latitudes(g.nlat)
+            pt, ht = legendre_tables(g.trunc, mu)
+            tables = (mu, w, pt, ht, p.m_of, p.n_of)
+        _P[key] = SphericalShallowWaterOracle(g.trunc, g.nlat, g.nlon, tables=tables)
+    return _P[key]
+
+
+def test_sweep_nodes_and_final_node_bit_exact():
+    """sdcsw_sweep_nodes / sdcsw_final_node == oracle diag_rhs + solve + f_impl, bitwise."""
+    import torch
+
+    from paper_2403_20135_b200.integrators import diagonal_step_coefficients
+    from paper_2403_20135_b200.parallel_nodes import CudaNodeBackend
+
+    p = gpu(63)
+    o = oracle_for(p)
+    rng = np.random.default_rng(0)
+    m_count, k_count, dt = 4, 3, 90.0
+    S = p.state_size
+    cfg = SdcConfig(table=CollocationTable.radau_right(m_count), n_sweeps=k_count,
+                    mode=SweepMode.DIAGONAL_SEQUENTIAL)
+    coef = diagonal_step_coefficients(cfg, dt, p.mean_geopotential)
+    blk = m_count * (m_count + 4)
+    u0 = rng.standard_normal(S) + 1j * rng.standard_normal(S)
+    fe = rng.standard_normal((m_count, S)) + 1j * rng.standard_normal((m_count, S))
+    fi = rng.standard_normal((m_count, S)) + 1j * rng.standard_normal((m_count, S))
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(p.device)  # noqa: E731
+    be = CudaNodeBackend(p)
+    u_out = p.empty_states(m_count)
+    fi_out = p.empty_states(m_count)
+    c1 = np.ascontiguousarray(coef[blk : 2 * blk])  # sweep index 2
+    be.sweep_nodes(m_count, 0, m_count, c1, dev(u0), dev(fe), 1, dev(fi), 1, False, u_out, fi_out)
+    slots = osdc.Slots(u0, fe[0], fi[0], m_count)
+    slots.fe = [fe[j] for j in range(m_count)]
+    slots.fi = [fi[j] for j in range(m_count)]
+    from paper_2403_20135_b200.collocation import DiagonalPreconditioner, diagonal_coefficients
+
+    table = cfg.table
+    diag = diagonal_coefficients(DiagonalPreconditioner.MIN_SR_FLEX, table, 2)
+    osdc.diag_rhs(slots, table.q_matrix, dt, diag)
+    for m in range(m_count):
+        ref_u = o.implicit_solve(dt * diag[m], slots.fi[m])
+        assert np.array_equal(u_out[m].cpu().numpy(), ref_u)
+        assert np.array_equal(fi_out[m].cpu().numpy(), o.f_impl(ref_u))
+    # final node (sweep index K) and the first-sweep aliasing (stride 0, inline f_I(u0))
+    out = p.empty_states(1)
+    fin = np.ascontiguousarray(coef[(k_count - 1) * blk :])
+    be.final_node(m_count, fin, dev(u0), dev(fe), 1, dev(fi), 1, False, out)
+    slots = osdc.Slots(u0, fe[0], fi[0], m_count)
+    slots.fe = [fe[j] for j in range(m_count)]
+    slots.fi = [fi[j] for j in range(m_count)]
+    diag = diagonal_coefficients(DiagonalPreconditioner.MIN_SR_FLEX, table, k_count)
+    ref = o.implicit_solve(dt * diag[-1], osdc.final_rhs(slots, table.q_matrix, dt, diag))
+    assert np.array_equal(out[0].cpu().numpy(), ref)
+    be.sweep_nodes(m_count, 1, 2, np.ascontiguousarray(coef[:blk]), dev(u0), dev(fe[0]), 0,
+                   dev(fi), 0, True, u_out, fi_out)
+    slots = osdc.Slots(u0, fe[0], o.f_impl(u0), m_count)
+    diag = diagonal_coefficients(DiagonalPreconditioner.MIN_SR_FLEX, table, 1)
+    osdc.diag_rhs(slots, table.q_matrix, dt, diag)
+    for q, m in enumerate((1, 2)):
+        assert np.array_equal(u_out[q].cpu().numpy(), o.implicit_solve(dt * diag[m], slots.fi[m]))
+
+
+def test_transforms_deterministic_and_batch_invariant():
+    import torch
+
+    p = gpu(127)
+    states = np.stack([random_initial_state(p.grid, s) for s in range(6)])
+    states[:, : p.n_coef] = 3e-3 * states[:, p.n_coef : 2 * p.n_coef] * 1e6
+    u = torch.from_numpy(states).to(p.device)
+    outs = []
+    for nb in (6, 6, 4, 1):
+        o = p.empty_states(6)
+        if nb == 6:
+            p.f_expl_device(u, o, 6)
+        elif nb == 4:
+            p.f_expl_device(u[:4].contiguous(), o[:4], 4)
+            p.f_expl_device(u[4:].contiguous(), o[4:], 2)
+        else:
+            for b in range(6):
+                p.f_expl_device(u[b : b + 1].contiguous(), o[b : b + 1], 1)
+        outs.append(o.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])  # run-to-run deterministic
+    assert np.array_equal(outs[0], outs[2])  # independent of the batch split
+    assert np.array_equal(outs[0], outs[3])
+
+
+@pytest.mark.parametrize("trunc,tol", [(255, 1e-11)])
+def test_f_expl_large_truncation(trunc, tol):
+    p = gpu(trunc, max_batch=4)
+    o = oracle_for(p)
+    u = random_initial_state(p.grid, 2)
+    u[: p.n_coef] = 5e-3 * u[p.n_coef : 2 * p.n_coef] * 1e6
+    assert max(relative_l2(p.f_expl(u), o.f_expl(u), o)) < tol
+
+
+def test_t511_properties():
+    """T511 (config 3 size): size-independent checks - exact mass conservation,
+    finiteness, f_E linear in Phi' where it should be, solve contract."""
+    import torch
+
+    from _contracts import assert_implicit_solve_contract
+
+    p = gpu(511, max_batch=5)
+    u0 = random_initial_state(p.grid, 3)
+    cfg = SdcConfig(table=CollocationTable.radau_right(5), n_sweeps=5,
+                    mode=SweepMode.DIAGONAL_PARALLEL, time_threads=5)
+    traj = integrate(p, u0, 30.0, 3, DiagonalSdcStepper(cfg))
+    u = traj.states[-1]
+    assert np.isfinite(u).all()
+    assert u[0] == 0.0  # mean geopotential anomaly: exactly conserved (H_00 = 0)
+    assert u[p.n_coef] == 0.0 and u[2 * p.n_coef] == 0.0
+    beta = u.copy()
+    beta[: p.n_coef] += 1e2 * u[p.n_coef : 2 * p.n_coef] * 1e4
+    assert_implicit_solve_contract(p, beta)
+    cfg.close()
+    del torch
+
+
+def test_config1_parity_20_steps():
+    """BASELINE config 1 (T127, M=4, K=4, dt=90 s) on one GPU, 20 steps, <= 1e-10."""
+    p = gpu(127)
+    o = oracle_for(p)
+    u0 = random_initial_state(p.grid, 1)
+    table = CollocationTable.radau_right(4)
+    cfg = SdcConfig(table=table, n_sweeps=4, mode=SweepMode.DIAGONAL_PARALLEL, time_threads=4)
+    traj = integrate(p, u0, 90.0, 20, DiagonalSdcStepper(cfg), checkpoint_interval=10)
+    ref = u0
+    for _ in range(20):
+        ref = osdc.dsdc(o, ref, 90.0, table, 4)
+    assert max(relative_l2(traj.states[-1], ref, o)) <= 1e-10
+    assert traj.times == [0.0, 900.0, 1800.0]
+    assert [r.n_solve for r in traj.reports] == [13] * 20
+    cfg.close()
+
+
+def test_serial_sdc_parity_10_steps():
+    p = gpu(63)
+    o = oracle_for(p)
+    u0 = random_initial_state(p.grid, 4)
+    table = CollocationTable.radau_right(3)
+    cfg = SdcConfig(table=table, n_sweeps=3, mode=SweepMode.SERIAL)
+    traj = integrate(p, u0, 120.0, 10, SerialSdcStepper(cfg))
+    ref = u0
+    for _ in range(10):
+        ref = osdc.serial_sdc(o, ref, 120.0, table, 3)
+    assert max(relative_l2(traj.states[-1], ref, o)) <= 1e-10
+    cfg.close()
+
+
+def test_device_divergence_reports_step():
+    p = gpu(63)
+    u0 = random_initial_state(p.grid, 0) * 1e140  # overflows within the first steps
+    table = CollocationTable.radau_right(3)
+    cfg = SdcConfig(table=table, n_sweeps=3, mode=SweepMode.DIAGONAL_SEQUENTIAL)
+    o = oracle_for(p)
+    step = lambda pr, s, dt: osdc.dsdc(pr, s, dt, table, 3)  # noqa: E731
+    with pytest.raises(DivergenceError) as ref:
+        osdc.march(o, u0, 120.0, 6, step)
+    with pytest.raises(DivergenceError) as got:
+        integrate(p, u0, 120.0, 6, DiagonalSdcStepper(cfg), checkpoint_interval=6)
+    assert got.value.step_index == ref.value.step_index
+    cfg.close()
+
+
+def test_node_parallel_single_rank_matches_fused_stepper():
+    """The multi-GPU orchestration at world size 1 (NCCL) equals the fused stepper bitwise."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_20135_b200.integrators import DeviceStepper
+    from paper_2403_20135_b200.parallel_nodes import CudaNodeBackend, NodeParallelDsdc
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29611")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    p = gpu(63)
+    table = CollocationTable.radau_right(3)
+    cfg = SdcConfig(table=table, n_sweeps=3, mode=SweepMode.DIAGONAL_PARALLEL, time_threads=1)
+    u0 = torch.from_numpy(random_initial_state(p.grid, 8)).to(p.device)
+    a = u0.clone()
+    npd = NodeParallelDsdc(CudaNodeBackend(p), cfg, 120.0, p.mean_geopotential, p.state_size)
+    for _ in range(3):
+        npd.step(a)
+    b = u0.clone()
+    st = DeviceStepper(p, cfg, 120.0, serial=False)
+    st.run(b, 3)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    st.close()
+    dist.destroy_process_group()
