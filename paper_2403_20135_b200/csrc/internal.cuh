@@ -43,6 +43,8 @@ struct Plan {
   int* moff;        // [T+2] triangular offsets
   double* lam;      // [C]
   double* inv_nn;   // [C] 1/(n(n+1)), 0 for n = 0
+  double2* xscale;  // [C] (m a / (n(n+1)), a / (n(n+1))): synthesis B-operand scales
+  int* idx_row;     // [C] absolute packed table row of coefficient idx
   double* mu;       // [J] northern nodes
   double* wsyn;     // [J] 2 pi w_j / (a (1 - mu_j^2))
   double* wke;      // [J] 2 pi w_j
@@ -55,6 +57,8 @@ struct Plan {
   double2* fsyn;    // [max_batch][J][L][4][2]
   double2* gan;     // [max_batch][L][J][2 (S,A)][kNumSlots]  (GEMM-ready for the analysis)
   double* coef_dev; // small per-call coefficient staging [kCoefCap]
+  double* xsyn;     // [rows][max_batch][12] synthesis B operand for API calls
+  int xsyn_nb;      // record batch of the last API prep (padding rows zero for it)
   int ring_threads;
   size_t ring_smem;
 };
@@ -64,8 +68,42 @@ constexpr int kCoefCap = 4096;
 void set_error(const std::string& msg);
 int cuda_status(cudaError_t e, const char* where);
 
+// Synthesis B operand ("xsyn"): per packed table row r and batch entry b a
+// record of kXsyn doubles at xsyn[(r * nb + b) * kXsyn]:
+//   P part: U re, U im, V re, V im, zeta re, zeta im, Phi re, Phi im
+//   H part: U re, U im, V re, V im
+// with U_P = i m chi / a, V_P = i m psi / a, U_H = -psi / a, V_H = chi / a.
+// Producers write only valid rows; padding rows of a buffer must stay zero.
+constexpr int kXsyn = 12;
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void write_xsyn_half(double* __restrict__ rec, int ri, double phi,
+                                                double zeta, double delta, double2 sc) {
+  // ri = 0 holds real parts, ri = 1 imaginary parts; (x + i y)(-i s) = s y - i s x
+  const double sm = sc.x, sa = sc.y;
+  if (ri == 0) {
+    rec[1] = -sm * delta;  // U_P im
+    rec[3] = -sm * zeta;   // V_P im
+    rec[4] = zeta;
+    rec[6] = phi;
+    rec[8] = sa * zeta;    // U_H re
+    rec[10] = -sa * delta; // V_H re
+  } else {
+    rec[0] = sm * delta;   // U_P re
+    rec[2] = sm * zeta;    // V_P re
+    rec[5] = zeta;
+    rec[7] = phi;
+    rec[9] = sa * zeta;    // U_H im
+    rec[11] = -sa * delta; // V_H im
+  }
+}
+
+#endif
+
 // launchers (return cudaError_t of the launch)
-cudaError_t launch_synthesis(const Plan& p, const double2* u, int nb, cudaStream_t s,
+cudaError_t launch_synth_prep(const Plan& p, const double2* u, int nb, double* xsyn,
+                              cudaStream_t s);
+cudaError_t launch_synthesis(const Plan& p, const double* xsyn, int nb, cudaStream_t s,
                              int* step_counter);
 cudaError_t launch_ring(const Plan& p, int nb, cudaStream_t s);
 cudaError_t launch_analysis(const Plan& p, double2* fe, int nb, cudaStream_t s);
@@ -76,11 +114,11 @@ cudaError_t launch_solve(const Plan& p, const double* coef_host, const double2* 
 cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, const double* coef_host,
                                const double2* u0, const double2* fe, long long fe_stride,
                                const double2* fi, long long fi_stride, int first, double2* u_out,
-                               double2* fi_out, cudaStream_t s);
+                               double2* fi_out, double* xsyn_out, cudaStream_t s);
 cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, const double2* u0,
                               const double2* fe, long long fe_stride, const double2* fi,
                               long long fi_stride, int first, double2* u_out, int* diverged,
-                              const int* step_counter, cudaStream_t s);
+                              const int* step_counter, double* xsyn_out, cudaStream_t s);
 cudaError_t launch_serial_quad(const Plan& p, int M, const double* w_host, const double2* u0,
                                const double2* fe, long long fe_stride, const double2* fi,
                                long long fi_stride, int first, double2* quad, cudaStream_t s);
@@ -88,15 +126,18 @@ cudaError_t launch_serial_node(const Plan& p, int M, int m, const double* coef_h
                                const double2* quad, const double2* corr, const double2* u0,
                                const double2* fi_old, int first, double2* u_out, double2* u_out2,
                                double2* fi_new, int* diverged, const int* step_counter,
-                               cudaStream_t s);
+                               double* xsyn_out, cudaStream_t s);
 cudaError_t launch_serial_update(const Plan& p, int m, double we, double wi, double2* corr,
                                  const double2* fe_new, const double2* fe_old,
                                  const double2* fi_new, const double2* fi_old, const double2* u0,
                                  int first, cudaStream_t s);
 cudaError_t launch_check_finite(const double* x, long long n, int* flag, cudaStream_t s);
 
-// f_E = synthesis -> ring -> analysis
-cudaError_t f_expl(const Plan& p, const double2* u, double2* fe, int nb, cudaStream_t s,
+// f_E = (prep) -> synthesis -> ring -> analysis; f_expl_prepped starts from an
+// xsyn operand a producer kernel already wrote
+cudaError_t f_expl(Plan& p, const double2* u, double2* fe, int nb, cudaStream_t s,
                    int* step_counter);
+cudaError_t f_expl_prepped(const Plan& p, const double* xsyn, double2* fe, int nb, cudaStream_t s,
+                           int* step_counter);
 
 }  // namespace sdcsw

@@ -16,6 +16,20 @@
 //   out[n,c] = sum_j P[n,j] Xfold[j,c] + sum_j H[n,j] Yfold[j,c]
 //   with the fold (N+S or N-S) chosen by the parity class of row n.
 #include "internal.cuh"
+#ifndef SDCSW_EXP
+#define SDCSW_EXP 0
+#endif
+#if SDCSW_EXP == 3
+__device__ unsigned long long g_times[1 << 17];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+extern "C" int sdcsw_debug_times(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_times, n * sizeof(unsigned long long));
+}
+#endif
 
 namespace sdcsw {
 
@@ -38,18 +52,33 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 constexpr int kWarps = 4;
 
 // ---------------------------------------------------------------------------
-// synthesis: u [nb][3][C] -> fsyn [nb][J][L][4 (U,V,zeta,Phi)][2 (N,S)]
-// grid (J / (16 WJ), T+1, ceil(nb/NB)), block 32*kWarps
-// P columns: (U,V) of all b (4 NB), then (zeta,Phi) of all b; H columns: (U,V).
+// synthesis B-operand prep for API calls: xsyn record per (valid row, b)
+// grid (ceil(2C/256), nb): one thread per (coefficient, re/im, batch entry)
 // ---------------------------------------------------------------------------
-template <int NB>
+__global__ void __launch_bounds__(256) k_synth_prep(const double* __restrict__ u, int C2, int nb,
+                                                    const double2* __restrict__ xscale,
+                                                    const int* __restrict__ idx_row,
+                                                    double* __restrict__ xsyn) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= C2) return;
+  const int b = blockIdx.y;
+  const double* s = u + (size_t)b * 3 * C2;
+  const int idx = e >> 1;
+  double* rec = xsyn + ((size_t)idx_row[idx] * nb + b) * kXsyn;
+  write_xsyn_half(rec, e & 1, s[e], s[C2 + e], s[2 * C2 + e], xscale[idx]);
+}
+
+// ---------------------------------------------------------------------------
+// synthesis: xsyn -> fsyn [nb][J][L][4 (U,V,zeta,Phi)][2 (N,S)]
+// grid (J / (16 WJ), T+1, ceil(nb/NB)), block 32*kWarps
+// column tile c = batch entry b0 + c: P cols (U,V,zeta,Phi) x (re,im);
+// the H tile reuses the same column positions (zeta/Phi columns zero).
+// ---------------------------------------------------------------------------
+template <int NB, int PF>
 __global__ void __launch_bounds__(32 * kWarps) k_synthesis(
-    const double2* __restrict__ u, int nb, int T, int J, int C, const double* __restrict__ ptab,
+    const double* __restrict__ xsyn, int nb, int T, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
-    const int* __restrict__ n_even, const int* __restrict__ row_n, const int* __restrict__ moff,
-    const double* __restrict__ inv_nn, double radius, double2* __restrict__ fsyn,
-    int* step_counter, int WJ) {
-  constexpr int TH = (NB + 1) / 2;  // H tiles
+    const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ) {
   constexpr int NACC = 2 * NB * 4;  // doubles per lane (E and O, re and im)
   __shared__ double red[kWarps * 32 * NACC];
 
@@ -59,6 +88,12 @@ __global__ void __launch_bounds__(32 * kWarps) k_synthesis(
   const int WK = kWarps / WJ;
   const int jt = warp % WJ, ks = warp / WJ;
   const int j0 = (blockIdx.x * WJ + jt) * kRowsPerWarp;
+#if SDCSW_EXP == 3
+  const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
+  unsigned long long t_start = gtimer();
+  int smid;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+#endif
   const int b0 = blockIdx.z * NB;
   const int L = T + 1;
   if (step_counter != nullptr && (blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0)
@@ -67,26 +102,17 @@ __global__ void __launch_bounds__(32 * kWarps) k_synthesis(
   const int r0m = rowoff[m];
   const int rows = rowoff[m + 1] - r0m;
   const int le = n_even[m];
-  const int mo = moff[m];
+#if SDCSW_EXP == 3
+  unsigned long long t_pro = 0, t_f1 = 0, t_kl = 0;
+  if (rows < 0) t_pro = 1;  // force the loads to complete
+  t_pro += gtimer();
+#endif
   const double* P = ptab + (size_t)r0m * J + j0 + g;
   const double* H = htab + (size_t)r0m * J + j0 + g;
-  const double dm = (double)m;
-
-  // this lane's B columns: P tile c holds column 8c + g
-  int pb[NB], pf[NB], pr[NB];
-#pragma unroll
-  for (int c = 0; c < NB; ++c) {
-    const int col = 8 * c + g;
-    if (col < 4 * NB) { pb[c] = col >> 2; pf[c] = (col & 3) >> 1; }      // 0 = U, 1 = V
-    else { pb[c] = (col - 4 * NB) >> 2; pf[c] = 2 + (((col - 4 * NB) & 3) >> 1); }  // zeta, Phi
-    pr[c] = col & 1;
-  }
-  const double2* ub[NB];
-#pragma unroll
-  for (int c = 0; c < NB; ++c) {
-    const int bb = b0 + pb[c] < nb ? b0 + pb[c] : -1;
-    ub[c] = bb >= 0 ? u + (size_t)bb * 3 * C + mo - m : nullptr;
-  }
+  // B fragment of tile c: record (row r0m + r + t, batch b0 + c), P column g / H column g (g < 4)
+  const int nbv = nb - b0 < NB ? nb - b0 : NB;
+  const double* X = xsyn + ((size_t)r0m * nb + b0) * kXsyn;
+  const int rstride = nb * kXsyn;
 
   double accE[2][NB][2], accO[2][NB][2];
 #pragma unroll
@@ -94,99 +120,125 @@ __global__ void __launch_bounds__(32 * kWarps) k_synthesis(
 #pragma unroll
     for (int c = 0; c < NB; ++c) accE[a][c][0] = accE[a][c][1] = accO[a][c][0] = accO[a][c][1] = 0.0;
 
-  const int nsteps = rows >> 2;
-#pragma unroll 4
-  for (int s = ks; s < nsteps; s += WK) {
+  // K loop in two branch-free ranges (n - m even rows, then odd rows), with
+  // the fragments of step s + WK loaded before the DMMAs of step s.
+  struct Frag {
+    double aP0, aP1, aH0, aH1, bP[NB], bH[NB];
+  };
+  auto fetch = [&](int s, Frag& f) {
     const int r = 4 * s;
     const size_t off = (size_t)(r + t) * J;
-    const double aP0 = __ldg(P + off), aP1 = __ldg(P + off + 8);
-    const double aH0 = __ldg(H + off), aH1 = __ldg(H + off + 8);
-    const int n = __ldg(row_n + r0m + r + t);
-    double bP[NB], bH[TH];
+#if SDCSW_EXP == 1
+    f.aP0 = f.aP1 = f.aH0 = f.aH1 = 1e-3 * (double)r;
+#else
+    f.aP0 = __ldg(P + off);
+    f.aP1 = __ldg(P + off + 8);
+    f.aH0 = __ldg(H + off);
+    f.aH1 = __ldg(H + off + 8);
+#endif
+    const double* rec = X + (size_t)(r + t) * rstride;
 #pragma unroll
     for (int c = 0; c < NB; ++c) {
-      double x = 0.0, y = 0.0;
-      if (n >= 0 && ub[c] != nullptr) {
-        const double il = __ldg(inv_nn + mo + n - m);
-        const double2* s3 = ub[c] + n;
-        const int f = pf[c];
-        if (f == 0) {  // U: P part i m chi / a = -i m a il delta ; H part -psi/a = a il zeta
-          const double2 d = s3[2 * C];
-          const double sm = dm * radius * il;
-          x = pr[c] ? -sm * d.x : sm * d.y;
-          if (c < TH) { const double2 z = s3[C]; y = radius * il * (pr[c] ? z.y : z.x); }
-        } else if (f == 1) {  // V: P part i m psi / a ; H part chi / a = -a il delta
-          const double2 z = s3[C];
-          const double sm = dm * radius * il;
-          x = pr[c] ? -sm * z.x : sm * z.y;
-          if (c < TH) { const double2 d = s3[2 * C]; y = -radius * il * (pr[c] ? d.y : d.x); }
-        } else {
-          const double2 v = f == 2 ? s3[C] : s3[0];
-          x = pr[c] ? v.y : v.x;
+      const bool ok = c < nbv;
+#if SDCSW_EXP == 2
+      f.bP[c] = f.bH[c] = ok ? 1e-3 * r : 0.0;
+#else
+      f.bP[c] = ok ? __ldg(rec + c * kXsyn + g) : 0.0;
+      f.bH[c] = (ok && g < 4) ? __ldg(rec + c * kXsyn + 8 + g) : 0.0;
+#endif
+    }
+  };
+  const int nsteps = rows >> 2;
+  const int se = le >> 2;  // steps [0, se) are even-class rows
+#pragma unroll
+  for (int cls = 0; cls < 2; ++cls) {
+    const int lo = cls == 0 ? 0 : se, hi = cls == 0 ? se : nsteps;
+    int s = lo + ((ks - lo) % WK + WK) % WK;  // first step of this warp in [lo, hi)
+    if (s >= hi) continue;
+    // PF = prefetch distance in steps (2 for latency-bound small truncations,
+    // 1 where occupancy matters more)
+    Frag cur, nx1, nx2;
+    fetch(s, cur);
+    if (PF == 2) fetch(s + WK < hi ? s + WK : s, nx1);
+#if SDCSW_EXP == 3
+    if (cls == 0) { if (cur.aP0 == 12345.0) t_f1 = 1; t_f1 += gtimer(); }
+#endif
+    for (; s < hi; s += WK) {
+      const int sn = s + PF * WK < hi ? s + PF * WK : s;  // clamped: always a valid address
+      fetch(sn, PF == 2 ? nx2 : nx1);
+      if (cls == 0) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          dmma(accE[0][c], cur.aP0, cur.bP[c]); dmma(accE[1][c], cur.aP1, cur.bP[c]);
+          dmma(accO[0][c], cur.aH0, cur.bH[c]); dmma(accO[1][c], cur.aH1, cur.bH[c]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          dmma(accO[0][c], cur.aP0, cur.bP[c]); dmma(accO[1][c], cur.aP1, cur.bP[c]);
+          dmma(accE[0][c], cur.aH0, cur.bH[c]); dmma(accE[1][c], cur.aH1, cur.bH[c]);
         }
       }
-      bP[c] = x;
-      if (c < TH) bH[c] = y;
-    }
-    if (r < le) {
-#pragma unroll
-      for (int c = 0; c < NB; ++c) { dmma(accE[0][c], aP0, bP[c]); dmma(accE[1][c], aP1, bP[c]); }
-#pragma unroll
-      for (int c = 0; c < TH; ++c) { dmma(accO[0][c], aH0, bH[c]); dmma(accO[1][c], aH1, bH[c]); }
-    } else {
-#pragma unroll
-      for (int c = 0; c < NB; ++c) { dmma(accO[0][c], aP0, bP[c]); dmma(accO[1][c], aP1, bP[c]); }
-#pragma unroll
-      for (int c = 0; c < TH; ++c) { dmma(accE[0][c], aH0, bH[c]); dmma(accE[1][c], aH1, bH[c]); }
+      cur = nx1;
+      if (PF == 2) nx1 = nx2;
     }
   }
+#if SDCSW_EXP == 3
+  if (accE[0][0][0] == 12345.0) t_kl = 1;
+  t_kl += gtimer();
+#endif
   // fixed-order reduction over the K-splits of each row tile
-  if (WK > 1) {
-    double* d = red + (warp * 32 + lane) * NACC;
+  if (WK > 1) {  // lane-fastest layout: conflict-free shared-memory traffic
+    double* d = red + warp * NACC * 32 + lane;
     int q = 0;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
-        d[q++] = accE[a][c][0]; d[q++] = accE[a][c][1];
-        d[q++] = accO[a][c][0]; d[q++] = accO[a][c][1];
+        d[32 * q++] = accE[a][c][0]; d[32 * q++] = accE[a][c][1];
+        d[32 * q++] = accO[a][c][0]; d[32 * q++] = accO[a][c][1];
       }
     __syncthreads();
     if (ks != 0) return;
     for (int w = 1; w < WK; ++w) {
-      const double* e = red + ((w * WJ + jt) * 32 + lane) * NACC;
+      const double* e = red + (w * WJ + jt) * NACC * 32 + lane;
       int qq = 0;
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int c = 0; c < NB; ++c) {
-          accE[a][c][0] += e[qq++]; accE[a][c][1] += e[qq++];
-          accO[a][c][0] += e[qq++]; accO[a][c][1] += e[qq++];
+          accE[a][c][0] += e[32 * qq++]; accE[a][c][1] += e[32 * qq++];
+          accO[a][c][0] += e[32 * qq++]; accO[a][c][1] += e[32 * qq++];
         }
     }
   }
+#if SDCSW_EXP == 3
+  unsigned long long t_loop = gtimer();
+#endif
   if (j0 >= J) return;
-  // epilogue: thread holds (re, im) of column pair 8c + 2t at rows j0 + 8a + g
+  // epilogue: lane holds (re, im) of field f = t (U, V, zeta, Phi) of batch b0 + c
 #pragma unroll
   for (int c = 0; c < NB; ++c) {
-    const int col = 8 * c + 2 * t;
-    int b, f;
-    if (col < 4 * NB) {
-      b = col >> 2;
-      f = (col & 3) >> 1;
-    } else {
-      b = (col - 4 * NB) >> 2;
-      f = 2 + (((col - 4 * NB) & 3) >> 1);
-    }
-    if (b0 + b >= nb) continue;
+    if (c >= nbv) continue;
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
       const int j = j0 + 8 * a + g;
-      double2* dst = fsyn + ((((size_t)(b0 + b) * J + j) * L + m) * 4 + f) * 2;
+      double2* dst = fsyn + ((((size_t)(b0 + c) * J + j) * L + m) * 4 + t) * 2;
       dst[0] = make_double2(accE[a][c][0] + accO[a][c][0], accE[a][c][1] + accO[a][c][1]);
       dst[1] = make_double2(accE[a][c][0] - accO[a][c][0], accE[a][c][1] - accO[a][c][1]);
     }
   }
+#if SDCSW_EXP == 3
+  if (threadIdx.x == 0 && cta_id < (1 << 14)) {
+    g_times[8 * cta_id] = t_start;
+    g_times[8 * cta_id + 1] = t_loop;
+    g_times[8 * cta_id + 2] = gtimer();
+    g_times[8 * cta_id + 3] = smid;
+    g_times[8 * cta_id + 4] = t_pro;
+    g_times[8 * cta_id + 5] = t_f1;
+    g_times[8 * cta_id + 6] = t_kl;
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -195,7 +247,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_synthesis(
 // WJ 16-row tiles (m-major order)
 // P columns: (phi, zeta, delta) of all b (6 NB), then ke of all b; H: first 6 NB.
 // ---------------------------------------------------------------------------
-template <int NB>
+template <int NB, int PF>
 __global__ void __launch_bounds__(32 * kWarps) k_analysis(
     const double2* __restrict__ gan, int nb, int T, int J, int C, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
@@ -257,51 +309,69 @@ __global__ void __launch_bounds__(32 * kWarps) k_analysis(
     for (int c = 0; c < NB; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
 
   if (live) {
-    const int nsteps = J >> 2;
-#pragma unroll 4
-    for (int s = ks; s < nsteps; s += WK) {
+    // fragments of step s + WK are loaded before the DMMAs of step s
+    struct Frag {
+      double aP0, aP1, aH0, aH1, bPs[NB], bPa[NB], bHs[TH], bHa[TH];
+    };
+    auto fetch = [&](int s, Frag& f) {
       const int k = 4 * s;
-      const double aP0 = __ldg(P + k), aP1 = __ldg(P + k + 8 * (size_t)J);
-      const double aH0 = __ldg(H + k), aH1 = __ldg(H + k + 8 * (size_t)J);
+      f.aP0 = __ldg(P + k);
+      f.aP1 = __ldg(P + k + 8 * (size_t)J);
+      f.aH0 = __ldg(H + k);
+      f.aH1 = __ldg(H + k + 8 * (size_t)J);
       const long long jrec = (long long)(k + t) * 28;
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
-        double bs = 0.0, ba = 0.0;
-        if (pbase[c] >= 0) {
-          bs = __ldg(gb + pbase[c] + jrec + pel[c]);
-          ba = __ldg(gb + pbase[c] + jrec + 14 + pel[c]);
-        }
-        dmma(acc[0][c], aP0, ev0 ? bs : ba);
-        dmma(acc[1][c], aP1, ev1 ? bs : ba);
+        const bool ok = pbase[c] >= 0;
+        f.bPs[c] = ok ? __ldg(gb + pbase[c] + jrec + pel[c]) : 0.0;
+        f.bPa[c] = ok ? __ldg(gb + pbase[c] + jrec + 14 + pel[c]) : 0.0;
       }
 #pragma unroll
       for (int c = 0; c < TH; ++c) {
-        double bs = 0.0, ba = 0.0;
-        if (hbase[c] >= 0) {
-          bs = __ldg(gb + hbase[c] + jrec + hel[c]);
-          ba = __ldg(gb + hbase[c] + jrec + 14 + hel[c]);
+        const bool ok = hbase[c] >= 0;
+        f.bHs[c] = ok ? __ldg(gb + hbase[c] + jrec + hel[c]) : 0.0;
+        f.bHa[c] = ok ? __ldg(gb + hbase[c] + jrec + 14 + hel[c]) : 0.0;
+      }
+    };
+    const int nsteps = J >> 2;
+    int s = ks;
+    if (s < nsteps) {
+      Frag cur, nx1, nx2;
+      fetch(s, cur);
+      if (PF == 2) fetch(s + WK < nsteps ? s + WK : s, nx1);
+      for (; s < nsteps; s += WK) {
+        fetch(s + PF * WK < nsteps ? s + PF * WK : s, PF == 2 ? nx2 : nx1);
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          dmma(acc[0][c], cur.aP0, ev0 ? cur.bPs[c] : cur.bPa[c]);
+          dmma(acc[1][c], cur.aP1, ev1 ? cur.bPs[c] : cur.bPa[c]);
         }
-        dmma(acc[0][c], aH0, ev0 ? ba : bs);
-        dmma(acc[1][c], aH1, ev1 ? ba : bs);
+#pragma unroll
+        for (int c = 0; c < TH; ++c) {
+          dmma(acc[0][c], cur.aH0, ev0 ? cur.bHa[c] : cur.bHs[c]);
+          dmma(acc[1][c], cur.aH1, ev1 ? cur.bHa[c] : cur.bHs[c]);
+        }
+        cur = nx1;
+        if (PF == 2) nx1 = nx2;
       }
     }
   }
-  if (WK > 1) {
-    double* d = red + (warp * 32 + lane) * NACC;
+  if (WK > 1) {  // lane-fastest layout: conflict-free shared-memory traffic
+    double* d = red + warp * NACC * 32 + lane;
     int q = 0;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int c = 0; c < NB; ++c) { d[q++] = acc[a][c][0]; d[q++] = acc[a][c][1]; }
+      for (int c = 0; c < NB; ++c) { d[32 * q++] = acc[a][c][0]; d[32 * q++] = acc[a][c][1]; }
     __syncthreads();
     if (ks == 0) {
       for (int w = 1; w < WK; ++w) {
-        const double* e = red + ((w * WJ + rt) * 32 + lane) * NACC;
+        const double* e = red + (w * WJ + rt) * NACC * 32 + lane;
         int qq = 0;
 #pragma unroll
         for (int a = 0; a < 2; ++a)
 #pragma unroll
-          for (int c = 0; c < NB; ++c) { acc[a][c][0] += e[qq++]; acc[a][c][1] += e[qq++]; }
+          for (int c = 0; c < NB; ++c) { acc[a][c][0] += e[32 * qq++]; acc[a][c][1] += e[32 * qq++]; }
       }
     }
     __syncthreads();
@@ -341,17 +411,29 @@ static int pick_nb(int nb) { return nb <= 6 ? nb : 4; }
 
 #define SDCSW_NB_LIST(X) X(1) X(2) X(3) X(4) X(5) X(6)
 
-cudaError_t launch_synthesis(const Plan& p, const double2* u, int nb, cudaStream_t s,
+cudaError_t launch_synth_prep(const Plan& p, const double2* u, int nb, double* xsyn,
+                              cudaStream_t s) {
+  k_synth_prep<<<dim3((2 * p.C + 255) / 256, nb), 256, 0, s>>>(
+      reinterpret_cast<const double*>(u), 2 * p.C, nb, p.xscale, p.idx_row, xsyn);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synthesis(const Plan& p, const double* xsyn, int nb, cudaStream_t s,
                              int* step_counter) {
   const int NB = pick_nb(nb);
   const int WJ = p.synth_wj;
   dim3 grid(p.J / (kRowsPerWarp * WJ), p.T + 1, (nb + NB - 1) / NB);
-#define SDCSW_SYN(NBV)                                                                           \
-  if (NB == NBV) {                                                                               \
-    k_synthesis<NBV><<<grid, 32 * kWarps, 0, s>>>(u, nb, p.T, p.J, p.C, p.ptab, p.htab,          \
-                                                  p.rowoff, p.n_even, p.row_n, p.moff, p.inv_nn, \
-                                                  p.radius, p.fsyn, step_counter, WJ);           \
-    return cudaGetLastError();                                                                   \
+#define SDCSW_SYN(NBV)                                                                         \
+  if (NB == NBV) {                                                                             \
+    if (p.T < 200)                                                                             \
+      k_synthesis<NBV, 2><<<grid, 32 * kWarps, 0, s>>>(xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
+                                                       p.rowoff, p.n_even, p.fsyn,             \
+                                                       step_counter, WJ);                      \
+    else                                                                                       \
+      k_synthesis<NBV, 1><<<grid, 32 * kWarps, 0, s>>>(xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
+                                                       p.rowoff, p.n_even, p.fsyn,             \
+                                                       step_counter, WJ);                      \
+    return cudaGetLastError();                                                                 \
   }
   SDCSW_NB_LIST(SDCSW_SYN)
 #undef SDCSW_SYN
@@ -363,9 +445,14 @@ cudaError_t launch_analysis(const Plan& p, double2* fe, int nb, cudaStream_t s) 
   dim3 grid(p.n_anal_work, (nb + NB - 1) / NB);
 #define SDCSW_ANA(NBV)                                                                          \
   if (NB == NBV) {                                                                              \
-    k_analysis<NBV><<<grid, 32 * kWarps, 0, s>>>(p.gan, nb, p.T, p.J, p.C, p.ptab, p.htab,      \
-                                                 p.rowoff, p.n_even, p.row_n, p.moff, p.lam,    \
-                                                 p.anal_work, fe, p.anal_wj);                   \
+    if (p.T < 200)                                                                              \
+      k_analysis<NBV, 2><<<grid, 32 * kWarps, 0, s>>>(p.gan, nb, p.T, p.J, p.C, p.ptab, p.htab, \
+                                                      p.rowoff, p.n_even, p.row_n, p.moff,      \
+                                                      p.lam, p.anal_work, fe, p.anal_wj);       \
+    else                                                                                        \
+      k_analysis<NBV, 1><<<grid, 32 * kWarps, 0, s>>>(p.gan, nb, p.T, p.J, p.C, p.ptab, p.htab, \
+                                                      p.rowoff, p.n_even, p.row_n, p.moff,      \
+                                                      p.lam, p.anal_work, fe, p.anal_wj);       \
     return cudaGetLastError();                                                                  \
   }
   SDCSW_NB_LIST(SDCSW_ANA)

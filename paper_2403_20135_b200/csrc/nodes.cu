@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
     int C2, int M, int lo, NodeArgs cf, const double* __restrict__ u0,
     const double* __restrict__ fe, long long fe_stride, const double* __restrict__ fi,
     long long fi_stride, int first, double phibar, const double* __restrict__ lamv,
-    double* __restrict__ u_out, double* fi_out) {
+    double* __restrict__ u_out, double* fi_out, const double2* __restrict__ xscale,
+    const int* __restrict__ idx_row, double* __restrict__ xsyn) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
   const int q = blockIdx.y, m = lo + q;
@@ -113,6 +114,9 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
   const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
   store_tri(u_out + (size_t)q * 3 * C2, C2, e, u);
   store_tri(fi_out + (size_t)q * 3 * C2, C2, e, f_impl_tri(u, phibar, lam));
+  if (xsyn != nullptr)  // synthesis B operand of the f_E that follows (batch = this launch)
+    write_xsyn_half(xsyn + ((size_t)idx_row[e >> 1] * gridDim.y + q) * kXsyn, e & 1, u.phi,
+                    u.zeta, u.delta, xscale[e >> 1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -122,7 +126,8 @@ __global__ void __launch_bounds__(256) k_final_node(
     int C2, int M, NodeArgs cf, const double* __restrict__ u0, const double* __restrict__ fe,
     long long fe_stride, const double* __restrict__ fi, long long fi_stride, int first,
     double phibar, const double* __restrict__ lamv, double* u_out, int* diverged,
-    const int* step_counter) {
+    const int* step_counter, const double2* __restrict__ xscale, const int* __restrict__ idx_row,
+    double* __restrict__ xsyn) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
   const double lam = lamv[e >> 1];
@@ -140,6 +145,9 @@ __global__ void __launch_bounds__(256) k_final_node(
   const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
   store_tri(u_out, C2, e, u);
   if (diverged != nullptr && !finite_tri(u)) atomicMin(diverged, step_counter ? *step_counter : 1);
+  if (xsyn != nullptr)  // B operand of the next step's f_E(u0)
+    write_xsyn_half(xsyn + (size_t)idx_row[e >> 1] * kXsyn, e & 1, u.phi, u.zeta, u.delta,
+                    xscale[e >> 1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -173,7 +181,9 @@ __global__ void __launch_bounds__(256) k_serial_node(
     const double* __restrict__ quad, const double* __restrict__ corr,
     const double* __restrict__ u0, const double* __restrict__ fi_old, int first, double phibar,
     const double* __restrict__ lamv, double* __restrict__ u_out, double* u_out2,
-    double* __restrict__ fi_new, int* diverged, const int* step_counter) {
+    double* __restrict__ fi_new, int* diverged, const int* step_counter,
+    const double2* __restrict__ xscale, const int* __restrict__ idx_row,
+    double* __restrict__ xsyn) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
   const double lam = lamv[e >> 1];
@@ -184,6 +194,9 @@ __global__ void __launch_bounds__(256) k_serial_node(
   const Tri u = solve_tri(b, alpha, a_phi, a2_phi, lam);
   store_tri(u_out, C2, e, u);
   store_tri(fi_new, C2, e, f_impl_tri(u, phibar, lam));
+  if (xsyn != nullptr)
+    write_xsyn_half(xsyn + (size_t)idx_row[e >> 1] * kXsyn, e & 1, u.phi, u.zeta, u.delta,
+                    xscale[e >> 1]);
   if (u_out2 != nullptr) {
     store_tri(u_out2, C2, e, u);
     if (diverged != nullptr && !finite_tri(u)) atomicMin(diverged, step_counter ? *step_counter : 1);
@@ -278,23 +291,25 @@ cudaError_t launch_solve(const Plan& p, const double* coef_host, const double2* 
 cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, const double* coef_host,
                                const double2* u0, const double2* fe, long long fe_stride,
                                const double2* fi, long long fi_stride, int first, double2* u_out,
-                               double2* fi_out, cudaStream_t s) {
+                               double2* fi_out, double* xsyn_out, cudaStream_t s) {
   const long long S2 = 6LL * p.C;  // doubles per state
   k_sweep_nodes<<<grid_for(p.C, count), 256, 0, s>>>(2 * p.C, M, node_lo, pack(coef_host, M * (M + 4)),
                                                      D(u0), D(fe), fe_stride * S2, D(fi),
                                                      fi_stride * S2, first, p.phibar, p.lam,
-                                                     W(u_out), W(fi_out));
+                                                     W(u_out), W(fi_out), p.xscale, p.idx_row,
+                                                     xsyn_out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, const double2* u0,
                               const double2* fe, long long fe_stride, const double2* fi,
                               long long fi_stride, int first, double2* u_out, int* diverged,
-                              const int* step_counter, cudaStream_t s) {
+                              const int* step_counter, double* xsyn_out, cudaStream_t s) {
   const long long S2 = 6LL * p.C;
   k_final_node<<<grid_for(p.C), 256, 0, s>>>(2 * p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
                                              fe_stride * S2, D(fi), fi_stride * S2, first, p.phibar,
-                                             p.lam, W(u_out), diverged, step_counter);
+                                             p.lam, W(u_out), diverged, step_counter, p.xscale,
+                                             p.idx_row, xsyn_out);
   return cudaGetLastError();
 }
 
@@ -312,12 +327,13 @@ cudaError_t launch_serial_node(const Plan& p, int M, int m, const double* coef_h
                                const double2* quad, const double2* corr, const double2* u0,
                                const double2* fi_old, int first, double2* u_out, double2* u_out2,
                                double2* fi_new, int* diverged, const int* step_counter,
-                               cudaStream_t s) {
+                               double* xsyn_out, cudaStream_t s) {
   (void)M;
   k_serial_node<<<grid_for(p.C), 256, 0, s>>>(2 * p.C, coef_host[0], coef_host[1], coef_host[2],
                                               m > 0, D(quad), D(corr), D(u0), D(fi_old), first,
                                               p.phibar, p.lam, W(u_out), W(u_out2), W(fi_new),
-                                              diverged, step_counter);
+                                              diverged, step_counter, p.xscale, p.idx_row,
+                                              xsyn_out);
   return cudaGetLastError();
 }
 

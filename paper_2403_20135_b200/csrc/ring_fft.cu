@@ -81,6 +81,13 @@ __device__ __forceinline__ void dft(double2 (&u)[R]) {
   }
 }
 
+// Shared-memory FFT arrays are padded by one element every 8: Stockham writes
+// at stride R (and the radix-8 first pass in particular) then hit 8 distinct
+// 16-byte bank groups per quarter-warp instead of one.
+__device__ __forceinline__ int pz(int k) { return k + (k >> 3); }
+template <int N>
+constexpr int padded() { return N + N / 8; }
+
 // Compile-time radix plan for nlon = 3 * 2^k: as many radix-8 passes as
 // possible, then radix 4, then the radix-3 pass (p is a power of two before it).
 constexpr int pow2_of(int n) { return n % 3 == 0 ? n / 3 : n; }
@@ -109,10 +116,10 @@ __device__ __forceinline__ void pass(double2* Z, const double2* tw) {
     const int it = threadIdx.x + q * THREADS;
     if (ITEMS % THREADS == 0 || it < ITEMS) {
       const int f = it / NR, i = it - f * NR;
-      const double2* X = Z + f * N;
+      const double2* X = Z + f * padded<N>();
       const int k = i % P;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[q][r] = X[i + r * NR];
+      for (int r = 0; r < R; ++r) v[q][r] = X[pz(i + r * NR)];
       if (P > 1 && k) {
 #pragma unroll
         for (int r = 1; r < R; ++r) {
@@ -130,11 +137,11 @@ __device__ __forceinline__ void pass(double2* Z, const double2* tw) {
     const int it = threadIdx.x + q * THREADS;
     if (ITEMS % THREADS == 0 || it < ITEMS) {
       const int f = it / NR, i = it - f * NR;
-      double2* X = Z + f * N;
+      double2* X = Z + f * padded<N>();
       const int k = i % P;
       const int jo = (i - k) * R + k;
 #pragma unroll
-      for (int r = 0; r < R; ++r) X[jo + r * P] = v[q][r];
+      for (int r = 0; r < R; ++r) X[pz(jo + r * P)] = v[q][r];
     }
   }
   __syncthreads();
@@ -159,8 +166,9 @@ __global__ void __launch_bounds__(THREADS) k_ring(const double2* __restrict__ fs
                                                   double two_omega) {
   extern __shared__ double2 sm2[];
   const int L = T + 1;
-  double2* Z = sm2;            // [5][N]
-  double2* tw = sm2 + 5 * N;   // [N]
+  constexpr int NP = padded<N>();
+  double2* Z = sm2;             // [5][NP] (padded)
+  double2* tw = sm2 + 5 * NP;   // [N]
   const int j = blockIdx.x, b = blockIdx.y;
   const double2* F = fsyn + ((size_t)b * J + j) * L * 8;
 
@@ -178,7 +186,7 @@ __global__ void __launch_bounds__(THREADS) k_ring(const double2* __restrict__ fs
       const double2 xn = F[(m * 4 + f) * 2], xs = F[(m * 4 + f) * 2 + 1];
       z = make_double2(xn.x + xs.y, xs.x - xn.y);
     }
-    Z[f * N + k] = z;
+    Z[f * NP + pz(k)] = z;
   }
   __syncthreads();
   passes<N, 0, 1, true, 4, THREADS>(Z, tw);
@@ -187,14 +195,15 @@ __global__ void __launch_bounds__(THREADS) k_ring(const double2* __restrict__ fs
   const double muj = mu[j];
   const double cor_n = two_omega * muj, cor_s = -two_omega * muj;
   const double ke_scale = 0.5 / ((1.0 - muj) * (1.0 + muj));
-  for (int k = threadIdx.x; k < N; k += THREADS) {
-    const double2 U = Z[k], V = Z[N + k], Zt = Z[2 * N + k], Ph = Z[3 * N + k];
+  for (int k0 = threadIdx.x; k0 < N; k0 += THREADS) {
+    const int k = pz(k0);
+    const double2 U = Z[k], V = Z[NP + k], Zt = Z[2 * NP + k], Ph = Z[3 * NP + k];
     const double en = Zt.x + cor_n, es = Zt.y + cor_s;
-    Z[k] = make_double2(en * U.x, es * U.y);                      // A = eta U
-    Z[N + k] = make_double2(en * V.x, es * V.y);                  // B = eta V
-    Z[2 * N + k] = make_double2(Ph.x * U.x, Ph.y * U.y);          // C = Phi U
-    Z[3 * N + k] = make_double2(Ph.x * V.x, Ph.y * V.y);          // D = Phi V
-    Z[4 * N + k] = make_double2((U.x * U.x + V.x * V.x) * ke_scale,
+    Z[k] = make_double2(en * U.x, es * U.y);                       // A = eta U
+    Z[NP + k] = make_double2(en * V.x, es * V.y);                  // B = eta V
+    Z[2 * NP + k] = make_double2(Ph.x * U.x, Ph.y * U.y);          // C = Phi U
+    Z[3 * NP + k] = make_double2(Ph.x * V.x, Ph.y * V.y);          // D = Phi V
+    Z[4 * NP + k] = make_double2((U.x * U.x + V.x * V.x) * ke_scale,
                                 (U.y * U.y + V.y * V.y) * ke_scale);  // kinetic energy
   }
   __syncthreads();
@@ -206,7 +215,7 @@ __global__ void __launch_bounds__(THREADS) k_ring(const double2* __restrict__ fs
   double2* out = gan + ((size_t)b * L * J + j) * (kNumSlots * 2);
   for (int idx = threadIdx.x; idx < 5 * L; idx += THREADS) {
     const int m = idx / 5, o = idx - 5 * m;
-    const double2 zm = Z[o * N + m], zc = Z[o * N + (m == 0 ? 0 : N - m)];
+    const double2 zm = Z[o * NP + pz(m)], zc = Z[o * NP + pz(m == 0 ? 0 : N - m)];
     // X = FFT(north)/N, Y = FFT(south)/N; S = X + Y, A = X - Y
     const double2 X = make_double2(h * (zm.x + zc.x), h * (zm.y - zc.y));
     const double2 Y = make_double2(h * (zm.y + zc.y), -h * (zm.x - zc.x));
@@ -261,7 +270,7 @@ cudaError_t configure_ring(size_t smem) {
   return e;
 }
 
-size_t ring_smem_bytes(int nlon) { return (size_t)nlon * 6 * sizeof(double2); }
+size_t ring_smem_bytes(int nlon) { return (size_t)(5 * (nlon + nlon / 8) + nlon) * sizeof(double2); }
 
 cudaError_t launch_ring(const Plan& p, int nb, cudaStream_t s) {
   dim3 grid(p.J, nb);

@@ -26,13 +26,26 @@ cudaError_t configure_ring(size_t smem);
 size_t ring_smem_bytes(int nlon);
 bool ring_supported(int nlon);
 
-cudaError_t f_expl(const Plan& p, const double2* u, double2* fe, int nb, cudaStream_t s,
-                   int* step_counter) {
-  cudaError_t e = launch_synthesis(p, u, nb, s, step_counter);
+cudaError_t f_expl_prepped(const Plan& p, const double* xsyn, double2* fe, int nb, cudaStream_t s,
+                           int* step_counter) {
+  cudaError_t e = launch_synthesis(p, xsyn, nb, s, step_counter);
   if (e != cudaSuccess) return e;
   e = launch_ring(p, nb, s);
   if (e != cudaSuccess) return e;
   return launch_analysis(p, fe, nb, s);
+}
+
+cudaError_t f_expl(Plan& p, const double2* u, double2* fe, int nb, cudaStream_t s,
+                   int* step_counter) {
+  cudaError_t e;
+  if (p.xsyn_nb != nb) {  // record layout changes: padding rows must read as zero
+    e = cudaMemsetAsync(p.xsyn, 0, (size_t)p.rows * nb * kXsyn * sizeof(double), s);
+    if (e != cudaSuccess) return e;
+    p.xsyn_nb = nb;
+  }
+  e = launch_synth_prep(p, u, nb, p.xsyn, s);
+  if (e != cudaSuccess) return e;
+  return f_expl_prepped(p, p.xsyn, fe, nb, s, step_counter);
 }
 
 template <typename T>
@@ -60,6 +73,7 @@ struct sdcsw_stepper {
   double2* buf;  // all sweep storage in one allocation
   size_t S;      // one state, in double2
   double2 *fe0, *fe, *fi, *ustage, *quad, *corr, *feB, *fiB;
+  double *xsyn1, *xsynM;  // synthesis operands (nb = 1 / nb = M); padding rows stay zero
   int* flags;    // [0] first diverged step (INT_MAX = none), [1] step counter
   cudaStream_t cap;
   cudaGraph_t graph;
@@ -112,8 +126,23 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   std::vector<int> moff(T + 2);
   for (int m = 0; m <= T + 1; ++m) moff[m] = m * (T + 1) - m * (m - 1) / 2;
   std::vector<double> inv_nn(C), wsyn(J), wke(J);
+  std::vector<double2> xscale(C);
+  std::vector<int> idx_row(C, -1);
   for (int m = 0; m <= T; ++m)
-    for (int n = m; n <= T; ++n) inv_nn[moff[m] + n - m] = n == 0 ? 0.0 : 1.0 / (double(n) * (n + 1.0));
+    for (int n = m; n <= T; ++n) {
+      const int idx = moff[m] + n - m;
+      inv_nn[idx] = n == 0 ? 0.0 : 1.0 / (double(n) * (n + 1.0));
+      xscale[idx] = make_double2((double)m * cfg->radius * inv_nn[idx], cfg->radius * inv_nn[idx]);
+    }
+  for (int m = 0; m <= T; ++m)
+    for (int r = rowoff[m]; r < rowoff[m + 1]; ++r)
+      if (row_n[r] >= 0) idx_row[moff[m] + row_n[r] - m] = r;
+  for (int i = 0; i < C; ++i)
+    if (idx_row[i] < 0) {
+      set_error("sdcsw_plan_create: row_n does not cover every coefficient");
+      delete h;
+      return SDCSW_ERR_PARAM;
+    }
   const double twopi = 6.283185307179586476925286766559;
   for (int j = 0; j < J; ++j) {
     const double mu = mu_north[j];
@@ -173,6 +202,9 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
       (e = upload(&p.moff, moff.data(), moff.size())) != cudaSuccess ||
       (e = upload(&p.lam, lam, (size_t)C)) != cudaSuccess ||
       (e = upload(&p.inv_nn, inv_nn.data(), inv_nn.size())) != cudaSuccess ||
+      (e = upload(&p.xscale, xscale.data(), xscale.size())) != cudaSuccess ||
+      (e = upload(&p.idx_row, idx_row.data(), idx_row.size())) != cudaSuccess ||
+      (e = cudaMalloc(&p.xsyn, (size_t)p.rows * p.max_batch * kXsyn * sizeof(double))) != cudaSuccess ||
       (e = upload(&p.mu, mu_north, (size_t)J)) != cudaSuccess ||
       (e = upload(&p.wsyn, wsyn.data(), wsyn.size())) != cudaSuccess ||
       (e = upload(&p.wke, wke.data(), wke.size())) != cudaSuccess ||
@@ -186,12 +218,14 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
       (e = cudaDeviceSynchronize()) != cudaSuccess) {
     int st = cuda_status(e, "sdcsw_plan_create");
     void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
-                    p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev};
+                    p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev,
+                    p.xscale, p.idx_row, p.xsyn};
     for (void* q : ptrs)
       if (q) cudaFree(q);
     delete h;
     return st;
   }
+  p.xsyn_nb = -1;
   h->alive = true;
   *out = h;
   return SDCSW_OK;
@@ -206,7 +240,8 @@ int sdcsw_plan_destroy(sdcsw_plan* h) {
   cudaDeviceSynchronize();
   Plan& p = h->p;
   void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
-                  p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev};
+                  p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev,
+                  p.xscale, p.idx_row, p.xsyn};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   h->alive = false;
@@ -268,7 +303,7 @@ int sdcsw_sweep_nodes(sdcsw_plan* h, int n_nodes, int node_lo, int count, const 
   return cuda_status(launch_sweep_nodes(h->p, n_nodes, node_lo, count, node_coef,
                                         (const double2*)u0, (const double2*)fe, fe_stride,
                                         (const double2*)fi, fi_stride, first, (double2*)u_out,
-                                        (double2*)fi_out, (cudaStream_t)stream),
+                                        (double2*)fi_out, nullptr, (cudaStream_t)stream),
                      "sdcsw_sweep_nodes");
 }
 
@@ -280,7 +315,7 @@ int sdcsw_final_node(sdcsw_plan* h, int n_nodes, const double* final_coef, const
   if (n_nodes < 1 || n_nodes > 16 || !final_coef) return SDCSW_ERR_PARAM;
   return cuda_status(launch_final_node(h->p, n_nodes, final_coef, (const double2*)u0,
                                        (const double2*)fe, fe_stride, (const double2*)fi, fi_stride,
-                                       first, (double2*)u_out, nullptr, nullptr,
+                                       first, (double2*)u_out, nullptr, nullptr, nullptr,
                                        (cudaStream_t)stream),
                      "sdcsw_final_node");
 }
@@ -292,10 +327,19 @@ int sdcsw_transform_stage(sdcsw_plan* h, int stage, const double* in, double* ou
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
   switch (stage) {
-    case 0: e = launch_synthesis(h->p, (const double2*)in, nb, s, nullptr); break;
+    case 0:
+      if (h->p.xsyn_nb != nb) {
+        e = cudaMemsetAsync(h->p.xsyn, 0, (size_t)h->p.rows * nb * kXsyn * sizeof(double), s);
+        if (e != cudaSuccess) break;
+        h->p.xsyn_nb = nb;
+      }
+      e = launch_synth_prep(h->p, (const double2*)in, nb, h->p.xsyn, s);
+      if (e == cudaSuccess) e = launch_synthesis(h->p, h->p.xsyn, nb, s, nullptr);
+      break;
+    case 3: e = launch_synthesis(h->p, h->p.xsyn, nb, s, nullptr); break;
     case 1: e = launch_ring(h->p, nb, s); break;
     case 2: e = launch_analysis(h->p, (double2*)out, nb, s); break;
-    default: set_error("sdcsw_transform_stage: stage must be 0, 1 or 2"); return SDCSW_ERR_PARAM;
+    default: set_error("sdcsw_transform_stage: stage must be 0..3"); return SDCSW_ERR_PARAM;
   }
   return cuda_status(e, "sdcsw_transform_stage");
 }
@@ -326,7 +370,9 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
   const size_t S = st->S;
   int* diverged = st->flags;
   int* counter = st->flags + 1;
-  cudaError_t e = f_expl(p, u, st->fe0, 1, s, counter);
+  // f_E(u0) from the operand the previous step's last kernel (or the run's
+  // prep) wrote into xsyn1
+  cudaError_t e = f_expl_prepped(p, st->xsyn1, st->fe0, 1, s, counter);
   if (e != cudaSuccess) return e;
   if (st->mode == 0) {
     // fi alternates between two buffers: every node reads all fi_j while
@@ -338,16 +384,16 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
       double2* fi_new = (k % 2) ? st->fi : st->fiB;
       e = launch_sweep_nodes(p, M, 0, M, st->coef.data() + (size_t)(k - 1) * cstride, u,
                              first ? st->fe0 : st->fe, first ? 0 : 1, fi_cur, first ? 0 : 1,
-                             first, st->ustage, fi_new, s);
+                             first, st->ustage, fi_new, st->xsynM, s);
       if (e != cudaSuccess) return e;
-      e = f_expl(p, st->ustage, st->fe, M, s, nullptr);
+      e = f_expl_prepped(p, st->xsynM, st->fe, M, s, nullptr);
       if (e != cudaSuccess) return e;
       fi_cur = fi_new;
     }
     const bool first = K == 1;
     return launch_final_node(p, M, st->coef.data() + (size_t)(K - 1) * cstride, u,
                              first ? st->fe0 : st->fe, first ? 0 : 1, fi_cur, first ? 0 : 1,
-                             first, u, diverged, counter, s);
+                             first, u, diverged, counter, st->xsyn1, s);
   }
   // serial SDC: old/new tendency buffers alternate between sweeps
   const double* W = st->coef.data();
@@ -367,9 +413,10 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
       const bool last = (k == K && m == M - 1);
       e = launch_serial_node(p, M, m, sc + 3 * m, st->quad + m * S, st->corr, u,
                              old_fi + old_stride * m * S, first, st->ustage, last ? u : nullptr,
-                             nfi + m * S, last ? diverged : nullptr, last ? counter : nullptr, s);
+                             nfi + m * S, last ? diverged : nullptr, last ? counter : nullptr,
+                             st->xsyn1, s);
       if (e != cudaSuccess) return e;
-      e = f_expl(p, st->ustage, nfe + m * S, 1, s, nullptr);
+      e = f_expl_prepped(p, st->xsyn1, nfe + m * S, 1, s, nullptr);
       if (e != cudaSuccess) return e;
       if (m + 1 < M) {
         e = launch_serial_update(p, m, we[m], wi[m], st->corr, nfe + m * S,
@@ -422,10 +469,15 @@ int sdcsw_stepper_create(sdcsw_plan* h, int mode, int n_nodes, int n_sweeps, con
   cudaError_t e = cudaSetDevice(p.device);
   if (e == cudaSuccess) e = cudaMalloc(&s->buf, nstates * s->S * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc(&s->flags, 2 * sizeof(int));
+  const size_t xs = (size_t)p.rows * kXsyn * sizeof(double);
+  if (e == cudaSuccess) e = cudaMalloc(&s->xsyn1, xs * (1 + M));
+  if (e == cudaSuccess) e = cudaMemset(s->xsyn1, 0, xs * (1 + M));
+  s->xsynM = s->xsyn1 ? s->xsyn1 + (size_t)p.rows * kXsyn : nullptr;
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     if (s->buf) cudaFree(s->buf);
     if (s->flags) cudaFree(s->flags);
+    if (s->xsyn1) cudaFree(s->xsyn1);
     delete s;
     return cuda_status(e, "sdcsw_stepper_create");
   }
@@ -443,7 +495,7 @@ int sdcsw_stepper_create(sdcsw_plan* h, int mode, int n_nodes, int n_sweeps, con
   }
   const int init[2] = {INT_MAX, 0};
   cudaMemcpy(s->flags, init, sizeof(init), cudaMemcpyHostToDevice);
-  s->launches = mode == 0 ? 4 * K : 3 + K * 5 * M;
+  s->launches = mode == 0 ? 4 * K : 3 + K * 5 * M;  // (+1 operand prep per run)
   *out = s;
   return SDCSW_OK;
 }
@@ -457,6 +509,7 @@ int sdcsw_stepper_destroy(sdcsw_stepper* s) {
   cudaStreamDestroy(s->cap);
   cudaFree(s->buf);
   cudaFree(s->flags);
+  cudaFree(s->xsyn1);
   delete s;
   return SDCSW_OK;
 }
@@ -484,6 +537,10 @@ int sdcsw_stepper_run(sdcsw_stepper* s, double* u, int n_steps, int use_graph, v
   cudaStream_t cs = (cudaStream_t)stream;
   cudaError_t e = cudaSetDevice(s->plan->p.device);
   if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+  if (n_steps == 0) return SDCSW_OK;
+  // the caller may have changed u since the last step: rebuild its synthesis operand
+  e = launch_synth_prep(s->plan->p, (const double2*)u, 1, s->xsyn1, cs);
+  if (e != cudaSuccess) return cuda_status(e, "sdcsw_stepper_run prep");
   if (!use_graph) {
     for (int i = 0; i < n_steps; ++i) {
       e = enqueue_step(s, (double2*)u, cs);
