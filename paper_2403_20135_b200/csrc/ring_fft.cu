@@ -6,7 +6,7 @@
 // restatement (A=eta U, B=eta V, C=Phi' U, D=Phi' V,
 // E=(U^2+V^2)/(2(1-mu^2))).
 //
-// FFT: mixed-radix (8, 4, 3) Stockham autosort over nlon = 3*2^k complex
+// FFT: mixed-radix (16, 8, 4, 3) Stockham autosort over nlon = 3*2^k complex
 // points (kernel templated on nlon: 96 ... 1536), in place: every pass reads all butterfly inputs of all the
 // concurrent transforms into registers, synchronises, then writes.  The two
 // real rings of a pair are packed into one complex transform (z = x_N + i x_S),
@@ -17,7 +17,22 @@
 // (N+S) / antisymmetric (N-S) parts.
 #include "internal.cuh"
 
+#ifndef SDCSW_EXP
+#define SDCSW_EXP 0
+#endif
+
 namespace sdcsw {
+#if SDCSW_EXP == 4
+__device__ unsigned long long g_rtimes[1 << 16];
+__device__ __forceinline__ unsigned long long gtimer_r() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define RT(i) if (threadIdx.x == 0 && cta < 8192) g_rtimes[8 * cta + (i)] = gtimer_r();
+#else
+#define RT(i)
+#endif
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -57,6 +72,36 @@ __device__ __forceinline__ void dft(double2 (&u)[R]) {
     u[2] = csub(t2, isd);
   } else if constexpr (R == 4) {
     dft4<INV>(u[0], u[1], u[2], u[3]);
+  } else if constexpr (R == 16) {
+    // 16 = 4 x 4: X_b[c] = DFT4_a(u[4a + b]); X_b[c] *= w16^(b c); y[c + 4d] = DFT4_b(X_b[c])
+    constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173;
+    constexpr double H = 0.70710678118654752440;
+    // cos / sin of 2 pi e / 16 for e = 0..9
+    constexpr double cs[10][2] = {{1, 0},   {C1, S1}, {H, H},     {S1, C1},   {0, 1},
+                                  {-S1, C1}, {-H, H}, {-C1, S1}, {-1, 0},   {-C1, -S1}};
+#pragma unroll
+    for (int b = 0; b < 4; ++b) dft4<INV>(u[b], u[4 + b], u[8 + b], u[12 + b]);
+#pragma unroll
+    for (int b = 1; b < 4; ++b)
+#pragma unroll
+      for (int c = 1; c < 4; ++c) {
+        const int e = b * c;
+        // w = exp(-/+ i 2 pi e / 16) = cos -/+ i sin
+        const double2 w = make_double2(cs[e][0], INV ? cs[e][1] : -cs[e][1]);
+        u[4 * c + b] = cmul(u[4 * c + b], w);
+      }
+    double2 y[16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double2 t0 = u[4 * c], t1 = u[4 * c + 1], t2 = u[4 * c + 2], t3 = u[4 * c + 3];
+      dft4<INV>(t0, t1, t2, t3);
+      y[c] = t0;
+      y[c + 4] = t1;
+      y[c + 8] = t2;
+      y[c + 12] = t3;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) u[q] = y[q];
   } else {  // R == 8: a_r = u_r + u_{r+4}, b_r = (u_r - u_{r+4}) w8^r, y_2q = DFT4(a), y_2q+1 = DFT4(b)
     const double h = 0.70710678118654752440;
     double2 a[4], b[4];
@@ -82,28 +127,30 @@ __device__ __forceinline__ void dft(double2 (&u)[R]) {
 }
 
 // Shared-memory FFT arrays are padded by one element every 8: Stockham writes
-// at stride R (and the radix-8 first pass in particular) then hit 8 distinct
-// 16-byte bank groups per quarter-warp instead of one.
+// at stride R then hit distinct 16-byte bank groups within a quarter-warp.
 __device__ __forceinline__ int pz(int k) { return k + (k >> 3); }
 template <int N>
 constexpr int padded() { return N + N / 8; }
 
-// Compile-time radix plan for nlon = 3 * 2^k: as many radix-8 passes as
-// possible, then radix 4, then the radix-3 pass (p is a power of two before it).
-constexpr int pow2_of(int n) { return n % 3 == 0 ? n / 3 : n; }
-constexpr int log2i(int n) { return n <= 1 ? 0 : 1 + log2i(n / 2); }
-constexpr int n8_of(int n) {
-  return log2i(pow2_of(n)) % 3 == 1 ? log2i(pow2_of(n)) / 3 - 1 : log2i(pow2_of(n)) / 3;
-}
-constexpr int n4_of(int n) {
-  return log2i(pow2_of(n)) % 3 == 1 ? 2 : (log2i(pow2_of(n)) % 3 == 2 ? 1 : 0);
-}
-constexpr int nstages_of(int n) { return n8_of(n) + n4_of(n) + (n % 3 == 0 ? 1 : 0); }
-constexpr int radix_of(int n, int s) { return s < n8_of(n) ? 8 : (s < n8_of(n) + n4_of(n) ? 4 : 3); }
+// Compile-time radix plans.  The inverse plan ends with radix 3 and the
+// forward plan (its reverse) starts with it, so the last inverse pass, the
+// grid products and the first forward pass run fused in registers on the
+// same points (Stockham: the last pass of a plan writes exactly the points
+// the first pass of the reversed plan reads).
+template <int N> struct RadixPlan;
+template <> struct RadixPlan<96> { static constexpr int n = 3; static constexpr int r[4] = {8, 4, 3, 0}; };
+template <> struct RadixPlan<192> { static constexpr int n = 3; static constexpr int r[4] = {16, 4, 3, 0}; };
+template <> struct RadixPlan<384> { static constexpr int n = 3; static constexpr int r[4] = {16, 8, 3, 0}; };
+template <> struct RadixPlan<768> { static constexpr int n = 3; static constexpr int r[4] = {16, 16, 3, 0}; };
+template <> struct RadixPlan<1536> { static constexpr int n = 4; static constexpr int r[4] = {16, 8, 4, 3}; };
+
+template <int N>
+constexpr int inv_radix(int s) { return RadixPlan<N>::r[s]; }
+template <int N>
+constexpr int fwd_radix(int s) { return RadixPlan<N>::r[RadixPlan<N>::n - 1 - s]; }
 
 // One in-place Stockham pass (radix R, sub-length P) over NF concurrent
-// transforms of length N stored at Z[f * N]; all index arithmetic is by
-// compile-time constants.  tw[k] = exp(-2 pi i k / N) in shared memory.
+// transforms of length N at Z[f * padded<N>()]; tw[k] = exp(-2 pi i k / N).
 template <int N, int R, int P, bool INV, int NF, int THREADS>
 __device__ __forceinline__ void pass(double2* Z, const double2* tw) {
   constexpr int NR = N / R;
@@ -147,17 +194,30 @@ __device__ __forceinline__ void pass(double2* Z, const double2* tw) {
   __syncthreads();
 }
 
-template <int N, int S, int P, bool INV, int NF, int THREADS>
-__device__ __forceinline__ void passes(double2* Z, const double2* tw) {
-  if constexpr (S < nstages_of(N)) {
-    constexpr int R = radix_of(N, S);
-    pass<N, R, P, INV, NF, THREADS>(Z, tw);
-    passes<N, S + 1, P * R, INV, NF, THREADS>(Z, tw);
+// generic inverse passes s in [S, n-1) and forward passes s in [S, n)
+template <int N, int S, int P, int NF, int THREADS>
+__device__ __forceinline__ void inverse_mid(double2* Z, const double2* tw) {
+  if constexpr (S < RadixPlan<N>::n - 1) {
+    pass<N, inv_radix<N>(S), P, true, NF, THREADS>(Z, tw);
+    inverse_mid<N, S + 1, P * inv_radix<N>(S), NF, THREADS>(Z, tw);
   }
+}
+template <int N, int S, int P, int NF, int THREADS>
+__device__ __forceinline__ void forward_rest(double2* Z, const double2* tw) {
+  if constexpr (S < RadixPlan<N>::n) {
+    pass<N, fwd_radix<N>(S), P, false, NF, THREADS>(Z, tw);
+    forward_rest<N, S + 1, P * fwd_radix<N>(S), NF, THREADS>(Z, tw);
+  }
+}
+template <int N, int S>
+constexpr int inv_prefix() {  // product of the first S inverse radices
+  int p = 1;
+  for (int s = 0; s < S; ++s) p *= inv_radix<N>(s);
+  return p;
 }
 
 template <int N, int THREADS>
-__global__ void __launch_bounds__(THREADS) k_ring(const double2* __restrict__ fsyn,
+__global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const double2* __restrict__ fsyn,
                                                   double2* __restrict__ gan, int J, int T,
                                                   const double* __restrict__ mu,
                                                   const double* __restrict__ wsyn,
@@ -165,54 +225,122 @@ __global__ void __launch_bounds__(THREADS) k_ring(const double2* __restrict__ fs
                                                   const double2* __restrict__ twg,
                                                   double two_omega) {
   extern __shared__ double2 sm2[];
-  const int L = T + 1;
   constexpr int NP = padded<N>();
+  constexpr int NS = RadixPlan<N>::n;
   double2* Z = sm2;             // [5][NP] (padded)
   double2* tw = sm2 + 5 * NP;   // [N]
+  const int L = T + 1;
   const int j = blockIdx.x, b = blockIdx.y;
   const double2* F = fsyn + ((size_t)b * J + j) * L * 8;
-
+#if SDCSW_EXP == 4
+  const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+#endif
+  RT(0)
   for (int k = threadIdx.x; k < N; k += THREADS) tw[k] = twg[k];
-  // spectra of U, V, zeta, Phi:  Z_m = X_m + i Y_m,  Z_{N-m} = conj(X_m) + i conj(Y_m)
-  for (int idx = threadIdx.x; idx < 4 * N; idx += THREADS) {
-    const int k = idx >> 2, f = idx & 3;
-    double2 z = make_double2(0.0, 0.0);
-    if (k <= T) {
-      double2 xn = F[(k * 4 + f) * 2], xs = F[(k * 4 + f) * 2 + 1];
-      if (k == 0) xn.y = xs.y = 0.0;
-      z = make_double2(xn.x - xs.y, xn.y + xs.x);
-    } else if (k >= N - T) {
-      const int m = N - k;
-      const double2 xn = F[(m * 4 + f) * 2], xs = F[(m * 4 + f) * 2 + 1];
-      z = make_double2(xn.x + xs.y, xs.x - xn.y);
-    }
-    Z[f * NP + pz(k)] = z;
-  }
-  __syncthreads();
-  passes<N, 0, 1, true, 4, THREADS>(Z, tw);
 
-  // products on the grid: re = north ring, im = south ring
-  const double muj = mu[j];
-  const double cor_n = two_omega * muj, cor_s = -two_omega * muj;
-  const double ke_scale = 0.5 / ((1.0 - muj) * (1.0 + muj));
-  for (int k0 = threadIdx.x; k0 < N; k0 += THREADS) {
-    const int k = pz(k0);
-    const double2 U = Z[k], V = Z[NP + k], Zt = Z[2 * NP + k], Ph = Z[3 * NP + k];
-    const double en = Zt.x + cor_n, es = Zt.y + cor_s;
-    Z[k] = make_double2(en * U.x, es * U.y);                       // A = eta U
-    Z[NP + k] = make_double2(en * V.x, es * V.y);                  // B = eta V
-    Z[2 * NP + k] = make_double2(Ph.x * U.x, Ph.y * U.y);          // C = Phi U
-    Z[3 * NP + k] = make_double2(Ph.x * V.x, Ph.y * V.y);          // D = Phi V
-    Z[4 * NP + k] = make_double2((U.x * U.x + V.x * V.x) * ke_scale,
-                                (U.y * U.y + V.y * V.y) * ke_scale);  // kinetic energy
+  // ---- inverse pass 0 (P = 1, no twiddles) straight from the Fourier
+  //      coefficients: Z_m = X_m + i Y_m, Z_{N-m} = conj(X_m) + i conj(Y_m)
+  {
+    constexpr int R = inv_radix<N>(0);
+    constexpr int NR = N / R;
+    constexpr int ITEMS = 4 * NR;
+    for (int it = threadIdx.x; it < ITEMS; it += THREADS) {
+      const int i = it >> 2, f = it & 3;
+      double2 v[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int k = i + r * NR;
+        double2 z = make_double2(0.0, 0.0);
+        if (k <= T) {
+          double2 xn = F[(k * 4 + f) * 2], xs = F[(k * 4 + f) * 2 + 1];
+          if (k == 0) xn.y = xs.y = 0.0;
+          z = make_double2(xn.x - xs.y, xn.y + xs.x);
+        } else if (k >= N - T) {
+          const int m = N - k;
+          const double2 xn = F[(m * 4 + f) * 2], xs = F[(m * 4 + f) * 2 + 1];
+          z = make_double2(xn.x + xs.y, xs.x - xn.y);
+        }
+        v[r] = z;
+      }
+      dft<R, true>(v);
+      double2* X = Z + f * NP;
+#pragma unroll
+      for (int r = 0; r < R; ++r) X[pz(i * R + r)] = v[r];
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  passes<N, 0, 1, false, 5, THREADS>(Z, tw);
+  RT(1)
+  inverse_mid<N, 1, inv_radix<N>(0), 4, THREADS>(Z, tw);
+  RT(2)
+
+  // ---- fused: last inverse pass (radix 3, P = N/3), grid products, first
+  //      forward pass (radix 3, P = 1) on the points i + r N/3
+  {
+    constexpr int N3 = N / 3;
+    static_assert(inv_prefix<N, NS - 1>() == N3, "inverse plan must end with radix 3");
+    static_assert(inv_radix<N>(NS - 1) == 3, "inverse plan must end with radix 3");
+    const double muj = mu[j];
+    const double cor_n = two_omega * muj, cor_s = -two_omega * muj;
+    const double ke_scale = 0.5 / ((1.0 - muj) * (1.0 + muj));
+    constexpr int MAXIT = (N3 + THREADS - 1) / THREADS;
+    double2 out[MAXIT][5][3];
+#pragma unroll
+    for (int q = 0; q < MAXIT; ++q) {
+      const int i = threadIdx.x + q * THREADS;
+      if (N3 % THREADS == 0 || i < N3) {
+        double2 g[4][3];
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          const double2* X = Z + f * NP;
+#pragma unroll
+          for (int r = 0; r < 3; ++r) g[f][r] = X[pz(i + r * N3)];
+          if (i) {  // twiddles exp(+2 pi i r i / N)
+#pragma unroll
+            for (int r = 1; r < 3; ++r) {
+              double2 w = tw[r * i];
+              w.y = -w.y;
+              g[f][r] = cmul(g[f][r], w);
+            }
+          }
+          dft<3, true>(g[f]);
+        }
+        // products at the three points (re = north ring, im = south ring)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double2 U = g[0][r], V = g[1][r], Zt = g[2][r], Ph = g[3][r];
+          const double en = Zt.x + cor_n, es = Zt.y + cor_s;
+          out[q][0][r] = make_double2(en * U.x, es * U.y);   // A = eta U
+          out[q][1][r] = make_double2(en * V.x, es * V.y);   // B = eta V
+          out[q][2][r] = make_double2(Ph.x * U.x, Ph.y * U.y);  // C = Phi U
+          out[q][3][r] = make_double2(Ph.x * V.x, Ph.y * V.y);  // D = Phi V
+          out[q][4][r] = make_double2((U.x * U.x + V.x * V.x) * ke_scale,
+                                      (U.y * U.y + V.y * V.y) * ke_scale);  // kinetic energy
+        }
+#pragma unroll
+        for (int o = 0; o < 5; ++o) dft<3, false>(out[q][o]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < MAXIT; ++q) {
+      const int i = threadIdx.x + q * THREADS;
+      if (N3 % THREADS == 0 || i < N3) {
+#pragma unroll
+        for (int o = 0; o < 5; ++o)
+#pragma unroll
+          for (int r = 0; r < 3; ++r) Z[o * NP + pz(3 * i + r)] = out[q][o][r];
+      }
+    }
+    __syncthreads();
+  }
+  RT(3)
+  forward_rest<N, 1, 3, 5, THREADS>(Z, tw);
+  RT(4)
 
   const double ws = wsyn[j], wk = wke[j];
   const double h = 0.5 / (double)N;
   // analysis layout: [b][m][j][fold][slot]
-  double2* out = gan + ((size_t)b * L * J + j) * (kNumSlots * 2);
+  double2* outp = gan + ((size_t)b * L * J + j) * (kNumSlots * 2);
   for (int idx = threadIdx.x; idx < 5 * L; idx += THREADS) {
     const int m = idx / 5, o = idx - 5 * m;
     const double2 zm = Z[o * NP + pz(m)], zc = Z[o * NP + pz(m == 0 ? 0 : N - m)];
@@ -221,7 +349,7 @@ __global__ void __launch_bounds__(THREADS) k_ring(const double2* __restrict__ fs
     const double2 Y = make_double2(h * (zm.y + zc.y), -h * (zm.x - zc.x));
     const double2 S = cadd(X, Y), A = csub(X, Y);
     const double dm = (double)m;
-    double2* dst = out + (size_t)m * J * (kNumSlots * 2);
+    double2* dst = outp + (size_t)m * J * (kNumSlots * 2);
     switch (o) {
       case 0:  // A = eta U:  X_zeta = -(i m A) ws,  Y_delta = A ws
         dst[0 * kNumSlots + kXZeta] = make_double2(dm * S.y * ws, -dm * S.x * ws);
@@ -249,6 +377,10 @@ __global__ void __launch_bounds__(THREADS) k_ring(const double2* __restrict__ fs
         break;
     }
   }
+#if SDCSW_EXP == 4
+  __syncthreads();
+#endif
+  RT(5)
 }
 
 #define SDCSW_RING_SIZES(X) X(96, 256) X(192, 256) X(384, 256) X(768, 256) X(1536, 512)
@@ -269,6 +401,12 @@ cudaError_t configure_ring(size_t smem) {
 #undef SDCSW_RING_CFG
   return e;
 }
+
+#if SDCSW_EXP == 4
+extern "C" int sdcsw_debug_rtimes(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_rtimes, n * sizeof(unsigned long long));
+}
+#endif
 
 size_t ring_smem_bytes(int nlon) { return (size_t)(5 * (nlon + nlon / 8) + nlon) * sizeof(double2); }
 

@@ -1,0 +1,25 @@
+import ctypes, sys
+sys.path.insert(0, '/root/repo')
+import numpy as np
+from paper_2403_20135_b200 import _native
+_native.LIB_PATH = '/root/repo/tools/exp/libsdcsw_exp4.so'
+L = _native.load(_native.LIB_PATH)
+import bench, torch
+from paper_2403_20135_b200.problem import SphericalShallowWater
+for cfg, nb in (('c1', 1), ('c1', 4)):
+    c = bench.CONFIGS[cfg]
+    p = SphericalShallowWater(c['trunc'], max_batch=4)
+    bench.time_stage(p, 0, nb, reps=3)
+    u = p.empty_states(nb); out = p.empty_states(nb)
+    for _ in range(3):
+        L.sdcsw_transform_stage(p.handle, 1, u.data_ptr(), out.data_ptr(), nb, p.stream())
+    torch.cuda.synchronize()
+    n = p.grid.nlat // 2 * nb
+    buf = (ctypes.c_ulonglong * (8 * n))()
+    L.sdcsw_debug_rtimes.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    L.sdcsw_debug_rtimes(buf, 8 * n)
+    t = np.array(buf, dtype=np.float64).reshape(n, 8)[:, :6]
+    t = (t - t[:, :1].min()) / 1e3
+    d = np.diff(t, axis=1)
+    print(cfg, nb, 'span %.2f' % t[:, 5].max(), 'start max %.2f' % t[:, 0].max(),
+          'phase means (build, inv, prod, fwd, out):', np.round(d.mean(0), 2), 'max', np.round(d.max(0), 2))
