@@ -64,6 +64,39 @@ struct Plan {
 };
 constexpr int kCoefCap = 4096;
 
+// Programmatic dependent launch: every kernel is launched with programmatic
+// stream serialization, releases its dependents at entry and waits for its
+// predecessor's memory (griddepcontrol.wait) before reading anything the
+// predecessor produced.  The next kernel's launch and prologue then overlap
+// the previous kernel's tail, in streams and in captured graphs alike.
+#ifdef __CUDACC__
+// (Releasing dependents at kernel entry measured slower than the implicit
+// release at exit, so SDCSW_PDL_ENTRY is empty unless SDCSW_EARLY_TRIGGER.)
+#ifdef SDCSW_EARLY_TRIGGER
+#define SDCSW_PDL_ENTRY() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
+#else
+#define SDCSW_PDL_ENTRY()
+#endif
+#define SDCSW_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#endif
+extern bool g_pdl;  // runtime switch (SDCSW_PDL=0 disables)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // error plumbing
 void set_error(const std::string& msg);
 int cuda_status(cudaError_t e, const char* where);
@@ -100,13 +133,24 @@ __device__ __forceinline__ void write_xsyn_half(double* __restrict__ rec, int ri
 
 #endif
 
+// Transform workspaces of one f_E chain (Fourier + analysis data); concurrent
+// chains use disjoint batch slices of the plan's workspaces.
+struct Work {
+  double2* fsyn;
+  double2* gan;
+};
+inline Work plan_work(const Plan& p, int batch_offset = 0) {
+  const size_t per = (size_t)p.J * p.L * 2;
+  return Work{p.fsyn + per * 4 * batch_offset, p.gan + per * kNumSlots * batch_offset};
+}
+
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_synth_prep(const Plan& p, const double2* u, int nb, double* xsyn,
                               cudaStream_t s);
-cudaError_t launch_synthesis(const Plan& p, const double* xsyn, int nb, cudaStream_t s,
-                             int* step_counter);
-cudaError_t launch_ring(const Plan& p, int nb, cudaStream_t s);
-cudaError_t launch_analysis(const Plan& p, double2* fe, int nb, cudaStream_t s);
+cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, int nb,
+                             cudaStream_t s, int* step_counter);
+cudaError_t launch_ring(const Plan& p, const Work& w, int nb, cudaStream_t s);
+cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s);
 cudaError_t launch_f_impl(const Plan& p, const double2* u, double2* fi, int nb, cudaStream_t s);
 // coefficient pointers below are HOST memory; values travel as kernel parameters
 cudaError_t launch_solve(const Plan& p, const double* coef_host, const double2* beta, double2* u,
@@ -137,7 +181,7 @@ cudaError_t launch_check_finite(const double* x, long long n, int* flag, cudaStr
 // xsyn operand a producer kernel already wrote
 cudaError_t f_expl(Plan& p, const double2* u, double2* fe, int nb, cudaStream_t s,
                    int* step_counter);
-cudaError_t f_expl_prepped(const Plan& p, const double* xsyn, double2* fe, int nb, cudaStream_t s,
-                           int* step_counter);
+cudaError_t f_expl_prepped(const Plan& p, const Work& w, const double* xsyn, double2* fe, int nb,
+                           cudaStream_t s, int* step_counter);
 
 }  // namespace sdcsw

@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(256) k_synth_prep(const double* __restrict__ u
                                                     const double2* __restrict__ xscale,
                                                     const int* __restrict__ idx_row,
                                                     double* __restrict__ xsyn) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
   const int b = blockIdx.y;
@@ -79,6 +81,8 @@ __global__ void __launch_bounds__(32 * kWarps) k_synthesis(
     const double* __restrict__ xsyn, int nb, int T, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
   constexpr int NACC = 2 * NB * 4;  // doubles per lane (E and O, re and im)
   __shared__ double red[kWarps * 32 * NACC];
 
@@ -254,6 +258,8 @@ __global__ void __launch_bounds__(32 * kWarps) k_analysis(
     const int* __restrict__ n_even, const int* __restrict__ row_n, const int* __restrict__ moff,
     const double* __restrict__ lam, const int* __restrict__ work, double2* __restrict__ fe,
     int WJ) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
   constexpr int HU = 6 * NB;
   constexpr int TH = (HU + 7) / 8;
   constexpr int PC = 8 * NB;
@@ -413,25 +419,25 @@ static int pick_nb(int nb) { return nb <= 6 ? nb : 4; }
 
 cudaError_t launch_synth_prep(const Plan& p, const double2* u, int nb, double* xsyn,
                               cudaStream_t s) {
-  k_synth_prep<<<dim3((2 * p.C + 255) / 256, nb), 256, 0, s>>>(
+  launch_k(k_synth_prep, dim3((2 * p.C + 255) / 256, nb), 256, 0, s, 
       reinterpret_cast<const double*>(u), 2 * p.C, nb, p.xscale, p.idx_row, xsyn);
   return cudaGetLastError();
 }
 
-cudaError_t launch_synthesis(const Plan& p, const double* xsyn, int nb, cudaStream_t s,
-                             int* step_counter) {
+cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, int nb,
+                             cudaStream_t s, int* step_counter) {
   const int NB = pick_nb(nb);
   const int WJ = p.synth_wj;
   dim3 grid(p.J / (kRowsPerWarp * WJ), p.T + 1, (nb + NB - 1) / NB);
 #define SDCSW_SYN(NBV)                                                                         \
   if (NB == NBV) {                                                                             \
     if (p.T < 200)                                                                             \
-      k_synthesis<NBV, 2><<<grid, 32 * kWarps, 0, s>>>(xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
-                                                       p.rowoff, p.n_even, p.fsyn,             \
+      launch_k(k_synthesis<NBV, 2>, grid, 32 * kWarps, 0, s, xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
+                                                       p.rowoff, p.n_even, w.fsyn,             \
                                                        step_counter, WJ);                      \
     else                                                                                       \
-      k_synthesis<NBV, 1><<<grid, 32 * kWarps, 0, s>>>(xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
-                                                       p.rowoff, p.n_even, p.fsyn,             \
+      launch_k(k_synthesis<NBV, 1>, grid, 32 * kWarps, 0, s, xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
+                                                       p.rowoff, p.n_even, w.fsyn,             \
                                                        step_counter, WJ);                      \
     return cudaGetLastError();                                                                 \
   }
@@ -440,17 +446,17 @@ cudaError_t launch_synthesis(const Plan& p, const double* xsyn, int nb, cudaStre
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_analysis(const Plan& p, double2* fe, int nb, cudaStream_t s) {
+cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s) {
   const int NB = pick_nb(nb);
   dim3 grid(p.n_anal_work, (nb + NB - 1) / NB);
 #define SDCSW_ANA(NBV)                                                                          \
   if (NB == NBV) {                                                                              \
     if (p.T < 200)                                                                              \
-      k_analysis<NBV, 2><<<grid, 32 * kWarps, 0, s>>>(p.gan, nb, p.T, p.J, p.C, p.ptab, p.htab, \
+      launch_k(k_analysis<NBV, 2>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab, p.htab, \
                                                       p.rowoff, p.n_even, p.row_n, p.moff,      \
                                                       p.lam, p.anal_work, fe, p.anal_wj);       \
     else                                                                                        \
-      k_analysis<NBV, 1><<<grid, 32 * kWarps, 0, s>>>(p.gan, nb, p.T, p.J, p.C, p.ptab, p.htab, \
+      launch_k(k_analysis<NBV, 1>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab, p.htab, \
                                                       p.rowoff, p.n_even, p.row_n, p.moff,      \
                                                       p.lam, p.anal_work, fe, p.anal_wj);       \
     return cudaGetLastError();                                                                  \

@@ -96,6 +96,8 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
     long long fi_stride, int first, double phibar, const double* __restrict__ lamv,
     double* __restrict__ u_out, double* fi_out, const double2* __restrict__ xscale,
     const int* __restrict__ idx_row, double* __restrict__ xsyn) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
   const int q = blockIdx.y, m = lo + q;
@@ -128,6 +130,8 @@ __global__ void __launch_bounds__(256) k_final_node(
     double phibar, const double* __restrict__ lamv, double* u_out, int* diverged,
     const int* step_counter, const double2* __restrict__ xscale, const int* __restrict__ idx_row,
     double* __restrict__ xsyn) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
   const double lam = lamv[e >> 1];
@@ -158,6 +162,8 @@ __global__ void __launch_bounds__(256) k_serial_quad(
     int C2, int M, NodeArgs cf, const double* __restrict__ u0, const double* __restrict__ fe,
     long long fe_stride, const double* __restrict__ fi, long long fi_stride, int first,
     double phibar, const double* __restrict__ lamv, double* __restrict__ quad) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
   const int m = blockIdx.y;
@@ -184,6 +190,8 @@ __global__ void __launch_bounds__(256) k_serial_node(
     double* __restrict__ fi_new, int* diverged, const int* step_counter,
     const double2* __restrict__ xscale, const int* __restrict__ idx_row,
     double* __restrict__ xsyn) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
   const double lam = lamv[e >> 1];
@@ -209,6 +217,8 @@ __global__ void __launch_bounds__(256) k_serial_update(
     const double* __restrict__ fe_new, const double* __restrict__ fe_old,
     const double* __restrict__ fi_new, const double* __restrict__ fi_old,
     const double* __restrict__ u0, int first, double phibar, const double* __restrict__ lamv) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
   const double lam = lamv[e >> 1];
@@ -231,6 +241,8 @@ __global__ void __launch_bounds__(256) k_serial_update(
 __global__ void __launch_bounds__(256) k_f_impl(int C2, const double* __restrict__ u,
                                                 double* __restrict__ fi, double phibar,
                                                 const double* __restrict__ lamv) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
   const size_t b = blockIdx.y;
@@ -240,6 +252,8 @@ __global__ void __launch_bounds__(256) k_f_impl(int C2, const double* __restrict
 __global__ void __launch_bounds__(256) k_solve(int C2, NodeArgs cf, const double* __restrict__ beta,
                                                double* __restrict__ u,
                                                const double* __restrict__ lamv) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
   const int b = blockIdx.y;
@@ -250,6 +264,8 @@ __global__ void __launch_bounds__(256) k_solve(int C2, NodeArgs cf, const double
 }
 
 __global__ void k_check_finite(const double* __restrict__ x, long long n, int* flag) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
   bool bad = false;
@@ -270,7 +286,7 @@ static NodeArgs pack(const double* v, int n) {
 #define W(x) reinterpret_cast<double*>(x)
 
 cudaError_t launch_f_impl(const Plan& p, const double2* u, double2* fi, int nb, cudaStream_t s) {
-  k_f_impl<<<grid_for(p.C, nb), 256, 0, s>>>(2 * p.C, D(u), W(fi), p.phibar, p.lam);
+  launch_k(k_f_impl, grid_for(p.C, nb), 256, 0, s, 2 * p.C, D(u), W(fi), p.phibar, p.lam);
   return cudaGetLastError();
 }
 
@@ -279,7 +295,7 @@ cudaError_t launch_solve(const Plan& p, const double* coef_host, const double2* 
   // coefficients travel by value; batches above 100 states are split
   for (int b0 = 0; b0 < nb; b0 += 100) {
     const int n = nb - b0 < 100 ? nb - b0 : 100;
-    k_solve<<<grid_for(p.C, n), 256, 0, s>>>(2 * p.C, pack(coef_host + 3 * b0, 3 * n),
+    launch_k(k_solve, grid_for(p.C, n), 256, 0, s, 2 * p.C, pack(coef_host + 3 * b0, 3 * n),
                                               D(beta + (size_t)b0 * 3 * p.C),
                                               W(u + (size_t)b0 * 3 * p.C), p.lam);
     cudaError_t e = cudaGetLastError();
@@ -293,7 +309,7 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                const double2* fi, long long fi_stride, int first, double2* u_out,
                                double2* fi_out, double* xsyn_out, cudaStream_t s) {
   const long long S2 = 6LL * p.C;  // doubles per state
-  k_sweep_nodes<<<grid_for(p.C, count), 256, 0, s>>>(2 * p.C, M, node_lo, pack(coef_host, M * (M + 4)),
+  launch_k(k_sweep_nodes, grid_for(p.C, count), 256, 0, s, 2 * p.C, M, node_lo, pack(coef_host, M * (M + 4)),
                                                      D(u0), D(fe), fe_stride * S2, D(fi),
                                                      fi_stride * S2, first, p.phibar, p.lam,
                                                      W(u_out), W(fi_out), p.xscale, p.idx_row,
@@ -306,7 +322,7 @@ cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, con
                               long long fi_stride, int first, double2* u_out, int* diverged,
                               const int* step_counter, double* xsyn_out, cudaStream_t s) {
   const long long S2 = 6LL * p.C;
-  k_final_node<<<grid_for(p.C), 256, 0, s>>>(2 * p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
+  launch_k(k_final_node, grid_for(p.C), 256, 0, s, 2 * p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
                                              fe_stride * S2, D(fi), fi_stride * S2, first, p.phibar,
                                              p.lam, W(u_out), diverged, step_counter, p.xscale,
                                              p.idx_row, xsyn_out);
@@ -317,7 +333,7 @@ cudaError_t launch_serial_quad(const Plan& p, int M, const double* w_host, const
                                const double2* fe, long long fe_stride, const double2* fi,
                                long long fi_stride, int first, double2* quad, cudaStream_t s) {
   const long long S2 = 6LL * p.C;
-  k_serial_quad<<<grid_for(p.C, M), 256, 0, s>>>(2 * p.C, M, pack(w_host, M * M), D(u0), D(fe),
+  launch_k(k_serial_quad, grid_for(p.C, M), 256, 0, s, 2 * p.C, M, pack(w_host, M * M), D(u0), D(fe),
                                                  fe_stride * S2, D(fi), fi_stride * S2, first,
                                                  p.phibar, p.lam, W(quad));
   return cudaGetLastError();
@@ -329,7 +345,7 @@ cudaError_t launch_serial_node(const Plan& p, int M, int m, const double* coef_h
                                double2* fi_new, int* diverged, const int* step_counter,
                                double* xsyn_out, cudaStream_t s) {
   (void)M;
-  k_serial_node<<<grid_for(p.C), 256, 0, s>>>(2 * p.C, coef_host[0], coef_host[1], coef_host[2],
+  launch_k(k_serial_node, grid_for(p.C), 256, 0, s, 2 * p.C, coef_host[0], coef_host[1], coef_host[2],
                                               m > 0, D(quad), D(corr), D(u0), D(fi_old), first,
                                               p.phibar, p.lam, W(u_out), W(u_out2), W(fi_new),
                                               diverged, step_counter, p.xscale, p.idx_row,
@@ -341,7 +357,7 @@ cudaError_t launch_serial_update(const Plan& p, int m, double we, double wi, dou
                                  const double2* fe_new, const double2* fe_old,
                                  const double2* fi_new, const double2* fi_old, const double2* u0,
                                  int first, cudaStream_t s) {
-  k_serial_update<<<grid_for(p.C), 256, 0, s>>>(2 * p.C, we, wi, m > 0, W(corr), D(fe_new),
+  launch_k(k_serial_update, grid_for(p.C), 256, 0, s, 2 * p.C, we, wi, m > 0, W(corr), D(fe_new),
                                                 D(fe_old), D(fi_new), D(fi_old), D(u0), first,
                                                 p.phibar, p.lam);
   return cudaGetLastError();
@@ -351,7 +367,7 @@ cudaError_t launch_check_finite(const double* x, long long n, int* flag, cudaStr
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
-  k_check_finite<<<(unsigned)blocks, 256, 0, s>>>(x, n, flag);
+  launch_k(k_check_finite, (unsigned)blocks, 256, 0, s, x, n, flag);
   return cudaGetLastError();
 }
 

@@ -224,6 +224,8 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
                                                   const double* __restrict__ wke,
                                                   const double2* __restrict__ twg,
                                                   double two_omega) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
   extern __shared__ double2 sm2[];
   constexpr int NP = padded<N>();
   constexpr int NS = RadixPlan<N>::n;
@@ -410,11 +412,11 @@ extern "C" int sdcsw_debug_rtimes(unsigned long long* host, int n) {
 
 size_t ring_smem_bytes(int nlon) { return (size_t)(5 * (nlon + nlon / 8) + nlon) * sizeof(double2); }
 
-cudaError_t launch_ring(const Plan& p, int nb, cudaStream_t s) {
+cudaError_t launch_ring(const Plan& p, const Work& w, int nb, cudaStream_t s) {
   dim3 grid(p.J, nb);
 #define SDCSW_RING_LAUNCH(NV, TV)                                                                  \
   if (p.nlon == NV) {                                                                              \
-    k_ring<NV, TV><<<grid, TV, p.ring_smem, s>>>(p.fsyn, p.gan, p.J, p.T, p.mu, p.wsyn, p.wke,      \
+    launch_k(k_ring<NV, TV>, grid, TV, p.ring_smem, s, w.fsyn, w.gan, p.J, p.T, p.mu, p.wsyn, p.wke,      \
                                                  p.twiddle, 2.0 * p.omega);                        \
     return cudaGetLastError();                                                                     \
   }

@@ -2,6 +2,7 @@
 // problem operations, the fused sweep operations and the device-resident
 // stepper that replays one captured CUDA graph per time step.
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -13,6 +14,12 @@
 namespace sdcsw {
 
 static thread_local std::string g_error;
+
+static bool pdl_default() {
+  const char* e = getenv("SDCSW_PDL");
+  return !(e && e[0] == '0');
+}
+bool g_pdl = pdl_default();
 
 void set_error(const std::string& msg) { g_error = msg; }
 
@@ -26,13 +33,13 @@ cudaError_t configure_ring(size_t smem);
 size_t ring_smem_bytes(int nlon);
 bool ring_supported(int nlon);
 
-cudaError_t f_expl_prepped(const Plan& p, const double* xsyn, double2* fe, int nb, cudaStream_t s,
-                           int* step_counter) {
-  cudaError_t e = launch_synthesis(p, xsyn, nb, s, step_counter);
+cudaError_t f_expl_prepped(const Plan& p, const Work& w, const double* xsyn, double2* fe, int nb,
+                           cudaStream_t s, int* step_counter) {
+  cudaError_t e = launch_synthesis(p, w, xsyn, nb, s, step_counter);
   if (e != cudaSuccess) return e;
-  e = launch_ring(p, nb, s);
+  e = launch_ring(p, w, nb, s);
   if (e != cudaSuccess) return e;
-  return launch_analysis(p, fe, nb, s);
+  return launch_analysis(p, w, fe, nb, s);
 }
 
 cudaError_t f_expl(Plan& p, const double2* u, double2* fe, int nb, cudaStream_t s,
@@ -45,7 +52,7 @@ cudaError_t f_expl(Plan& p, const double2* u, double2* fe, int nb, cudaStream_t 
   }
   e = launch_synth_prep(p, u, nb, p.xsyn, s);
   if (e != cudaSuccess) return e;
-  return f_expl_prepped(p, p.xsyn, fe, nb, s, step_counter);
+  return f_expl_prepped(p, plan_work(p), p.xsyn, fe, nb, s, step_counter);
 }
 
 template <typename T>
@@ -73,7 +80,10 @@ struct sdcsw_stepper {
   double2* buf;  // all sweep storage in one allocation
   size_t S;      // one state, in double2
   double2 *fe0, *fe, *fi, *ustage, *quad, *corr, *feB, *fiB;
-  double *xsyn1, *xsynM;  // synthesis operands (nb = 1 / nb = M); padding rows stay zero
+  double *xsyn1, *xsynM;  // synthesis operands (nb = 1 / node groups); padding rows stay zero
+  int chains;             // concurrent node chains per sweep (graph branches)
+  cudaStream_t side[16];
+  cudaEvent_t ev_fork, ev_join[16];
   int* flags;    // [0] first diverged step (INT_MAX = none), [1] step counter
   cudaStream_t cap;
   cudaGraph_t graph;
@@ -334,11 +344,11 @@ int sdcsw_transform_stage(sdcsw_plan* h, int stage, const double* in, double* ou
         h->p.xsyn_nb = nb;
       }
       e = launch_synth_prep(h->p, (const double2*)in, nb, h->p.xsyn, s);
-      if (e == cudaSuccess) e = launch_synthesis(h->p, h->p.xsyn, nb, s, nullptr);
+      if (e == cudaSuccess) e = launch_synthesis(h->p, plan_work(h->p), h->p.xsyn, nb, s, nullptr);
       break;
-    case 3: e = launch_synthesis(h->p, h->p.xsyn, nb, s, nullptr); break;
-    case 1: e = launch_ring(h->p, nb, s); break;
-    case 2: e = launch_analysis(h->p, (double2*)out, nb, s); break;
+    case 3: e = launch_synthesis(h->p, plan_work(h->p), h->p.xsyn, nb, s, nullptr); break;
+    case 1: e = launch_ring(h->p, plan_work(h->p), nb, s); break;
+    case 2: e = launch_analysis(h->p, plan_work(h->p), (double2*)out, nb, s); break;
     default: set_error("sdcsw_transform_stage: stage must be 0..3"); return SDCSW_ERR_PARAM;
   }
   return cuda_status(e, "sdcsw_transform_stage");
@@ -372,22 +382,43 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
   int* counter = st->flags + 1;
   // f_E(u0) from the operand the previous step's last kernel (or the run's
   // prep) wrote into xsyn1
-  cudaError_t e = f_expl_prepped(p, st->xsyn1, st->fe0, 1, s, counter);
+  cudaError_t e = f_expl_prepped(p, plan_work(p), st->xsyn1, st->fe0, 1, s, counter);
   if (e != cudaSuccess) return e;
   if (st->mode == 0) {
     // fi alternates between two buffers: every node reads all fi_j while
-    // writing its own fi_m, so the update cannot be in place
+    // writing its own fi_m, so the update cannot be in place.  The M node
+    // updates of a sweep are independent (the paper's parallel-across-the-
+    // method structure): they run as `chains` concurrent graph branches, each
+    // a contiguous node group doing solve -> synthesis -> ring -> analysis.
     const int cstride = M * (M + 4);
+    const int G = st->chains;
     double2* fi_cur = st->fi;
     for (int k = 1; k < K; ++k) {
       const bool first = k == 1;
       double2* fi_new = (k % 2) ? st->fi : st->fiB;
-      e = launch_sweep_nodes(p, M, 0, M, st->coef.data() + (size_t)(k - 1) * cstride, u,
-                             first ? st->fe0 : st->fe, first ? 0 : 1, fi_cur, first ? 0 : 1,
-                             first, st->ustage, fi_new, st->xsynM, s);
-      if (e != cudaSuccess) return e;
-      e = f_expl_prepped(p, st->xsynM, st->fe, M, s, nullptr);
-      if (e != cudaSuccess) return e;
+      const double* coef = st->coef.data() + (size_t)(k - 1) * cstride;
+      if (G > 1) {
+        if ((e = cudaEventRecord(st->ev_fork, s)) != cudaSuccess) return e;
+        for (int g = 0; g < G; ++g)
+          if ((e = cudaStreamWaitEvent(st->side[g], st->ev_fork, 0)) != cudaSuccess) return e;
+      }
+      for (int g = 0; g < G; ++g) {
+        const int lo = g * M / G, hi = (g + 1) * M / G, cnt = hi - lo;
+        cudaStream_t sg = G > 1 ? st->side[g] : s;
+        double* xs = st->xsynM + (size_t)lo * p.rows * kXsyn;
+        e = launch_sweep_nodes(p, M, lo, cnt, coef, u, first ? st->fe0 : st->fe, first ? 0 : 1,
+                               fi_cur, first ? 0 : 1, first, st->ustage + lo * S,
+                               fi_new + lo * S, xs, sg);
+        if (e != cudaSuccess) return e;
+        e = f_expl_prepped(p, plan_work(p, lo), xs, st->fe + lo * S, cnt, sg, nullptr);
+        if (e != cudaSuccess) return e;
+      }
+      if (G > 1) {
+        for (int g = 0; g < G; ++g) {
+          if ((e = cudaEventRecord(st->ev_join[g], st->side[g])) != cudaSuccess) return e;
+          if ((e = cudaStreamWaitEvent(s, st->ev_join[g], 0)) != cudaSuccess) return e;
+        }
+      }
       fi_cur = fi_new;
     }
     const bool first = K == 1;
@@ -416,7 +447,7 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
                              nfi + m * S, last ? diverged : nullptr, last ? counter : nullptr,
                              st->xsyn1, s);
       if (e != cudaSuccess) return e;
-      e = f_expl_prepped(p, st->xsyn1, nfe + m * S, 1, s, nullptr);
+      e = f_expl_prepped(p, plan_work(p), st->xsyn1, nfe + m * S, 1, s, nullptr);
       if (e != cudaSuccess) return e;
       if (m + 1 < M) {
         e = launch_serial_update(p, m, we[m], wi[m], st->corr, nfe + m * S,
@@ -495,7 +526,24 @@ int sdcsw_stepper_create(sdcsw_plan* h, int mode, int n_nodes, int n_sweeps, con
   }
   const int init[2] = {INT_MAX, 0};
   cudaMemcpy(s->flags, init, sizeof(init), cudaMemcpyHostToDevice);
-  s->launches = mode == 0 ? 4 * K : 3 + K * 5 * M;  // (+1 operand prep per run)
+  // concurrent node chains: small truncations are latency-bound (one chain per
+  // node fills the GPU); large ones batch all nodes through the GEMMs (table
+  // reuse).  SDCSW_CHAINS overrides.
+  s->chains = 1;
+  if (mode == 0) {
+    s->chains = p.T < 200 ? (M < 2 ? M : 2) : 1;
+    if (const char* env = getenv("SDCSW_CHAINS")) s->chains = atoi(env);
+    if (s->chains < 1) s->chains = 1;
+    if (s->chains > M) s->chains = M;
+  }
+  if (s->chains > 1) {
+    cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
+    for (int g = 0; g < s->chains; ++g) {
+      cudaStreamCreateWithFlags(&s->side[g], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&s->ev_join[g], cudaEventDisableTiming);
+    }
+  }
+  s->launches = mode == 0 ? 4 * K + (K - 1) * 4 * (s->chains - 1) : 3 + K * 5 * M;
   *out = s;
   return SDCSW_OK;
 }
@@ -506,6 +554,13 @@ int sdcsw_stepper_destroy(sdcsw_stepper* s) {
   cudaDeviceSynchronize();
   if (s->exec) cudaGraphExecDestroy(s->exec);
   if (s->graph) cudaGraphDestroy(s->graph);
+  if (s->chains > 1) {
+    cudaEventDestroy(s->ev_fork);
+    for (int g = 0; g < s->chains; ++g) {
+      cudaStreamDestroy(s->side[g]);
+      cudaEventDestroy(s->ev_join[g]);
+    }
+  }
   cudaStreamDestroy(s->cap);
   cudaFree(s->buf);
   cudaFree(s->flags);
