@@ -40,6 +40,9 @@ CONFIGS = {
     "c1": dict(trunc=127, nodes=4, sweeps=4, dt=90.0, steps=200, seed=1),
     "c2": dict(trunc=255, nodes=4, sweeps=4, dt=60.0, steps=100, seed=2),
     "c3": dict(trunc=511, nodes=5, sweeps=5, dt=30.0, steps=50, seed=3),
+    # ensemble: 64 independent T127 members (seeds 100..163), aggregate member-steps/s;
+    # under torchrun the members are sharded over ranks (nodes kept local)
+    "c4": dict(trunc=127, nodes=4, sweeps=4, dt=90.0, steps=100, seed=100, members=64),
 }
 METRIC = "simulated steps/sec (fp64, dSDC)"
 UNIT = "steps/s"
@@ -221,9 +224,13 @@ def time_stage(problem, stage, nb, reps=50):
     return e0.elapsed_time(e1) * 1e-3 / reps
 
 
-def stage_roofline(problem, c):
-    """Per-stage time per simulated step; roofline of the dominant kernel."""
-    m, k = c["nodes"], c["sweeps"]
+def stage_roofline(problem, c, members=1):
+    """Per-stage time per simulated step; roofline of the dominant kernel.
+
+    The sweep launches carry nodes x members states, the init launch members."""
+    k = c["sweeps"]
+    m = c["nodes"] * members
+    one = members
     g = problem.grid
     cc, j, ll = g.n_coef, g.nlat // 2, g.trunc + 1
     # algorithmic work per launch for a batch of nb states
@@ -232,10 +239,10 @@ def stage_roofline(problem, c):
     per_step = {}
     detail = {}
     for stage, name in ((3, "legendre_synthesis"), (1, "ring_fft_products"), (2, "legendre_analysis")):
-        t1 = time_stage(problem, stage, 1)
+        t1 = time_stage(problem, stage, one)
         tm = time_stage(problem, stage, m)
         per_step[name] = t1 + (k - 1) * tm
-        detail[name] = {"us_nb1": t1 * 1e6, f"us_nb{m}": tm * 1e6}
+        detail[name] = {f"us_nb{one}": t1 * 1e6, f"us_nb{m}": tm * 1e6}
     dom = max(per_step, key=per_step.get)
     tm = detail[dom][f"us_nb{m}"] * 1e-6
     if dom == "ring_fft_products":
@@ -284,9 +291,20 @@ def run_device(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = CONFIGS[args.config]
     m_nodes, k_sw, dt, nsteps = c["nodes"], c["sweeps"], c["dt"], c["steps"]
-    problem = SphericalShallowWater(c["trunc"], device=local, max_batch=max(m_nodes, 1))
-    u0_host = random_initial_state(problem.grid, c["seed"])
-    u0 = problem._to_device(u0_host).reshape(-1).contiguous()
+    total_members = c.get("members", 1)
+    ensemble = total_members > 1
+    if ensemble and total_members % world:
+        raise SystemExit(f"{total_members} members do not shard over {world} ranks")
+    members = total_members // world if ensemble else 1
+    problem = SphericalShallowWater(c["trunc"], device=local, max_batch=max(m_nodes * members, 1))
+    if ensemble:
+        mem0 = rank * members
+        u0_host = np.stack([random_initial_state(problem.grid, c["seed"] + mem0 + e)
+                            for e in range(members)])
+        u0 = torch.from_numpy(u0_host).to(problem.device).contiguous()
+    else:
+        u0_host = random_initial_state(problem.grid, c["seed"])
+        u0 = problem._to_device(u0_host).reshape(-1).contiguous()
     table = CollocationTable.radau_right(m_nodes)
     cfg = SdcConfig(table=table, n_sweeps=k_sw, mode=SweepMode.DIAGONAL_PARALLEL,
                     time_threads=min(m_nodes, max(1, world)) if world > 1 else 1)
@@ -297,8 +315,8 @@ def run_device(args):
     u = torch.empty_like(u0)
     stream = torch.cuda.current_stream(problem.device)
 
-    if world == 1:
-        stepper = DeviceStepper(problem, cfg, dt, serial=False)
+    if world == 1 or ensemble:
+        stepper = DeviceStepper(problem, cfg, dt, serial=False, members=members)
         launches_per_sim_step = stepper.launches_per_step
 
         def one_run():
@@ -341,7 +359,7 @@ def run_device(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_dev = float(t.item())
     sim_steps = args.steps * nsteps
-    value = sim_steps / t_dev
+    value = sim_steps * (total_members if ensemble else 1) / t_dev
     node_sweeps = (k_sw - 1) * m_nodes + 1
 
     # divergence check of the timed runs (device flag)
@@ -351,7 +369,23 @@ def run_device(args):
     if rank == 0:
         # --- e2e through the public API (host numpy state in, host state out)
         e2e = None
-        if world == 1:
+        if ensemble:
+            # public API: host ensemble in (pinned H2D), device run, host ensemble out
+            pinned = torch.from_numpy(u0_host).pin_memory()
+            ue = torch.empty_like(u0)
+            stepper.run(ue.copy_(pinned, non_blocking=True), 1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                ue.copy_(pinned, non_blocking=True)
+                stepper.run(ue, nsteps)
+                out_host = ue.cpu()
+            t_e2e = time.perf_counter() - t0
+            e2e = {"value": sim_steps * members / t_e2e, "unit": UNIT,
+                   "h2d_bytes_per_step": int(pinned.numel() * 16),
+                   "d2h_bytes_per_step": int(out_host.numel() * 16),
+                   "note": f"rank 0: {members} members, pinned H2D + DeviceStepper.run + D2H per bench step"}
+        elif world == 1:
             dcfg = SdcConfig(table=table, n_sweeps=k_sw, mode=SweepMode.DIAGONAL_PARALLEL)
             integrate(problem, u0_host, dt, nsteps, DiagonalSdcStepper(dcfg))  # warm-up
             t0 = time.perf_counter()
@@ -366,7 +400,7 @@ def run_device(args):
         # --- serial SDC on one GPU (the paper's sequential baseline)
         scfg = SdcConfig(table=table, n_sweeps=k_sw, mode=SweepMode.SERIAL)
         sst = DeviceStepper(problem, scfg, dt, serial=True)
-        us = u0.clone()
+        us = (u0[0] if ensemble else u0).clone().contiguous()
         sst.run(us, 5)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -377,9 +411,9 @@ def run_device(args):
         e1.synchronize()
         serial_rate = nsteps / (e0.elapsed_time(e1) * 1e-3)
         sst.close()
-        roof, stage_us, stage_detail = stage_roofline(problem, c)
+        roof, stage_us, stage_detail = stage_roofline(problem, c, members)
         cpu = None
-        if world == 1 and not args.no_cpu:
+        if world == 1 and not args.no_cpu and not ensemble:
             r, cores, wall = cpu_oracle_rate(args.config, args.cpu_sample)
             cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",
                    "sample": f"{args.cpu_sample} dSDC steps of {args.config} (of {nsteps}) after 1 "
@@ -388,17 +422,20 @@ def run_device(args):
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "higher_is_better": True,
+            "scaling": "weak" if (ensemble or world == 1) else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded n^-1.5 SH spectra, max wind 20 m/s)",
             "config": {
                 "workload": f"{args.config}: T{c['trunc']} {problem.grid.nlon}x{problem.grid.nlat} "
-                            f"M={m_nodes} K={k_sw} dt={dt} s, {nsteps} time steps per bench step",
+                            f"M={m_nodes} K={k_sw} dt={dt} s, {nsteps} time steps per bench step"
+                            + (f", {total_members} ensemble members ({members} per GPU), value = aggregate member-steps/s"
+                               if ensemble else ""),
                 "bench_step": f"one full {nsteps}-step run", "l2": "flushed between bench steps (256 MiB write, untimed)",
                 "parallelism": "1 GPU: M nodes as concurrent graph branches / batched GEMM columns" if world == 1 else f"node blocks over {world} GPUs + NCCL all-gather per sweep",
                 "ms_per_sim_step": t_dev / sim_steps * 1e3,
                 "node_sweeps_per_s": value * node_sweeps,
                 "serial_sdc_steps_per_s_1gpu": serial_rate,
-                "dsdc_vs_serial_speedup_1gpu": value / serial_rate if world == 1 else None,
+                "dsdc_vs_serial_speedup_1gpu": value / serial_rate if (world == 1 and not ensemble) else None,
                 "stage_us_per_sim_step": stage_us, "stage_us": stage_detail,
                 "finite": finite,
             },

@@ -106,6 +106,13 @@ int sdcsw_final_node(sdcsw_plan* plan, int n_nodes, const double* final_coef, co
  *           [M] implicit correction weights dt*dtau, [M][3] solve coefs. */
 int sdcsw_stepper_create(sdcsw_plan* plan, int mode, int n_nodes, int n_sweeps,
                          const double* coef, int n_coef, sdcsw_stepper** out);
+/* Ensemble variant: `members` independent states advanced together (BASELINE
+ * config 4); u holds `members` consecutive states and every f_E carries
+ * members x nodes GEMM columns.  Plan max_batch must be >= members x nodes.
+ * Mode 0 only for members > 1. */
+int sdcsw_stepper_create_ensemble(sdcsw_plan* plan, int mode, int n_nodes, int n_sweeps,
+                                  int members, const double* coef, int n_coef,
+                                  sdcsw_stepper** out);
 int sdcsw_stepper_destroy(sdcsw_stepper* st);
 
 /* Advance the device state u (one state, in place) by n_steps steps on

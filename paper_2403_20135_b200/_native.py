@@ -22,6 +22,7 @@ EXPORTS = (
     "sdcsw_sweep_nodes",
     "sdcsw_final_node",
     "sdcsw_stepper_create",
+    "sdcsw_stepper_create_ensemble",
     "sdcsw_stepper_destroy",
     "sdcsw_stepper_run",
     "sdcsw_stepper_diverged",
@@ -64,6 +65,7 @@ _SIGS = {
     "sdcsw_sweep_nodes": [_p, _i, _i, _i, _dp, _p, _p, _ll, _p, _ll, _i, _p, _p, _p],
     "sdcsw_final_node": [_p, _i, _dp, _p, _p, _ll, _p, _ll, _i, _p, _p],
     "sdcsw_stepper_create": [_p, _i, _i, _i, _dp, _i, ctypes.POINTER(_p)],
+    "sdcsw_stepper_create_ensemble": [_p, _i, _i, _i, _i, _dp, _i, ctypes.POINTER(_p)],
     "sdcsw_stepper_destroy": [_p],
     "sdcsw_stepper_run": [_p, _p, _i, _i, _p],
     "sdcsw_stepper_diverged": [_p, _ip],

@@ -158,11 +158,13 @@ cudaError_t launch_solve(const Plan& p, const double* coef_host, const double2* 
 cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, const double* coef_host,
                                const double2* u0, const double2* fe, long long fe_stride,
                                const double2* fi, long long fi_stride, int first, double2* u_out,
-                               double2* fi_out, double* xsyn_out, cudaStream_t s);
+                               double2* fi_out, double* xsyn_out, cudaStream_t s, int members = 1,
+                               long long fe_mstride = 0, long long fi_mstride = 0);
 cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, const double2* u0,
                               const double2* fe, long long fe_stride, const double2* fi,
                               long long fi_stride, int first, double2* u_out, int* diverged,
-                              const int* step_counter, double* xsyn_out, cudaStream_t s);
+                              const int* step_counter, double* xsyn_out, cudaStream_t s,
+                              int members = 1, long long fe_mstride = 0, long long fi_mstride = 0);
 cudaError_t launch_serial_quad(const Plan& p, int M, const double* w_host, const double2* u0,
                                const double2* fe, long long fe_stride, const double2* fi,
                                long long fi_stride, int first, double2* quad, cudaStream_t s);

@@ -90,17 +90,25 @@ __device__ __forceinline__ bool finite_tri(const Tri& t) {
 // diagonal sweep, nodes [lo, lo+count): grid (ceil(2C/256), count)
 // coef layout per node m: w[0..M-1], wd, alpha, a_phi, a2_phi  (stride M+4)
 // ---------------------------------------------------------------------------
+// grid (ceil(2C/256), count, members); member z reads u0 + z S, fe + z fe_mstride,
+// fi + z fi_mstride and writes batch entry z * count + q of the outputs.
 __global__ void __launch_bounds__(256) k_sweep_nodes(
     int C2, int M, int lo, NodeArgs cf, const double* __restrict__ u0,
     const double* __restrict__ fe, long long fe_stride, const double* __restrict__ fi,
     long long fi_stride, int first, double phibar, const double* __restrict__ lamv,
     double* __restrict__ u_out, double* fi_out, const double2* __restrict__ xscale,
-    const int* __restrict__ idx_row, double* __restrict__ xsyn) {
+    const int* __restrict__ idx_row, double* __restrict__ xsyn, long long fe_mstride,
+    long long fi_mstride) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
+  const int z = blockIdx.z;
+  u0 += (size_t)z * 3 * C2;
+  fe += z * fe_mstride;
+  fi += z * fi_mstride;
   const int q = blockIdx.y, m = lo + q;
+  const int ob = z * gridDim.y + q;  // output batch entry
   const double lam = lamv[e >> 1];
   const Tri a0 = load_tri(u0, C2, e);
   const Tri fi0 = f_impl_tri(a0, phibar, lam);
@@ -114,11 +122,11 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
   }
   b = axmy_tri(b, c[M], fim);
   const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
-  store_tri(u_out + (size_t)q * 3 * C2, C2, e, u);
-  store_tri(fi_out + (size_t)q * 3 * C2, C2, e, f_impl_tri(u, phibar, lam));
+  store_tri(u_out + (size_t)ob * 3 * C2, C2, e, u);
+  store_tri(fi_out + (size_t)ob * 3 * C2, C2, e, f_impl_tri(u, phibar, lam));
   if (xsyn != nullptr)  // synthesis B operand of the f_E that follows (batch = this launch)
-    write_xsyn_half(xsyn + ((size_t)idx_row[e >> 1] * gridDim.y + q) * kXsyn, e & 1, u.phi,
-                    u.zeta, u.delta, xscale[e >> 1]);
+    write_xsyn_half(xsyn + ((size_t)idx_row[e >> 1] * gridDim.y * gridDim.z + ob) * kXsyn, e & 1,
+                    u.phi, u.zeta, u.delta, xscale[e >> 1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -129,11 +137,16 @@ __global__ void __launch_bounds__(256) k_final_node(
     long long fe_stride, const double* __restrict__ fi, long long fi_stride, int first,
     double phibar, const double* __restrict__ lamv, double* u_out, int* diverged,
     const int* step_counter, const double2* __restrict__ xscale, const int* __restrict__ idx_row,
-    double* __restrict__ xsyn) {
+    double* __restrict__ xsyn, long long fe_mstride, long long fi_mstride) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= C2) return;
+  const int z = blockIdx.z;  // ensemble member
+  u0 += (size_t)z * 3 * C2;
+  u_out += (size_t)z * 3 * C2;
+  fe += z * fe_mstride;
+  fi += z * fi_mstride;
   const double lam = lamv[e >> 1];
   const Tri a0 = load_tri(u0, C2, e);
   const Tri fi0 = f_impl_tri(a0, phibar, lam);
@@ -149,9 +162,9 @@ __global__ void __launch_bounds__(256) k_final_node(
   const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
   store_tri(u_out, C2, e, u);
   if (diverged != nullptr && !finite_tri(u)) atomicMin(diverged, step_counter ? *step_counter : 1);
-  if (xsyn != nullptr)  // B operand of the next step's f_E(u0)
-    write_xsyn_half(xsyn + (size_t)idx_row[e >> 1] * kXsyn, e & 1, u.phi, u.zeta, u.delta,
-                    xscale[e >> 1]);
+  if (xsyn != nullptr)  // B operand of the next step's f_E(u0) (batch = members)
+    write_xsyn_half(xsyn + ((size_t)idx_row[e >> 1] * gridDim.z + z) * kXsyn, e & 1, u.phi,
+                    u.zeta, u.delta, xscale[e >> 1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -307,25 +320,31 @@ cudaError_t launch_solve(const Plan& p, const double* coef_host, const double2* 
 cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, const double* coef_host,
                                const double2* u0, const double2* fe, long long fe_stride,
                                const double2* fi, long long fi_stride, int first, double2* u_out,
-                               double2* fi_out, double* xsyn_out, cudaStream_t s) {
+                               double2* fi_out, double* xsyn_out, cudaStream_t s, int members,
+                               long long fe_mstride, long long fi_mstride) {
   const long long S2 = 6LL * p.C;  // doubles per state
-  launch_k(k_sweep_nodes, grid_for(p.C, count), 256, 0, s, 2 * p.C, M, node_lo, pack(coef_host, M * (M + 4)),
+  dim3 grid = grid_for(p.C, count);
+  grid.z = members;
+  launch_k(k_sweep_nodes, grid, 256, 0, s, 2 * p.C, M, node_lo, pack(coef_host, M * (M + 4)),
                                                      D(u0), D(fe), fe_stride * S2, D(fi),
                                                      fi_stride * S2, first, p.phibar, p.lam,
                                                      W(u_out), W(fi_out), p.xscale, p.idx_row,
-                                                     xsyn_out);
+                                                     xsyn_out, fe_mstride * S2, fi_mstride * S2);
   return cudaGetLastError();
 }
 
 cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, const double2* u0,
                               const double2* fe, long long fe_stride, const double2* fi,
                               long long fi_stride, int first, double2* u_out, int* diverged,
-                              const int* step_counter, double* xsyn_out, cudaStream_t s) {
+                              const int* step_counter, double* xsyn_out, cudaStream_t s,
+                              int members, long long fe_mstride, long long fi_mstride) {
   const long long S2 = 6LL * p.C;
-  launch_k(k_final_node, grid_for(p.C), 256, 0, s, 2 * p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
+  dim3 grid = grid_for(p.C);
+  grid.z = members;
+  launch_k(k_final_node, grid, 256, 0, s, 2 * p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
                                              fe_stride * S2, D(fi), fi_stride * S2, first, p.phibar,
                                              p.lam, W(u_out), diverged, step_counter, p.xscale,
-                                             p.idx_row, xsyn_out);
+                                             p.idx_row, xsyn_out, fe_mstride * S2, fi_mstride * S2);
   return cudaGetLastError();
 }
 

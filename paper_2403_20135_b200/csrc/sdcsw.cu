@@ -82,6 +82,7 @@ struct sdcsw_stepper {
   double2 *fe0, *fe, *fi, *ustage, *quad, *corr, *feB, *fiB;
   double *xsyn1, *xsynM;  // synthesis operands (nb = 1 / node groups); padding rows stay zero
   int chains;             // concurrent node chains per sweep (graph branches)
+  int members;            // ensemble members advanced together (batched GEMM columns)
   cudaStream_t side[16];
   cudaEvent_t ev_fork, ev_join[16];
   int* flags;    // [0] first diverged step (INT_MAX = none), [1] step counter
@@ -380,9 +381,10 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
   const size_t S = st->S;
   int* diverged = st->flags;
   int* counter = st->flags + 1;
-  // f_E(u0) from the operand the previous step's last kernel (or the run's
-  // prep) wrote into xsyn1
-  cudaError_t e = f_expl_prepped(p, plan_work(p), st->xsyn1, st->fe0, 1, s, counter);
+  // f_E(u0) of every member from the operand the previous step's last kernel
+  // (or the run's prep) wrote into xsyn1
+  const int E = st->members;
+  cudaError_t e = f_expl_prepped(p, plan_work(p), st->xsyn1, st->fe0, E, s, counter);
   if (e != cudaSuccess) return e;
   if (st->mode == 0) {
     // fi alternates between two buffers: every node reads all fi_j while
@@ -390,8 +392,11 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
     // updates of a sweep are independent (the paper's parallel-across-the-
     // method structure): they run as `chains` concurrent graph branches, each
     // a contiguous node group doing solve -> synthesis -> ring -> analysis.
+    // Tendency buffers are member-major [E][M]; an ensemble runs as one chain
+    // whose GEMMs carry all E * M states as columns.
     const int cstride = M * (M + 4);
     const int G = st->chains;
+    const long long mS = M;  // member stride of the node buffers, in states
     double2* fi_cur = st->fi;
     for (int k = 1; k < K; ++k) {
       const bool first = k == 1;
@@ -405,12 +410,12 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
       for (int g = 0; g < G; ++g) {
         const int lo = g * M / G, hi = (g + 1) * M / G, cnt = hi - lo;
         cudaStream_t sg = G > 1 ? st->side[g] : s;
-        double* xs = st->xsynM + (size_t)lo * p.rows * kXsyn;
+        double* xs = st->xsynM + (size_t)lo * E * p.rows * kXsyn;
         e = launch_sweep_nodes(p, M, lo, cnt, coef, u, first ? st->fe0 : st->fe, first ? 0 : 1,
                                fi_cur, first ? 0 : 1, first, st->ustage + lo * S,
-                               fi_new + lo * S, xs, sg);
+                               fi_new + lo * S, xs, sg, E, first ? 1 : mS, mS);
         if (e != cudaSuccess) return e;
-        e = f_expl_prepped(p, plan_work(p, lo), xs, st->fe + lo * S, cnt, sg, nullptr);
+        e = f_expl_prepped(p, plan_work(p, lo), xs, st->fe + lo * S, cnt * E, sg, nullptr);
         if (e != cudaSuccess) return e;
       }
       if (G > 1) {
@@ -424,7 +429,7 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
     const bool first = K == 1;
     return launch_final_node(p, M, st->coef.data() + (size_t)(K - 1) * cstride, u,
                              first ? st->fe0 : st->fe, first ? 0 : 1, fi_cur, first ? 0 : 1,
-                             first, u, diverged, counter, st->xsyn1, s);
+                             first, u, diverged, counter, st->xsyn1, s, E, first ? 1 : mS, mS);
   }
   // serial SDC: old/new tendency buffers alternate between sweeps
   const double* W = st->coef.data();
@@ -466,11 +471,17 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
 
 int sdcsw_stepper_create(sdcsw_plan* h, int mode, int n_nodes, int n_sweeps, const double* coef,
                          int n_coef, sdcsw_stepper** out) {
+  return sdcsw_stepper_create_ensemble(h, mode, n_nodes, n_sweeps, 1, coef, n_coef, out);
+}
+
+int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sweeps, int members,
+                                  const double* coef, int n_coef, sdcsw_stepper** out) {
   int st = check_plan(h, 1, "sdcsw_stepper_create");
   if (st) return st;
-  const int M = n_nodes, K = n_sweeps;
-  if ((mode != 0 && mode != 1) || M < 1 || M > 16 || K < 1 || !coef || !out) {
-    set_error("sdcsw_stepper_create: bad mode / node / sweep count");
+  const int M = n_nodes, K = n_sweeps, E = members;
+  if ((mode != 0 && mode != 1) || M < 1 || M > 16 || K < 1 || !coef || !out || E < 1 ||
+      (mode == 1 && E != 1) || E > 65535) {
+    set_error("sdcsw_stepper_create: bad mode / node / sweep / member count");
     return SDCSW_ERR_PARAM;
   }
   const int want = mode == 0 ? K * M * (M + 4) : M * M + 2 * M + 3 * M;
@@ -479,13 +490,13 @@ int sdcsw_stepper_create(sdcsw_plan* h, int mode, int n_nodes, int n_sweeps, con
     set_error("sdcsw_stepper_create: coefficient array too short");
     return SDCSW_ERR_PARAM;
   }
-  if (mode == 0 && M > h->p.max_batch) {
-    set_error("sdcsw_stepper_create: plan max_batch < node count");
+  if (mode == 0 && M * E > h->p.max_batch) {
+    set_error("sdcsw_stepper_create: plan max_batch < nodes x members");
     return SDCSW_ERR_PARAM;
   }
   sdcsw_stepper* s = new (std::nothrow) sdcsw_stepper();
   if (!s) return SDCSW_ERR_PARAM;
-  s->plan = h; s->mode = mode; s->M = M; s->K = K;
+  s->plan = h; s->mode = mode; s->M = M; s->K = K; s->members = E;
   s->coef.assign(coef, coef + need);
   if (mode == 0) {
     // pad: final block stored at index K-1
@@ -496,14 +507,14 @@ int sdcsw_stepper_create(sdcsw_plan* h, int mode, int n_nodes, int n_sweeps, con
   }
   const Plan& p = h->p;
   s->S = (size_t)3 * p.C;
-  const size_t nstates = 1 + 4 * (size_t)M + (mode == 1 ? (size_t)2 * M + 1 : 0);
+  const size_t nstates = (size_t)E * (1 + 4 * (size_t)M) + (mode == 1 ? (size_t)2 * M + 1 : 0);
   cudaError_t e = cudaSetDevice(p.device);
   if (e == cudaSuccess) e = cudaMalloc(&s->buf, nstates * s->S * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc(&s->flags, 2 * sizeof(int));
   const size_t xs = (size_t)p.rows * kXsyn * sizeof(double);
-  if (e == cudaSuccess) e = cudaMalloc(&s->xsyn1, xs * (1 + M));
-  if (e == cudaSuccess) e = cudaMemset(s->xsyn1, 0, xs * (1 + M));
-  s->xsynM = s->xsyn1 ? s->xsyn1 + (size_t)p.rows * kXsyn : nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&s->xsyn1, xs * E * (1 + M));
+  if (e == cudaSuccess) e = cudaMemset(s->xsyn1, 0, xs * E * (1 + M));
+  s->xsynM = s->xsyn1 ? s->xsyn1 + (size_t)E * p.rows * kXsyn : nullptr;
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     if (s->buf) cudaFree(s->buf);
@@ -514,11 +525,11 @@ int sdcsw_stepper_create(sdcsw_plan* h, int mode, int n_nodes, int n_sweeps, con
   }
   cudaMemset(s->buf, 0, nstates * s->S * sizeof(double2));
   double2* q = s->buf;
-  s->fe0 = q; q += s->S;
-  s->fe = q; q += M * s->S;
-  s->fi = q; q += M * s->S;
-  s->ustage = q; q += M * s->S;
-  s->fiB = q; q += M * s->S;
+  s->fe0 = q; q += E * s->S;
+  s->fe = q; q += E * M * s->S;
+  s->fi = q; q += E * M * s->S;
+  s->ustage = q; q += E * M * s->S;
+  s->fiB = q; q += E * M * s->S;
   if (mode == 1) {
     s->quad = q; q += M * s->S;
     s->feB = q; q += M * s->S;
@@ -531,10 +542,11 @@ int sdcsw_stepper_create(sdcsw_plan* h, int mode, int n_nodes, int n_sweeps, con
   // reuse).  SDCSW_CHAINS overrides.
   s->chains = 1;
   if (mode == 0) {
-    s->chains = p.T < 200 ? (M < 2 ? M : 2) : 1;
+    s->chains = (p.T < 200 && E == 1) ? (M < 2 ? M : 2) : 1;
     if (const char* env = getenv("SDCSW_CHAINS")) s->chains = atoi(env);
     if (s->chains < 1) s->chains = 1;
     if (s->chains > M) s->chains = M;
+    if (E > 1) s->chains = 1;
   }
   if (s->chains > 1) {
     cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
@@ -594,7 +606,7 @@ int sdcsw_stepper_run(sdcsw_stepper* s, double* u, int n_steps, int use_graph, v
   if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
   if (n_steps == 0) return SDCSW_OK;
   // the caller may have changed u since the last step: rebuild its synthesis operand
-  e = launch_synth_prep(s->plan->p, (const double2*)u, 1, s->xsyn1, cs);
+  e = launch_synth_prep(s->plan->p, (const double2*)u, s->members, s->xsyn1, cs);
   if (e != cudaSuccess) return cuda_status(e, "sdcsw_stepper_run prep");
   if (!use_graph) {
     for (int i = 0; i < n_steps; ++i) {

@@ -192,10 +192,13 @@ def serial_step_coefficients(cfg, dt, phibar):
 class DeviceStepper:
     """One ``sdcsw_stepper``: sweep storage on the GPU plus a CUDA graph of one step."""
 
-    def __init__(self, problem, cfg, dt, serial):
+    def __init__(self, problem, cfg, dt, serial, members=1):
         self.problem = problem
         self.lib = problem._lib
         self.serial = serial
+        self.members = int(members)
+        if self.members < 1 or (serial and self.members != 1):
+            raise ParameterError("ensembles (members > 1) are supported for diagonal SDC only")
         self.n_nodes = cfg.table.n_nodes
         self.n_sweeps = cfg.n_sweeps
         if serial:
@@ -205,9 +208,10 @@ class DeviceStepper:
         self._coef = np.ascontiguousarray(coef)
         handle = ctypes.c_void_p()
         _native.check(
-            self.lib.sdcsw_stepper_create(problem.handle, 1 if serial else 0, self.n_nodes,
-                                          self.n_sweeps, _native.dptr(self._coef), self._coef.size,
-                                          ctypes.byref(handle)),
+            self.lib.sdcsw_stepper_create_ensemble(problem.handle, 1 if serial else 0,
+                                                   self.n_nodes, self.n_sweeps, self.members,
+                                                   _native.dptr(self._coef), self._coef.size,
+                                                   ctypes.byref(handle)),
             "sdcsw_stepper_create",
         )
         self.handle = handle
@@ -226,13 +230,15 @@ class DeviceStepper:
         _native.check(self.lib.sdcsw_stepper_reset(self.handle, self.problem.stream()))
 
     def run(self, u, n_steps, use_graph=True):
-        """Advance the device state tensor ``u`` (one state) in place."""
+        """Advance the device state tensor ``u`` (``members`` states) in place."""
+        if u.numel() != self.members * self.problem.state_size:
+            raise ParameterError("state tensor does not hold `members` states")
         _native.check(
             self.lib.sdcsw_stepper_run(self.handle, u.data_ptr(), int(n_steps), int(bool(use_graph)),
                                        self.problem.stream()),
             "sdcsw_stepper_run",
         )
-        self.problem.add_counts(*(c * n_steps for c in self.counts_per_step()))
+        self.problem.add_counts(*(c * n_steps * self.members for c in self.counts_per_step()))
 
     def diverged(self):
         idx = ctypes.c_int()

@@ -234,3 +234,27 @@ def test_node_parallel_single_rank_matches_fused_stepper():
     assert torch.equal(a, b)
     st.close()
     dist.destroy_process_group()
+
+
+def test_ensemble_members_match_single_runs():
+    """BASELINE config 4 mechanism: members batched through the GEMMs give, per
+    member, exactly the single-state result (bitwise)."""
+    import torch
+
+    from paper_2403_20135_b200.integrators import DeviceStepper
+
+    p = gpu(63, max_batch=12)
+    table = CollocationTable.radau_right(3)
+    cfg = SdcConfig(table=table, n_sweeps=3, mode=SweepMode.DIAGONAL_PARALLEL, time_threads=3)
+    states = np.stack([random_initial_state(p.grid, 20 + e) for e in range(4)])
+    ens = torch.from_numpy(states).to(p.device).contiguous()
+    st = DeviceStepper(p, cfg, 120.0, serial=False, members=4)
+    st.run(ens, 3)
+    single = DeviceStepper(p, cfg, 120.0, serial=False)
+    for e in range(4):
+        u = torch.from_numpy(states[e]).to(p.device).contiguous()
+        single.run(u, 3)
+        assert torch.equal(u, ens[e])
+    assert st.diverged() == 0
+    st.close()
+    single.close()
