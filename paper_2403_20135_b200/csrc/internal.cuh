@@ -49,8 +49,10 @@ struct Plan {
   double* wsyn;     // [J] 2 pi w_j / (a (1 - mu_j^2))
   double* wke;      // [J] 2 pi w_j
   double2* twiddle; // [nlon] exp(-2 pi i k / nlon)
-  int* anal_work;   // [n_anal_work] (m << 16 | row block)
+  int* anal_work;   // [n_anal_work] (m << 16 | row block of anal_wj tiles)
   int n_anal_work;
+  int* anal_work4;  // [n_anal_work4] row blocks of 4 tiles (throughput regime)
+  int n_anal_work4;
   int synth_wj, anal_wj;  // row tiles per CTA (the other warps split K)
   FftPlan fft;
   // workspaces
@@ -59,6 +61,7 @@ struct Plan {
   double* coef_dev; // small per-call coefficient staging [kCoefCap]
   double* xsyn;     // [rows][max_batch][12] synthesis B operand for API calls
   int xsyn_nb;      // record batch of the last API prep (padding rows zero for it)
+  int fe_chunk;     // f_E batch chunk keeping the Fourier workspaces L2-resident (0 = no chunking)
   int ring_threads;
   size_t ring_smem;
 };
@@ -146,7 +149,7 @@ inline Work plan_work(const Plan& p, int batch_offset = 0) {
 
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_synth_prep(const Plan& p, const double2* u, int nb, double* xsyn,
-                              cudaStream_t s);
+                              cudaStream_t s, int chunk = 0);
 cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, int nb,
                              cudaStream_t s, int* step_counter);
 cudaError_t launch_ring(const Plan& p, const Work& w, int nb, cudaStream_t s);
@@ -159,7 +162,7 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                const double2* u0, const double2* fe, long long fe_stride,
                                const double2* fi, long long fi_stride, int first, double2* u_out,
                                double2* fi_out, double* xsyn_out, cudaStream_t s, int members = 1,
-                               long long fe_mstride = 0, long long fi_mstride = 0);
+                               long long fe_mstride = 0, long long fi_mstride = 0, int chunk = 0);
 cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, const double2* u0,
                               const double2* fe, long long fe_stride, const double2* fi,
                               long long fi_stride, int first, double2* u_out, int* diverged,
@@ -184,6 +187,6 @@ cudaError_t launch_check_finite(const double* x, long long n, int* flag, cudaStr
 cudaError_t f_expl(Plan& p, const double2* u, double2* fe, int nb, cudaStream_t s,
                    int* step_counter);
 cudaError_t f_expl_prepped(const Plan& p, const Work& w, const double* xsyn, double2* fe, int nb,
-                           cudaStream_t s, int* step_counter);
+                           cudaStream_t s, int* step_counter, int chunk = 0);
 
 }  // namespace sdcsw

@@ -58,7 +58,7 @@ constexpr int kWarps = 4;
 __global__ void __launch_bounds__(256) k_synth_prep(const double* __restrict__ u, int C2, int nb,
                                                     const double2* __restrict__ xscale,
                                                     const int* __restrict__ idx_row,
-                                                    double* __restrict__ xsyn) {
+                                                    double* __restrict__ xsyn, int rows, int chunk) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -66,39 +66,41 @@ __global__ void __launch_bounds__(256) k_synth_prep(const double* __restrict__ u
   const int b = blockIdx.y;
   const double* s = u + (size_t)b * 3 * C2;
   const int idx = e >> 1;
-  double* rec = xsyn + ((size_t)idx_row[idx] * nb + b) * kXsyn;
+  const int ch = chunk > 0 ? chunk : nb;  // chunk-major record layout (see f_expl_prepped)
+  const int cb = b / ch, w = nb - cb * ch < ch ? nb - cb * ch : ch;
+  double* rec = xsyn + ((size_t)cb * rows * ch + (size_t)idx_row[idx] * w + (b - cb * ch)) * kXsyn;
   write_xsyn_half(rec, e & 1, s[e], s[C2 + e], s[2 * C2 + e], xscale[idx]);
 }
 
 // ---------------------------------------------------------------------------
 // synthesis: xsyn -> fsyn [nb][J][L][4 (U,V,zeta,Phi)][2 (N,S)]
-// grid (J / (16 WJ), T+1, ceil(nb/NB)), block 32*kWarps
-// column tile c = batch entry b0 + c: P cols (U,V,zeta,Phi) x (re,im);
-// the H tile reuses the same column positions (zeta/Phi columns zero).
+// grid (J / (16 WJ), T+1, ceil(nb / (NB NBC))), block 32 WJ WK
+// Batch entries are taken in pairs (b, b+1).  Column tile 2p of pair p holds
+// (U, V) x (re, im) of both entries, tile 2p + 1 their (zeta, Phi); the H-table
+// contribution (U and V only) has exactly the (U, V) tile's columns, so it
+// accumulates into the same registers - no zero columns, no extra accumulators.
+// A CTA loops over NBC batch blocks of NB entries; its table slice is then
+// re-read from L1 instead of being re-fetched by a separate CTA per block.
 // ---------------------------------------------------------------------------
 template <int NB, int PF>
 __global__ void __launch_bounds__(32 * kWarps) k_synthesis(
     const double* __restrict__ xsyn, int nb, int T, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
-    const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ) {
+    const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ,
+    int NBC) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
-  constexpr int NACC = 2 * NB * 4;  // doubles per lane (E and O, re and im)
-  __shared__ double red[kWarps * 32 * NACC];
+  constexpr int NPAIR = (NB + 1) / 2;
+  constexpr int NT = 2 * NPAIR;     // column tiles: (U,V) and (zeta,Phi) per pair
+  constexpr int NACC = NT * 2 * 4;  // doubles per lane: tiles x row tiles x (E,O) x (re,im)
+  __shared__ double red[2 * 32 * NACC];  // two warps' partials (tree reduction)
 
   const int m = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int WK = kWarps / WJ;
+  const int WK = (blockDim.x >> 5) / WJ;
   const int jt = warp % WJ, ks = warp / WJ;
   const int j0 = (blockIdx.x * WJ + jt) * kRowsPerWarp;
-#if SDCSW_EXP == 3
-  const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
-  unsigned long long t_start = gtimer();
-  int smid;
-  asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-#endif
-  const int b0 = blockIdx.z * NB;
   const int L = T + 1;
   if (step_counter != nullptr && (blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0)
     atomicAdd(step_counter, 1);
@@ -106,143 +108,124 @@ __global__ void __launch_bounds__(32 * kWarps) k_synthesis(
   const int r0m = rowoff[m];
   const int rows = rowoff[m + 1] - r0m;
   const int le = n_even[m];
-#if SDCSW_EXP == 3
-  unsigned long long t_pro = 0, t_f1 = 0, t_kl = 0;
-  if (rows < 0) t_pro = 1;  // force the loads to complete
-  t_pro += gtimer();
-#endif
   const double* P = ptab + (size_t)r0m * J + j0 + g;
   const double* H = htab + (size_t)r0m * J + j0 + g;
-  // B fragment of tile c: record (row r0m + r + t, batch b0 + c), P column g / H column g (g < 4)
-  const int nbv = nb - b0 < NB ? nb - b0 : NB;
-  const double* X = xsyn + ((size_t)r0m * nb + b0) * kXsyn;
   const int rstride = nb * kXsyn;
-
-  double accE[2][NB][2], accO[2][NB][2];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int c = 0; c < NB; ++c) accE[a][c][0] = accE[a][c][1] = accO[a][c][0] = accO[a][c][1] = 0.0;
-
-  // K loop in two branch-free ranges (n - m even rows, then odd rows), with
-  // the fragments of step s + WK loaded before the DMMAs of step s.
-  struct Frag {
-    double aP0, aP1, aH0, aH1, bP[NB], bH[NB];
-  };
-  auto fetch = [&](int s, Frag& f) {
-    const int r = 4 * s;
-    const size_t off = (size_t)(r + t) * J;
-#if SDCSW_EXP == 1
-    f.aP0 = f.aP1 = f.aH0 = f.aH1 = 1e-3 * (double)r;
-#else
-    f.aP0 = __ldg(P + off);
-    f.aP1 = __ldg(P + off + 8);
-    f.aH0 = __ldg(H + off);
-    f.aH1 = __ldg(H + off + 8);
-#endif
-    const double* rec = X + (size_t)(r + t) * rstride;
-#pragma unroll
-    for (int c = 0; c < NB; ++c) {
-      const bool ok = c < nbv;
-#if SDCSW_EXP == 2
-      f.bP[c] = f.bH[c] = ok ? 1e-3 * r : 0.0;
-#else
-      f.bP[c] = ok ? __ldg(rec + c * kXsyn + g) : 0.0;
-      f.bH[c] = (ok && g < 4) ? __ldg(rec + c * kXsyn + 8 + g) : 0.0;
-#endif
-    }
-  };
   const int nsteps = rows >> 2;
   const int se = le >> 2;  // steps [0, se) are even-class rows
-#pragma unroll
-  for (int cls = 0; cls < 2; ++cls) {
-    const int lo = cls == 0 ? 0 : se, hi = cls == 0 ? se : nsteps;
-    int s = lo + ((ks - lo) % WK + WK) % WK;  // first step of this warp in [lo, hi)
-    if (s >= hi) continue;
-    // PF = prefetch distance in steps (2 for latency-bound small truncations,
-    // 1 where occupancy matters more)
-    Frag cur, nx1, nx2;
-    fetch(s, cur);
-    if (PF == 2) fetch(s + WK < hi ? s + WK : s, nx1);
-#if SDCSW_EXP == 3
-    if (cls == 0) { if (cur.aP0 == 12345.0) t_f1 = 1; t_f1 += gtimer(); }
-#endif
-    for (; s < hi; s += WK) {
-      const int sn = s + PF * WK < hi ? s + PF * WK : s;  // clamped: always a valid address
-      fetch(sn, PF == 2 ? nx2 : nx1);
-      if (cls == 0) {
-#pragma unroll
-        for (int c = 0; c < NB; ++c) {
-          dmma(accE[0][c], cur.aP0, cur.bP[c]); dmma(accE[1][c], cur.aP1, cur.bP[c]);
-          dmma(accO[0][c], cur.aH0, cur.bH[c]); dmma(accO[1][c], cur.aH1, cur.bH[c]);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < NB; ++c) {
-          dmma(accO[0][c], cur.aP0, cur.bP[c]); dmma(accO[1][c], cur.aP1, cur.bP[c]);
-          dmma(accE[0][c], cur.aH0, cur.bH[c]); dmma(accE[1][c], cur.aH1, cur.bH[c]);
-        }
-      }
-      cur = nx1;
-      if (PF == 2) nx1 = nx2;
-    }
-  }
-#if SDCSW_EXP == 3
-  if (accE[0][0][0] == 12345.0) t_kl = 1;
-  t_kl += gtimer();
-#endif
-  // fixed-order reduction over the K-splits of each row tile
-  if (WK > 1) {  // lane-fastest layout: conflict-free shared-memory traffic
-    double* d = red + warp * NACC * 32 + lane;
-    int q = 0;
+  const int gb = g >> 2, gc = g & 3;  // lane's entry within the pair, column within the entry
+
+  for (int bb = 0; bb < NBC; ++bb) {
+    const int b0 = (blockIdx.z * NBC + bb) * NB;
+    if (b0 >= nb) break;
+    const int nbv = nb - b0 < NB ? nb - b0 : NB;
+    const double* X = xsyn + ((size_t)r0m * nb + b0) * kXsyn;
+
+    double aE[2][NT][2], aO[2][NT][2];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        d[32 * q++] = accE[a][c][0]; d[32 * q++] = accE[a][c][1];
-        d[32 * q++] = accO[a][c][0]; d[32 * q++] = accO[a][c][1];
+      for (int c = 0; c < NT; ++c) aE[a][c][0] = aE[a][c][1] = aO[a][c][0] = aO[a][c][1] = 0.0;
+
+    // K loop in two branch-free ranges (even rows, then odd rows); fragments of
+    // step s + PF WK are loaded before the DMMAs of step s
+    struct Frag {
+      double aP0, aP1, aH0, aH1, bP[NT], bH[NPAIR];
+    };
+    auto fetch = [&](int s, Frag& f) {
+      const int r = 4 * s;
+      const size_t off = (size_t)(r + t) * J;
+      f.aP0 = __ldg(P + off);
+      f.aP1 = __ldg(P + off + 8);
+      f.aH0 = __ldg(H + off);
+      f.aH1 = __ldg(H + off + 8);
+      const double* rec = X + (size_t)(r + t) * rstride;
+#pragma unroll
+      for (int p = 0; p < NPAIR; ++p) {
+        const int be = 2 * p + gb;
+        const bool ok = be < nbv;
+        const double* rb = rec + be * kXsyn;
+        f.bP[2 * p] = ok ? __ldg(rb + gc) : 0.0;          // U, V (P part)
+        f.bP[2 * p + 1] = ok ? __ldg(rb + 4 + gc) : 0.0;  // zeta, Phi
+        f.bH[p] = ok ? __ldg(rb + 8 + gc) : 0.0;          // U, V (H part)
       }
-    __syncthreads();
-    if (ks != 0) return;
-    for (int w = 1; w < WK; ++w) {
-      const double* e = red + (w * WJ + jt) * NACC * 32 + lane;
-      int qq = 0;
+    };
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+    for (int cls = 0; cls < 2; ++cls) {
+      const int lo = cls == 0 ? 0 : se, hi = cls == 0 ? se : nsteps;
+      int s = lo + ((ks - lo) % WK + WK) % WK;  // first step of this warp in [lo, hi)
+      if (s >= hi) continue;
+      Frag cur, nx1, nx2;
+      fetch(s, cur);
+      if (PF == 2) fetch(s + WK < hi ? s + WK : s, nx1);
+      for (; s < hi; s += WK) {
+        const int sn = s + PF * WK < hi ? s + PF * WK : s;  // clamped: always a valid address
+        fetch(sn, PF == 2 ? nx2 : nx1);
+        if (cls == 0) {  // n - m even: P symmetric (E), H antisymmetric (O)
 #pragma unroll
-        for (int c = 0; c < NB; ++c) {
-          accE[a][c][0] += e[32 * qq++]; accE[a][c][1] += e[32 * qq++];
-          accO[a][c][0] += e[32 * qq++]; accO[a][c][1] += e[32 * qq++];
+          for (int c = 0; c < NT; ++c) { dmma(aE[0][c], cur.aP0, cur.bP[c]); dmma(aE[1][c], cur.aP1, cur.bP[c]); }
+#pragma unroll
+          for (int p = 0; p < NPAIR; ++p) { dmma(aO[0][2 * p], cur.aH0, cur.bH[p]); dmma(aO[1][2 * p], cur.aH1, cur.bH[p]); }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NT; ++c) { dmma(aO[0][c], cur.aP0, cur.bP[c]); dmma(aO[1][c], cur.aP1, cur.bP[c]); }
+#pragma unroll
+          for (int p = 0; p < NPAIR; ++p) { dmma(aE[0][2 * p], cur.aH0, cur.bH[p]); dmma(aE[1][2 * p], cur.aH1, cur.bH[p]); }
         }
+        cur = nx1;
+        if (PF == 2) nx1 = nx2;
+      }
+    }
+    // fixed-order tree reduction over the K-splits ((w0 + w2) + (w1 + w3));
+    // lane-fastest layout, conflict-free
+    bool owner = true;
+    if (WK > 1) {
+      for (int half = WK / 2; half >= 1; half /= 2) {
+        __syncthreads();  // `red` is free
+        if (ks >= half && ks < 2 * half) {
+          double* d = red + ((ks - half) * WJ + jt) * NACC * 32 + lane;
+          int q = 0;
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int c = 0; c < NT; ++c) {
+              d[32 * q++] = aE[a][c][0]; d[32 * q++] = aE[a][c][1];
+              d[32 * q++] = aO[a][c][0]; d[32 * q++] = aO[a][c][1];
+            }
+        }
+        __syncthreads();
+        if (ks < half) {
+          const double* e = red + (ks * WJ + jt) * NACC * 32 + lane;
+          int q = 0;
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int c = 0; c < NT; ++c) {
+              aE[a][c][0] += e[32 * q++]; aE[a][c][1] += e[32 * q++];
+              aO[a][c][0] += e[32 * q++]; aO[a][c][1] += e[32 * q++];
+            }
+        }
+      }
+      owner = ks == 0;
+    }
+    if (owner && j0 < J) {
+      // epilogue: lane (g, t) of tile c holds batch b0 + 2 (c/2) + (t >> 1),
+      // field (t & 1) + 2 (c & 1)  (U, V, zeta, Phi)
+#pragma unroll
+      for (int c = 0; c < NT; ++c) {
+        const int be = 2 * (c >> 1) + (t >> 1);
+        const int f = (t & 1) + 2 * (c & 1);
+        if (be >= nbv) continue;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const int j = j0 + 8 * a + g;
+          double2* dst = fsyn + ((((size_t)(b0 + be) * J + j) * L + m) * 4 + f) * 2;
+          dst[0] = make_double2(aE[a][c][0] + aO[a][c][0], aE[a][c][1] + aO[a][c][1]);
+          dst[1] = make_double2(aE[a][c][0] - aO[a][c][0], aE[a][c][1] - aO[a][c][1]);
+        }
+      }
     }
   }
-#if SDCSW_EXP == 3
-  unsigned long long t_loop = gtimer();
-#endif
-  if (j0 >= J) return;
-  // epilogue: lane holds (re, im) of field f = t (U, V, zeta, Phi) of batch b0 + c
-#pragma unroll
-  for (int c = 0; c < NB; ++c) {
-    if (c >= nbv) continue;
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      const int j = j0 + 8 * a + g;
-      double2* dst = fsyn + ((((size_t)(b0 + c) * J + j) * L + m) * 4 + t) * 2;
-      dst[0] = make_double2(accE[a][c][0] + accO[a][c][0], accE[a][c][1] + accO[a][c][1]);
-      dst[1] = make_double2(accE[a][c][0] - accO[a][c][0], accE[a][c][1] - accO[a][c][1]);
-    }
-  }
-#if SDCSW_EXP == 3
-  if (threadIdx.x == 0 && cta_id < (1 << 14)) {
-    g_times[8 * cta_id] = t_start;
-    g_times[8 * cta_id + 1] = t_loop;
-    g_times[8 * cta_id + 2] = gtimer();
-    g_times[8 * cta_id + 3] = smid;
-    g_times[8 * cta_id + 4] = t_pro;
-    g_times[8 * cta_id + 5] = t_f1;
-    g_times[8 * cta_id + 6] = t_kl;
-  }
-#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -418,27 +401,37 @@ static int pick_nb(int nb) { return nb <= 6 ? nb : 4; }
 #define SDCSW_NB_LIST(X) X(1) X(2) X(3) X(4) X(5) X(6)
 
 cudaError_t launch_synth_prep(const Plan& p, const double2* u, int nb, double* xsyn,
-                              cudaStream_t s) {
+                              cudaStream_t s, int chunk) {
   launch_k(k_synth_prep, dim3((2 * p.C + 255) / 256, nb), 256, 0, s, 
-      reinterpret_cast<const double*>(u), 2 * p.C, nb, p.xscale, p.idx_row, xsyn);
+      reinterpret_cast<const double*>(u), 2 * p.C, nb, p.xscale, p.idx_row, xsyn, p.rows, chunk);
   return cudaGetLastError();
 }
 
 cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, int nb,
                              cudaStream_t s, int* step_counter) {
   const int NB = pick_nb(nb);
-  const int WJ = p.synth_wj;
-  dim3 grid(p.J / (kRowsPerWarp * WJ), p.T + 1, (nb + NB - 1) / NB);
+  const int nblk = (nb + NB - 1) / NB;
+  // latency regime (few batch blocks): 1 row tile x 4 K-splits (small T) or the
+  // plan's WJ x (4 / WJ); throughput regime (many batch blocks): 4 row tiles,
+  // no K-split, NBC batch blocks per CTA so the table slice is reused from L1
+  int WJ = p.synth_wj, WK = kWarps / WJ, NBC = 1;
+  if (nblk >= 4) {
+    WJ = (p.J / kRowsPerWarp) % 4 == 0 ? 4 : ((p.J / kRowsPerWarp) % 3 == 0 ? 3 : 2);
+    WK = 1;
+    NBC = nblk >= 32 ? 8 : (nblk >= 8 ? 4 : 2);
+  }
+  dim3 grid(p.J / (kRowsPerWarp * WJ), p.T + 1, (nblk + NBC - 1) / NBC);
+  const dim3 block(32 * WJ * WK);
 #define SDCSW_SYN(NBV)                                                                         \
   if (NB == NBV) {                                                                             \
     if (p.T < 200)                                                                             \
-      launch_k(k_synthesis<NBV, 2>, grid, 32 * kWarps, 0, s, xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
+      launch_k(k_synthesis<NBV, 2>, grid, block, 0, s, xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
                                                        p.rowoff, p.n_even, w.fsyn,             \
-                                                       step_counter, WJ);                      \
+                                                       step_counter, WJ, NBC);                 \
     else                                                                                       \
-      launch_k(k_synthesis<NBV, 1>, grid, 32 * kWarps, 0, s, xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
+      launch_k(k_synthesis<NBV, 1>, grid, block, 0, s, xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
                                                        p.rowoff, p.n_even, w.fsyn,             \
-                                                       step_counter, WJ);                      \
+                                                       step_counter, WJ, NBC);                 \
     return cudaGetLastError();                                                                 \
   }
   SDCSW_NB_LIST(SDCSW_SYN)

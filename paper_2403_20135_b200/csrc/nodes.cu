@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
     long long fi_stride, int first, double phibar, const double* __restrict__ lamv,
     double* __restrict__ u_out, double* fi_out, const double2* __restrict__ xscale,
     const int* __restrict__ idx_row, double* __restrict__ xsyn, long long fe_mstride,
-    long long fi_mstride) {
+    long long fi_mstride, int rows, int chunk) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -124,9 +124,12 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
   const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
   store_tri(u_out + (size_t)ob * 3 * C2, C2, e, u);
   store_tri(fi_out + (size_t)ob * 3 * C2, C2, e, f_impl_tri(u, phibar, lam));
-  if (xsyn != nullptr)  // synthesis B operand of the f_E that follows (batch = this launch)
-    write_xsyn_half(xsyn + ((size_t)idx_row[e >> 1] * gridDim.y * gridDim.z + ob) * kXsyn, e & 1,
-                    u.phi, u.zeta, u.delta, xscale[e >> 1]);
+  if (xsyn != nullptr) {  // synthesis B operand of the f_E that follows, in batch chunks
+    const int nbt = gridDim.y * gridDim.z, ch = chunk > 0 ? chunk : nbt;
+    const int cb = ob / ch, w = nbt - cb * ch < ch ? nbt - cb * ch : ch;
+    write_xsyn_half(xsyn + ((size_t)cb * rows * ch + (size_t)idx_row[e >> 1] * w + (ob - cb * ch)) * kXsyn,
+                    e & 1, u.phi, u.zeta, u.delta, xscale[e >> 1]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(256) k_final_node(
     long long fe_stride, const double* __restrict__ fi, long long fi_stride, int first,
     double phibar, const double* __restrict__ lamv, double* u_out, int* diverged,
     const int* step_counter, const double2* __restrict__ xscale, const int* __restrict__ idx_row,
-    double* __restrict__ xsyn, long long fe_mstride, long long fi_mstride) {
+    double* __restrict__ xsyn, long long fe_mstride, long long fi_mstride, int rows, int chunk) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -162,9 +165,12 @@ __global__ void __launch_bounds__(256) k_final_node(
   const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
   store_tri(u_out, C2, e, u);
   if (diverged != nullptr && !finite_tri(u)) atomicMin(diverged, step_counter ? *step_counter : 1);
-  if (xsyn != nullptr)  // B operand of the next step's f_E(u0) (batch = members)
-    write_xsyn_half(xsyn + ((size_t)idx_row[e >> 1] * gridDim.z + z) * kXsyn, e & 1, u.phi,
-                    u.zeta, u.delta, xscale[e >> 1]);
+  if (xsyn != nullptr) {  // B operand of the next step's f_E(u0) (batch = members, chunked)
+    const int nbt = gridDim.z, ch = chunk > 0 ? chunk : nbt;
+    const int cb = z / ch, w = nbt - cb * ch < ch ? nbt - cb * ch : ch;
+    write_xsyn_half(xsyn + ((size_t)cb * rows * ch + (size_t)idx_row[e >> 1] * w + (z - cb * ch)) * kXsyn,
+                    e & 1, u.phi, u.zeta, u.delta, xscale[e >> 1]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -321,7 +327,7 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                const double2* u0, const double2* fe, long long fe_stride,
                                const double2* fi, long long fi_stride, int first, double2* u_out,
                                double2* fi_out, double* xsyn_out, cudaStream_t s, int members,
-                               long long fe_mstride, long long fi_mstride) {
+                               long long fe_mstride, long long fi_mstride, int chunk) {
   const long long S2 = 6LL * p.C;  // doubles per state
   dim3 grid = grid_for(p.C, count);
   grid.z = members;
@@ -329,7 +335,8 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                                      D(u0), D(fe), fe_stride * S2, D(fi),
                                                      fi_stride * S2, first, p.phibar, p.lam,
                                                      W(u_out), W(fi_out), p.xscale, p.idx_row,
-                                                     xsyn_out, fe_mstride * S2, fi_mstride * S2);
+                                                     xsyn_out, fe_mstride * S2, fi_mstride * S2,
+                                                     p.rows, chunk);
   return cudaGetLastError();
 }
 
@@ -344,7 +351,8 @@ cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, con
   launch_k(k_final_node, grid, 256, 0, s, 2 * p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
                                              fe_stride * S2, D(fi), fi_stride * S2, first, p.phibar,
                                              p.lam, W(u_out), diverged, step_counter, p.xscale,
-                                             p.idx_row, xsyn_out, fe_mstride * S2, fi_mstride * S2);
+                                             p.idx_row, xsyn_out, fe_mstride * S2, fi_mstride * S2,
+                                             p.rows, p.fe_chunk);
   return cudaGetLastError();
 }
 

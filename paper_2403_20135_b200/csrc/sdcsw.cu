@@ -34,12 +34,22 @@ size_t ring_smem_bytes(int nlon);
 bool ring_supported(int nlon);
 
 cudaError_t f_expl_prepped(const Plan& p, const Work& w, const double* xsyn, double2* fe, int nb,
-                           cudaStream_t s, int* step_counter) {
-  cudaError_t e = launch_synthesis(p, w, xsyn, nb, s, step_counter);
-  if (e != cudaSuccess) return e;
-  e = launch_ring(p, w, nb, s);
-  if (e != cudaSuccess) return e;
-  return launch_analysis(p, w, fe, nb, s);
+                           cudaStream_t s, int* step_counter, int chunk) {
+  // chunk > 0: the operand is chunk-major ([nb/chunk][rows][chunk][kXsyn]) and
+  // each chunk runs synthesis -> ring -> analysis on its own (L2-resident)
+  const int ch = chunk > 0 && chunk < nb ? chunk : nb;
+  for (int b0 = 0; b0 < nb; b0 += ch) {
+    const int n = nb - b0 < ch ? nb - b0 : ch;
+    const double* xs = xsyn + (size_t)b0 * p.rows * kXsyn;
+    double2* out = fe + (size_t)b0 * 3 * p.C;
+    cudaError_t e = launch_synthesis(p, w, xs, n, s, b0 == 0 ? step_counter : nullptr);
+    if (e != cudaSuccess) return e;
+    e = launch_ring(p, w, n, s);
+    if (e != cudaSuccess) return e;
+    e = launch_analysis(p, w, out, n, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t f_expl(Plan& p, const double2* u, double2* fe, int nb, cudaStream_t s,
@@ -201,6 +211,12 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
     for (int rb = 0; rb * per < rows; ++rb) work.push_back((m << 16) | rb);
   }
   p.n_anal_work = (int)work.size();
+  std::vector<int> work4;
+  for (int m = 0; m <= T; ++m) {
+    const int rows = rowoff[m + 1] - rowoff[m];
+    for (int rb = 0; rb * 4 * kRowsPerWarp < rows; ++rb) work4.push_back((m << 16) | rb);
+  }
+  p.n_anal_work4 = (int)work4.size();
   p.ring_threads = 256;
   p.ring_smem = ring_smem_bytes(nlon);
 
@@ -221,6 +237,7 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
       (e = upload(&p.wke, wke.data(), wke.size())) != cudaSuccess ||
       (e = upload(&p.twiddle, tw.data(), tw.size())) != cudaSuccess ||
       (e = upload(&p.anal_work, work.data(), work.size())) != cudaSuccess ||
+      (e = upload(&p.anal_work4, work4.data(), work4.size())) != cudaSuccess ||
       (e = cudaMalloc(&p.fsyn, (size_t)p.max_batch * J * p.L * 8 * sizeof(double2))) != cudaSuccess ||
       (e = cudaMalloc(&p.gan, (size_t)p.max_batch * J * p.L * kNumSlots * 2 * sizeof(double2))) !=
           cudaSuccess ||
@@ -230,13 +247,28 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
     int st = cuda_status(e, "sdcsw_plan_create");
     void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
                     p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev,
-                    p.xscale, p.idx_row, p.xsyn};
+                    p.xscale, p.idx_row, p.xsyn, p.anal_work4};
     for (void* q : ptrs)
       if (q) cudaFree(q);
     delete h;
     return st;
   }
   p.xsyn_nb = -1;
+  {
+    // Chunk big f_E batches so that one chunk's Fourier + analysis workspaces
+    // (22 complex per (pair, m) and state) and the tables fit in ~half the L2;
+    // only when the tables themselves are L2-resident (otherwise batching
+    // amortises their HBM stream instead).  SDCSW_FE_CHUNK overrides.
+    const double per_state = (double)J * p.L * 22 * sizeof(double2);
+    const double tables = 2.0 * p.rows * J * sizeof(double);
+    // measured on B200: chunking the c4 ensemble (T127, 256 states) to keep
+    // the workspaces L2-resident was slower than one big batch, so it is off
+    // unless requested
+    (void)per_state;
+    (void)tables;
+    p.fe_chunk = 0;
+    if (const char* env = getenv("SDCSW_FE_CHUNK")) p.fe_chunk = atoi(env);
+  }
   h->alive = true;
   *out = h;
   return SDCSW_OK;
@@ -252,7 +284,7 @@ int sdcsw_plan_destroy(sdcsw_plan* h) {
   Plan& p = h->p;
   void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
                   p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev,
-                  p.xscale, p.idx_row, p.xsyn};
+                  p.xscale, p.idx_row, p.xsyn, p.anal_work4};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   h->alive = false;
@@ -384,7 +416,7 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
   // f_E(u0) of every member from the operand the previous step's last kernel
   // (or the run's prep) wrote into xsyn1
   const int E = st->members;
-  cudaError_t e = f_expl_prepped(p, plan_work(p), st->xsyn1, st->fe0, E, s, counter);
+  cudaError_t e = f_expl_prepped(p, plan_work(p), st->xsyn1, st->fe0, E, s, counter, p.fe_chunk);
   if (e != cudaSuccess) return e;
   if (st->mode == 0) {
     // fi alternates between two buffers: every node reads all fi_j while
@@ -413,9 +445,10 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
         double* xs = st->xsynM + (size_t)lo * E * p.rows * kXsyn;
         e = launch_sweep_nodes(p, M, lo, cnt, coef, u, first ? st->fe0 : st->fe, first ? 0 : 1,
                                fi_cur, first ? 0 : 1, first, st->ustage + lo * S,
-                               fi_new + lo * S, xs, sg, E, first ? 1 : mS, mS);
+                               fi_new + lo * S, xs, sg, E, first ? 1 : mS, mS, p.fe_chunk);
         if (e != cudaSuccess) return e;
-        e = f_expl_prepped(p, plan_work(p, lo), xs, st->fe + lo * S, cnt * E, sg, nullptr);
+        e = f_expl_prepped(p, plan_work(p, lo), xs, st->fe + lo * S, cnt * E, sg, nullptr,
+                           p.fe_chunk);
         if (e != cudaSuccess) return e;
       }
       if (G > 1) {
@@ -606,7 +639,8 @@ int sdcsw_stepper_run(sdcsw_stepper* s, double* u, int n_steps, int use_graph, v
   if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
   if (n_steps == 0) return SDCSW_OK;
   // the caller may have changed u since the last step: rebuild its synthesis operand
-  e = launch_synth_prep(s->plan->p, (const double2*)u, s->members, s->xsyn1, cs);
+  e = launch_synth_prep(s->plan->p, (const double2*)u, s->members, s->xsyn1, cs,
+                        s->plan->p.fe_chunk);
   if (e != cudaSuccess) return cuda_status(e, "sdcsw_stepper_run prep");
   if (!use_graph) {
     for (int i = 0; i < n_steps; ++i) {
