@@ -64,6 +64,10 @@ struct Plan {
   int fe_chunk;     // f_E batch chunk keeping the Fourier workspaces L2-resident (0 = no chunking)
   int ring_threads;
   size_t ring_smem;
+  // TMA tensor maps (CUtensorMap, 128 B each) over the P / H tables for the
+  // table-streaming analysis (T >= 400); tma_ok = maps built
+  alignas(64) unsigned long long tmap[2][16];
+  bool tma_ok;
 };
 constexpr int kCoefCap = 4096;
 
@@ -181,6 +185,10 @@ cudaError_t launch_serial_update(const Plan& p, int m, double we, double wi, dou
                                  const double2* fi_new, const double2* fi_old, const double2* u0,
                                  int first, cudaStream_t s);
 cudaError_t launch_check_finite(const double* x, long long n, int* flag, cudaStream_t s);
+
+cudaError_t make_table_maps(Plan& p);
+bool launch_analysis_tma(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s,
+                         cudaError_t* err);
 
 // f_E = (prep) -> synthesis -> ring -> analysis; f_expl_prepped starts from an
 // xsyn operand a producer kernel already wrote

@@ -440,6 +440,8 @@ cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, i
 }
 
 cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s) {
+  cudaError_t err;
+  if (launch_analysis_tma(p, w, fe, nb, s, &err)) return err;  // table-streaming regime
   const int NB = pick_nb(nb);
   dim3 grid(p.n_anal_work, (nb + NB - 1) / NB);
 #define SDCSW_ANA(NBV)                                                                          \

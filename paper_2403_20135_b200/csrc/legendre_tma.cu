@@ -1,0 +1,296 @@
+// Table-streaming Legendre analysis for large truncations (T >= 400, where the
+// P/H tables - 403 MB each at T511 - live in HBM, not L2).
+//
+// The A operand (table rows x latitudes) is streamed into shared memory by the
+// Tensor Memory Accelerator: cp.async.bulk.tensor.2d boxes of 64 rows x 16
+// latitudes (8 KB per table), 128-byte swizzled, completing on an mbarrier,
+// in a kStages-deep ring.  One elected thread issues the copies; the four
+// warps (one 16-row tile each) read DMMA A fragments from the swizzled tiles
+// and B fragments (analysis data, shared by all four warps) through L1.  The
+// table stream is thus decoupled from register prefetching, which is what
+// limited the register-only kernel (k_analysis) at T511.
+//
+// Same contraction and epilogue as k_analysis in legendre.cu:
+//   out[n,c] = sum_j P[n,j] Xfold[j,c] + sum_j H[n,j] Yfold[j,c]
+//   (pkg/src/parsdc/problems/swe.py:180-190 restated on the sphere).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "internal.cuh"
+
+namespace sdcsw {
+
+constexpr int kTmaRows = 64;   // table rows per CTA (4 warps x 16)
+constexpr int kTmaLat = 16;    // latitudes per stage (128 B per row, the swizzle span)
+constexpr int kStages = 4;
+constexpr int kTileBytes = kTmaRows * kTmaLat * 8;  // 8 KB per table per stage
+
+__device__ __forceinline__ void dmma_t(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// element (row, k) of a 128B-swizzled [rows][16] double tile
+__device__ __forceinline__ double swz(const double* tile, int row, int k) {
+  const int chunk = (k >> 1) ^ (row & 7);
+  return tile[row * 16 + chunk * 2 + (k & 1)];
+}
+
+template <int NB>
+__global__ void __launch_bounds__(128) k_analysis_tma(
+    const __grid_constant__ CUtensorMap pmap, const __grid_constant__ CUtensorMap hmap,
+    const double2* __restrict__ gan, int nb, int T, int J, int C, const int* __restrict__ rowoff,
+    const int* __restrict__ n_even, const int* __restrict__ row_n, const int* __restrict__ moff,
+    const double* __restrict__ lam, const int* __restrict__ work, double2* __restrict__ fe) {
+  SDCSW_PDL_ENTRY();
+  constexpr int HU = 6 * NB;
+  constexpr int TH = (HU + 7) / 8;
+  constexpr int PC = 8 * NB;
+  constexpr int OS = PC + 1;
+  extern __shared__ __align__(1024) unsigned char tma_smem[];
+  double* ptile = reinterpret_cast<double*>(tma_smem);                    // [kStages][64][16]
+  double* htile = reinterpret_cast<double*>(tma_smem + kStages * kTileBytes);
+  unsigned long long* full =
+      reinterpret_cast<unsigned long long*>(tma_smem + 2 * kStages * kTileBytes);
+
+  const int wk = work[blockIdx.x];
+  const int m = wk >> 16, rb = wk & 0xffff;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int b0 = blockIdx.y * NB;
+  const int L = T + 1;
+  const int r0m = rowoff[m];
+  const int rows = rowoff[m + 1] - r0m;
+  const int le = n_even[m];
+  const int rblock = r0m + rb * kTmaRows;  // first table row of this CTA
+  const int rw = rb * kTmaRows + warp * kRowsPerWarp;
+  const bool live = rw < rows;
+  const bool ev0 = rw < le, ev1 = rw + 8 < le;
+  const int nchunks = J / kTmaLat;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  // the tables are constant: start streaming before waiting for the producer kernel
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages && s < nchunks; ++s) {
+      mbar_expect_tx(&full[s], 2 * kTileBytes);
+      tma_load_2d(ptile + s * kTmaRows * kTmaLat, &pmap, s * kTmaLat, rblock, &full[s]);
+      tma_load_2d(htile + s * kTmaRows * kTmaLat, &hmap, s * kTmaLat, rblock, &full[s]);
+    }
+  }
+  SDCSW_PDL_WAIT();
+
+  // B columns of this lane (one per tile), as in k_analysis
+  const double* gb = reinterpret_cast<const double*>(gan);
+  long long pbase[NB], hbase[TH];
+  int pel[NB], hel[TH];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    const int col = 8 * c + g;
+    int b, slot;
+    if (col < HU) { b = col / 6; slot = kXPhi + (col % 6) / 2; }
+    else { b = (col - HU) >> 1; slot = kXKe; }
+    pbase[c] = b0 + b < nb ? (((long long)(b0 + b) * L + m) * J) * 28 : -1;
+    pel[c] = slot * 2 + (col & 1);
+  }
+#pragma unroll
+  for (int c = 0; c < TH; ++c) {
+    const int col = 8 * c + g;
+    const int b = col / 6;
+    hbase[c] = (col < HU && b0 + b < nb) ? (((long long)(b0 + b) * L + m) * J) * 28 : -1;
+    hel[c] = (kYPhi + (col % 6) / 2) * 2 + (col & 1);
+  }
+
+  double acc[2][NB][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+
+  const int row0 = warp * kRowsPerWarp + g;  // tile rows of this lane (a = 0; a = 1 adds 8)
+  struct BFrag {
+    double ps[NB], pa[NB], hs[TH], ha[TH];
+  };
+  auto fetch_b = [&](int lat, BFrag& f) {
+    const long long jrec = (long long)lat * 28;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      const bool ok = pbase[c] >= 0;
+      f.ps[c] = ok ? __ldg(gb + pbase[c] + jrec + pel[c]) : 0.0;
+      f.pa[c] = ok ? __ldg(gb + pbase[c] + jrec + 14 + pel[c]) : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < TH; ++c) {
+      const bool ok = hbase[c] >= 0;
+      f.hs[c] = ok ? __ldg(gb + hbase[c] + jrec + hel[c]) : 0.0;
+      f.ha[c] = ok ? __ldg(gb + hbase[c] + jrec + 14 + hel[c]) : 0.0;
+    }
+  };
+  BFrag cur, nxt;
+  fetch_b(t, cur);  // latitude 4 q + t of chunk 0, q = 0
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int st = ch % kStages;
+    mbar_wait(&full[st], (ch / kStages) & 1);
+    const double* pt = ptile + st * kTmaRows * kTmaLat;
+    const double* ht = htile + st * kTmaRows * kTmaLat;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      // B of the next k-step (next chunk's first after q = 3), loaded ahead
+      const int nl = q < 3 ? ch * kTmaLat + 4 * (q + 1) + t
+                           : (ch + 1 < nchunks ? (ch + 1) * kTmaLat + t : ch * kTmaLat + t);
+      fetch_b(nl, nxt);
+      if (live) {
+        const int k = 4 * q + t;
+        const double aP0 = swz(pt, row0, k), aP1 = swz(pt, row0 + 8, k);
+        const double aH0 = swz(ht, row0, k), aH1 = swz(ht, row0 + 8, k);
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          dmma_t(acc[0][c], aP0, ev0 ? cur.ps[c] : cur.pa[c]);
+          dmma_t(acc[1][c], aP1, ev1 ? cur.ps[c] : cur.pa[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < TH; ++c) {
+          dmma_t(acc[0][c], aH0, ev0 ? cur.ha[c] : cur.hs[c]);
+          dmma_t(acc[1][c], aH1, ev1 ? cur.ha[c] : cur.hs[c]);
+        }
+      }
+      cur = nxt;
+    }
+    __syncthreads();  // every warp is done with stage st
+    if (threadIdx.x == 0 && ch + kStages < nchunks) {
+      const int nc = ch + kStages;
+      mbar_expect_tx(&full[st], 2 * kTileBytes);
+      tma_load_2d(ptile + st * kTmaRows * kTmaLat, &pmap, nc * kTmaLat, rblock, &full[st]);
+      tma_load_2d(htile + st * kTmaRows * kTmaLat, &hmap, nc * kTmaLat, rblock, &full[st]);
+    }
+  }
+  if (!live) return;
+  // epilogue through a per-warp shared tile (reuses the stage buffers: all
+  // copies completed and were consumed before the last barrier)
+  double* o = ptile + warp * kRowsPerWarp * OS;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      o[(8 * a + g) * OS + 8 * c + 2 * t] = acc[a][c][0];
+      o[(8 * a + g) * OS + 8 * c + 2 * t + 1] = acc[a][c][1];
+    }
+  __syncwarp();
+  const int mo = moff[m];
+  for (int it = lane; it < kRowsPerWarp * NB; it += 32) {
+    const int rr = it % kRowsPerWarp, b = it / kRowsPerWarp;
+    if (rw + rr >= rows || b0 + b >= nb) continue;
+    const int n = row_n[r0m + rw + rr];
+    if (n < 0) continue;
+    const int idx = mo + n - m;
+    const double* row = o + rr * OS;
+    const double l = lam[idx];
+    double2 phi = make_double2(row[6 * b + 0], row[6 * b + 1]);
+    double2 zeta = make_double2(row[6 * b + 2], row[6 * b + 3]);
+    double2 delta = make_double2(row[6 * b + 4] + l * row[6 * NB + 2 * b],
+                                 row[6 * b + 5] + l * row[6 * NB + 2 * b + 1]);
+    if (m == 0) phi.y = zeta.y = delta.y = 0.0;
+    double2* dst = fe + (size_t)(b0 + b) * 3 * C;
+    dst[idx] = phi;
+    dst[C + idx] = zeta;
+    dst[2 * C + idx] = delta;
+  }
+}
+
+constexpr size_t kTmaSmem = 2 * kStages * kTileBytes + 64;
+
+static_assert(kRowsPerWarp * (8 * 6 + 1) * 4 * 8 <= 2 * kStages * kTileBytes,
+              "epilogue tiles fit in the stage buffers");
+
+// Tensor maps over the packed tables: dims {J, rows + 16}, box {16, 64},
+// 128-byte swizzle; out-of-range rows read as zero.
+cudaError_t make_table_maps(Plan& p) {
+  p.tma_ok = false;
+  if (p.T < 400 || p.J % kTmaLat) return cudaSuccess;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || !fn || q != cudaDriverEntryPointSuccess) return cudaSuccess;
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  const cuuint64_t dims[2] = {(cuuint64_t)p.J, (cuuint64_t)p.rows + 16};
+  const cuuint64_t strides[1] = {(cuuint64_t)p.J * sizeof(double)};
+  const cuuint32_t box[2] = {kTmaLat, kTmaRows};
+  const cuuint32_t elem[2] = {1, 1};
+  double* tabs[2] = {p.ptab, p.htab};
+  for (int i = 0; i < 2; ++i) {
+    CUresult r = encode(reinterpret_cast<CUtensorMap*>(&p.tmap[i]), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                        tabs[i], dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaSuccess;  // fall back to k_analysis (also sm_100a)
+  }
+#define SDCSW_TMA_ATTR(NBV)                                                                     \
+  e = cudaFuncSetAttribute(k_analysis_tma<NBV>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                           (int)kTmaSmem);                                                      \
+  if (e != cudaSuccess) return e;
+  SDCSW_TMA_ATTR(1) SDCSW_TMA_ATTR(2) SDCSW_TMA_ATTR(3) SDCSW_TMA_ATTR(4) SDCSW_TMA_ATTR(5)
+  SDCSW_TMA_ATTR(6)
+#undef SDCSW_TMA_ATTR
+  p.tma_ok = true;
+  return cudaSuccess;
+}
+
+bool launch_analysis_tma(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s,
+                         cudaError_t* err) {
+  if (!p.tma_ok || p.anal_wj != 4) return false;
+  const int NB = nb <= 6 ? nb : 4;
+  dim3 grid(p.n_anal_work, (nb + NB - 1) / NB);
+  const CUtensorMap& pm = *reinterpret_cast<const CUtensorMap*>(&p.tmap[0]);
+  const CUtensorMap& hm = *reinterpret_cast<const CUtensorMap*>(&p.tmap[1]);
+#define SDCSW_TMA_LAUNCH(NBV)                                                                  \
+  if (NB == NBV) {                                                                             \
+    *err = launch_k(k_analysis_tma<NBV>, grid, dim3(128), kTmaSmem, s, pm, hm, w.gan, nb, p.T,  \
+                    p.J, p.C, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.anal_work, fe);    \
+    return true;                                                                               \
+  }
+  SDCSW_TMA_LAUNCH(1) SDCSW_TMA_LAUNCH(2) SDCSW_TMA_LAUNCH(3) SDCSW_TMA_LAUNCH(4)
+  SDCSW_TMA_LAUNCH(5) SDCSW_TMA_LAUNCH(6)
+#undef SDCSW_TMA_LAUNCH
+  return false;
+}
+
+}  // namespace sdcsw

@@ -243,6 +243,7 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
           cudaSuccess ||
       (e = cudaMalloc(&p.coef_dev, kCoefCap * sizeof(double))) != cudaSuccess ||
       (e = configure_ring(p.ring_smem)) != cudaSuccess ||
+      (e = make_table_maps(p)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess) {
     int st = cuda_status(e, "sdcsw_plan_create");
     void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
