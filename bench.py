@@ -324,8 +324,11 @@ def run_device(args):
     else:
         from paper_2403_20135_b200.parallel_nodes import CudaNodeBackend, NodeParallelDsdc
 
+        # node groups x spectral parts: the largest node-group count <= M dividing N
+        groups = max(g for g in range(1, min(world, m_nodes) + 1) if world % g == 0)
+        spectral = world // groups
         npd = NodeParallelDsdc(CudaNodeBackend(problem), cfg, dt, problem.mean_geopotential,
-                               problem.state_size)
+                               problem.state_size, spectral_parts=spectral)
         launches_per_sim_step = 3 * (1 + (k_sw - 1)) + (k_sw - 1) + 1
 
         def one_run():
@@ -431,7 +434,9 @@ def run_device(args):
                             + (f", {total_members} ensemble members ({members} per GPU), value = aggregate member-steps/s"
                                if ensemble else ""),
                 "bench_step": f"one full {nsteps}-step run", "l2": "flushed between bench steps (256 MiB write, untimed)",
-                "parallelism": "1 GPU: M nodes as concurrent graph branches / batched GEMM columns" if world == 1 else f"node blocks over {world} GPUs + NCCL all-gather per sweep",
+                "parallelism": ("1 GPU: M nodes as concurrent graph branches / batched GEMM columns" if world == 1
+                                else f"{world} GPUs: ensemble members sharded" if ensemble
+                                else f"{world} GPUs: node blocks x spectral (m) split, NCCL all-gathers per sweep / per f_E"),
                 "ms_per_sim_step": t_dev / sim_steps * 1e3,
                 "node_sweeps_per_s": value * node_sweeps,
                 "serial_sdc_steps_per_s_1gpu": serial_rate,

@@ -143,6 +143,22 @@ int sdcsw_transform_stage(sdcsw_plan* plan, int stage, const double* in, double*
  * which 1 = analysis data [max_batch][T+1][nlat/2][2 (N+S, N-S)][7] complex. */
 int sdcsw_workspace(sdcsw_plan* plan, int which, void** ptr, long long* bytes);
 
+/* Spectral split (more GPUs than collocation nodes): the plan's
+ * wavenumbers are partitioned over the S ranks of a spectral group, pairs
+ * (m, T-m) dealt round-robin, and this rank keeps part sp.  Afterwards
+ * sdcsw_sweep_nodes / sdcsw_final_node touch only own-m coefficients, and f_E
+ * runs as begin (operand prep + synthesis of own m into part sp of `fourier`,
+ * a caller-owned part-major buffer [S][nb][nlat/2][Lp][4][2] complex) ->
+ * caller all-gathers the S parts of `fourier` (NCCL) -> end (ring kernel over
+ * all latitudes + analysis of own m into fe).  S = 1 restores the unsplit plan.
+ * The per-m and per-latitude arithmetic is unchanged, so results are
+ * bit-identical to the unsplit plan.  Replaces nothing in the reference (its
+ * space parallelism is scipy.fft worker threads, problems/swe.py:148-153). */
+int sdcsw_plan_set_split(sdcsw_plan* plan, int S, int sp, void* fourier, long long bytes);
+int sdcsw_split_info(sdcsw_plan* plan, int* Lp, int* n_own_m, int* n_own_idx);
+int sdcsw_split_f_expl_begin(sdcsw_plan* plan, const double* u, int nb, void* stream);
+int sdcsw_split_f_expl_end(sdcsw_plan* plan, double* fe, int nb, void* stream);
+
 /* Any non-finite entry among n doubles -> *flag = 1 (device int).
  * Replaces check_finite (core.py:42-50) without a host round trip. */
 int sdcsw_check_finite(const double* x, long long n, int* flag, void* stream);

@@ -31,6 +31,10 @@ EXPORTS = (
     "sdcsw_check_finite",
     "sdcsw_transform_stage",
     "sdcsw_workspace",
+    "sdcsw_plan_set_split",
+    "sdcsw_split_info",
+    "sdcsw_split_f_expl_begin",
+    "sdcsw_split_f_expl_end",
     "sdcsw_last_error",
     "sdcsw_version",
 )
@@ -74,6 +78,10 @@ _SIGS = {
     "sdcsw_check_finite": [_p, _ll, _p, _p],
     "sdcsw_transform_stage": [_p, _i, _p, _p, _i, _p],
     "sdcsw_workspace": [_p, _i, ctypes.POINTER(_p), ctypes.POINTER(_ll)],
+    "sdcsw_plan_set_split": [_p, _i, _i, _p, _ll],
+    "sdcsw_split_info": [_p, _ip, _ip, _ip],
+    "sdcsw_split_f_expl_begin": [_p, _p, _i, _p],
+    "sdcsw_split_f_expl_end": [_p, _p, _i, _p],
     "sdcsw_last_error": [],
     "sdcsw_version": [],
 }

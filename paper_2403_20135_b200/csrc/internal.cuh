@@ -68,6 +68,19 @@ struct Plan {
   // table-streaming analysis (T >= 400); tma_ok = maps built
   alignas(64) unsigned long long tmap[2][16];
   bool tma_ok;
+  // spectral split: the wavenumbers are partitioned over S ranks of a
+  // spectral group (pairs (m, T-m) dealt round-robin); this rank owns part
+  // split_sp.  S = 1: unsplit (m_part = 0, m_k = m, Lp = L, lists null).
+  int split_S, split_sp, Lp;
+  int* m_part;      // [L] part owning m
+  int* m_k;         // [L] position of m in its part's list
+  int* own_m;       // [n_own_m] own wavenumbers, ascending (= k order)
+  int n_own_m;
+  int* own_work;    // analysis work items of own m
+  int n_own_work;
+  int* own_idx;     // own coefficient indices, ascending
+  int n_own_idx;
+  double2* fsyn_ext;  // part-major Fourier buffer [S][nb][J][Lp][4][2] (caller-owned)
 };
 constexpr int kCoefCap = 4096;
 
@@ -154,6 +167,10 @@ inline Work plan_work(const Plan& p, int batch_offset = 0) {
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_synth_prep(const Plan& p, const double2* u, int nb, double* xsyn,
                               cudaStream_t s, int chunk = 0);
+// split-mode synthesis into part split_sp of the external Fourier buffer
+cudaError_t launch_synthesis_split(const Plan& p, const double* xsyn, int nb, cudaStream_t s);
+// ring over all latitudes reading a part-major Fourier buffer (fsyn_ext)
+cudaError_t launch_ring_split(const Plan& p, const Work& w, int nb, cudaStream_t s);
 cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, int nb,
                              cudaStream_t s, int* step_counter);
 cudaError_t launch_ring(const Plan& p, const Work& w, int nb, cudaStream_t s);

@@ -58,10 +58,15 @@ constexpr int kWarps = 4;
 __global__ void __launch_bounds__(256) k_synth_prep(const double* __restrict__ u, int C2, int nb,
                                                     const double2* __restrict__ xscale,
                                                     const int* __restrict__ idx_row,
-                                                    double* __restrict__ xsyn, int rows, int chunk) {
+                                                    double* __restrict__ xsyn, int rows, int chunk,
+                                                    const int* __restrict__ idx_list, int n_list) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx_list != nullptr) {  // spectral split: own coefficients only
+    if (e >= 2 * n_list) return;
+    e = 2 * idx_list[e >> 1] + (e & 1);
+  }
   if (e >= C2) return;
   const int b = blockIdx.y;
   const double* s = u + (size_t)b * 3 * C2;
@@ -87,7 +92,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_synthesis(
     const double* __restrict__ xsyn, int nb, int T, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ,
-    int NBC) {
+    int NBC, const int* __restrict__ mlist, int Lp) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
   constexpr int NPAIR = (NB + 1) / 2;
@@ -95,13 +100,15 @@ __global__ void __launch_bounds__(32 * kWarps) k_synthesis(
   constexpr int NACC = NT * 2 * 4;  // doubles per lane: tiles x row tiles x (E,O) x (re,im)
   __shared__ double red[2 * 32 * NACC];  // two warps' partials (tree reduction)
 
-  const int m = blockIdx.y;
+  // unsplit: m = k = blockIdx.y, Lp = T + 1; spectral split: m = own list[k]
+  const int kpos = blockIdx.y;
+  const int m = mlist != nullptr ? mlist[kpos] : kpos;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int WK = (blockDim.x >> 5) / WJ;
   const int jt = warp % WJ, ks = warp / WJ;
   const int j0 = (blockIdx.x * WJ + jt) * kRowsPerWarp;
-  const int L = T + 1;
+  (void)T;
   if (step_counter != nullptr && (blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0)
     atomicAdd(step_counter, 1);
 
@@ -219,7 +226,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_synthesis(
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
           const int j = j0 + 8 * a + g;
-          double2* dst = fsyn + ((((size_t)(b0 + be) * J + j) * L + m) * 4 + f) * 2;
+          double2* dst = fsyn + ((((size_t)(b0 + be) * J + j) * Lp + kpos) * 4 + f) * 2;
           dst[0] = make_double2(aE[a][c][0] + aO[a][c][0], aE[a][c][1] + aO[a][c][1]);
           dst[1] = make_double2(aE[a][c][0] - aO[a][c][0], aE[a][c][1] - aO[a][c][1]);
         }
@@ -402,13 +409,28 @@ static int pick_nb(int nb) { return nb <= 6 ? nb : 4; }
 
 cudaError_t launch_synth_prep(const Plan& p, const double2* u, int nb, double* xsyn,
                               cudaStream_t s, int chunk) {
-  launch_k(k_synth_prep, dim3((2 * p.C + 255) / 256, nb), 256, 0, s, 
-      reinterpret_cast<const double*>(u), 2 * p.C, nb, p.xscale, p.idx_row, xsyn, p.rows, chunk);
+  const int n = p.own_idx ? p.n_own_idx : p.C;
+  launch_k(k_synth_prep, dim3((2 * n + 255) / 256, nb), 256, 0, s, 
+      reinterpret_cast<const double*>(u), 2 * p.C, nb, p.xscale, p.idx_row, xsyn, p.rows, chunk, p.own_idx,
+           p.n_own_idx);
   return cudaGetLastError();
 }
 
+static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist, int nm, int Lp,
+                                  const double* xsyn, int nb, cudaStream_t s, int* step_counter);
+
 cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, int nb,
                              cudaStream_t s, int* step_counter) {
+  return synthesis_impl(p, w.fsyn, nullptr, p.T + 1, p.T + 1, xsyn, nb, s, step_counter);
+}
+
+cudaError_t launch_synthesis_split(const Plan& p, const double* xsyn, int nb, cudaStream_t s) {
+  double2* part = p.fsyn_ext + (size_t)p.split_sp * nb * p.J * p.Lp * 8;
+  return synthesis_impl(p, part, p.own_m, p.n_own_m, p.Lp, xsyn, nb, s, nullptr);
+}
+
+static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist, int nm, int Lp,
+                                  const double* xsyn, int nb, cudaStream_t s, int* step_counter) {
   const int NB = pick_nb(nb);
   const int nblk = (nb + NB - 1) / NB;
   // latency regime (few batch blocks): 1 row tile x 4 K-splits (small T) or the
@@ -420,18 +442,18 @@ cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, i
     WK = 1;
     NBC = nblk >= 32 ? 8 : (nblk >= 8 ? 4 : 2);
   }
-  dim3 grid(p.J / (kRowsPerWarp * WJ), p.T + 1, (nblk + NBC - 1) / NBC);
+  dim3 grid(p.J / (kRowsPerWarp * WJ), nm, (nblk + NBC - 1) / NBC);
   const dim3 block(32 * WJ * WK);
 #define SDCSW_SYN(NBV)                                                                         \
   if (NB == NBV) {                                                                             \
     if (p.T < 200)                                                                             \
       launch_k(k_synthesis<NBV, 2>, grid, block, 0, s, xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
-                                                       p.rowoff, p.n_even, w.fsyn,             \
-                                                       step_counter, WJ, NBC);                 \
+                                                       p.rowoff, p.n_even, fsyn,               \
+                                                       step_counter, WJ, NBC, mlist, Lp);      \
     else                                                                                       \
       launch_k(k_synthesis<NBV, 1>, grid, block, 0, s, xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
-                                                       p.rowoff, p.n_even, w.fsyn,             \
-                                                       step_counter, WJ, NBC);                 \
+                                                       p.rowoff, p.n_even, fsyn,               \
+                                                       step_counter, WJ, NBC, mlist, Lp);      \
     return cudaGetLastError();                                                                 \
   }
   SDCSW_NB_LIST(SDCSW_SYN)
@@ -443,17 +465,19 @@ cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, c
   cudaError_t err;
   if (launch_analysis_tma(p, w, fe, nb, s, &err)) return err;  // table-streaming regime
   const int NB = pick_nb(nb);
-  dim3 grid(p.n_anal_work, (nb + NB - 1) / NB);
+  const int* work = p.own_work != nullptr ? p.own_work : p.anal_work;
+  const int nwork = p.own_work != nullptr ? p.n_own_work : p.n_anal_work;
+  dim3 grid(nwork, (nb + NB - 1) / NB);
 #define SDCSW_ANA(NBV)                                                                          \
   if (NB == NBV) {                                                                              \
     if (p.T < 200)                                                                              \
       launch_k(k_analysis<NBV, 2>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab, p.htab, \
                                                       p.rowoff, p.n_even, p.row_n, p.moff,      \
-                                                      p.lam, p.anal_work, fe, p.anal_wj);       \
+                                                      p.lam, work, fe, p.anal_wj);              \
     else                                                                                        \
       launch_k(k_analysis<NBV, 1>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab, p.htab, \
                                                       p.rowoff, p.n_even, p.row_n, p.moff,      \
-                                                      p.lam, p.anal_work, fe, p.anal_wj);       \
+                                                      p.lam, work, fe, p.anal_wj);              \
     return cudaGetLastError();                                                                  \
   }
   SDCSW_NB_LIST(SDCSW_ANA)

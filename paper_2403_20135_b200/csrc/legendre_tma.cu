@@ -278,13 +278,15 @@ bool launch_analysis_tma(const Plan& p, const Work& w, double2* fe, int nb, cuda
                          cudaError_t* err) {
   if (!p.tma_ok || p.anal_wj != 4) return false;
   const int NB = nb <= 6 ? nb : 4;
-  dim3 grid(p.n_anal_work, (nb + NB - 1) / NB);
+  const int* work = p.own_work != nullptr ? p.own_work : p.anal_work;
+  const int nwork = p.own_work != nullptr ? p.n_own_work : p.n_anal_work;
+  dim3 grid(nwork, (nb + NB - 1) / NB);
   const CUtensorMap& pm = *reinterpret_cast<const CUtensorMap*>(&p.tmap[0]);
   const CUtensorMap& hm = *reinterpret_cast<const CUtensorMap*>(&p.tmap[1]);
 #define SDCSW_TMA_LAUNCH(NBV)                                                                  \
   if (NB == NBV) {                                                                             \
     *err = launch_k(k_analysis_tma<NBV>, grid, dim3(128), kTmaSmem, s, pm, hm, w.gan, nb, p.T,  \
-                    p.J, p.C, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.anal_work, fe);    \
+                    p.J, p.C, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, work, fe);           \
     return true;                                                                               \
   }
   SDCSW_TMA_LAUNCH(1) SDCSW_TMA_LAUNCH(2) SDCSW_TMA_LAUNCH(3) SDCSW_TMA_LAUNCH(4)

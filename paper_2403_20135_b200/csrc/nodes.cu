@@ -98,10 +98,14 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
     long long fi_stride, int first, double phibar, const double* __restrict__ lamv,
     double* __restrict__ u_out, double* fi_out, const double2* __restrict__ xscale,
     const int* __restrict__ idx_row, double* __restrict__ xsyn, long long fe_mstride,
-    long long fi_mstride, int rows, int chunk) {
+    long long fi_mstride, int rows, int chunk, const int* __restrict__ idx_list, int n_list) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx_list != nullptr) {  // spectral split: own coefficients only
+    if (e >= 2 * n_list) return;
+    e = 2 * idx_list[e >> 1] + (e & 1);
+  }
   if (e >= C2) return;
   const int z = blockIdx.z;
   u0 += (size_t)z * 3 * C2;
@@ -140,10 +144,15 @@ __global__ void __launch_bounds__(256) k_final_node(
     long long fe_stride, const double* __restrict__ fi, long long fi_stride, int first,
     double phibar, const double* __restrict__ lamv, double* u_out, int* diverged,
     const int* step_counter, const double2* __restrict__ xscale, const int* __restrict__ idx_row,
-    double* __restrict__ xsyn, long long fe_mstride, long long fi_mstride, int rows, int chunk) {
+    double* __restrict__ xsyn, long long fe_mstride, long long fi_mstride, int rows, int chunk,
+    const int* __restrict__ idx_list, int n_list) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx_list != nullptr) {  // spectral split: own coefficients only
+    if (e >= 2 * n_list) return;
+    e = 2 * idx_list[e >> 1] + (e & 1);
+  }
   if (e >= C2) return;
   const int z = blockIdx.z;  // ensemble member
   u0 += (size_t)z * 3 * C2;
@@ -329,14 +338,14 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                double2* fi_out, double* xsyn_out, cudaStream_t s, int members,
                                long long fe_mstride, long long fi_mstride, int chunk) {
   const long long S2 = 6LL * p.C;  // doubles per state
-  dim3 grid = grid_for(p.C, count);
+  dim3 grid = grid_for(p.own_idx ? p.n_own_idx : p.C, count);
   grid.z = members;
   launch_k(k_sweep_nodes, grid, 256, 0, s, 2 * p.C, M, node_lo, pack(coef_host, M * (M + 4)),
                                                      D(u0), D(fe), fe_stride * S2, D(fi),
                                                      fi_stride * S2, first, p.phibar, p.lam,
                                                      W(u_out), W(fi_out), p.xscale, p.idx_row,
                                                      xsyn_out, fe_mstride * S2, fi_mstride * S2,
-                                                     p.rows, chunk);
+                                                     p.rows, chunk, p.own_idx, p.n_own_idx);
   return cudaGetLastError();
 }
 
@@ -346,13 +355,13 @@ cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, con
                               const int* step_counter, double* xsyn_out, cudaStream_t s,
                               int members, long long fe_mstride, long long fi_mstride) {
   const long long S2 = 6LL * p.C;
-  dim3 grid = grid_for(p.C);
+  dim3 grid = grid_for(p.own_idx ? p.n_own_idx : p.C);
   grid.z = members;
   launch_k(k_final_node, grid, 256, 0, s, 2 * p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
                                              fe_stride * S2, D(fi), fi_stride * S2, first, p.phibar,
                                              p.lam, W(u_out), diverged, step_counter, p.xscale,
                                              p.idx_row, xsyn_out, fe_mstride * S2, fi_mstride * S2,
-                                             p.rows, p.fe_chunk);
+                                             p.rows, p.fe_chunk, p.own_idx, p.n_own_idx);
   return cudaGetLastError();
 }
 

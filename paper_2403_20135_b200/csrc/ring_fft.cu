@@ -223,7 +223,9 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
                                                   const double* __restrict__ wsyn,
                                                   const double* __restrict__ wke,
                                                   const double2* __restrict__ twg,
-                                                  double two_omega) {
+                                                  double two_omega,
+                                                  const int* __restrict__ m_part,
+                                                  const int* __restrict__ m_k, int Lp, int nbg) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
   extern __shared__ double2 sm2[];
@@ -233,7 +235,12 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
   double2* tw = sm2 + 5 * NP;   // [N]
   const int L = T + 1;
   const int j = blockIdx.x, b = blockIdx.y;
-  const double2* F = fsyn + ((size_t)b * J + j) * L * 8;
+  // Fourier coefficients of (b, j, m): part-major [part][nbg][J][Lp][4][2]
+  // (unsplit: one part, k = m, Lp = L)
+  auto Fm = [&](int m) -> const double2* {
+    const int part = m_part != nullptr ? m_part[m] : 0, k = m_k != nullptr ? m_k[m] : m;
+    return fsyn + ((((size_t)part * nbg + b) * J + j) * Lp + k) * 8;
+  };
 #if SDCSW_EXP == 4
   const int cta = blockIdx.y * gridDim.x + blockIdx.x;
 #endif
@@ -254,12 +261,13 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
         const int k = i + r * NR;
         double2 z = make_double2(0.0, 0.0);
         if (k <= T) {
-          double2 xn = F[(k * 4 + f) * 2], xs = F[(k * 4 + f) * 2 + 1];
+          const double2* F = Fm(k);
+          double2 xn = F[f * 2], xs = F[f * 2 + 1];
           if (k == 0) xn.y = xs.y = 0.0;
           z = make_double2(xn.x - xs.y, xn.y + xs.x);
         } else if (k >= N - T) {
-          const int m = N - k;
-          const double2 xn = F[(m * 4 + f) * 2], xs = F[(m * 4 + f) * 2 + 1];
+          const double2* F = Fm(N - k);
+          const double2 xn = F[f * 2], xs = F[f * 2 + 1];
           z = make_double2(xn.x + xs.y, xs.x - xn.y);
         }
         v[r] = z;
@@ -412,17 +420,27 @@ extern "C" int sdcsw_debug_rtimes(unsigned long long* host, int n) {
 
 size_t ring_smem_bytes(int nlon) { return (size_t)(5 * (nlon + nlon / 8) + nlon) * sizeof(double2); }
 
-cudaError_t launch_ring(const Plan& p, const Work& w, int nb, cudaStream_t s) {
+static cudaError_t ring_impl(const Plan& p, const double2* fsyn, double2* gan, const int* m_part,
+                             const int* m_k, int Lp, int nb, cudaStream_t s) {
   dim3 grid(p.J, nb);
 #define SDCSW_RING_LAUNCH(NV, TV)                                                                  \
   if (p.nlon == NV) {                                                                              \
-    launch_k(k_ring<NV, TV>, grid, TV, p.ring_smem, s, w.fsyn, w.gan, p.J, p.T, p.mu, p.wsyn, p.wke,      \
-                                                 p.twiddle, 2.0 * p.omega);                        \
+    launch_k(k_ring<NV, TV>, grid, TV, p.ring_smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn, p.wke,   \
+             p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb);                                    \
     return cudaGetLastError();                                                                     \
   }
   SDCSW_RING_SIZES(SDCSW_RING_LAUNCH)
 #undef SDCSW_RING_LAUNCH
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_ring(const Plan& p, const Work& w, int nb, cudaStream_t s) {
+  // workspace Fourier buffers are unsplit ([nb][J][L][4][2]; part 0, k = m)
+  return ring_impl(p, w.fsyn, w.gan, nullptr, nullptr, p.T + 1, nb, s);
+}
+
+cudaError_t launch_ring_split(const Plan& p, const Work& w, int nb, cudaStream_t s) {
+  return ring_impl(p, p.fsyn_ext, w.gan, p.m_part, p.m_k, p.Lp, nb, s);
 }
 
 }  // namespace sdcsw

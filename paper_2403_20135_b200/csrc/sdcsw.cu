@@ -255,6 +255,9 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
     return st;
   }
   p.xsyn_nb = -1;
+  p.split_S = 1;
+  p.split_sp = 0;
+  p.Lp = p.L;
   {
     // Chunk big f_E batches so that one chunk's Fourier + analysis workspaces
     // (22 complex per (pair, m) and state) and the tables fit in ~half the L2;
@@ -283,6 +286,8 @@ int sdcsw_plan_destroy(sdcsw_plan* h) {
   cudaSetDevice(h->p.device);
   cudaDeviceSynchronize();
   Plan& p = h->p;
+  for (void* q : {(void*)p.m_part, (void*)p.m_k, (void*)p.own_m, (void*)p.own_work, (void*)p.own_idx})
+    if (q) cudaFree(q);
   void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
                   p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev,
                   p.xscale, p.idx_row, p.xsyn, p.anal_work4};
@@ -308,6 +313,10 @@ static int check_plan(sdcsw_plan* h, int nb, const char* where) {
 int sdcsw_f_expl(sdcsw_plan* h, const double* u, double* fe, int nb, void* stream) {
   int st = check_plan(h, nb, "sdcsw_f_expl");
   if (st) return st;
+  if (h->p.split_S > 1) {
+    set_error("sdcsw_f_expl: plan is spectrally split; use sdcsw_split_f_expl_begin/end");
+    return SDCSW_ERR_STATE;
+  }
   if (nb == 0) return SDCSW_OK;
   return cuda_status(f_expl(h->p, (const double2*)u, (double2*)fe, nb, (cudaStream_t)stream, nullptr),
                      "sdcsw_f_expl");
@@ -397,6 +406,113 @@ int sdcsw_workspace(sdcsw_plan* h, int which, void** ptr, long long* bytes) {
   *ptr = which == 0 ? (void*)p.fsyn : (void*)p.gan;
   *bytes = which == 0 ? per * 4 : per * kNumSlots;  // see sdcsw.h for the layouts
   return SDCSW_OK;
+}
+
+int sdcsw_plan_set_split(sdcsw_plan* h, int S, int sp, void* fourier, long long bytes) {
+  int st = check_plan(h, 1, "sdcsw_plan_set_split");
+  if (st) return st;
+  Plan& p = h->p;
+  if (S < 1 || sp < 0 || sp >= S || S > p.L) {
+    set_error("sdcsw_plan_set_split: need 1 <= S <= T+1 and 0 <= sp < S");
+    return SDCSW_ERR_PARAM;
+  }
+  cudaSetDevice(p.device);
+  cudaDeviceSynchronize();
+  for (int** q : {&p.m_part, &p.m_k, &p.own_m, &p.own_work, &p.own_idx}) {
+    if (*q) cudaFree(*q);
+    *q = nullptr;
+  }
+  p.split_S = S;
+  p.split_sp = sp;
+  p.Lp = p.L;
+  p.fsyn_ext = nullptr;
+  p.n_own_m = p.L;
+  p.n_own_work = p.n_own_idx = 0;
+  if (S == 1) return SDCSW_OK;
+  // pairs (m, T - m) dealt round-robin to the parts: equal coefficient counts
+  const int T = p.T, L = p.L;
+  std::vector<int> part(L), kpos(L), cnt(S, 0);
+  for (int i = 0, m = 0; m <= T - m; ++m, ++i) {
+    part[m] = i % S;
+    part[T - m] = i % S;
+  }
+  std::vector<int> own;
+  for (int m = 0; m < L; ++m) {
+    kpos[m] = cnt[part[m]]++;
+    if (part[m] == sp) own.push_back(m);
+  }
+  int Lp = 0;
+  for (int q = 0; q < S; ++q) Lp = cnt[q] > Lp ? cnt[q] : Lp;
+  const long long need = (long long)S * p.max_batch * p.J * Lp * 8 * sizeof(double2);
+  if (!fourier || bytes < need) {
+    set_error("sdcsw_plan_set_split: Fourier buffer smaller than S * max_batch * (nlat/2) * Lp * 128 B");
+    return SDCSW_ERR_PARAM;
+  }
+  // own analysis work items and coefficient indices
+  std::vector<int> work(p.n_anal_work), wown, idx;
+  cudaMemcpy(work.data(), p.anal_work, work.size() * sizeof(int), cudaMemcpyDeviceToHost);
+  for (int w : work)
+    if (part[w >> 16] == sp) wown.push_back(w);
+  for (int m : own) {
+    const int mo = m * (T + 1) - m * (m - 1) / 2;
+    for (int n = m; n <= T; ++n) idx.push_back(mo + n - m);
+  }
+  cudaError_t e;
+  if ((e = upload(&p.m_part, part.data(), part.size())) != cudaSuccess ||
+      (e = upload(&p.m_k, kpos.data(), kpos.size())) != cudaSuccess ||
+      (e = upload(&p.own_m, own.data(), own.size())) != cudaSuccess ||
+      (e = upload(&p.own_work, wown.data(), wown.size())) != cudaSuccess ||
+      (e = upload(&p.own_idx, idx.data(), idx.size())) != cudaSuccess)
+    return cuda_status(e, "sdcsw_plan_set_split");
+  p.Lp = Lp;
+  p.n_own_m = (int)own.size();
+  p.n_own_work = (int)wown.size();
+  p.n_own_idx = (int)idx.size();
+  p.fsyn_ext = (double2*)fourier;
+  p.xsyn_nb = -1;  // the operand buffer is rebuilt for the own rows
+  return SDCSW_OK;
+}
+
+int sdcsw_split_info(sdcsw_plan* h, int* Lp, int* n_own_m, int* n_own_idx) {
+  int st = check_plan(h, 1, "sdcsw_split_info");
+  if (st) return st;
+  if (Lp) *Lp = h->p.split_S > 1 ? h->p.Lp : 0;
+  if (n_own_m) *n_own_m = h->p.n_own_m;
+  if (n_own_idx) *n_own_idx = h->p.split_S > 1 ? h->p.n_own_idx : h->p.C;
+  return SDCSW_OK;
+}
+
+int sdcsw_split_f_expl_begin(sdcsw_plan* h, const double* u, int nb, void* stream) {
+  int st = check_plan(h, nb, "sdcsw_split_f_expl_begin");
+  if (st) return st;
+  Plan& p = h->p;
+  if (p.split_S < 2) {
+    set_error("sdcsw_split_f_expl_begin: plan is not split");
+    return SDCSW_ERR_STATE;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  if (p.xsyn_nb != nb) {
+    e = cudaMemsetAsync(p.xsyn, 0, (size_t)p.rows * nb * kXsyn * sizeof(double), s);
+    p.xsyn_nb = nb;
+  }
+  if (e == cudaSuccess) e = launch_synth_prep(p, (const double2*)u, nb, p.xsyn, s);
+  if (e == cudaSuccess) e = launch_synthesis_split(p, p.xsyn, nb, s);
+  return cuda_status(e, "sdcsw_split_f_expl_begin");
+}
+
+int sdcsw_split_f_expl_end(sdcsw_plan* h, double* fe, int nb, void* stream) {
+  int st = check_plan(h, nb, "sdcsw_split_f_expl_end");
+  if (st) return st;
+  const Plan& p = h->p;
+  if (p.split_S < 2) {
+    set_error("sdcsw_split_f_expl_end: plan is not split");
+    return SDCSW_ERR_STATE;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_ring_split(p, plan_work(p), nb, s);
+  if (e == cudaSuccess) e = launch_analysis(p, plan_work(p), (double2*)fe, nb, s);
+  return cuda_status(e, "sdcsw_split_f_expl_end");
 }
 
 int sdcsw_check_finite(const double* x, long long n, int* flag, void* stream) {
@@ -523,6 +639,10 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   if (n_coef < need) {
     set_error("sdcsw_stepper_create: coefficient array too short");
     return SDCSW_ERR_PARAM;
+  }
+  if (h->p.split_S > 1) {
+    set_error("sdcsw_stepper_create: plan is spectrally split (use the node/spectral orchestration)");
+    return SDCSW_ERR_STATE;
   }
   if (mode == 0 && M * E > h->p.max_batch) {
     set_error("sdcsw_stepper_create: plan max_batch < nodes x members");

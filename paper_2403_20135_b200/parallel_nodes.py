@@ -1,4 +1,4 @@
-"""Node-parallel diagonal SDC across GPUs (one process per GPU).
+"""Node- and spectrally-parallel diagonal SDC across GPUs (one process per GPU).
 
 The M node updates of a diagonal sweep are independent
 (``pkg/src/parsdc/integrators.py:254-267``, paper Alg. 2); the reference runs
@@ -21,6 +21,16 @@ Gathered layout: ``G[world * P][2][S]`` (node-major; fe then fi), so node j's
 fe is ``G + 2 j S`` and its fi ``G + (2 j + 1) S`` - the sweep kernels take
 these with element stride 2 states.  The compute backend is pluggable:
 :class:`CudaNodeBackend` calls ``libsdcsw.so``; tests supply a numpy backend.
+
+With more GPUs than nodes the G ranks form NG node groups of
+S spectral parts (G = NG S, rank r -> node group r // S, part r % S).  Part
+sp owns the wavenumbers of pairs (m, T-m) dealt round-robin
+(:func:`spectral_parts`); the state is m-partitioned, so node kernels,
+synthesis and analysis touch own-m coefficients only, and each f_E adds one
+all-gather of the synthesised Fourier coefficients inside the spectral group
+(the ring FFTs need every m of a latitude).  The (fe, fi) all-gather runs in
+the node-group communicator (same part, different node groups).  Every per-m
+and per-latitude operation is unchanged, so results stay bit-identical.
 """
 
 import math
@@ -29,6 +39,17 @@ import numpy as np
 
 from .errors import ParameterError
 from .integrators import diagonal_step_coefficients
+
+
+def spectral_parts(trunc, n_parts):
+    """part[m] for m = 0..T: pairs (m, T - m) dealt round-robin (as sdcsw_plan_set_split)."""
+    part = [0] * (trunc + 1)
+    i, m = 0, 0
+    while m <= trunc - m:
+        part[m] = part[trunc - m] = i % n_parts
+        i += 1
+        m += 1
+    return part
 
 
 def node_block(n_nodes, world, rank):
@@ -45,6 +66,45 @@ class CudaNodeBackend:
     def __init__(self, problem):
         self.problem = problem
         self.lib = problem._lib
+        self.fourier = None
+
+    def set_split(self, n_parts, part, max_batch):
+        """Partition the plan's wavenumbers; returns the part-major Fourier buffer."""
+        import ctypes
+
+        import torch
+
+        from . import _native
+
+        p = self.problem
+        if n_parts == 1:
+            _native.check(self.lib.sdcsw_plan_set_split(p.handle, 1, 0, None, 0))
+            self.fourier = None
+            return None
+        counts = [0] * n_parts
+        for q in spectral_parts(p.trunc, n_parts):
+            counts[q] += 1
+        lp = max(counts)
+        j = p.grid.nlat // 2
+        self.fourier = torch.zeros((n_parts, max_batch * j * lp * 8), dtype=torch.complex128,
+                                   device=p.device)
+        _native.check(self.lib.sdcsw_plan_set_split(p.handle, n_parts, part, self.fourier.data_ptr(),
+                                                    self.fourier.numel() * 16), "sdcsw_plan_set_split")
+        self._part_elems = max_batch * j * lp * 8
+        self._j, self._lp = j, lp
+        return self.fourier
+
+    def f_expl_split(self, u, out, nb, gather):
+        """Split f_E: own-m synthesis, all-gather of the Fourier parts, ring + own-m analysis."""
+        from . import _native
+
+        p = self.problem
+        _native.check(self.lib.sdcsw_split_f_expl_begin(p.handle, u.data_ptr(), nb, p.stream()))
+        per = nb * self._j * self._lp * 8  # the kernels index parts with the call's batch
+        flat = self.fourier.view(-1)
+        parts = [flat[q * per : (q + 1) * per] for q in range(self.fourier.shape[0])]
+        gather(parts)
+        _native.check(self.lib.sdcsw_split_f_expl_end(p.handle, out.data_ptr(), nb, p.stream()))
 
     def empty(self, n_states):
         return self.problem.empty_states(n_states)
@@ -79,16 +139,35 @@ class CudaNodeBackend:
 
 
 class NodeParallelDsdc:
-    """One dSDC step with nodes partitioned over the ranks of ``group``."""
+    """One dSDC step with nodes (and, with ``spectral_parts`` > 1, wavenumbers)
+    partitioned over the ranks of ``group``."""
 
-    def __init__(self, backend, cfg, dt, phibar, state_size, group=None):
+    def __init__(self, backend, cfg, dt, phibar, state_size, group=None, spectral_parts=1):
         import torch.distributed as dist
 
         self.dist = dist
-        self.group = group
         self.backend = backend
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        S = int(spectral_parts)
+        if S < 1 or world % S:
+            raise ParameterError(f"{world} ranks do not split into spectral groups of {S}")
+        self.nparts = S
+        self.part = rank % S
+        node_group_index = rank // S
+        n_groups = world // S
+        if S == 1:
+            self.group = group
+            self.spectral_group = None
+        else:
+            # every rank must create every group, in the same order
+            ranks = list(range(world)) if group is None else dist.get_process_group_ranks(group)
+            node_groups = [dist.new_group([ranks[g * S + q] for g in range(n_groups)]) for q in range(S)]
+            spec_groups = [dist.new_group([ranks[g * S + q] for q in range(S)]) for g in range(n_groups)]
+            self.group = node_groups[self.part]
+            self.spectral_group = spec_groups[node_group_index]
+        self.world = n_groups
+        self.rank = node_group_index
         self.m = cfg.table.n_nodes
         self.k = cfg.n_sweeps
         self.lo, self.count, self.per = node_block(self.m, self.world, self.rank)
@@ -108,6 +187,18 @@ class NodeParallelDsdc:
         self.chunks = list(self.gathered.view(self.world, 2 * p, -1).unbind(0))
         if self.m > 16:
             raise ParameterError("at most 16 nodes")
+        if self.nparts > 1:
+            backend.set_split(self.nparts, self.part, max(p, 1))
+
+    def _f_expl(self, u, out, nb):
+        if self.nparts == 1:
+            self.backend.f_expl(u, out, nb)
+            return
+
+        def gather(parts):  # the one Fourier exchange of a split f_E
+            self.dist.all_gather(parts, parts[self.part].clone(), group=self.spectral_group)
+
+        self.backend.f_expl_split(u, out, nb, gather)
 
     def counts_per_step(self):
         """Per-rank work: own nodes only (the redundant init/final are counted once per rank)."""
@@ -118,7 +209,7 @@ class NodeParallelDsdc:
         """Advance the replicated state tensor ``u`` (shape [1, S] or [S]) in place."""
         b = self.backend
         g = self.gathered
-        b.f_expl(u, self.fe0, 1)
+        self._f_expl(u, self.fe0, 1)
         fe_src, fe_stride = self.fe0, 0
         fi_src, fi_stride = self.fe0, 0
         first = True
@@ -128,7 +219,7 @@ class NodeParallelDsdc:
             if self.count:
                 b.sweep_nodes(self.m, self.lo, self.count, self.sweep_coef[k - 1], u, fe_src,
                               fe_stride, fi_src, fi_stride, first, self.ustage, self.fi_tmp)
-                b.f_expl(self.ustage, self.fe_tmp, self.count)
+                self._f_expl(self.ustage, self.fe_tmp, self.count)
                 loc = self.local.view(self.per, 2, -1)
                 loc[: self.count, 0].copy_(self.fe_tmp.view(-1, self.S)[: self.count])
                 loc[: self.count, 1].copy_(self.fi_tmp.view(-1, self.S)[: self.count])

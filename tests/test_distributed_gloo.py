@@ -13,11 +13,91 @@ import torch.multiprocessing as mp
 
 
 class NumpyNodeBackend:
-    """The node arithmetic of oracle/sdc.py behind the backend interface."""
+    """The node arithmetic of oracle/sdc.py behind the backend interface; in
+    split mode the oracle's f_E restated per owned wavenumber (same per-m
+    numpy operations, so the gathered result is bit-identical)."""
 
     def __init__(self, prob):
         self.p = prob
         self.S = prob.state_size
+        self.part_of = None
+
+    def set_split(self, n_parts, part, max_batch):
+        from paper_2403_20135_b200.parallel_nodes import spectral_parts
+
+        p = self.p
+        self.part_of = np.array(spectral_parts(p.trunc, n_parts))
+        self.part = part
+        self.own_m = np.nonzero(self.part_of == part)[0]
+        self.nf = p.nlon // 2 + 1
+        self.fourier = torch.zeros((n_parts, max_batch * p.nlat * self.nf * 4), dtype=torch.complex128)
+        return self.fourier
+
+    def _synth_own(self, coef, tab):
+        p = self.p
+        out = np.zeros((p.nlat, self.nf), dtype=complex)
+        for m in self.own_m:
+            sl = slice(p.bounds[m], p.bounds[m + 1])
+            out[:, m] = coef[sl] @ tab[sl]
+        return out
+
+    def _anal_own(self, fourier, tab, weight, out):
+        p = self.p
+        wf = (2.0 * np.pi * weight)[:, None] * fourier
+        for m in self.own_m:
+            sl = slice(p.bounds[m], p.bounds[m + 1])
+            out[sl] = tab[sl] @ wf[:, m]
+
+    def f_expl_split(self, u, out, nb, gather):
+        p = self.p
+        c = p.n_coef
+        per = p.nlat * self.nf * 4
+        flat = self.fourier.view(-1)
+        parts = [flat[q * nb * per : (q + 1) * nb * per] for q in range(self.fourier.shape[0])]
+        uu = u.reshape(-1, self.S)
+        mine = parts[self.part].view(nb, 4, p.nlat, self.nf)
+        for b in range(nb):
+            phi, zeta, delta = p.views(uu[b].numpy())
+            a = p.radius
+            psi, chi = -zeta * p.inv_lam, -delta * p.inv_lam
+            im = 1j * p.m_of
+            uf = (self._synth_own(im * chi, p.p) - self._synth_own(psi, p.h)) / a
+            vf = (self._synth_own(im * psi, p.p) + self._synth_own(chi, p.h)) / a
+            for f, arr in enumerate((uf, vf, self._synth_own(zeta, p.p), self._synth_own(phi, p.p))):
+                mine[b, f] = torch.from_numpy(arr)
+        gather(parts)
+        for b in range(nb):
+            full = np.zeros((4, p.nlat, self.nf), dtype=complex)
+            for m in range(p.trunc + 1):
+                q = self.part_of[m]
+                full[:, :, m] = parts[q].view(nb, 4, p.nlat, self.nf)[b, :, :, m].numpy()
+            uf, vf, zf, pf = full
+            ug, vg = p.to_grid(uf), p.to_grid(vf)
+            zg, pg = p.to_grid(zf), p.to_grid(pf)
+            eta = zg + (2.0 * p.omega * p.mu)[:, None]
+            fa, fb = p.to_fourier(eta * ug), p.to_fourier(eta * vg)
+            fc, fd = p.to_fourier(pg * ug), p.to_fourier(pg * vg)
+            fke = p.to_fourier((ug * ug + vg * vg) / (2.0 * p.coslat2)[:, None])
+            wt = p.w / p.coslat2
+            res = out.reshape(-1, self.S)[b].numpy()
+            t = {k: np.zeros(c, dtype=complex) for k in ("cp", "dh", "ap", "bh", "bp", "ah", "ke")}
+            self._anal_own(fc, p.p, wt, t["cp"])
+            self._anal_own(fd, p.h, wt, t["dh"])
+            self._anal_own(fa, p.p, wt, t["ap"])
+            self._anal_own(fb, p.h, wt, t["bh"])
+            self._anal_own(fb, p.p, wt, t["bp"])
+            self._anal_own(fa, p.h, wt, t["ah"])
+            self._anal_own(fke, p.p, p.w, t["ke"])
+            im = 1j * p.m_of
+            own = np.isin(p.m_of, self.own_m)
+            div_mass = (im * t["cp"] - t["dh"]) / p.radius
+            div_abs = (im * t["ap"] - t["bh"]) / p.radius
+            curl_abs = (im * t["bp"] + t["ah"]) / p.radius
+            vals = [-div_mass, -div_abs, curl_abs + p.lam * t["ke"]]
+            for k in range(3):
+                seg = vals[k]
+                seg[p.m_of == 0] = seg[p.m_of == 0].real
+                res[k * c : (k + 1) * c][own] = seg[own]
 
     def empty(self, n):
         return torch.zeros((n, self.S), dtype=torch.complex128)
@@ -64,7 +144,7 @@ class NumpyNodeBackend:
         u_out.reshape(-1)[:] = torch.from_numpy(u)
 
 
-def _worker(rank, world, port, m_count, k_count, out_path):
+def _worker(rank, world, port, m_count, k_count, out_path, nparts=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle.sphere_swe import SphericalShallowWaterOracle
@@ -76,7 +156,8 @@ def _worker(rank, world, port, m_count, k_count, out_path):
     prob = SphericalShallowWaterOracle(g.trunc, g.nlat, g.nlon)
     cfg = SdcConfig(table=CollocationTable.radau_right(m_count), n_sweeps=k_count,
                     mode=SweepMode.DIAGONAL_PARALLEL, time_threads=min(world, m_count))
-    stepper = NodeParallelDsdc(NumpyNodeBackend(prob), cfg, 900.0, prob.phibar, prob.state_size)
+    stepper = NodeParallelDsdc(NumpyNodeBackend(prob), cfg, 900.0, prob.phibar, prob.state_size,
+                               spectral_parts=nparts)
     u = torch.from_numpy(random_initial_state(g, 5)).reshape(1, -1).clone()
     for _ in range(2):
         stepper.step(u)
@@ -104,3 +185,36 @@ def test_node_partition_matches_single_process(tmp_path, world, m_count, k_count
     for r in range(world):
         got = np.load(out + f".{r}.npy")
         assert np.array_equal(got, ref), (r, np.abs(got - ref).max())
+
+
+def test_node_and_spectral_split_matches_single_process(tmp_path):
+    """4 ranks = 2 node groups x 2 spectral parts: every rank owns
+    half the wavenumbers; the assembled state equals the single-process oracle
+    bit for bit."""
+    from oracle import sdc as osdc
+    from oracle.sphere_swe import SphericalShallowWaterOracle
+    from paper_2403_20135_b200 import CollocationTable
+    from paper_2403_20135_b200.parallel_nodes import spectral_parts
+    from paper_2403_20135_b200.sphere import SphereGrid, random_initial_state
+
+    world, nparts, m_count, k_count = 4, 2, 3, 3
+    port = 29700 + (os.getpid() % 1000)
+    out = str(tmp_path / "u")
+    mp.spawn(_worker, args=(world, port, m_count, k_count, out, nparts), nprocs=world, join=True)
+    g = SphereGrid(trunc=10, nlat=16, nlon=32)
+    prob = SphericalShallowWaterOracle(g.trunc, g.nlat, g.nlon)
+    table = CollocationTable.radau_right(m_count)
+    ref = random_initial_state(g, 5)
+    for _ in range(2):
+        ref = osdc.dsdc(prob, ref, 900.0, table, k_count)
+    part_of = np.array(spectral_parts(g.trunc, nparts))
+    c = prob.n_coef
+    for ng in range(world // nparts):
+        got = np.zeros_like(ref)
+        for q in range(nparts):
+            st = np.load(out + f".{ng * nparts + q}.npy")
+            own = np.tile(part_of[prob.m_of] == q, 3)
+            got[own] = st[own]
+        assert np.array_equal(got, ref), np.abs(got - ref).max()
+    assert sorted(set(part_of.tolist())) == [0, 1]
+    assert abs((part_of[prob.m_of] == 0).sum() - c / 2) <= g.trunc + 1

@@ -258,3 +258,47 @@ def test_ensemble_members_match_single_runs():
     assert st.diverged() == 0
     st.close()
     single.close()
+
+
+@pytest.mark.parametrize("trunc,nparts", [(127, 2), (127, 4), (255, 2)])
+def test_spectral_split_f_expl_bitwise(trunc, nparts):
+    """Spectral split kernels on one device: the parts are run one
+    after another into a shared part-major Fourier buffer (no inter-rank
+    waiting), and the own-m tendencies they produce, combined, equal the
+    unsplit f_E bit for bit."""
+    import torch
+
+    from paper_2403_20135_b200 import _native
+    from paper_2403_20135_b200.parallel_nodes import CudaNodeBackend, spectral_parts
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    p = SphericalShallowWater(trunc, max_batch=2)
+    nb = 2
+    states = np.stack([random_initial_state(p.grid, 40 + b) for b in range(nb)])
+    states[:, : p.n_coef] = 2e-3 * states[:, p.n_coef : 2 * p.n_coef] * 1e6
+    u = torch.from_numpy(states).to(p.device).contiguous()
+    ref = p.empty_states(nb)
+    p.f_expl_device(u, ref, nb)
+    be = CudaNodeBackend(p)
+    be.set_split(nparts, 0, nb)
+    got = torch.zeros_like(ref)
+    outs = []
+    for q in range(nparts):  # all synthesis parts first (the all-gather's effect)
+        _native.check(p._lib.sdcsw_plan_set_split(p.handle, nparts, q, be.fourier.data_ptr(),
+                                                  be.fourier.numel() * 16))
+        _native.check(p._lib.sdcsw_split_f_expl_begin(p.handle, u.data_ptr(), nb, p.stream()))
+    for q in range(nparts):
+        # re-select part q without clearing the shared Fourier buffer
+        _native.check(p._lib.sdcsw_plan_set_split(p.handle, nparts, q, be.fourier.data_ptr(),
+                                                  be.fourier.numel() * 16))
+        o = torch.zeros_like(ref)
+        _native.check(p._lib.sdcsw_split_f_expl_end(p.handle, o.data_ptr(), nb, p.stream()))
+        outs.append(o)
+    part_of = np.array(spectral_parts(trunc, nparts))
+    for q in range(nparts):
+        own = torch.from_numpy(np.tile(part_of[p.m_of] == q, 3)).to(p.device)
+        got[:, own] = outs[q][:, own]
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    _native.check(p._lib.sdcsw_plan_set_split(p.handle, 1, 0, None, 0))
+    p.close()
