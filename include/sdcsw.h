@@ -159,6 +159,11 @@ int sdcsw_split_info(sdcsw_plan* plan, int* Lp, int* n_own_m, int* n_own_idx);
 int sdcsw_split_f_expl_begin(sdcsw_plan* plan, const double* u, int nb, void* stream);
 int sdcsw_split_f_expl_end(sdcsw_plan* plan, double* fe, int nb, void* stream);
 
+/* out = x + w * y over n doubles, rounded as numpy's `x + w * y` (product, then
+ * sum); out may alias x.  The vector update of the reference schemes
+ * imex_o2_step / ab2_si_step (integrators.py:387-420). */
+int sdcsw_axpy(long long n, const double* x, double w, const double* y, double* out, void* stream);
+
 /* Any non-finite entry among n doubles -> *flag = 1 (device int).
  * Replaces check_finite (core.py:42-50) without a host round trip. */
 int sdcsw_check_finite(const double* x, long long n, int* flag, void* stream);

@@ -185,3 +185,40 @@ class DahlquistOracle:
             return beta.copy()
         self.counters.tally_solve()
         return beta / (1.0 - alpha * self.lambda_impl)
+
+
+# -- reference schemes (integrators.py:387-420) -----------------------------------
+
+THETA = 3.0 / 5.0
+W_NOW = 1.5 + 0.1
+W_PREV = -(0.5 + 0.1)
+
+
+def _trap_half(problem, state, dt):
+    beta = state + (0.25 * dt) * problem.f_impl(state)
+    return problem.implicit_solve(0.25 * dt, beta, guess=beta)
+
+
+def imex_o2(problem, state, dt):
+    u = _trap_half(problem, state, dt)
+    rate = problem.f_expl(u)
+    pred = u + dt * rate
+    u = u + (0.5 * dt) * rate + (0.5 * dt) * problem.f_expl(pred)
+    return _trap_half(problem, u, dt)
+
+
+def theta_step(problem, state, dt, fe_now, fe_prev):
+    beta = state + (dt * (1.0 - THETA)) * problem.f_impl(state)
+    beta += (dt * W_NOW) * fe_now
+    beta += (dt * W_PREV) * fe_prev
+    return problem.implicit_solve(THETA * dt, beta, guess=beta)
+
+
+def ab2_run(problem, state, dt, n_steps):
+    """Ab2SiStepper semantics: IMEX-o2 bootstrap, then theta steps with cached history."""
+    prev = None
+    for _ in range(n_steps):
+        now = problem.f_expl(state)
+        state = imex_o2(problem, state, dt) if prev is None else theta_step(problem, state, dt, now, prev)
+        prev = now
+    return state

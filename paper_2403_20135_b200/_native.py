@@ -29,6 +29,7 @@ EXPORTS = (
     "sdcsw_stepper_reset",
     "sdcsw_stepper_launches_per_step",
     "sdcsw_check_finite",
+    "sdcsw_axpy",
     "sdcsw_transform_stage",
     "sdcsw_workspace",
     "sdcsw_plan_set_split",
@@ -76,6 +77,7 @@ _SIGS = {
     "sdcsw_stepper_reset": [_p, _p],
     "sdcsw_stepper_launches_per_step": [_p, _ip],
     "sdcsw_check_finite": [_p, _ll, _p, _p],
+    "sdcsw_axpy": [_ll, _p, ctypes.c_double, _p, _p, _p],
     "sdcsw_transform_stage": [_p, _i, _p, _p, _i, _p],
     "sdcsw_workspace": [_p, _i, ctypes.POINTER(_p), ctypes.POINTER(_ll)],
     "sdcsw_plan_set_split": [_p, _i, _i, _p, _ll],

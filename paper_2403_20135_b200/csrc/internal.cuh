@@ -202,6 +202,8 @@ cudaError_t launch_serial_update(const Plan& p, int m, double we, double wi, dou
                                  const double2* fi_new, const double2* fi_old, const double2* u0,
                                  int first, cudaStream_t s);
 cudaError_t launch_check_finite(const double* x, long long n, int* flag, cudaStream_t s);
+cudaError_t launch_axpy(long long n, const double* x, double w, const double* y, double* out,
+                        cudaStream_t s);
 
 cudaError_t make_table_maps(Plan& p);
 bool launch_analysis_tma(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s,

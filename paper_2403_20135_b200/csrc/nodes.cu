@@ -291,6 +291,16 @@ __global__ void __launch_bounds__(256) k_solve(int C2, NodeArgs cf, const double
   store_tri(u + (size_t)b * 3 * C2, C2, e, r);
 }
 
+// out = x + w * y element-wise, two roundings (numpy's `x + w * y`); n doubles
+__global__ void __launch_bounds__(256) k_axpy(long long n, const double* __restrict__ x, double w,
+                                              const double* __restrict__ y, double* out) {
+  SDCSW_PDL_ENTRY();
+  SDCSW_PDL_WAIT();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = __dadd_rn(x[i], __dmul_rn(w, y[i]));
+}
+
 __global__ void k_check_finite(const double* __restrict__ x, long long n, int* flag) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
@@ -396,6 +406,15 @@ cudaError_t launch_serial_update(const Plan& p, int m, double we, double wi, dou
   launch_k(k_serial_update, grid_for(p.C), 256, 0, s, 2 * p.C, we, wi, m > 0, W(corr), D(fe_new),
                                                 D(fe_old), D(fi_new), D(fi_old), D(u0), first,
                                                 p.phibar, p.lam);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpy(long long n, const double* x, double w, const double* y, double* out,
+                        cudaStream_t s) {
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  launch_k(k_axpy, dim3((unsigned)blocks), 256, 0, s, n, x, w, y, out);
   return cudaGetLastError();
 }
 

@@ -515,6 +515,12 @@ int sdcsw_split_f_expl_end(sdcsw_plan* h, double* fe, int nb, void* stream) {
   return cuda_status(e, "sdcsw_split_f_expl_end");
 }
 
+int sdcsw_axpy(long long n, const double* x, double w, const double* y, double* out, void* stream) {
+  if (n < 0 || !x || !y || !out) return SDCSW_ERR_PARAM;
+  if (n == 0) return SDCSW_OK;
+  return cuda_status(launch_axpy(n, x, w, y, out, (cudaStream_t)stream), "sdcsw_axpy");
+}
+
 int sdcsw_check_finite(const double* x, long long n, int* flag, void* stream) {
   if (n < 0 || !flag) return SDCSW_ERR_PARAM;
   if (n == 0) return SDCSW_OK;

@@ -1,0 +1,58 @@
+"""Spherical shallow-water snapshots.
+
+The spherical analogue of the reference's planar ``PSWSNAP1`` binary format
+(``pkg/src/parsdc/problems/swe.py:280-327``): an 8-byte magic ``SSWSNAP1``, a
+little-endian header ``<IIIdddddd`` = (T, nlat, nlon, radius, gravity, omega,
+mean depth, time, reserved) and the three complex128 spectra (Phi', zeta,
+delta) in the fixed triangular m-major layout of :mod:`.sphere`.  Used for
+checkpoints / resume and to exchange states between the CPU oracle and the
+GPU path.  Errors follow the reference: ``ValidationError`` for a wrong magic,
+a truncated header or a coefficient count that does not match the header.
+"""
+
+import struct
+
+import numpy as np
+
+from .errors import ValidationError
+from .sphere import SphereGrid
+
+SNAPSHOT_MAGIC = b"SSWSNAP1"
+_HEADER = struct.Struct("<IIIdddddd")
+
+
+def _grid_of(problem_or_grid):
+    return problem_or_grid.grid if hasattr(problem_or_grid, "grid") else problem_or_grid
+
+
+def write_snapshot(path, problem, state, time=0.0):
+    """Binary snapshot of one state (numpy array or CUDA tensor)."""
+    g = _grid_of(problem)
+    if hasattr(state, "detach"):
+        state = state.detach().reshape(-1).cpu().numpy()
+    state = np.ascontiguousarray(state, dtype=np.complex128).reshape(-1)
+    if state.size != g.state_size:
+        raise ValidationError(f"state has {state.size} coefficients, expected {g.state_size}")
+    with open(path, "wb") as handle:
+        handle.write(SNAPSHOT_MAGIC)
+        handle.write(_HEADER.pack(g.trunc, g.nlat, g.nlon, g.radius, g.gravity, g.omega,
+                                  g.mean_depth, float(time), 0.0))
+        handle.write(state.tobytes())
+
+
+def read_snapshot(path):
+    """Returns ``(meta, state)``; ``meta`` holds the grid (``SphereGrid``) and time."""
+    with open(path, "rb") as handle:
+        magic = handle.read(len(SNAPSHOT_MAGIC))
+        if magic != SNAPSHOT_MAGIC:
+            raise ValidationError(f"{path} is not a spherical shallow-water snapshot")
+        header = handle.read(_HEADER.size)
+        if len(header) != _HEADER.size:
+            raise ValidationError(f"{path} is truncated")
+        trunc, nlat, nlon, radius, gravity, omega, depth, time, _ = _HEADER.unpack(header)
+        grid = SphereGrid(trunc=int(trunc), nlat=int(nlat), nlon=int(nlon), radius=radius,
+                          gravity=gravity, omega=omega, mean_depth=depth)
+        data = np.frombuffer(handle.read(), dtype=np.complex128)
+        if data.size != grid.state_size:
+            raise ValidationError(f"{path} holds {data.size} coefficients, expected {grid.state_size}")
+    return {"grid": grid, "time": time}, data.copy()

@@ -26,7 +26,9 @@ sys.path.insert(0, "/root/reference/pkg/src")
 
 from parsdc import collocation as rc  # noqa: E402
 from parsdc.integrators import (  # noqa: E402
+    Ab2SiStepper,
     DiagonalSdcStepper,
+    ImexO2Stepper,
     SdcConfig,
     SerialSdcStepper,
     SweepMode,
@@ -92,6 +94,12 @@ def sphere_steps():
     cfg = SdcConfig(table=table, n_sweeps=3, mode=SweepMode.SERIAL)
     traj = integrate(prob, u0, 600.0, 3, SerialSdcStepper(cfg))
     out["integrate_serial_final"] = traj.states[-1]
+    traj = integrate(prob, u0, 300.0, 3, ImexO2Stepper())
+    out["imex_o2_final"] = traj.states[-1]
+    out["imex_o2_counts"] = np.array([[r.n_f_expl, r.n_f_impl, r.n_solve] for r in traj.reports])
+    traj = integrate(prob, u0, 300.0, 4, Ab2SiStepper())
+    out["ab2_si_final"] = traj.states[-1]
+    out["ab2_si_counts"] = np.array([[r.n_f_expl, r.n_f_impl, r.n_solve] for r in traj.reports])
     np.savez_compressed(os.path.join(HERE, "sphere_steps.npz"), **out)
 
 

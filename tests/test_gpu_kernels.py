@@ -302,3 +302,21 @@ def test_spectral_split_f_expl_bitwise(trunc, nparts):
     assert torch.equal(got, ref)
     _native.check(p._lib.sdcsw_plan_set_split(p.handle, 1, 0, None, 0))
     p.close()
+
+
+def test_reference_schemes_on_gpu():
+    """IMEX-o2 / AB2-SI on the device problem vs the oracle restatement (pinned to the reference)."""
+    from paper_2403_20135_b200.schemes import Ab2SiStepper, ImexO2Stepper
+
+    p = gpu(63)
+    o = oracle_for(p)
+    u0 = random_initial_state(p.grid, 6)
+    traj = integrate(p, u0, 120.0, 5, ImexO2Stepper())
+    ref = u0
+    for _ in range(5):
+        ref = osdc.imex_o2(o, ref, 120.0)
+    assert max(relative_l2(traj.states[-1], ref, o)) <= 1e-10
+    assert [(r.n_f_expl, r.n_f_impl, r.n_solve) for r in traj.reports] == [(2, 2, 2)] * 5
+    traj = integrate(p, u0, 120.0, 5, Ab2SiStepper())
+    assert max(relative_l2(traj.states[-1], osdc.ab2_run(o, u0, 120.0, 5), o)) <= 1e-10
+    assert [(r.n_f_expl, r.n_f_impl, r.n_solve) for r in traj.reports] == [(3, 2, 2)] + [(1, 1, 1)] * 4

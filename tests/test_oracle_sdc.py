@@ -95,3 +95,14 @@ def test_live_reference_dsdc(reference, sphere21):
     ref, _ = dsdc_step(sphere21, SPH["u0"], 300.0, cfg)
     mine = osdc.dsdc(sphere21, SPH["u0"], 300.0, CollocationTable.radau_right(4), 3)
     assert np.array_equal(ref, mine)
+
+
+def test_reference_schemes_bitwise(sphere21):
+    """IMEX-o2 and AB2-SI restatements vs the reference's own steppers (golden)."""
+    u = SPH["u0"]
+    for _ in range(3):
+        u = osdc.imex_o2(sphere21, u, 300.0)
+    assert np.array_equal(u, SPH["imex_o2_final"])
+    assert np.array_equal(osdc.ab2_run(sphere21, SPH["u0"], 300.0, 4), SPH["ab2_si_final"])
+    assert SPH["imex_o2_counts"].tolist() == [[2, 2, 2]] * 3
+    assert SPH["ab2_si_counts"].tolist() == [[3, 2, 2]] + [[1, 1, 1]] * 3
