@@ -126,6 +126,17 @@ int sdcsw_stepper_run(sdcsw_stepper* st, double* u, int n_steps, int use_graph, 
 int sdcsw_stepper_diverged(sdcsw_stepper* st, int* step_index);
 int sdcsw_stepper_reset(sdcsw_stepper* st, void* stream);
 
+/* option 0: concurrent node chains per sweep (1..M); option 1: sequential
+ * node updates (1 = the DIAGONAL_SEQUENTIAL analogue: one node at a time on
+ * one stream).  Rebuilds the step graph. */
+int sdcsw_stepper_set_option(sdcsw_stepper* st, int option, int value);
+
+/* One step launched stage by stage with CUDA events (no graph) for the cost
+ * model (perfmodel.fit_costs, pkg/src/parsdc/perfmodel.py:78-111): stage_ms =
+ * [init, sweep 1 .. sweep K-1, final node] for dSDC, [init, sweep 1 .. K] for
+ * serial SDC; n >= K + 1.  Synchronises. */
+int sdcsw_stepper_profile(sdcsw_stepper* st, double* u, double* stage_ms, int n, void* stream);
+
 /* Number of kernels one step launches (for the bench's gpu_launches). */
 int sdcsw_stepper_launches_per_step(sdcsw_stepper* st, int* n);
 

@@ -28,6 +28,8 @@ EXPORTS = (
     "sdcsw_stepper_diverged",
     "sdcsw_stepper_reset",
     "sdcsw_stepper_launches_per_step",
+    "sdcsw_stepper_set_option",
+    "sdcsw_stepper_profile",
     "sdcsw_check_finite",
     "sdcsw_axpy",
     "sdcsw_transform_stage",
@@ -76,6 +78,8 @@ _SIGS = {
     "sdcsw_stepper_diverged": [_p, _ip],
     "sdcsw_stepper_reset": [_p, _p],
     "sdcsw_stepper_launches_per_step": [_p, _ip],
+    "sdcsw_stepper_set_option": [_p, _i, _i],
+    "sdcsw_stepper_profile": [_p, _p, _dp, _i, _p],
     "sdcsw_check_finite": [_p, _ll, _p, _p],
     "sdcsw_axpy": [_ll, _p, ctypes.c_double, _p, _p, _p],
     "sdcsw_transform_stage": [_p, _i, _p, _p, _i, _p],

@@ -93,6 +93,10 @@ struct sdcsw_stepper {
   double *xsyn1, *xsynM;  // synthesis operands (nb = 1 / node groups); padding rows stay zero
   int chains;             // concurrent node chains per sweep (graph branches)
   int members;            // ensemble members advanced together (batched GEMM columns)
+  int sequential;         // 1: node updates one after another (DIAGONAL_SEQUENTIAL analogue)
+  int ncreated;           // side streams created
+  cudaEvent_t prof[40];   // stage events of a profiled step (created on demand)
+  bool prof_ready;
   cudaStream_t side[16];
   cudaEvent_t ev_fork, ev_join[16];
   int* flags;    // [0] first diverged step (INT_MAX = none), [1] step counter
@@ -530,7 +534,8 @@ int sdcsw_check_finite(const double* x, long long n, int* flag, void* stream) {
 // ---------------------------------------------------------------------------
 // stepper
 // ---------------------------------------------------------------------------
-static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
+static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
+                                cudaEvent_t* marks = nullptr) {
   const Plan& p = st->plan->p;
   const int M = st->M, K = st->K;
   const size_t S = st->S;
@@ -539,8 +544,10 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
   // f_E(u0) of every member from the operand the previous step's last kernel
   // (or the run's prep) wrote into xsyn1
   const int E = st->members;
+  if (marks) cudaEventRecord(marks[0], s);
   cudaError_t e = f_expl_prepped(p, plan_work(p), st->xsyn1, st->fe0, E, s, counter, p.fe_chunk);
   if (e != cudaSuccess) return e;
+  if (marks) cudaEventRecord(marks[1], s);
   if (st->mode == 0) {
     // fi alternates between two buffers: every node reads all fi_j while
     // writing its own fi_m, so the update cannot be in place.  The M node
@@ -550,21 +557,22 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
     // Tendency buffers are member-major [E][M]; an ensemble runs as one chain
     // whose GEMMs carry all E * M states as columns.
     const int cstride = M * (M + 4);
-    const int G = st->chains;
+    const int G = st->sequential ? M : st->chains;
+    const bool seq = st->sequential != 0;  // groups of one node, all on stream s
     const long long mS = M;  // member stride of the node buffers, in states
     double2* fi_cur = st->fi;
     for (int k = 1; k < K; ++k) {
       const bool first = k == 1;
       double2* fi_new = (k % 2) ? st->fi : st->fiB;
       const double* coef = st->coef.data() + (size_t)(k - 1) * cstride;
-      if (G > 1) {
+      if (G > 1 && !seq) {
         if ((e = cudaEventRecord(st->ev_fork, s)) != cudaSuccess) return e;
         for (int g = 0; g < G; ++g)
           if ((e = cudaStreamWaitEvent(st->side[g], st->ev_fork, 0)) != cudaSuccess) return e;
       }
       for (int g = 0; g < G; ++g) {
         const int lo = g * M / G, hi = (g + 1) * M / G, cnt = hi - lo;
-        cudaStream_t sg = G > 1 ? st->side[g] : s;
+        cudaStream_t sg = (G > 1 && !seq) ? st->side[g] : s;
         double* xs = st->xsynM + (size_t)lo * E * p.rows * kXsyn;
         e = launch_sweep_nodes(p, M, lo, cnt, coef, u, first ? st->fe0 : st->fe, first ? 0 : 1,
                                fi_cur, first ? 0 : 1, first, st->ustage + lo * S,
@@ -574,15 +582,23 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
                            p.fe_chunk);
         if (e != cudaSuccess) return e;
       }
-      if (G > 1) {
+      if (G > 1 && !seq) {
         for (int g = 0; g < G; ++g) {
           if ((e = cudaEventRecord(st->ev_join[g], st->side[g])) != cudaSuccess) return e;
           if ((e = cudaStreamWaitEvent(s, st->ev_join[g], 0)) != cudaSuccess) return e;
         }
       }
+      if (marks) cudaEventRecord(marks[1 + k], s);
       fi_cur = fi_new;
     }
     const bool first = K == 1;
+    if (marks) {
+      e = launch_final_node(p, M, st->coef.data() + (size_t)(K - 1) * cstride, u,
+                            first ? st->fe0 : st->fe, first ? 0 : 1, fi_cur, first ? 0 : 1,
+                            first, u, diverged, counter, st->xsyn1, s, E, first ? 1 : mS, mS);
+      cudaEventRecord(marks[K + 1], s);
+      return e;
+    }
     return launch_final_node(p, M, st->coef.data() + (size_t)(K - 1) * cstride, u,
                              first ? st->fe0 : st->fe, first ? 0 : 1, fi_cur, first ? 0 : 1,
                              first, u, diverged, counter, st->xsyn1, s, E, first ? 1 : mS, mS);
@@ -621,6 +637,7 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s) {
     old_fi = nfi;
     old_stride = 1;
     first = 0;
+    if (marks) cudaEventRecord(marks[1 + k], s);
   }
   return cudaSuccess;
 }
@@ -708,9 +725,10 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
     if (s->chains > M) s->chains = M;
     if (E > 1) s->chains = 1;
   }
-  if (s->chains > 1) {
+  s->ncreated = mode == 0 && E == 1 ? M : 0;  // side streams for up to M chains
+  if (s->ncreated > 1) {
     cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
-    for (int g = 0; g < s->chains; ++g) {
+    for (int g = 0; g < s->ncreated; ++g) {
       cudaStreamCreateWithFlags(&s->side[g], cudaStreamNonBlocking);
       cudaEventCreateWithFlags(&s->ev_join[g], cudaEventDisableTiming);
     }
@@ -726,13 +744,15 @@ int sdcsw_stepper_destroy(sdcsw_stepper* s) {
   cudaDeviceSynchronize();
   if (s->exec) cudaGraphExecDestroy(s->exec);
   if (s->graph) cudaGraphDestroy(s->graph);
-  if (s->chains > 1) {
+  if (s->ncreated > 1) {
     cudaEventDestroy(s->ev_fork);
-    for (int g = 0; g < s->chains; ++g) {
+    for (int g = 0; g < s->ncreated; ++g) {
       cudaStreamDestroy(s->side[g]);
       cudaEventDestroy(s->ev_join[g]);
     }
   }
+  if (s->prof_ready)
+    for (int i = 0; i < s->K + 2; ++i) cudaEventDestroy(s->prof[i]);
   cudaStreamDestroy(s->cap);
   cudaFree(s->buf);
   cudaFree(s->flags);
@@ -751,6 +771,8 @@ int sdcsw_stepper_reset(sdcsw_stepper* s, void* stream) {
 
 int sdcsw_stepper_launches_per_step(sdcsw_stepper* s, int* n) {
   if (!s || !n) return SDCSW_ERR_STATE;
+  const int G = s->sequential ? s->M : s->chains;
+  s->launches = s->mode == 0 ? 4 + 4 * G * (s->K - 1) : 3 + s->K * 5 * s->M;
   *n = s->launches;
   return SDCSW_OK;
 }
@@ -792,6 +814,46 @@ int sdcsw_stepper_run(sdcsw_stepper* s, double* u, int n_steps, int use_graph, v
   for (int i = 0; i < n_steps; ++i) {
     e = cudaGraphLaunch(s->exec, cs);
     if (e != cudaSuccess) return cuda_status(e, "cudaGraphLaunch");
+  }
+  return SDCSW_OK;
+}
+
+int sdcsw_stepper_set_option(sdcsw_stepper* s, int option, int value) {
+  if (!s) return SDCSW_ERR_STATE;
+  if (option == 0) {  // concurrent node chains
+    if (value < 1 || value > s->M || (value > 1 && s->ncreated < value)) return SDCSW_ERR_PARAM;
+    s->chains = value;
+  } else if (option == 1) {  // sequential node updates
+    if (s->mode != 0 || s->members != 1) return SDCSW_ERR_PARAM;
+    s->sequential = value ? 1 : 0;
+  } else {
+    return SDCSW_ERR_PARAM;
+  }
+  if (s->exec) { cudaGraphExecDestroy(s->exec); s->exec = nullptr; }
+  if (s->graph) { cudaGraphDestroy(s->graph); s->graph = nullptr; }
+  return SDCSW_OK;
+}
+
+int sdcsw_stepper_profile(sdcsw_stepper* s, double* u, double* stage_ms, int n, void* stream) {
+  if (!s || !u || !stage_ms || n < s->K + 1) return SDCSW_ERR_PARAM;
+  cudaStream_t cs = (cudaStream_t)stream;
+  cudaError_t e = cudaSetDevice(s->plan->p.device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+  if (!s->prof_ready) {
+    for (int i = 0; i < s->K + 2; ++i) cudaEventCreate(&s->prof[i]);
+    s->prof_ready = true;
+  }
+  e = launch_synth_prep(s->plan->p, (const double2*)u, s->members, s->xsyn1, cs, s->plan->p.fe_chunk);
+  if (e == cudaSuccess) e = enqueue_step(s, (double2*)u, cs, s->prof);
+  if (e != cudaSuccess) return cuda_status(e, "sdcsw_stepper_profile");
+  e = cudaEventSynchronize(s->prof[s->mode == 0 ? s->K + 1 : s->K]);
+  if (e != cudaSuccess) return cuda_status(e, "sdcsw_stepper_profile");
+  // stage_ms = [init, sweep_1 .. sweep_{K-1 or K}, final (dSDC)]
+  const int nstages = s->mode == 0 ? s->K + 1 : s->K + 1;
+  for (int i = 0; i < nstages; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s->prof[i], s->prof[i + 1]);
+    stage_ms[i] = ms;
   }
   return SDCSW_OK;
 }

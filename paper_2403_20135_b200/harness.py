@@ -1,0 +1,296 @@
+"""Benchmark harness for the GPU path: ``sphere-swe`` TOML configurations.
+
+Mirrors the reference harness (``pkg/src/parsdc/bench/config.py``,
+``harness.py``, ``cli.py``) for the spherical problem on
+the device:
+
+``[problem]``  ``kind = "sphere-swe"``, ``trunc``, optional ``nlat``/``nlon``
+               and physical constants, ``seed`` (seeded BASELINE spectrum,
+               SURVEY 8d) or ``initial = "<snapshot path>"``.
+``[stepper]``  ``scheme`` in {dsdc, sdc-serial, imex-o2, ab2-si}, ``n_nodes``,
+               ``n_sweeps``, ``preconditioner`` (min-sr-flex | implicit-euler),
+               ``dt``.
+``[run]``      ``t_end``, optional ``checkpoint_interval`` (steps), ``reps``.
+``[[speedup.candidate]]``  ``scheme`` and ``dt``.
+
+Reports: ``run_report.json`` + ``final_state.snap`` (:mod:`.snapshot`),
+``speedup.json`` / ``speedup.csv``, ``perf_model.json`` (cost model fitted from
+CUDA-event stage timings, S_theory vs the measured sequential/parallel ratio).
+"""
+
+import csv
+import json
+import math
+import os
+import platform
+import time
+
+try:
+    import tomllib
+except ModuleNotFoundError:  # pragma: no cover
+    import tomli as tomllib
+
+import numpy as np
+
+from .collocation import MAX_NODES, CollocationTable, DiagonalPreconditioner
+from .core import evaluation_counters, state_norm
+from .errors import ConfigError
+from .integrators import (
+    DeviceStepper,
+    DiagonalSdcStepper,
+    SdcConfig,
+    SerialSdcStepper,
+    SweepMode,
+    integrate,
+)
+from .perfmodel import fit_costs, perf_report
+
+SCHEMES = ("dsdc", "sdc-serial", "imex-o2", "ab2-si")
+_PRECOND = {"min-sr-flex": DiagonalPreconditioner.MIN_SR_FLEX,
+            "implicit-euler": DiagonalPreconditioner.IMPLICIT_EULER_DTAU}
+
+
+class ExperimentConfig:
+    """Validated contents of one TOML file (ConfigError on any violation)."""
+
+    def __init__(self, data):
+        def get(section, key, default=None, required=False):
+            sec = data.get(section, {})
+            if key not in sec:
+                if required:
+                    raise ConfigError(f"[{section}] {key} is required")
+                return default
+            return sec[key]
+
+        self.title = data.get("title", "")
+        kind = get("problem", "kind", required=True)
+        if kind != "sphere-swe":
+            raise ConfigError(f"problem kind must be 'sphere-swe', got {kind!r}")
+        self.problem_kind = kind
+        self.trunc = int(get("problem", "trunc", required=True))
+        if self.trunc < 1:
+            raise ConfigError("trunc must be positive")
+        self.problem_params = {k: get("problem", k) for k in
+                               ("nlat", "nlon", "radius", "gravity", "omega", "mean_depth")
+                               if get("problem", k) is not None}
+        self.seed = int(get("problem", "seed", 0))
+        self.initial = get("problem", "initial")
+        self.scheme = get("stepper", "scheme", required=True)
+        if self.scheme not in SCHEMES:
+            raise ConfigError(f"scheme must be one of {SCHEMES}, got {self.scheme!r}")
+        self.n_nodes = int(get("stepper", "n_nodes", 3))
+        if not 1 <= self.n_nodes <= MAX_NODES:
+            raise ConfigError(f"n_nodes must be in [1, {MAX_NODES}]")
+        self.n_sweeps = int(get("stepper", "n_sweeps", self.n_nodes))
+        if self.n_sweeps < 1:
+            raise ConfigError("n_sweeps must be positive")
+        pc = get("stepper", "preconditioner", "min-sr-flex")
+        if pc not in _PRECOND:
+            raise ConfigError(f"unknown preconditioner {pc!r}")
+        self.preconditioner = _PRECOND[pc]
+        self.dt = float(get("stepper", "dt", required=True))
+        self.t_end = float(get("run", "t_end", required=True))
+        if self.dt <= 0 or self.t_end <= 0:
+            raise ConfigError("dt and t_end must be positive")
+        self.checkpoint_interval = get("run", "checkpoint_interval")
+        self.reps = int(get("run", "reps", 1))
+        self.candidates = [dict(c) for c in data.get("speedup", {}).get("candidate", [])]
+        for c in self.candidates:
+            if c.get("scheme") not in SCHEMES or float(c.get("dt", 0)) <= 0:
+                raise ConfigError(f"bad speedup candidate {c}")
+        self.n_steps(self.dt)
+        for c in self.candidates:
+            self.n_steps(float(c["dt"]))
+
+    def n_steps(self, dt=None):
+        dt = self.dt if dt is None else dt
+        n = self.t_end / dt
+        if abs(n - round(n)) > 1e-9 * max(1.0, n):
+            raise ConfigError(f"dt = {dt} does not divide t_end = {self.t_end}")
+        return int(round(n))
+
+
+def load_config(path):
+    try:
+        with open(path, "rb") as f:
+            data = tomllib.load(f)
+    except (OSError, tomllib.TOMLDecodeError) as exc:
+        raise ConfigError(f"cannot read {path}: {exc}") from exc
+    return ExperimentConfig(data)
+
+
+def build_problem(config):
+    from .problem import SphericalShallowWater
+
+    return SphericalShallowWater(config.trunc, max_batch=max(8, config.n_nodes),
+                                 **config.problem_params)
+
+
+def build_initial_state(config, problem):
+    if config.initial:
+        from .snapshot import read_snapshot
+
+        meta, state = read_snapshot(config.initial)
+        if meta["grid"].trunc != config.trunc:
+            raise ConfigError("snapshot truncation does not match the problem")
+        return state
+    from .sphere import random_initial_state
+
+    return random_initial_state(problem.grid, config.seed)
+
+
+def build_stepper(config, scheme=None):
+    scheme = config.scheme if scheme is None else scheme
+    if scheme == "imex-o2":
+        from .schemes import ImexO2Stepper
+
+        return ImexO2Stepper()
+    if scheme == "ab2-si":
+        from .schemes import Ab2SiStepper
+
+        return Ab2SiStepper()
+    table = CollocationTable.radau_right(config.n_nodes)
+    if scheme == "sdc-serial":
+        return SerialSdcStepper(SdcConfig(table=table, n_sweeps=config.n_sweeps, mode=SweepMode.SERIAL))
+    return DiagonalSdcStepper(SdcConfig(table=table, n_sweeps=config.n_sweeps,
+                                        preconditioner=config.preconditioner,
+                                        mode=SweepMode.DIAGONAL_PARALLEL,
+                                        time_threads=config.n_nodes))
+
+
+def environment_info():
+    import torch
+
+    from . import __version__
+
+    return {
+        "platform": platform.platform(),
+        "python": platform.python_version(),
+        "torch": torch.__version__,
+        "gpu": torch.cuda.get_device_name(0) if torch.cuda.is_available() else None,
+        "package": __version__,
+    }
+
+
+def _timed(problem, state, dt, n, stepper, interval=None):
+    import torch
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    traj = integrate(problem, state, dt, n, stepper, checkpoint_interval=interval)
+    torch.cuda.synchronize()
+    return traj, time.perf_counter() - t0
+
+
+def run_single(config, out_dir):
+    """One integration; writes run_report.json and final_state.snap."""
+    from .snapshot import write_snapshot
+
+    os.makedirs(out_dir, exist_ok=True)
+    problem = build_problem(config)
+    state = build_initial_state(config, problem)
+    stepper = build_stepper(config)
+    n = config.n_steps()
+    try:
+        traj, wall = _timed(problem, state, config.dt, n, stepper, config.checkpoint_interval)
+    finally:
+        if getattr(stepper, "cfg", None) is not None:
+            stepper.cfg.close()
+    final = traj.states[-1]
+    c = problem.n_coef
+    walls = [r.wall_s for r in traj.reports]
+    report = {
+        "title": config.title, "problem": config.problem_kind, "scheme": traj.scheme,
+        "trunc": config.trunc, "grid": [problem.grid.nlon, problem.grid.nlat], "dt": config.dt,
+        "n_steps": n, "t_end": config.t_end, "wall_s": wall,
+        "steps_per_s": n / wall,
+        "step_wall_s": {"min": min(walls), "median": float(np.median(walls)), "max": max(walls)},
+        "counters": dict(zip(("n_f_expl", "n_f_impl", "n_solve"), evaluation_counters(problem))),
+        "checkpoint_times": traj.times,
+        "final": {"state_norm": state_norm(final),
+                  "mean_geopotential_anomaly": float(final[0].real),
+                  "vorticity_norm": float(np.linalg.norm(final[c : 2 * c]))},
+        "environment": environment_info(),
+    }
+    write_snapshot(os.path.join(out_dir, "final_state.snap"), problem, final, config.t_end)
+    with open(os.path.join(out_dir, "run_report.json"), "w") as f:
+        json.dump(report, f, indent=2, sort_keys=True)
+    problem.close()
+    return report
+
+
+def speedup_report(config, out_dir):
+    """Wall-time ratios of each candidate against the configured scheme."""
+    os.makedirs(out_dir, exist_ok=True)
+    problem = build_problem(config)
+    state = build_initial_state(config, problem)
+    rows = []
+    runs = [(config.scheme, config.dt)] + [(c["scheme"], float(c["dt"])) for c in config.candidates]
+    base = None
+    for scheme, dt in runs:
+        n = config.n_steps(dt)
+        best = math.inf
+        for _ in range(max(1, config.reps)):
+            stepper = build_stepper(config, scheme)
+            _, wall = _timed(problem, state, dt, n, stepper)
+            if getattr(stepper, "cfg", None) is not None:
+                stepper.cfg.close()
+            best = min(best, wall)
+        base = best if base is None else base
+        rows.append({"scheme": scheme, "dt": dt, "n_steps": n, "wall_s": best,
+                     "speedup_vs_base": base / best})
+    with open(os.path.join(out_dir, "speedup.json"), "w") as f:
+        json.dump({"base": config.scheme, "rows": rows}, f, indent=2)
+    with open(os.path.join(out_dir, "speedup.csv"), "w", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=list(rows[0]))
+        w.writeheader()
+        w.writerows(rows)
+    problem.close()
+    return rows
+
+
+def perf_model_report(config, out_dir, n_profile=6):
+    """Fit (c_E, c_S) from per-stage CUDA-event timings of sequential-node dSDC
+    steps (perfmodel.fit_costs) and compare S_theory with the measured ratio of
+    sequential-node to concurrent-node step times on this GPU."""
+    import torch
+
+    os.makedirs(out_dir, exist_ok=True)
+    problem = build_problem(config)
+    state = build_initial_state(config, problem)
+    cfg = SdcConfig(table=CollocationTable.radau_right(config.n_nodes), n_sweeps=config.n_sweeps,
+                    preconditioner=config.preconditioner, mode=SweepMode.DIAGONAL_PARALLEL,
+                    time_threads=config.n_nodes)
+    st = DeviceStepper(problem, cfg, config.dt, serial=False)
+    u = problem._to_device(state).reshape(-1).contiguous()
+    st.set_sequential(True)
+    st.profile_step(u)  # warm-up
+    reports = [st.profile_step(u) for _ in range(n_profile)]
+    model = fit_costs(reports, config.n_nodes)
+
+    def per_step(n=20):
+        st.run(u, 2)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st.run(u, n)
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) * 1e-3 / n
+
+    t_seq = per_step()
+    st.set_sequential(False)
+    st.set_chains(config.n_nodes)
+    t_par_chains = per_step()
+    st.set_chains(1)
+    t_par_batched = per_step()
+    t_par = min(t_par_chains, t_par_batched)
+    rep = perf_report(model, s_measured=t_seq / t_par)
+    rep.update({"t_step_sequential_s": t_seq, "t_step_parallel_chains_s": t_par_chains,
+                "t_step_parallel_batched_s": t_par_batched,
+                "stage_reports": [r.__dict__ for r in reports], "environment": environment_info()})
+    with open(os.path.join(out_dir, "perf_model.json"), "w") as f:
+        json.dump(rep, f, indent=2, default=list)
+    st.close()
+    problem.close()
+    return rep

@@ -219,6 +219,30 @@ class DeviceStepper:
         _native.check(self.lib.sdcsw_stepper_launches_per_step(handle, ctypes.byref(n)))
         self.launches_per_step = n.value
 
+    def set_chains(self, n):
+        """Concurrent node chains per sweep (1 = batched on one stream)."""
+        _native.check(self.lib.sdcsw_stepper_set_option(self.handle, 0, int(n)), "set_option")
+
+    def set_sequential(self, on=True):
+        """One node update at a time (the DIAGONAL_SEQUENTIAL analogue)."""
+        _native.check(self.lib.sdcsw_stepper_set_option(self.handle, 1, int(bool(on))), "set_option")
+
+    def profile_step(self, u):
+        """Advance ``u`` one step stage by stage; returns a StepReport with CUDA-event stage times."""
+        n = self.n_sweeps + 2
+        ms = np.zeros(n)
+        _native.check(self.lib.sdcsw_stepper_profile(self.handle, u.data_ptr(), _native.dptr(ms), n,
+                                                     self.problem.stream()), "sdcsw_stepper_profile")
+        self.problem.add_counts(*(c * self.members for c in self.counts_per_step()))
+        s = ms * 1e-3
+        if self.serial:
+            sweeps = tuple(s[1 : 1 + self.n_sweeps])
+            return StepReport(float(s[: 1 + self.n_sweeps].sum()), float(s[0]), sweeps, 0.0,
+                              *self.counts_per_step())
+        sweeps = tuple(s[1 : self.n_sweeps])
+        return StepReport(float(s[: self.n_sweeps + 1].sum()), float(s[0]), sweeps,
+                          float(s[self.n_sweeps]), *self.counts_per_step())
+
     def counts_per_step(self):
         m, k = self.n_nodes, self.n_sweeps
         if self.serial:

@@ -1,0 +1,91 @@
+"""Harness configuration (CPU) and the GPU CLI path (mirrors
+pkg/tests/test_bench_config.py and test_bench_harness.py)."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from paper_2403_20135_b200.errors import ConfigError
+from paper_2403_20135_b200.harness import load_config
+from paper_2403_20135_b200.perfmodel import PerfModel, fit_costs, perf_report, theoretical_speedup
+from paper_2403_20135_b200.integrators import StepReport
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SMALL = """
+[problem]
+kind = "sphere-swe"
+trunc = 63
+seed = 2
+[stepper]
+scheme = "{scheme}"
+n_nodes = 3
+n_sweeps = 3
+dt = 120.0
+[run]
+t_end = {t_end}
+"""
+
+
+def write(tmp_path, text, name="c.toml"):
+    p = tmp_path / name
+    p.write_text(text)
+    return str(p)
+
+
+def test_load_example():
+    cfg = load_config(os.path.join(ROOT, "examples", "t127_dsdc.toml"))
+    assert cfg.n_steps() == 200 and cfg.trunc == 127 and len(cfg.candidates) == 2
+
+
+@pytest.mark.parametrize("bad", [
+    SMALL.format(scheme="rk4", t_end=1200.0),
+    SMALL.format(scheme="dsdc", t_end=1000.0),  # dt does not divide t_end
+    SMALL.replace("sphere-swe", "planar-swe").format(scheme="dsdc", t_end=1200.0),
+    "[problem]\nkind='sphere-swe'\n",
+])
+def test_config_errors(tmp_path, bad):
+    with pytest.raises(ConfigError):
+        load_config(write(tmp_path, bad))
+
+
+def test_cli_exit_code_on_bad_config(tmp_path):
+    path = write(tmp_path, SMALL.format(scheme="rk4", t_end=1200.0))
+    r = subprocess.run([sys.executable, "-m", "paper_2403_20135_b200.cli", "run", "--config", path,
+                        "--out", str(tmp_path / "o")], cwd=ROOT, capture_output=True, text=True)
+    assert r.returncode == 2
+
+
+def test_perfmodel_matches_reference_formulas(reference):
+    from parsdc import perfmodel as rp
+
+    for m in (2, 3, 4, 5):
+        for r in (0.0, 0.3):
+            assert theoretical_speedup(m, r) == rp.theoretical_speedup(m, r)
+    reps = [StepReport(1.0, 0.01 + 1e-4 * i, (0.05, 0.05, 0.05), 0.02, 0, 0, 0) for i in range(4)]
+    ref_reps = [rp.__dict__ and __import__("parsdc").integrators.StepReport(**r.__dict__) for r in reps]
+    a, b = fit_costs(reps, 4), rp.fit_costs(ref_reps, 4)
+    assert (a.c_e, a.c_s, a.n_sweeps) == (b.c_e, b.c_s, b.n_sweeps)
+    assert perf_report(a, 2.0) == rp.perf_report(b, 2.0)
+    assert PerfModel(4, 4, 1.0, 1.0).c_tilde_e == 0.0
+
+
+@pytest.mark.gpu
+def test_cli_run_speedup_perf_model(tmp_path):
+    path = write(tmp_path, SMALL.format(scheme="dsdc", t_end=1200.0) +
+                 '\n[[speedup.candidate]]\nscheme = "sdc-serial"\ndt = 120.0\n')
+    out = tmp_path / "o"
+    for cmd in ("run", "speedup", "perf-model"):
+        r = subprocess.run([sys.executable, "-m", "paper_2403_20135_b200.cli", cmd, "--config", path,
+                            "--out", str(out)], cwd=ROOT, capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+    rep = json.load(open(out / "run_report.json"))
+    assert rep["n_steps"] == 10 and rep["counters"]["n_solve"] == 70
+    assert rep["final"]["mean_geopotential_anomaly"] == 0.0
+    assert (out / "final_state.snap").exists()
+    sp = json.load(open(out / "speedup.json"))
+    assert sp["rows"][1]["scheme"] == "sdc-serial"
+    pm = json.load(open(out / "perf_model.json"))
+    assert pm["M"] == 3 and pm["S_theory"] > 1 and pm["c_E"] > 0 and pm["S_measured"] > 0
