@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) k_synth_prep(const double* __restrict__ u
 // re-read from L1 instead of being re-fetched by a separate CTA per block.
 // ---------------------------------------------------------------------------
 template <int NB, int PF>
-__global__ void __launch_bounds__(32 * kWarps) k_synthesis(
+__global__ void __launch_bounds__(32 * kWarps, 3) k_synthesis(
     const double* __restrict__ xsyn, int nb, int T, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ,

@@ -216,7 +216,7 @@ constexpr int inv_prefix() {  // product of the first S inverse radices
   return p;
 }
 
-template <int N, int THREADS>
+template <int N, int THREADS, bool SPLIT>
 __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const double2* __restrict__ fsyn,
                                                   double2* __restrict__ gan, int J, int T,
                                                   const double* __restrict__ mu,
@@ -237,9 +237,14 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
   const int j = blockIdx.x, b = blockIdx.y;
   // Fourier coefficients of (b, j, m): part-major [part][nbg][J][Lp][4][2]
   // (unsplit: one part, k = m, Lp = L)
+  const double2* F0 = fsyn + ((size_t)b * J + j) * Lp * 8;  // unsplit: part 0, k = m
   auto Fm = [&](int m) -> const double2* {
-    const int part = m_part != nullptr ? m_part[m] : 0, k = m_k != nullptr ? m_k[m] : m;
-    return fsyn + ((((size_t)part * nbg + b) * J + j) * Lp + k) * 8;
+    if constexpr (!SPLIT) {
+      return F0 + (size_t)m * 8;
+    } else {
+      const int part = m_part[m], k = m_k[m];
+      return fsyn + ((((size_t)part * nbg + b) * J + j) * Lp + k) * 8;
+    }
   };
 #if SDCSW_EXP == 4
   const int cta = blockIdx.y * gridDim.x + blockIdx.x;
@@ -406,7 +411,11 @@ cudaError_t configure_ring(size_t smem) {
   cudaError_t e = cudaSuccess;
 #define SDCSW_RING_CFG(NV, TV)                                                                     \
   if (e == cudaSuccess)                                                                            \
-    e = cudaFuncSetAttribute(k_ring<NV, TV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(k_ring<NV, TV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                             (int)smem);                                                           \
+  if (e == cudaSuccess)                                                                            \
+    e = cudaFuncSetAttribute(k_ring<NV, TV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                             (int)smem);
   SDCSW_RING_SIZES(SDCSW_RING_CFG)
 #undef SDCSW_RING_CFG
   return e;
@@ -425,8 +434,12 @@ static cudaError_t ring_impl(const Plan& p, const double2* fsyn, double2* gan, c
   dim3 grid(p.J, nb);
 #define SDCSW_RING_LAUNCH(NV, TV)                                                                  \
   if (p.nlon == NV) {                                                                              \
-    launch_k(k_ring<NV, TV>, grid, TV, p.ring_smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn, p.wke,   \
-             p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb);                                    \
+    if (m_part != nullptr)                                                                         \
+      launch_k(k_ring<NV, TV, true>, grid, TV, p.ring_smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn,  \
+               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb);                            \
+    else                                                                                           \
+      launch_k(k_ring<NV, TV, false>, grid, TV, p.ring_smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn, \
+               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb);                            \
     return cudaGetLastError();                                                                     \
   }
   SDCSW_RING_SIZES(SDCSW_RING_LAUNCH)
