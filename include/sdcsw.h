@@ -128,7 +128,10 @@ int sdcsw_stepper_reset(sdcsw_stepper* st, void* stream);
 
 /* option 0: concurrent node chains per sweep (1..M); option 1: sequential
  * node updates (1 = the DIAGONAL_SEQUENTIAL analogue: one node at a time on
- * one stream).  Rebuilds the step graph. */
+ * one stream); option 2: node updates fused into the analysis epilogue (1 =
+ * on, the default for dSDC with one member, M <= 6 and the latency-regime
+ * analysis; takes effect with chains = 1 and sequential = 0).  Bit-identical
+ * results in every setting.  Rebuilds the step graph. */
 int sdcsw_stepper_set_option(sdcsw_stepper* st, int option, int value);
 
 /* One step launched stage by stage with CUDA events (no graph) for the cost

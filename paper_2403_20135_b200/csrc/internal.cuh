@@ -175,6 +175,28 @@ cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, i
                              cudaStream_t s, int* step_counter);
 cudaError_t launch_ring(const Plan& p, const Work& w, int nb, cudaStream_t s);
 cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s);
+// Sweep-fused analysis (latency regime, one state, M <= kFuseMaxNodes): the
+// epilogue takes f_E of every node straight from shared memory and runs the
+// next sweep's node updates (mode 1) or the closing last-node solve (mode 2),
+// so f_E never reaches HBM and the node kernels disappear from the step.
+constexpr int kFuseMaxNodes = 6;
+struct FuseArgs {
+  int mode;                 // 1: next sweep's node updates; 2: closing solve
+  int M, first;             // first: every node's tendencies are f_E(u0), f_I(u0)
+  const double* u0;         // step-start state
+  double* fi;               // f_I of the nodes [M][3C]: read, and (mode 1) updated in place
+  double* u_out;            // mode 2: the step's result (may alias u0)
+  double* xsyn;             // next synthesis operand (nb = M in mode 1, 1 in mode 2)
+  int* diverged;            // mode 2: atomicMin(step index) on a non-finite result
+  const int* step_counter;
+  double phibar;
+  double cf[kFuseMaxNodes * (kFuseMaxNodes + 4)];  // mode 1: [M][M+4]; mode 2: [M+4]
+};
+inline bool fuse_supported(const Plan& p, int M) {
+  return !p.tma_ok && p.own_idx == nullptr && M >= 1 && M <= kFuseMaxNodes;
+}
+cudaError_t launch_analysis_fused(const Plan& p, const Work& w, int nb, const FuseArgs& fz,
+                                  cudaStream_t s);
 cudaError_t launch_f_impl(const Plan& p, const double2* u, double2* fi, int nb, cudaStream_t s);
 // coefficient pointers below are HOST memory; values travel as kernel parameters
 cudaError_t launch_solve(const Plan& p, const double* coef_host, const double2* beta, double2* u,

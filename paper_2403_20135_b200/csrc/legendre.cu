@@ -15,7 +15,7 @@
 // Analysis (replaces the forward transforms, swe.py:180-190):
 //   out[n,c] = sum_j P[n,j] Xfold[j,c] + sum_j H[n,j] Yfold[j,c]
 //   with the fold (N+S or N-S) chosen by the parity class of row n.
-#include "internal.cuh"
+#include "node_math.cuh"
 #ifndef SDCSW_EXP
 #define SDCSW_EXP 0
 #endif
@@ -241,13 +241,85 @@ __global__ void __launch_bounds__(32 * kWarps, 3) k_synthesis(
 // WJ 16-row tiles (m-major order)
 // P columns: (phi, zeta, delta) of all b (6 NB), then ke of all b; H: first 6 NB.
 // ---------------------------------------------------------------------------
-template <int NB, int PF>
+// Sweep-fused epilogue (FuseArgs, internal.cuh).  Lane (rr, ri) of the warp's
+// 16-row output tile owns one real component of one coefficient for all M
+// nodes: it forms f_E of each node from the tile (the plain epilogue's
+// arithmetic), then the node update of k_sweep_nodes / k_final_node (nodes.cu)
+// in the same rounded order, so results are bit-identical to the unfused step.
+template <int NB>
+__device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o, int rw, int rows,
+                                            const int* __restrict__ row_n, int mo, int m, int C,
+                                            const double* __restrict__ lamv,
+                                            const double2* __restrict__ xscale,
+                                            const int* __restrict__ idx_row, int lane) {
+  constexpr int OS = 8 * NB + 1;
+  constexpr int MX = kFuseMaxNodes;
+  const int rr = lane & 15, ri = lane >> 4;
+  if (rw + rr >= rows) return;
+  const int n = row_n[rw + rr];
+  if (n < 0) return;
+  const int idx = mo + n - m;
+  const int C2 = 2 * C, e = 2 * idx + ri;
+  const size_t S2 = 3 * (size_t)C2;
+  const double* row = o + rr * OS;
+  const double l = lamv[idx];
+  const bool zero = m == 0 && ri == 1;
+  Tri fe[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    fe[b].phi = zero ? 0.0 : row[6 * b + ri];
+    fe[b].zeta = zero ? 0.0 : row[6 * b + 2 + ri];
+    fe[b].delta = zero ? 0.0 : __fma_rn(l, row[6 * NB + 2 * b + ri], row[6 * b + 4 + ri]);
+  }
+  const int M = fz.M;
+  const Tri a0 = load_tri(fz.u0, C2, e);
+  const Tri fi0 = f_impl_tri(a0, fz.phibar, l);
+  Tri fi[MX];
+#pragma unroll
+  for (int j = 0; j < MX; ++j)
+    if (j < M) fi[j] = fz.first ? fi0 : load_tri(fz.fi + j * S2, C2, e);
+  if (fz.mode == 1) {
+    const int rec = idx_row[idx] * M;
+    const double2 sc = xscale[idx];
+#pragma unroll
+    for (int q = 0; q < MX; ++q) {
+      if (q >= M) break;
+      const double* c = fz.cf + q * (M + 4);
+      Tri b = a0;
+#pragma unroll
+      for (int j = 0; j < MX; ++j)
+        if (j < M) b = axpy_tri(b, c[j], add_tri(fe[j < NB ? j : NB - 1], fi[j]));
+      b = axmy_tri(b, c[M], fi[q]);
+      const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], l);
+      store_tri(fz.fi + q * S2, C2, e, f_impl_tri(u, fz.phibar, l));
+      write_xsyn_half(fz.xsyn + (size_t)(rec + q) * kXsyn, ri, u.phi, u.zeta, u.delta, sc);
+    }
+  } else {
+    const double* c = fz.cf;
+    Tri b = a0, fil = fi0;
+#pragma unroll
+    for (int j = 0; j < MX; ++j)
+      if (j < M) {
+        b = axpy_tri(axpy_tri(b, c[j], fe[j < NB ? j : NB - 1]), c[j], fi[j]);
+        fil = fi[j];
+      }
+    b = axmy_tri(b, c[M], fil);
+    const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], l);
+    store_tri(fz.u_out, C2, e, u);
+    if (fz.diverged != nullptr && !finite_tri(u))
+      atomicMin(fz.diverged, fz.step_counter ? *fz.step_counter : 1);
+    write_xsyn_half(fz.xsyn + (size_t)idx_row[idx] * kXsyn, ri, u.phi, u.zeta, u.delta,
+                    xscale[idx]);
+  }
+}
+
+template <int NB, int PF, bool FZ>
 __global__ void __launch_bounds__(32 * kWarps) k_analysis(
     const double2* __restrict__ gan, int nb, int T, int J, int C, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, const int* __restrict__ row_n, const int* __restrict__ moff,
     const double* __restrict__ lam, const int* __restrict__ work, double2* __restrict__ fe,
-    int WJ) {
+    int WJ, const FuseArgs fz, const double2* __restrict__ xscale, const int* __restrict__ idx_row) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
   constexpr int HU = 6 * NB;
@@ -383,6 +455,10 @@ __global__ void __launch_bounds__(32 * kWarps) k_analysis(
     }
   __syncwarp();
   const int mo = moff[m];
+  if constexpr (FZ) {
+    fused_nodes<NB>(fz, o, rw, rows, row_n + r0m, mo, m, C, lam, xscale, idx_row, lane);
+    return;
+  }
   for (int it = lane; it < kRowsPerWarp * NB; it += 32) {
     const int rr = it % kRowsPerWarp, b = it / kRowsPerWarp;
     if (rw + rr >= rows || b0 + b >= nb) continue;
@@ -393,8 +469,8 @@ __global__ void __launch_bounds__(32 * kWarps) k_analysis(
     const double l = lam[idx];
     double2 phi = make_double2(row[6 * b + 0], row[6 * b + 1]);
     double2 zeta = make_double2(row[6 * b + 2], row[6 * b + 3]);
-    double2 delta = make_double2(row[6 * b + 4] + l * row[6 * NB + 2 * b],
-                                 row[6 * b + 5] + l * row[6 * NB + 2 * b + 1]);
+    double2 delta = make_double2(__fma_rn(l, row[6 * NB + 2 * b], row[6 * b + 4]),
+                                 __fma_rn(l, row[6 * NB + 2 * b + 1], row[6 * b + 5]));
     if (m == 0) phi.y = zeta.y = delta.y = 0.0;
     double2* dst = fe + (size_t)(b0 + b) * 3 * C;
     dst[idx] = phi;
@@ -461,9 +537,9 @@ static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s) {
-  cudaError_t err;
-  if (launch_analysis_tma(p, w, fe, nb, s, &err)) return err;  // table-streaming regime
+template <bool FZ>
+static cudaError_t analysis_impl(const Plan& p, const Work& w, double2* fe, int nb,
+                                 const FuseArgs& fz, cudaStream_t s) {
   const int NB = pick_nb(nb);
   const int* work = p.own_work != nullptr ? p.own_work : p.anal_work;
   const int nwork = p.own_work != nullptr ? p.n_own_work : p.n_anal_work;
@@ -471,18 +547,33 @@ cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, c
 #define SDCSW_ANA(NBV)                                                                          \
   if (NB == NBV) {                                                                              \
     if (p.T < 200)                                                                              \
-      launch_k(k_analysis<NBV, 2>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab, p.htab, \
-                                                      p.rowoff, p.n_even, p.row_n, p.moff,      \
-                                                      p.lam, work, fe, p.anal_wj);              \
+      launch_k(k_analysis<NBV, 2, FZ>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab, \
+               p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, work, fe, p.anal_wj, fz,    \
+               p.xscale, p.idx_row);                                                            \
     else                                                                                        \
-      launch_k(k_analysis<NBV, 1>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab, p.htab, \
-                                                      p.rowoff, p.n_even, p.row_n, p.moff,      \
-                                                      p.lam, work, fe, p.anal_wj);              \
+      launch_k(k_analysis<NBV, 1, FZ>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab, \
+               p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, work, fe, p.anal_wj, fz,    \
+               p.xscale, p.idx_row);                                                            \
     return cudaGetLastError();                                                                  \
   }
   SDCSW_NB_LIST(SDCSW_ANA)
 #undef SDCSW_ANA
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s) {
+  cudaError_t err;
+  if (launch_analysis_tma(p, w, fe, nb, s, &err)) return err;  // table-streaming regime
+  FuseArgs none{};
+  return analysis_impl<false>(p, w, fe, nb, none, s);
+}
+
+cudaError_t launch_analysis_fused(const Plan& p, const Work& w, int nb, const FuseArgs& fz,
+                                  cudaStream_t s) {
+  // one batch block must hold every node (NB = nb), and the epilogue fixes M
+  if (!fuse_supported(p, fz.M) || nb > kFuseMaxNodes || (nb != 1 && nb != fz.M))
+    return cudaErrorInvalidValue;
+  return analysis_impl<true>(p, w, nullptr, nb, fz, s);
 }
 
 }  // namespace sdcsw

@@ -94,6 +94,7 @@ struct sdcsw_stepper {
   int chains;             // concurrent node chains per sweep (graph branches)
   int members;            // ensemble members advanced together (batched GEMM columns)
   int sequential;         // 1: node updates one after another (DIAGONAL_SEQUENTIAL analogue)
+  int fuse;               // 1: node updates run in the analysis epilogue (launch_analysis_fused)
   int ncreated;           // side streams created
   cudaEvent_t prof[40];   // stage events of a profiled step (created on demand)
   bool prof_ready;
@@ -534,8 +535,47 @@ int sdcsw_check_finite(const double* x, long long n, int* flag, void* stream) {
 // ---------------------------------------------------------------------------
 // stepper
 // ---------------------------------------------------------------------------
+static bool fused_active(const sdcsw_stepper* st) {
+  return st->fuse && st->mode == 0 && st->members == 1 && st->chains == 1 && !st->sequential &&
+         fuse_supported(st->plan->p, st->M);
+}
+
+// dSDC with every node update in the epilogue of the analysis that produced
+// its f_E operands: K x (synthesis -> ring -> fused analysis).  f_I of the
+// nodes is updated in place (a thread owns one element for all nodes).
+static cudaError_t enqueue_step_fused(sdcsw_stepper* st, double2* u, cudaStream_t s) {
+  const Plan& p = st->plan->p;
+  const int M = st->M, K = st->K;
+  const int cstride = M * (M + 4);
+  FuseArgs fz{};
+  fz.M = M;
+  fz.u0 = reinterpret_cast<const double*>(u);
+  fz.fi = reinterpret_cast<double*>(st->fi);
+  fz.u_out = reinterpret_cast<double*>(u);
+  fz.diverged = st->flags;
+  fz.step_counter = st->flags + 1;
+  fz.phibar = p.phibar;
+  const Work w = plan_work(p);
+  for (int k = 1; k <= K; ++k) {
+    const int nb = k == 1 ? 1 : M;
+    cudaError_t e = launch_synthesis(p, w, k == 1 ? st->xsyn1 : st->xsynM, nb, s,
+                                     k == 1 ? st->flags + 1 : nullptr);
+    if (e != cudaSuccess) return e;
+    if ((e = launch_ring(p, w, nb, s)) != cudaSuccess) return e;
+    fz.first = k == 1;
+    fz.mode = k < K ? 1 : 2;
+    fz.xsyn = k < K ? st->xsynM : st->xsyn1;
+    const double* c = st->coef.data() + (size_t)(k - 1) * cstride;
+    const int nc = k < K ? cstride : M + 4;
+    for (int q = 0; q < nc; ++q) fz.cf[q] = c[q];
+    if ((e = launch_analysis_fused(p, w, nb, fz, s)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
                                 cudaEvent_t* marks = nullptr) {
+  if (marks == nullptr && fused_active(st)) return enqueue_step_fused(st, u, s);
   const Plan& p = st->plan->p;
   const int M = st->M, K = st->K;
   const size_t S = st->S;
@@ -549,8 +589,9 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
   if (e != cudaSuccess) return e;
   if (marks) cudaEventRecord(marks[1], s);
   if (st->mode == 0) {
-    // fi alternates between two buffers: every node reads all fi_j while
-    // writing its own fi_m, so the update cannot be in place.  The M node
+    // fe and fi alternate between two buffers: every node reads all fe_j, fi_j
+    // of the previous sweep while its own new values are written (by a
+    // concurrent chain, or by an earlier node in sequential mode).  The M node
     // updates of a sweep are independent (the paper's parallel-across-the-
     // method structure): they run as `chains` concurrent graph branches, each
     // a contiguous node group doing solve -> synthesis -> ring -> analysis.
@@ -561,9 +602,11 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
     const bool seq = st->sequential != 0;  // groups of one node, all on stream s
     const long long mS = M;  // member stride of the node buffers, in states
     double2* fi_cur = st->fi;
+    double2* fe_cur = st->fe0;
     for (int k = 1; k < K; ++k) {
       const bool first = k == 1;
       double2* fi_new = (k % 2) ? st->fi : st->fiB;
+      double2* fe_new = (k % 2) ? st->fe : st->feB;
       const double* coef = st->coef.data() + (size_t)(k - 1) * cstride;
       if (G > 1 && !seq) {
         if ((e = cudaEventRecord(st->ev_fork, s)) != cudaSuccess) return e;
@@ -574,11 +617,11 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
         const int lo = g * M / G, hi = (g + 1) * M / G, cnt = hi - lo;
         cudaStream_t sg = (G > 1 && !seq) ? st->side[g] : s;
         double* xs = st->xsynM + (size_t)lo * E * p.rows * kXsyn;
-        e = launch_sweep_nodes(p, M, lo, cnt, coef, u, first ? st->fe0 : st->fe, first ? 0 : 1,
+        e = launch_sweep_nodes(p, M, lo, cnt, coef, u, fe_cur, first ? 0 : 1,
                                fi_cur, first ? 0 : 1, first, st->ustage + lo * S,
                                fi_new + lo * S, xs, sg, E, first ? 1 : mS, mS, p.fe_chunk);
         if (e != cudaSuccess) return e;
-        e = f_expl_prepped(p, plan_work(p, lo), xs, st->fe + lo * S, cnt * E, sg, nullptr,
+        e = f_expl_prepped(p, plan_work(p, lo), xs, fe_new + lo * S, cnt * E, sg, nullptr,
                            p.fe_chunk);
         if (e != cudaSuccess) return e;
       }
@@ -590,17 +633,18 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
       }
       if (marks) cudaEventRecord(marks[1 + k], s);
       fi_cur = fi_new;
+      fe_cur = fe_new;
     }
     const bool first = K == 1;
     if (marks) {
       e = launch_final_node(p, M, st->coef.data() + (size_t)(K - 1) * cstride, u,
-                            first ? st->fe0 : st->fe, first ? 0 : 1, fi_cur, first ? 0 : 1,
+                            fe_cur, first ? 0 : 1, fi_cur, first ? 0 : 1,
                             first, u, diverged, counter, st->xsyn1, s, E, first ? 1 : mS, mS);
       cudaEventRecord(marks[K + 1], s);
       return e;
     }
     return launch_final_node(p, M, st->coef.data() + (size_t)(K - 1) * cstride, u,
-                             first ? st->fe0 : st->fe, first ? 0 : 1, fi_cur, first ? 0 : 1,
+                             fe_cur, first ? 0 : 1, fi_cur, first ? 0 : 1,
                              first, u, diverged, counter, st->xsyn1, s, E, first ? 1 : mS, mS);
   }
   // serial SDC: old/new tendency buffers alternate between sweeps
@@ -684,7 +728,7 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   }
   const Plan& p = h->p;
   s->S = (size_t)3 * p.C;
-  const size_t nstates = (size_t)E * (1 + 4 * (size_t)M) + (mode == 1 ? (size_t)2 * M + 1 : 0);
+  const size_t nstates = (size_t)E * (1 + 5 * (size_t)M) + (mode == 1 ? (size_t)M + 1 : 0);
   cudaError_t e = cudaSetDevice(p.device);
   if (e == cudaSuccess) e = cudaMalloc(&s->buf, nstates * s->S * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc(&s->flags, 2 * sizeof(int));
@@ -707,9 +751,9 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   s->fi = q; q += E * M * s->S;
   s->ustage = q; q += E * M * s->S;
   s->fiB = q; q += E * M * s->S;
+  s->feB = q; q += E * M * s->S;
   if (mode == 1) {
     s->quad = q; q += M * s->S;
-    s->feB = q; q += M * s->S;
     s->corr = q; q += s->S;
   }
   const int init[2] = {INT_MAX, 0};
@@ -718,8 +762,10 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   // node fills the GPU); large ones batch all nodes through the GEMMs (table
   // reuse).  SDCSW_CHAINS overrides.
   s->chains = 1;
+  s->fuse = mode == 0 && E == 1 && fuse_supported(p, M);
+  if (const char* env = getenv("SDCSW_FUSE")) s->fuse = s->fuse && atoi(env) != 0;
   if (mode == 0) {
-    s->chains = (p.T < 200 && E == 1) ? (M < 2 ? M : 2) : 1;
+    s->chains = (p.T < 200 && E == 1 && !s->fuse) ? (M < 2 ? M : 2) : 1;
     if (const char* env = getenv("SDCSW_CHAINS")) s->chains = atoi(env);
     if (s->chains < 1) s->chains = 1;
     if (s->chains > M) s->chains = M;
@@ -733,7 +779,7 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
       cudaEventCreateWithFlags(&s->ev_join[g], cudaEventDisableTiming);
     }
   }
-  s->launches = mode == 0 ? 4 * K + (K - 1) * 4 * (s->chains - 1) : 3 + K * 5 * M;
+  sdcsw_stepper_launches_per_step(s, &s->launches);
   *out = s;
   return SDCSW_OK;
 }
@@ -772,7 +818,8 @@ int sdcsw_stepper_reset(sdcsw_stepper* s, void* stream) {
 int sdcsw_stepper_launches_per_step(sdcsw_stepper* s, int* n) {
   if (!s || !n) return SDCSW_ERR_STATE;
   const int G = s->sequential ? s->M : s->chains;
-  s->launches = s->mode == 0 ? 4 + 4 * G * (s->K - 1) : 3 + s->K * 5 * s->M;
+  s->launches = s->mode == 0 ? (fused_active(s) ? 3 * s->K : 4 + 4 * G * (s->K - 1))
+                             : 3 + s->K * 5 * s->M;
   *n = s->launches;
   return SDCSW_OK;
 }
@@ -826,6 +873,10 @@ int sdcsw_stepper_set_option(sdcsw_stepper* s, int option, int value) {
   } else if (option == 1) {  // sequential node updates
     if (s->mode != 0 || s->members != 1) return SDCSW_ERR_PARAM;
     s->sequential = value ? 1 : 0;
+  } else if (option == 2) {  // node updates fused into the analysis epilogue
+    if (value && (s->mode != 0 || s->members != 1 || !fuse_supported(s->plan->p, s->M)))
+      return SDCSW_ERR_PARAM;
+    s->fuse = value ? 1 : 0;
   } else {
     return SDCSW_ERR_PARAM;
   }

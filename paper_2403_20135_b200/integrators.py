@@ -227,6 +227,13 @@ class DeviceStepper:
         """One node update at a time (the DIAGONAL_SEQUENTIAL analogue)."""
         _native.check(self.lib.sdcsw_stepper_set_option(self.handle, 1, int(bool(on))), "set_option")
 
+    def set_fused(self, on=True):
+        """Node updates in the analysis epilogue (default where supported: T < 400, M <= 6)."""
+        _native.check(self.lib.sdcsw_stepper_set_option(self.handle, 2, int(bool(on))), "set_option")
+        n = ctypes.c_int()
+        _native.check(self.lib.sdcsw_stepper_launches_per_step(self.handle, ctypes.byref(n)))
+        self.launches_per_step = n.value
+
     def profile_step(self, u):
         """Advance ``u`` one step stage by stage; returns a StepReport with CUDA-event stage times."""
         n = self.n_sweeps + 2

@@ -236,6 +236,64 @@ def test_node_parallel_single_rank_matches_fused_stepper():
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("trunc,m_count,k_count", [(63, 1, 1), (63, 2, 3), (63, 3, 1), (63, 4, 4),
+                                                   (63, 5, 2), (63, 6, 3), (255, 4, 3)])
+def test_fused_node_epilogue_bitwise(trunc, m_count, k_count):
+    """Node updates fused into the analysis epilogue == separate node kernels
+    (batched, chained and sequential), bitwise; launches per step 3K vs 4+4(K-1)."""
+    import torch
+
+    from paper_2403_20135_b200.integrators import DeviceStepper
+
+    p = gpu(trunc)
+    cfg = SdcConfig(table=CollocationTable.radau_right(m_count), n_sweeps=k_count,
+                    mode=SweepMode.DIAGONAL_PARALLEL, time_threads=m_count)
+    u0 = torch.from_numpy(random_initial_state(p.grid, 30 + m_count)).to(p.device).contiguous()
+    st = DeviceStepper(p, cfg, 90.0, serial=False)
+    st.set_chains(1)
+    st.set_fused(True)
+    assert st.launches_per_step == 3 * k_count
+    results = []
+    for setup in ("fused", "batched", "chains", "sequential"):
+        if setup == "batched":
+            st.set_fused(False)
+            assert st.launches_per_step == 4 + 4 * (k_count - 1)
+        elif setup == "chains":
+            st.set_chains(m_count)
+        elif setup == "sequential":
+            st.set_chains(1)
+            st.set_sequential(True)
+        u = u0.clone()
+        st.run(u, 4)
+        torch.cuda.synchronize()
+        results.append(u)
+    for r in results[1:]:
+        assert torch.equal(results[0], r)
+    assert st.diverged() == 0
+    st.close()
+
+
+def test_fused_path_divergence_step():
+    """The fused closing solve raises the device divergence flag with the step index."""
+    from paper_2403_20135_b200.integrators import DeviceStepper
+
+    p = gpu(63)
+    table = CollocationTable.radau_right(3)
+    cfg = SdcConfig(table=table, n_sweeps=3, mode=SweepMode.DIAGONAL_PARALLEL, time_threads=3)
+    u0 = random_initial_state(p.grid, 0) * 1e140
+    o = oracle_for(p)
+    step = lambda pr, s, dt: osdc.dsdc(pr, s, dt, table, 3)  # noqa: E731
+    with pytest.raises(DivergenceError) as ref:
+        osdc.march(o, u0, 120.0, 6, step)
+    st = DeviceStepper(p, cfg, 120.0, serial=False)
+    st.set_chains(1)
+    st.set_fused(True)
+    u = p._to_device(u0).reshape(-1).contiguous()
+    st.run(u, 6)
+    assert st.diverged() == ref.value.step_index
+    st.close()
+
+
 def test_ensemble_members_match_single_runs():
     """BASELINE config 4 mechanism: members batched through the GEMMs give, per
     member, exactly the single-state result (bitwise)."""
