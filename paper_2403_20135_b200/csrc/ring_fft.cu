@@ -24,10 +24,8 @@
 namespace sdcsw {
 #if SDCSW_EXP == 4
 __device__ unsigned long long g_rtimes[1 << 16];
-__device__ __forceinline__ unsigned long long gtimer_r() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
+__device__ __forceinline__ unsigned long long gtimer_r() {  // SM cycles (phase differences only)
+  return (unsigned long long)clock64();
 }
 #define RT(i) if (threadIdx.x == 0 && cta < 8192) g_rtimes[8 * cta + (i)] = gtimer_r();
 #else
@@ -138,11 +136,11 @@ constexpr int padded() { return N + N / 8; }
 // same points (Stockham: the last pass of a plan writes exactly the points
 // the first pass of the reversed plan reads).
 template <int N> struct RadixPlan;
-template <> struct RadixPlan<96> { static constexpr int n = 3; static constexpr int r[4] = {8, 4, 3, 0}; };
-template <> struct RadixPlan<192> { static constexpr int n = 3; static constexpr int r[4] = {16, 4, 3, 0}; };
-template <> struct RadixPlan<384> { static constexpr int n = 3; static constexpr int r[4] = {16, 8, 3, 0}; };
-template <> struct RadixPlan<768> { static constexpr int n = 3; static constexpr int r[4] = {16, 16, 3, 0}; };
-template <> struct RadixPlan<1536> { static constexpr int n = 4; static constexpr int r[4] = {16, 8, 4, 3}; };
+template <> struct RadixPlan<96> { static constexpr int n = 3; static constexpr int r[6] = {8, 4, 3}; };
+template <> struct RadixPlan<192> { static constexpr int n = 3; static constexpr int r[6] = {16, 4, 3}; };
+template <> struct RadixPlan<384> { static constexpr int n = 3; static constexpr int r[6] = {16, 8, 3}; };
+template <> struct RadixPlan<768> { static constexpr int n = 3; static constexpr int r[6] = {16, 16, 3}; };
+template <> struct RadixPlan<1536> { static constexpr int n = 4; static constexpr int r[6] = {16, 8, 4, 3}; };
 
 template <int N>
 constexpr int inv_radix(int s) { return RadixPlan<N>::r[s]; }
@@ -252,35 +250,52 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
   RT(0)
   for (int k = threadIdx.x; k < N; k += THREADS) tw[k] = twg[k];
 
-  // ---- inverse pass 0 (P = 1, no twiddles) straight from the Fourier
-  //      coefficients: Z_m = X_m + i Y_m, Z_{N-m} = conj(X_m) + i conj(Y_m)
+  // ---- inverse pass 0 (P = 1, no twiddles) from the Fourier coefficients:
+  //      Z_m = X_m + i Y_m, Z_{N-m} = conj(X_m) + i conj(Y_m).
+  //      The coefficients are first staged (coalesced, all loads in flight)
+  //      into the Z area; the pass then reads them from shared memory, syncs
+  //      and writes its outputs over them (the in-place Stockham pattern).
   {
     constexpr int R = inv_radix<N>(0);
     constexpr int NR = N / R;
     constexpr int ITEMS = 4 * NR;
-    for (int it = threadIdx.x; it < ITEMS; it += THREADS) {
-      const int i = it >> 2, f = it & 3;
-      double2 v[R];
+    constexpr int MAXIT = (ITEMS + THREADS - 1) / THREADS;
+    double2* Fs = Z;  // [L][8]: (U, V, zeta, Phi) x (north, south)
+    for (int e = threadIdx.x; e < 8 * L; e += THREADS) Fs[e] = Fm(e >> 3)[e & 7];
+    __syncthreads();
+    double2 v[MAXIT][R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int k = i + r * NR;
-        double2 z = make_double2(0.0, 0.0);
-        if (k <= T) {
-          const double2* F = Fm(k);
-          double2 xn = F[f * 2], xs = F[f * 2 + 1];
+    for (int q = 0; q < MAXIT; ++q) {
+      const int it = threadIdx.x + q * THREADS;
+      if (ITEMS % THREADS == 0 || it < ITEMS) {
+        const int i = it >> 2, f = it & 3;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int k = i + r * NR;
+          const bool lo = k <= T, hi = k >= N - T;
+          double2 xn = make_double2(0.0, 0.0), xs = xn;
+          if (lo || hi) {
+            const double2* F = Fs + (lo ? k : N - k) * 8;
+            xn = F[f * 2];
+            xs = F[f * 2 + 1];
+          }
           if (k == 0) xn.y = xs.y = 0.0;
-          z = make_double2(xn.x - xs.y, xn.y + xs.x);
-        } else if (k >= N - T) {
-          const double2* F = Fm(N - k);
-          const double2 xn = F[f * 2], xs = F[f * 2 + 1];
-          z = make_double2(xn.x + xs.y, xs.x - xn.y);
+          v[q][r] = lo ? make_double2(xn.x - xs.y, xn.y + xs.x)
+                       : make_double2(xn.x + xs.y, xs.x - xn.y);
         }
-        v[r] = z;
+        dft<R, true>(v[q]);
       }
-      dft<R, true>(v);
-      double2* X = Z + f * NP;
+    }
+    __syncthreads();
 #pragma unroll
-      for (int r = 0; r < R; ++r) X[pz(i * R + r)] = v[r];
+    for (int q = 0; q < MAXIT; ++q) {
+      const int it = threadIdx.x + q * THREADS;
+      if (ITEMS % THREADS == 0 || it < ITEMS) {
+        const int i = it >> 2, f = it & 3;
+        double2* X = Z + f * NP;
+#pragma unroll
+        for (int r = 0; r < R; ++r) X[pz(i * R + r)] = v[q][r];
+      }
     }
     __syncthreads();
   }
@@ -354,43 +369,31 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
 
   const double ws = wsyn[j], wk = wke[j];
   const double h = 0.5 / (double)N;
-  // analysis layout: [b][m][j][fold][slot]
+  // analysis layout: [b][m][j][fold][slot]; thread (m, fold) writes the fold's
+  // seven slots (112 contiguous bytes), the pair of folds a 224-byte record
   double2* outp = gan + ((size_t)b * L * J + j) * (kNumSlots * 2);
-  for (int idx = threadIdx.x; idx < 5 * L; idx += THREADS) {
-    const int m = idx / 5, o = idx - 5 * m;
-    const double2 zm = Z[o * NP + pz(m)], zc = Z[o * NP + pz(m == 0 ? 0 : N - m)];
-    // X = FFT(north)/N, Y = FFT(south)/N; S = X + Y, A = X - Y
-    const double2 X = make_double2(h * (zm.x + zc.x), h * (zm.y - zc.y));
-    const double2 Y = make_double2(h * (zm.y + zc.y), -h * (zm.x - zc.x));
-    const double2 S = cadd(X, Y), A = csub(X, Y);
+  for (int it = threadIdx.x; it < 2 * L; it += THREADS) {
+    const int m = it >> 1, fold = it & 1;
     const double dm = (double)m;
-    double2* dst = outp + (size_t)m * J * (kNumSlots * 2);
-    switch (o) {
-      case 0:  // A = eta U:  X_zeta = -(i m A) ws,  Y_delta = A ws
-        dst[0 * kNumSlots + kXZeta] = make_double2(dm * S.y * ws, -dm * S.x * ws);
-        dst[1 * kNumSlots + kXZeta] = make_double2(dm * A.y * ws, -dm * A.x * ws);
-        dst[0 * kNumSlots + kYDelta] = make_double2(S.x * ws, S.y * ws);
-        dst[1 * kNumSlots + kYDelta] = make_double2(A.x * ws, A.y * ws);
-        break;
-      case 1:  // B = eta V:  X_delta = (i m B) ws,  Y_zeta = B ws
-        dst[0 * kNumSlots + kXDelta] = make_double2(-dm * S.y * ws, dm * S.x * ws);
-        dst[1 * kNumSlots + kXDelta] = make_double2(-dm * A.y * ws, dm * A.x * ws);
-        dst[0 * kNumSlots + kYZeta] = make_double2(S.x * ws, S.y * ws);
-        dst[1 * kNumSlots + kYZeta] = make_double2(A.x * ws, A.y * ws);
-        break;
-      case 2:  // C = Phi U:  X_phi = -(i m C) ws
-        dst[0 * kNumSlots + kXPhi] = make_double2(dm * S.y * ws, -dm * S.x * ws);
-        dst[1 * kNumSlots + kXPhi] = make_double2(dm * A.y * ws, -dm * A.x * ws);
-        break;
-      case 3:  // D = Phi V:  Y_phi = D ws
-        dst[0 * kNumSlots + kYPhi] = make_double2(S.x * ws, S.y * ws);
-        dst[1 * kNumSlots + kYPhi] = make_double2(A.x * ws, A.y * ws);
-        break;
-      default:  // kinetic energy: X_ke = E wk
-        dst[0 * kNumSlots + kXKe] = make_double2(S.x * wk, S.y * wk);
-        dst[1 * kNumSlots + kXKe] = make_double2(A.x * wk, A.y * wk);
-        break;
+    double2 v[5];
+#pragma unroll
+    for (int o = 0; o < 5; ++o) {
+      const double2 zm = Z[o * NP + pz(m)], zc = Z[o * NP + pz(m == 0 ? 0 : N - m)];
+      // X = FFT(north)/N, Y = FFT(south)/N; fold 0: S = X + Y, fold 1: A = X - Y
+      const double2 X = make_double2(h * (zm.x + zc.x), h * (zm.y - zc.y));
+      const double2 Y = make_double2(h * (zm.y + zc.y), -h * (zm.x - zc.x));
+      v[o] = fold ? csub(X, Y) : cadd(X, Y);
     }
+    double2* dst = outp + (size_t)m * J * (kNumSlots * 2) + fold * kNumSlots;
+    // A = eta U: X_zeta = -(i m A) ws, Y_delta = A ws; B = eta V: X_delta = (i m B) ws,
+    // Y_zeta = B ws; C = Phi U: X_phi = -(i m C) ws; D = Phi V: Y_phi = D ws; X_ke = E wk
+    dst[kXPhi] = make_double2(dm * v[2].y * ws, -dm * v[2].x * ws);
+    dst[kXZeta] = make_double2(dm * v[0].y * ws, -dm * v[0].x * ws);
+    dst[kXDelta] = make_double2(-dm * v[1].y * ws, dm * v[1].x * ws);
+    dst[kXKe] = make_double2(v[4].x * wk, v[4].y * wk);
+    dst[kYPhi] = make_double2(v[3].x * ws, v[3].y * ws);
+    dst[kYZeta] = make_double2(v[1].x * ws, v[1].y * ws);
+    dst[kYDelta] = make_double2(v[0].x * ws, v[0].y * ws);
   }
 #if SDCSW_EXP == 4
   __syncthreads();

@@ -19,7 +19,6 @@ for cfg, nb in (('c1', 1), ('c1', 4)):
     L.sdcsw_debug_rtimes.argtypes = [ctypes.c_void_p, ctypes.c_int]
     L.sdcsw_debug_rtimes(buf, 8 * n)
     t = np.array(buf, dtype=np.float64).reshape(n, 8)[:, :6]
-    t = (t - t[:, :1].min()) / 1e3
-    d = np.diff(t, axis=1)
-    print(cfg, nb, 'span %.2f' % t[:, 5].max(), 'start max %.2f' % t[:, 0].max(),
-          'phase means (build, inv, prod, fwd, out):', np.round(d.mean(0), 2), 'max', np.round(d.max(0), 2))
+    d = np.diff(t, axis=1)  # SM cycles per phase
+    print(cfg, nb, 'cycles per phase (build, inv, prod, fwd, out): mean', np.round(d.mean(0)),
+          'max', np.round(d.max(0)), 'total mean', round(d.sum(1).mean()))
