@@ -88,7 +88,15 @@ __global__ void __launch_bounds__(256) k_synth_prep(const double* __restrict__ u
 // re-read from L1 instead of being re-fetched by a separate CTA per block.
 // ---------------------------------------------------------------------------
 template <int NB, int PF>
-__global__ void __launch_bounds__(32 * kWarps, 3) k_synthesis(
+#ifndef SDCSW_SYN_MINB
+#define SDCSW_SYN_MINB 4
+#endif
+#ifdef SDCSW_ANA_MIN
+#define SDCSW_ANA_LB __launch_bounds__(32 * kWarps, SDCSW_ANA_MIN)
+#else
+#define SDCSW_ANA_LB __launch_bounds__(32 * kWarps)
+#endif
+__global__ void __launch_bounds__(32 * kWarps, SDCSW_SYN_MINB) k_synthesis(
     const double* __restrict__ xsyn, int nb, int T, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ,
@@ -314,7 +322,7 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
 }
 
 template <int NB, int PF, bool FZ>
-__global__ void __launch_bounds__(32 * kWarps) k_analysis(
+__global__ void SDCSW_ANA_LB k_analysis(
     const double2* __restrict__ gan, int nb, int T, int J, int C, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, const int* __restrict__ row_n, const int* __restrict__ moff,
@@ -457,8 +465,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_analysis(
   const int mo = moff[m];
   if constexpr (FZ) {
     fused_nodes<NB>(fz, o, rw, rows, row_n + r0m, mo, m, C, lam, xscale, idx_row, lane);
-    return;
-  }
+  } else {
   for (int it = lane; it < kRowsPerWarp * NB; it += 32) {
     const int rr = it % kRowsPerWarp, b = it / kRowsPerWarp;
     if (rw + rr >= rows || b0 + b >= nb) continue;
@@ -476,6 +483,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_analysis(
     dst[idx] = phi;
     dst[C + idx] = zeta;
     dst[2 * C + idx] = delta;
+  }
   }
 }
 
@@ -520,16 +528,12 @@ static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist
   }
   dim3 grid(p.J / (kRowsPerWarp * WJ), nm, (nblk + NBC - 1) / NBC);
   const dim3 block(32 * WJ * WK);
+  // prefetch depth 1: a deeper register prefetch costs a resident CTA per SM,
+  // which the latency-bound small truncations need more (measured on B200)
 #define SDCSW_SYN(NBV)                                                                         \
   if (NB == NBV) {                                                                             \
-    if (p.T < 200)                                                                             \
-      launch_k(k_synthesis<NBV, 2>, grid, block, 0, s, xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
-                                                       p.rowoff, p.n_even, fsyn,               \
-                                                       step_counter, WJ, NBC, mlist, Lp);      \
-    else                                                                                       \
-      launch_k(k_synthesis<NBV, 1>, grid, block, 0, s, xsyn, nb, p.T, p.J, p.ptab, p.htab,     \
-                                                       p.rowoff, p.n_even, fsyn,               \
-                                                       step_counter, WJ, NBC, mlist, Lp);      \
+    launch_k(k_synthesis<NBV, 1>, grid, block, 0, s, xsyn, nb, p.T, p.J, p.ptab, p.htab,       \
+             p.rowoff, p.n_even, fsyn, step_counter, WJ, NBC, mlist, Lp);                      \
     return cudaGetLastError();                                                                 \
   }
   SDCSW_NB_LIST(SDCSW_SYN)
@@ -544,16 +548,12 @@ static cudaError_t analysis_impl(const Plan& p, const Work& w, double2* fe, int 
   const int* work = p.own_work != nullptr ? p.own_work : p.anal_work;
   const int nwork = p.own_work != nullptr ? p.n_own_work : p.n_anal_work;
   dim3 grid(nwork, (nb + NB - 1) / NB);
+  // prefetch depth 1 (see synthesis_impl)
 #define SDCSW_ANA(NBV)                                                                          \
   if (NB == NBV) {                                                                              \
-    if (p.T < 200)                                                                              \
-      launch_k(k_analysis<NBV, 2, FZ>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab, \
-               p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, work, fe, p.anal_wj, fz,    \
-               p.xscale, p.idx_row);                                                            \
-    else                                                                                        \
-      launch_k(k_analysis<NBV, 1, FZ>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab, \
-               p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, work, fe, p.anal_wj, fz,    \
-               p.xscale, p.idx_row);                                                            \
+    launch_k(k_analysis<NBV, 1, FZ>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab,  \
+             p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, work, fe, p.anal_wj, fz,      \
+             p.xscale, p.idx_row);                                                              \
     return cudaGetLastError();                                                                  \
   }
   SDCSW_NB_LIST(SDCSW_ANA)
