@@ -48,7 +48,7 @@ struct Plan {
   double* mu;       // [J] northern nodes
   double* wsyn;     // [J] 2 pi w_j / (a (1 - mu_j^2))
   double* wke;      // [J] 2 pi w_j
-  double2* twiddle; // [nlon] exp(-2 pi i k / nlon)
+  double2* twiddle; // ring FFT per-pass twiddle tables (ring_pass_twiddles)
   int* anal_work;   // [n_anal_work] (m << 16 | row block of anal_wj tiles)
   int n_anal_work;
   int* anal_work4;  // [n_anal_work4] row blocks of 4 tiles (throughput regime)

@@ -15,6 +15,8 @@
 // Output per (b, pair, m <= T): the seven analysis data slots, pre-weighted,
 // pre-multiplied by i m where the analysis needs it and folded into symmetric
 // (N+S) / antisymmetric (N-S) parts.
+#include <vector>
+
 #include "internal.cuh"
 
 #ifndef SDCSW_EXP
@@ -124,11 +126,14 @@ __device__ __forceinline__ void dft(double2 (&u)[R]) {
   }
 }
 
-// Shared-memory FFT arrays are padded by one element every 8: Stockham writes
-// at stride R then hit distinct 16-byte bank groups within a quarter-warp.
-__device__ __forceinline__ int pz(int k) { return k + (k >> 3); }
+// Shared-memory FFT arrays are padded: element k of a transform lives at
+// k + (k >> SH) (SH = 0: unpadded).  Each array generation between two passes
+// gets its own SH, chosen at compile time by a bank model of the writing and
+// the reading pass (16-byte accesses: a quarter-warp of 8 lanes is one
+// 128-byte wavefront when the 8 addresses fall in distinct 16-byte bank groups).
+__host__ __device__ constexpr int pzv(int k, int sh) { return sh ? k + (k >> sh) : k; }
 template <int N>
-constexpr int padded() { return N + N / 8; }
+constexpr int padded() { return N + N / 8; }  // room for the densest padding (SH = 3)
 
 // Compile-time radix plans.  The inverse plan ends with radix 3 and the
 // forward plan (its reverse) starts with it, so the last inverse pass, the
@@ -146,14 +151,128 @@ template <int N>
 constexpr int inv_radix(int s) { return RadixPlan<N>::r[s]; }
 template <int N>
 constexpr int fwd_radix(int s) { return RadixPlan<N>::r[RadixPlan<N>::n - 1 - s]; }
+template <int N>
+constexpr int inv_prefix(int s) {  // product of the first s inverse radices
+  int p = 1;
+  for (int q = 0; q < s; ++q) p *= inv_radix<N>(q);
+  return p;
+}
+template <int N>
+constexpr int fwd_prefix(int s) {
+  int p = 1;
+  for (int q = 0; q < s; ++q) p *= fwd_radix<N>(q);
+  return p;
+}
+
+// ---- bank model ------------------------------------------------------------
+// Wavefronts of one 16-byte shared access by lanes it = 0..63 (two warps),
+// lane address given in 16-byte units.
+template <typename F>
+constexpr int wavefronts(F addr) {
+  int total = 0;
+  for (int ph = 0; ph < 8; ++ph) {  // 8 quarter-warps
+    int a[8] = {};
+    for (int l = 0; l < 8; ++l) a[l] = addr(ph * 8 + l);
+    int worst = 1;
+    for (int g = 0; g < 8; ++g) {
+      int cnt = 0;
+      for (int l = 0; l < 8; ++l) {
+        if (a[l] < 0 || ((a[l] % 8) + 8) % 8 != g) continue;
+        bool dup = false;
+        for (int q = 0; q < l; ++q) dup = dup || a[q] == a[l];
+        if (!dup) ++cnt;
+      }
+      worst = cnt > worst ? cnt : worst;
+    }
+    total += worst;
+  }
+  return total;
+}
+// Stockham pass (R, P) over NF field-major transforms: read of input r, write of output r
+template <int N>
+constexpr int pass_read_cost(int R, int NF, int sh) {
+  int c = 0;
+  const int NR = N / R;
+  for (int r = 0; r < R; ++r)
+    c += wavefronts([&](int it) {
+      if (it >= NF * NR) return -1;
+      const int f = it / NR, i = it % NR;
+      return f * padded<N>() + pzv(i + r * NR, sh);
+    });
+  return c;
+}
+template <int N>
+constexpr int pass_write_cost(int R, int P, int NF, int sh) {
+  int c = 0;
+  const int NR = N / R;
+  for (int r = 0; r < R; ++r)
+    c += wavefronts([&](int it) {
+      if (it >= NF * NR) return -1;
+      const int f = it / NR, i = it % NR, k = i % P;
+      return f * padded<N>() + pzv((i - k) * R + k + r * P, sh);
+    });
+  return c;
+}
+// Array generation b (between consecutive passes): inverse passes 0..n-1 (the
+// last fused with the products and forward pass 0), forward passes 1..n-1.
+// b < n-1: inverse pass b -> inverse pass b+1 (b = n-2: the fused phase reads)
+// b = n-1: fused phase (forward pass 0) -> forward pass 1
+// b >= n : forward pass b-n+1 -> forward pass b-n+2 (last: the output phase)
+template <int N>
+constexpr int generation_cost(int b, int sh) {
+  constexpr int n = RadixPlan<N>::n;
+  int c = 0;
+  if (b < n - 1) {
+    c += pass_write_cost<N>(inv_radix<N>(b), inv_prefix<N>(b), 4, sh);
+    c += pass_read_cost<N>(inv_radix<N>(b + 1), b + 1 == n - 1 ? 1 : 4, sh);
+  } else {
+    const int s = b - (n - 1);  // forward pass writing this generation
+    c += pass_write_cost<N>(fwd_radix<N>(s), fwd_prefix<N>(s), s == 0 ? 1 : 5, sh);
+    if (s + 1 < n) c += pass_read_cost<N>(fwd_radix<N>(s + 1), 5, sh);
+  }
+  return c;
+}
+template <int N>
+constexpr int gen_shift(int b) {
+  const int cand[4] = {3, 4, 5, 0};
+  int best = cand[0], bc = generation_cost<N>(b, cand[0]);
+  for (int q = 1; q < 4; ++q) {
+    const int c = generation_cost<N>(b, cand[q]);
+    if (c < bc) { bc = c; best = cand[q]; }
+  }
+  return best;
+}
+
+// ---- per-pass twiddle tables -------------------------------------------------
+// Pass (R, P) needs w(r, k) = exp(-2 pi i r k / (R P)) for r = 1..R-1, k < P,
+// stored at [(r - 1) P + k] so that lanes with consecutive k read consecutive
+// entries.  Tables: inverse passes 1..n-1, then forward passes 1..n-1.
+template <int N>
+constexpr int tw_size_inv(int s) { return (inv_radix<N>(s) - 1) * inv_prefix<N>(s); }
+template <int N>
+constexpr int tw_size_fwd(int s) { return (fwd_radix<N>(s) - 1) * fwd_prefix<N>(s); }
+template <int N>
+constexpr int tw_off_inv(int s) {
+  int o = 0;
+  for (int q = 1; q < s; ++q) o += tw_size_inv<N>(q);
+  return o;
+}
+template <int N>
+constexpr int tw_off_fwd(int s) {
+  int o = tw_off_inv<N>(RadixPlan<N>::n);
+  for (int q = 1; q < s; ++q) o += tw_size_fwd<N>(q);
+  return o;
+}
+template <int N>
+constexpr int tw_total() { return tw_off_fwd<N>(RadixPlan<N>::n); }
 
 // One in-place Stockham pass (radix R, sub-length P) over NF concurrent
-// transforms of length N at Z[f * padded<N>()]; tw[k] = exp(-2 pi i k / N).
-template <int N, int R, int P, bool INV, int NF, int THREADS>
-__device__ __forceinline__ void pass(double2* Z, const double2* tw) {
+// transforms of length N at Z[f * padded<N>()], reading generation SHI and
+// writing generation SHO; twp = this pass's twiddle table.
+template <int N, int R, int P, bool INV, int NF, int THREADS, int SHI, int SHO>
+__device__ __forceinline__ void pass(double2* Z, const double2* twp) {
   constexpr int NR = N / R;
   constexpr int ITEMS = NF * NR;
-  constexpr int TS = N / (R * P);
   constexpr int MAXIT = (ITEMS + THREADS - 1) / THREADS;
   double2 v[MAXIT][R];
 #pragma unroll
@@ -164,11 +283,11 @@ __device__ __forceinline__ void pass(double2* Z, const double2* tw) {
       const double2* X = Z + f * padded<N>();
       const int k = i % P;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[q][r] = X[pz(i + r * NR)];
+      for (int r = 0; r < R; ++r) v[q][r] = X[pzv(i + r * NR, SHI)];
       if (P > 1 && k) {
 #pragma unroll
         for (int r = 1; r < R; ++r) {
-          double2 w = tw[r * k * TS];
+          double2 w = twp[(r - 1) * P + k];
           if (INV) w.y = -w.y;
           v[q][r] = cmul(v[q][r], w);
         }
@@ -186,32 +305,43 @@ __device__ __forceinline__ void pass(double2* Z, const double2* tw) {
       const int k = i % P;
       const int jo = (i - k) * R + k;
 #pragma unroll
-      for (int r = 0; r < R; ++r) X[pz(jo + r * P)] = v[q][r];
+      for (int r = 0; r < R; ++r) X[pzv(jo + r * P, SHO)] = v[q][r];
     }
   }
   __syncthreads();
 }
 
-// generic inverse passes s in [S, n-1) and forward passes s in [S, n)
-template <int N, int S, int P, int NF, int THREADS>
+// inverse passes s in [S, n-1) and forward passes s in [S, n)
+template <int N, int S, int THREADS>
 __device__ __forceinline__ void inverse_mid(double2* Z, const double2* tw) {
   if constexpr (S < RadixPlan<N>::n - 1) {
-    pass<N, inv_radix<N>(S), P, true, NF, THREADS>(Z, tw);
-    inverse_mid<N, S + 1, P * inv_radix<N>(S), NF, THREADS>(Z, tw);
+    pass<N, inv_radix<N>(S), inv_prefix<N>(S), true, 4, THREADS, gen_shift<N>(S - 1),
+         gen_shift<N>(S)>(Z, tw + tw_off_inv<N>(S));
+    inverse_mid<N, S + 1, THREADS>(Z, tw);
   }
 }
-template <int N, int S, int P, int NF, int THREADS>
+template <int N, int S, int THREADS>
 __device__ __forceinline__ void forward_rest(double2* Z, const double2* tw) {
-  if constexpr (S < RadixPlan<N>::n) {
-    pass<N, fwd_radix<N>(S), P, false, NF, THREADS>(Z, tw);
-    forward_rest<N, S + 1, P * fwd_radix<N>(S), NF, THREADS>(Z, tw);
+  constexpr int n = RadixPlan<N>::n;
+  if constexpr (S < n) {
+    pass<N, fwd_radix<N>(S), fwd_prefix<N>(S), false, 5, THREADS, gen_shift<N>(n - 2 + S),
+         gen_shift<N>(n - 1 + S)>(Z, tw + tw_off_fwd<N>(S));
+    forward_rest<N, S + 1, THREADS>(Z, tw);
   }
 }
-template <int N, int S>
-constexpr int inv_prefix() {  // product of the first S inverse radices
-  int p = 1;
-  for (int s = 0; s < S; ++s) p *= inv_radix<N>(s);
-  return p;
+
+// host: the per-pass twiddle tables gathered from w[k] = exp(-2 pi i k / N)
+template <int N>
+static void build_pass_twiddles(const double2* w, std::vector<double2>& out) {
+  constexpr int n = RadixPlan<N>::n;
+  out.assign(tw_total<N>(), make_double2(0.0, 0.0));
+  auto fill = [&](int off, int R, int P) {
+    const int TS = N / (R * P);
+    for (int r = 1; r < R; ++r)
+      for (int k = 0; k < P; ++k) out[off + (r - 1) * P + k] = w[r * k * TS];
+  };
+  for (int s = 1; s < n; ++s) fill(tw_off_inv<N>(s), inv_radix<N>(s), inv_prefix<N>(s));
+  for (int s = 1; s < n; ++s) fill(tw_off_fwd<N>(s), fwd_radix<N>(s), fwd_prefix<N>(s));
 }
 
 template <int N, int THREADS, bool SPLIT>
@@ -229,8 +359,9 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
   extern __shared__ double2 sm2[];
   constexpr int NP = padded<N>();
   constexpr int NS = RadixPlan<N>::n;
+  constexpr int TWN = tw_total<N>();
   double2* Z = sm2;             // [5][NP] (padded)
-  double2* tw = sm2 + 5 * NP;   // [N]
+  double2* tw = sm2 + 5 * NP;   // per-pass twiddle tables
   const int L = T + 1;
   const int j = blockIdx.x, b = blockIdx.y;
   // Fourier coefficients of (b, j, m): part-major [part][nbg][J][Lp][4][2]
@@ -248,36 +379,44 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
   const int cta = blockIdx.y * gridDim.x + blockIdx.x;
 #endif
   RT(0)
-  for (int k = threadIdx.x; k < N; k += THREADS) tw[k] = twg[k];
+  for (int k = threadIdx.x; k < TWN; k += THREADS) tw[k] = twg[k];
 
   // ---- inverse pass 0 (P = 1, no twiddles) from the Fourier coefficients:
   //      Z_m = X_m + i Y_m, Z_{N-m} = conj(X_m) + i conj(Y_m).
   //      The coefficients are first staged (coalesced, all loads in flight)
-  //      into the Z area; the pass then reads them from shared memory, syncs
-  //      and writes its outputs over them (the in-place Stockham pattern).
+  //      into the Z area as Fs[hemisphere][field][m] (row stride L + 1); the
+  //      pass then reads them, syncs and writes its outputs over them (the
+  //      in-place Stockham pattern).
   {
     constexpr int R = inv_radix<N>(0);
     constexpr int NR = N / R;
     constexpr int ITEMS = 4 * NR;
     constexpr int MAXIT = (ITEMS + THREADS - 1) / THREADS;
-    double2* Fs = Z;  // [L][8]: (U, V, zeta, Phi) x (north, south)
-    for (int e = threadIdx.x; e < 8 * L; e += THREADS) Fs[e] = Fm(e >> 3)[e & 7];
+    constexpr int SHO = gen_shift<N>(0);
+    double2* Fs = Z;
+    const int LS = L + 1;
+    for (int e = threadIdx.x; e < 8 * L; e += THREADS) {
+      const int m = e >> 3, fh = e & 7;  // fh = 2 field + hemisphere
+      Fs[((fh & 1) * 4 + (fh >> 1)) * LS + m] = Fm(m)[fh];
+    }
     __syncthreads();
     double2 v[MAXIT][R];
 #pragma unroll
     for (int q = 0; q < MAXIT; ++q) {
       const int it = threadIdx.x + q * THREADS;
       if (ITEMS % THREADS == 0 || it < ITEMS) {
-        const int i = it >> 2, f = it & 3;
+        const int f = it / NR, i = it - f * NR;
+        const double2* FN = Fs + f * LS;
+        const double2* FS = Fs + (4 + f) * LS;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int k = i + r * NR;
           const bool lo = k <= T, hi = k >= N - T;
           double2 xn = make_double2(0.0, 0.0), xs = xn;
           if (lo || hi) {
-            const double2* F = Fs + (lo ? k : N - k) * 8;
-            xn = F[f * 2];
-            xs = F[f * 2 + 1];
+            const int mm = lo ? k : N - k;
+            xn = FN[mm];
+            xs = FS[mm];
           }
           if (k == 0) xn.y = xs.y = 0.0;
           v[q][r] = lo ? make_double2(xn.x - xs.y, xn.y + xs.x)
@@ -291,24 +430,26 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
     for (int q = 0; q < MAXIT; ++q) {
       const int it = threadIdx.x + q * THREADS;
       if (ITEMS % THREADS == 0 || it < ITEMS) {
-        const int i = it >> 2, f = it & 3;
+        const int f = it / NR, i = it - f * NR;
         double2* X = Z + f * NP;
 #pragma unroll
-        for (int r = 0; r < R; ++r) X[pz(i * R + r)] = v[q][r];
+        for (int r = 0; r < R; ++r) X[pzv(i * R + r, SHO)] = v[q][r];
       }
     }
     __syncthreads();
   }
   RT(1)
-  inverse_mid<N, 1, inv_radix<N>(0), 4, THREADS>(Z, tw);
+  inverse_mid<N, 1, THREADS>(Z, tw);
   RT(2)
 
   // ---- fused: last inverse pass (radix 3, P = N/3), grid products, first
   //      forward pass (radix 3, P = 1) on the points i + r N/3
   {
     constexpr int N3 = N / 3;
-    static_assert(inv_prefix<N, NS - 1>() == N3, "inverse plan must end with radix 3");
+    constexpr int SHI = gen_shift<N>(NS - 2), SHO = gen_shift<N>(NS - 1);
+    static_assert(inv_prefix<N>(NS - 1) == N3, "inverse plan must end with radix 3");
     static_assert(inv_radix<N>(NS - 1) == 3, "inverse plan must end with radix 3");
+    const double2* twp = tw + tw_off_inv<N>(NS - 1);
     const double muj = mu[j];
     const double cor_n = two_omega * muj, cor_s = -two_omega * muj;
     const double ke_scale = 0.5 / ((1.0 - muj) * (1.0 + muj));
@@ -323,11 +464,11 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
         for (int f = 0; f < 4; ++f) {
           const double2* X = Z + f * NP;
 #pragma unroll
-          for (int r = 0; r < 3; ++r) g[f][r] = X[pz(i + r * N3)];
+          for (int r = 0; r < 3; ++r) g[f][r] = X[pzv(i + r * N3, SHI)];
           if (i) {  // twiddles exp(+2 pi i r i / N)
 #pragma unroll
             for (int r = 1; r < 3; ++r) {
-              double2 w = tw[r * i];
+              double2 w = twp[(r - 1) * N3 + i];
               w.y = -w.y;
               g[f][r] = cmul(g[f][r], w);
             }
@@ -358,13 +499,13 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
 #pragma unroll
         for (int o = 0; o < 5; ++o)
 #pragma unroll
-          for (int r = 0; r < 3; ++r) Z[o * NP + pz(3 * i + r)] = out[q][o][r];
+          for (int r = 0; r < 3; ++r) Z[o * NP + pzv(3 * i + r, SHO)] = out[q][o][r];
       }
     }
     __syncthreads();
   }
   RT(3)
-  forward_rest<N, 1, 3, 5, THREADS>(Z, tw);
+  forward_rest<N, 1, THREADS>(Z, tw);
   RT(4)
 
   const double ws = wsyn[j], wk = wke[j];
@@ -372,13 +513,14 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
   // analysis layout: [b][m][j][fold][slot]; thread (m, fold) writes the fold's
   // seven slots (112 contiguous bytes), the pair of folds a 224-byte record
   double2* outp = gan + ((size_t)b * L * J + j) * (kNumSlots * 2);
+  constexpr int SHL = gen_shift<N>(2 * NS - 2);
   for (int it = threadIdx.x; it < 2 * L; it += THREADS) {
     const int m = it >> 1, fold = it & 1;
     const double dm = (double)m;
     double2 v[5];
 #pragma unroll
     for (int o = 0; o < 5; ++o) {
-      const double2 zm = Z[o * NP + pz(m)], zc = Z[o * NP + pz(m == 0 ? 0 : N - m)];
+      const double2 zm = Z[o * NP + pzv(m, SHL)], zc = Z[o * NP + pzv(m == 0 ? 0 : N - m, SHL)];
       // X = FFT(north)/N, Y = FFT(south)/N; fold 0: S = X + Y, fold 1: A = X - Y
       const double2 X = make_double2(h * (zm.x + zc.x), h * (zm.y - zc.y));
       const double2 Y = make_double2(h * (zm.y + zc.y), -h * (zm.x - zc.x));
@@ -430,7 +572,22 @@ extern "C" int sdcsw_debug_rtimes(unsigned long long* host, int n) {
 }
 #endif
 
-size_t ring_smem_bytes(int nlon) { return (size_t)(5 * (nlon + nlon / 8) + nlon) * sizeof(double2); }
+size_t ring_smem_bytes(int nlon) {
+#define SDCSW_RING_SMEM(NV, TV) \
+  if (nlon == NV) return (size_t)(5 * padded<NV>() + tw_total<NV>()) * sizeof(double2);
+  SDCSW_RING_SIZES(SDCSW_RING_SMEM)
+#undef SDCSW_RING_SMEM
+  return 0;
+}
+
+// per-pass twiddle tables of the ring FFT plan for nlon, from w[k] = exp(-2 pi i k / nlon)
+bool ring_pass_twiddles(int nlon, const double2* w, std::vector<double2>& out) {
+#define SDCSW_RING_TW(NV, TV) \
+  if (nlon == NV) { build_pass_twiddles<NV>(w, out); return true; }
+  SDCSW_RING_SIZES(SDCSW_RING_TW)
+#undef SDCSW_RING_TW
+  return false;
+}
 
 static cudaError_t ring_impl(const Plan& p, const double2* fsyn, double2* gan, const int* m_part,
                              const int* m_k, int Lp, int nb, cudaStream_t s) {

@@ -31,6 +31,7 @@ int cuda_status(cudaError_t e, const char* where) {
 
 cudaError_t configure_ring(size_t smem);
 size_t ring_smem_bytes(int nlon);
+bool ring_pass_twiddles(int nlon, const double2* w, std::vector<double2>& out);
 bool ring_supported(int nlon);
 
 cudaError_t f_expl_prepped(const Plan& p, const Work& w, const double* xsyn, double2* fe, int nb,
@@ -224,6 +225,8 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   p.n_anal_work4 = (int)work4.size();
   p.ring_threads = 256;
   p.ring_smem = ring_smem_bytes(nlon);
+  std::vector<double2> twp;
+  ring_pass_twiddles(nlon, tw.data(), twp);
 
   const size_t tab = (size_t)p.rows * J;
   if ((e = upload(&p.ptab, ptab, tab, (size_t)16 * J)) != cudaSuccess ||
@@ -240,7 +243,7 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
       (e = upload(&p.mu, mu_north, (size_t)J)) != cudaSuccess ||
       (e = upload(&p.wsyn, wsyn.data(), wsyn.size())) != cudaSuccess ||
       (e = upload(&p.wke, wke.data(), wke.size())) != cudaSuccess ||
-      (e = upload(&p.twiddle, tw.data(), tw.size())) != cudaSuccess ||
+      (e = upload(&p.twiddle, twp.data(), twp.size())) != cudaSuccess ||
       (e = upload(&p.anal_work, work.data(), work.size())) != cudaSuccess ||
       (e = upload(&p.anal_work4, work4.data(), work4.size())) != cudaSuccess ||
       (e = cudaMalloc(&p.fsyn, (size_t)p.max_batch * J * p.L * 8 * sizeof(double2))) != cudaSuccess ||
