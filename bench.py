@@ -224,10 +224,12 @@ def time_stage(problem, stage, nb, reps=50):
     return e0.elapsed_time(e1) * 1e-3 / reps
 
 
-def stage_roofline(problem, c, members=1):
+def stage_roofline(problem, c, members=1, fused=False):
     """Per-stage time per simulated step; roofline of the dominant kernel.
 
-    The sweep launches carry nodes x members states, the init launch members."""
+    The sweep launches carry nodes x members states, the init launch members.
+    ``fused``: the step runs the analysis with the node-update epilogue
+    (transform stage 4), so that is the kernel timed for the analysis."""
     k = c["sweeps"]
     m = c["nodes"] * members
     one = members
@@ -238,7 +240,8 @@ def stage_roofline(problem, c, members=1):
     ring_bytes = lambda nb: (8 + 14) * 16.0 * j * ll * nb  # noqa: E731  read Fourier, write analysis data
     per_step = {}
     detail = {}
-    for stage, name in ((3, "legendre_synthesis"), (1, "ring_fft_products"), (2, "legendre_analysis")):
+    for stage, name in ((3, "legendre_synthesis"), (1, "ring_fft_products"),
+                        (4 if fused else 2, "legendre_analysis")):
         t1 = time_stage(problem, stage, one)
         tm = time_stage(problem, stage, m)
         per_step[name] = t1 + (k - 1) * tm
@@ -414,7 +417,9 @@ def run_device(args):
         e1.synchronize()
         serial_rate = nsteps / (e0.elapsed_time(e1) * 1e-3)
         sst.close()
-        roof, stage_us, stage_detail = stage_roofline(problem, c, members)
+        fused = (not ensemble and world == 1
+                 and launches_per_sim_step == 3 * k_sw)  # node updates in the analysis epilogue
+        roof, stage_us, stage_detail = stage_roofline(problem, c, members, fused)
         cpu = None
         if world == 1 and not args.no_cpu and not ensemble:
             r, cores, wall = cpu_oracle_rate(args.config, args.cpu_sample)

@@ -146,9 +146,12 @@ int sdcsw_stepper_launches_per_step(sdcsw_stepper* st, int* n);
 /* One stage of f_E on the plan's internal workspaces, for per-kernel timing
  * and stage-level parity tests: stage 0 = Legendre synthesis (u -> Fourier
  * workspace), 1 = ring FFT + products (Fourier -> analysis workspace),
- * 2 = Legendre analysis (analysis workspace -> out).  `in`/`out` are
- * ignored where the stage reads/writes a workspace.  sdcsw_f_expl is the
- * three stages back to back. */
+ * 2 = Legendre analysis (analysis workspace -> out), 3 = synthesis from the
+ * operand stage 0 prepared, 4 = analysis with the dSDC step's fused
+ * node-update epilogue (nb nodes; in = u0, out = their f_I, updated in place;
+ * zero coefficients - for timing the kernel the step runs).  `in`/`out` are
+ * ignored where the stage reads/writes a workspace.  sdcsw_f_expl is stages
+ * 0, 1, 2 back to back. */
 int sdcsw_transform_stage(sdcsw_plan* plan, int stage, const double* in, double* out, int nb,
                           void* stream);
 

@@ -210,6 +210,8 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   // in flight), large ones give each warp its own row tile (B reuse via L1)
   p.anal_wj = T < 200 ? 1 : (T < 400 ? 2 : 4);
   p.synth_wj = T < 200 ? 1 : (T < 400 ? 2 : 4);
+  if (const char* env = getenv("SDCSW_ANAL_WJ")) p.anal_wj = atoi(env);
+  if (const char* env = getenv("SDCSW_SYNTH_WJ")) p.synth_wj = atoi(env);
   while ((J / kRowsPerWarp) % p.synth_wj) p.synth_wj /= 2;
   for (int m = 0; m <= T; ++m) {
     const int rows = rowoff[m + 1] - rowoff[m];
@@ -400,7 +402,23 @@ int sdcsw_transform_stage(sdcsw_plan* h, int stage, const double* in, double* ou
     case 3: e = launch_synthesis(h->p, plan_work(h->p), h->p.xsyn, nb, s, nullptr); break;
     case 1: e = launch_ring(h->p, plan_work(h->p), nb, s); break;
     case 2: e = launch_analysis(h->p, plan_work(h->p), (double2*)out, nb, s); break;
-    default: set_error("sdcsw_transform_stage: stage must be 0..3"); return SDCSW_ERR_PARAM;
+    case 4: {  // analysis with the fused node-update epilogue, as in the dSDC step (nb nodes)
+      if (!fuse_supported(h->p, nb)) {
+        set_error("sdcsw_transform_stage: no fused analysis for this plan / batch");
+        return SDCSW_ERR_PARAM;
+      }
+      FuseArgs fz{};
+      fz.mode = 1;
+      fz.M = nb;
+      fz.u0 = in;
+      fz.fi = out;
+      fz.xsyn = h->p.xsyn;
+      fz.phibar = h->p.phibar;
+      h->p.xsyn_nb = -1;  // the operand layout is overwritten
+      e = launch_analysis_fused(h->p, plan_work(h->p), nb, fz, s);
+      break;
+    }
+    default: set_error("sdcsw_transform_stage: stage must be 0..4"); return SDCSW_ERR_PARAM;
   }
   return cuda_status(e, "sdcsw_transform_stage");
 }

@@ -49,8 +49,8 @@ def full(path):
         if d.get("Metric Name") in WANT:
             per.setdefault(key, {})[WANT[d["Metric Name"]]] = d["Metric Value"] + (
                 " " + d["Metric Unit"] if d["Metric Name"] == "Duration" else "")
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--print-units", "base"],
+                         capture_output=True, text=True).stdout
     rr = list(csv.reader(raw.splitlines()))
     h2 = rr[0]
     cols = {n: i for i, n in enumerate(h2)}
@@ -72,11 +72,45 @@ def full(path):
         e = extra.get(key, {})
         dm = e.get("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "")
         out.append(f"| {key[0]} | `{key[1]}` | " + " | ".join(d.get(v, "") for v in WANT.values())
-                   + f" | {e.get('dram__bytes_read.sum', '')} | {e.get('dram__bytes_write.sum', '')} | {dm} |")
+                   + f" | {mb(e.get('dram__bytes_read.sum'))} | {mb(e.get('dram__bytes_write.sum'))} | {dm} |")
     return "\n".join(out)
 
 
+def mb(v):
+    try:
+        return f"{float(v.replace(',', '')) / 1e6:.3f}"
+    except (AttributeError, ValueError):
+        return ""
+
+
+STAGE = {"k_synthesis": "legendre_synthesis", "k_ring": "ring_fft_products",
+         "k_analysis": "legendre_analysis"}
+
+
+def traffic(path):
+    """{stage: dram read + write bytes of the largest captured launch of that kernel}."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--print-units", "base"],
+                         capture_output=True, text=True).stdout
+    rr = list(csv.reader(raw.splitlines()))
+    cols = {n: i for i, n in enumerate(rr[0])}
+    out = {}
+    for r in rr[2:]:
+        name = r[cols["Kernel Name"]].split("(")[0].split("<")[0].replace("void ", "").split("::")[-1]
+        for prefix, stage in STAGE.items():
+            if name.startswith(prefix):
+                b = sum(float(r[cols[k]].replace(",", "")) for k in ("dram__bytes_read.sum",
+                                                                      "dram__bytes_write.sum"))
+                out[stage] = max(out.get(stage, 0.0), b)
+    return out
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "--traffic":  # --traffic REPORT OUT.json
+        import json
+
+        with open(sys.argv[3], "w") as f:
+            json.dump(traffic(sys.argv[2]), f, indent=1)
+        sys.exit(0)
     for p in sys.argv[1:]:
         print(f"### {p}\n")
         print(launches(p) if p.endswith(".csv") else full(p))

@@ -1,0 +1,17 @@
+#!/bin/bash
+# GPU-box evidence pass: bench line (+ reference arm), ncu launch list of the
+# bench command, one ncu --set full capture of a steady-state step of CONFIG.
+# usage: bash tools/round_profile.sh TAG [CONFIG]
+set -u
+TAG=$1
+CFG=${2:-c1}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+python bench.py --config $CFG > $OUT/bench.json 2> $OUT/bench.err || { tail -20 $OUT/bench.err; exit 1; }
+python bench.py --config $CFG --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
+    python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu > $OUT/ncu_launch.log 2>&1
+python tools/exp/step_run.py $CFG 4 > /dev/null 2>&1 && \
+ncu --set full --import-source on --clock-control none -k regex:"k_synthesis|k_ring|k_analysis" \
+    --launch-skip 9 --launch-count 9 -o $OUT/prof python tools/exp/step_run.py $CFG 4 > $OUT/ncu_full.log 2>&1
+tail -c 600 $OUT/bench.json
