@@ -85,10 +85,12 @@ struct Plan {
 constexpr int kCoefCap = 4096;
 
 // Programmatic dependent launch: every kernel is launched with programmatic
-// stream serialization, releases its dependents at entry and waits for its
-// predecessor's memory (griddepcontrol.wait) before reading anything the
-// predecessor produced.  The next kernel's launch and prologue then overlap
-// the previous kernel's tail, in streams and in captured graphs alike.
+// stream serialization and waits for its predecessor's memory
+// (griddepcontrol.wait) before reading anything the predecessor produced;
+// constant plan data (tables, index lists, twiddles) is read before the wait.
+// Dependents are released at exit, except by the ring kernel, which releases
+// them before its output phase (measured).  The next kernel's launch and
+// prologue then overlap the previous kernel's tail, in streams and graphs alike.
 #ifdef __CUDACC__
 // (Releasing dependents at kernel entry measured slower than the implicit
 // release at exit, so SDCSW_PDL_ENTRY is empty unless SDCSW_EARLY_TRIGGER.)
@@ -98,6 +100,17 @@ constexpr int kCoefCap = 4096;
 #define SDCSW_PDL_ENTRY()
 #endif
 #define SDCSW_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+// explicit release at a kernel-chosen point (per-kernel experiments: 0 = exit)
+#define SDCSW_PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
+#ifndef SDCSW_TRIG_RING
+#define SDCSW_TRIG_RING 2  // measured: ring releases before its output phase
+#endif
+#ifndef SDCSW_TRIG_ANA
+#define SDCSW_TRIG_ANA 0
+#endif
+#ifndef SDCSW_TRIG_SYN
+#define SDCSW_TRIG_SYN 0
+#endif
 #endif
 extern bool g_pdl;  // runtime switch (SDCSW_PDL=0 disables)
 

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(32 * kWarps, SDCSW_SYN_MINB) k_synthesis(
     const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ,
     int NBC, const int* __restrict__ mlist, int Lp) {
   SDCSW_PDL_ENTRY();
-  SDCSW_PDL_WAIT();
+  if (SDCSW_TRIG_SYN == 1) SDCSW_PDL_TRIGGER();
   constexpr int NPAIR = (NB + 1) / 2;
   constexpr int NT = 2 * NPAIR;     // column tiles: (U,V) and (zeta,Phi) per pair
   constexpr int NACC = NT * 2 * 4;  // doubles per lane: tiles x row tiles x (E,O) x (re,im)
@@ -117,12 +117,13 @@ __global__ void __launch_bounds__(32 * kWarps, SDCSW_SYN_MINB) k_synthesis(
   const int jt = warp % WJ, ks = warp / WJ;
   const int j0 = (blockIdx.x * WJ + jt) * kRowsPerWarp;
   (void)T;
-  if (step_counter != nullptr && (blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0)
-    atomicAdd(step_counter, 1);
-
+  // constant plan data before the dependency wait (overlaps the producer's tail)
   const int r0m = rowoff[m];
   const int rows = rowoff[m + 1] - r0m;
   const int le = n_even[m];
+  SDCSW_PDL_WAIT();
+  if (step_counter != nullptr && (blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0)
+    atomicAdd(step_counter, 1);
   const double* P = ptab + (size_t)r0m * J + j0 + g;
   const double* H = htab + (size_t)r0m * J + j0 + g;
   const int rstride = nb * kXsyn;
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(32 * kWarps, SDCSW_SYN_MINB) k_synthesis(
         if (PF == 2) nx1 = nx2;
       }
     }
+    if (SDCSW_TRIG_SYN == 2) SDCSW_PDL_TRIGGER();
     // fixed-order tree reduction over the K-splits ((w0 + w2) + (w1 + w3));
     // lane-fastest layout, conflict-free
     bool owner = true;
@@ -329,7 +331,7 @@ __global__ void SDCSW_ANA_LB k_analysis(
     const double* __restrict__ lam, const int* __restrict__ work, double2* __restrict__ fe,
     int WJ, const FuseArgs fz, const double2* __restrict__ xscale, const int* __restrict__ idx_row) {
   SDCSW_PDL_ENTRY();
-  SDCSW_PDL_WAIT();
+  if (SDCSW_TRIG_ANA == 1) SDCSW_PDL_TRIGGER();
   constexpr int HU = 6 * NB;
   constexpr int TH = (HU + 7) / 8;
   constexpr int PC = 8 * NB;
@@ -389,12 +391,15 @@ __global__ void SDCSW_ANA_LB k_analysis(
     struct Frag {
       double aP0, aP1, aH0, aH1, bPs[NB], bPa[NB], bHs[TH], bHa[TH];
     };
-    auto fetch = [&](int s, Frag& f) {
+    auto fetchA = [&](int s, Frag& f) {
       const int k = 4 * s;
       f.aP0 = __ldg(P + k);
       f.aP1 = __ldg(P + k + 8 * (size_t)J);
       f.aH0 = __ldg(H + k);
       f.aH1 = __ldg(H + k + 8 * (size_t)J);
+    };
+    auto fetchB = [&](int s, Frag& f) {
+      const int k = 4 * s;
       const long long jrec = (long long)(k + t) * 28;
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
@@ -409,11 +414,15 @@ __global__ void SDCSW_ANA_LB k_analysis(
         f.bHa[c] = ok ? __ldg(gb + hbase[c] + jrec + 14 + hel[c]) : 0.0;
       }
     };
+    auto fetch = [&](int s, Frag& f) { fetchA(s, f); fetchB(s, f); };
     const int nsteps = J >> 2;
     int s = ks;
+    Frag cur, nx1, nx2;
+    // table fragments and plan data are constant: loaded before the dependency wait
+    if (s < nsteps) fetchA(s, cur);
+    SDCSW_PDL_WAIT();
     if (s < nsteps) {
-      Frag cur, nx1, nx2;
-      fetch(s, cur);
+      fetchB(s, cur);
       if (PF == 2) fetch(s + WK < nsteps ? s + WK : s, nx1);
       for (; s < nsteps; s += WK) {
         fetch(s + PF * WK < nsteps ? s + PF * WK : s, PF == 2 ? nx2 : nx1);
@@ -432,6 +441,7 @@ __global__ void SDCSW_ANA_LB k_analysis(
       }
     }
   }
+  if (SDCSW_TRIG_ANA == 2) SDCSW_PDL_TRIGGER();
   if (WK > 1) {  // lane-fastest layout: conflict-free shared-memory traffic
     double* d = red + warp * NACC * 32 + lane;
     int q = 0;

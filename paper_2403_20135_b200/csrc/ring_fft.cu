@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
                                                   const int* __restrict__ m_part,
                                                   const int* __restrict__ m_k, int Lp, int nbg) {
   SDCSW_PDL_ENTRY();
-  SDCSW_PDL_WAIT();
+  if (SDCSW_TRIG_RING == 1) SDCSW_PDL_TRIGGER();
   extern __shared__ double2 sm2[];
   constexpr int NP = padded<N>();
   constexpr int NS = RadixPlan<N>::n;
@@ -379,7 +379,10 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
   const int cta = blockIdx.y * gridDim.x + blockIdx.x;
 #endif
   RT(0)
+  // constant plan data before the dependency wait (overlaps the producer's tail)
   for (int k = threadIdx.x; k < TWN; k += THREADS) tw[k] = twg[k];
+  const double muj = mu[j], ws = wsyn[j], wk = wke[j];
+  SDCSW_PDL_WAIT();
 
   // ---- inverse pass 0 (P = 1, no twiddles) from the Fourier coefficients:
   //      Z_m = X_m + i Y_m, Z_{N-m} = conj(X_m) + i conj(Y_m).
@@ -450,7 +453,6 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
     static_assert(inv_prefix<N>(NS - 1) == N3, "inverse plan must end with radix 3");
     static_assert(inv_radix<N>(NS - 1) == 3, "inverse plan must end with radix 3");
     const double2* twp = tw + tw_off_inv<N>(NS - 1);
-    const double muj = mu[j];
     const double cor_n = two_omega * muj, cor_s = -two_omega * muj;
     const double ke_scale = 0.5 / ((1.0 - muj) * (1.0 + muj));
     constexpr int MAXIT = (N3 + THREADS - 1) / THREADS;
@@ -506,9 +508,9 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
   }
   RT(3)
   forward_rest<N, 1, THREADS>(Z, tw);
+  if (SDCSW_TRIG_RING == 2) SDCSW_PDL_TRIGGER();
   RT(4)
 
-  const double ws = wsyn[j], wk = wke[j];
   const double h = 0.5 / (double)N;
   // analysis layout: [b][m][j][fold][slot]; thread (m, fold) writes the fold's
   // seven slots (112 contiguous bytes), the pair of folds a 224-byte record

@@ -17,7 +17,8 @@ start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
 rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
 h = rows[0]
 ia, isrc, iss = h.index("Address"), h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
-data = [(k, r[isrc], int(r[iss] or 0)) for k, r in enumerate(rows[1:])]
+data = [(k, r[isrc], int(r[iss] or 0)) for k, r in enumerate(rows[1:])
+        if len(r) > iss and (r[iss] or "0").isdigit()]
 total = sum(d[2] for d in data)
 print(lines[0][:160])
 print("instructions", len(data), "samples", total)
