@@ -57,6 +57,25 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
                       const double* lam, sdcsw_plan** out);
 int sdcsw_plan_destroy(sdcsw_plan* plan);
 
+typedef struct {
+  int n_grid;                /* N: 8, 12, 16, 24, ..., 768, 1024 (2^k or 3*2^k) */
+  int max_batch;             /* largest nb any call on this plan will use */
+  double domain_length;      /* L (informational; the wavenumbers carry it) */
+  double mean_geopotential;  /* phibar > 0 */
+  double coriolis;           /* f0 */
+  double hyperviscosity;     /* nu >= 0 */
+} sdcsw_planar_config;
+
+/* Planar doubly periodic problem (PlanarShallowWater, problems/swe.py:57-138):
+ * state = three [N][N/2+1] rfft2 spectra (Phi', zeta, delta), C = N (N/2+1)
+ * coefficients per field.  kx [N] = 2 pi fftfreq, ky [N/2+1] = 2 pi rfftfreq,
+ * lam [C] = kx^2 + ky^2 (the reference's laplacian_symbol), host arrays built
+ * with the reference's expressions.  sdcsw_f_expl / f_impl / implicit_solve /
+ * sweep_nodes / final_node / the steppers accept the plan; the spherical-only
+ * entry points (transform stages, workspaces, spectral split) reject it. */
+int sdcsw_plan_create_planar(int device, const sdcsw_planar_config* cfg, const double* kx,
+                             const double* ky, const double* lam, sdcsw_plan** out);
+
 /* fe[b] = f_E(u[b]) for b < nb.  Replaces SplitProblem.f_expl (core.py:102-104)
  * and the planar _f_expl (problems/swe.py:174-196). */
 int sdcsw_f_expl(sdcsw_plan* plan, const double* u, double* fe, int nb, void* stream);

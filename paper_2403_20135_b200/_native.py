@@ -15,6 +15,7 @@ SDCSW_OK, SDCSW_ERR_PARAM, SDCSW_ERR_CUDA, SDCSW_ERR_STATE, SDCSW_ERR_DIVERGED =
 
 EXPORTS = (
     "sdcsw_plan_create",
+    "sdcsw_plan_create_planar",
     "sdcsw_plan_destroy",
     "sdcsw_f_expl",
     "sdcsw_f_impl",
@@ -55,6 +56,17 @@ class Config(ctypes.Structure):
     ]
 
 
+class PlanarConfig(ctypes.Structure):
+    _fields_ = [
+        ("n_grid", ctypes.c_int),
+        ("max_batch", ctypes.c_int),
+        ("domain_length", ctypes.c_double),
+        ("mean_geopotential", ctypes.c_double),
+        ("coriolis", ctypes.c_double),
+        ("hyperviscosity", ctypes.c_double),
+    ]
+
+
 _LIB = None
 _p = ctypes.c_void_p
 _i = ctypes.c_int
@@ -65,6 +77,8 @@ _ip = ctypes.POINTER(ctypes.c_int)
 _SIGS = {
     "sdcsw_plan_create": [_i, ctypes.POINTER(Config), _dp, _dp, _dp, _dp, _ip, _ip, _ip, _dp,
                           ctypes.POINTER(_p)],
+    "sdcsw_plan_create_planar": [_i, ctypes.POINTER(PlanarConfig), _dp, _dp, _dp,
+                                 ctypes.POINTER(_p)],
     "sdcsw_plan_destroy": [_p],
     "sdcsw_f_expl": [_p, _p, _p, _i, _p],
     "sdcsw_f_impl": [_p, _p, _p, _i, _p],

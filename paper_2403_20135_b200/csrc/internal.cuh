@@ -29,6 +29,7 @@ struct FftPlan {
 };
 
 struct Plan {
+  int kind;      // 0: spherical (Legendre + ring FFTs); 1: planar doubly periodic (2-D FFTs)
   int device;
   int T, nlat, nlon, J, C, L;  // L = T+1 (Fourier modes kept)
   int max_batch;
@@ -81,6 +82,15 @@ struct Plan {
   int* own_idx;     // own coefficient indices, ascending
   int n_own_idx;
   double2* fsyn_ext;  // part-major Fourier buffer [S][nb][J][Lp][4][2] (caller-owned)
+  // planar problem (kind 1): N x N grid, spectra [N (kx)][NH = N/2 + 1 (ky)],
+  // C = N * NH coefficients per field (lam = k^2 = laplacian symbol)
+  int pn, pnh;
+  double pf0, pnu;     // Coriolis parameter f0, hyperviscosity nu
+  double* pkx;         // [N] x wavenumbers (2 pi fftfreq)
+  double* pky;         // [NH] y wavenumbers (2 pi rfftfreq)
+  double2* ptw;        // [N] exp(-2 pi i k / N)
+  double2* pw1;        // [max_batch][4][N][NH] (U, V, zeta, Phi') after the column inverse FFTs
+  double2* pw2;        // [max_batch][5][N][NH] row spectra of the five grid products
 };
 constexpr int kCoefCap = 4096;
 
@@ -206,7 +216,7 @@ struct FuseArgs {
   double cf[kFuseMaxNodes * (kFuseMaxNodes + 4)];  // mode 1: [M][M+4]; mode 2: [M+4]
 };
 inline bool fuse_supported(const Plan& p, int M) {
-  return !p.tma_ok && p.own_idx == nullptr && M >= 1 && M <= kFuseMaxNodes;
+  return p.kind == 0 && !p.tma_ok && p.own_idx == nullptr && M >= 1 && M <= kFuseMaxNodes;
 }
 cudaError_t launch_analysis_fused(const Plan& p, const Work& w, int nb, const FuseArgs& fz,
                                   cudaStream_t s);
@@ -243,6 +253,13 @@ cudaError_t launch_axpy(long long n, const double* x, double w, const double* y,
 cudaError_t make_table_maps(Plan& p);
 bool launch_analysis_tma(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s,
                          cudaError_t* err);
+
+// planar f_E: column inverse FFTs -> row FFTs with the grid products -> column
+// forward FFTs and the tendency assembly (planar.cu)
+cudaError_t planar_f_expl(const Plan& p, const double2* u, double2* fe, int nb, cudaStream_t s,
+                          int* step_counter);
+bool planar_supported(int n);
+cudaError_t configure_planar(int n);
 
 // f_E = (prep) -> synthesis -> ring -> analysis; f_expl_prepped starts from an
 // xsyn operand a producer kernel already wrote

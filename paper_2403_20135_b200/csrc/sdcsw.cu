@@ -300,11 +300,78 @@ int sdcsw_plan_destroy(sdcsw_plan* h) {
     if (q) cudaFree(q);
   void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
                   p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev,
-                  p.xscale, p.idx_row, p.xsyn, p.anal_work4};
+                  p.xscale, p.idx_row, p.xsyn, p.anal_work4, p.pkx, p.pky, p.ptw, p.pw1, p.pw2};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   h->alive = false;
   delete h;
+  return SDCSW_OK;
+}
+
+int sdcsw_plan_create_planar(int device, const sdcsw_planar_config* cfg, const double* kx,
+                             const double* ky, const double* lam, sdcsw_plan** out) {
+  if (!cfg || !out || !kx || !ky || !lam) {
+    set_error("sdcsw_plan_create_planar: null argument");
+    return SDCSW_ERR_PARAM;
+  }
+  const int n = cfg->n_grid;
+  if (!planar_supported(n) || cfg->max_batch < 1 || !(cfg->mean_geopotential > 0.0) ||
+      cfg->hyperviscosity < 0.0) {
+    set_error("sdcsw_plan_create_planar: n_grid must be 8, 12, 16, 24, ..., 768 or 1024 "
+              "(2^k or 3*2^k), max_batch >= 1, mean_geopotential > 0, hyperviscosity >= 0");
+    return SDCSW_ERR_PARAM;
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+  sdcsw_plan* h = new (std::nothrow) sdcsw_plan();
+  if (!h) {
+    set_error("out of host memory");
+    return SDCSW_ERR_PARAM;
+  }
+  std::memset(&h->p, 0, sizeof(Plan));
+  Plan& p = h->p;
+  p.kind = 1;
+  p.device = device;
+  p.pn = n;
+  p.pnh = n / 2 + 1;
+  p.C = n * p.pnh;
+  p.max_batch = cfg->max_batch;
+  p.phibar = cfg->mean_geopotential;
+  p.pf0 = cfg->coriolis;
+  p.pnu = cfg->hyperviscosity;
+  p.split_S = 1;
+  p.xsyn_nb = -1;
+  std::vector<double2> tw(n);
+  for (int k = 0; k < n; ++k) {
+    const long double a = -2.0L * 3.14159265358979323846264338327950288L * k / n;
+    tw[k] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  const size_t wbytes = (size_t)p.max_batch * p.C * sizeof(double2);
+  if ((e = upload(&p.pkx, kx, (size_t)n)) != cudaSuccess ||
+      (e = upload(&p.pky, ky, (size_t)p.pnh)) != cudaSuccess ||
+      (e = upload(&p.lam, lam, (size_t)p.C)) != cudaSuccess ||
+      (e = upload(&p.ptw, tw.data(), tw.size())) != cudaSuccess ||
+      (e = cudaMalloc(&p.pw1, 4 * wbytes)) != cudaSuccess ||
+      (e = cudaMalloc(&p.pw2, 5 * wbytes)) != cudaSuccess ||
+      (e = cudaMalloc(&p.coef_dev, kCoefCap * sizeof(double))) != cudaSuccess ||
+      (e = configure_planar(n)) != cudaSuccess) {
+    const int st = cuda_status(e, "sdcsw_plan_create_planar");
+    for (void* q : {(void*)p.pkx, (void*)p.pky, (void*)p.lam, (void*)p.ptw, (void*)p.pw1,
+                    (void*)p.pw2, (void*)p.coef_dev})
+      if (q) cudaFree(q);
+    delete h;
+    return st;
+  }
+  h->alive = true;
+  *out = h;
+  return SDCSW_OK;
+}
+
+static int check_spherical(sdcsw_plan* h, const char* where) {
+  if (h->p.kind != 0) {
+    set_error(std::string(where) + ": spherical plans only");
+    return SDCSW_ERR_STATE;
+  }
   return SDCSW_OK;
 }
 
@@ -328,6 +395,10 @@ int sdcsw_f_expl(sdcsw_plan* h, const double* u, double* fe, int nb, void* strea
     return SDCSW_ERR_STATE;
   }
   if (nb == 0) return SDCSW_OK;
+  if (h->p.kind == 1)
+    return cuda_status(planar_f_expl(h->p, (const double2*)u, (double2*)fe, nb,
+                                     (cudaStream_t)stream, nullptr),
+                       "sdcsw_f_expl");
   return cuda_status(f_expl(h->p, (const double2*)u, (double2*)fe, nb, (cudaStream_t)stream, nullptr),
                      "sdcsw_f_expl");
 }
@@ -387,6 +458,7 @@ int sdcsw_transform_stage(sdcsw_plan* h, int stage, const double* in, double* ou
                           void* stream) {
   int st = check_plan(h, nb, "sdcsw_transform_stage");
   if (st) return st;
+  if ((st = check_spherical(h, "sdcsw_transform_stage"))) return st;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
   switch (stage) {
@@ -426,6 +498,7 @@ int sdcsw_transform_stage(sdcsw_plan* h, int stage, const double* in, double* ou
 int sdcsw_workspace(sdcsw_plan* h, int which, void** ptr, long long* bytes) {
   int st = check_plan(h, 1, "sdcsw_workspace");
   if (st) return st;
+  if ((st = check_spherical(h, "sdcsw_workspace"))) return st;
   if (!ptr || !bytes || which < 0 || which > 1) return SDCSW_ERR_PARAM;
   const Plan& p = h->p;
   const long long per = (long long)p.max_batch * p.J * p.L * 2 * sizeof(double2);
@@ -437,6 +510,7 @@ int sdcsw_workspace(sdcsw_plan* h, int which, void** ptr, long long* bytes) {
 int sdcsw_plan_set_split(sdcsw_plan* h, int S, int sp, void* fourier, long long bytes) {
   int st = check_plan(h, 1, "sdcsw_plan_set_split");
   if (st) return st;
+  if ((st = check_spherical(h, "sdcsw_plan_set_split"))) return st;
   Plan& p = h->p;
   if (S < 1 || sp < 0 || sp >= S || S > p.L) {
     set_error("sdcsw_plan_set_split: need 1 <= S <= T+1 and 0 <= sp < S");
@@ -502,6 +576,7 @@ int sdcsw_plan_set_split(sdcsw_plan* h, int S, int sp, void* fourier, long long 
 int sdcsw_split_info(sdcsw_plan* h, int* Lp, int* n_own_m, int* n_own_idx) {
   int st = check_plan(h, 1, "sdcsw_split_info");
   if (st) return st;
+  if ((st = check_spherical(h, "sdcsw_split_info"))) return st;
   if (Lp) *Lp = h->p.split_S > 1 ? h->p.Lp : 0;
   if (n_own_m) *n_own_m = h->p.n_own_m;
   if (n_own_idx) *n_own_idx = h->p.split_S > 1 ? h->p.n_own_idx : h->p.C;
@@ -511,6 +586,7 @@ int sdcsw_split_info(sdcsw_plan* h, int* Lp, int* n_own_m, int* n_own_idx) {
 int sdcsw_split_f_expl_begin(sdcsw_plan* h, const double* u, int nb, void* stream) {
   int st = check_plan(h, nb, "sdcsw_split_f_expl_begin");
   if (st) return st;
+  if ((st = check_spherical(h, "sdcsw_split_f_expl_begin"))) return st;
   Plan& p = h->p;
   if (p.split_S < 2) {
     set_error("sdcsw_split_f_expl_begin: plan is not split");
@@ -530,6 +606,7 @@ int sdcsw_split_f_expl_begin(sdcsw_plan* h, const double* u, int nb, void* strea
 int sdcsw_split_f_expl_end(sdcsw_plan* h, double* fe, int nb, void* stream) {
   int st = check_plan(h, nb, "sdcsw_split_f_expl_end");
   if (st) return st;
+  if ((st = check_spherical(h, "sdcsw_split_f_expl_end"))) return st;
   const Plan& p = h->p;
   if (p.split_S < 2) {
     set_error("sdcsw_split_f_expl_end: plan is not split");
@@ -606,7 +683,10 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
   // (or the run's prep) wrote into xsyn1
   const int E = st->members;
   if (marks) cudaEventRecord(marks[0], s);
-  cudaError_t e = f_expl_prepped(p, plan_work(p), st->xsyn1, st->fe0, E, s, counter, p.fe_chunk);
+  const bool planar = p.kind == 1;  // planar: f_E reads the node states, no operand records
+  cudaError_t e = planar ? planar_f_expl(p, u, st->fe0, E, s, counter)
+                         : f_expl_prepped(p, plan_work(p), st->xsyn1, st->fe0, E, s, counter,
+                                          p.fe_chunk);
   if (e != cudaSuccess) return e;
   if (marks) cudaEventRecord(marks[1], s);
   if (st->mode == 0) {
@@ -637,13 +717,14 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
       for (int g = 0; g < G; ++g) {
         const int lo = g * M / G, hi = (g + 1) * M / G, cnt = hi - lo;
         cudaStream_t sg = (G > 1 && !seq) ? st->side[g] : s;
-        double* xs = st->xsynM + (size_t)lo * E * p.rows * kXsyn;
+        double* xs = planar ? nullptr : st->xsynM + (size_t)lo * E * p.rows * kXsyn;
         e = launch_sweep_nodes(p, M, lo, cnt, coef, u, fe_cur, first ? 0 : 1,
                                fi_cur, first ? 0 : 1, first, st->ustage + lo * S,
                                fi_new + lo * S, xs, sg, E, first ? 1 : mS, mS, p.fe_chunk);
         if (e != cudaSuccess) return e;
-        e = f_expl_prepped(p, plan_work(p, lo), xs, fe_new + lo * S, cnt * E, sg, nullptr,
-                           p.fe_chunk);
+        e = planar ? planar_f_expl(p, st->ustage + lo * S, fe_new + lo * S, cnt * E, sg, nullptr)
+                   : f_expl_prepped(p, plan_work(p, lo), xs, fe_new + lo * S, cnt * E, sg,
+                                    nullptr, p.fe_chunk);
         if (e != cudaSuccess) return e;
       }
       if (G > 1 && !seq) {
@@ -657,16 +738,17 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
       fe_cur = fe_new;
     }
     const bool first = K == 1;
+    double* xs1 = planar ? nullptr : st->xsyn1;
     if (marks) {
       e = launch_final_node(p, M, st->coef.data() + (size_t)(K - 1) * cstride, u,
                             fe_cur, first ? 0 : 1, fi_cur, first ? 0 : 1,
-                            first, u, diverged, counter, st->xsyn1, s, E, first ? 1 : mS, mS);
+                            first, u, diverged, counter, xs1, s, E, first ? 1 : mS, mS);
       cudaEventRecord(marks[K + 1], s);
       return e;
     }
     return launch_final_node(p, M, st->coef.data() + (size_t)(K - 1) * cstride, u,
                              fe_cur, first ? 0 : 1, fi_cur, first ? 0 : 1,
-                             first, u, diverged, counter, st->xsyn1, s, E, first ? 1 : mS, mS);
+                             first, u, diverged, counter, xs1, s, E, first ? 1 : mS, mS);
   }
   // serial SDC: old/new tendency buffers alternate between sweeps
   const double* W = st->coef.data();
@@ -687,9 +769,10 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
       e = launch_serial_node(p, M, m, sc + 3 * m, st->quad + m * S, st->corr, u,
                              old_fi + old_stride * m * S, first, st->ustage, last ? u : nullptr,
                              nfi + m * S, last ? diverged : nullptr, last ? counter : nullptr,
-                             st->xsyn1, s);
+                             planar ? nullptr : st->xsyn1, s);
       if (e != cudaSuccess) return e;
-      e = f_expl_prepped(p, plan_work(p), st->xsyn1, nfe + m * S, 1, s, nullptr);
+      e = planar ? planar_f_expl(p, st->ustage, nfe + m * S, 1, s, nullptr)
+                 : f_expl_prepped(p, plan_work(p), st->xsyn1, nfe + m * S, 1, s, nullptr);
       if (e != cudaSuccess) return e;
       if (m + 1 < M) {
         e = launch_serial_update(p, m, we[m], wi[m], st->corr, nfe + m * S,
@@ -786,13 +869,13 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   s->fuse = mode == 0 && E == 1 && fuse_supported(p, M);
   if (const char* env = getenv("SDCSW_FUSE")) s->fuse = s->fuse && atoi(env) != 0;
   if (mode == 0) {
-    s->chains = (p.T < 200 && E == 1 && !s->fuse) ? (M < 2 ? M : 2) : 1;
+    s->chains = (p.kind == 0 && p.T < 200 && E == 1 && !s->fuse) ? (M < 2 ? M : 2) : 1;
     if (const char* env = getenv("SDCSW_CHAINS")) s->chains = atoi(env);
     if (s->chains < 1) s->chains = 1;
     if (s->chains > M) s->chains = M;
-    if (E > 1) s->chains = 1;
+    if (E > 1 || p.kind == 1) s->chains = 1;  // planar f_E shares one workspace
   }
-  s->ncreated = mode == 0 && E == 1 ? M : 0;  // side streams for up to M chains
+  s->ncreated = mode == 0 && E == 1 && p.kind == 0 ? M : 0;  // side streams for up to M chains
   if (s->ncreated > 1) {
     cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
     for (int g = 0; g < s->ncreated; ++g) {
@@ -856,9 +939,11 @@ int sdcsw_stepper_run(sdcsw_stepper* s, double* u, int n_steps, int use_graph, v
   if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
   if (n_steps == 0) return SDCSW_OK;
   // the caller may have changed u since the last step: rebuild its synthesis operand
-  e = launch_synth_prep(s->plan->p, (const double2*)u, s->members, s->xsyn1, cs,
-                        s->plan->p.fe_chunk);
-  if (e != cudaSuccess) return cuda_status(e, "sdcsw_stepper_run prep");
+  if (s->plan->p.kind == 0) {
+    e = launch_synth_prep(s->plan->p, (const double2*)u, s->members, s->xsyn1, cs,
+                          s->plan->p.fe_chunk);
+    if (e != cudaSuccess) return cuda_status(e, "sdcsw_stepper_run prep");
+  }
   if (!use_graph) {
     for (int i = 0; i < n_steps; ++i) {
       e = enqueue_step(s, (double2*)u, cs);
@@ -915,7 +1000,9 @@ int sdcsw_stepper_profile(sdcsw_stepper* s, double* u, double* stage_ms, int n, 
     for (int i = 0; i < s->K + 2; ++i) cudaEventCreate(&s->prof[i]);
     s->prof_ready = true;
   }
-  e = launch_synth_prep(s->plan->p, (const double2*)u, s->members, s->xsyn1, cs, s->plan->p.fe_chunk);
+  if (s->plan->p.kind == 0)
+    e = launch_synth_prep(s->plan->p, (const double2*)u, s->members, s->xsyn1, cs,
+                          s->plan->p.fe_chunk);
   if (e == cudaSuccess) e = enqueue_step(s, (double2*)u, cs, s->prof);
   if (e != cudaSuccess) return cuda_status(e, "sdcsw_stepper_profile");
   e = cudaEventSynchronize(s->prof[s->mode == 0 ? s->K + 1 : s->K]);

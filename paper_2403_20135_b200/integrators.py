@@ -137,14 +137,23 @@ def _solve_scalars(alpha, phibar):
     return alpha * phibar, alpha * alpha * phibar
 
 
-def diagonal_step_coefficients(cfg, dt, phibar):
+def _scalars_for(phibar, solve_scalars):
+    if solve_scalars is None:
+        return lambda alpha: _solve_scalars(alpha, phibar)
+    return solve_scalars
+
+
+def diagonal_step_coefficients(cfg, dt, phibar, solve_scalars=None):
     """Flattened per-sweep node coefficients for the device stepper.
 
     Sweep k (1..K-1), node m: ``dt * q[m, j]`` for all j (``integrators.py:273-276``),
     ``dt * diag[m]`` (``:276``), then the solve scalars of ``alpha = dt * diag[m]``
     (``:237``).  The final block is row M of the quadrature and
-    ``diagonal_coefficients(..., K)`` (``:291-303``).
+    ``diagonal_coefficients(..., K)`` (``:291-303``).  ``solve_scalars(alpha)``
+    gives (alpha Phibar, alpha^2 Phibar) as the problem's own solve forms them
+    (default ``alpha * alpha * phibar``).
     """
+    scalars = _scalars_for(phibar, solve_scalars)
     table = cfg.table
     m_count = table.n_nodes
     q = table.q_matrix
@@ -156,19 +165,20 @@ def diagonal_step_coefficients(cfg, dt, phibar):
             out.extend(dt * q[m, j] for j in range(m_count))
             out.append(dt * diag[m])
             out.append(alpha)
-            out.extend(_solve_scalars(alpha, phibar))
+            out.extend(scalars(alpha))
     diag = diagonal_coefficients(cfg.preconditioner, table, cfg.n_sweeps)
     last = m_count - 1
     alpha = dt * diag[last]
     out.extend(dt * q[last, j] for j in range(m_count))
     out.append(dt * diag[last])
     out.append(alpha)
-    out.extend(_solve_scalars(alpha, phibar))
+    out.extend(scalars(alpha))
     return np.array(out, dtype=np.float64)
 
 
-def serial_step_coefficients(cfg, dt, phibar):
+def serial_step_coefficients(cfg, dt, phibar, solve_scalars=None):
     """W = dt*q, dt*explicit weights, dt*dtau, solve scalars (``integrators.py:183-230``)."""
+    scalars = _scalars_for(phibar, solve_scalars)
     table = cfg.table
     m_count = table.n_nodes
     dtau = table.dtau
@@ -182,7 +192,7 @@ def serial_step_coefficients(cfg, dt, phibar):
     for m in range(m_count):
         alpha = dt * dtau[m]
         out.append(alpha)
-        out.extend(_solve_scalars(alpha, phibar))
+        out.extend(scalars(alpha))
     return np.array(out, dtype=np.float64)
 
 
@@ -201,10 +211,11 @@ class DeviceStepper:
             raise ParameterError("ensembles (members > 1) are supported for diagonal SDC only")
         self.n_nodes = cfg.table.n_nodes
         self.n_sweeps = cfg.n_sweeps
+        scalars = getattr(problem, "solve_coefficients", None)
         if serial:
-            coef = serial_step_coefficients(cfg, dt, problem.mean_geopotential)
+            coef = serial_step_coefficients(cfg, dt, problem.mean_geopotential, scalars)
         else:
-            coef = diagonal_step_coefficients(cfg, dt, problem.mean_geopotential)
+            coef = diagonal_step_coefficients(cfg, dt, problem.mean_geopotential, scalars)
         self._coef = np.ascontiguousarray(coef)
         handle = ctypes.c_void_p()
         _native.check(

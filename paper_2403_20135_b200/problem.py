@@ -36,82 +36,13 @@ from .sphere import (
 )
 
 
-class SphericalShallowWater(SplitProblem):
-    """Rotating shallow water on the sphere, T-truncated spherical harmonics, on one B200.
+class DeviceProblem(SplitProblem):
+    """Plumbing shared by the CUDA problems: the plan handle, device-resident
+    operations on torch complex128 tensors, and the numpy ``SplitProblem``
+    contract on top of them (one C-ABI call per evaluation, no CPU fallback).
 
-    Parameters
-    ----------
-    trunc : int
-        Triangular truncation T.
-    nlat, nlon : int, optional
-        Gaussian grid; defaults to the BASELINE grids (T63 192x96 ... T511 1536x768).
-    device : int
-        CUDA device ordinal.
-    max_batch : int
-        Largest number of states one batched call may carry (nodes x members).
-    """
-
-    def __init__(self, trunc, nlat=None, nlon=None, radius=EARTH_RADIUS, gravity=GRAVITY,
-                 omega=OMEGA, mean_depth=MEAN_DEPTH, device=0, max_batch=8):
-        super().__init__()
-        import torch
-
-        base = grid_for(trunc)
-        self.grid = SphereGrid(
-            trunc=trunc,
-            nlat=nlat or base.nlat,
-            nlon=nlon or base.nlon,
-            radius=float(radius),
-            gravity=float(gravity),
-            omega=float(omega),
-            mean_depth=float(mean_depth),
-        )
-        if max_batch < 1:
-            raise ParameterError("max_batch must be positive")
-        self._lib = _native.lib()
-        self.device = torch.device("cuda", device)
-        self.trunc = trunc
-        self.n_coef = self.grid.n_coef
-        self.state_size = self.grid.state_size
-        self.mean_geopotential = self.grid.mean_geopotential
-        self.phibar = self.mean_geopotential
-        self.max_batch = int(max_batch)
-        self.m_of, self.n_of = spectral_index(trunc)
-        self.lam = laplacian_eigenvalues(self.grid)
-
-        mu, w = gaussian_latitudes(self.grid.nlat)
-        half = self.grid.nlat // 2
-        self.mu, self.weights = mu, w
-        ptab, htab = legendre_tables(trunc, mu[:half])
-        tabs = pack_device_tables(self.grid, ptab, htab)
-        cfg = _native.Config(
-            trunc=trunc,
-            nlat=self.grid.nlat,
-            nlon=self.grid.nlon,
-            max_batch=self.max_batch,
-            radius=self.grid.radius,
-            omega=self.grid.omega,
-            phibar=self.mean_geopotential,
-        )
-        arrays = dict(
-            mu=np.ascontiguousarray(mu[:half]),
-            w=np.ascontiguousarray(w[:half]),
-            lam=np.ascontiguousarray(self.lam),
-            p=tabs.p, h=tabs.h, rowoff=tabs.rowoff, n_even=tabs.n_even4, row_n=tabs.row_n,
-        )
-        handle = ctypes.c_void_p()
-        with torch.cuda.device(self.device):
-            _native.check(
-                self._lib.sdcsw_plan_create(
-                    device, ctypes.byref(cfg), _native.dptr(arrays["mu"]), _native.dptr(arrays["w"]),
-                    _native.dptr(arrays["p"]), _native.dptr(arrays["h"]),
-                    _native.iptr(arrays["rowoff"]), _native.iptr(arrays["n_even"]),
-                    _native.iptr(arrays["row_n"]), _native.dptr(arrays["lam"]), ctypes.byref(handle),
-                ),
-                "sdcsw_plan_create",
-            )
-        self._plan = handle
-        self.table_bytes = 2 * tabs.p.nbytes
+    Subclasses set ``_lib``, ``_plan``, ``device``, ``state_size``,
+    ``max_batch`` and ``mean_geopotential``."""
 
     # -- lifecycle ------------------------------------------------------------
 
@@ -129,10 +60,6 @@ class SphericalShallowWater(SplitProblem):
     @property
     def handle(self):
         return self._plan
-
-    @property
-    def n_dof(self):
-        return self.grid.n_dof
 
     def stream(self):
         import torch
@@ -221,7 +148,90 @@ class SphericalShallowWater(SplitProblem):
         out = self.empty_states(1)
         return self._to_host(self.implicit_solve_device([alpha], b, out))
 
+
+
+class SphericalShallowWater(DeviceProblem):
+    """Rotating shallow water on the sphere, T-truncated spherical harmonics, on one B200.
+
+    Parameters
+    ----------
+    trunc : int
+        Triangular truncation T.
+    nlat, nlon : int, optional
+        Gaussian grid; defaults to the BASELINE grids (T63 192x96 ... T511 1536x768).
+    device : int
+        CUDA device ordinal.
+    max_batch : int
+        Largest number of states one batched call may carry (nodes x members).
+    """
+
+    def __init__(self, trunc, nlat=None, nlon=None, radius=EARTH_RADIUS, gravity=GRAVITY,
+                 omega=OMEGA, mean_depth=MEAN_DEPTH, device=0, max_batch=8):
+        super().__init__()
+        import torch
+
+        base = grid_for(trunc)
+        self.grid = SphereGrid(
+            trunc=trunc,
+            nlat=nlat or base.nlat,
+            nlon=nlon or base.nlon,
+            radius=float(radius),
+            gravity=float(gravity),
+            omega=float(omega),
+            mean_depth=float(mean_depth),
+        )
+        if max_batch < 1:
+            raise ParameterError("max_batch must be positive")
+        self._lib = _native.lib()
+        self.device = torch.device("cuda", device)
+        self.trunc = trunc
+        self.n_coef = self.grid.n_coef
+        self.state_size = self.grid.state_size
+        self.mean_geopotential = self.grid.mean_geopotential
+        self.phibar = self.mean_geopotential
+        self.max_batch = int(max_batch)
+        self.m_of, self.n_of = spectral_index(trunc)
+        self.lam = laplacian_eigenvalues(self.grid)
+
+        mu, w = gaussian_latitudes(self.grid.nlat)
+        half = self.grid.nlat // 2
+        self.mu, self.weights = mu, w
+        ptab, htab = legendre_tables(trunc, mu[:half])
+        tabs = pack_device_tables(self.grid, ptab, htab)
+        cfg = _native.Config(
+            trunc=trunc,
+            nlat=self.grid.nlat,
+            nlon=self.grid.nlon,
+            max_batch=self.max_batch,
+            radius=self.grid.radius,
+            omega=self.grid.omega,
+            phibar=self.mean_geopotential,
+        )
+        arrays = dict(
+            mu=np.ascontiguousarray(mu[:half]),
+            w=np.ascontiguousarray(w[:half]),
+            lam=np.ascontiguousarray(self.lam),
+            p=tabs.p, h=tabs.h, rowoff=tabs.rowoff, n_even=tabs.n_even4, row_n=tabs.row_n,
+        )
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _native.check(
+                self._lib.sdcsw_plan_create(
+                    device, ctypes.byref(cfg), _native.dptr(arrays["mu"]), _native.dptr(arrays["w"]),
+                    _native.dptr(arrays["p"]), _native.dptr(arrays["h"]),
+                    _native.iptr(arrays["rowoff"]), _native.iptr(arrays["n_even"]),
+                    _native.iptr(arrays["row_n"]), _native.dptr(arrays["lam"]), ctypes.byref(handle),
+                ),
+                "sdcsw_plan_create",
+            )
+        self._plan = handle
+        self.table_bytes = 2 * tabs.p.nbytes
+
     # -- layout helpers ----------------------------------------------------------
+
+    @property
+    def n_dof(self):
+        return self.grid.n_dof
 
     def spectral_views(self, state):
         c = self.n_coef
