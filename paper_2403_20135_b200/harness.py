@@ -6,14 +6,17 @@ the device:
 
 ``[problem]``  ``kind = "sphere-swe"``, ``trunc``, optional ``nlat``/``nlon``
                and physical constants, ``seed`` (seeded BASELINE spectrum,
-               SURVEY 8d) or ``initial = "<snapshot path>"``.
+               SURVEY 8d) or ``initial = "<snapshot path>"``; or the
+               reference's ``kind = "planar-swe"`` (``n_grid``, ``domain_length``,
+               ``mean_geopotential``, ``coriolis``, ``hyperviscosity``, optional
+               ``[problem.jet]``), run on the GPU planar problem.
 ``[stepper]``  ``scheme`` in {dsdc, sdc-serial, imex-o2, ab2-si}, ``n_nodes``,
                ``n_sweeps``, ``preconditioner`` (min-sr-flex | implicit-euler),
                ``dt``.
 ``[run]``      ``t_end``, optional ``checkpoint_interval`` (steps), ``reps``.
 ``[[speedup.candidate]]``  ``scheme`` and ``dt``.
 
-Reports: ``run_report.json`` + ``final_state.snap`` (:mod:`.snapshot`),
+Reports: ``run_report.json`` + ``final_state.snap`` (:mod:`.snapshot`; PSWSNAP1 for planar),
 ``speedup.json`` / ``speedup.csv``, ``perf_model.json`` (cost model fitted from
 CUDA-event stage timings, S_theory vs the measured sequential/parallel ratio).
 """
@@ -34,7 +37,7 @@ import numpy as np
 
 from .collocation import MAX_NODES, CollocationTable, DiagonalPreconditioner
 from .core import evaluation_counters, state_norm
-from .errors import ConfigError
+from .errors import ConfigError, ParameterError
 from .integrators import (
     DeviceStepper,
     DiagonalSdcStepper,
@@ -64,15 +67,40 @@ class ExperimentConfig:
 
         self.title = data.get("title", "")
         kind = get("problem", "kind", required=True)
-        if kind != "sphere-swe":
-            raise ConfigError(f"problem kind must be 'sphere-swe', got {kind!r}")
+        if kind not in ("sphere-swe", "planar-swe"):
+            raise ConfigError(f"problem kind must be 'sphere-swe' or 'planar-swe', got {kind!r}")
         self.problem_kind = kind
-        self.trunc = int(get("problem", "trunc", required=True))
-        if self.trunc < 1:
-            raise ConfigError("trunc must be positive")
-        self.problem_params = {k: get("problem", k) for k in
-                               ("nlat", "nlon", "radius", "gravity", "omega", "mean_depth")
-                               if get("problem", k) is not None}
+        self.jet_params = {}
+        if kind == "sphere-swe":
+            self.trunc = int(get("problem", "trunc", required=True))
+            if self.trunc < 1:
+                raise ConfigError("trunc must be positive")
+            self.problem_params = {k: get("problem", k) for k in
+                                   ("nlat", "nlon", "radius", "gravity", "omega", "mean_depth")
+                                   if get("problem", k) is not None}
+        else:  # the reference's planar kind and defaults (bench/config.py:178-233)
+            self.trunc = None
+            self.problem_params = {
+                "n_grid": int(get("problem", "n_grid", required=True)),
+                "domain_length": float(get("problem", "domain_length", 4.0e6)),
+                "mean_geopotential": float(get("problem", "mean_geopotential", 1.0e5)),
+                "coriolis": float(get("problem", "coriolis", 1.0e-4)),
+                "hyperviscosity": float(get("problem", "hyperviscosity", 0.0)),
+            }
+            if self.problem_params["n_grid"] < 1 or self.problem_params["domain_length"] <= 0 \
+                    or self.problem_params["mean_geopotential"] <= 0:
+                raise ConfigError("planar-swe needs positive n_grid, domain_length, mean_geopotential")
+            jet = data.get("problem", {}).get("jet", {})
+            if not isinstance(jet, dict):
+                raise ConfigError("[problem.jet] must be a table")
+            self.jet_params = {
+                "u_max": float(jet.get("u_max", 80.0)),
+                "perturbation_amplitude": float(jet.get("perturbation_amplitude", 1.0e-4)),
+                "perturbation_wavenumber": int(jet.get("perturbation_wavenumber", 3)),
+            }
+            for opt in ("y_center", "width"):
+                if opt in jet:
+                    self.jet_params[opt] = float(jet[opt])
         self.seed = int(get("problem", "seed", 0))
         self.initial = get("problem", "initial")
         self.scheme = get("stepper", "scheme", required=True)
@@ -120,6 +148,10 @@ def load_config(path):
 
 
 def build_problem(config):
+    if config.problem_kind == "planar-swe":
+        from .planar import PlanarShallowWater
+
+        return PlanarShallowWater(max_batch=max(8, config.n_nodes), **config.problem_params)
     from .problem import SphericalShallowWater
 
     return SphericalShallowWater(config.trunc, max_batch=max(8, config.n_nodes),
@@ -127,6 +159,10 @@ def build_problem(config):
 
 
 def build_initial_state(config, problem):
+    if config.problem_kind == "planar-swe":
+        from .planar import JetConfig, jet_initial_condition
+
+        return jet_initial_condition(problem, JetConfig(**config.jet_params))
     if config.initial:
         from .snapshot import read_snapshot
 
@@ -184,7 +220,7 @@ def _timed(problem, state, dt, n, stepper, interval=None):
 
 def run_single(config, out_dir):
     """One integration; writes run_report.json and final_state.snap."""
-    from .snapshot import write_snapshot
+    from .snapshot import write_planar_snapshot, write_snapshot
 
     os.makedirs(out_dir, exist_ok=True)
     problem = build_problem(config)
@@ -199,20 +235,24 @@ def run_single(config, out_dir):
     final = traj.states[-1]
     c = problem.n_coef
     walls = [r.wall_s for r in traj.reports]
+    planar = config.problem_kind == "planar-swe"
+    grid = [problem.n_grid] * 2 if planar else [problem.grid.nlon, problem.grid.nlat]
+    mean_phi = problem.mean_geopotential_anomaly(final) if planar else float(final[0].real)
     report = {
         "title": config.title, "problem": config.problem_kind, "scheme": traj.scheme,
-        "trunc": config.trunc, "grid": [problem.grid.nlon, problem.grid.nlat], "dt": config.dt,
+        "trunc": config.trunc, "grid": grid, "dt": config.dt,
         "n_steps": n, "t_end": config.t_end, "wall_s": wall,
         "steps_per_s": n / wall,
         "step_wall_s": {"min": min(walls), "median": float(np.median(walls)), "max": max(walls)},
         "counters": dict(zip(("n_f_expl", "n_f_impl", "n_solve"), evaluation_counters(problem))),
         "checkpoint_times": traj.times,
         "final": {"state_norm": state_norm(final),
-                  "mean_geopotential_anomaly": float(final[0].real),
+                  "mean_geopotential_anomaly": mean_phi,
                   "vorticity_norm": float(np.linalg.norm(final[c : 2 * c]))},
         "environment": environment_info(),
     }
-    write_snapshot(os.path.join(out_dir, "final_state.snap"), problem, final, config.t_end)
+    writer = write_planar_snapshot if planar else write_snapshot
+    writer(os.path.join(out_dir, "final_state.snap"), problem, final, config.t_end)
     with open(os.path.join(out_dir, "run_report.json"), "w") as f:
         json.dump(report, f, indent=2, sort_keys=True)
     problem.close()
@@ -280,11 +320,14 @@ def perf_model_report(config, out_dir, n_profile=6):
 
     t_seq = per_step()
     st.set_sequential(False)
-    st.set_chains(config.n_nodes)
-    t_par_chains = per_step()
-    st.set_chains(1)
+    try:  # concurrent node chains (spherical plans; the planar f_E shares one workspace)
+        st.set_chains(config.n_nodes)
+        t_par_chains = per_step()
+        st.set_chains(1)
+    except ParameterError:
+        t_par_chains = None
     t_par_batched = per_step()
-    t_par = min(t_par_chains, t_par_batched)
+    t_par = min(t for t in (t_par_chains, t_par_batched) if t is not None)
     rep = perf_report(model, s_measured=t_seq / t_par)
     rep.update({"t_step_sequential_s": t_seq, "t_step_parallel_chains_s": t_par_chains,
                 "t_step_parallel_batched_s": t_par_batched,

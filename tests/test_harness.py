@@ -89,3 +89,56 @@ def test_cli_run_speedup_perf_model(tmp_path):
     assert sp["rows"][1]["scheme"] == "sdc-serial"
     pm = json.load(open(out / "perf_model.json"))
     assert pm["M"] == 3 and pm["S_theory"] > 1 and pm["c_E"] > 0 and pm["S_measured"] > 0
+
+
+PLANAR = """
+[problem]
+kind = "planar-swe"
+n_grid = 24
+[problem.jet]
+perturbation_amplitude = 1e-4
+[stepper]
+scheme = "dsdc"
+n_nodes = 4
+n_sweeps = 4
+dt = 60.0
+[run]
+t_end = 300.0
+"""
+
+
+def test_planar_config_defaults(tmp_path, request):
+    """The reference's planar-swe kind and defaults (bench/config.py:178-233)."""
+    cfg = load_config(write(tmp_path, PLANAR))
+    assert cfg.problem_kind == "planar-swe" and cfg.n_steps() == 5
+    assert cfg.problem_params == dict(n_grid=24, domain_length=4.0e6, mean_geopotential=1.0e5,
+                                      coriolis=1.0e-4, hyperviscosity=0.0)
+    assert cfg.jet_params["perturbation_amplitude"] == 1e-4 and cfg.jet_params["u_max"] == 80.0
+    if os.path.isdir("/root/reference/pkg/src"):
+        parsdc = request.getfixturevalue("reference")
+        from parsdc.bench.config import load_config as ref_load
+
+        ref = ref_load(write(tmp_path, PLANAR, "r.toml"))
+        assert ref.problem_params == cfg.problem_params
+        assert {k: v for k, v in ref.jet_params.items()} == cfg.jet_params
+        del parsdc
+
+
+@pytest.mark.gpu
+def test_cli_planar_run_matches_reference_vectors(tmp_path):
+    import numpy as np
+
+    from oracle.planar_swe import relative_l2_fields
+    from paper_2403_20135_b200.snapshot import read_planar_snapshot
+
+    path = write(tmp_path, PLANAR)
+    out = tmp_path / "p"
+    r = subprocess.run([sys.executable, "-m", "paper_2403_20135_b200.cli", "run", "--config", path,
+                        "--out", str(out)], cwd=ROOT, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    rep = json.load(open(out / "run_report.json"))
+    assert rep["grid"] == [24, 24] and rep["counters"]["n_solve"] == 5 * 13
+    meta, state = read_planar_snapshot(str(out / "final_state.snap"))
+    assert meta["n_grid"] == 24 and meta["time"] == 300.0
+    gold = np.load(os.path.join(ROOT, "tests", "golden", "planar.npz"))
+    assert max(relative_l2_fields(state, gold["jet24_dsdc5"])) <= 1e-10
