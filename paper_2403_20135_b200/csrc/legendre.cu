@@ -19,6 +19,18 @@
 #ifndef SDCSW_EXP
 #define SDCSW_EXP 0
 #endif
+#if SDCSW_EXP == 5
+__device__ long long g_ph[8 * 4096];
+extern "C" int sdcsw_debug_phases(long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_ph, n * sizeof(long long));
+}
+#define PH(i) if (threadIdx.x == 0 && blockIdx.x < 4096 && blockIdx.y == 0) { g_ph[8 * blockIdx.x + (i)] = clock64(); \
+  if ((i) == 0 || (i) == 4) { unsigned long long gt; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt)); \
+    g_ph[8 * blockIdx.x + 5 + ((i) == 4)] = (long long)gt; } \
+  if ((i) == 0) { unsigned sm; asm volatile("mov.u32 %0, %smid;" : "=r"(sm)); g_ph[8 * blockIdx.x + 7] = sm; } }
+#else
+#define PH(i)
+#endif
 #if SDCSW_EXP == 3
 __device__ unsigned long long g_times[1 << 17];
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -91,11 +103,9 @@ template <int NB, int PF>
 #ifndef SDCSW_SYN_MINB
 #define SDCSW_SYN_MINB 4
 #endif
-#ifdef SDCSW_ANA_MIN
-#define SDCSW_ANA_LB __launch_bounds__(32 * kWarps, SDCSW_ANA_MIN)
-#else
-#define SDCSW_ANA_LB __launch_bounds__(32 * kWarps)
-#endif
+// NB <= 4: cap the registers at 128 so that 4 CTAs fit per SM - the c1 sweep
+// analysis (576 CTAs) then runs in one wave (measured)
+#define SDCSW_ANA_LB __launch_bounds__(32 * kWarps) __maxnreg__(NB == 1 && !FZ ? 64 : (NB <= 4 ? 128 : 255))
 __global__ void __launch_bounds__(32 * kWarps, SDCSW_SYN_MINB) k_synthesis(
     const double* __restrict__ xsyn, int nb, int T, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
@@ -331,6 +341,7 @@ __global__ void SDCSW_ANA_LB k_analysis(
     const double* __restrict__ lam, const int* __restrict__ work, double2* __restrict__ fe,
     int WJ, const FuseArgs fz, const double2* __restrict__ xscale, const int* __restrict__ idx_row) {
   SDCSW_PDL_ENTRY();
+  PH(0)
   if (SDCSW_TRIG_ANA == 1) SDCSW_PDL_TRIGGER();
   constexpr int HU = 6 * NB;
   constexpr int TH = (HU + 7) / 8;
@@ -398,20 +409,23 @@ __global__ void SDCSW_ANA_LB k_analysis(
       f.aH0 = __ldg(H + k);
       f.aH1 = __ldg(H + k + 8 * (size_t)J);
     };
+    // only the folds this warp's parity classes use are read (warp-uniform): a
+    // single-class tile (the common case) reads half of each record
+    const bool any_ev = ev0 || ev1, any_od = !ev0 || !ev1;
     auto fetchB = [&](int s, Frag& f) {
       const int k = 4 * s;
       const long long jrec = (long long)(k + t) * 28;
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
         const bool ok = pbase[c] >= 0;
-        f.bPs[c] = ok ? __ldg(gb + pbase[c] + jrec + pel[c]) : 0.0;
-        f.bPa[c] = ok ? __ldg(gb + pbase[c] + jrec + 14 + pel[c]) : 0.0;
+        f.bPs[c] = ok && any_ev ? __ldg(gb + pbase[c] + jrec + pel[c]) : 0.0;
+        f.bPa[c] = ok && any_od ? __ldg(gb + pbase[c] + jrec + 14 + pel[c]) : 0.0;
       }
 #pragma unroll
       for (int c = 0; c < TH; ++c) {
         const bool ok = hbase[c] >= 0;
-        f.bHs[c] = ok ? __ldg(gb + hbase[c] + jrec + hel[c]) : 0.0;
-        f.bHa[c] = ok ? __ldg(gb + hbase[c] + jrec + 14 + hel[c]) : 0.0;
+        f.bHs[c] = ok && any_od ? __ldg(gb + hbase[c] + jrec + hel[c]) : 0.0;
+        f.bHa[c] = ok && any_ev ? __ldg(gb + hbase[c] + jrec + 14 + hel[c]) : 0.0;
       }
     };
     auto fetch = [&](int s, Frag& f) { fetchA(s, f); fetchB(s, f); };
@@ -421,6 +435,7 @@ __global__ void SDCSW_ANA_LB k_analysis(
     // table fragments and plan data are constant: loaded before the dependency wait
     if (s < nsteps) fetchA(s, cur);
     SDCSW_PDL_WAIT();
+    PH(1)
     if (s < nsteps) {
       fetchB(s, cur);
       if (PF == 2) fetch(s + WK < nsteps ? s + WK : s, nx1);
@@ -442,6 +457,7 @@ __global__ void SDCSW_ANA_LB k_analysis(
     }
   }
   if (SDCSW_TRIG_ANA == 2) SDCSW_PDL_TRIGGER();
+  PH(2)
   if (WK > 1) {  // lane-fastest layout: conflict-free shared-memory traffic
     double* d = red + warp * NACC * 32 + lane;
     int q = 0;
@@ -462,6 +478,7 @@ __global__ void SDCSW_ANA_LB k_analysis(
     }
     __syncthreads();
   }
+  PH(3)
   if (ks != 0 || !live) return;
   double* o = red + rt * kRowsPerWarp * OS;
 #pragma unroll
@@ -475,6 +492,8 @@ __global__ void SDCSW_ANA_LB k_analysis(
   const int mo = moff[m];
   if constexpr (FZ) {
     fused_nodes<NB>(fz, o, rw, rows, row_n + r0m, mo, m, C, lam, xscale, idx_row, lane);
+    __syncwarp();
+    PH(4)
   } else {
   for (int it = lane; it < kRowsPerWarp * NB; it += 32) {
     const int rr = it % kRowsPerWarp, b = it / kRowsPerWarp;
