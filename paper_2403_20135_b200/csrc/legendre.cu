@@ -267,16 +267,13 @@ __global__ void __launch_bounds__(32 * kWarps, SDCSW_SYN_MINB) k_synthesis(
 // arithmetic), then the node update of k_sweep_nodes / k_final_node (nodes.cu)
 // in the same rounded order, so results are bit-identical to the unfused step.
 template <int NB>
-__device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o, int rw, int rows,
-                                            const int* __restrict__ row_n, int mo, int m, int C,
-                                            const double* __restrict__ lamv,
-                                            const double2* __restrict__ xscale,
-                                            const int* __restrict__ idx_row, int lane) {
+__device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o, int n, int mo,
+                                            int m, int C, const double* __restrict__ lamv,
+                                            const double2* __restrict__ xscale, double* stage,
+                                            int lane) {
   constexpr int OS = 8 * NB + 1;
   constexpr int MX = kFuseMaxNodes;
   const int rr = lane & 15, ri = lane >> 4;
-  if (rw + rr >= rows) return;
-  const int n = row_n[rw + rr];
   if (n < 0) return;
   const int idx = mo + n - m;
   const int C2 = 2 * C, e = 2 * idx + ri;
@@ -299,7 +296,6 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
   for (int j = 0; j < MX; ++j)
     if (j < M) fi[j] = fz.first ? fi0 : load_tri(fz.fi + j * S2, C2, e);
   if (fz.mode == 1) {
-    const int rec = idx_row[idx] * M;
     const double2 sc = xscale[idx];
 #pragma unroll
     for (int q = 0; q < MX; ++q) {
@@ -312,7 +308,7 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
       b = axmy_tri(b, c[M], fi[q]);
       const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], l);
       store_tri(fz.fi + q * S2, C2, e, f_impl_tri(u, fz.phibar, l));
-      write_xsyn_half(fz.xsyn + (size_t)(rec + q) * kXsyn, ri, u.phi, u.zeta, u.delta, sc);
+      write_xsyn_half(stage + (size_t)(rr * M + q) * kXsyn, ri, u.phi, u.zeta, u.delta, sc);
     }
   } else {
     const double* c = fz.cf;
@@ -328,8 +324,7 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
     store_tri(fz.u_out, C2, e, u);
     if (fz.diverged != nullptr && !finite_tri(u))
       atomicMin(fz.diverged, fz.step_counter ? *fz.step_counter : 1);
-    write_xsyn_half(fz.xsyn + (size_t)idx_row[idx] * kXsyn, ri, u.phi, u.zeta, u.delta,
-                    xscale[idx]);
+    write_xsyn_half(stage + (size_t)rr * kXsyn, ri, u.phi, u.zeta, u.delta, xscale[idx]);
   }
 }
 
@@ -396,6 +391,16 @@ __global__ void SDCSW_ANA_LB k_analysis(
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int c = 0; c < NB; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+
+  // fused epilogue: this lane's degree n (constant plan data, read ahead of the GEMM)
+  int fn = -1, fmo = 0;
+  if constexpr (FZ) {
+    const int rr = lane & 15;
+    if (live && ks == 0 && rw + rr < rows) {
+      fn = row_n[r0m + rw + rr];
+      fmo = moff[m];
+    }
+  }
 
   if (live) {
     // fragments of step s + WK are loaded before the DMMAs of step s
@@ -491,8 +496,20 @@ __global__ void SDCSW_ANA_LB k_analysis(
   __syncwarp();
   const int mo = moff[m];
   if constexpr (FZ) {
-    fused_nodes<NB>(fz, o, rw, rows, row_n + r0m, mo, m, C, lam, xscale, idx_row, lane);
+    // next synthesis operand: the tile's rows r0m + rw .. are consecutive operand
+    // records, staged in shared memory (zero for padding rows) and written out
+    // with coalesced 16-byte stores
+    __shared__ alignas(16) double xstage[2][kRowsPerWarp * kFuseMaxNodes * kXsyn];
+    double* stage = xstage[rt & 1];
+    const int per = (fz.mode == 1 ? fz.M : 1) * kXsyn;  // doubles per tile row
+    for (int i = lane; i < kRowsPerWarp * per; i += 32) stage[i] = 0.0;
     __syncwarp();
+    fused_nodes<NB>(fz, o, fn, fmo, m, C, lam, xscale, stage, lane);
+    __syncwarp();
+    const int nrow = rows - rw < kRowsPerWarp ? rows - rw : kRowsPerWarp;
+    double2* dst = reinterpret_cast<double2*>(fz.xsyn + (size_t)(r0m + rw) * per);
+    const double2* src = reinterpret_cast<const double2*>(stage);
+    for (int i = lane; i < nrow * per / 2; i += 32) dst[i] = src[i];
     PH(4)
   } else {
   for (int it = lane; it < kRowsPerWarp * NB; it += 32) {
