@@ -36,8 +36,14 @@ struct Plan {
   int rows;                    // packed table rows
   double radius, omega, phibar;
   // device constants
-  double* ptab;     // [rows][J]
+  double* ptab;     // [rows][J] (the TMA analysis streams this layout)
   double* htab;     // [rows][J]
+  // the same tables in DMMA-fragment order: one warp's A fragment (8 x 4 for
+  // the analysis, 4 x 8 for the synthesis) is 32 consecutive doubles
+  double* ptab_a;   // [rows/8][J/4][8 rows][4 lats]
+  double* htab_a;
+  double* ptab_s;   // [rows/4][J/8][4 rows][8 lats]
+  double* htab_s;
   int* rowoff;      // [T+2]
   int* n_even;      // [T+1]
   int* row_n;       // [rows]

@@ -19,6 +19,9 @@
 #ifndef SDCSW_EXP
 #define SDCSW_EXP 0
 #endif
+#ifndef SDCSW_SYN_MB1
+#define SDCSW_SYN_MB1 5  // synthesis NB <= 2: 5 CTAs per SM (one wave at T127; measured)
+#endif
 #if SDCSW_EXP == 5
 __device__ long long g_ph[8 * 4096];
 extern "C" int sdcsw_debug_phases(long long* host, int n) {
@@ -106,7 +109,7 @@ template <int NB, int PF>
 // NB <= 4: cap the registers at 128 so that 4 CTAs fit per SM - the c1 sweep
 // analysis (576 CTAs) then runs in one wave (measured)
 #define SDCSW_ANA_LB __launch_bounds__(32 * kWarps) __maxnreg__(NB == 1 && !FZ ? 64 : (NB <= 4 ? 128 : 255))
-__global__ void __launch_bounds__(32 * kWarps, SDCSW_SYN_MINB) k_synthesis(
+__global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : SDCSW_SYN_MINB) k_synthesis(
     const double* __restrict__ xsyn, int nb, int T, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ,
@@ -134,8 +137,11 @@ __global__ void __launch_bounds__(32 * kWarps, SDCSW_SYN_MINB) k_synthesis(
   SDCSW_PDL_WAIT();
   if (step_counter != nullptr && (blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0)
     atomicAdd(step_counter, 1);
-  const double* P = ptab + (size_t)r0m * J + j0 + g;
-  const double* H = htab + (size_t)r0m * J + j0 + g;
+  // fragment-order tables ([rows/4][J/8][4][8]): lane (g, t) of k-step s reads
+  // row r0m + 4 s + t, latitudes j0 + g and j0 + 8 + g; a warp load is 256 bytes
+  const size_t qstride = (size_t)(J / 8) * 32;
+  const double* P = ptab + ((size_t)(r0m / 4) * (J / 8) + j0 / 8) * 32 + t * 8 + g;
+  const double* H = htab + ((size_t)(r0m / 4) * (J / 8) + j0 / 8) * 32 + t * 8 + g;
   const int rstride = nb * kXsyn;
   const int nsteps = rows >> 2;
   const int se = le >> 2;  // steps [0, se) are even-class rows
@@ -160,11 +166,11 @@ __global__ void __launch_bounds__(32 * kWarps, SDCSW_SYN_MINB) k_synthesis(
     };
     auto fetch = [&](int s, Frag& f) {
       const int r = 4 * s;
-      const size_t off = (size_t)(r + t) * J;
+      const size_t off = (size_t)s * qstride;
       f.aP0 = __ldg(P + off);
-      f.aP1 = __ldg(P + off + 8);
+      f.aP1 = __ldg(P + off + 32);
       f.aH0 = __ldg(H + off);
-      f.aH1 = __ldg(H + off + 8);
+      f.aH1 = __ldg(H + off + 32);
       const double* rec = X + (size_t)(r + t) * rstride;
 #pragma unroll
       for (int p = 0; p < NPAIR; ++p) {
@@ -361,8 +367,11 @@ __global__ void SDCSW_ANA_LB k_analysis(
   const int rw = (rb * WJ + rt) * kRowsPerWarp;
   const bool live = rw < rows;
   const bool ev0 = rw < le, ev1 = rw + 8 < le;
-  const double* P = ptab + (size_t)(r0m + rw + g) * J + t;
-  const double* H = htab + (size_t)(r0m + rw + g) * J + t;
+  // fragment-order tables ([rows/8][J/4][8][4]): lane (g, t) of k-step s reads
+  // rows r0m + rw + g (+ 8), latitude 4 s + t; a warp load is 256 bytes
+  const size_t tstride = (size_t)(J / 4) * 32;
+  const double* P = ptab + (size_t)((r0m + rw) / 8) * tstride + g * 4 + t;
+  const double* H = htab + (size_t)((r0m + rw) / 8) * tstride + g * 4 + t;
 
   // this lane's B columns (one per tile): data element offsets within a (b, m, j) record
   // record = [fold 0 (S): 7 complex][fold 1 (A): 7 complex] = 28 doubles
@@ -408,11 +417,11 @@ __global__ void SDCSW_ANA_LB k_analysis(
       double aP0, aP1, aH0, aH1, bPs[NB], bPa[NB], bHs[TH], bHa[TH];
     };
     auto fetchA = [&](int s, Frag& f) {
-      const int k = 4 * s;
+      const size_t k = (size_t)s * 32;
       f.aP0 = __ldg(P + k);
-      f.aP1 = __ldg(P + k + 8 * (size_t)J);
+      f.aP1 = __ldg(P + k + tstride);
       f.aH0 = __ldg(H + k);
-      f.aH1 = __ldg(H + k + 8 * (size_t)J);
+      f.aH1 = __ldg(H + k + tstride);
     };
     // only the folds this warp's parity classes use are read (warp-uniform): a
     // single-class tile (the common case) reads half of each record
@@ -578,7 +587,7 @@ static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist
   // which the latency-bound small truncations need more (measured on B200)
 #define SDCSW_SYN(NBV)                                                                         \
   if (NB == NBV) {                                                                             \
-    launch_k(k_synthesis<NBV, 1>, grid, block, 0, s, xsyn, nb, p.T, p.J, p.ptab, p.htab,       \
+    launch_k(k_synthesis<NBV, 1>, grid, block, 0, s, xsyn, nb, p.T, p.J, p.ptab_s, p.htab_s, \
              p.rowoff, p.n_even, fsyn, step_counter, WJ, NBC, mlist, Lp);                      \
     return cudaGetLastError();                                                                 \
   }
@@ -597,8 +606,8 @@ static cudaError_t analysis_impl(const Plan& p, const Work& w, double2* fe, int 
   // prefetch depth 1 (see synthesis_impl)
 #define SDCSW_ANA(NBV)                                                                          \
   if (NB == NBV) {                                                                              \
-    launch_k(k_analysis<NBV, 1, FZ>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab,  \
-             p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, work, fe, p.anal_wj, fz,      \
+    launch_k(k_analysis<NBV, 1, FZ>, grid, 32 * kWarps, 0, s, w.gan, nb, p.T, p.J, p.C, p.ptab_a, \
+             p.htab_a, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, work, fe, p.anal_wj, fz,      \
              p.xscale, p.idx_row);                                                              \
     return cudaGetLastError();                                                                  \
   }

@@ -231,8 +231,24 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   ring_pass_twiddles(nlon, tw.data(), twp);
 
   const size_t tab = (size_t)p.rows * J;
+  // fragment-order copies (coalesced 256-byte A-fragment loads in both GEMMs)
+  std::vector<double> pa(tab), ha(tab), ps(tab), hs(tab);
+  for (int r = 0; r < p.rows; ++r)
+    for (int j = 0; j < J; ++j) {
+      const size_t src = (size_t)r * J + j;
+      const size_t a = (((size_t)(r / 8) * (J / 4) + j / 4) * 8 + r % 8) * 4 + j % 4;
+      const size_t q = (((size_t)(r / 4) * (J / 8) + j / 8) * 4 + r % 4) * 8 + j % 8;
+      pa[a] = ptab[src];
+      ha[a] = htab[src];
+      ps[q] = ptab[src];
+      hs[q] = htab[src];
+    }
   if ((e = upload(&p.ptab, ptab, tab, (size_t)16 * J)) != cudaSuccess ||
       (e = upload(&p.htab, htab, tab, (size_t)16 * J)) != cudaSuccess ||
+      (e = upload(&p.ptab_a, pa.data(), tab, (size_t)16 * J)) != cudaSuccess ||
+      (e = upload(&p.htab_a, ha.data(), tab, (size_t)16 * J)) != cudaSuccess ||
+      (e = upload(&p.ptab_s, ps.data(), tab, (size_t)16 * J)) != cudaSuccess ||
+      (e = upload(&p.htab_s, hs.data(), tab, (size_t)16 * J)) != cudaSuccess ||
       (e = upload(&p.rowoff, rowoff, (size_t)T + 2)) != cudaSuccess ||
       (e = upload(&p.n_even, n_even, (size_t)T + 1)) != cudaSuccess ||
       (e = upload(&p.row_n, row_n, (size_t)p.rows, 16)) != cudaSuccess ||
@@ -258,7 +274,8 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
     int st = cuda_status(e, "sdcsw_plan_create");
     void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
                     p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev,
-                    p.xscale, p.idx_row, p.xsyn, p.anal_work4};
+                    p.xscale, p.idx_row, p.xsyn, p.anal_work4, p.ptab_a, p.htab_a,
+                    p.ptab_s, p.htab_s};
     for (void* q : ptrs)
       if (q) cudaFree(q);
     delete h;
@@ -300,7 +317,8 @@ int sdcsw_plan_destroy(sdcsw_plan* h) {
     if (q) cudaFree(q);
   void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
                   p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev,
-                  p.xscale, p.idx_row, p.xsyn, p.anal_work4, p.pkx, p.pky, p.ptw, p.pw1, p.pw2};
+                  p.xscale, p.idx_row, p.xsyn, p.anal_work4, p.pkx, p.pky, p.ptw, p.pw1, p.pw2,
+                  p.ptab_a, p.htab_a, p.ptab_s, p.htab_s};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   h->alive = false;
