@@ -176,7 +176,9 @@ int sdcsw_transform_stage(sdcsw_plan* plan, int stage, const double* in, double*
 
 /* Device pointers and sizes of the internal workspaces: which 0 = Fourier
  * coefficients [max_batch][nlat/2][T+1][4 (U,V,zeta,Phi)][2 (N,S)] complex,
- * which 1 = analysis data [max_batch][T+1][nlat/2][2 (N+S, N-S)][7] complex. */
+ * which 1 = analysis data, [max_batch][T+1] blocks of nlat/2 x 28 doubles:
+ * [nlat/2][2 (N+S, N-S)][7 slots] complex when T < 400, in DMMA-fragment
+ * order for the table-streaming analysis (T >= 400; gan_off in internal.cuh). */
 int sdcsw_workspace(sdcsw_plan* plan, int which, void** ptr, long long* bytes);
 
 /* Spectral split (more GPUs than collocation nodes): the plan's

@@ -22,6 +22,22 @@ constexpr int kRowPad = 8;
 // P-data: X_phi, X_zeta, X_delta, X_ke; H-data: Y_phi, Y_zeta, Y_delta.
 enum { kXPhi = 0, kXZeta, kXDelta, kXKe, kYPhi, kYZeta, kYDelta, kNumSlots };
 
+// Analysis data layouts of one (state b, wavenumber m) block of J x 28 doubles.
+// Record order (k_analysis, latency regime): [j][fold S, A][7 slots][re, im].
+// Fragment order (k_analysis_tma, table-streaming regime; gan_off): per k-step
+// of 4 latitudes and fold, [P part: 4 lat x slots 0-3 x (re, im) = 32][H part:
+// 4 lat x slots 4-6 x (re, im) = 24], so that one DMMA B fragment (the 8 P
+// columns or 6 H columns of one state) is 32 (24) consecutive doubles.
+// (Measured: fragment order speeds the TMA analysis up by 20% at T511 and
+// slows the latency-regime analysis at T127-T255.)
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int gan_off(int j, int fold, int slot, int ri) {
+  const int base = ((j >> 2) * 2 + fold) * 56, t = j & 3;
+  return slot < 4 ? base + t * 8 + slot * 2 + ri : base + 32 + t * 6 + (slot - 4) * 2 + ri;
+}
+
 struct FftPlan {
   int n;           // nlon
   int nstages;     // number of radix passes
@@ -221,6 +237,8 @@ struct FuseArgs {
   double phibar;
   double cf[kFuseMaxNodes * (kFuseMaxNodes + 4)];  // mode 1: [M][M+4]; mode 2: [M+4]
 };
+// the TMA analysis (and the fragment-order analysis data it reads) is in use
+inline bool tma_active(const Plan& p) { return p.tma_ok && p.anal_wj == 4; }
 inline bool fuse_supported(const Plan& p, int M) {
   return p.kind == 0 && !p.tma_ok && p.own_idx == nullptr && M >= 1 && M <= kFuseMaxNodes;
 }

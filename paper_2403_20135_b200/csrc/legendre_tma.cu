@@ -79,8 +79,6 @@ __global__ void __launch_bounds__(128) k_analysis_tma(
     const int* __restrict__ n_even, const int* __restrict__ row_n, const int* __restrict__ moff,
     const double* __restrict__ lam, const int* __restrict__ work, double2* __restrict__ fe) {
   SDCSW_PDL_ENTRY();
-  constexpr int HU = 6 * NB;
-  constexpr int TH = (HU + 7) / 8;
   constexpr int PC = 8 * NB;
   constexpr int OS = PC + 1;
   extern __shared__ __align__(1024) unsigned char tma_smem[];
@@ -119,26 +117,18 @@ __global__ void __launch_bounds__(128) k_analysis_tma(
   }
   SDCSW_PDL_WAIT();
 
-  // B columns of this lane (one per tile), as in k_analysis
+  // B column tiles: tile c = state b0 + c.  P columns g = 2 slot + re/im over
+  // (X_phi, X_zeta, X_delta, X_ke); H columns g < 6 over (Y_phi, Y_zeta,
+  // Y_delta), accumulated into the same outputs.  Fragment-order analysis data
+  // (gan_off): the lanes of one tile read 32 (P) or 24 (H) consecutive doubles.
   const double* gb = reinterpret_cast<const double*>(gan);
-  long long pbase[NB], hbase[TH];
-  int pel[NB], hel[TH];
+  long long bbase[NB];
 #pragma unroll
-  for (int c = 0; c < NB; ++c) {
-    const int col = 8 * c + g;
-    int b, slot;
-    if (col < HU) { b = col / 6; slot = kXPhi + (col % 6) / 2; }
-    else { b = (col - HU) >> 1; slot = kXKe; }
-    pbase[c] = b0 + b < nb ? (((long long)(b0 + b) * L + m) * J) * 28 : -1;
-    pel[c] = slot * 2 + (col & 1);
-  }
-#pragma unroll
-  for (int c = 0; c < TH; ++c) {
-    const int col = 8 * c + g;
-    const int b = col / 6;
-    hbase[c] = (col < HU && b0 + b < nb) ? (((long long)(b0 + b) * L + m) * J) * 28 : -1;
-    hel[c] = (kYPhi + (col % 6) / 2) * 2 + (col & 1);
-  }
+  for (int c = 0; c < NB; ++c)
+    bbase[c] = b0 + c < nb ? ((long long)(b0 + c) * L + m) * J * 28 + t * 8 + g : -1;
+  const int hsh = 32 + t * 6 + g - (t * 8 + g);
+  const bool hcol = g < 6;
+  const bool any_ev = ev0 || ev1, any_od = !ev0 || !ev1;
 
   double acc[2][NB][2];
 #pragma unroll
@@ -148,21 +138,18 @@ __global__ void __launch_bounds__(128) k_analysis_tma(
 
   const int row0 = warp * kRowsPerWarp + g;  // tile rows of this lane (a = 0; a = 1 adds 8)
   struct BFrag {
-    double ps[NB], pa[NB], hs[TH], ha[TH];
+    double ps[NB], pa[NB], hs[NB], ha[NB];
   };
-  auto fetch_b = [&](int lat, BFrag& f) {
-    const long long jrec = (long long)lat * 28;
+  auto fetch_b = [&](int lat, BFrag& f) {  // lat = 4 s + t
+    const long long ks112 = (long long)(lat >> 2) * 112;
 #pragma unroll
     for (int c = 0; c < NB; ++c) {
-      const bool ok = pbase[c] >= 0;
-      f.ps[c] = ok ? __ldg(gb + pbase[c] + jrec + pel[c]) : 0.0;
-      f.pa[c] = ok ? __ldg(gb + pbase[c] + jrec + 14 + pel[c]) : 0.0;
-    }
-#pragma unroll
-    for (int c = 0; c < TH; ++c) {
-      const bool ok = hbase[c] >= 0;
-      f.hs[c] = ok ? __ldg(gb + hbase[c] + jrec + hel[c]) : 0.0;
-      f.ha[c] = ok ? __ldg(gb + hbase[c] + jrec + 14 + hel[c]) : 0.0;
+      const bool ok = bbase[c] >= 0;
+      const double* q = gb + bbase[c] + ks112;
+      f.ps[c] = ok && any_ev ? __ldg(q) : 0.0;
+      f.pa[c] = ok && any_od ? __ldg(q + 56) : 0.0;
+      f.hs[c] = ok && any_od && hcol ? __ldg(q + hsh) : 0.0;
+      f.ha[c] = ok && any_ev && hcol ? __ldg(q + 56 + hsh) : 0.0;
     }
   };
   BFrag cur, nxt;
@@ -188,7 +175,7 @@ __global__ void __launch_bounds__(128) k_analysis_tma(
           dmma_t(acc[1][c], aP1, ev1 ? cur.ps[c] : cur.pa[c]);
         }
 #pragma unroll
-        for (int c = 0; c < TH; ++c) {
+        for (int c = 0; c < NB; ++c) {
           dmma_t(acc[0][c], aH0, ev0 ? cur.ha[c] : cur.hs[c]);
           dmma_t(acc[1][c], aH1, ev1 ? cur.ha[c] : cur.hs[c]);
         }
@@ -224,10 +211,10 @@ __global__ void __launch_bounds__(128) k_analysis_tma(
     const int idx = mo + n - m;
     const double* row = o + rr * OS;
     const double l = lam[idx];
-    double2 phi = make_double2(row[6 * b + 0], row[6 * b + 1]);
-    double2 zeta = make_double2(row[6 * b + 2], row[6 * b + 3]);
-    double2 delta = make_double2(row[6 * b + 4] + l * row[6 * NB + 2 * b],
-                                 row[6 * b + 5] + l * row[6 * NB + 2 * b + 1]);
+    double2 phi = make_double2(row[8 * b + 0], row[8 * b + 1]);
+    double2 zeta = make_double2(row[8 * b + 2], row[8 * b + 3]);
+    double2 delta = make_double2(__fma_rn(l, row[8 * b + 6], row[8 * b + 4]),
+                                 __fma_rn(l, row[8 * b + 7], row[8 * b + 5]));
     if (m == 0) phi.y = zeta.y = delta.y = 0.0;
     double2* dst = fe + (size_t)(b0 + b) * 3 * C;
     dst[idx] = phi;
@@ -276,7 +263,7 @@ cudaError_t make_table_maps(Plan& p) {
 
 bool launch_analysis_tma(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s,
                          cudaError_t* err) {
-  if (!p.tma_ok || p.anal_wj != 4) return false;
+  if (!tma_active(p)) return false;
   const int NB = nb <= 6 ? nb : 4;
   const int* work = p.own_work != nullptr ? p.own_work : p.anal_work;
   const int nwork = p.own_work != nullptr ? p.n_own_work : p.n_anal_work;

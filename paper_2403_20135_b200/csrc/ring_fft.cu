@@ -261,7 +261,8 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
                                                   const double2* __restrict__ twg,
                                                   double two_omega,
                                                   const int* __restrict__ m_part,
-                                                  const int* __restrict__ m_k, int Lp, int nbg) {
+                                                  const int* __restrict__ m_k, int Lp, int nbg,
+                                                  int frag) {
   SDCSW_PDL_ENTRY();
   if (SDCSW_TRIG_RING == 1) SDCSW_PDL_TRIGGER();
   extern __shared__ double2 sm2[];
@@ -420,9 +421,13 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
   RT(4)
 
   const double h = 0.5 / (double)N;
-  // analysis layout: [b][m][j][fold][slot]; thread (m, fold) writes the fold's
-  // seven slots (112 contiguous bytes), the pair of folds a 224-byte record
-  double2* outp = gan + ((size_t)b * L * J + j) * (kNumSlots * 2);
+  // analysis data (internal.cuh): record order - thread (m, fold) writes the
+  // fold's seven slots (112 contiguous bytes); fragment order (frag, TMA
+  // analysis) - the four P slots (64 bytes) and three H slots (48 bytes)
+  double* outp = reinterpret_cast<double*>(gan) + (size_t)b * L * J * 28;
+  const int pofs = frag ? gan_off(j, 0, kXPhi, 0) : j * 28;
+  const int hofs = frag ? gan_off(j, 0, kYPhi, 0) : j * 28 + 2 * kYPhi;
+  const int fstride = frag ? 56 : 14;
   constexpr int SHL = gen_shift<N>(2 * NS - 2);
   for (int it = threadIdx.x; it < 2 * L; it += THREADS) {
     const int m = it >> 1, fold = it & 1;
@@ -436,16 +441,18 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
       const double2 Y = make_double2(h * (zm.y + zc.y), -h * (zm.x - zc.x));
       v[o] = fold ? csub(X, Y) : cadd(X, Y);
     }
-    double2* dst = outp + (size_t)m * J * (kNumSlots * 2) + fold * kNumSlots;
+    double* bm = outp + (size_t)m * J * 28 + fold * fstride;
+    double2* dp = reinterpret_cast<double2*>(bm + pofs);  // X_phi, X_zeta, X_delta, X_ke
+    double2* dh = reinterpret_cast<double2*>(bm + hofs);  // Y_phi, Y_zeta, Y_delta
     // A = eta U: X_zeta = -(i m A) ws, Y_delta = A ws; B = eta V: X_delta = (i m B) ws,
     // Y_zeta = B ws; C = Phi U: X_phi = -(i m C) ws; D = Phi V: Y_phi = D ws; X_ke = E wk
-    dst[kXPhi] = make_double2(dm * v[2].y * ws, -dm * v[2].x * ws);
-    dst[kXZeta] = make_double2(dm * v[0].y * ws, -dm * v[0].x * ws);
-    dst[kXDelta] = make_double2(-dm * v[1].y * ws, dm * v[1].x * ws);
-    dst[kXKe] = make_double2(v[4].x * wk, v[4].y * wk);
-    dst[kYPhi] = make_double2(v[3].x * ws, v[3].y * ws);
-    dst[kYZeta] = make_double2(v[1].x * ws, v[1].y * ws);
-    dst[kYDelta] = make_double2(v[0].x * ws, v[0].y * ws);
+    dp[kXPhi] = make_double2(dm * v[2].y * ws, -dm * v[2].x * ws);
+    dp[kXZeta] = make_double2(dm * v[0].y * ws, -dm * v[0].x * ws);
+    dp[kXDelta] = make_double2(-dm * v[1].y * ws, dm * v[1].x * ws);
+    dp[kXKe] = make_double2(v[4].x * wk, v[4].y * wk);
+    dh[kYPhi - kYPhi] = make_double2(v[3].x * ws, v[3].y * ws);
+    dh[kYZeta - kYPhi] = make_double2(v[1].x * ws, v[1].y * ws);
+    dh[kYDelta - kYPhi] = make_double2(v[0].x * ws, v[0].y * ws);
   }
 #if SDCSW_EXP == 4
   __syncthreads();
@@ -462,15 +469,19 @@ bool ring_supported(int nlon) {
   return false;
 }
 
-cudaError_t configure_ring(size_t smem) {
+size_t ring_smem_bytes(int nlon);
+
+// Each ring kernel's dynamic shared-memory limit is its own size's need (a
+// process-wide function attribute: it must not depend on which plan set it).
+cudaError_t configure_ring(size_t /*smem*/) {
   cudaError_t e = cudaSuccess;
 #define SDCSW_RING_CFG(NV, TV)                                                                     \
   if (e == cudaSuccess)                                                                            \
     e = cudaFuncSetAttribute(k_ring<NV, TV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                             (int)smem);                                                           \
+                             (int)ring_smem_bytes(NV));                                            \
   if (e == cudaSuccess)                                                                            \
     e = cudaFuncSetAttribute(k_ring<NV, TV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                             (int)smem);
+                             (int)ring_smem_bytes(NV));
   SDCSW_RING_SIZES(SDCSW_RING_CFG)
 #undef SDCSW_RING_CFG
   return e;
@@ -506,10 +517,10 @@ static cudaError_t ring_impl(const Plan& p, const double2* fsyn, double2* gan, c
   if (p.nlon == NV) {                                                                              \
     if (m_part != nullptr)                                                                         \
       launch_k(k_ring<NV, TV, true>, grid, TV, p.ring_smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn,  \
-               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb);                            \
+               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb, (int)tma_active(p));       \
     else                                                                                           \
       launch_k(k_ring<NV, TV, false>, grid, TV, p.ring_smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn, \
-               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb);                            \
+               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb, (int)tma_active(p));       \
     return cudaGetLastError();                                                                     \
   }
   SDCSW_RING_SIZES(SDCSW_RING_LAUNCH)

@@ -378,3 +378,44 @@ def test_reference_schemes_on_gpu():
     traj = integrate(p, u0, 120.0, 5, Ab2SiStepper())
     assert max(relative_l2(traj.states[-1], osdc.ab2_run(o, u0, 120.0, 5), o)) <= 1e-10
     assert [(r.n_f_expl, r.n_f_impl, r.n_solve) for r in traj.reports] == [(3, 2, 2)] + [(1, 1, 1)] * 4
+
+
+def test_tma_analysis_matches_latency_analysis_t511():
+    """T511: the table-streaming TMA analysis (fragment-order analysis data) and
+    the latency-regime analysis (record order; forced with SDCSW_ANAL_WJ=2) give
+    the same f_E to summation-order rounding."""
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    p = gpu(511, max_batch=5)
+    u = random_initial_state(p.grid, 11)
+    u[: p.n_coef] = 4e-3 * u[p.n_coef : 2 * p.n_coef] * 1e6
+    a = p.f_expl(u)
+    old = os.environ.get("SDCSW_ANAL_WJ")
+    os.environ["SDCSW_ANAL_WJ"] = "2"
+    try:
+        q = SphericalShallowWater(511, max_batch=2)
+    finally:
+        if old is None:
+            del os.environ["SDCSW_ANAL_WJ"]
+        else:
+            os.environ["SDCSW_ANAL_WJ"] = old
+    b = q.f_expl(u)
+    c = p.n_coef
+    for f in range(3):
+        x, y = a[f * c : (f + 1) * c], b[f * c : (f + 1) * c]
+        assert np.linalg.norm(x - y) <= 1e-12 * np.linalg.norm(y)
+    q.close()
+
+
+def test_plans_of_different_sizes_coexist():
+    """Kernel attributes are process-wide: creating a small plan after a large
+    one must not break the large one (ring shared-memory limits)."""
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    big = gpu(511, max_batch=5)
+    u = random_initial_state(big.grid, 12)
+    a = big.f_expl(u)
+    small = SphericalShallowWater(63, max_batch=2)
+    small.f_expl(random_initial_state(small.grid, 1))
+    assert np.array_equal(big.f_expl(u), a)
+    small.close()
