@@ -166,33 +166,44 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 void set_error(const std::string& msg);
 int cuda_status(cudaError_t e, const char* where);
 
-// Synthesis B operand ("xsyn"): per packed table row r and batch entry b a
-// record of kXsyn doubles at xsyn[(r * nb + b) * kXsyn]:
-//   P part: U re, U im, V re, V im, zeta re, zeta im, Phi re, Phi im
-//   H part: U re, U im, V re, V im
+// Synthesis B operand ("xsyn"), 12 doubles per (packed table row r, batch
+// entry b) in three parts of four:
+//   part 0: U_P re, U_P im, V_P re, V_P im;  part 1: zeta re, zeta im, Phi re, Phi im;
+//   part 2: U_H re, U_H im, V_H re, V_H im
 // with U_P = i m chi / a, V_P = i m psi / a, U_H = -psi / a, V_H = chi / a.
+// Fragment order for a batch of w entries: [row quad r/4][part][b][r % 4][4],
+// so that the synthesis B fragment of a pair of entries (4 rows x 2 entries x
+// 4 columns) is 32 consecutive doubles.  Element k of (r, b) is at
+// xsyn_off(r, b, w) + (k / 4) * 16 w + k % 4; a row quad spans 12 w doubles per
+// row, so rows [r0, r0 + 4q) are the contiguous range [12 w r0, 12 w (r0 + 4q)).
 // Producers write only valid rows; padding rows of a buffer must stay zero.
 constexpr int kXsyn = 12;
 
 #ifdef __CUDACC__
-__device__ __forceinline__ void write_xsyn_half(double* __restrict__ rec, int ri, double phi,
-                                                double zeta, double delta, double2 sc) {
+__device__ __forceinline__ size_t xsyn_off(int r, int b, int w) {
+  return ((size_t)(r >> 2) * 3 * w + b) * 16 + (r & 3) * 4;
+}
+// rec = xsyn_off(...) element pointer, pstride = 16 w (part stride)
+__device__ __forceinline__ void write_xsyn_half(double* __restrict__ rec, size_t pstride, int ri,
+                                                double phi, double zeta, double delta, double2 sc) {
   // ri = 0 holds real parts, ri = 1 imaginary parts; (x + i y)(-i s) = s y - i s x
   const double sm = sc.x, sa = sc.y;
+  double* p1 = rec + pstride;
+  double* p2 = rec + 2 * pstride;
   if (ri == 0) {
     rec[1] = -sm * delta;  // U_P im
     rec[3] = -sm * zeta;   // V_P im
-    rec[4] = zeta;
-    rec[6] = phi;
-    rec[8] = sa * zeta;    // U_H re
-    rec[10] = -sa * delta; // V_H re
+    p1[0] = zeta;
+    p1[2] = phi;
+    p2[0] = sa * zeta;     // U_H re
+    p2[2] = -sa * delta;   // V_H re
   } else {
     rec[0] = sm * delta;   // U_P re
     rec[2] = sm * zeta;    // V_P re
-    rec[5] = zeta;
-    rec[7] = phi;
-    rec[9] = sa * zeta;    // U_H im
-    rec[11] = -sa * delta; // V_H im
+    p1[1] = zeta;
+    p1[3] = phi;
+    p2[1] = sa * zeta;     // U_H im
+    p2[3] = -sa * delta;   // V_H im
   }
 }
 

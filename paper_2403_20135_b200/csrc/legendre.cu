@@ -88,8 +88,8 @@ __global__ void __launch_bounds__(256) k_synth_prep(const double* __restrict__ u
   const int idx = e >> 1;
   const int ch = chunk > 0 ? chunk : nb;  // chunk-major record layout (see f_expl_prepped)
   const int cb = b / ch, w = nb - cb * ch < ch ? nb - cb * ch : ch;
-  double* rec = xsyn + ((size_t)cb * rows * ch + (size_t)idx_row[idx] * w + (b - cb * ch)) * kXsyn;
-  write_xsyn_half(rec, e & 1, s[e], s[C2 + e], s[2 * C2 + e], xscale[idx]);
+  double* rec = xsyn + (size_t)cb * rows * ch * kXsyn + xsyn_off(idx_row[idx], b - cb * ch, w);
+  write_xsyn_half(rec, 16 * (size_t)w, e & 1, s[e], s[C2 + e], s[2 * C2 + e], xscale[idx]);
 }
 
 // ---------------------------------------------------------------------------
@@ -109,7 +109,7 @@ template <int NB, int PF>
 // NB <= 4: cap the registers at 128 so that 4 CTAs fit per SM - the c1 sweep
 // analysis (576 CTAs) then runs in one wave (measured)
 #define SDCSW_ANA_LB __launch_bounds__(32 * kWarps) __maxnreg__(NB == 1 && !FZ ? 64 : (NB <= 4 ? 128 : 255))
-__global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : SDCSW_SYN_MINB) k_synthesis(
+__global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : (NB <= 4 ? SDCSW_SYN_MINB : 3)) k_synthesis(
     const double* __restrict__ xsyn, int nb, int T, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ,
@@ -142,7 +142,8 @@ __global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : SDCSW_S
   const size_t qstride = (size_t)(J / 8) * 32;
   const double* P = ptab + ((size_t)(r0m / 4) * (J / 8) + j0 / 8) * 32 + t * 8 + g;
   const double* H = htab + ((size_t)(r0m / 4) * (J / 8) + j0 / 8) * 32 + t * 8 + g;
-  const int rstride = nb * kXsyn;
+  const size_t qstep = (size_t)3 * nb * 16;  // one row quad (k-step) of the operand
+  const size_t pstr = (size_t)16 * nb;         // part stride
   const int nsteps = rows >> 2;
   const int se = le >> 2;  // steps [0, se) are even-class rows
   const int gb = g >> 2, gc = g & 3;  // lane's entry within the pair, column within the entry
@@ -151,7 +152,9 @@ __global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : SDCSW_S
     const int b0 = (blockIdx.z * NBC + bb) * NB;
     if (b0 >= nb) break;
     const int nbv = nb - b0 < NB ? nb - b0 : NB;
-    const double* X = xsyn + ((size_t)r0m * nb + b0) * kXsyn;
+    // fragment-order operand: lane (g, t) of k-step s reads row quad r0m/4 + s,
+    // row t, entry b0 + 2p + gb, column gc - 32 consecutive doubles per warp load
+    const double* X = xsyn + (size_t)(r0m / 4) * qstep + (size_t)b0 * 16 + t * 4 + gc;
 
     double aE[2][NT][2], aO[2][NT][2];
 #pragma unroll
@@ -171,15 +174,15 @@ __global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : SDCSW_S
       f.aP1 = __ldg(P + off + 32);
       f.aH0 = __ldg(H + off);
       f.aH1 = __ldg(H + off + 32);
-      const double* rec = X + (size_t)(r + t) * rstride;
+      const double* rec = X + (size_t)s * qstep;
 #pragma unroll
       for (int p = 0; p < NPAIR; ++p) {
         const int be = 2 * p + gb;
         const bool ok = be < nbv;
-        const double* rb = rec + be * kXsyn;
-        f.bP[2 * p] = ok ? __ldg(rb + gc) : 0.0;          // U, V (P part)
-        f.bP[2 * p + 1] = ok ? __ldg(rb + 4 + gc) : 0.0;  // zeta, Phi
-        f.bH[p] = ok ? __ldg(rb + 8 + gc) : 0.0;          // U, V (H part)
+        const double* rb = rec + be * 16;
+        f.bP[2 * p] = ok ? __ldg(rb) : 0.0;                // U, V (P part)
+        f.bP[2 * p + 1] = ok ? __ldg(rb + pstr) : 0.0;     // zeta, Phi
+        f.bH[p] = ok ? __ldg(rb + 2 * pstr) : 0.0;         // U, V (H part)
       }
     };
 #pragma unroll
@@ -314,7 +317,7 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
       b = axmy_tri(b, c[M], fi[q]);
       const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], l);
       store_tri(fz.fi + q * S2, C2, e, f_impl_tri(u, fz.phibar, l));
-      write_xsyn_half(stage + (size_t)(rr * M + q) * kXsyn, ri, u.phi, u.zeta, u.delta, sc);
+      write_xsyn_half(stage + xsyn_off(rr, q, M), 16 * (size_t)M, ri, u.phi, u.zeta, u.delta, sc);
     }
   } else {
     const double* c = fz.cf;
@@ -330,7 +333,7 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
     store_tri(fz.u_out, C2, e, u);
     if (fz.diverged != nullptr && !finite_tri(u))
       atomicMin(fz.diverged, fz.step_counter ? *fz.step_counter : 1);
-    write_xsyn_half(stage + (size_t)rr * kXsyn, ri, u.phi, u.zeta, u.delta, xscale[idx]);
+    write_xsyn_half(stage + xsyn_off(rr, 0, 1), 16, ri, u.phi, u.zeta, u.delta, xscale[idx]);
   }
 }
 

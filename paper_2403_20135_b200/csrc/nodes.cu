@@ -64,8 +64,8 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
   if (xsyn != nullptr) {  // synthesis B operand of the f_E that follows, in batch chunks
     const int nbt = gridDim.y * gridDim.z, ch = chunk > 0 ? chunk : nbt;
     const int cb = ob / ch, w = nbt - cb * ch < ch ? nbt - cb * ch : ch;
-    write_xsyn_half(xsyn + ((size_t)cb * rows * ch + (size_t)idx_row[e >> 1] * w + (ob - cb * ch)) * kXsyn,
-                    e & 1, u.phi, u.zeta, u.delta, xscale[e >> 1]);
+    write_xsyn_half(xsyn + (size_t)cb * rows * ch * kXsyn + xsyn_off(idx_row[e >> 1], ob - cb * ch, w),
+                    16 * (size_t)w, e & 1, u.phi, u.zeta, u.delta, xscale[e >> 1]);
   }
 }
 
@@ -110,8 +110,8 @@ __global__ void __launch_bounds__(256) k_final_node(
   if (xsyn != nullptr) {  // B operand of the next step's f_E(u0) (batch = members, chunked)
     const int nbt = gridDim.z, ch = chunk > 0 ? chunk : nbt;
     const int cb = z / ch, w = nbt - cb * ch < ch ? nbt - cb * ch : ch;
-    write_xsyn_half(xsyn + ((size_t)cb * rows * ch + (size_t)idx_row[e >> 1] * w + (z - cb * ch)) * kXsyn,
-                    e & 1, u.phi, u.zeta, u.delta, xscale[e >> 1]);
+    write_xsyn_half(xsyn + (size_t)cb * rows * ch * kXsyn + xsyn_off(idx_row[e >> 1], z - cb * ch, w),
+                    16 * (size_t)w, e & 1, u.phi, u.zeta, u.delta, xscale[e >> 1]);
   }
 }
 
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(256) k_serial_node(
   store_tri(u_out, C2, e, u);
   store_tri(fi_new, C2, e, f_impl_tri(u, phibar, lam));
   if (xsyn != nullptr)
-    write_xsyn_half(xsyn + (size_t)idx_row[e >> 1] * kXsyn, e & 1, u.phi, u.zeta, u.delta,
+    write_xsyn_half(xsyn + xsyn_off(idx_row[e >> 1], 0, 1), 16, e & 1, u.phi, u.zeta, u.delta,
                     xscale[e >> 1]);
   if (u_out2 != nullptr) {
     store_tri(u_out2, C2, e, u);
