@@ -149,8 +149,10 @@ int sdcsw_stepper_reset(sdcsw_stepper* st, void* stream);
  * node updates (1 = the DIAGONAL_SEQUENTIAL analogue: one node at a time on
  * one stream); option 2: node updates fused into the analysis epilogue (1 =
  * on, the default for dSDC with one member, M <= 6 and the latency-regime
- * analysis; takes effect with chains = 1 and sequential = 0).  Bit-identical
- * results in every setting.  Rebuilds the step graph. */
+ * analysis; takes effect with chains = 1 and sequential = 0); option 3: steps
+ * per replayed CUDA graph (1..64, default 8; programmatic dependent launch then
+ * also overlaps step boundaries).  Bit-identical results in every setting.
+ * Rebuilds the step graph. */
 int sdcsw_stepper_set_option(sdcsw_stepper* st, int option, int value);
 
 /* One step launched stage by stage with CUDA events (no graph) for the cost

@@ -104,7 +104,10 @@ struct sdcsw_stepper {
   int* flags;    // [0] first diverged step (INT_MAX = none), [1] step counter
   cudaStream_t cap;
   cudaGraph_t graph;
-  cudaGraphExec_t exec;
+  cudaGraphExec_t exec;     // one step
+  cudaGraph_t graphK;
+  cudaGraphExec_t execK;    // graph_steps steps back to back (PDL across step boundaries)
+  int graph_steps;
   double* graph_u;
   int launches;
 };
@@ -901,17 +904,26 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
       cudaEventCreateWithFlags(&s->ev_join[g], cudaEventDisableTiming);
     }
   }
+  // several steps per replayed graph: PDL then also overlaps the step boundaries
+  s->graph_steps = 8;
+  if (const char* env = getenv("SDCSW_GRAPH_STEPS")) s->graph_steps = atoi(env) > 0 ? atoi(env) : 1;
   sdcsw_stepper_launches_per_step(s, &s->launches);
   *out = s;
   return SDCSW_OK;
+}
+
+static void drop_graphs(sdcsw_stepper* s) {
+  if (s->exec) { cudaGraphExecDestroy(s->exec); s->exec = nullptr; }
+  if (s->graph) { cudaGraphDestroy(s->graph); s->graph = nullptr; }
+  if (s->execK) { cudaGraphExecDestroy(s->execK); s->execK = nullptr; }
+  if (s->graphK) { cudaGraphDestroy(s->graphK); s->graphK = nullptr; }
 }
 
 int sdcsw_stepper_destroy(sdcsw_stepper* s) {
   if (!s) return SDCSW_ERR_STATE;
   cudaSetDevice(s->plan->p.device);
   cudaDeviceSynchronize();
-  if (s->exec) cudaGraphExecDestroy(s->exec);
-  if (s->graph) cudaGraphDestroy(s->graph);
+  drop_graphs(s);
   if (s->ncreated > 1) {
     cudaEventDestroy(s->ev_fork);
     for (int g = 0; g < s->ncreated; ++g) {
@@ -970,19 +982,30 @@ int sdcsw_stepper_run(sdcsw_stepper* s, double* u, int n_steps, int use_graph, v
     return SDCSW_OK;
   }
   if (!s->exec || s->graph_u != u) {
-    if (s->exec) { cudaGraphExecDestroy(s->exec); s->exec = nullptr; }
-    if (s->graph) { cudaGraphDestroy(s->graph); s->graph = nullptr; }
-    e = cudaStreamBeginCapture(s->cap, cudaStreamCaptureModeThreadLocal);
-    if (e != cudaSuccess) return cuda_status(e, "cudaStreamBeginCapture");
-    cudaError_t le = enqueue_step(s, (double2*)u, s->cap);
-    e = cudaStreamEndCapture(s->cap, &s->graph);
-    if (le != cudaSuccess) return cuda_status(le, "capture step");
-    if (e != cudaSuccess) return cuda_status(e, "cudaStreamEndCapture");
-    e = cudaGraphInstantiate(&s->exec, s->graph, 0);
-    if (e != cudaSuccess) return cuda_status(e, "cudaGraphInstantiate");
+    drop_graphs(s);
+    auto capture = [&](int steps, cudaGraph_t* g, cudaGraphExec_t* x) -> int {
+      cudaError_t ce = cudaStreamBeginCapture(s->cap, cudaStreamCaptureModeThreadLocal);
+      if (ce != cudaSuccess) return cuda_status(ce, "cudaStreamBeginCapture");
+      cudaError_t le = cudaSuccess;
+      for (int i = 0; i < steps && le == cudaSuccess; ++i) le = enqueue_step(s, (double2*)u, s->cap);
+      ce = cudaStreamEndCapture(s->cap, g);
+      if (le != cudaSuccess) return cuda_status(le, "capture step");
+      if (ce != cudaSuccess) return cuda_status(ce, "cudaStreamEndCapture");
+      ce = cudaGraphInstantiate(x, *g, 0);
+      return ce == cudaSuccess ? SDCSW_OK : cuda_status(ce, "cudaGraphInstantiate");
+    };
+    int st = capture(1, &s->graph, &s->exec);
+    if (st == SDCSW_OK && s->graph_steps > 1) st = capture(s->graph_steps, &s->graphK, &s->execK);
+    if (st != SDCSW_OK) return st;
     s->graph_u = u;
   }
-  for (int i = 0; i < n_steps; ++i) {
+  int i = 0;
+  if (s->execK)
+    for (; i + s->graph_steps <= n_steps; i += s->graph_steps) {
+      e = cudaGraphLaunch(s->execK, cs);
+      if (e != cudaSuccess) return cuda_status(e, "cudaGraphLaunch");
+    }
+  for (; i < n_steps; ++i) {
     e = cudaGraphLaunch(s->exec, cs);
     if (e != cudaSuccess) return cuda_status(e, "cudaGraphLaunch");
   }
@@ -997,6 +1020,9 @@ int sdcsw_stepper_set_option(sdcsw_stepper* s, int option, int value) {
   } else if (option == 1) {  // sequential node updates
     if (s->mode != 0 || s->members != 1) return SDCSW_ERR_PARAM;
     s->sequential = value ? 1 : 0;
+  } else if (option == 3) {  // steps per replayed graph
+    if (value < 1 || value > 64) return SDCSW_ERR_PARAM;
+    s->graph_steps = value;
   } else if (option == 2) {  // node updates fused into the analysis epilogue
     if (value && (s->mode != 0 || s->members != 1 || !fuse_supported(s->plan->p, s->M)))
       return SDCSW_ERR_PARAM;
@@ -1004,8 +1030,7 @@ int sdcsw_stepper_set_option(sdcsw_stepper* s, int option, int value) {
   } else {
     return SDCSW_ERR_PARAM;
   }
-  if (s->exec) { cudaGraphExecDestroy(s->exec); s->exec = nullptr; }
-  if (s->graph) { cudaGraphDestroy(s->graph); s->graph = nullptr; }
+  drop_graphs(s);
   return SDCSW_OK;
 }
 
