@@ -58,7 +58,7 @@ struct Plan {
   // the analysis, 4 x 8 for the synthesis) is 32 consecutive doubles
   double* ptab_a;   // [rows/8][J/4][8 rows][4 lats]
   double* htab_a;
-  double* ptab_s;   // [rows/4][J/8][4 rows][8 lats]
+  double* ptab_s;   // [rows/4][J/8][8 lats][4 rows] (lane order g * 4 + t)
   double* htab_s;
   int* rowoff;      // [T+2]
   int* n_even;      // [T+1]
@@ -77,6 +77,7 @@ struct Plan {
   int* anal_work4;  // [n_anal_work4] row blocks of 4 tiles (throughput regime)
   int n_anal_work4;
   int synth_wj, anal_wj;  // row tiles per CTA (the other warps split K)
+  int syn_cp;             // synthesis with the cp.async pipeline (k_synthesis_cp)
   FftPlan fft;
   // workspaces
   double2* fsyn;    // [max_batch][J][L][4][2]
@@ -286,6 +287,7 @@ cudaError_t launch_axpy(long long n, const double* x, double w, const double* y,
                         cudaStream_t s);
 
 cudaError_t make_table_maps(Plan& p);
+cudaError_t configure_synthesis();
 bool launch_analysis_tma(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s,
                          cudaError_t* err);
 

@@ -137,11 +137,12 @@ __global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : (NB <= 
   SDCSW_PDL_WAIT();
   if (step_counter != nullptr && (blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0)
     atomicAdd(step_counter, 1);
-  // fragment-order tables ([rows/4][J/8][4][8]): lane (g, t) of k-step s reads
-  // row r0m + 4 s + t, latitudes j0 + g and j0 + 8 + g; a warp load is 256 bytes
+  // fragment-order tables ([rows/4][J/8][8][4], lane order): lane (g, t) of
+  // k-step s reads row r0m + 4 s + t, latitudes j0 + g and j0 + 8 + g; a warp
+  // load is 256 contiguous bytes
   const size_t qstride = (size_t)(J / 8) * 32;
-  const double* P = ptab + ((size_t)(r0m / 4) * (J / 8) + j0 / 8) * 32 + t * 8 + g;
-  const double* H = htab + ((size_t)(r0m / 4) * (J / 8) + j0 / 8) * 32 + t * 8 + g;
+  const double* P = ptab + ((size_t)(r0m / 4) * (J / 8) + j0 / 8) * 32 + g * 4 + t;
+  const double* H = htab + ((size_t)(r0m / 4) * (J / 8) + j0 / 8) * 32 + g * 4 + t;
   const size_t qstep = (size_t)3 * nb * 16;  // one row quad (k-step) of the operand
   const size_t pstr = (size_t)16 * nb;         // part stride
   const int nsteps = rows >> 2;
@@ -168,7 +169,6 @@ __global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : (NB <= 
       double aP0, aP1, aH0, aH1, bP[NT], bH[NPAIR];
     };
     auto fetch = [&](int s, Frag& f) {
-      const int r = 4 * s;
       const size_t off = (size_t)s * qstride;
       f.aP0 = __ldg(P + off);
       f.aP1 = __ldg(P + off + 32);
@@ -262,6 +262,184 @@ __global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : (NB <= 
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Synthesis with a per-warp cp.async pipeline: the A (table) and B (operand)
+// fragments of a warp's next kSynStages-1 k-steps are in flight as async copies
+// into shared memory (no registers held), so the K loop is no longer bound by
+// one L2 round trip per k-step.  Same arithmetic and reduction as k_synthesis.
+// ---------------------------------------------------------------------------
+constexpr int kSynStages = 3;
+template <int NB>
+constexpr int syn_stage_doubles() { return 128 + 96 * ((NB + 1) / 2); }
+template <int NB>
+constexpr size_t syn_cp_smem() { return (size_t)kWarps * kSynStages * syn_stage_doubles<NB>() * 8; }
+
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, bool valid = true) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int NB>
+__global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : (NB <= 4 ? SDCSW_SYN_MINB : 3)) k_synthesis_cp(
+    const double* __restrict__ xsyn, int nb, int T, int J, const double* __restrict__ ptab,
+    const double* __restrict__ htab, const int* __restrict__ rowoff,
+    const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ,
+    int NBC, const int* __restrict__ mlist, int Lp) {
+  SDCSW_PDL_ENTRY();
+  constexpr int NPAIR = (NB + 1) / 2;
+  constexpr int NT = 2 * NPAIR;
+  constexpr int NACC = NT * 2 * 4;
+  constexpr int STG = syn_stage_doubles<NB>();
+  __shared__ double red[2 * 32 * NACC];
+  extern __shared__ __align__(16) double synstage[];  // [warp][kSynStages][STG]
+
+  const int kpos = blockIdx.y;
+  const int m = mlist != nullptr ? mlist[kpos] : kpos;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int WK = (blockDim.x >> 5) / WJ;
+  const int jt = warp % WJ, ks = warp / WJ;
+  const int j0 = (blockIdx.x * WJ + jt) * kRowsPerWarp;
+  (void)T;
+  const int r0m = rowoff[m];
+  const int rows = rowoff[m + 1] - r0m;
+  const int le = n_even[m];
+  SDCSW_PDL_WAIT();
+  if (step_counter != nullptr && (blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0)
+    atomicAdd(step_counter, 1);
+  const size_t qstride = (size_t)(J / 8) * 32;
+  const double* Pb = ptab + ((size_t)(r0m / 4) * (J / 8) + j0 / 8) * 32;
+  const double* Hb = htab + ((size_t)(r0m / 4) * (J / 8) + j0 / 8) * 32;
+  const size_t qstep = (size_t)3 * nb * 16;
+  const size_t pstr = (size_t)16 * nb;
+  const int nsteps = rows >> 2;
+  const int se = le >> 2;
+  const int gb = g >> 2, gc = g & 3;
+  double* mys = synstage + warp * kSynStages * STG;
+  const int nk = ks < nsteps ? (nsteps - ks + WK - 1) / WK : 0;  // this warp's k-steps
+
+  for (int bb = 0; bb < NBC; ++bb) {
+    const int b0 = (blockIdx.z * NBC + bb) * NB;
+    if (b0 >= nb) break;
+    const int nbv = nb - b0 < NB ? nb - b0 : NB;
+    const double* Xb = xsyn + (size_t)(r0m / 4) * qstep + (size_t)b0 * 16;
+    double aE[2][NT][2], aO[2][NT][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < NT; ++c) aE[a][c][0] = aE[a][c][1] = aO[a][c][0] = aO[a][c][1] = 0.0;
+
+    // stage of this warp's k-th step: [P: 64][H: 64][operand: 3 parts x NPAIR pairs x 32]
+    auto issue = [&](int k) {
+      if (k < nk) {
+        const int s = ks + k * WK;
+        double* st = mys + (k % kSynStages) * STG;
+        cp_async16(st + 2 * lane, Pb + s * qstride + 2 * lane);
+        cp_async16(st + 64 + 2 * lane, Hb + s * qstride + 2 * lane);
+        const double* xq = Xb + (size_t)s * qstep;
+        for (int ci = lane; ci < 3 * NPAIR * 16; ci += 32) {
+          const int q = ci / (NPAIR * 16), r2 = ci - q * NPAIR * 16, p = r2 >> 4, w = r2 & 15;
+          cp_async16(st + 128 + (q * NPAIR + p) * 32 + 2 * w, xq + q * pstr + p * 32 + 2 * w,
+                     2 * p + (w >> 3) < nbv);
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < kSynStages - 1; ++k) issue(k);
+    for (int k = 0; k < nk; ++k) {
+      issue(k + kSynStages - 1);
+      cp_async_wait<kSynStages - 1>();
+      __syncwarp();
+      const double* st = mys + (k % kSynStages) * STG;
+      const double aP0 = st[lane], aP1 = st[32 + lane], aH0 = st[64 + lane], aH1 = st[96 + lane];
+      double bP[NT], bH[NPAIR];
+#pragma unroll
+      for (int p = 0; p < NPAIR; ++p) {
+        const double* bq = st + 128 + p * 32 + gb * 16 + t * 4 + gc;
+        bP[2 * p] = bq[0];
+        bP[2 * p + 1] = bq[NPAIR * 32];
+        bH[p] = bq[2 * NPAIR * 32];
+      }
+      if (ks + k * WK < se) {  // n - m even: P symmetric (E), H antisymmetric (O)
+#pragma unroll
+        for (int c = 0; c < NT; ++c) { dmma(aE[0][c], aP0, bP[c]); dmma(aE[1][c], aP1, bP[c]); }
+#pragma unroll
+        for (int p = 0; p < NPAIR; ++p) { dmma(aO[0][2 * p], aH0, bH[p]); dmma(aO[1][2 * p], aH1, bH[p]); }
+      } else {
+#pragma unroll
+        for (int c = 0; c < NT; ++c) { dmma(aO[0][c], aP0, bP[c]); dmma(aO[1][c], aP1, bP[c]); }
+#pragma unroll
+        for (int p = 0; p < NPAIR; ++p) { dmma(aE[0][2 * p], aH0, bH[p]); dmma(aE[1][2 * p], aH1, bH[p]); }
+      }
+      __syncwarp();  // the stage is refilled by a later issue()
+    }
+    cp_async_wait<0>();
+    bool owner = true;
+    if (WK > 1) {
+      for (int half = WK / 2; half >= 1; half /= 2) {
+        __syncthreads();
+        if (ks >= half && ks < 2 * half) {
+          double* d = red + ((ks - half) * WJ + jt) * NACC * 32 + lane;
+          int q = 0;
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int c = 0; c < NT; ++c) {
+              d[32 * q++] = aE[a][c][0]; d[32 * q++] = aE[a][c][1];
+              d[32 * q++] = aO[a][c][0]; d[32 * q++] = aO[a][c][1];
+            }
+        }
+        __syncthreads();
+        if (ks < half) {
+          const double* e = red + (ks * WJ + jt) * NACC * 32 + lane;
+          int q = 0;
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int c = 0; c < NT; ++c) {
+              aE[a][c][0] += e[32 * q++]; aE[a][c][1] += e[32 * q++];
+              aO[a][c][0] += e[32 * q++]; aO[a][c][1] += e[32 * q++];
+            }
+        }
+      }
+      owner = ks == 0;
+    }
+    if (owner && j0 < J) {
+#pragma unroll
+      for (int c = 0; c < NT; ++c) {
+        const int be = 2 * (c >> 1) + (t >> 1);
+        const int f = (t & 1) + 2 * (c & 1);
+        if (be >= nbv) continue;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const int j = j0 + 8 * a + g;
+          double2* dst = fsyn + ((((size_t)(b0 + be) * J + j) * Lp + kpos) * 4 + f) * 2;
+          dst[0] = make_double2(aE[a][c][0] + aO[a][c][0], aE[a][c][1] + aO[a][c][1]);
+          dst[1] = make_double2(aE[a][c][0] - aO[a][c][0], aE[a][c][1] - aO[a][c][1]);
+        }
+      }
+    }
+  }
+}
+
+#define SDCSW_NB_LIST(X) X(1) X(2) X(3) X(4) X(5) X(6)
+cudaError_t configure_synthesis() {
+  cudaError_t e = cudaSuccess;
+#define SDCSW_SYN_CFG(NBV)                                                                        \
+  if (e == cudaSuccess)                                                                          \
+    e = cudaFuncSetAttribute(k_synthesis_cp<NBV>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                             (int)syn_cp_smem<NBV>());
+  SDCSW_NB_LIST(SDCSW_SYN_CFG)
+#undef SDCSW_SYN_CFG
+  return e;
 }
 
 // ---------------------------------------------------------------------------
@@ -547,7 +725,6 @@ __global__ void SDCSW_ANA_LB k_analysis(
 
 static int pick_nb(int nb) { return nb <= 6 ? nb : 4; }
 
-#define SDCSW_NB_LIST(X) X(1) X(2) X(3) X(4) X(5) X(6)
 
 cudaError_t launch_synth_prep(const Plan& p, const double2* u, int nb, double* xsyn,
                               cudaStream_t s, int chunk) {
@@ -590,6 +767,10 @@ static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist
   // which the latency-bound small truncations need more (measured on B200)
 #define SDCSW_SYN(NBV)                                                                         \
   if (NB == NBV) {                                                                             \
+    if (p.syn_cp)                                                                              \
+      launch_k(k_synthesis_cp<NBV>, grid, block, syn_cp_smem<NBV>(), s, xsyn, nb, p.T, p.J,    \
+               p.ptab_s, p.htab_s, p.rowoff, p.n_even, fsyn, step_counter, WJ, NBC, mlist, Lp); \
+    else                                                                                       \
     launch_k(k_synthesis<NBV, 1>, grid, block, 0, s, xsyn, nb, p.T, p.J, p.ptab_s, p.htab_s, \
              p.rowoff, p.n_even, fsyn, step_counter, WJ, NBC, mlist, Lp);                      \
     return cudaGetLastError();                                                                 \

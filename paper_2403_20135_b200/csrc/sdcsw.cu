@@ -213,6 +213,9 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   // in flight), large ones give each warp its own row tile (B reuse via L1)
   p.anal_wj = T < 200 ? 1 : (T < 400 ? 2 : 4);
   p.synth_wj = T < 200 ? 1 : (T < 400 ? 2 : 4);
+  // cp.async-pipelined synthesis: measured faster from T255 up, slower at T127
+  p.syn_cp = T >= 200 ? 1 : 0;
+  if (const char* env = getenv("SDCSW_SYN_CP")) p.syn_cp = atoi(env);
   if (const char* env = getenv("SDCSW_ANAL_WJ")) p.anal_wj = atoi(env);
   if (const char* env = getenv("SDCSW_SYNTH_WJ")) p.synth_wj = atoi(env);
   while ((J / kRowsPerWarp) % p.synth_wj) p.synth_wj /= 2;
@@ -240,7 +243,7 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
     for (int j = 0; j < J; ++j) {
       const size_t src = (size_t)r * J + j;
       const size_t a = (((size_t)(r / 8) * (J / 4) + j / 4) * 8 + r % 8) * 4 + j % 4;
-      const size_t q = (((size_t)(r / 4) * (J / 8) + j / 8) * 4 + r % 4) * 8 + j % 8;
+      const size_t q = (((size_t)(r / 4) * (J / 8) + j / 8) * 8 + j % 8) * 4 + r % 4;
       pa[a] = ptab[src];
       ha[a] = htab[src];
       ps[q] = ptab[src];
@@ -272,6 +275,7 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
           cudaSuccess ||
       (e = cudaMalloc(&p.coef_dev, kCoefCap * sizeof(double))) != cudaSuccess ||
       (e = configure_ring(p.ring_smem)) != cudaSuccess ||
+      (e = configure_synthesis()) != cudaSuccess ||
       (e = make_table_maps(p)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess) {
     int st = cuda_status(e, "sdcsw_plan_create");
