@@ -245,6 +245,10 @@ class DeviceStepper:
         _native.check(self.lib.sdcsw_stepper_launches_per_step(self.handle, ctypes.byref(n)))
         self.launches_per_step = n.value
 
+    def set_graph_steps(self, n):
+        """Steps per replayed CUDA graph (1..64; results are bit-identical for any value)."""
+        _native.check(self.lib.sdcsw_stepper_set_option(self.handle, 3, int(n)), "set_option")
+
     def profile_step(self, u):
         """Advance ``u`` one step stage by stage; returns a StepReport with CUDA-event stage times."""
         n = self.n_sweeps + 2

@@ -419,3 +419,27 @@ def test_plans_of_different_sizes_coexist():
     small.f_expl(random_initial_state(small.grid, 1))
     assert np.array_equal(big.f_expl(u), a)
     small.close()
+
+
+def test_graph_steps_bitwise():
+    """Several steps per replayed graph (PDL across step boundaries) == one step
+    per graph == eager launches, bitwise, including a remainder."""
+    import torch
+
+    from paper_2403_20135_b200.integrators import DeviceStepper
+
+    p = gpu(63)
+    cfg = SdcConfig(table=CollocationTable.radau_right(3), n_sweeps=3,
+                    mode=SweepMode.DIAGONAL_PARALLEL, time_threads=3)
+    u0 = torch.from_numpy(random_initial_state(p.grid, 40)).to(p.device).contiguous()
+    st = DeviceStepper(p, cfg, 120.0, serial=False)
+    out = []
+    for g, graph in ((1, True), (8, True), (5, True), (1, False)):
+        st.set_graph_steps(g)
+        u = u0.clone()
+        st.run(u, 11, use_graph=graph)
+        torch.cuda.synchronize()
+        out.append(u)
+    for o in out[1:]:
+        assert torch.equal(out[0], o)
+    st.close()
