@@ -77,7 +77,7 @@ struct Plan {
   int* anal_work4;  // [n_anal_work4] row blocks of 4 tiles (throughput regime)
   int n_anal_work4;
   int synth_wj, anal_wj;  // row tiles per CTA (the other warps split K)
-  int syn_cp;             // synthesis with the cp.async pipeline (k_synthesis_cp)
+  int syn_cp;             // synthesis with the cp.async pipeline: 1 / 0 / -1 = automatic
   FftPlan fft;
   // workspaces
   double2* fsyn;    // [max_batch][J][L][4][2]

@@ -763,11 +763,14 @@ static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist
   }
   dim3 grid(p.J / (kRowsPerWarp * WJ), nm, (nblk + NBC - 1) / NBC);
   const dim3 block(32 * WJ * WK);
+  // the cp.async pipeline pays off from T255 up and for many batch blocks; at
+  // T127 with few blocks the register-prefetch kernel is faster (measured)
+  const bool cp = p.syn_cp >= 0 ? p.syn_cp != 0 : (p.T >= 200 || nblk >= 4);
   // prefetch depth 1: a deeper register prefetch costs a resident CTA per SM,
   // which the latency-bound small truncations need more (measured on B200)
 #define SDCSW_SYN(NBV)                                                                         \
   if (NB == NBV) {                                                                             \
-    if (p.syn_cp)                                                                              \
+    if (cp)                                                                                    \
       launch_k(k_synthesis_cp<NBV>, grid, block, syn_cp_smem<NBV>(), s, xsyn, nb, p.T, p.J,    \
                p.ptab_s, p.htab_s, p.rowoff, p.n_even, fsyn, step_counter, WJ, NBC, mlist, Lp); \
     else                                                                                       \

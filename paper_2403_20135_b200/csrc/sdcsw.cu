@@ -213,8 +213,8 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   // in flight), large ones give each warp its own row tile (B reuse via L1)
   p.anal_wj = T < 200 ? 1 : (T < 400 ? 2 : 4);
   p.synth_wj = T < 200 ? 1 : (T < 400 ? 2 : 4);
-  // cp.async-pipelined synthesis: measured faster from T255 up, slower at T127
-  p.syn_cp = T >= 200 ? 1 : 0;
+  // cp.async-pipelined synthesis: -1 = automatic (see synthesis_impl)
+  p.syn_cp = -1;
   if (const char* env = getenv("SDCSW_SYN_CP")) p.syn_cp = atoi(env);
   if (const char* env = getenv("SDCSW_ANAL_WJ")) p.anal_wj = atoi(env);
   if (const char* env = getenv("SDCSW_SYNTH_WJ")) p.synth_wj = atoi(env);
