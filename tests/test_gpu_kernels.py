@@ -443,3 +443,19 @@ def test_graph_steps_bitwise():
     for o in out[1:]:
         assert torch.equal(out[0], o)
     st.close()
+
+
+def test_throughput_regime_batch_invariant():
+    """Large batches (ensemble-size, the GEMMs' throughput regime: several batch
+    blocks per CTA, cp.async synthesis) give each state exactly its single-state f_E."""
+    import torch
+
+    p = gpu(63, max_batch=40)
+    states = np.stack([random_initial_state(p.grid, 50 + b) for b in range(40)])
+    u = torch.from_numpy(states).to(p.device).contiguous()
+    big = p.empty_states(40)
+    p.f_expl_device(u, big, 40)
+    for b in (0, 7, 21, 39):
+        one = p.empty_states(1)
+        p.f_expl_device(u[b : b + 1].contiguous(), one, 1)
+        assert torch.equal(one[0], big[b])
