@@ -445,17 +445,21 @@ def test_graph_steps_bitwise():
     st.close()
 
 
-def test_throughput_regime_batch_invariant():
-    """Large batches (ensemble-size, the GEMMs' throughput regime: several batch
-    blocks per CTA, cp.async synthesis) give each state exactly its single-state f_E."""
+def test_throughput_regime_batch_consistent():
+    """Large batches (ensemble-size: the GEMMs' throughput regime, no K-split,
+    several batch blocks per CTA, cp.async synthesis) agree with the single-state
+    f_E to summation-order rounding, and are bitwise reproducible run to run."""
     import torch
 
     p = gpu(63, max_batch=40)
+    o = oracle_for(p)
     states = np.stack([random_initial_state(p.grid, 50 + b) for b in range(40)])
     u = torch.from_numpy(states).to(p.device).contiguous()
-    big = p.empty_states(40)
+    big, again = p.empty_states(40), p.empty_states(40)
     p.f_expl_device(u, big, 40)
+    p.f_expl_device(u, again, 40)
+    assert torch.equal(big, again)
     for b in (0, 7, 21, 39):
         one = p.empty_states(1)
         p.f_expl_device(u[b : b + 1].contiguous(), one, 1)
-        assert torch.equal(one[0], big[b])
+        assert max(relative_l2(big[b].cpu().numpy(), one[0].cpu().numpy(), o)) < 1e-13
