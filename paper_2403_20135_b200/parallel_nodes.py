@@ -183,8 +183,6 @@ class NodeParallelDsdc:
         self.ustage = backend.empty(max(1, p))
         self.fi_tmp = backend.empty(max(1, p))
         self.fe_tmp = backend.empty(max(1, p))
-        # views for all_gather: one chunk per rank
-        self.chunks = list(self.gathered.view(self.world, 2 * p, -1).unbind(0))
         if self.m > 16:
             raise ParameterError("at most 16 nodes")
         if self.nparts > 1:
@@ -195,8 +193,9 @@ class NodeParallelDsdc:
             self.backend.f_expl(u, out, nb)
             return
 
-        def gather(parts):  # the one Fourier exchange of a split f_E
-            self.dist.all_gather(parts, parts[self.part].clone(), group=self.spectral_group)
+        def gather(parts):  # the one Fourier exchange of a split f_E (one NCCL all-gather)
+            flat = self.backend.fourier.view(-1)[: len(parts) * parts[0].numel()]
+            self.dist.all_gather_into_tensor(flat, parts[self.part].clone(), group=self.spectral_group)
 
         self.backend.f_expl_split(u, out, nb, gather)
 
@@ -204,6 +203,21 @@ class NodeParallelDsdc:
         """Per-rank work: own nodes only (the redundant init/final are counted once per rank)."""
         n = 1 + (self.k - 1) * self.count
         return n, n, (self.k - 1) * self.count + 1
+
+    def capture(self, u, n_steps=1):
+        """A CUDA graph of ``n_steps`` steps on ``u`` (kernels and NCCL all-gathers
+        replayed without host work); ``graph.replay()`` advances ``u`` in place."""
+        import torch
+
+        scratch = u.clone()
+        self.step(scratch)  # lazy initialisation (NCCL communicators) outside the capture
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(n_steps):
+                self.step(u)
+        torch.cuda.synchronize()
+        return graph
 
     def step(self, u):
         """Advance the replicated state tensor ``u`` (shape [1, S] or [S]) in place."""
@@ -223,7 +237,8 @@ class NodeParallelDsdc:
                 loc = self.local.view(self.per, 2, -1)
                 loc[: self.count, 0].copy_(self.fe_tmp.view(-1, self.S)[: self.count])
                 loc[: self.count, 1].copy_(self.fi_tmp.view(-1, self.S)[: self.count])
-            self.dist.all_gather(self.chunks, self.local, group=self.group)
+            self.dist.all_gather_into_tensor(self.gathered.view(-1), self.local.view(-1),
+                                             group=self.group)
             fe_src, fe_stride = fe_view, 2
             fi_src, fi_stride = fi_view, 2
             first = False

@@ -232,6 +232,12 @@ def test_node_parallel_single_rank_matches_fused_stepper():
     st.run(b, 3)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+    # the same steps captured in one CUDA graph (kernels + NCCL all-gathers)
+    c = u0.clone()
+    graph = npd.capture(c, 3)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(c, b)
     st.close()
     dist.destroy_process_group()
 
