@@ -59,13 +59,75 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
   }
   b = axmy_tri(b, c[M], fim);
   const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
-  store_tri(u_out + (size_t)ob * 3 * C2, C2, e, u);
+  if (u_out != nullptr) store_tri(u_out + (size_t)ob * 3 * C2, C2, e, u);
   store_tri(fi_out + (size_t)ob * 3 * C2, C2, e, f_impl_tri(u, phibar, lam));
   if (xsyn != nullptr) {  // synthesis B operand of the f_E that follows, in batch chunks
     const int nbt = gridDim.y * gridDim.z, ch = chunk > 0 ? chunk : nbt;
     const int cb = ob / ch, w = nbt - cb * ch < ch ? nbt - cb * ch : ch;
     write_xsyn_half(xsyn + (size_t)cb * rows * ch * kXsyn + xsyn_off(idx_row[e >> 1], ob - cb * ch, w),
                     16 * (size_t)w, e & 1, u.phi, u.zeta, u.delta, xscale[e >> 1]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The same node updates with one thread per element for all nodes of the
+// block [lo, lo + count): u0 and every fe_j, fi_j are read once (instead of
+// once per node), which is what makes the sweep HBM-bound at large T.  Same
+// rounded arithmetic as k_sweep_nodes (bit-identical).  M <= kFuseMaxNodes.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sweep_nodes_all(
+    int C2, int M, int lo, int count, NodeArgs cf, const double* __restrict__ u0,
+    const double* __restrict__ fe, long long fe_stride, const double* __restrict__ fi,
+    long long fi_stride, int first, double phibar, const double* __restrict__ lamv,
+    double* __restrict__ u_out, double* fi_out, const double2* __restrict__ xscale,
+    const int* __restrict__ idx_row, double* __restrict__ xsyn, long long fe_mstride,
+    long long fi_mstride, int rows, int chunk, const int* __restrict__ idx_list, int n_list) {
+  SDCSW_PDL_ENTRY();
+  constexpr int MX = kFuseMaxNodes;
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx_list != nullptr) {  // spectral split: own coefficients only
+    if (e >= 2 * n_list) return;
+    e = 2 * idx_list[e >> 1] + (e & 1);
+  }
+  if (e >= C2) return;
+  const double lam = lamv[e >> 1];
+  const double2 sc = xscale != nullptr ? xscale[e >> 1] : make_double2(0.0, 0.0);
+  const int row = xsyn != nullptr ? idx_row[e >> 1] : 0;
+  SDCSW_PDL_WAIT();
+  const int z = blockIdx.z;
+  u0 += (size_t)z * 3 * C2;
+  fe += z * fe_mstride;
+  fi += z * fi_mstride;
+  const Tri a0 = load_tri(u0, C2, e);
+  const Tri fi0 = f_impl_tri(a0, phibar, lam);
+  Tri F[MX], I[MX];
+#pragma unroll
+  for (int j = 0; j < MX; ++j)
+    if (j < M) {
+      F[j] = load_tri(fe + j * fe_stride, C2, e);
+      I[j] = first ? fi0 : load_tri(fi + j * fi_stride, C2, e);
+    }
+  const int nbt = count * gridDim.z, ch = chunk > 0 ? chunk : nbt;
+  for (int q = 0; q < count; ++q) {
+    const int m = lo + q;
+    const int ob = z * count + q;  // output batch entry
+    const double* c = cf.v + m * (M + 4);
+    Tri b = a0, fim = fi0;
+#pragma unroll
+    for (int j = 0; j < MX; ++j)
+      if (j < M) {
+        b = axpy_tri(b, c[j], add_tri(F[j], I[j]));
+        if (j == m) fim = I[j];
+      }
+    b = axmy_tri(b, c[M], fim);
+    const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
+    if (u_out != nullptr) store_tri(u_out + (size_t)ob * 3 * C2, C2, e, u);
+    store_tri(fi_out + (size_t)ob * 3 * C2, C2, e, f_impl_tri(u, phibar, lam));
+    if (xsyn != nullptr) {
+      const int cb = ob / ch, w = nbt - cb * ch < ch ? nbt - cb * ch : ch;
+      write_xsyn_half(xsyn + (size_t)cb * rows * ch * kXsyn + xsyn_off(row, ob - cb * ch, w),
+                      16 * (size_t)w, e & 1, u.phi, u.zeta, u.delta, sc);
+    }
   }
 }
 
@@ -281,6 +343,15 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                double2* fi_out, double* xsyn_out, cudaStream_t s, int members,
                                long long fe_mstride, long long fi_mstride, int chunk) {
   const long long S2 = 6LL * p.C;  // doubles per state
+  if (M <= kFuseMaxNodes) {  // one thread per element for all nodes of the block
+    dim3 grid = grid_for(p.own_idx ? p.n_own_idx : p.C, 1);
+    grid.z = members;
+    launch_k(k_sweep_nodes_all, grid, 256, 0, s, 2 * p.C, M, node_lo, count,
+             pack(coef_host, M * (M + 4)), D(u0), D(fe), fe_stride * S2, D(fi), fi_stride * S2,
+             first, p.phibar, p.lam, W(u_out), W(fi_out), p.xscale, p.idx_row, xsyn_out,
+             fe_mstride * S2, fi_mstride * S2, p.rows, chunk, p.own_idx, p.n_own_idx);
+    return cudaGetLastError();
+  }
   dim3 grid = grid_for(p.own_idx ? p.n_own_idx : p.C, count);
   grid.z = members;
   launch_k(k_sweep_nodes, grid, 256, 0, s, 2 * p.C, M, node_lo, pack(coef_host, M * (M + 4)),

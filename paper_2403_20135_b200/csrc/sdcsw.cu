@@ -743,8 +743,10 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
         const int lo = g * M / G, hi = (g + 1) * M / G, cnt = hi - lo;
         cudaStream_t sg = (G > 1 && !seq) ? st->side[g] : s;
         double* xs = planar ? nullptr : st->xsynM + (size_t)lo * E * p.rows * kXsyn;
+        // spherical: the node states reach the f_E only as synthesis operands (xs),
+        // so they are not stored; the planar f_E reads them from ustage
         e = launch_sweep_nodes(p, M, lo, cnt, coef, u, fe_cur, first ? 0 : 1,
-                               fi_cur, first ? 0 : 1, first, st->ustage + lo * S,
+                               fi_cur, first ? 0 : 1, first, planar ? st->ustage + lo * S : nullptr,
                                fi_new + lo * S, xs, sg, E, first ? 1 : mS, mS, p.fe_chunk);
         if (e != cudaSuccess) return e;
         e = planar ? planar_f_expl(p, st->ustage + lo * S, fe_new + lo * S, cnt * E, sg, nullptr)
