@@ -69,6 +69,36 @@ __device__ __forceinline__ Tri solve_tri(const Tri& b, double alpha, double a_ph
   u.delta = axpy1(b.delta, __dmul_rn(alpha, lam), u.phi);
   return u;
 }
+// both components (re, im) of coefficient idx: 16-byte accesses
+__device__ __forceinline__ void load_tri2(const double* __restrict__ s, int C, int idx, Tri& re,
+                                          Tri& im) {
+  const double2* q = reinterpret_cast<const double2*>(s);
+  const double2 a = q[idx], b = q[C + idx], c = q[2 * C + idx];
+  re = Tri{a.x, b.x, c.x};
+  im = Tri{a.y, b.y, c.y};
+}
+__device__ __forceinline__ void store_tri2(double* __restrict__ s, int C, int idx, const Tri& re,
+                                           const Tri& im) {
+  double2* q = reinterpret_cast<double2*>(s);
+  q[idx] = make_double2(re.phi, im.phi);
+  q[C + idx] = make_double2(re.zeta, im.zeta);
+  q[2 * C + idx] = make_double2(re.delta, im.delta);
+}
+// the whole synthesis-operand record of one coefficient (both components):
+// three 32-byte chunks, values as write_xsyn_half (internal.cuh) computes them
+__device__ __forceinline__ void write_xsyn_full(double* __restrict__ rec, size_t pstride,
+                                                const Tri& re, const Tri& im, double2 sc) {
+  const double sm = sc.x, sa = sc.y;
+  double2* p0 = reinterpret_cast<double2*>(rec);
+  double2* p1 = reinterpret_cast<double2*>(rec + pstride);
+  double2* p2 = reinterpret_cast<double2*>(rec + 2 * pstride);
+  p0[0] = make_double2(sm * im.delta, -sm * re.delta);  // U_P re, im
+  p0[1] = make_double2(sm * im.zeta, -sm * re.zeta);    // V_P re, im
+  p1[0] = make_double2(re.zeta, im.zeta);
+  p1[1] = make_double2(re.phi, im.phi);
+  p2[0] = make_double2(sa * re.zeta, sa * im.zeta);     // U_H
+  p2[1] = make_double2(-sa * re.delta, -sa * im.delta); // V_H
+}
 __device__ __forceinline__ bool finite_tri(const Tri& t) {
   return isfinite(t.phi) && isfinite(t.zeta) && isfinite(t.delta);
 }

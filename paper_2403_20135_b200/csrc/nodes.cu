@@ -70,13 +70,15 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
 }
 
 // ---------------------------------------------------------------------------
-// The same node updates with one thread per element for all nodes of the
-// block [lo, lo + count): u0 and every fe_j, fi_j are read once (instead of
-// once per node), which is what makes the sweep HBM-bound at large T.  Same
-// rounded arithmetic as k_sweep_nodes (bit-identical).  M <= kFuseMaxNodes.
+// The same node updates with one thread per coefficient (both components,
+// 16-byte accesses) for all nodes of the block [lo, lo + count): u0 and every
+// fe_j, fi_j are read once (instead of once per node) and the synthesis
+// operand is written in whole 32-byte chunks - the sweep is HBM-bound at large
+// T.  Same rounded arithmetic as k_sweep_nodes (bit-identical).
+// M <= kFuseMaxNodes.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_sweep_nodes_all(
-    int C2, int M, int lo, int count, NodeArgs cf, const double* __restrict__ u0,
+    int C, int M, int lo, int count, NodeArgs cf, const double* __restrict__ u0,
     const double* __restrict__ fe, long long fe_stride, const double* __restrict__ fi,
     long long fi_stride, int first, double phibar, const double* __restrict__ lamv,
     double* __restrict__ u_out, double* fi_out, const double2* __restrict__ xscale,
@@ -84,96 +86,120 @@ __global__ void __launch_bounds__(256) k_sweep_nodes_all(
     long long fi_mstride, int rows, int chunk, const int* __restrict__ idx_list, int n_list) {
   SDCSW_PDL_ENTRY();
   constexpr int MX = kFuseMaxNodes;
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx_list != nullptr) {  // spectral split: own coefficients only
-    if (e >= 2 * n_list) return;
-    e = 2 * idx_list[e >> 1] + (e & 1);
+    if (idx >= n_list) return;
+    idx = idx_list[idx];
   }
-  if (e >= C2) return;
-  const double lam = lamv[e >> 1];
-  const double2 sc = xscale != nullptr ? xscale[e >> 1] : make_double2(0.0, 0.0);
-  const int row = xsyn != nullptr ? idx_row[e >> 1] : 0;
+  if (idx >= C) return;
+  const double lam = lamv[idx];
+  const double2 sc = xscale != nullptr ? xscale[idx] : make_double2(0.0, 0.0);
+  const int row = xsyn != nullptr ? idx_row[idx] : 0;
   SDCSW_PDL_WAIT();
   const int z = blockIdx.z;
+  const int C2 = 2 * C;
   u0 += (size_t)z * 3 * C2;
   fe += z * fe_mstride;
   fi += z * fi_mstride;
-  const Tri a0 = load_tri(u0, C2, e);
-  const Tri fi0 = f_impl_tri(a0, phibar, lam);
-  Tri F[MX], I[MX];
+  Tri a0r, a0i;
+  load_tri2(u0, C, idx, a0r, a0i);
+  const Tri f0r = f_impl_tri(a0r, phibar, lam), f0i = f_impl_tri(a0i, phibar, lam);
+  Tri Fr[MX], Fi[MX], Ir[MX], Ii[MX];
 #pragma unroll
   for (int j = 0; j < MX; ++j)
     if (j < M) {
-      F[j] = load_tri(fe + j * fe_stride, C2, e);
-      I[j] = first ? fi0 : load_tri(fi + j * fi_stride, C2, e);
+      load_tri2(fe + j * fe_stride, C, idx, Fr[j], Fi[j]);
+      if (first) {
+        Ir[j] = f0r;
+        Ii[j] = f0i;
+      } else {
+        load_tri2(fi + j * fi_stride, C, idx, Ir[j], Ii[j]);
+      }
     }
   const int nbt = count * gridDim.z, ch = chunk > 0 ? chunk : nbt;
   for (int q = 0; q < count; ++q) {
     const int m = lo + q;
     const int ob = z * count + q;  // output batch entry
     const double* c = cf.v + m * (M + 4);
-    Tri b = a0, fim = fi0;
+    Tri br = a0r, bi = a0i, fmr = f0r, fmi = f0i;
 #pragma unroll
     for (int j = 0; j < MX; ++j)
       if (j < M) {
-        b = axpy_tri(b, c[j], add_tri(F[j], I[j]));
-        if (j == m) fim = I[j];
+        br = axpy_tri(br, c[j], add_tri(Fr[j], Ir[j]));
+        bi = axpy_tri(bi, c[j], add_tri(Fi[j], Ii[j]));
+        if (j == m) {
+          fmr = Ir[j];
+          fmi = Ii[j];
+        }
       }
-    b = axmy_tri(b, c[M], fim);
-    const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
-    if (u_out != nullptr) store_tri(u_out + (size_t)ob * 3 * C2, C2, e, u);
-    store_tri(fi_out + (size_t)ob * 3 * C2, C2, e, f_impl_tri(u, phibar, lam));
+    br = axmy_tri(br, c[M], fmr);
+    bi = axmy_tri(bi, c[M], fmi);
+    const Tri ur = solve_tri(br, c[M + 1], c[M + 2], c[M + 3], lam);
+    const Tri ui = solve_tri(bi, c[M + 1], c[M + 2], c[M + 3], lam);
+    if (u_out != nullptr) store_tri2(u_out + (size_t)ob * 3 * C2, C, idx, ur, ui);
+    store_tri2(fi_out + (size_t)ob * 3 * C2, C, idx, f_impl_tri(ur, phibar, lam),
+               f_impl_tri(ui, phibar, lam));
     if (xsyn != nullptr) {
       const int cb = ob / ch, w = nbt - cb * ch < ch ? nbt - cb * ch : ch;
-      write_xsyn_half(xsyn + (size_t)cb * rows * ch * kXsyn + xsyn_off(row, ob - cb * ch, w),
-                      16 * (size_t)w, e & 1, u.phi, u.zeta, u.delta, sc);
+      write_xsyn_full(xsyn + (size_t)cb * rows * ch * kXsyn + xsyn_off(row, ob - cb * ch, w),
+                      16 * (size_t)w, ur, ui, sc);
     }
   }
 }
 
-// ---------------------------------------------------------------------------
-// closing last-node solve; coef: w[0..M-1], wd, alpha, a_phi, a2_phi
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_final_node(
-    int C2, int M, NodeArgs cf, const double* __restrict__ u0, const double* __restrict__ fe,
+// closing last-node solve, one thread per coefficient (both components)
+__global__ void __launch_bounds__(256) k_final_node_c(
+    int C, int M, NodeArgs cf, const double* __restrict__ u0, const double* __restrict__ fe,
     long long fe_stride, const double* __restrict__ fi, long long fi_stride, int first,
     double phibar, const double* __restrict__ lamv, double* u_out, int* diverged,
     const int* step_counter, const double2* __restrict__ xscale, const int* __restrict__ idx_row,
     double* __restrict__ xsyn, long long fe_mstride, long long fi_mstride, int rows, int chunk,
     const int* __restrict__ idx_list, int n_list) {
   SDCSW_PDL_ENTRY();
-  SDCSW_PDL_WAIT();
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx_list != nullptr) {  // spectral split: own coefficients only
-    if (e >= 2 * n_list) return;
-    e = 2 * idx_list[e >> 1] + (e & 1);
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx_list != nullptr) {
+    if (idx >= n_list) return;
+    idx = idx_list[idx];
   }
-  if (e >= C2) return;
+  if (idx >= C) return;
+  const double lam = lamv[idx];
+  const double2 sc = xsyn != nullptr ? xscale[idx] : make_double2(0.0, 0.0);
+  const int row = xsyn != nullptr ? idx_row[idx] : 0;
+  SDCSW_PDL_WAIT();
   const int z = blockIdx.z;  // ensemble member
+  const int C2 = 2 * C;
   u0 += (size_t)z * 3 * C2;
   u_out += (size_t)z * 3 * C2;
   fe += z * fe_mstride;
   fi += z * fi_mstride;
-  const double lam = lamv[e >> 1];
-  const Tri a0 = load_tri(u0, C2, e);
-  const Tri fi0 = f_impl_tri(a0, phibar, lam);
+  Tri a0r, a0i;
+  load_tri2(u0, C, idx, a0r, a0i);
+  const Tri f0r = f_impl_tri(a0r, phibar, lam), f0i = f_impl_tri(a0i, phibar, lam);
   const double* c = cf.v;
-  Tri b = a0, fil = fi0;
+  Tri br = a0r, bi = a0i, flr = f0r, fli = f0i;
   for (int j = 0; j < M; ++j) {
-    const Tri ej = load_tri(fe + j * fe_stride, C2, e);
-    const Tri ij = first ? fi0 : load_tri(fi + j * fi_stride, C2, e);
-    b = axpy_tri(axpy_tri(b, c[j], ej), c[j], ij);
-    if (j == M - 1) fil = ij;
+    Tri er, ei, ir = f0r, ii = f0i;
+    load_tri2(fe + j * fe_stride, C, idx, er, ei);
+    if (!first) load_tri2(fi + j * fi_stride, C, idx, ir, ii);
+    br = axpy_tri(axpy_tri(br, c[j], er), c[j], ir);
+    bi = axpy_tri(axpy_tri(bi, c[j], ei), c[j], ii);
+    if (j == M - 1) {
+      flr = ir;
+      fli = ii;
+    }
   }
-  b = axmy_tri(b, c[M], fil);
-  const Tri u = solve_tri(b, c[M + 1], c[M + 2], c[M + 3], lam);
-  store_tri(u_out, C2, e, u);
-  if (diverged != nullptr && !finite_tri(u)) atomicMin(diverged, step_counter ? *step_counter : 1);
+  br = axmy_tri(br, c[M], flr);
+  bi = axmy_tri(bi, c[M], fli);
+  const Tri ur = solve_tri(br, c[M + 1], c[M + 2], c[M + 3], lam);
+  const Tri ui = solve_tri(bi, c[M + 1], c[M + 2], c[M + 3], lam);
+  store_tri2(u_out, C, idx, ur, ui);
+  if (diverged != nullptr && !(finite_tri(ur) && finite_tri(ui)))
+    atomicMin(diverged, step_counter ? *step_counter : 1);
   if (xsyn != nullptr) {  // B operand of the next step's f_E(u0) (batch = members, chunked)
     const int nbt = gridDim.z, ch = chunk > 0 ? chunk : nbt;
     const int cb = z / ch, w = nbt - cb * ch < ch ? nbt - cb * ch : ch;
-    write_xsyn_half(xsyn + (size_t)cb * rows * ch * kXsyn + xsyn_off(idx_row[e >> 1], z - cb * ch, w),
-                    16 * (size_t)w, e & 1, u.phi, u.zeta, u.delta, xscale[e >> 1]);
+    write_xsyn_full(xsyn + (size_t)cb * rows * ch * kXsyn + xsyn_off(row, z - cb * ch, w),
+                    16 * (size_t)w, ur, ui, sc);
   }
 }
 
@@ -343,10 +369,9 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                double2* fi_out, double* xsyn_out, cudaStream_t s, int members,
                                long long fe_mstride, long long fi_mstride, int chunk) {
   const long long S2 = 6LL * p.C;  // doubles per state
-  if (M <= kFuseMaxNodes) {  // one thread per element for all nodes of the block
-    dim3 grid = grid_for(p.own_idx ? p.n_own_idx : p.C, 1);
-    grid.z = members;
-    launch_k(k_sweep_nodes_all, grid, 256, 0, s, 2 * p.C, M, node_lo, count,
+  if (M <= kFuseMaxNodes) {  // one thread per coefficient for all nodes of the block
+    dim3 grid(((p.own_idx ? p.n_own_idx : p.C) + 255) / 256, 1, members);
+    launch_k(k_sweep_nodes_all, grid, 256, 0, s, p.C, M, node_lo, count,
              pack(coef_host, M * (M + 4)), D(u0), D(fe), fe_stride * S2, D(fi), fi_stride * S2,
              first, p.phibar, p.lam, W(u_out), W(fi_out), p.xscale, p.idx_row, xsyn_out,
              fe_mstride * S2, fi_mstride * S2, p.rows, chunk, p.own_idx, p.n_own_idx);
@@ -369,9 +394,8 @@ cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, con
                               const int* step_counter, double* xsyn_out, cudaStream_t s,
                               int members, long long fe_mstride, long long fi_mstride) {
   const long long S2 = 6LL * p.C;
-  dim3 grid = grid_for(p.own_idx ? p.n_own_idx : p.C);
-  grid.z = members;
-  launch_k(k_final_node, grid, 256, 0, s, 2 * p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
+  dim3 grid(((p.own_idx ? p.n_own_idx : p.C) + 255) / 256, 1, members);
+  launch_k(k_final_node_c, grid, 256, 0, s, p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
                                              fe_stride * S2, D(fi), fi_stride * S2, first, p.phibar,
                                              p.lam, W(u_out), diverged, step_counter, p.xscale,
                                              p.idx_row, xsyn_out, fe_mstride * S2, fi_mstride * S2,
