@@ -116,10 +116,37 @@ class ExperimentConfig:
         if pc not in _PRECOND:
             raise ConfigError(f"unknown preconditioner {pc!r}")
         self.preconditioner = _PRECOND[pc]
-        self.dt = float(get("stepper", "dt", required=True))
+        dt = get("stepper", "dt")
+        dt_list = get("stepper", "dt_list")
+        if dt is None and dt_list is None:
+            raise ConfigError("[stepper] needs 'dt' or 'dt_list'")
+        if dt_list is not None:
+            if not isinstance(dt_list, list) or not dt_list or not all(
+                    isinstance(v, (int, float)) and not isinstance(v, bool) and v > 0 for v in dt_list):
+                raise ConfigError("stepper.dt_list must be a non-empty list of positive step sizes")
+            dt_list = [float(v) for v in dt_list]
+        self.dt = float(dt if dt is not None else dt_list[0])
+        self.dt_list = dt_list if dt_list is not None else [self.dt]
         self.t_end = float(get("run", "t_end", required=True))
         if self.dt <= 0 or self.t_end <= 0:
             raise ConfigError("dt and t_end must be positive")
+        # work-precision / scaling sections (reference bench/config.py:296-340)
+        self.metric = data.get("metric", {}).get("kind", "rel")
+        if self.metric not in ("rel", "abs"):
+            raise ConfigError(f"metric must be 'rel' or 'abs', got {self.metric!r}")
+        ref = data.get("reference", {})
+        self.reference_scheme = ref.get("scheme", "imex-o2")
+        if self.reference_scheme not in SCHEMES:
+            raise ConfigError(f"unknown reference scheme {self.reference_scheme!r}")
+        self.reference_dt = float(ref["dt"]) if "dt" in ref else None
+        self.wp_schemes = data.get("workprecision", {}).get("schemes", [self.scheme])
+        for name in self.wp_schemes:
+            if name not in SCHEMES:
+                raise ConfigError(f"unknown scheme {name!r} in workprecision.schemes")
+        self.scaling_splits = [tuple(v) for v in data.get("scaling", {}).get("splits", [[1, 1]])]
+        for pair in self.scaling_splits:
+            if len(pair) != 2 or not all(isinstance(v, int) and v >= 1 for v in pair):
+                raise ConfigError(f"scaling.splits entries must be [space, time] positive pairs, got {pair!r}")
         self.checkpoint_interval = get("run", "checkpoint_interval")
         self.reps = int(get("run", "reps", 1))
         self.candidates = [dict(c) for c in data.get("speedup", {}).get("candidate", [])]
@@ -127,6 +154,8 @@ class ExperimentConfig:
             if c.get("scheme") not in SCHEMES or float(c.get("dt", 0)) <= 0:
                 raise ConfigError(f"bad speedup candidate {c}")
         self.n_steps(self.dt)
+        for d in self.dt_list:
+            self.n_steps(d)
         for c in self.candidates:
             self.n_steps(float(c["dt"]))
 
@@ -257,6 +286,147 @@ def run_single(config, out_dir):
         json.dump(report, f, indent=2, sort_keys=True)
     problem.close()
     return report
+
+
+def _reference_dt(config):
+    finest = min(config.dt_list)
+    if config.reference_dt is not None:
+        if config.reference_dt > finest / 8.0:
+            raise ConfigError(f"reference dt {config.reference_dt} coarser than one eighth of the "
+                              f"finest candidate dt {finest}")
+        return config.reference_dt
+    return finest / 64.0
+
+
+def _aligned_intervals(dts, reference_dt):
+    """Checkpoint intervals on multiples of the coarsest dt (None: endpoints only)."""
+    coarsest = max(dts)
+    out = []
+    for dt in list(dts) + [reference_dt]:
+        r = coarsest / dt
+        if abs(r - round(r)) > 1e-9:
+            return [None] * len(dts), None
+        out.append(int(round(r)))
+    return out[:-1], out[-1]
+
+
+def work_precision(config, out_dir):
+    """Error against wall time per (scheme, dt) - the reference's work-precision
+    sweep (``bench/harness.py:228-270``) on the GPU steppers.  Writes
+    ``work_precision.csv`` (scheme, dt, wall_s, error, status); errors use
+    :func:`.metrics.error_linf_l2` on the vorticity grid field against a fine
+    reference trajectory at checkpoints aligned on the coarsest step."""
+    from .errors import DivergenceError
+    from .metrics import error_linf_l2
+
+    os.makedirs(out_dir, exist_ok=True)
+    dts = sorted(config.dt_list, reverse=True)
+    ref_dt = _reference_dt(config)
+    intervals, ref_interval = _aligned_intervals(dts, ref_dt)
+    problem = build_problem(config)
+    state = build_initial_state(config, problem)
+    ref_stepper = build_stepper(config, config.reference_scheme)
+    try:
+        reference, _ = _timed(problem, state, ref_dt, config.n_steps(ref_dt), ref_stepper, ref_interval)
+    finally:
+        if getattr(ref_stepper, "cfg", None) is not None:
+            ref_stepper.cfg.close()
+    points = []
+    for scheme in config.wp_schemes:
+        for dt, interval in zip(dts, intervals):
+            stepper = build_stepper(config, scheme)
+            try:
+                traj, wall = _timed(problem, state, dt, config.n_steps(dt), stepper, interval)
+                error = error_linf_l2(traj, reference, problem, relative=config.metric == "rel")
+                status = "ok"
+            except DivergenceError:
+                error = wall = float("nan")
+                status = "diverged"
+            finally:
+                if getattr(stepper, "cfg", None) is not None:
+                    stepper.cfg.close()
+            points.append({"scheme": scheme, "dt": dt, "wall_s": wall, "error": error, "status": status})
+    with open(os.path.join(out_dir, "work_precision.csv"), "w", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=["scheme", "dt", "wall_s", "error", "status"])
+        w.writeheader()
+        w.writerows(points)
+    problem.close()
+    return points
+
+
+def strong_scaling(config, out_dir):
+    """Wall time across (space, time) splits - the reference's thread-split sweep
+    (``bench/harness.py:273-333``) mapped onto one GPU: the time split is the
+    number of concurrent node groups per sweep (1 = one node after another, the
+    DIAGONAL_SEQUENTIAL analogue; M = every node on its own graph branch) and
+    the space split has no GPU meaning (each row records it; only 1 runs).  A
+    "device" row adds the default fused step (all nodes batched into the GEMMs).
+    Writes ``strong_scaling.csv`` with the reference's columns."""
+    import torch
+
+    os.makedirs(out_dir, exist_ok=True)
+    splits = list(config.scaling_splits)
+    if (1, 1) not in splits:
+        splits.insert(0, (1, 1))
+    n = config.n_steps()
+    problem = build_problem(config)
+    state = build_initial_state(config, problem)
+    u0 = problem._to_device(state).reshape(-1).contiguous()
+    table = CollocationTable.radau_right(config.n_nodes)
+    cfg = SdcConfig(table=table, n_sweeps=config.n_sweeps, preconditioner=config.preconditioner,
+                    mode=SweepMode.DIAGONAL_PARALLEL, time_threads=config.n_nodes)
+    st = DeviceStepper(problem, cfg, config.dt, serial=False)
+
+    def wall(setup):
+        best = math.inf
+        for _ in range(max(1, config.reps)):
+            setup()
+            u = u0.clone()
+            st.run(u, 1)
+            u.copy_(u0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            st.run(u, n)
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    rows = []
+    for space, tpar in splits + [("device", "fused")]:
+        row = {"space_threads": space, "time_threads": tpar,
+               "total_threads": space * tpar if isinstance(space, int) else "device",
+               "wall_s": float("nan"), "time_per_dof_s": float("nan"), "status": "ok"}
+        try:
+            if space == "device":
+                def setup():
+                    st.set_sequential(False)
+                    st.set_chains(1)
+                    st.set_fused(True)
+            elif space != 1:
+                raise ConfigError("space_threads has no GPU meaning (the transforms are one device)")
+            elif tpar > config.n_nodes:
+                raise ConfigError(f"time_threads {tpar} > n_nodes {config.n_nodes}")
+            else:
+                def setup(tpar=tpar):
+                    st.set_fused(False)
+                    st.set_sequential(tpar == 1)
+                    if tpar > 1:
+                        st.set_sequential(False)
+                        st.set_chains(tpar)
+            w = wall(setup)
+            row["wall_s"] = w
+            row["time_per_dof_s"] = w / (n * problem.n_dof)
+        except (ConfigError, ParameterError) as exc:
+            row["status"] = f"skipped: {exc}"
+        rows.append(row)
+    with open(os.path.join(out_dir, "strong_scaling.csv"), "w", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=["space_threads", "time_threads", "total_threads", "wall_s",
+                                          "time_per_dof_s", "status"])
+        w.writeheader()
+        w.writerows(rows)
+    st.close()
+    problem.close()
+    return rows
 
 
 def speedup_report(config, out_dir):

@@ -233,6 +233,21 @@ class SphericalShallowWater(DeviceProblem):
     def n_dof(self):
         return self.grid.n_dof
 
+    def vorticity_physical(self, state):
+        """Vorticity on the Gaussian grid (host synthesis; diagnostics, not the hot path)."""
+        from .sphere import HostTransforms
+
+        if getattr(self, "_host", None) is None:
+            self._host = HostTransforms(self.grid)
+        h = self._host
+        c = self.n_coef
+        zeta = np.asarray(state)[c : 2 * c]
+        return h.to_grid(h._fourier(zeta, h.ptab))
+
+    def error_field(self, state):
+        """Field entering the work-precision error norm (as the planar problem's)."""
+        return self.vorticity_physical(state)
+
     def spectral_views(self, state):
         c = self.n_coef
         return state[:c], state[c : 2 * c], state[2 * c :]

@@ -142,3 +142,53 @@ def test_cli_planar_run_matches_reference_vectors(tmp_path):
     assert meta["n_grid"] == 24 and meta["time"] == 300.0
     gold = np.load(os.path.join(ROOT, "tests", "golden", "planar.npz"))
     assert max(relative_l2_fields(state, gold["jet24_dsdc5"])) <= 1e-10
+
+
+WP = """
+[problem]
+kind = "sphere-swe"
+trunc = 63
+seed = 3
+[stepper]
+scheme = "dsdc"
+n_nodes = 3
+n_sweeps = 3
+dt_list = [240.0, 120.0]
+[run]
+t_end = 960.0
+reps = 1
+[workprecision]
+schemes = ["dsdc", "imex-o2"]
+[scaling]
+splits = [[1, 1], [1, 3], [2, 1]]
+"""
+
+
+def test_workprecision_scaling_config(tmp_path):
+    cfg = load_config(write(tmp_path, WP))
+    assert cfg.dt_list == [240.0, 120.0] and cfg.wp_schemes == ["dsdc", "imex-o2"]
+    assert cfg.scaling_splits == [(1, 1), (1, 3), (2, 1)] and cfg.reference_scheme == "imex-o2"
+    with pytest.raises(ConfigError):
+        load_config(write(tmp_path, WP.replace("dt_list = [240.0, 120.0]", "dt_list = [250.0]"), "b.toml"))
+
+
+@pytest.mark.gpu
+def test_cli_work_precision_and_scaling(tmp_path):
+    import csv as _csv
+
+    path = write(tmp_path, WP)
+    out = tmp_path / "wp"
+    for cmd in ("work-precision", "scaling"):
+        r = subprocess.run([sys.executable, "-m", "paper_2403_20135_b200.cli", cmd, "--config", path,
+                            "--out", str(out)], cwd=ROOT, capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+    pts = list(_csv.DictReader(open(out / "work_precision.csv")))
+    assert [p["scheme"] for p in pts] == ["dsdc", "dsdc", "imex-o2", "imex-o2"]
+    err = {(p["scheme"], float(p["dt"])): float(p["error"]) for p in pts}
+    # dSDC (M=K=3, order <= 5) is far more accurate than the second-order IMEX at the same dt
+    assert err[("dsdc", 120.0)] < err[("imex-o2", 120.0)]
+    assert err[("imex-o2", 120.0)] < err[("imex-o2", 240.0)]
+    rows = list(_csv.DictReader(open(out / "strong_scaling.csv")))
+    status = {(r["space_threads"], r["time_threads"]): r["status"] for r in rows}
+    assert status[("1", "1")] == "ok" and status[("1", "3")] == "ok" and status[("device", "fused")] == "ok"
+    assert status[("2", "1")].startswith("skipped")
