@@ -60,7 +60,7 @@ def main():
     print(json.dumps({"problem": f"planar-swe N={a.n} balanced jet (the reference's own problem)",
                       "scheme": f"dSDC M={a.nodes} K={a.sweeps} dt={a.dt}",
                       "gpu_steps_per_s": gpu_rate, "cpu_steps_per_s": cpu_rate,
-                      "cpu_threads": os.cpu_count(), "cpu_sample_steps": a.cpu_steps,
+                      "cpu_threads": 1, "cpu_sample_steps": a.cpu_steps,
                       "speedup": gpu_rate / cpu_rate}))
 
 
