@@ -238,16 +238,28 @@ cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, c
 // so f_E never reaches HBM and the node kernels disappear from the step.
 constexpr int kFuseMaxNodes = 6;
 struct FuseArgs {
-  int mode;                 // 1: next sweep's node updates; 2: closing solve
+  int mode;                 // 1: next sweep's node updates; 2: closing solve; 3: serial SDC node
   int M, first;             // first: every node's tendencies are f_E(u0), f_I(u0)
   const double* u0;         // step-start state
   double* fi;               // f_I of the nodes [M][3C]: read, and (mode 1) updated in place
-  double* u_out;            // mode 2: the step's result (may alias u0)
-  double* xsyn;             // next synthesis operand (nb = M in mode 1, 1 in mode 2)
-  int* diverged;            // mode 2: atomicMin(step index) on a non-finite result
+  double* u_out;            // mode 2: the step's result (may alias u0); mode 3: last node's
+  double* xsyn;             // next synthesis operand (nb = M in mode 1, 1 in modes 2, 3)
+  int* diverged;            // modes 2, 3: atomicMin(step index) on a non-finite result
   const int* step_counter;
   double phibar;
-  double cf[kFuseMaxNodes * (kFuseMaxNodes + 4)];  // mode 1: [M][M+4]; mode 2: [M+4]
+  // mode 3 (serial sweep, f_E of node m just computed; serial_update(m) and
+  // serial_node(m + 1) of nodes.cu follow in the epilogue):
+  double* fe_new;           // fe of node m (stored)
+  const double* fe_old;     // fe of node m in the previous sweep (fe0 when first)
+  const double* fi_old;     // fi of node m in the previous sweep (unused when first)
+  const double* fi_new;     // fi of node m of this sweep
+  double* corr;             // running correction, updated in place
+  const double* quad_next;  // quad of node m + 1 (null: m is the sweep's last node)
+  const double* fi_old_next;  // fi of node m + 1 in the previous sweep (unused when first)
+  double* fi_new_next;      // fi of node m + 1 (out)
+  int use_corr;             // m > 0: the correction exists
+  double cf[kFuseMaxNodes * (kFuseMaxNodes + 4)];  // mode 1: [M][M+4]; mode 2: [M+4];
+                                                   // mode 3: we, wi, alpha, a_phi, a2_phi
 };
 // the TMA analysis (and the fragment-order analysis data it reads) is in use
 inline bool tma_active(const Plan& p) { return p.tma_ok && p.anal_wj == 4; }

@@ -475,6 +475,38 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
     fe[b].zeta = zero ? 0.0 : row[6 * b + 2 + ri];
     fe[b].delta = zero ? 0.0 : __fma_rn(l, row[6 * NB + 2 * b + ri], row[6 * b + 4 + ri]);
   }
+  if (fz.mode == 3) {  // serial SDC: store fe_m, serial_update(m), serial_node(m + 1)
+    store_tri(fz.fe_new, C2, e, fe[0]);
+    if (fz.quad_next == nullptr) return;
+    const Tri a0 = load_tri(fz.u0, C2, e);
+    const Tri fi0 = f_impl_tri(a0, fz.phibar, l);
+    const Tri eo = load_tri(fz.fe_old, C2, e);
+    const Tri fn = load_tri(fz.fi_new, C2, e);
+    const Tri fo = fz.first ? fi0 : load_tri(fz.fi_old, C2, e);
+    const Tri de = sub_tri(fe[0], eo), di = sub_tri(fn, fo);
+    const double we = fz.cf[0], wi = fz.cf[1];
+    Tri c;
+    if (fz.use_corr) {
+      c = axpy_tri(load_tri(fz.corr, C2, e), we, de);
+    } else {
+      c = Tri{__dmul_rn(we, de.phi), __dmul_rn(we, de.zeta), __dmul_rn(we, de.delta)};
+    }
+    const Tri corr = axpy_tri(c, wi, di);
+    store_tri(fz.corr, C2, e, corr);
+    // node m + 1: beta = quad + corr - alpha fi_old; u = solve; fi_new = f_I(u)
+    Tri b = add_tri(load_tri(fz.quad_next, C2, e), corr);
+    const Tri fo2 = fz.first ? fi0 : load_tri(fz.fi_old_next, C2, e);
+    b = axmy_tri(b, fz.cf[2], fo2);
+    const Tri u = solve_tri(b, fz.cf[2], fz.cf[3], fz.cf[4], l);
+    store_tri(fz.fi_new_next, C2, e, f_impl_tri(u, fz.phibar, l));
+    if (fz.u_out != nullptr) {
+      store_tri(fz.u_out, C2, e, u);
+      if (fz.diverged != nullptr && !finite_tri(u))
+        atomicMin(fz.diverged, fz.step_counter ? *fz.step_counter : 1);
+    }
+    write_xsyn_half(stage + xsyn_off(rr, 0, 1), 16, ri, u.phi, u.zeta, u.delta, xscale[idx]);
+    return;
+  }
   const int M = fz.M;
   const Tri a0 = load_tri(fz.u0, C2, e);
   const Tri fi0 = f_impl_tri(a0, fz.phibar, l);
@@ -692,6 +724,7 @@ __global__ void SDCSW_ANA_LB k_analysis(
     __shared__ alignas(16) double xstage[2][kRowsPerWarp * kFuseMaxNodes * kXsyn];
     double* stage = xstage[rt & 1];
     const int per = (fz.mode == 1 ? fz.M : 1) * kXsyn;  // doubles per tile row
+    const bool writes_operand = fz.mode != 3 || fz.quad_next != nullptr;
     for (int i = lane; i < kRowsPerWarp * per; i += 32) stage[i] = 0.0;
     __syncwarp();
     fused_nodes<NB>(fz, o, fn, fmo, m, C, lam, xscale, stage, lane);
@@ -699,7 +732,8 @@ __global__ void SDCSW_ANA_LB k_analysis(
     const int nrow = rows - rw < kRowsPerWarp ? rows - rw : kRowsPerWarp;
     double2* dst = reinterpret_cast<double2*>(fz.xsyn + (size_t)(r0m + rw) * per);
     const double2* src = reinterpret_cast<const double2*>(stage);
-    for (int i = lane; i < nrow * per / 2; i += 32) dst[i] = src[i];
+    if (writes_operand)
+      for (int i = lane; i < nrow * per / 2; i += 32) dst[i] = src[i];
     PH(4)
   } else {
   for (int it = lane; it < kRowsPerWarp * NB; it += 32) {

@@ -658,6 +658,10 @@ int sdcsw_check_finite(const double* x, long long n, int* flag, void* stream) {
 // ---------------------------------------------------------------------------
 // stepper
 // ---------------------------------------------------------------------------
+static bool serial_fused_active(const sdcsw_stepper* st) {
+  return st->fuse && st->mode == 1 && st->members == 1 && fuse_supported(st->plan->p, st->M);
+}
+
 static bool fused_active(const sdcsw_stepper* st) {
   return st->fuse && st->mode == 0 && st->members == 1 && st->chains == 1 && !st->sequential &&
          fuse_supported(st->plan->p, st->M);
@@ -696,9 +700,80 @@ static cudaError_t enqueue_step_fused(sdcsw_stepper* st, double2* u, cudaStream_
   return cudaSuccess;
 }
 
+// serial SDC with serial_update(m) and serial_node(m + 1) in the epilogue of
+// node m's analysis: per sweep quad + node 0 + M x (synthesis, ring, analysis)
+static cudaError_t enqueue_serial_fused(sdcsw_stepper* st, double2* u, cudaStream_t s) {
+  const Plan& p = st->plan->p;
+  const int M = st->M, K = st->K;
+  const size_t S = st->S;
+  int* diverged = st->flags;
+  int* counter = st->flags + 1;
+  const double* W = st->coef.data();
+  const double* we = W + M * M;
+  const double* wi = we + M;
+  const double* sc = wi + M;
+  const Work w = plan_work(p);
+  cudaError_t e = f_expl_prepped(p, w, st->xsyn1, st->fe0, 1, s, counter, 0);
+  if (e != cudaSuccess) return e;
+  double2* old_fe = st->fe0;
+  double2* old_fi = st->fi;
+  long long old_stride = 0;
+  int first = 1;
+  auto D = [](const double2* q) { return reinterpret_cast<const double*>(q); };
+  auto Wr = [](double2* q) { return reinterpret_cast<double*>(q); };
+  for (int k = 1; k <= K; ++k) {
+    double2* nfe = (k % 2) ? st->fe : st->feB;
+    double2* nfi = (k % 2) ? st->fi : st->fiB;
+    if ((e = launch_serial_quad(p, M, W, u, old_fe, old_stride, old_fi, old_stride, first,
+                                st->quad, s)) != cudaSuccess)
+      return e;
+    const bool last0 = k == K && M == 1;
+    if ((e = launch_serial_node(p, M, 0, sc, st->quad, st->corr, u, old_fi, first, st->ustage,
+                                last0 ? u : nullptr, nfi, last0 ? diverged : nullptr,
+                                last0 ? counter : nullptr, st->xsyn1, s)) != cudaSuccess)
+      return e;
+    for (int m = 0; m < M; ++m) {
+      if ((e = launch_synthesis(p, w, st->xsyn1, 1, s, nullptr)) != cudaSuccess) return e;
+      if ((e = launch_ring(p, w, 1, s)) != cudaSuccess) return e;
+      FuseArgs fz{};
+      fz.mode = 3;
+      fz.M = M;
+      fz.first = first;
+      fz.u0 = D(u);
+      fz.phibar = p.phibar;
+      fz.xsyn = st->xsyn1;
+      fz.fe_new = Wr(nfe + m * S);
+      fz.fe_old = D(old_fe + old_stride * m * S);
+      fz.fi_old = D(old_fi + old_stride * m * S);
+      fz.fi_new = D(nfi + m * S);
+      fz.corr = Wr(st->corr);
+      fz.use_corr = m > 0;
+      if (m + 1 < M) {
+        const bool last = k == K && m + 1 == M - 1;
+        fz.quad_next = D(st->quad + (m + 1) * S);
+        fz.fi_old_next = D(old_fi + old_stride * (m + 1) * S);
+        fz.fi_new_next = Wr(nfi + (m + 1) * S);
+        fz.u_out = last ? Wr(u) : nullptr;
+        fz.diverged = last ? diverged : nullptr;
+        fz.step_counter = last ? counter : nullptr;
+        fz.cf[0] = we[m];
+        fz.cf[1] = wi[m];
+        for (int q = 0; q < 3; ++q) fz.cf[2 + q] = sc[3 * (m + 1) + q];
+      }
+      if ((e = launch_analysis_fused(p, w, 1, fz, s)) != cudaSuccess) return e;
+    }
+    old_fe = nfe;
+    old_fi = nfi;
+    old_stride = 1;
+    first = 0;
+  }
+  return cudaSuccess;
+}
+
 static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
                                 cudaEvent_t* marks = nullptr) {
   if (marks == nullptr && fused_active(st)) return enqueue_step_fused(st, u, s);
+  if (marks == nullptr && serial_fused_active(st)) return enqueue_serial_fused(st, u, s);
   const Plan& p = st->plan->p;
   const int M = st->M, K = st->K;
   const size_t S = st->S;
@@ -893,7 +968,7 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   // node fills the GPU); large ones batch all nodes through the GEMMs (table
   // reuse).  SDCSW_CHAINS overrides.
   s->chains = 1;
-  s->fuse = mode == 0 && E == 1 && fuse_supported(p, M);
+  s->fuse = E == 1 && fuse_supported(p, M);
   if (const char* env = getenv("SDCSW_FUSE")) s->fuse = s->fuse && atoi(env) != 0;
   if (mode == 0) {
     s->chains = (p.kind == 0 && p.T < 200 && E == 1 && !s->fuse) ? (M < 2 ? M : 2) : 1;
@@ -959,7 +1034,8 @@ int sdcsw_stepper_launches_per_step(sdcsw_stepper* s, int* n) {
   if (!s || !n) return SDCSW_ERR_STATE;
   const int G = s->sequential ? s->M : s->chains;
   s->launches = s->mode == 0 ? (fused_active(s) ? 3 * s->K : 4 + 4 * G * (s->K - 1))
-                             : 3 + s->K * 5 * s->M;
+                             : (serial_fused_active(s) ? 3 + s->K * (2 + 3 * s->M)
+                                                       : 3 + s->K * 5 * s->M);
   *n = s->launches;
   return SDCSW_OK;
 }
@@ -1030,7 +1106,7 @@ int sdcsw_stepper_set_option(sdcsw_stepper* s, int option, int value) {
     if (value < 1 || value > 64) return SDCSW_ERR_PARAM;
     s->graph_steps = value;
   } else if (option == 2) {  // node updates fused into the analysis epilogue
-    if (value && (s->mode != 0 || s->members != 1 || !fuse_supported(s->plan->p, s->M)))
+    if (value && (s->members != 1 || !fuse_supported(s->plan->p, s->M)))
       return SDCSW_ERR_PARAM;
     s->fuse = value ? 1 : 0;
   } else {

@@ -469,3 +469,45 @@ def test_throughput_regime_batch_consistent():
         one = p.empty_states(1)
         p.f_expl_device(u[b : b + 1].contiguous(), one, 1)
         assert max(relative_l2(big[b].cpu().numpy(), one[0].cpu().numpy(), o)) < 1e-13
+
+
+@pytest.mark.parametrize("trunc,m_count,k_count", [(63, 3, 3), (63, 1, 2), (127, 4, 4), (63, 5, 1)])
+def test_serial_fused_epilogue_bitwise(trunc, m_count, k_count):
+    """Serial SDC with serial_update / serial_node in the analysis epilogue ==
+    the separate serial kernels, bitwise (divergence flag untouched)."""
+    import torch
+
+    from paper_2403_20135_b200.integrators import DeviceStepper
+
+    p = gpu(trunc)
+    cfg = SdcConfig(table=CollocationTable.radau_right(m_count), n_sweeps=k_count,
+                    mode=SweepMode.SERIAL)
+    u0 = torch.from_numpy(random_initial_state(p.grid, 60 + m_count)).to(p.device).contiguous()
+    st = DeviceStepper(p, cfg, 90.0, serial=True)
+    st.set_fused(True)
+    assert st.launches_per_step == 3 + k_count * (2 + 3 * m_count)
+    a = u0.clone()
+    st.run(a, 3)
+    st.set_fused(False)
+    assert st.launches_per_step == 3 + k_count * 5 * m_count
+    b = u0.clone()
+    st.run(b, 3)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert st.diverged() == 0
+    st.close()
+
+
+def test_serial_divergence_reports_step():
+    p = gpu(63)
+    u0 = random_initial_state(p.grid, 0) * 1e140
+    table = CollocationTable.radau_right(3)
+    cfg = SdcConfig(table=table, n_sweeps=3, mode=SweepMode.SERIAL)
+    o = oracle_for(p)
+    step = lambda pr, s, dt: osdc.serial_sdc(pr, s, dt, table, 3)  # noqa: E731
+    with pytest.raises(DivergenceError) as ref:
+        osdc.march(o, u0, 120.0, 6, step)
+    with pytest.raises(DivergenceError) as got:
+        integrate(p, u0, 120.0, 6, SerialSdcStepper(cfg), checkpoint_interval=6)
+    assert got.value.step_index == ref.value.step_index
+    cfg.close()
