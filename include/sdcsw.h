@@ -199,6 +199,51 @@ int sdcsw_split_info(sdcsw_plan* plan, int* Lp, int* n_own_m, int* n_own_idx);
 int sdcsw_split_f_expl_begin(sdcsw_plan* plan, const double* u, int nb, void* stream);
 int sdcsw_split_f_expl_end(sdcsw_plan* plan, double* fe, int nb, void* stream);
 
+/* Node-parallel dSDC over peer memory (replaces the reference's
+ * per-sweep thread-pool barrier, integrators.py:278-288, and the all-gather of
+ * the node tendencies).  One exchange object per rank (one process per GPU):
+ * rank r owns the contiguous node block [r P, min((r+1) P, M)), P = ceil(M /
+ * world).  Per full sweep the rank solves its nodes, evaluates their f_E, and
+ * the analysis kernel's epilogue stores (f_E, f_I) of its nodes straight into
+ * every rank's exchange buffer over NVLink (option 0 = 0: a copy kernel after
+ * a plain analysis instead); a one-thread signal kernel then posts the
+ * exchange number into every rank's flag word (release, system scope), and
+ * the next node kernel of every rank spins (acquire) until all ranks posted.
+ * The closing last-node solve and the next f_E(u0) run redundantly on every
+ * rank, so the state stays replicated and bit-identical to one GPU.  No NCCL
+ * call on the data path.
+ *   create: coef as sdcsw_stepper_create (mode 0); world <= 16.
+ *   ipc_handle / open_peers: export this rank's buffer (a cudaIpcMemHandle_t,
+ *     SDCSW_IPC_HANDLE_BYTES bytes) and open the handles of all ranks
+ *     (world x SDCSW_IPC_HANDLE_BYTES, rank order; the own entry is skipped).
+ *   base / attach_peer: the same for peers that live in this process
+ *     (device pointers of other exchange objects, peer access enabled).
+ *   phase: enqueue one phase of a step on u - 0 = operand prep + f_E(u0),
+ *     k = 1..K-1 = full sweep k with its exchange, K = closing solve.  A
+ *     caller may interleave the phases of several ranks on one stream.
+ *   run: n_steps steps (operand prep first); use_graph replays a captured
+ *     graph of up to 8 steps.
+ *   option 0: publish fused into the analysis epilogue (default 1 where the
+ *     plan supports it: spherical, T < 400, unsplit).
+ *   info: own node block and kernels per step.
+ * Every rank must run the same number of steps (the exchange counters stay
+ * in lock step); a rank with no nodes still signals every exchange. */
+#define SDCSW_IPC_HANDLE_BYTES 64
+typedef struct sdcsw_exchange sdcsw_exchange;
+int sdcsw_exchange_create(sdcsw_plan* plan, int n_nodes, int n_sweeps, const double* coef,
+                          int n_coef, int world, int rank, sdcsw_exchange** out);
+int sdcsw_exchange_ipc_handle(sdcsw_exchange* x, void* handle, int bytes);
+int sdcsw_exchange_open_peers(sdcsw_exchange* x, const void* handles, int bytes_each);
+int sdcsw_exchange_base(sdcsw_exchange* x, void** base);
+int sdcsw_exchange_attach_peer(sdcsw_exchange* x, int peer, void* base);
+int sdcsw_exchange_phase(sdcsw_exchange* x, double* u, int phase, void* stream);
+int sdcsw_exchange_run(sdcsw_exchange* x, double* u, int n_steps, int use_graph, void* stream);
+int sdcsw_exchange_set_option(sdcsw_exchange* x, int option, int value);
+int sdcsw_exchange_info(sdcsw_exchange* x, int* node_lo, int* node_count, int* launches_per_step);
+int sdcsw_exchange_diverged(sdcsw_exchange* x, int* step_index);
+int sdcsw_exchange_reset(sdcsw_exchange* x, void* stream);
+int sdcsw_exchange_destroy(sdcsw_exchange* x);
+
 /* out = x + w * y over n doubles, rounded as numpy's `x + w * y` (product, then
  * sum); out may alias x.  The vector update of the reference schemes
  * imex_o2_step / ab2_si_step (integrators.py:387-420). */

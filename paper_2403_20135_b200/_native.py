@@ -12,6 +12,7 @@ from .errors import DeviceError, DivergenceError, ParameterError
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsdcsw.so")
 
 SDCSW_OK, SDCSW_ERR_PARAM, SDCSW_ERR_CUDA, SDCSW_ERR_STATE, SDCSW_ERR_DIVERGED = range(5)
+IPC_HANDLE_BYTES = 64  # SDCSW_IPC_HANDLE_BYTES
 
 EXPORTS = (
     "sdcsw_plan_create",
@@ -39,6 +40,18 @@ EXPORTS = (
     "sdcsw_split_info",
     "sdcsw_split_f_expl_begin",
     "sdcsw_split_f_expl_end",
+    "sdcsw_exchange_create",
+    "sdcsw_exchange_ipc_handle",
+    "sdcsw_exchange_open_peers",
+    "sdcsw_exchange_base",
+    "sdcsw_exchange_attach_peer",
+    "sdcsw_exchange_phase",
+    "sdcsw_exchange_run",
+    "sdcsw_exchange_set_option",
+    "sdcsw_exchange_info",
+    "sdcsw_exchange_diverged",
+    "sdcsw_exchange_reset",
+    "sdcsw_exchange_destroy",
     "sdcsw_last_error",
     "sdcsw_version",
 )
@@ -102,6 +115,18 @@ _SIGS = {
     "sdcsw_split_info": [_p, _ip, _ip, _ip],
     "sdcsw_split_f_expl_begin": [_p, _p, _i, _p],
     "sdcsw_split_f_expl_end": [_p, _p, _i, _p],
+    "sdcsw_exchange_create": [_p, _i, _i, _dp, _i, _i, _i, ctypes.POINTER(_p)],
+    "sdcsw_exchange_ipc_handle": [_p, _p, _i],
+    "sdcsw_exchange_open_peers": [_p, _p, _i],
+    "sdcsw_exchange_base": [_p, ctypes.POINTER(_p)],
+    "sdcsw_exchange_attach_peer": [_p, _i, _p],
+    "sdcsw_exchange_phase": [_p, _p, _i, _p],
+    "sdcsw_exchange_run": [_p, _p, _i, _i, _p],
+    "sdcsw_exchange_set_option": [_p, _i, _i],
+    "sdcsw_exchange_info": [_p, _ip, _ip, _ip],
+    "sdcsw_exchange_diverged": [_p, _ip],
+    "sdcsw_exchange_reset": [_p, _p],
+    "sdcsw_exchange_destroy": [_p],
     "sdcsw_last_error": [],
     "sdcsw_version": [],
 }

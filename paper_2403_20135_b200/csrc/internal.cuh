@@ -232,13 +232,59 @@ cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, i
                              cudaStream_t s, int* step_counter);
 cudaError_t launch_ring(const Plan& p, const Work& w, int nb, cudaStream_t s);
 cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s);
+// ---------------------------------------------------------------------------
+// Peer exchange of node-parallel dSDC (peer.cu).  Each rank owns one exchange
+// buffer X = [2 parities][M nodes][2 (fe, fi)][3C] complex, mapped into every
+// peer (CUDA IPC over NVLink), and a control block.  Exchange n (the n-th
+// sweep of the run with a gather) is written by every rank into parity n & 1
+// of every rank's X with plain peer stores; the rank then posts n into
+// flag[rank] of every peer (release, system scope).  A consumer waits until
+// all flags >= its own seq = n (acquire) and reads parity n & 1 locally.  Two
+// parities suffice: a rank can only write exchange n + 2 after every rank
+// posted n + 1, which each rank does after it finished reading exchange n.
+// ---------------------------------------------------------------------------
+constexpr int kMaxPeers = 16;
+struct PeerCtrl {
+  unsigned long long seq;        // exchanges completed by this rank (its own posts)
+  unsigned long long pad[15];
+  unsigned long long flag[kMaxPeers];  // flag[q]: last exchange rank q posted here
+};
+struct PeerWait {
+  const PeerCtrl* ctrl;  // local control block (null: no exchange, plain pointers)
+  int world;
+  long long par_stride;  // doubles between the two parities of X
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Called by every thread of the CTA before any early return: waits for the
+// latest exchange of every rank and returns the parity offset (doubles) of X.
+__device__ __forceinline__ long long peer_wait(const PeerWait& pw) {
+  if (pw.ctrl == nullptr) return 0;
+  SDCSW_PDL_WAIT();  // seq was written by the preceding signal kernel
+  const unsigned long long s = *reinterpret_cast<const volatile unsigned long long*>(&pw.ctrl->seq);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < pw.world; ++q)
+      while (ld_acquire_sys(&pw.ctrl->flag[q]) < s) __nanosleep(32);
+  __syncthreads();
+  return (long long)(s & 1) * pw.par_stride;
+}
+#endif
+
 // Sweep-fused analysis (latency regime, one state, M <= kFuseMaxNodes): the
 // epilogue takes f_E of every node straight from shared memory and runs the
 // next sweep's node updates (mode 1) or the closing last-node solve (mode 2),
 // so f_E never reaches HBM and the node kernels disappear from the step.
 constexpr int kFuseMaxNodes = 6;
 struct FuseArgs {
-  int mode;                 // 1: next sweep's node updates; 2: closing solve; 3: serial SDC node
+  int mode;                 // 1: next sweep's node updates; 2: closing solve; 3: serial SDC node;
+                            // 4: publish f_E and f_I to the peers (node-parallel dSDC)
   int M, first;             // first: every node's tendencies are f_E(u0), f_I(u0)
   const double* u0;         // step-start state
   double* fi;               // f_I of the nodes [M][3C]: read, and (mode 1) updated in place
@@ -258,6 +304,13 @@ struct FuseArgs {
   const double* fi_old_next;  // fi of node m + 1 in the previous sweep (unused when first)
   double* fi_new_next;      // fi of node m + 1 (out)
   int use_corr;             // m > 0: the correction exists
+  // mode 4 (node-parallel publish, peer.cu): f_E of this rank's nodes
+  // [peer_lo, peer_lo + nb) and their f_I (peer_fi, [nb][3C]) are stored into
+  // parity (seq + 1) & 1 of every rank's exchange buffer
+  int peer_world, peer_lo;
+  const PeerCtrl* peer_ctrl;
+  const double* peer_fi;
+  double* peer_x[kMaxPeers];
   double cf[kFuseMaxNodes * (kFuseMaxNodes + 4)];  // mode 1: [M][M+4]; mode 2: [M+4];
                                                    // mode 3: we, wi, alpha, a_phi, a2_phi
 };
@@ -276,12 +329,14 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                const double2* u0, const double2* fe, long long fe_stride,
                                const double2* fi, long long fi_stride, int first, double2* u_out,
                                double2* fi_out, double* xsyn_out, cudaStream_t s, int members = 1,
-                               long long fe_mstride = 0, long long fi_mstride = 0, int chunk = 0);
+                               long long fe_mstride = 0, long long fi_mstride = 0, int chunk = 0,
+                               const PeerWait* pw = nullptr);
 cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, const double2* u0,
                               const double2* fe, long long fe_stride, const double2* fi,
                               long long fi_stride, int first, double2* u_out, int* diverged,
                               const int* step_counter, double* xsyn_out, cudaStream_t s,
-                              int members = 1, long long fe_mstride = 0, long long fi_mstride = 0);
+                              int members = 1, long long fe_mstride = 0, long long fi_mstride = 0,
+                              const PeerWait* pw = nullptr);
 cudaError_t launch_serial_quad(const Plan& p, int M, const double* w_host, const double2* u0,
                                const double2* fe, long long fe_stride, const double2* fi,
                                long long fi_stride, int first, double2* quad, cudaStream_t s);
@@ -318,3 +373,10 @@ cudaError_t f_expl_prepped(const Plan& p, const Work& w, const double* xsyn, dou
                            cudaStream_t s, int* step_counter, int chunk = 0);
 
 }  // namespace sdcsw
+
+// the C-ABI plan handle (include/sdcsw.h)
+struct sdcsw_plan {
+  sdcsw::Plan p;
+  bool alive;
+};
+

@@ -457,7 +457,7 @@ template <int NB>
 __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o, int n, int mo,
                                             int m, int C, const double* __restrict__ lamv,
                                             const double2* __restrict__ xscale, double* stage,
-                                            int lane) {
+                                            int lane, int b0, int nb) {
   constexpr int OS = 8 * NB + 1;
   constexpr int MX = kFuseMaxNodes;
   const int rr = lane & 15, ri = lane >> 4;
@@ -474,6 +474,21 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
     fe[b].phi = zero ? 0.0 : row[6 * b + ri];
     fe[b].zeta = zero ? 0.0 : row[6 * b + 2 + ri];
     fe[b].delta = zero ? 0.0 : __fma_rn(l, row[6 * NB + 2 * b + ri], row[6 * b + 4 + ri]);
+  }
+  if (fz.mode == 4) {  // node-parallel: publish (fe, fi) of this rank's nodes to every rank
+    const long long par = (long long)((fz.peer_ctrl->seq + 1) & 1);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      if (b0 + b >= nb) break;
+      const Tri fi = load_tri(fz.peer_fi + (size_t)(b0 + b) * S2, C2, e);
+      const size_t slot = ((size_t)par * fz.M + fz.peer_lo + b0 + b) * 2 * S2;
+      for (int q = 0; q < fz.peer_world; ++q) {
+        store_tri(fz.peer_x[q] + slot, C2, e, fe[b]);
+        store_tri(fz.peer_x[q] + slot + S2, C2, e, fi);
+      }
+    }
+    __threadfence_system();  // performed system-wide before this grid completes
+    return;
   }
   if (fz.mode == 3) {  // serial SDC: store fe_m, serial_update(m), serial_node(m + 1)
     store_tri(fz.fe_new, C2, e, fe[0]);
@@ -724,10 +739,11 @@ __global__ void SDCSW_ANA_LB k_analysis(
     __shared__ alignas(16) double xstage[2][kRowsPerWarp * kFuseMaxNodes * kXsyn];
     double* stage = xstage[rt & 1];
     const int per = (fz.mode == 1 ? fz.M : 1) * kXsyn;  // doubles per tile row
-    const bool writes_operand = fz.mode != 3 || fz.quad_next != nullptr;
-    for (int i = lane; i < kRowsPerWarp * per; i += 32) stage[i] = 0.0;
+    const bool writes_operand = fz.mode != 4 && (fz.mode != 3 || fz.quad_next != nullptr);
+    if (writes_operand)
+      for (int i = lane; i < kRowsPerWarp * per; i += 32) stage[i] = 0.0;
     __syncwarp();
-    fused_nodes<NB>(fz, o, fn, fmo, m, C, lam, xscale, stage, lane);
+    fused_nodes<NB>(fz, o, fn, fmo, m, C, lam, xscale, stage, lane, b0, nb);
     __syncwarp();
     const int nrow = rows - rw < kRowsPerWarp ? rows - rw : kRowsPerWarp;
     double2* dst = reinterpret_cast<double2*>(fz.xsyn + (size_t)(r0m + rw) * per);
@@ -846,7 +862,14 @@ cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, c
 
 cudaError_t launch_analysis_fused(const Plan& p, const Work& w, int nb, const FuseArgs& fz,
                                   cudaStream_t s) {
-  // one batch block must hold every node (NB = nb), and the epilogue fixes M
+  // one batch block must hold every node (NB = nb), and the epilogue fixes M;
+  // publishing (mode 4) handles any batch
+  if (fz.mode == 4) {
+    if (p.kind != 0 || p.tma_ok || p.own_idx != nullptr || fz.peer_world < 1 ||
+        fz.peer_world > kMaxPeers || nb < 1)
+      return cudaErrorInvalidValue;
+    return analysis_impl<true>(p, w, nullptr, nb, fz, s);
+  }
   if (!fuse_supported(p, fz.M) || nb > kFuseMaxNodes || (nb != 1 && nb != fz.M))
     return cudaErrorInvalidValue;
   return analysis_impl<true>(p, w, nullptr, nb, fz, s);

@@ -31,9 +31,13 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
     long long fi_stride, int first, double phibar, const double* __restrict__ lamv,
     double* __restrict__ u_out, double* fi_out, const double2* __restrict__ xscale,
     const int* __restrict__ idx_row, double* __restrict__ xsyn, long long fe_mstride,
-    long long fi_mstride, int rows, int chunk, const int* __restrict__ idx_list, int n_list) {
+    long long fi_mstride, int rows, int chunk, const int* __restrict__ idx_list, int n_list,
+    PeerWait pw) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
+  const long long par = peer_wait(pw);  // node-parallel: the latest exchange's parity
+  fe += par;
+  fi += par;
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx_list != nullptr) {  // spectral split: own coefficients only
     if (e >= 2 * n_list) return;
@@ -83,9 +87,13 @@ __global__ void __launch_bounds__(256) k_sweep_nodes_all(
     long long fi_stride, int first, double phibar, const double* __restrict__ lamv,
     double* __restrict__ u_out, double* fi_out, const double2* __restrict__ xscale,
     const int* __restrict__ idx_row, double* __restrict__ xsyn, long long fe_mstride,
-    long long fi_mstride, int rows, int chunk, const int* __restrict__ idx_list, int n_list) {
+    long long fi_mstride, int rows, int chunk, const int* __restrict__ idx_list, int n_list,
+    PeerWait pw) {
   SDCSW_PDL_ENTRY();
   constexpr int MX = kFuseMaxNodes;
+  const long long par = peer_wait(pw);  // node-parallel: the latest exchange's parity
+  fe += par;
+  fi += par;
   int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx_list != nullptr) {  // spectral split: own coefficients only
     if (idx >= n_list) return;
@@ -154,8 +162,11 @@ __global__ void __launch_bounds__(256) k_final_node_c(
     double phibar, const double* __restrict__ lamv, double* u_out, int* diverged,
     const int* step_counter, const double2* __restrict__ xscale, const int* __restrict__ idx_row,
     double* __restrict__ xsyn, long long fe_mstride, long long fi_mstride, int rows, int chunk,
-    const int* __restrict__ idx_list, int n_list) {
+    const int* __restrict__ idx_list, int n_list, PeerWait pw) {
   SDCSW_PDL_ENTRY();
+  const long long par = peer_wait(pw);  // node-parallel: the latest exchange's parity
+  fe += par;
+  fi += par;
   int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx_list != nullptr) {
     if (idx >= n_list) return;
@@ -367,14 +378,16 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                const double2* u0, const double2* fe, long long fe_stride,
                                const double2* fi, long long fi_stride, int first, double2* u_out,
                                double2* fi_out, double* xsyn_out, cudaStream_t s, int members,
-                               long long fe_mstride, long long fi_mstride, int chunk) {
+                               long long fe_mstride, long long fi_mstride, int chunk,
+                               const PeerWait* pw) {
   const long long S2 = 6LL * p.C;  // doubles per state
+  const PeerWait pwv = pw != nullptr ? *pw : PeerWait{nullptr, 0, 0};
   if (M <= kFuseMaxNodes) {  // one thread per coefficient for all nodes of the block
     dim3 grid(((p.own_idx ? p.n_own_idx : p.C) + 255) / 256, 1, members);
     launch_k(k_sweep_nodes_all, grid, 256, 0, s, p.C, M, node_lo, count,
              pack(coef_host, M * (M + 4)), D(u0), D(fe), fe_stride * S2, D(fi), fi_stride * S2,
              first, p.phibar, p.lam, W(u_out), W(fi_out), p.xscale, p.idx_row, xsyn_out,
-             fe_mstride * S2, fi_mstride * S2, p.rows, chunk, p.own_idx, p.n_own_idx);
+             fe_mstride * S2, fi_mstride * S2, p.rows, chunk, p.own_idx, p.n_own_idx, pwv);
     return cudaGetLastError();
   }
   dim3 grid = grid_for(p.own_idx ? p.n_own_idx : p.C, count);
@@ -384,7 +397,7 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                                      fi_stride * S2, first, p.phibar, p.lam,
                                                      W(u_out), W(fi_out), p.xscale, p.idx_row,
                                                      xsyn_out, fe_mstride * S2, fi_mstride * S2,
-                                                     p.rows, chunk, p.own_idx, p.n_own_idx);
+                                                     p.rows, chunk, p.own_idx, p.n_own_idx, pwv);
   return cudaGetLastError();
 }
 
@@ -392,14 +405,16 @@ cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, con
                               const double2* fe, long long fe_stride, const double2* fi,
                               long long fi_stride, int first, double2* u_out, int* diverged,
                               const int* step_counter, double* xsyn_out, cudaStream_t s,
-                              int members, long long fe_mstride, long long fi_mstride) {
+                              int members, long long fe_mstride, long long fi_mstride,
+                              const PeerWait* pw) {
   const long long S2 = 6LL * p.C;
+  const PeerWait pwv = pw != nullptr ? *pw : PeerWait{nullptr, 0, 0};
   dim3 grid(((p.own_idx ? p.n_own_idx : p.C) + 255) / 256, 1, members);
   launch_k(k_final_node_c, grid, 256, 0, s, p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
                                              fe_stride * S2, D(fi), fi_stride * S2, first, p.phibar,
                                              p.lam, W(u_out), diverged, step_counter, p.xscale,
                                              p.idx_row, xsyn_out, fe_mstride * S2, fi_mstride * S2,
-                                             p.rows, p.fe_chunk, p.own_idx, p.n_own_idx);
+                                             p.rows, p.fe_chunk, p.own_idx, p.n_own_idx, pwv);
   return cudaGetLastError();
 }
 

@@ -79,11 +79,6 @@ static cudaError_t upload(T** dst, const T* src, size_t n, size_t pad = 0) {
 
 using namespace sdcsw;
 
-struct sdcsw_plan {
-  Plan p;
-  bool alive;
-};
-
 struct sdcsw_stepper {
   sdcsw_plan* plan;
   int mode, M, K;

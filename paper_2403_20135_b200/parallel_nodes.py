@@ -244,3 +244,138 @@ class NodeParallelDsdc:
             first = False
         b.final_node(self.m, self.final_coef, u, fe_src, fe_stride, fi_src, fi_stride, first, u)
         return u
+
+
+class PeerNodeParallelDsdc:
+    """Node-parallel dSDC with the per-sweep exchange done by the kernels over
+    peer memory (``sdcsw_exchange_*``, ``csrc/peer.cu``): the analysis epilogue
+    of each rank stores (f_E, f_I) of its own nodes into every rank's exchange
+    buffer through NVLink and the next node kernel waits on per-rank flags -
+    no NCCL call and no host synchronisation on the data path.  Same node
+    partition and bit-identical results as :class:`NodeParallelDsdc`.
+
+    ``group`` (torch.distributed) is used once, to exchange the CUDA IPC
+    handles of the buffers; with ``world == 1`` no process group is needed."""
+
+    def __init__(self, problem, cfg, dt, group=None, world=None, rank=None, fused=None,
+                 exchange_handles=True):
+        import ctypes
+
+        from . import _native
+
+        self.problem = problem
+        self.lib = problem._lib
+        if world is None:
+            import torch.distributed as dist
+
+            if dist.is_available() and dist.is_initialized():
+                world, rank = dist.get_world_size(group), dist.get_rank(group)
+            else:
+                world, rank = 1, 0
+        self.world, self.rank = int(world), int(rank)
+        self.m = cfg.table.n_nodes
+        self.k = cfg.n_sweeps
+        scalars = getattr(problem, "solve_coefficients", None)
+        self._coef = np.ascontiguousarray(
+            diagonal_step_coefficients(cfg, dt, problem.mean_geopotential, scalars))
+        handle = ctypes.c_void_p()
+        _native.check(
+            self.lib.sdcsw_exchange_create(problem.handle, self.m, self.k, _native.dptr(self._coef),
+                                           self._coef.size, self.world, self.rank,
+                                           ctypes.byref(handle)),
+            "sdcsw_exchange_create",
+        )
+        self.handle = handle
+        if fused is not None:
+            self.set_fused(fused)
+        if self.world > 1 and exchange_handles:
+            import torch.distributed as dist
+
+            mine = ctypes.create_string_buffer(_native.IPC_HANDLE_BYTES)
+            _native.check(self.lib.sdcsw_exchange_ipc_handle(handle, mine, _native.IPC_HANDLE_BYTES))
+            every = [None] * self.world
+            dist.all_gather_object(every, mine.raw, group=group)
+            blob = ctypes.create_string_buffer(b"".join(every), self.world * _native.IPC_HANDLE_BYTES)
+            _native.check(self.lib.sdcsw_exchange_open_peers(handle, blob, _native.IPC_HANDLE_BYTES),
+                          "sdcsw_exchange_open_peers")
+
+    @classmethod
+    def in_process(cls, problem, cfg, dt, world, fused=None):
+        """``world`` exchange objects of one process on one device, attached to
+        each other directly (no IPC) - for driving several ranks' phases in
+        stream order (:meth:`phase`)."""
+        import ctypes
+
+        from . import _native
+
+        ranks = [cls(problem, cfg, dt, world=world, rank=r, fused=fused, exchange_handles=False)
+                 for r in range(world)]
+        bases = []
+        for x in ranks:
+            b = ctypes.c_void_p()
+            _native.check(x.lib.sdcsw_exchange_base(x.handle, ctypes.byref(b)))
+            bases.append(b)
+        for x in ranks:
+            for q, b in enumerate(bases):
+                if q != x.rank:
+                    _native.check(x.lib.sdcsw_exchange_attach_peer(x.handle, q, b),
+                                  "sdcsw_exchange_attach_peer")
+        return ranks
+
+    def set_fused(self, on=True):
+        """Publish from the analysis epilogue (default where supported) or by a copy kernel."""
+        from . import _native
+
+        _native.check(self.lib.sdcsw_exchange_set_option(self.handle, 0, int(bool(on))),
+                      "sdcsw_exchange_set_option")
+
+    def info(self):
+        """(node_lo, node_count, kernels per step) of this rank."""
+        import ctypes
+
+        lo, cnt, n = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        self.lib.sdcsw_exchange_info(self.handle, ctypes.byref(lo), ctypes.byref(cnt), ctypes.byref(n))
+        return lo.value, cnt.value, n.value
+
+    def counts_per_step(self):
+        """Per-rank evaluations (own nodes; the redundant init/final counted once per rank)."""
+        _, count, _ = self.info()
+        n = 1 + (self.k - 1) * count
+        return n, n, (self.k - 1) * count + 1
+
+    def phase(self, u, phase):
+        """Enqueue one phase of a step on ``u``: 0 = f_E(u0), 1..K-1 = sweep with its exchange,
+        K = closing solve."""
+        from . import _native
+
+        _native.check(self.lib.sdcsw_exchange_phase(self.handle, u.data_ptr(), int(phase),
+                                                    self.problem.stream()), "sdcsw_exchange_phase")
+
+    def run(self, u, n_steps, use_graph=True):
+        """Advance the replicated device state ``u`` by ``n_steps`` steps in place."""
+        from . import _native
+
+        _native.check(self.lib.sdcsw_exchange_run(self.handle, u.data_ptr(), int(n_steps),
+                                                  int(bool(use_graph)), self.problem.stream()),
+                      "sdcsw_exchange_run")
+
+    def diverged(self):
+        """First non-finite step index of the run (0 = none); synchronises."""
+        import ctypes
+
+        v = ctypes.c_int()
+        from . import _native
+
+        _native.check(self.lib.sdcsw_exchange_diverged(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def close(self):
+        if self.handle is not None:
+            self.lib.sdcsw_exchange_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,159 @@
+"""Node-parallel dSDC over peer memory (csrc/peer.cu, sdcsw_exchange_*) on one
+B200.
+
+World size 1 runs the full protocol (publish into the exchange buffer, post
+the flag, wait, read the parity) against the process's own buffer.  Larger
+worlds run as several exchange objects of one process attached to each other,
+with the phases of all ranks interleaved on ONE stream: every wait is already
+satisfied by kernels earlier in the stream, so no kernel ever waits on a
+concurrently running one.  Each rank must end bit-identical to the
+single-GPU stepper (the reference's thread-count invariance,
+pkg/tests/test_integrators.py:190-225)."""
+
+import pytest
+
+from paper_2403_20135_b200 import CollocationTable, SdcConfig, SweepMode, random_initial_state
+
+pytestmark = pytest.mark.gpu
+
+_P = {}
+
+
+def gpu(trunc, max_batch=8):
+    key = (trunc, max_batch)
+    if key not in _P:
+        from paper_2403_20135_b200.problem import SphericalShallowWater
+
+        _P[key] = SphericalShallowWater(trunc, max_batch=max_batch)
+    return _P[key]
+
+
+def _cfg(m, k):
+    return SdcConfig(table=CollocationTable.radau_right(m), n_sweeps=k,
+                     mode=SweepMode.DIAGONAL_PARALLEL, time_threads=1)
+
+
+def _stepper_result(p, cfg, dt, u0, n):
+    from paper_2403_20135_b200.integrators import DeviceStepper
+
+    b = u0.clone()
+    st = DeviceStepper(p, cfg, dt, serial=False)
+    st.run(b, n)
+    st.close()
+    return b
+
+
+@pytest.mark.parametrize("trunc,m,k", [(63, 3, 3), (127, 4, 4), (63, 2, 1), (63, 6, 2)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_exchange_single_rank_bitwise(trunc, m, k, fused):
+    import torch
+
+    from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+
+    p = gpu(trunc)
+    cfg = _cfg(m, k)
+    u0 = torch.from_numpy(random_initial_state(p.grid, 3)).to(p.device)
+    ref = _stepper_result(p, cfg, 90.0, u0, 5)
+    x = PeerNodeParallelDsdc(p, cfg, 90.0, world=1, rank=0, fused=fused)
+    assert x.info()[:2] == (0, m)
+    a = u0.clone()
+    x.run(a, 5, use_graph=False)
+    torch.cuda.synchronize()
+    assert torch.equal(a, ref)
+    c = u0.clone()
+    x.run(c, 2, use_graph=True)   # one-step graph twice
+    x.run(c, 3, use_graph=True)
+    torch.cuda.synchronize()
+    assert torch.equal(c, ref)
+    x.close()
+
+
+@pytest.mark.parametrize("m,world", [(4, 2), (4, 4), (3, 2), (5, 3), (2, 4), (6, 4)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_exchange_ranks_interleaved_bitwise(m, world, fused):
+    import torch
+
+    from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc, node_block
+
+    p = gpu(63)
+    k = 3
+    cfg = _cfg(m, k)
+    u0 = torch.from_numpy(random_initial_state(p.grid, 11)).to(p.device)
+    n_steps = 4
+    ref = _stepper_result(p, cfg, 120.0, u0, n_steps)
+    ranks = PeerNodeParallelDsdc.in_process(p, cfg, 120.0, world, fused=fused)
+    for x in ranks:
+        lo, count, _ = node_block(m, world, x.rank)
+        assert x.info()[:2] == (lo, count)
+    states = [u0.clone() for _ in ranks]
+    for _ in range(n_steps):
+        for ph in range(k + 1):
+            for x, u in zip(ranks, states):
+                x.phase(u, ph)
+    torch.cuda.synchronize()
+    for u in states:
+        assert torch.equal(u, ref)
+    for x in ranks:
+        assert x.diverged() == 0
+        x.close()
+
+
+def test_exchange_table_streaming_copy_publish():
+    """T511 (TMA analysis, no fused epilogue): the copy-kernel publish."""
+    import torch
+
+    from paper_2403_20135_b200.errors import ParameterError
+    from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+
+    p = gpu(511, max_batch=4)
+    cfg = _cfg(3, 2)
+    u0 = torch.from_numpy(random_initial_state(p.grid, 5)).to(p.device)
+    ref = _stepper_result(p, cfg, 30.0, u0, 2)
+    ranks = PeerNodeParallelDsdc.in_process(p, cfg, 30.0, 2)
+    with pytest.raises(ParameterError):
+        ranks[0].set_fused(True)
+    states = [u0.clone() for _ in ranks]
+    for _ in range(2):
+        for ph in range(3):
+            for x, u in zip(ranks, states):
+                x.phase(u, ph)
+    torch.cuda.synchronize()
+    for u in states:
+        assert torch.equal(u, ref)
+    for x in ranks:
+        x.close()
+
+
+def test_exchange_divergence_step_index():
+    import torch
+
+    from paper_2403_20135_b200.integrators import DeviceStepper
+    from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+
+    p = gpu(63)
+    cfg = _cfg(3, 3)
+    u0 = torch.from_numpy(random_initial_state(p.grid, 0) * 1e140).to(p.device)
+    st = DeviceStepper(p, cfg, 120.0, serial=False)
+    b = u0.clone()
+    st.run(b, 6)
+    want = st.diverged()
+    st.close()
+    assert want > 0
+    x = PeerNodeParallelDsdc(p, cfg, 120.0, world=1, rank=0)
+    a = u0.clone()
+    x.run(a, 6)
+    assert x.diverged() == want
+    x.close()
+
+
+def test_exchange_launch_count():
+    from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+
+    p = gpu(127)
+    ranks = PeerNodeParallelDsdc.in_process(p, _cfg(4, 4), 90.0, 4)
+    # init f_E 3 + 3 sweeps x (node, synthesis, ring, analysis, signal) + final
+    assert [x.info()[2] for x in ranks] == [19] * 4
+    ranks[0].set_fused(False)
+    assert ranks[0].info()[2] == 22
+    for x in ranks:
+        x.close()
