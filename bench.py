@@ -328,6 +328,16 @@ def run_device(args):
 
         def one_run():
             stepper.run(u, nsteps, use_graph=True)
+    elif args.transport == "p2p" and world <= m_nodes:
+        from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+
+        # node blocks over the ranks; the per-sweep exchange runs in the kernels
+        # over peer memory (analysis epilogue stores + flags), no NCCL on the data path
+        xpeer = PeerNodeParallelDsdc(problem, cfg, dt)
+        launches_per_sim_step = xpeer.info()[2]
+
+        def one_run():
+            xpeer.run(u, nsteps, use_graph=True)
     else:
         from paper_2403_20135_b200.parallel_nodes import CudaNodeBackend, NodeParallelDsdc
 
@@ -467,9 +477,11 @@ def run_device(args):
                             + (f", {total_members} ensemble members ({members} per GPU), value = aggregate member-steps/s"
                                if ensemble else ""),
                 "bench_step": f"one full {nsteps}-step run", "l2": "flushed between bench steps (256 MiB write, untimed)",
-                "parallelism": ("1 GPU: M nodes as concurrent graph branches / batched GEMM columns" if world == 1
+                "parallelism": ("1 GPU: M nodes as concurrent graph branches / batched GEMM columns" if world == 1 and not multi
                                 else f"{world} GPUs: ensemble members sharded" if ensemble
-                                else f"{world} GPUs: node blocks x spectral (m) split, NCCL all-gathers per sweep / per f_E"),
+                                else (f"{world} GPUs: node blocks, (f_E, f_I) exchanged over peer memory by the analysis epilogue (no NCCL on the data path)"
+                                      if args.transport == "p2p" and world <= m_nodes
+                                      else f"{world} GPUs: node blocks x spectral (m) split, NCCL all-gathers per sweep / per f_E")),
                 "ms_per_sim_step": t_dev / sim_steps * 1e3,
                 "node_sweeps_per_s": value * node_sweeps,
                 "serial_sdc_steps_per_s_1gpu": serial_rate,
@@ -504,6 +516,9 @@ def main():
     ap.add_argument("--node-parallel", action="store_true",
                     help="use the multi-GPU node/spectral orchestration even at world size 1 "
                          "(exercises the N>1 code path on one GPU)")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="node-parallel exchange: kernels over peer memory (default; world <= M) "
+                         "or NCCL all-gathers (also the spectral split when world > M)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

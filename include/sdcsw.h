@@ -206,9 +206,9 @@ int sdcsw_split_f_expl_end(sdcsw_plan* plan, double* fe, int nb, void* stream);
  * world).  Per full sweep the rank solves its nodes, evaluates their f_E, and
  * the analysis kernel's epilogue stores (f_E, f_I) of its nodes straight into
  * every rank's exchange buffer over NVLink (option 0 = 0: a copy kernel after
- * a plain analysis instead); a one-thread signal kernel then posts the
- * exchange number into every rank's flag word (release, system scope), and
- * the next node kernel of every rank spins (acquire) until all ranks posted.
+ * a plain analysis instead); the next node kernel of every rank first posts
+ * the exchange number into every rank's flag word (system-scope atomic, after
+ * the publishing grid completed) and spins (acquire) until all ranks posted.
  * The closing last-node solve and the next f_E(u0) run redundantly on every
  * rank, so the state stays replicated and bit-identical to one GPU.  No NCCL
  * call on the data path.
@@ -219,15 +219,20 @@ int sdcsw_split_f_expl_end(sdcsw_plan* plan, double* fe, int nb, void* stream);
  *   base / attach_peer: the same for peers that live in this process
  *     (device pointers of other exchange objects, peer access enabled).
  *   phase: enqueue one phase of a step on u - 0 = operand prep + f_E(u0),
- *     k = 1..K-1 = full sweep k with its exchange, K = closing solve.  A
- *     caller may interleave the phases of several ranks on one stream.
+ *     k = 1..K-1 = full sweep k (publishing exchange k), K = closing solve;
+ *     phases k >= 2 start by posting and waiting for exchange k - 1.
+ *   post: enqueue only the post of exchange k of the current step (idempotent).
+ *     A driver of several ranks on ONE stream posts exchange k - 1 for every
+ *     rank before any rank's phase k, so no wait depends on a later kernel.
  *   run: n_steps steps (operand prep first); use_graph replays a captured
  *     graph of up to 8 steps.
  *   option 0: publish fused into the analysis epilogue (default 1 where the
  *     plan supports it: spherical, T < 400, unsplit).
  *   info: own node block and kernels per step.
- * Every rank must run the same number of steps (the exchange counters stay
- * in lock step); a rank with no nodes still signals every exchange. */
+ *   reset: divergence is reported relative to the step count at the reset.
+ * Every rank must run the same number of steps (the exchange numbers derive
+ * from a device step counter that is never reset, so they stay in lock step);
+ * a rank with no nodes still posts every exchange. */
 #define SDCSW_IPC_HANDLE_BYTES 64
 typedef struct sdcsw_exchange sdcsw_exchange;
 int sdcsw_exchange_create(sdcsw_plan* plan, int n_nodes, int n_sweeps, const double* coef,
@@ -237,6 +242,7 @@ int sdcsw_exchange_open_peers(sdcsw_exchange* x, const void* handles, int bytes_
 int sdcsw_exchange_base(sdcsw_exchange* x, void** base);
 int sdcsw_exchange_attach_peer(sdcsw_exchange* x, int peer, void* base);
 int sdcsw_exchange_phase(sdcsw_exchange* x, double* u, int phase, void* stream);
+int sdcsw_exchange_post(sdcsw_exchange* x, int k, void* stream);
 int sdcsw_exchange_run(sdcsw_exchange* x, double* u, int n_steps, int use_graph, void* stream);
 int sdcsw_exchange_set_option(sdcsw_exchange* x, int option, int value);
 int sdcsw_exchange_info(sdcsw_exchange* x, int* node_lo, int* node_count, int* launches_per_step);

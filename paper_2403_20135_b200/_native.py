@@ -9,7 +9,8 @@ import os
 
 from .errors import DeviceError, DivergenceError, ParameterError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsdcsw.so")
+LIB_PATH = os.environ.get("SDCSW_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libsdcsw.so")  # env: experiment builds only
 
 SDCSW_OK, SDCSW_ERR_PARAM, SDCSW_ERR_CUDA, SDCSW_ERR_STATE, SDCSW_ERR_DIVERGED = range(5)
 IPC_HANDLE_BYTES = 64  # SDCSW_IPC_HANDLE_BYTES
@@ -46,6 +47,7 @@ EXPORTS = (
     "sdcsw_exchange_base",
     "sdcsw_exchange_attach_peer",
     "sdcsw_exchange_phase",
+    "sdcsw_exchange_post",
     "sdcsw_exchange_run",
     "sdcsw_exchange_set_option",
     "sdcsw_exchange_info",
@@ -121,6 +123,7 @@ _SIGS = {
     "sdcsw_exchange_base": [_p, ctypes.POINTER(_p)],
     "sdcsw_exchange_attach_peer": [_p, _i, _p],
     "sdcsw_exchange_phase": [_p, _p, _i, _p],
+    "sdcsw_exchange_post": [_p, _i, _p],
     "sdcsw_exchange_run": [_p, _p, _i, _i, _p],
     "sdcsw_exchange_set_option": [_p, _i, _i],
     "sdcsw_exchange_info": [_p, _ip, _ip, _ip],

@@ -235,24 +235,35 @@ cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, c
 // ---------------------------------------------------------------------------
 // Peer exchange of node-parallel dSDC (peer.cu).  Each rank owns one exchange
 // buffer X = [2 parities][M nodes][2 (fe, fi)][3C] complex, mapped into every
-// peer (CUDA IPC over NVLink), and a control block.  Exchange n (the n-th
-// sweep of the run with a gather) is written by every rank into parity n & 1
-// of every rank's X with plain peer stores; the rank then posts n into
-// flag[rank] of every peer (release, system scope).  A consumer waits until
-// all flags >= its own seq = n (acquire) and reads parity n & 1 locally.  Two
-// parities suffice: a rank can only write exchange n + 2 after every rank
-// posted n + 1, which each rank does after it finished reading exchange n.
+// peer (CUDA IPC over NVLink), and a flag block.  Exchanges are numbered
+// n = (epoch - 1) (K - 1) + k for full sweep k = 1..K-1 of the rank's epoch-th
+// step (epoch: a device step counter, never reset), so every kernel derives n
+// from device state and the captured graphs replay unchanged.
+//   publish  the analysis (or a copy kernel) of sweep k stores the rank's
+//            (fe, fi) into parity n & 1 of every rank's X (plain peer stores);
+//   post     the next kernel that consumes exchange n (node kernel of sweep
+//            k + 1, or the closing solve) first raises flag[rank] of every rank
+//            to n - its own publishing grid has completed and flushed its
+//            stores by then (griddepcontrol.wait); a system-scope fence
+//            then orders the post (system-scope atomic max) after them;
+//   wait     then spins until flag[q] >= n for all q (acquire) and reads
+//            parity n & 1 locally.
+// Two parities suffice: a rank publishes n + 2 only after passing the wait for
+// n + 1, i.e. after every rank posted n + 1, which each rank does after its
+// reads of exchange n have completed.
 // ---------------------------------------------------------------------------
 constexpr int kMaxPeers = 16;
-struct PeerCtrl {
-  unsigned long long seq;        // exchanges completed by this rank (its own posts)
-  unsigned long long pad[15];
+struct PeerFlags {
   unsigned long long flag[kMaxPeers];  // flag[q]: last exchange rank q posted here
 };
 struct PeerWait {
-  const PeerCtrl* ctrl;  // local control block (null: no exchange, plain pointers)
+  const PeerFlags* flags;   // local flag block (null: no exchange, plain pointers)
+  const int* epoch;         // device step counter of the exchange (incremented per step)
+  int k;                    // consumed exchange's sweep index within the step (1..K-1)
+  int kx;                   // exchanges per step (K - 1)
   int world;
-  long long par_stride;  // doubles between the two parities of X
+  long long par_stride;     // doubles between the two parities of X
+  unsigned long long* post[kMaxPeers];  // &flags_q->flag[rank] of every rank q
 };
 #ifdef __CUDACC__
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -260,20 +271,29 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ unsigned long long exchange_number(const int* epoch, int k, int kx) {
+  return (unsigned long long)(*epoch - 1) * (unsigned long long)kx + (unsigned long long)k;
 }
-// Called by every thread of the CTA before any early return: waits for the
-// latest exchange of every rank and returns the parity offset (doubles) of X.
+// Post + wait; called by every thread of the CTA before any early return.
+// Returns the parity offset (doubles) of exchange n in X.
 __device__ __forceinline__ long long peer_wait(const PeerWait& pw) {
-  if (pw.ctrl == nullptr) return 0;
-  SDCSW_PDL_WAIT();  // seq was written by the preceding signal kernel
-  const unsigned long long s = *reinterpret_cast<const volatile unsigned long long*>(&pw.ctrl->seq);
-  if (threadIdx.x == 0)
+  if (pw.flags == nullptr) return 0;
+  SDCSW_PDL_WAIT();  // the publishing grid (and the epoch increment) completed
+  const unsigned long long n = exchange_number(pw.epoch, pw.k, pw.kx);
+  if (threadIdx.x == 0) {
+    // The data of exchange n were stored by this rank's previous grid, which
+    // has completed (griddepcontrol.wait above).  Across devices the post is
+    // ordered after those peer stores by a system-scope fence (its latency,
+    // 4 us per exchange on B200, is the price of not relying on how NVLink
+    // orders a later store against earlier striped ones); within one device
+    // the kernel boundary already orders them.
+    if (pw.world > 1) __threadfence_system();
+    for (int q = 0; q < pw.world; ++q) atomicMax_system(pw.post[q], n);
     for (int q = 0; q < pw.world; ++q)
-      while (ld_acquire_sys(&pw.ctrl->flag[q]) < s) __nanosleep(32);
+      while (ld_acquire_sys(&pw.flags->flag[q]) < n) __nanosleep(32);
+  }
   __syncthreads();
-  return (long long)(s & 1) * pw.par_stride;
+  return (long long)(n & 1) * pw.par_stride;
 }
 #endif
 
@@ -306,9 +326,9 @@ struct FuseArgs {
   int use_corr;             // m > 0: the correction exists
   // mode 4 (node-parallel publish, peer.cu): f_E of this rank's nodes
   // [peer_lo, peer_lo + nb) and their f_I (peer_fi, [nb][3C]) are stored into
-  // parity (seq + 1) & 1 of every rank's exchange buffer
-  int peer_world, peer_lo;
-  const PeerCtrl* peer_ctrl;
+  // parity n & 1 of every rank's exchange buffer
+  int peer_world, peer_lo, peer_k, peer_kx;  // exchange n = (epoch - 1) kx + k
+  const int* peer_epoch;
   const double* peer_fi;
   double* peer_x[kMaxPeers];
   double cf[kFuseMaxNodes * (kFuseMaxNodes + 4)];  // mode 1: [M][M+4]; mode 2: [M+4];

@@ -476,7 +476,7 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
     fe[b].delta = zero ? 0.0 : __fma_rn(l, row[6 * NB + 2 * b + ri], row[6 * b + 4 + ri]);
   }
   if (fz.mode == 4) {  // node-parallel: publish (fe, fi) of this rank's nodes to every rank
-    const long long par = (long long)((fz.peer_ctrl->seq + 1) & 1);
+    const long long par = (long long)(exchange_number(fz.peer_epoch, fz.peer_k, fz.peer_kx) & 1);
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       if (b0 + b >= nb) break;
@@ -487,8 +487,7 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
         store_tri(fz.peer_x[q] + slot + S2, C2, e, fi);
       }
     }
-    __threadfence_system();  // performed system-wide before this grid completes
-    return;
+    return;  // posted by the consumer after this grid completed (peer_wait)
   }
   if (fz.mode == 3) {  // serial SDC: store fe_m, serial_update(m), serial_node(m + 1)
     store_tri(fz.fe_new, C2, e, fe[0]);

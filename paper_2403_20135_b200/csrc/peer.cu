@@ -12,14 +12,14 @@
 //   synthesis -> ring -> analysis  (own nodes; the analysis epilogue stores
 //                 f_E and f_I of own nodes into every rank's buffer through
 //                 NVLink - FuseArgs mode 4 - tile by tile as they are formed)
-//   signal       (one thread: seq += 1, release-store seq into flag[rank] of
-//                 every rank)
+//   (the next consumer first posts the exchange number into every rank's
+//    flag word, then waits until every rank has posted it)
 //
 // and after the last exchange every rank computes the closing solve and the
 // next f_E(u0) redundantly (no further communication; the state stays
 // replicated and bit-identical to the single-GPU stepper because every node
 // kernel and transform is batch-invariant).  Protocol and buffer layout:
-// internal.cuh (PeerCtrl).
+// internal.cuh (PeerFlags, PeerWait).
 #include <climits>
 #include <cstring>
 #include <new>
@@ -30,27 +30,24 @@
 
 namespace sdcsw {
 
-struct PeerFlags {
-  unsigned long long* flag[kMaxPeers];  // &ctrl_q->flag[rank] of every rank q
-};
 struct PeerBases {
   double* x[kMaxPeers];  // exchange buffer of every rank q
 };
 
 // Copy-kernel publish (plans without the fused epilogue: T >= 400 TMA
-// analysis): own nodes' fe (from a plain analysis) and fi into parity
-// (seq + 1) & 1 of every rank's buffer.  grid (ceil(S2 / 2 / 256), count)
+// analysis): own nodes' fe (from a plain analysis) and fi into parity n & 1
+// of every rank's buffer.  grid (ceil(S / 256), count)
 __global__ void __launch_bounds__(256) k_peer_publish(long long S, int M, int lo,
                                                       const double2* __restrict__ fe_loc,
                                                       const double2* __restrict__ fi_loc,
-                                                      const PeerCtrl* ctrl, PeerBases pb,
-                                                      int world) {
+                                                      const int* epoch, int k, int kx,
+                                                      PeerBases pb, int world) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= S) return;
   const int b = blockIdx.y;
-  const long long par = (long long)((ctrl->seq + 1) & 1);
+  const long long par = (long long)(exchange_number(epoch, k, kx) & 1);
   const double2 e = fe_loc[(size_t)b * S + i];
   const double2 f = fi_loc[(size_t)b * S + i];
   const size_t slot = ((size_t)par * M + lo + b) * 2 * S;  // in double2
@@ -59,20 +56,16 @@ __global__ void __launch_bounds__(256) k_peer_publish(long long S, int M, int lo
     X[slot + i] = e;
     X[slot + S + i] = f;
   }
-  __threadfence_system();
 }
 
-// The exchange's completion: every store of this rank's publish is performed
-// (its grid completed, each thread fenced at system scope), so the exchange
-// number is posted to every rank.
-__global__ void k_peer_signal(PeerCtrl* ctrl, PeerFlags f, int world) {
+// Post only: a rank without nodes publishes nothing but still posts every
+// exchange of the step (the closing solve posts and waits for the last one).
+__global__ void k_peer_post(PeerWait pw) {
   SDCSW_PDL_ENTRY();
   SDCSW_PDL_WAIT();
   if (threadIdx.x == 0) {
-    const unsigned long long s = ctrl->seq + 1;
-    ctrl->seq = s;
-    __threadfence_system();
-    for (int q = 0; q < world; ++q) st_release_sys(f.flag[q], s);
+    const unsigned long long n = exchange_number(pw.epoch, pw.k, pw.kx);
+    for (int q = 0; q < pw.world; ++q) atomicMax_system(pw.post[q], n);
   }
 }
 
@@ -87,15 +80,16 @@ struct sdcsw_exchange {
   size_t S;                  // one state, in double2
   char* mem;                 // exchange buffer + control block (the IPC allocation)
   double2* X;                // [2][M][2][S]
-  PeerCtrl* ctrl;
+  PeerFlags* pflag;          // flag block (after X in the IPC allocation)
   char* local;               // private buffers
   double2 *fe0, *fe_loc, *fi_loc;
   double *xsyn1, *xsynM;
-  int* flags;                // [0] first diverged step (INT_MAX = none), [1] step counter
+  int* flags;                // [0] first diverged epoch (INT_MAX = none), [1] epoch (never reset)
+  int base_epoch;            // epoch at the last reset (divergence step = epoch - base)
   cudaIpcMemHandle_t handle;
   void* opened[kMaxPeers];   // IPC mappings to close
   PeerBases bases;
-  PeerFlags pflags;
+  unsigned long long* post[kMaxPeers];  // &flag block of rank q ->flag[rank]
   int attached;              // ranks with a known base (own included)
   int fuse;
   cudaStream_t cap;
@@ -128,8 +122,17 @@ void drop_graphs(sdcsw_exchange* x) {
   x->graph_u = nullptr;
 }
 
-PeerWait peer_wait_args(const sdcsw_exchange* x) {
-  return PeerWait{x->ctrl, x->world, (long long)x->M * 2 * (long long)x->S * 2};
+// consumer of exchange k (1..K-1) of the current step
+PeerWait peer_wait_args(const sdcsw_exchange* x, int k) {
+  PeerWait pw{};
+  pw.flags = x->pflag;
+  pw.epoch = x->flags + 1;
+  pw.k = k;
+  pw.kx = x->K - 1;
+  pw.world = x->world;
+  pw.par_stride = (long long)x->M * 2 * (long long)x->S * 2;
+  for (int q = 0; q < x->world; ++q) pw.post[q] = x->post[q];
+  return pw;
 }
 
 // phase 0: f_E(u0) from the operand in xsyn1 (written by the previous step's
@@ -140,13 +143,15 @@ cudaError_t enqueue_phase(sdcsw_exchange* x, double2* u, int phase, cudaStream_t
   const size_t S = x->S;
   const int cstride = M * (M + 4);
   const Work w = plan_work(p);
-  const PeerWait pw = peer_wait_args(x);
   cudaError_t e;
   if (phase == 0) return f_expl_prepped(p, w, x->xsyn1, x->fe0, 1, s, x->flags + 1, 0);
   if (phase < K) {
     const int k = phase;
     const bool first = k == 1;
-    if (x->count > 0) {
+    const PeerWait pw = peer_wait_args(x, k - 1);  // sweep k consumes exchange k - 1
+    if (x->count == 0)
+      return first ? cudaSuccess : launch_k(k_peer_post, dim3(1), dim3(32), 0, s, pw);
+    {
       // first sweep: every node's tendencies are f(u0) (fe0, f_I(u0)); later:
       // the gathered [M][2][S] of the latest exchange (fe at 2j, fi at 2j + 1)
       const double2* fe = first ? x->fe0 : x->X;
@@ -165,7 +170,9 @@ cudaError_t enqueue_phase(sdcsw_exchange* x, double2* u, int phase, cudaStream_t
         fz.phibar = p.phibar;
         fz.peer_world = x->world;
         fz.peer_lo = x->lo;
-        fz.peer_ctrl = x->ctrl;
+        fz.peer_epoch = x->flags + 1;
+        fz.peer_k = k;
+        fz.peer_kx = K - 1;
         fz.peer_fi = reinterpret_cast<const double*>(x->fi_loc);
         for (int q = 0; q < x->world; ++q) fz.peer_x[q] = x->bases.x[q];
         if ((e = launch_analysis_fused(p, w, x->count, fz, s)) != cudaSuccess) return e;
@@ -174,17 +181,18 @@ cudaError_t enqueue_phase(sdcsw_exchange* x, double2* u, int phase, cudaStream_t
         dim3 grid((unsigned)((S + 255) / 256), x->count);
         e = launch_k(k_peer_publish, grid, 256, 0, s, (long long)S, M, x->lo,
                      (const double2*)x->fe_loc, (const double2*)x->fi_loc,
-                     (const PeerCtrl*)x->ctrl, x->bases, x->world);
+                     (const int*)(x->flags + 1), k, K - 1, x->bases, x->world);
         if (e != cudaSuccess) return e;
       }
     }
-    return launch_k(k_peer_signal, dim3(1), dim3(32), 0, s, x->ctrl, x->pflags, x->world);
+    return cudaSuccess;
   }
   // closing solve (K == 1: straight from f(u0))
   const bool first = K == 1;
   const double2* fe = first ? x->fe0 : x->X;
   const double2* fi = first ? x->fe0 : x->X + S;
   const long long st = first ? 0 : 2;
+  const PeerWait pw = peer_wait_args(x, K - 1);
   return launch_final_node(p, M, x->coef.data() + (size_t)(K - 1) * cstride, u, fe, st, fi, st,
                            first, u, x->flags, x->flags + 1, x->xsyn1, s, 1, 0, 0,
                            first ? nullptr : &pw);
@@ -259,9 +267,9 @@ int sdcsw_exchange_create(sdcsw_plan* h, int n_nodes, int n_sweeps, const double
   const size_t xs = (size_t)p.rows * kXsyn * sizeof(double);
   const size_t lbytes = (1 + 2 * cnt) * x->S * sizeof(double2) + xs * (1 + cnt) + 2 * sizeof(int);
   cudaError_t e = cudaSetDevice(p.device);
-  if (e == cudaSuccess) e = cudaMalloc(&x->mem, xbytes + sizeof(PeerCtrl));
+  if (e == cudaSuccess) e = cudaMalloc(&x->mem, xbytes + sizeof(PeerFlags));
   if (e == cudaSuccess) e = cudaMalloc(&x->local, lbytes);
-  if (e == cudaSuccess) e = cudaMemset(x->mem, 0, xbytes + sizeof(PeerCtrl));
+  if (e == cudaSuccess) e = cudaMemset(x->mem, 0, xbytes + sizeof(PeerFlags));
   if (e == cudaSuccess) e = cudaMemset(x->local, 0, lbytes);
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&x->handle, x->mem);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&x->cap, cudaStreamNonBlocking);
@@ -273,7 +281,7 @@ int sdcsw_exchange_create(sdcsw_plan* h, int n_nodes, int n_sweeps, const double
     return cuda_status(e, "sdcsw_exchange_create");
   }
   x->X = reinterpret_cast<double2*>(x->mem);
-  x->ctrl = reinterpret_cast<PeerCtrl*>(x->mem + xbytes);
+  x->pflag = reinterpret_cast<PeerFlags*>(x->mem + xbytes);
   double2* q = reinterpret_cast<double2*>(x->local);
   x->fe0 = q; q += x->S;
   x->fe_loc = q; q += cnt * x->S;
@@ -284,7 +292,7 @@ int sdcsw_exchange_create(sdcsw_plan* h, int n_nodes, int n_sweeps, const double
   const int init[2] = {INT_MAX, 0};
   cudaMemcpy(x->flags, init, sizeof(init), cudaMemcpyHostToDevice);
   x->bases.x[rank] = reinterpret_cast<double*>(x->X);
-  x->pflags.flag[rank] = &x->ctrl->flag[rank];
+  x->post[rank] = &x->pflag->flag[rank];
   x->attached = 1;
   *out = x;
   return SDCSW_OK;
@@ -301,8 +309,8 @@ static int attach(sdcsw_exchange* x, int q, char* base) {
   const size_t xbytes = (size_t)2 * x->M * 2 * x->S * sizeof(double2);
   const bool fresh = q != x->rank && x->bases.x[q] == nullptr;
   x->bases.x[q] = reinterpret_cast<double*>(base);
-  // this rank posts into flag[rank] of rank q's control block
-  x->pflags.flag[q] = &reinterpret_cast<PeerCtrl*>(base + xbytes)->flag[x->rank];
+  // this rank posts into flag[rank] of rank q's flag block
+  x->post[q] = &reinterpret_cast<PeerFlags*>(base + xbytes)->flag[x->rank];
   if (fresh) ++x->attached;
   drop_graphs(x);
   return SDCSW_OK;
@@ -349,6 +357,16 @@ int sdcsw_exchange_phase(sdcsw_exchange* x, double* u, int phase, void* stream) 
     e = launch_synth_prep(x->plan->p, (const double2*)u, 1, x->xsyn1, s);
   if (e == cudaSuccess) e = enqueue_phase(x, (double2*)u, phase, s);
   return cuda_status(e, "sdcsw_exchange_phase");
+}
+
+int sdcsw_exchange_post(sdcsw_exchange* x, int k, void* stream) {
+  if (int st = check_x(x, "sdcsw_exchange_post")) return st;
+  if (int st = ready(x, "sdcsw_exchange_post")) return st;
+  if (k < 1 || k >= x->K) return SDCSW_ERR_PARAM;
+  cudaError_t e = cudaSetDevice(x->plan->p.device);
+  if (e == cudaSuccess)
+    e = launch_k(k_peer_post, dim3(1), dim3(32), 0, (cudaStream_t)stream, peer_wait_args(x, k));
+  return cuda_status(e, "sdcsw_exchange_post");
 }
 
 int sdcsw_exchange_run(sdcsw_exchange* x, double* u, int n_steps, int use_graph, void* stream) {
@@ -410,9 +428,9 @@ int sdcsw_exchange_info(sdcsw_exchange* x, int* node_lo, int* node_count, int* l
   if (node_lo) *node_lo = x->lo;
   if (node_count) *node_count = x->count;
   if (launches) {
-    // init f_E (3) + per exchange (node, synthesis, ring, analysis [+ copy], signal) + final
-    const int per = x->count > 0 ? (x->fuse ? 5 : 6) : 1;
-    *launches = 3 + (x->K - 1) * per + 1;
+    // init f_E (3) + per full sweep (node, synthesis, ring, analysis [+ copy];
+    // no nodes: a post from sweep 2 on) + closing solve
+    *launches = 3 + 1 + (x->count > 0 ? (x->K - 1) * (x->fuse ? 4 : 5) : (x->K > 2 ? x->K - 2 : 0));
   }
   return SDCSW_OK;
 }
@@ -425,17 +443,23 @@ int sdcsw_exchange_diverged(sdcsw_exchange* x, int* step_index) {
   cudaDeviceSynchronize();
   cudaError_t e = cudaMemcpy(v, x->flags, sizeof(v), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_status(e, "sdcsw_exchange_diverged");
-  *step_index = v[0] == INT_MAX ? 0 : v[0];
+  *step_index = v[0] == INT_MAX ? 0 : v[0] - x->base_epoch;
   return SDCSW_OK;
 }
 
 int sdcsw_exchange_reset(sdcsw_exchange* x, void* stream) {
   if (int st = check_x(x, "sdcsw_exchange_reset")) return st;
-  // the exchange counters are never reset (they stay in lock step across ranks)
-  const int init[2] = {INT_MAX, 0};
-  return cuda_status(cudaMemcpyAsync(x->flags, init, sizeof(init), cudaMemcpyHostToDevice,
-                                     (cudaStream_t)stream),
-                     "sdcsw_exchange_reset");
+  // the epoch is never reset (exchange numbers stay in lock step across
+  // ranks): divergence is reported relative to the epoch at the reset
+  cudaStream_t s = (cudaStream_t)stream;
+  int epoch = 0;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaMemcpy(&epoch, x->flags + 1, sizeof(int), cudaMemcpyDeviceToHost);
+  const int none = INT_MAX;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(x->flags, &none, sizeof(int), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  x->base_epoch = epoch;
+  return cuda_status(e, "sdcsw_exchange_reset");
 }
 
 int sdcsw_exchange_destroy(sdcsw_exchange* x) {

@@ -250,8 +250,9 @@ class PeerNodeParallelDsdc:
     """Node-parallel dSDC with the per-sweep exchange done by the kernels over
     peer memory (``sdcsw_exchange_*``, ``csrc/peer.cu``): the analysis epilogue
     of each rank stores (f_E, f_I) of its own nodes into every rank's exchange
-    buffer through NVLink and the next node kernel waits on per-rank flags -
-    no NCCL call and no host synchronisation on the data path.  Same node
+    buffer through NVLink; the next node kernel posts the exchange number into
+    every rank's flag word and waits until all ranks posted it - no NCCL call
+    and no host synchronisation on the data path.  Same node
     partition and bit-identical results as :class:`NodeParallelDsdc`.
 
     ``group`` (torch.distributed) is used once, to exchange the CUDA IPC
@@ -351,6 +352,27 @@ class PeerNodeParallelDsdc:
         _native.check(self.lib.sdcsw_exchange_phase(self.handle, u.data_ptr(), int(phase),
                                                     self.problem.stream()), "sdcsw_exchange_phase")
 
+    def post(self, k):
+        """Enqueue only the post of exchange ``k`` of the current step."""
+        from . import _native
+
+        _native.check(self.lib.sdcsw_exchange_post(self.handle, int(k), self.problem.stream()),
+                      "sdcsw_exchange_post")
+
+    @staticmethod
+    def run_in_stream_order(ranks, states, n_steps):
+        """Advance the in-process ranks (:meth:`in_process`) on one stream:
+        per phase every rank first posts the exchange the phase consumes, then
+        every rank runs the phase - each wait is satisfied by earlier kernels."""
+        k_sweeps = ranks[0].k
+        for _ in range(n_steps):
+            for ph in range(k_sweeps + 1):
+                if ph >= 2:  # phase ph (a sweep or the closing solve) consumes exchange ph - 1
+                    for x in ranks:
+                        x.post(ph - 1)
+                for x, u in zip(ranks, states):
+                    x.phase(u, ph)
+
     def run(self, u, n_steps, use_graph=True):
         """Advance the replicated device state ``u`` by ``n_steps`` steps in place."""
         from . import _native
@@ -359,8 +381,15 @@ class PeerNodeParallelDsdc:
                                                   int(bool(use_graph)), self.problem.stream()),
                       "sdcsw_exchange_run")
 
+    def reset(self):
+        """Clear the divergence flag; later step indices count from here."""
+        from . import _native
+
+        _native.check(self.lib.sdcsw_exchange_reset(self.handle, self.problem.stream()),
+                      "sdcsw_exchange_reset")
+
     def diverged(self):
-        """First non-finite step index of the run (0 = none); synchronises."""
+        """First non-finite step index since creation / reset (0 = none); synchronises."""
         import ctypes
 
         v = ctypes.c_int()

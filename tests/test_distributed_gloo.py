@@ -218,3 +218,69 @@ def test_node_and_spectral_split_matches_single_process(tmp_path):
         assert np.array_equal(got, ref), np.abs(got - ref).max()
     assert sorted(set(part_of.tolist())) == [0, 1]
     assert abs((part_of[prob.m_of] == 0).sum() - c / 2) <= g.trunc + 1
+
+
+class _FakeExchangeLib:
+    """Records the exchange calls of PeerNodeParallelDsdc (host logic only)."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.calls = []
+
+    def sdcsw_exchange_create(self, plan, m, k, coef, n_coef, world, rank, out):
+        self.calls.append(("create", m, k, n_coef, world, rank))
+        out._obj.value = 1000 + rank
+        return 0
+
+    def sdcsw_exchange_ipc_handle(self, h, buf, nbytes):
+        import ctypes
+
+        ctypes.memmove(buf, bytes([self.rank + 1]) * nbytes, nbytes)
+        return 0
+
+    def sdcsw_exchange_open_peers(self, h, blob, each):
+        self.calls.append(("open", blob.raw, each))
+        return 0
+
+    def sdcsw_exchange_destroy(self, h):
+        return 0
+
+
+class _FakeProblem:
+    handle = None
+    mean_geopotential = 9.80616e4
+
+    def __init__(self, rank):
+        self._lib = _FakeExchangeLib(rank)
+
+
+def _peer_worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2403_20135_b200 import CollocationTable, SdcConfig, SweepMode
+    from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+
+    cfg = SdcConfig(table=CollocationTable.radau_right(4), n_sweeps=3,
+                    mode=SweepMode.DIAGONAL_PARALLEL, time_threads=1)
+    prob = _FakeProblem(rank)
+    x = PeerNodeParallelDsdc(prob, cfg, 90.0)
+    create = prob._lib.calls[0]
+    opened = prob._lib.calls[1]
+    np.save(out_path + f".{rank}.npy", np.frombuffer(opened[1], dtype=np.uint8))
+    assert create == ("create", 4, 3, x._coef.size, world, rank), create
+    assert x._coef.size >= 2 * 4 * 8 + 8
+    assert x.handle.value == 1000 + rank
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_peer_exchange_handles_gathered_in_rank_order(tmp_path):
+    """PeerNodeParallelDsdc (world 3, gloo): every rank creates its exchange
+    with (world, rank) and opens the IPC handles of all ranks in rank order."""
+    world = 3
+    port = 29900 + (os.getpid() % 97)
+    out = str(tmp_path / "h")
+    mp.spawn(_peer_worker, args=(world, port, out), nprocs=world, join=True)
+    want = np.concatenate([np.full(64, q + 1, dtype=np.uint8) for q in range(world)])
+    for r in range(world):
+        assert np.array_equal(np.load(out + f".{r}.npy"), want)

@@ -4,9 +4,10 @@ B200.
 World size 1 runs the full protocol (publish into the exchange buffer, post
 the flag, wait, read the parity) against the process's own buffer.  Larger
 worlds run as several exchange objects of one process attached to each other,
-with the phases of all ranks interleaved on ONE stream: every wait is already
-satisfied by kernels earlier in the stream, so no kernel ever waits on a
-concurrently running one.  Each rank must end bit-identical to the
+with the phases of all ranks interleaved on ONE stream and the posts a phase
+consumes enqueued for every rank before it (run_in_stream_order): every wait
+is already satisfied by kernels earlier in the stream, so no kernel ever waits
+on a concurrently running one.  Each rank must end bit-identical to the
 single-GPU stepper (the reference's thread-count invariance,
 pkg/tests/test_integrators.py:190-225)."""
 
@@ -86,10 +87,7 @@ def test_exchange_ranks_interleaved_bitwise(m, world, fused):
         lo, count, _ = node_block(m, world, x.rank)
         assert x.info()[:2] == (lo, count)
     states = [u0.clone() for _ in ranks]
-    for _ in range(n_steps):
-        for ph in range(k + 1):
-            for x, u in zip(ranks, states):
-                x.phase(u, ph)
+    PeerNodeParallelDsdc.run_in_stream_order(ranks, states, n_steps)
     torch.cuda.synchronize()
     for u in states:
         assert torch.equal(u, ref)
@@ -113,10 +111,7 @@ def test_exchange_table_streaming_copy_publish():
     with pytest.raises(ParameterError):
         ranks[0].set_fused(True)
     states = [u0.clone() for _ in ranks]
-    for _ in range(2):
-        for ph in range(3):
-            for x, u in zip(ranks, states):
-                x.phase(u, ph)
+    PeerNodeParallelDsdc.run_in_stream_order(ranks, states, 2)
     torch.cuda.synchronize()
     for u in states:
         assert torch.equal(u, ref)
@@ -151,9 +146,39 @@ def test_exchange_launch_count():
 
     p = gpu(127)
     ranks = PeerNodeParallelDsdc.in_process(p, _cfg(4, 4), 90.0, 4)
-    # init f_E 3 + 3 sweeps x (node, synthesis, ring, analysis, signal) + final
-    assert [x.info()[2] for x in ranks] == [19] * 4
+    # init f_E 3 + 3 sweeps x (node, synthesis, ring, analysis) + closing solve
+    assert [x.info()[2] for x in ranks] == [16] * 4
     ranks[0].set_fused(False)
-    assert ranks[0].info()[2] == 22
+    assert ranks[0].info()[2] == 19
     for x in ranks:
         x.close()
+    # a rank without nodes: init + posts for sweeps 2, 3 + closing solve
+    ranks = PeerNodeParallelDsdc.in_process(p, _cfg(2, 4), 90.0, 4)
+    assert [x.info()[1:] for x in ranks] == [(1, 16), (1, 16), (0, 6), (0, 6)]
+    for x in ranks:
+        x.close()
+
+
+def test_exchange_reset_rebases_divergence():
+    import torch
+
+    from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+
+    p = gpu(63)
+    cfg = _cfg(3, 3)
+    x = PeerNodeParallelDsdc(p, cfg, 120.0, world=1, rank=0)
+    a = torch.from_numpy(random_initial_state(p.grid, 2)).to(p.device)
+    x.run(a, 3)
+    assert x.diverged() == 0
+    x.reset()
+    b = torch.from_numpy(random_initial_state(p.grid, 0) * 1e140).to(p.device)
+    ref = b.clone()
+    x.run(b, 6)
+    got = x.diverged()
+    from paper_2403_20135_b200.integrators import DeviceStepper
+
+    st = DeviceStepper(p, cfg, 120.0, serial=False)
+    st.run(ref, 6)
+    assert got == st.diverged() > 0
+    st.close()
+    x.close()
