@@ -460,7 +460,20 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
   RT(5)
 }
 
-#define SDCSW_RING_SIZES(X) X(96, 256) X(192, 256) X(384, 256) X(768, 256) X(1536, 512)
+#ifndef SDCSW_RT96
+#define SDCSW_RT96 256
+#endif
+#ifndef SDCSW_RT192
+#define SDCSW_RT192 256
+#endif
+#ifndef SDCSW_RT384
+#define SDCSW_RT384 256
+#endif
+#ifndef SDCSW_RT768
+#define SDCSW_RT768 256
+#endif
+#define SDCSW_RING_SIZES(X) \
+  X(96, SDCSW_RT96) X(192, SDCSW_RT192) X(384, SDCSW_RT384) X(768, SDCSW_RT768) X(1536, 512)
 
 bool ring_supported(int nlon) {
 #define SDCSW_RING_OK(NV, TV) if (nlon == NV) return true;
