@@ -22,6 +22,12 @@
 #ifndef SDCSW_EXP
 #define SDCSW_EXP 0
 #endif
+// Twiddle tables in shared memory (staged per CTA) or read from global
+// memory through L1 (saves the staging and shared memory).  Measured per size
+// on B200: global reads win only at nlon = 384 with 128-thread CTAs (T127:
+// -1.2% per step, 64-member ensemble -2.6%); shared memory elsewhere.
+template <int N>
+constexpr bool ring_twg() { return N == 384; }
 
 namespace sdcsw {
 #if SDCSW_EXP == 4
@@ -270,7 +276,9 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
   constexpr int NS = RadixPlan<N>::n;
   constexpr int TWN = tw_total<N>();
   double2* Z = sm2;             // [5][NP] (padded)
-  double2* tw = sm2 + 5 * NP;   // per-pass twiddle tables
+  constexpr bool TWG = ring_twg<N>();
+  // per-pass twiddle tables: global (read through L1) or staged in shared memory
+  const double2* tw = TWG ? twg : sm2 + 5 * NP;
   const int L = T + 1;
   const int j = blockIdx.x, b = blockIdx.y;
   // Fourier coefficients of (b, j, m): part-major [part][nbg][J][Lp][4][2]
@@ -289,7 +297,8 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
 #endif
   RT(0)
   // constant plan data before the dependency wait (overlaps the producer's tail)
-  for (int k = threadIdx.x; k < TWN; k += THREADS) tw[k] = twg[k];
+  if constexpr (!TWG)
+    for (int k = threadIdx.x; k < TWN; k += THREADS) sm2[5 * NP + k] = twg[k];
   const double muj = mu[j], ws = wsyn[j], wk = wke[j];
   SDCSW_PDL_WAIT();
 
@@ -467,7 +476,7 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const 
 #define SDCSW_RT192 256
 #endif
 #ifndef SDCSW_RT384
-#define SDCSW_RT384 256
+#define SDCSW_RT384 128
 #endif
 #ifndef SDCSW_RT768
 #define SDCSW_RT768 256
@@ -508,7 +517,7 @@ extern "C" int sdcsw_debug_rtimes(unsigned long long* host, int n) {
 
 size_t ring_smem_bytes(int nlon) {
 #define SDCSW_RING_SMEM(NV, TV) \
-  if (nlon == NV) return (size_t)(5 * padded<NV>() + tw_total<NV>()) * sizeof(double2);
+  if (nlon == NV) return (size_t)(5 * padded<NV>() + (ring_twg<NV>() ? 0 : tw_total<NV>())) * sizeof(double2);
   SDCSW_RING_SIZES(SDCSW_RING_SMEM)
 #undef SDCSW_RING_SMEM
   return 0;

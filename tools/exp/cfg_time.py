@@ -13,13 +13,18 @@ from paper_2403_20135_b200.problem import SphericalShallowWater  # noqa: E402
 
 for name in sys.argv[1:] or ["c0", "c1", "c2"]:
     c = bench.CONFIGS[name]
-    prob = SphericalShallowWater(c["trunc"], max_batch=c["nodes"])
+    E = c.get("members", 1)
+    prob = SphericalShallowWater(c["trunc"], max_batch=c["nodes"] * E)
     cfg = SdcConfig(table=CollocationTable.radau_right(c["nodes"]), n_sweeps=c["sweeps"],
                     mode=SweepMode.DIAGONAL_PARALLEL)
-    st = DeviceStepper(prob, cfg, c["dt"], serial=False)
-    u0 = prob._to_device(random_initial_state(prob.grid, c["seed"])).reshape(-1).contiguous()
+    st = DeviceStepper(prob, cfg, c["dt"], serial=False, members=E)
+    import numpy as np
+    u0 = torch.from_numpy(np.stack([random_initial_state(prob.grid, c["seed"] + e) for e in range(E)])
+                          ).to(prob.device).reshape(E, -1).contiguous()
+    if E == 1:
+        u0 = u0.reshape(-1)
     u = u0.clone()
-    n = c["steps"]
+    n = c["steps"] if E == 1 else 10
     st.run(u, 16)
     best = 1e9
     for _ in range(3):
