@@ -258,8 +258,14 @@ static void build_pass_twiddles(const double2* w, std::vector<double2>& out) {
   for (int s = 1; s < n; ++s) fill(tw_off_fwd<N>(s), fwd_radix<N>(s), fwd_prefix<N>(s));
 }
 
+#ifndef SDCSW_RING_MINB128
+#define SDCSW_RING_MINB128 5  // 96 registers: 5 CTAs per SM (64-member ensemble -3.9%, T127 unchanged)
+#endif
+template <int THREADS>
+constexpr int ring_min_blocks() { return THREADS <= 128 ? SDCSW_RING_MINB128 : (THREADS <= 256 ? 3 : 1); }
+
 template <int N, int THREADS, bool SPLIT>
-__global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 3 : 1) k_ring(const double2* __restrict__ fsyn,
+__global__ void __launch_bounds__(THREADS, ring_min_blocks<THREADS>()) k_ring(const double2* __restrict__ fsyn,
                                                   double2* __restrict__ gan, int J, int T,
                                                   const double* __restrict__ mu,
                                                   const double* __restrict__ wsyn,
