@@ -44,7 +44,7 @@ def _stepper_result(p, cfg, dt, u0, n):
     return b
 
 
-@pytest.mark.parametrize("trunc,m,k", [(63, 3, 3), (127, 4, 4), (63, 2, 1), (63, 6, 2)])
+@pytest.mark.parametrize("trunc,m,k", [(63, 3, 3), (127, 4, 4), (63, 2, 1), (63, 6, 2), (63, 8, 3)])
 @pytest.mark.parametrize("fused", [True, False])
 def test_exchange_single_rank_bitwise(trunc, m, k, fused):
     import torch
@@ -69,7 +69,7 @@ def test_exchange_single_rank_bitwise(trunc, m, k, fused):
     x.close()
 
 
-@pytest.mark.parametrize("m,world", [(4, 2), (4, 4), (3, 2), (5, 3), (2, 4), (6, 4)])
+@pytest.mark.parametrize("m,world", [(4, 2), (4, 4), (3, 2), (5, 3), (2, 4), (6, 4), (7, 2), (8, 3)])
 @pytest.mark.parametrize("fused", [True, False])
 def test_exchange_ranks_interleaved_bitwise(m, world, fused):
     import torch
