@@ -812,9 +812,9 @@ static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist
   }
   dim3 grid(p.J / (kRowsPerWarp * WJ), nm, (nblk + NBC - 1) / NBC);
   const dim3 block(32 * WJ * WK);
-  // the cp.async pipeline pays off from T255 up and for many batch blocks; at
-  // T127 with few blocks the register-prefetch kernel is faster (measured)
-  const bool cp = p.syn_cp >= 0 ? p.syn_cp != 0 : (p.T >= 200 || nblk >= 4);
+  // the cp.async pipeline pays off from T255 up, for many batch blocks and at
+  // T63; at T127 with few blocks the register-prefetch kernel is faster (measured)
+  const bool cp = p.syn_cp >= 0 ? p.syn_cp != 0 : (p.T >= 200 || p.T < 100 || nblk >= 4);
   // prefetch depth 1: a deeper register prefetch costs a resident CTA per SM,
   // which the latency-bound small truncations need more (measured on B200)
 #define SDCSW_SYN(NBV)                                                                         \
