@@ -270,7 +270,10 @@ __global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : (NB <= 
 // into shared memory (no registers held), so the K loop is no longer bound by
 // one L2 round trip per k-step.  Same arithmetic and reduction as k_synthesis.
 // ---------------------------------------------------------------------------
-constexpr int kSynStages = 3;
+#ifndef SDCSW_SYN_STAGES
+#define SDCSW_SYN_STAGES 3
+#endif
+constexpr int kSynStages = SDCSW_SYN_STAGES;
 template <int NB>
 constexpr int syn_stage_doubles() { return 128 + 96 * ((NB + 1) / 2); }
 template <int NB>
