@@ -328,12 +328,14 @@ def run_device(args):
 
         def one_run():
             stepper.run(u, nsteps, use_graph=True)
-    elif args.transport == "p2p" and world <= m_nodes:
+    elif args.transport == "p2p":
         from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
 
-        # node blocks over the ranks; the per-sweep exchange runs in the kernels
-        # over peer memory (analysis epilogue stores + flags), no NCCL on the data path
-        xpeer = PeerNodeParallelDsdc(problem, cfg, dt)
+        # node groups x spectral parts (the largest node-group count <= M dividing N);
+        # the exchanges run in the kernels over peer memory (analysis epilogue and
+        # split synthesis stores + flags), no NCCL on the data path
+        groups = max(g for g in range(1, min(world, m_nodes) + 1) if world % g == 0)
+        xpeer = PeerNodeParallelDsdc(problem, cfg, dt, spectral_parts=world // groups)
         launches_per_sim_step = xpeer.info()[2]
 
         def one_run():
@@ -479,8 +481,8 @@ def run_device(args):
                 "bench_step": f"one full {nsteps}-step run", "l2": "flushed between bench steps (256 MiB write, untimed)",
                 "parallelism": ("1 GPU: M nodes as concurrent graph branches / batched GEMM columns" if world == 1 and not multi
                                 else f"{world} GPUs: ensemble members sharded" if ensemble
-                                else (f"{world} GPUs: node blocks, (f_E, f_I) exchanged over peer memory by the analysis epilogue (no NCCL on the data path)"
-                                      if args.transport == "p2p" and world <= m_nodes
+                                else (f"{world} GPUs: node blocks x spectral (m) split; (f_E, f_I) and Fourier parts exchanged over peer memory by the analysis epilogue / split synthesis (no NCCL on the data path)"
+                                      if args.transport == "p2p"
                                       else f"{world} GPUs: node blocks x spectral (m) split, NCCL all-gathers per sweep / per f_E")),
                 "ms_per_sim_step": t_dev / sim_steps * 1e3,
                 "node_sweeps_per_s": value * node_sweeps,
@@ -517,8 +519,7 @@ def main():
                     help="use the multi-GPU node/spectral orchestration even at world size 1 "
                          "(exercises the N>1 code path on one GPU)")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
-                    help="node-parallel exchange: kernels over peer memory (default; world <= M) "
-                         "or NCCL all-gathers (also the spectral split when world > M)")
+                    help="multi-GPU exchanges: kernels over peer memory (default) or NCCL all-gathers")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

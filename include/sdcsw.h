@@ -218,12 +218,23 @@ int sdcsw_split_f_expl_end(sdcsw_plan* plan, double* fe, int nb, void* stream);
  *     (world x SDCSW_IPC_HANDLE_BYTES, rank order; the own entry is skipped).
  *   base / attach_peer: the same for peers that live in this process
  *     (device pointers of other exchange objects, peer access enabled).
- *   phase: enqueue one phase of a step on u - 0 = operand prep + f_E(u0),
- *     k = 1..K-1 = full sweep k (publishing exchange k), K = closing solve;
- *     phases k >= 2 start by posting and waiting for exchange k - 1.
- *   post: enqueue only the post of exchange k of the current step (idempotent).
- *     A driver of several ranks on ONE stream posts exchange k - 1 for every
- *     rank before any rank's phase k, so no wait depends on a later kernel.
+ *   create_split: world = G node groups x S spectral parts (rank = g S + sp,
+ *     G <= M when S > 1).  The exchange splits the plan (sdcsw_plan_set_split
+ *     with its own peer-mapped Fourier buffer); the state is m-partitioned
+ *     (own wavenumbers valid).  Each f_E's split synthesis stores its part into
+ *     every spectral peer's Fourier buffer and the ring kernel posts and waits
+ *     for all parts before reading them; the node exchange runs among the G
+ *     ranks sharing part sp.  create = create_split with S = 1.
+ *   phase: enqueue one half-phase of a step on u - for f_E k = 0..K-1 (k = 0:
+ *     f_E(u0), with the operand prep at phase 0; k >= 1: full sweep k,
+ *     publishing node exchange k) phase 2k = [node kernel k] + synthesis and
+ *     2k + 1 = ring + analysis; phase 2K = closing solve.  Phases 2k (k >= 2)
+ *     and 2K wait for node exchange k - 1; phases 2k + 1 of a split exchange
+ *     wait for the Fourier exchange of f_E k.
+ *   post: enqueue only a post (idempotent): channel 0 = node exchange k of the
+ *     current step, channel 1 = the next Fourier exchange.  A driver of
+ *     several ranks on ONE stream posts for every rank before any rank's
+ *     phase that waits, so no wait depends on a later kernel.
  *   run: n_steps steps (operand prep first); use_graph replays a captured
  *     graph of up to 8 steps.
  *   option 0: publish fused into the analysis epilogue (default 1 where the
@@ -237,12 +248,15 @@ int sdcsw_split_f_expl_end(sdcsw_plan* plan, double* fe, int nb, void* stream);
 typedef struct sdcsw_exchange sdcsw_exchange;
 int sdcsw_exchange_create(sdcsw_plan* plan, int n_nodes, int n_sweeps, const double* coef,
                           int n_coef, int world, int rank, sdcsw_exchange** out);
+int sdcsw_exchange_create_split(sdcsw_plan* plan, int n_nodes, int n_sweeps, const double* coef,
+                                int n_coef, int world, int rank, int spectral_parts,
+                                sdcsw_exchange** out);
 int sdcsw_exchange_ipc_handle(sdcsw_exchange* x, void* handle, int bytes);
 int sdcsw_exchange_open_peers(sdcsw_exchange* x, const void* handles, int bytes_each);
 int sdcsw_exchange_base(sdcsw_exchange* x, void** base);
 int sdcsw_exchange_attach_peer(sdcsw_exchange* x, int peer, void* base);
 int sdcsw_exchange_phase(sdcsw_exchange* x, double* u, int phase, void* stream);
-int sdcsw_exchange_post(sdcsw_exchange* x, int k, void* stream);
+int sdcsw_exchange_post(sdcsw_exchange* x, int channel, int k, void* stream);
 int sdcsw_exchange_run(sdcsw_exchange* x, double* u, int n_steps, int use_graph, void* stream);
 int sdcsw_exchange_set_option(sdcsw_exchange* x, int option, int value);
 int sdcsw_exchange_info(sdcsw_exchange* x, int* node_lo, int* node_count, int* launches_per_step);

@@ -42,6 +42,7 @@ EXPORTS = (
     "sdcsw_split_f_expl_begin",
     "sdcsw_split_f_expl_end",
     "sdcsw_exchange_create",
+    "sdcsw_exchange_create_split",
     "sdcsw_exchange_ipc_handle",
     "sdcsw_exchange_open_peers",
     "sdcsw_exchange_base",
@@ -118,12 +119,13 @@ _SIGS = {
     "sdcsw_split_f_expl_begin": [_p, _p, _i, _p],
     "sdcsw_split_f_expl_end": [_p, _p, _i, _p],
     "sdcsw_exchange_create": [_p, _i, _i, _dp, _i, _i, _i, ctypes.POINTER(_p)],
+    "sdcsw_exchange_create_split": [_p, _i, _i, _dp, _i, _i, _i, _i, ctypes.POINTER(_p)],
     "sdcsw_exchange_ipc_handle": [_p, _p, _i],
     "sdcsw_exchange_open_peers": [_p, _p, _i],
     "sdcsw_exchange_base": [_p, ctypes.POINTER(_p)],
     "sdcsw_exchange_attach_peer": [_p, _i, _p],
     "sdcsw_exchange_phase": [_p, _p, _i, _p],
-    "sdcsw_exchange_post": [_p, _i, _p],
+    "sdcsw_exchange_post": [_p, _i, _i, _p],
     "sdcsw_exchange_run": [_p, _p, _i, _i, _p],
     "sdcsw_exchange_set_option": [_p, _i, _i],
     "sdcsw_exchange_info": [_p, _ip, _ip, _ip],

@@ -228,6 +228,14 @@ cudaError_t launch_synth_prep(const Plan& p, const double2* u, int nb, double* x
 cudaError_t launch_synthesis_split(const Plan& p, const double* xsyn, int nb, cudaStream_t s);
 // ring over all latitudes reading a part-major Fourier buffer (fsyn_ext)
 cudaError_t launch_ring_split(const Plan& p, const Work& w, int nb, cudaStream_t s);
+// split synthesis of own m published into every spectral peer's buffer, and
+// the ring that waits for all parts (peer.cu)
+struct SynDst;
+struct RingPeer;
+cudaError_t launch_synthesis_peer(const Plan& p, const double* xsyn, int nb, cudaStream_t s,
+                                  const SynDst& d, int* step_counter);
+cudaError_t launch_ring_peer(const Plan& p, const Work& w, const double2* fbase, int nb,
+                             cudaStream_t s, const RingPeer& rp);
 cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, int nb,
                              cudaStream_t s, int* step_counter);
 cudaError_t launch_ring(const Plan& p, const Work& w, int nb, cudaStream_t s);
@@ -296,6 +304,29 @@ __device__ __forceinline__ long long peer_wait(const PeerWait& pw) {
   return (long long)(n & 1) * pw.par_stride;
 }
 #endif
+
+// Spectral split over peer memory (peer.cu): the S ranks of a spectral group
+// exchange the synthesised Fourier coefficients of their wavenumbers once per
+// f_E.  Fourier exchange n (n = fseq + 1, fseq counting this rank's completed
+// exchanges) is written by every rank's synthesis into part sp of parity
+// n & 1 of every spectral peer's part-major buffer; the ring kernel posts n
+// into flag[sp] of every spectral peer, waits for all S posts, reads parity
+// n & 1, and its last CTA to finish sets fseq = n (every CTA has read fseq by
+// then).  Double buffering as for the node exchange.
+struct SynDst {
+  int n;                           // destinations (0: plain synthesis into fsyn)
+  long long par_stride;            // double2 per parity of a Fourier exchange buffer
+  const unsigned long long* fseq;  // completed Fourier exchanges of this rank
+  double2* dst[kMaxPeers];         // part sp of every spectral peer's buffer (parity 0)
+};
+struct RingPeer {
+  const PeerFlags* flags;          // local Fourier flag block (null: no exchange)
+  unsigned long long* fseq;
+  unsigned int* done;              // CTAs finished (reset by the last one)
+  int world;
+  long long par_stride;            // double2 per parity
+  unsigned long long* post[kMaxPeers];  // &fourier flags of spectral peer q ->flag[sp]
+};
 
 // Sweep-fused analysis (latency regime, one state, M <= kFuseMaxNodes): the
 // epilogue takes f_E of every node straight from shared memory and runs the

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : (NB <= 
     const double* __restrict__ xsyn, int nb, int T, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ,
-    int NBC, const int* __restrict__ mlist, int Lp) {
+    int NBC, const int* __restrict__ mlist, int Lp, const SynDst sd) {
   SDCSW_PDL_ENTRY();
   if (SDCSW_TRIG_SYN == 1) SDCSW_PDL_TRIGGER();
   constexpr int NPAIR = (NB + 1) / 2;
@@ -255,9 +255,19 @@ __global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : (NB <= 
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
           const int j = j0 + 8 * a + g;
-          double2* dst = fsyn + ((((size_t)(b0 + be) * J + j) * Lp + kpos) * 4 + f) * 2;
-          dst[0] = make_double2(aE[a][c][0] + aO[a][c][0], aE[a][c][1] + aO[a][c][1]);
-          dst[1] = make_double2(aE[a][c][0] - aO[a][c][0], aE[a][c][1] - aO[a][c][1]);
+          const size_t off = ((((size_t)(b0 + be) * J + j) * Lp + kpos) * 4 + f) * 2;
+          const double2 vn = make_double2(aE[a][c][0] + aO[a][c][0], aE[a][c][1] + aO[a][c][1]);
+          const double2 vs = make_double2(aE[a][c][0] - aO[a][c][0], aE[a][c][1] - aO[a][c][1]);
+          if (sd.n == 0) {
+            fsyn[off] = vn;
+            fsyn[off + 1] = vs;
+          } else {  // spectral split over peer memory: every spectral peer's buffer
+            const long long par = (long long)((*sd.fseq + 1) & 1) * sd.par_stride;
+            for (int q = 0; q < sd.n; ++q) {
+              sd.dst[q][par + off] = vn;
+              sd.dst[q][par + off + 1] = vs;
+            }
+          }
         }
       }
     }
@@ -294,7 +304,7 @@ __global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : (NB <= 
     const double* __restrict__ xsyn, int nb, int T, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter, int WJ,
-    int NBC, const int* __restrict__ mlist, int Lp) {
+    int NBC, const int* __restrict__ mlist, int Lp, const SynDst sd) {
   SDCSW_PDL_ENTRY();
   constexpr int NPAIR = (NB + 1) / 2;
   constexpr int NT = 2 * NPAIR;
@@ -424,9 +434,19 @@ __global__ void __launch_bounds__(32 * kWarps, NB <= 2 ? SDCSW_SYN_MB1 : (NB <= 
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
           const int j = j0 + 8 * a + g;
-          double2* dst = fsyn + ((((size_t)(b0 + be) * J + j) * Lp + kpos) * 4 + f) * 2;
-          dst[0] = make_double2(aE[a][c][0] + aO[a][c][0], aE[a][c][1] + aO[a][c][1]);
-          dst[1] = make_double2(aE[a][c][0] - aO[a][c][0], aE[a][c][1] - aO[a][c][1]);
+          const size_t off = ((((size_t)(b0 + be) * J + j) * Lp + kpos) * 4 + f) * 2;
+          const double2 vn = make_double2(aE[a][c][0] + aO[a][c][0], aE[a][c][1] + aO[a][c][1]);
+          const double2 vs = make_double2(aE[a][c][0] - aO[a][c][0], aE[a][c][1] - aO[a][c][1]);
+          if (sd.n == 0) {
+            fsyn[off] = vn;
+            fsyn[off + 1] = vs;
+          } else {  // spectral split over peer memory: every spectral peer's buffer
+            const long long par = (long long)((*sd.fseq + 1) & 1) * sd.par_stride;
+            for (int q = 0; q < sd.n; ++q) {
+              sd.dst[q][par + off] = vn;
+              sd.dst[q][par + off + 1] = vs;
+            }
+          }
         }
       }
     }
@@ -788,20 +808,28 @@ cudaError_t launch_synth_prep(const Plan& p, const double2* u, int nb, double* x
 }
 
 static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist, int nm, int Lp,
-                                  const double* xsyn, int nb, cudaStream_t s, int* step_counter);
+                                  const double* xsyn, int nb, cudaStream_t s, int* step_counter,
+                                  const SynDst& sd);
 
 cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, int nb,
                              cudaStream_t s, int* step_counter) {
-  return synthesis_impl(p, w.fsyn, nullptr, p.T + 1, p.T + 1, xsyn, nb, s, step_counter);
+  return synthesis_impl(p, w.fsyn, nullptr, p.T + 1, p.T + 1, xsyn, nb, s, step_counter, SynDst{});
 }
 
 cudaError_t launch_synthesis_split(const Plan& p, const double* xsyn, int nb, cudaStream_t s) {
   double2* part = p.fsyn_ext + (size_t)p.split_sp * nb * p.J * p.Lp * 8;
-  return synthesis_impl(p, part, p.own_m, p.n_own_m, p.Lp, xsyn, nb, s, nullptr);
+  return synthesis_impl(p, part, p.own_m, p.n_own_m, p.Lp, xsyn, nb, s, nullptr, SynDst{});
+}
+
+cudaError_t launch_synthesis_peer(const Plan& p, const double* xsyn, int nb, cudaStream_t s,
+                                  const SynDst& d, int* step_counter) {
+  if (p.split_S < 2 || d.n < 1 || d.n > kMaxPeers) return cudaErrorInvalidValue;
+  return synthesis_impl(p, nullptr, p.own_m, p.n_own_m, p.Lp, xsyn, nb, s, step_counter, d);
 }
 
 static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist, int nm, int Lp,
-                                  const double* xsyn, int nb, cudaStream_t s, int* step_counter) {
+                                  const double* xsyn, int nb, cudaStream_t s, int* step_counter,
+                                  const SynDst& sd) {
   const int NB = pick_nb(nb);
   const int nblk = (nb + NB - 1) / NB;
   // latency regime (few batch blocks): 1 row tile x 4 K-splits (small T) or the
@@ -824,10 +852,11 @@ static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist
   if (NB == NBV) {                                                                             \
     if (cp)                                                                                    \
       launch_k(k_synthesis_cp<NBV>, grid, block, syn_cp_smem<NBV>(), s, xsyn, nb, p.T, p.J,    \
-               p.ptab_s, p.htab_s, p.rowoff, p.n_even, fsyn, step_counter, WJ, NBC, mlist, Lp); \
+               p.ptab_s, p.htab_s, p.rowoff, p.n_even, fsyn, step_counter, WJ, NBC, mlist, Lp, \
+               sd);                                                                            \
     else                                                                                       \
     launch_k(k_synthesis<NBV, 1>, grid, block, 0, s, xsyn, nb, p.T, p.J, p.ptab_s, p.htab_s, \
-             p.rowoff, p.n_even, fsyn, step_counter, WJ, NBC, mlist, Lp);                      \
+             p.rowoff, p.n_even, fsyn, step_counter, WJ, NBC, mlist, Lp, sd);                  \
     return cudaGetLastError();                                                                 \
   }
   SDCSW_NB_LIST(SDCSW_SYN)
@@ -866,8 +895,8 @@ cudaError_t launch_analysis_fused(const Plan& p, const Work& w, int nb, const Fu
                                   cudaStream_t s) {
   // one batch block must hold every node (NB = nb), and the epilogue fixes M;
   // publishing (mode 4) handles any batch
-  if (fz.mode == 4) {
-    if (p.kind != 0 || p.tma_ok || p.own_idx != nullptr || fz.peer_world < 1 ||
+  if (fz.mode == 4) {  // (a split plan's analysis computes, and so publishes, own m only)
+    if (p.kind != 0 || p.tma_ok || fz.peer_world < 1 ||
         fz.peer_world > kMaxPeers || nb < 1)
       return cudaErrorInvalidValue;
     return analysis_impl<true>(p, w, nullptr, nb, fz, s);

@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<THREADS>()) k_ring(co
                                                   double two_omega,
                                                   const int* __restrict__ m_part,
                                                   const int* __restrict__ m_k, int Lp, int nbg,
-                                                  int frag) {
+                                                  int frag, const RingPeer rp) {
   SDCSW_PDL_ENTRY();
   if (SDCSW_TRIG_RING == 1) SDCSW_PDL_TRIGGER();
   extern __shared__ double2 sm2[];
@@ -307,6 +307,20 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<THREADS>()) k_ring(co
     for (int k = threadIdx.x; k < TWN; k += THREADS) sm2[5 * NP + k] = twg[k];
   const double muj = mu[j], ws = wsyn[j], wk = wke[j];
   SDCSW_PDL_WAIT();
+  unsigned long long fx = 0;  // spectral split over peer memory: Fourier exchange number
+  if constexpr (SPLIT) {
+    if (rp.flags != nullptr) {
+      fx = *reinterpret_cast<volatile unsigned long long*>(rp.fseq) + 1;
+      if (threadIdx.x == 0) {  // post own part (written by the completed synthesis), wait for all
+        if (rp.world > 1) __threadfence_system();
+        for (int q = 0; q < rp.world; ++q) atomicMax_system(rp.post[q], fx);
+        for (int q = 0; q < rp.world; ++q)
+          while (ld_acquire_sys(&rp.flags->flag[q]) < fx) __nanosleep(32);
+      }
+      __syncthreads();
+      fsyn += (fx & 1) * rp.par_stride;
+    }
+  }
 
   // ---- inverse pass 0 (P = 1, no twiddles) from the Fourier coefficients:
   //      Z_m = X_m + i Y_m, Z_{N-m} = conj(X_m) + i conj(Y_m).
@@ -469,6 +483,16 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<THREADS>()) k_ring(co
     dh[kYZeta - kYPhi] = make_double2(v[1].x * ws, v[1].y * ws);
     dh[kYDelta - kYPhi] = make_double2(v[0].x * ws, v[0].y * ws);
   }
+  if constexpr (SPLIT) {
+    if (rp.flags != nullptr) {  // the last CTA to finish completes exchange fx for this rank
+      __syncthreads();
+      if (threadIdx.x == 0 &&
+          atomicAdd(rp.done, 1u) == gridDim.x * gridDim.y - 1) {
+        *rp.done = 0;
+        *rp.fseq = fx;
+      }
+    }
+  }
 #if SDCSW_EXP == 4
   __syncthreads();
 #endif
@@ -539,16 +563,17 @@ bool ring_pass_twiddles(int nlon, const double2* w, std::vector<double2>& out) {
 }
 
 static cudaError_t ring_impl(const Plan& p, const double2* fsyn, double2* gan, const int* m_part,
-                             const int* m_k, int Lp, int nb, cudaStream_t s) {
+                             const int* m_k, int Lp, int nb, cudaStream_t s,
+                             const RingPeer& rp = RingPeer{}) {
   dim3 grid(p.J, nb);
 #define SDCSW_RING_LAUNCH(NV, TV)                                                                  \
   if (p.nlon == NV) {                                                                              \
     if (m_part != nullptr)                                                                         \
       launch_k(k_ring<NV, TV, true>, grid, TV, p.ring_smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn,  \
-               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb, (int)tma_active(p));       \
+               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb, (int)tma_active(p), rp);   \
     else                                                                                           \
       launch_k(k_ring<NV, TV, false>, grid, TV, p.ring_smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn, \
-               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb, (int)tma_active(p));       \
+               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb, (int)tma_active(p), rp);   \
     return cudaGetLastError();                                                                     \
   }
   SDCSW_RING_SIZES(SDCSW_RING_LAUNCH)
@@ -563,6 +588,13 @@ cudaError_t launch_ring(const Plan& p, const Work& w, int nb, cudaStream_t s) {
 
 cudaError_t launch_ring_split(const Plan& p, const Work& w, int nb, cudaStream_t s) {
   return ring_impl(p, p.fsyn_ext, w.gan, p.m_part, p.m_k, p.Lp, nb, s);
+}
+
+cudaError_t launch_ring_peer(const Plan& p, const Work& w, const double2* fbase, int nb,
+                             cudaStream_t s, const RingPeer& rp) {
+  if (p.split_S < 2 || rp.flags == nullptr || rp.world < 1 || rp.world > kMaxPeers)
+    return cudaErrorInvalidValue;
+  return ring_impl(p, fbase, w.gan, p.m_part, p.m_k, p.Lp, nb, s, rp);
 }
 
 }  // namespace sdcsw

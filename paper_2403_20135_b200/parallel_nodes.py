@@ -259,7 +259,7 @@ class PeerNodeParallelDsdc:
     handles of the buffers; with ``world == 1`` no process group is needed."""
 
     def __init__(self, problem, cfg, dt, group=None, world=None, rank=None, fused=None,
-                 exchange_handles=True):
+                 exchange_handles=True, spectral_parts=1):
         import ctypes
 
         from . import _native
@@ -274,6 +274,8 @@ class PeerNodeParallelDsdc:
             else:
                 world, rank = 1, 0
         self.world, self.rank = int(world), int(rank)
+        self.nparts = int(spectral_parts)
+        self.part = self.rank % self.nparts
         self.m = cfg.table.n_nodes
         self.k = cfg.n_sweeps
         scalars = getattr(problem, "solve_coefficients", None)
@@ -281,9 +283,10 @@ class PeerNodeParallelDsdc:
             diagonal_step_coefficients(cfg, dt, problem.mean_geopotential, scalars))
         handle = ctypes.c_void_p()
         _native.check(
-            self.lib.sdcsw_exchange_create(problem.handle, self.m, self.k, _native.dptr(self._coef),
-                                           self._coef.size, self.world, self.rank,
-                                           ctypes.byref(handle)),
+            self.lib.sdcsw_exchange_create_split(problem.handle, self.m, self.k,
+                                                 _native.dptr(self._coef), self._coef.size,
+                                                 self.world, self.rank, self.nparts,
+                                                 ctypes.byref(handle)),
             "sdcsw_exchange_create",
         )
         self.handle = handle
@@ -301,15 +304,20 @@ class PeerNodeParallelDsdc:
                           "sdcsw_exchange_open_peers")
 
     @classmethod
-    def in_process(cls, problem, cfg, dt, world, fused=None):
+    def in_process(cls, problem, cfg, dt, world, fused=None, spectral_parts=1):
         """``world`` exchange objects of one process on one device, attached to
         each other directly (no IPC) - for driving several ranks' phases in
-        stream order (:meth:`phase`)."""
+        stream order (:meth:`run_in_stream_order`).  ``problem`` is one problem
+        or, with spectral parts (each rank splits its plan), one per rank."""
         import ctypes
 
         from . import _native
 
-        ranks = [cls(problem, cfg, dt, world=world, rank=r, fused=fused, exchange_handles=False)
+        probs = problem if isinstance(problem, (list, tuple)) else [problem] * world
+        if spectral_parts > 1 and len({id(q) for q in probs}) != world:
+            raise ParameterError("spectral parts need one problem (plan) per rank")
+        ranks = [cls(probs[r], cfg, dt, world=world, rank=r, fused=fused, exchange_handles=False,
+                     spectral_parts=spectral_parts)
                  for r in range(world)]
         bases = []
         for x in ranks:
@@ -345,33 +353,54 @@ class PeerNodeParallelDsdc:
         return n, n, (self.k - 1) * count + 1
 
     def phase(self, u, phase):
-        """Enqueue one phase of a step on ``u``: 0 = f_E(u0), 1..K-1 = sweep with its exchange,
-        K = closing solve."""
+        """Enqueue one half-phase of a step on ``u`` (``sdcsw_exchange_phase``):
+        2k = [node kernel k] + synthesis and 2k + 1 = ring + analysis of f_E k
+        (k = 0: f_E(u0)), 2K = closing solve."""
         from . import _native
 
         _native.check(self.lib.sdcsw_exchange_phase(self.handle, u.data_ptr(), int(phase),
                                                     self.problem.stream()), "sdcsw_exchange_phase")
 
-    def post(self, k):
-        """Enqueue only the post of exchange ``k`` of the current step."""
+    def post(self, channel, k=0):
+        """Enqueue only a post: channel 0 = node exchange ``k`` of the current
+        step, channel 1 = the next Fourier exchange (spectral parts)."""
         from . import _native
 
-        _native.check(self.lib.sdcsw_exchange_post(self.handle, int(k), self.problem.stream()),
-                      "sdcsw_exchange_post")
+        _native.check(self.lib.sdcsw_exchange_post(self.handle, int(channel), int(k),
+                                                   self.problem.stream()), "sdcsw_exchange_post")
 
     @staticmethod
     def run_in_stream_order(ranks, states, n_steps):
         """Advance the in-process ranks (:meth:`in_process`) on one stream:
-        per phase every rank first posts the exchange the phase consumes, then
-        every rank runs the phase - each wait is satisfied by earlier kernels."""
+        before each half-phase every rank posts what the half-phase waits for,
+        then every rank runs it - each wait is satisfied by earlier kernels."""
         k_sweeps = ranks[0].k
+        split = ranks[0].nparts > 1
+        # without spectral parts the ranks may share one plan (one workspace):
+        # each rank then runs both halves of an f_E back to back
+        groups = ([[h] for h in range(2 * k_sweeps + 1)] if split else
+                  [[2 * k, 2 * k + 1] for k in range(k_sweeps)] + [[2 * k_sweeps]])
         for _ in range(n_steps):
-            for ph in range(k_sweeps + 1):
-                if ph >= 2:  # phase ph (a sweep or the closing solve) consumes exchange ph - 1
+            for hs in groups:
+                k = hs[0] // 2
+                if hs[0] % 2 == 0 and k >= 2:  # node kernel k / closing solve: node exchange k - 1
                     for x in ranks:
-                        x.post(ph - 1)
+                        x.post(0, k - 1)
+                if hs[0] % 2 == 1:  # (split) ring of f_E k: its Fourier exchange
+                    for x in ranks:
+                        if k == 0 or x.info()[1] > 0:
+                            x.post(1)
                 for x, u in zip(ranks, states):
-                    x.phase(u, ph)
+                    for h in hs:
+                        x.phase(u, h)
+
+    def own_coefficients(self):
+        """Boolean mask over one field's coefficients (m-major triangle): the
+        entries this rank's state holds (all unless spectral parts)."""
+        trunc = self.problem.trunc
+        part = np.array(spectral_parts(trunc, self.nparts))
+        ms = np.concatenate([np.full(trunc + 1 - m, m) for m in range(trunc + 1)])
+        return part[ms] == self.part
 
     def run(self, u, n_steps, use_graph=True):
         """Advance the replicated device state ``u`` by ``n_steps`` steps in place."""

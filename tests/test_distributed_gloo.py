@@ -227,8 +227,8 @@ class _FakeExchangeLib:
         self.rank = rank
         self.calls = []
 
-    def sdcsw_exchange_create(self, plan, m, k, coef, n_coef, world, rank, out):
-        self.calls.append(("create", m, k, n_coef, world, rank))
+    def sdcsw_exchange_create_split(self, plan, m, k, coef, n_coef, world, rank, parts, out):
+        self.calls.append(("create", m, k, n_coef, world, rank, parts))
         out._obj.value = 1000 + rank
         return 0
 
@@ -267,7 +267,7 @@ def _peer_worker(rank, world, port, out_path):
     create = prob._lib.calls[0]
     opened = prob._lib.calls[1]
     np.save(out_path + f".{rank}.npy", np.frombuffer(opened[1], dtype=np.uint8))
-    assert create == ("create", 4, 3, x._coef.size, world, rank), create
+    assert create == ("create", 4, 3, x._coef.size, world, rank, 1), create
     assert x._coef.size >= 2 * 4 * 8 + 8
     assert x.handle.value == 1000 + rank
     dist.barrier()

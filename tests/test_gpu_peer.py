@@ -182,3 +182,37 @@ def test_exchange_reset_rebases_divergence():
     assert got == st.diverged() > 0
     st.close()
     x.close()
+
+
+@pytest.mark.parametrize("m,k,world,parts", [(3, 3, 2, 2), (3, 3, 4, 2), (3, 3, 6, 2), (3, 2, 3, 3),
+                                             (4, 4, 8, 2), (2, 3, 4, 4)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_exchange_spectral_split_bitwise(m, k, world, parts, fused):
+    """G node groups x S spectral parts over peer memory: every rank's own
+    wavenumbers equal the single-GPU stepper's, bitwise."""
+    import torch
+
+    from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    ref_p = gpu(63)
+    cfg = _cfg(m, k)
+    u0 = torch.from_numpy(random_initial_state(ref_p.grid, 4)).to(ref_p.device)
+    n_steps = 3
+    ref = _stepper_result(ref_p, cfg, 120.0, u0, n_steps).reshape(3, -1)
+    probs = [SphericalShallowWater(63, max_batch=4) for _ in range(world)]
+    ranks = PeerNodeParallelDsdc.in_process(probs, cfg, 120.0, world, fused=fused,
+                                            spectral_parts=parts)
+    states = [u0.clone() for _ in ranks]
+    PeerNodeParallelDsdc.run_in_stream_order(ranks, states, n_steps)
+    torch.cuda.synchronize()
+    covered = torch.zeros(ref.shape[1], dtype=torch.bool)
+    for x, u in zip(ranks, states):
+        own = torch.from_numpy(x.own_coefficients())
+        got = u.reshape(3, -1)[:, own.to(u.device)]
+        assert torch.equal(got, ref[:, own.to(u.device)]), (x.rank, x.part)
+        covered |= own
+        assert x.diverged() == 0
+    assert bool(covered.all())
+    for x in ranks:
+        x.close()
