@@ -335,6 +335,10 @@ def run_device(args):
         # the exchanges run in the kernels over peer memory (analysis epilogue and
         # split synthesis stores + flags), no NCCL on the data path
         groups = max(g for g in range(1, min(world, m_nodes) + 1) if world % g == 0)
+        if c["trunc"] >= 400:
+            # table-streaming regime: keep all nodes batched per GEMM (M x the
+            # arithmetic intensity) and split the wavenumbers only
+            groups = 1
         xpeer = PeerNodeParallelDsdc(problem, cfg, dt, spectral_parts=world // groups)
         launches_per_sim_step = xpeer.info()[2]
 
