@@ -216,3 +216,25 @@ def test_exchange_spectral_split_bitwise(m, k, world, parts, fused):
     assert bool(covered.all())
     for x in ranks:
         x.close()
+
+
+def test_exchange_spectral_split_table_streaming():
+    """T511 (TMA analysis, cp.async synthesis): 1 node group x 2 parts, all nodes batched."""
+    import torch
+
+    from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    ref_p = gpu(511, max_batch=4)
+    cfg = _cfg(3, 2)
+    u0 = torch.from_numpy(random_initial_state(ref_p.grid, 6)).to(ref_p.device)
+    ref = _stepper_result(ref_p, cfg, 30.0, u0, 2).reshape(3, -1)
+    probs = [SphericalShallowWater(511, max_batch=3) for _ in range(2)]
+    ranks = PeerNodeParallelDsdc.in_process(probs, cfg, 30.0, 2, spectral_parts=2)
+    states = [u0.clone() for _ in ranks]
+    PeerNodeParallelDsdc.run_in_stream_order(ranks, states, 2)
+    torch.cuda.synchronize()
+    for x, u in zip(ranks, states):
+        own = torch.from_numpy(x.own_coefficients()).to(u.device)
+        assert torch.equal(u.reshape(3, -1)[:, own], ref[:, own])
+        x.close()
