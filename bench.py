@@ -322,24 +322,41 @@ def run_device(args):
     stream = torch.cuda.current_stream(problem.device)
 
     multi = (world > 1 or args.node_parallel) and not ensemble
+    split_plan = False  # the multi-GPU orchestration m-partitioned the plan
+    transport = args.transport
+    if multi and transport == "p2p":
+        # peer mappings must work on every rank, else all ranks take NCCL
+        from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+
+        groups = max(g for g in range(1, min(world, m_nodes) + 1) if world % g == 0)
+        if c["trunc"] >= 400:
+            # table-streaming regime: keep all nodes batched per GEMM (M x the
+            # arithmetic intensity) and split the wavenumbers only (SURVEY 8e)
+            groups = 1
+        xpeer, p2p_error = None, None
+        try:
+            xpeer = PeerNodeParallelDsdc(problem, cfg, dt, spectral_parts=world // groups)
+        except Exception as exc:  # noqa: BLE001 - reported in the JSON line
+            p2p_error = f"{type(exc).__name__}: {exc}"
+        ok = torch.tensor([0 if p2p_error else 1], dtype=torch.int32, device=problem.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not int(ok.item()):
+            if xpeer is not None:
+                xpeer.close()
+            problem._lib.sdcsw_plan_set_split(problem.handle, 1, 0, None, 0)
+            transport = "nccl"
+            print(f"[bench] peer exchange unavailable ({p2p_error}); NCCL transport", file=sys.stderr)
     if not multi:
         stepper = DeviceStepper(problem, cfg, dt, serial=False, members=members)
         launches_per_sim_step = stepper.launches_per_step
 
         def one_run():
             stepper.run(u, nsteps, use_graph=True)
-    elif args.transport == "p2p":
-        from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
-
+    elif transport == "p2p":
         # node groups x spectral parts (the largest node-group count <= M dividing N);
         # the exchanges run in the kernels over peer memory (analysis epilogue and
         # split synthesis stores + flags), no NCCL on the data path
-        groups = max(g for g in range(1, min(world, m_nodes) + 1) if world % g == 0)
-        if c["trunc"] >= 400:
-            # table-streaming regime: keep all nodes batched per GEMM (M x the
-            # arithmetic intensity) and split the wavenumbers only (SURVEY 8e)
-            groups = 1
-        xpeer = PeerNodeParallelDsdc(problem, cfg, dt, spectral_parts=world // groups)
+        split_plan = world // groups > 1
         launches_per_sim_step = xpeer.info()[2]
 
         def one_run():
@@ -352,6 +369,7 @@ def run_device(args):
         spectral = world // groups
         npd = NodeParallelDsdc(CudaNodeBackend(problem), cfg, dt, problem.mean_geopotential,
                                problem.state_size, spectral_parts=spectral)
+        split_plan = spectral > 1
         launches_per_sim_step = 3 * (1 + (k_sw - 1)) + (k_sw - 1) + 1
         # the steps (kernels and NCCL all-gathers) replay as CUDA graphs of `chunk` steps
         chunk = max(c for c in range(1, 26) if nsteps % c == 0)
@@ -449,7 +467,10 @@ def run_device(args):
                    "note": "integrate() with a host numpy state per bench step (one 200-step run)"}
         # --- serial SDC on one GPU (the paper's sequential baseline)
         scfg = SdcConfig(table=table, n_sweeps=k_sw, mode=SweepMode.SERIAL)
-        sst = DeviceStepper(problem, scfg, dt, serial=True)
+        # serial SDC and the stage timings need an unsplit plan
+        aux = (SphericalShallowWater(c["trunc"], device=local, max_batch=max(m_nodes * members, 1))
+               if split_plan else problem)
+        sst = DeviceStepper(aux, scfg, dt, serial=True)
         us = (u0[0] if ensemble else u0).clone().contiguous()
         sst.run(us, 5)
         torch.cuda.synchronize()
@@ -463,7 +484,7 @@ def run_device(args):
         sst.close()
         fused = (not ensemble and world == 1
                  and launches_per_sim_step == 3 * k_sw)  # node updates in the analysis epilogue
-        roof, stage_us, stage_detail = stage_roofline(problem, c, members, fused)
+        roof, stage_us, stage_detail = stage_roofline(aux, c, members, fused)
         cpu = None
         if world == 1 and not args.no_cpu and not ensemble:
             r, cores, wall = cpu_oracle_rate(args.config, args.cpu_sample)
@@ -486,7 +507,7 @@ def run_device(args):
                 "parallelism": ("1 GPU: M nodes as concurrent graph branches / batched GEMM columns" if world == 1 and not multi
                                 else f"{world} GPUs: ensemble members sharded" if ensemble
                                 else (f"{world} GPUs: node blocks x spectral (m) split; (f_E, f_I) and Fourier parts exchanged over peer memory by the analysis epilogue / split synthesis (no NCCL on the data path)"
-                                      if args.transport == "p2p"
+                                      if transport == "p2p"
                                       else f"{world} GPUs: node blocks x spectral (m) split, NCCL all-gathers per sweep / per f_E")),
                 "ms_per_sim_step": t_dev / sim_steps * 1e3,
                 "node_sweeps_per_s": value * node_sweeps,
@@ -494,6 +515,7 @@ def run_device(args):
                 "dsdc_vs_serial_speedup_1gpu": value / serial_rate if (world == 1 and not ensemble) else None,
                 "stage_us_per_sim_step": stage_us, "stage_us": stage_detail,
                 "finite": finite,
+                "multi_gpu_transport": transport if multi else None,
             },
             "roofline": roof,
             "cpu_baseline": cpu,
