@@ -13,6 +13,7 @@
 // Same contraction and epilogue as k_analysis in legendre.cu:
 //   out[n,c] = sum_j P[n,j] Xfold[j,c] + sum_j H[n,j] Yfold[j,c]
 //   (pkg/src/parsdc/problems/swe.py:180-190 restated on the sphere).
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -232,7 +233,9 @@ static_assert(kRowsPerWarp * (8 * 6 + 1) * 4 * 8 <= 2 * kStages * kTileBytes,
 // 128-byte swizzle; out-of-range rows read as zero.
 cudaError_t make_table_maps(Plan& p) {
   p.tma_ok = false;
-  if (p.T < 400 || p.J % kTmaLat) return cudaSuccess;
+  const char* env = getenv("SDCSW_TMA_MIN_T");  // table-streaming analysis from this truncation
+  const int tmin = env ? atoi(env) : 400;
+  if (p.T < tmin || p.J % kTmaLat) return cudaSuccess;
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
