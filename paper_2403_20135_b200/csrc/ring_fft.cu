@@ -22,12 +22,6 @@
 #ifndef SDCSW_EXP
 #define SDCSW_EXP 0
 #endif
-// Twiddle tables in shared memory (staged per CTA) or read from global
-// memory through L1 (saves the staging and shared memory).  Measured per size
-// on B200: global reads win only at nlon = 384 with 128-thread CTAs (T127:
-// -1.2% per step, 64-member ensemble -2.6%); shared memory elsewhere.
-template <int N>
-constexpr bool ring_twg() { return N == 384; }
 
 namespace sdcsw {
 #if SDCSW_EXP == 4
@@ -180,6 +174,18 @@ constexpr int tw_off_fwd(int s) {
 template <int N>
 constexpr int tw_total() { return tw_off_fwd<N>(RadixPlan<N>::n); }
 
+// Twiddle tables in shared memory (staged per CTA) or read from global
+// memory through L1 (saves the staging and shared memory).  Measured on B200:
+// global reads win only for the throughput variant at nlon = 384 (128-thread
+// CTAs, 5 per SM: 64-member ensemble -6% per step); the latency regime keeps
+// 256-thread CTAs with staged twiddles.
+template <int N, int THREADS>
+constexpr bool ring_twg() { return N == 384 && THREADS == 128; }
+template <int N, int THREADS>
+constexpr size_t ring_smem_t() {
+  return (size_t)(5 * padded<N>() + (ring_twg<N, THREADS>() ? 0 : tw_total<N>())) * sizeof(double2);
+}
+
 // One in-place Stockham pass (radix R, sub-length P) over NF concurrent
 // transforms of length N at Z[f * padded<N>()], reading generation SHI and
 // writing generation SHO; twp = this pass's twiddle table.
@@ -259,7 +265,7 @@ static void build_pass_twiddles(const double2* w, std::vector<double2>& out) {
 }
 
 #ifndef SDCSW_RING_MINB128
-#define SDCSW_RING_MINB128 5  // 96 registers: 5 CTAs per SM (64-member ensemble -3.9%, T127 unchanged)
+#define SDCSW_RING_MINB128 5  // 96 registers: 5 CTAs per SM (throughput variant)
 #endif
 template <int THREADS>
 constexpr int ring_min_blocks() { return THREADS <= 128 ? SDCSW_RING_MINB128 : (THREADS <= 256 ? 3 : 1); }
@@ -282,7 +288,7 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<THREADS>()) k_ring(co
   constexpr int NS = RadixPlan<N>::n;
   constexpr int TWN = tw_total<N>();
   double2* Z = sm2;             // [5][NP] (padded)
-  constexpr bool TWG = ring_twg<N>();
+  constexpr bool TWG = ring_twg<N, THREADS>();
   // per-pass twiddle tables: global (read through L1) or staged in shared memory
   const double2* tw = TWG ? twg : sm2 + 5 * NP;
   const int L = T + 1;
@@ -506,13 +512,16 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<THREADS>()) k_ring(co
 #define SDCSW_RT192 256
 #endif
 #ifndef SDCSW_RT384
-#define SDCSW_RT384 128
+#define SDCSW_RT384 256
 #endif
 #ifndef SDCSW_RT768
 #define SDCSW_RT768 256
 #endif
 #define SDCSW_RING_SIZES(X) \
   X(96, SDCSW_RT96) X(192, SDCSW_RT192) X(384, SDCSW_RT384) X(768, SDCSW_RT768) X(1536, 512)
+// throughput variants (batches of at least kRingTputBatch states)
+#define SDCSW_RING_TPUT(X) X(384, 128)
+constexpr int kRingTputBatch = 16;
 
 bool ring_supported(int nlon) {
 #define SDCSW_RING_OK(NV, TV) if (nlon == NV) return true;
@@ -530,11 +539,12 @@ cudaError_t configure_ring(size_t /*smem*/) {
 #define SDCSW_RING_CFG(NV, TV)                                                                     \
   if (e == cudaSuccess)                                                                            \
     e = cudaFuncSetAttribute(k_ring<NV, TV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                             (int)ring_smem_bytes(NV));                                            \
+                             (int)ring_smem_t<NV, TV>());                                          \
   if (e == cudaSuccess)                                                                            \
     e = cudaFuncSetAttribute(k_ring<NV, TV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                             (int)ring_smem_bytes(NV));
+                             (int)ring_smem_t<NV, TV>());
   SDCSW_RING_SIZES(SDCSW_RING_CFG)
+  SDCSW_RING_TPUT(SDCSW_RING_CFG)
 #undef SDCSW_RING_CFG
   return e;
 }
@@ -547,7 +557,7 @@ extern "C" int sdcsw_debug_rtimes(unsigned long long* host, int n) {
 
 size_t ring_smem_bytes(int nlon) {
 #define SDCSW_RING_SMEM(NV, TV) \
-  if (nlon == NV) return (size_t)(5 * padded<NV>() + (ring_twg<NV>() ? 0 : tw_total<NV>())) * sizeof(double2);
+  if (nlon == NV) return ring_smem_t<NV, TV>();
   SDCSW_RING_SIZES(SDCSW_RING_SMEM)
 #undef SDCSW_RING_SMEM
   return 0;
@@ -568,13 +578,17 @@ static cudaError_t ring_impl(const Plan& p, const double2* fsyn, double2* gan, c
   dim3 grid(p.J, nb);
 #define SDCSW_RING_LAUNCH(NV, TV)                                                                  \
   if (p.nlon == NV) {                                                                              \
+    constexpr size_t smem = ring_smem_t<NV, TV>();                                                 \
     if (m_part != nullptr)                                                                         \
-      launch_k(k_ring<NV, TV, true>, grid, TV, p.ring_smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn,  \
+      launch_k(k_ring<NV, TV, true>, grid, TV, smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn,        \
                p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb, (int)tma_active(p), rp);   \
     else                                                                                           \
-      launch_k(k_ring<NV, TV, false>, grid, TV, p.ring_smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn, \
+      launch_k(k_ring<NV, TV, false>, grid, TV, smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn,       \
                p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb, (int)tma_active(p), rp);   \
     return cudaGetLastError();                                                                     \
+  }
+  if (nb >= kRingTputBatch) {
+    SDCSW_RING_TPUT(SDCSW_RING_LAUNCH)
   }
   SDCSW_RING_SIZES(SDCSW_RING_LAUNCH)
 #undef SDCSW_RING_LAUNCH
