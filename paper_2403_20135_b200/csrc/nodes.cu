@@ -188,15 +188,39 @@ __global__ void __launch_bounds__(256) k_final_node_c(
   const Tri f0r = f_impl_tri(a0r, phibar, lam), f0i = f_impl_tri(a0i, phibar, lam);
   const double* c = cf.v;
   Tri br = a0r, bi = a0i, flr = f0r, fli = f0i;
-  for (int j = 0; j < M; ++j) {
-    Tri er, ei, ir = f0r, ii = f0i;
-    load_tri2(fe + j * fe_stride, C, idx, er, ei);
-    if (!first) load_tri2(fi + j * fi_stride, C, idx, ir, ii);
-    br = axpy_tri(axpy_tri(br, c[j], er), c[j], ir);
-    bi = axpy_tri(axpy_tri(bi, c[j], ei), c[j], ii);
-    if (j == M - 1) {
-      flr = ir;
-      fli = ii;
+  if (M <= kFuseMaxNodes) {
+    // every load in flight before the first use (HBM-bound at large T)
+    constexpr int MX = kFuseMaxNodes;
+    Tri er[MX], ei[MX], ir[MX], ii[MX];
+#pragma unroll
+    for (int j = 0; j < MX; ++j)
+      if (j < M) {
+        load_tri2(fe + j * fe_stride, C, idx, er[j], ei[j]);
+        ir[j] = f0r;
+        ii[j] = f0i;
+        if (!first) load_tri2(fi + j * fi_stride, C, idx, ir[j], ii[j]);
+      }
+#pragma unroll
+    for (int j = 0; j < MX; ++j)
+      if (j < M) {
+        br = axpy_tri(axpy_tri(br, c[j], er[j]), c[j], ir[j]);
+        bi = axpy_tri(axpy_tri(bi, c[j], ei[j]), c[j], ii[j]);
+        if (j == M - 1) {
+          flr = ir[j];
+          fli = ii[j];
+        }
+      }
+  } else {
+    for (int j = 0; j < M; ++j) {
+      Tri er, ei, ir = f0r, ii = f0i;
+      load_tri2(fe + j * fe_stride, C, idx, er, ei);
+      if (!first) load_tri2(fi + j * fi_stride, C, idx, ir, ii);
+      br = axpy_tri(axpy_tri(br, c[j], er), c[j], ir);
+      bi = axpy_tri(axpy_tri(bi, c[j], ei), c[j], ii);
+      if (j == M - 1) {
+        flr = ir;
+        fli = ii;
+      }
     }
   }
   br = axmy_tri(br, c[M], flr);
