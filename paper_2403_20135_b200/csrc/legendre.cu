@@ -16,6 +16,10 @@
 //   out[n,c] = sum_j P[n,j] Xfold[j,c] + sum_j H[n,j] Yfold[j,c]
 //   with the fold (N+S or N-S) chosen by the parity class of row n.
 #include "node_math.cuh"
+
+#ifndef SDCSW_EPI_PRELOAD
+#define SDCSW_EPI_PRELOAD 1  // fused epilogue node data loaded before the split-K reduction
+#endif
 #ifndef SDCSW_EXP
 #define SDCSW_EXP 0
 #endif
@@ -480,7 +484,8 @@ template <int NB>
 __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o, int n, int mo,
                                             int m, int C, const double* __restrict__ lamv,
                                             const double2* __restrict__ xscale, double* stage,
-                                            int lane, int b0, int nb) {
+                                            int lane, int b0, int nb, const Tri& pre_a0,
+                                            const Tri* pre_fi) {
   constexpr int OS = 8 * NB + 1;
   constexpr int MX = kFuseMaxNodes;
   const int rr = lane & 15, ri = lane >> 4;
@@ -545,12 +550,12 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
     return;
   }
   const int M = fz.M;
-  const Tri a0 = load_tri(fz.u0, C2, e);
+  const Tri a0 = SDCSW_EPI_PRELOAD ? pre_a0 : load_tri(fz.u0, C2, e);
   const Tri fi0 = f_impl_tri(a0, fz.phibar, l);
   Tri fi[MX];
 #pragma unroll
   for (int j = 0; j < MX; ++j)
-    if (j < M) fi[j] = fz.first ? fi0 : load_tri(fz.fi + j * S2, C2, e);
+    if (j < M) fi[j] = fz.first ? fi0 : (SDCSW_EPI_PRELOAD ? pre_fi[j] : load_tri(fz.fi + j * S2, C2, e));
   if (fz.mode == 1) {
     const double2 sc = xscale[idx];
 #pragma unroll
@@ -721,6 +726,21 @@ __global__ void SDCSW_ANA_LB k_analysis(
     }
   }
   if (SDCSW_TRIG_ANA == 2) SDCSW_PDL_TRIGGER();
+  // fused epilogue (modes 1, 2): the node data (u0, f_I of every node) are
+  // loaded now, so their latency overlaps the split-K reduction
+  Tri pre_a0{}, pre_fi[FZ ? kFuseMaxNodes : 1];
+  if constexpr (FZ) {
+    if (SDCSW_EPI_PRELOAD && fn >= 0 && (fz.mode == 1 || fz.mode == 2)) {
+      const int C2 = 2 * C;
+      const int e = 2 * (fmo + fn - m) + (lane >> 4);
+      pre_a0 = load_tri(fz.u0, C2, e);
+      if (!fz.first) {
+#pragma unroll
+        for (int j = 0; j < kFuseMaxNodes; ++j)
+          if (j < fz.M) pre_fi[j] = load_tri(fz.fi + (size_t)j * 3 * C2, C2, e);
+      }
+    }
+  }
   PH(2)
   if (WK > 1) {  // lane-fastest layout: conflict-free shared-memory traffic
     double* d = red + warp * NACC * 32 + lane;
@@ -765,7 +785,7 @@ __global__ void SDCSW_ANA_LB k_analysis(
     if (writes_operand)
       for (int i = lane; i < kRowsPerWarp * per; i += 32) stage[i] = 0.0;
     __syncwarp();
-    fused_nodes<NB>(fz, o, fn, fmo, m, C, lam, xscale, stage, lane, b0, nb);
+    fused_nodes<NB>(fz, o, fn, fmo, m, C, lam, xscale, stage, lane, b0, nb, pre_a0, pre_fi);
     __syncwarp();
     const int nrow = rows - rw < kRowsPerWarp ? rows - rw : kRowsPerWarp;
     double2* dst = reinterpret_cast<double2*>(fz.xsyn + (size_t)(r0m + rw) * per);
