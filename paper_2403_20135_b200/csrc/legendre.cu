@@ -485,7 +485,7 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
                                             int m, int C, const double* __restrict__ lamv,
                                             const double2* __restrict__ xscale, double* stage,
                                             int lane, int b0, int nb, const Tri& pre_a0,
-                                            const Tri* pre_fi) {
+                                            const Tri* pre_fi, double pre_l, double2 pre_sc) {
   constexpr int OS = 8 * NB + 1;
   constexpr int MX = kFuseMaxNodes;
   const int rr = lane & 15, ri = lane >> 4;
@@ -494,7 +494,8 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
   const int C2 = 2 * C, e = 2 * idx + ri;
   const size_t S2 = 3 * (size_t)C2;
   const double* row = o + rr * OS;
-  const double l = lamv[idx];
+  const bool pre = SDCSW_EPI_PRELOAD && (fz.mode == 1 || fz.mode == 2);
+  const double l = pre ? pre_l : lamv[idx];
   const bool zero = m == 0 && ri == 1;
   Tri fe[NB];
 #pragma unroll
@@ -557,7 +558,7 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
   for (int j = 0; j < MX; ++j)
     if (j < M) fi[j] = fz.first ? fi0 : (SDCSW_EPI_PRELOAD ? pre_fi[j] : load_tri(fz.fi + j * S2, C2, e));
   if (fz.mode == 1) {
-    const double2 sc = xscale[idx];
+    const double2 sc = pre ? pre_sc : xscale[idx];
 #pragma unroll
     for (int q = 0; q < MX; ++q) {
       if (q >= M) break;
@@ -585,7 +586,8 @@ __device__ __forceinline__ void fused_nodes(const FuseArgs& fz, const double* o,
     store_tri(fz.u_out, C2, e, u);
     if (fz.diverged != nullptr && !finite_tri(u))
       atomicMin(fz.diverged, fz.step_counter ? *fz.step_counter : 1);
-    write_xsyn_half(stage + xsyn_off(rr, 0, 1), 16, ri, u.phi, u.zeta, u.delta, xscale[idx]);
+    write_xsyn_half(stage + xsyn_off(rr, 0, 1), 16, ri, u.phi, u.zeta, u.delta,
+                    pre ? pre_sc : xscale[idx]);
   }
 }
 
@@ -729,10 +731,15 @@ __global__ void SDCSW_ANA_LB k_analysis(
   // fused epilogue (modes 1, 2): the node data (u0, f_I of every node) are
   // loaded now, so their latency overlaps the split-K reduction
   Tri pre_a0{}, pre_fi[FZ ? kFuseMaxNodes : 1];
+  double pre_l = 0.0;
+  double2 pre_sc = make_double2(0.0, 0.0);
   if constexpr (FZ) {
     if (SDCSW_EPI_PRELOAD && fn >= 0 && (fz.mode == 1 || fz.mode == 2)) {
       const int C2 = 2 * C;
-      const int e = 2 * (fmo + fn - m) + (lane >> 4);
+      const int idx = fmo + fn - m;
+      const int e = 2 * idx + (lane >> 4);
+      pre_l = lam[idx];
+      pre_sc = xscale[idx];
       pre_a0 = load_tri(fz.u0, C2, e);
       if (!fz.first) {
 #pragma unroll
@@ -785,7 +792,8 @@ __global__ void SDCSW_ANA_LB k_analysis(
     if (writes_operand)
       for (int i = lane; i < kRowsPerWarp * per; i += 32) stage[i] = 0.0;
     __syncwarp();
-    fused_nodes<NB>(fz, o, fn, fmo, m, C, lam, xscale, stage, lane, b0, nb, pre_a0, pre_fi);
+    fused_nodes<NB>(fz, o, fn, fmo, m, C, lam, xscale, stage, lane, b0, nb, pre_a0, pre_fi,
+                    pre_l, pre_sc);
     __syncwarp();
     const int nrow = rows - rw < kRowsPerWarp ? rows - rw : kRowsPerWarp;
     double2* dst = reinterpret_cast<double2*>(fz.xsyn + (size_t)(r0m + rw) * per);
