@@ -78,6 +78,8 @@ struct Plan {
   int n_anal_work4;
   int synth_wj, anal_wj;  // row tiles per CTA (the other warps split K)
   int syn_cp;             // synthesis with the cp.async pipeline: 1 / 0 / -1 = automatic
+  int ana_bulk;           // table-streaming analysis with the B operand staged: 1 (default) / 0
+  int syn_bulk;           // CTA-staged bulk-copy synthesis (T >= 400): 1 / 0 / -1 = automatic
   FftPlan fft;
   // workspaces
   double2* fsyn;    // [max_batch][J][L][4][2]
@@ -405,6 +407,12 @@ cudaError_t launch_axpy(long long n, const double* x, double w, const double* y,
                         cudaStream_t s);
 
 cudaError_t make_table_maps(Plan& p);
+cudaError_t configure_synthesis_bulk();
+cudaError_t configure_analysis_bulk();
+bool synthesis_bulk_ok(const Plan& p, int nb);
+cudaError_t launch_synthesis_bulk(const Plan& p, double2* fsyn, const int* mlist, int nm, int Lp,
+                                  const double* xsyn, int nb, cudaStream_t s, int* step_counter,
+                                  const SynDst& sd);
 cudaError_t configure_synthesis();
 bool launch_analysis_tma(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s,
                          cudaError_t* err);

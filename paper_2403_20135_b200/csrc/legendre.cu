@@ -858,6 +858,8 @@ cudaError_t launch_synthesis_peer(const Plan& p, const double* xsyn, int nb, cud
 static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist, int nm, int Lp,
                                   const double* xsyn, int nb, cudaStream_t s, int* step_counter,
                                   const SynDst& sd) {
+  if (synthesis_bulk_ok(p, nb))  // table-streaming regime (legendre_tma.cu)
+    return launch_synthesis_bulk(p, fsyn, mlist, nm, Lp, xsyn, nb, s, step_counter, sd);
   const int NB = pick_nb(nb);
   const int nblk = (nb + NB - 1) / NB;
   // latency regime (few batch blocks): 1 row tile x 4 K-splits (small T) or the

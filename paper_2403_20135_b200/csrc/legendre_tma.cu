@@ -264,12 +264,19 @@ cudaError_t make_table_maps(Plan& p) {
   return cudaSuccess;
 }
 
+static cudaError_t launch_analysis_bulk(const Plan& p, const Work& w, double2* fe, int nb,
+                                        int NB, const int* work, int nwork, cudaStream_t s);
+
 bool launch_analysis_tma(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s,
                          cudaError_t* err) {
   if (!tma_active(p)) return false;
   const int NB = nb <= 6 ? nb : 4;
   const int* work = p.own_work != nullptr ? p.own_work : p.anal_work;
   const int nwork = p.own_work != nullptr ? p.n_own_work : p.n_anal_work;
+  if (p.ana_bulk != 0) {  // B operand staged with the tables (default)
+    *err = launch_analysis_bulk(p, w, fe, nb, NB, work, nwork, s);
+    return true;
+  }
   dim3 grid(nwork, (nb + NB - 1) / NB);
   const CUtensorMap& pm = *reinterpret_cast<const CUtensorMap*>(&p.tmap[0]);
   const CUtensorMap& hm = *reinterpret_cast<const CUtensorMap*>(&p.tmap[1]);
@@ -283,6 +290,415 @@ bool launch_analysis_tma(const Plan& p, const Work& w, double2* fe, int nb, cuda
   SDCSW_TMA_LAUNCH(5) SDCSW_TMA_LAUNCH(6)
 #undef SDCSW_TMA_LAUNCH
   return false;
+}
+
+// ---------------------------------------------------------------------------
+// Table-streaming Legendre synthesis (large truncations): CTA-staged operands.
+//
+// k_synthesis_cp stages every warp's own A and B fragments with 16-byte
+// cp.async copies; at T511 that costs ~280 instructions (address arithmetic,
+// copies, waits) per 18 DMMAs, so the kernel is issue-bound with the DMMA pipe
+// ~57% busy.  Here one thread feeds a kSynBS-deep ring of stages with bulk
+// copies (cp.async.bulk, completing on an mbarrier): per stage kSynKQ row
+// quads of the CTA's P and H slices (WJ x 2 latitude octets, contiguous in the
+// fragment-ordered tables) and the operand records of the same rows for all
+// states (contiguous too: [row/4][part][state][row%4][4]).  The operand is
+// staged once per CTA instead of once per warp, and the K loop is LDS + DMMA
+// only.  Same contraction, parity handling and output as k_synthesis_cp, with
+// no K-split (the sums run over k in the same order as its WK = 1 plan).
+// ---------------------------------------------------------------------------
+#ifndef SDCSW_SYNB_STAGES
+#define SDCSW_SYNB_STAGES 2
+#endif
+#ifndef SDCSW_SYNB_KQ
+#define SDCSW_SYNB_KQ 4
+#endif
+#ifndef SDCSW_SYNB_MINB
+#define SDCSW_SYNB_MINB 4  // resident CTAs per SM (NB > 2): 16 warps, <= 128 registers
+#endif
+#ifndef SDCSW_SYNB_MINB1
+#define SDCSW_SYNB_MINB1 6  // NB <= 2
+#endif
+constexpr int kSynKQ = SDCSW_SYNB_KQ;      // row quads (4 table rows each) per stage
+constexpr int kSynBS = SDCSW_SYNB_STAGES;  // stages in flight
+
+__host__ __device__ constexpr int synb_stage_doubles(int wj, int nbt) {
+  return kSynKQ * (2 * wj * 64 + 48 * nbt) + 16;  // + pad: odd-pair reads past the last quad
+}
+__host__ __device__ constexpr size_t synb_smem(int wj, int nbt) {
+  return (size_t)kSynBS * synb_stage_doubles(wj, nbt) * 8 + 8 * kSynBS;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int NB>
+__global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_MINB) k_synthesis_bulk(
+    const double* __restrict__ xsyn, int J, const double* __restrict__ ptab,
+    const double* __restrict__ htab, const int* __restrict__ rowoff,
+    const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter,
+    const int* __restrict__ mlist, int Lp, const SynDst sd) {
+  SDCSW_PDL_ENTRY();
+  constexpr int NPAIR = (NB + 1) / 2;
+  constexpr int NT = 2 * NPAIR;
+  constexpr int QX = 48 * NB;  // operand doubles per row quad (3 parts x NB states x 16)
+  extern __shared__ __align__(128) unsigned char synb_raw[];
+  const int WJ = blockDim.x >> 5;
+  const int SD = synb_stage_doubles(WJ, NB);
+  const int TQ = WJ * 64;  // table doubles per row quad of this CTA's latitudes
+  double* stages = reinterpret_cast<double*>(synb_raw);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(synb_raw + (size_t)kSynBS * SD * 8);
+
+  const int kpos = blockIdx.y;
+  const int m = mlist != nullptr ? mlist[kpos] : kpos;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int gb = g >> 2, gc = g & 3;
+  const int j0 = (blockIdx.x * WJ + warp) * kRowsPerWarp;
+  const int r0m = rowoff[m];
+  const int nsteps = (rowoff[m + 1] - r0m) >> 2;
+  const int se = n_even[m] >> 2;
+  const int nstage = (nsteps + kSynKQ - 1) / kSynKQ;
+  const size_t qstride = (size_t)(J / 8) * 32;
+  const double* Pc = ptab + (size_t)(r0m / 4) * qstride + (size_t)blockIdx.x * TQ;
+  const double* Hc = htab + (size_t)(r0m / 4) * qstride + (size_t)blockIdx.x * TQ;
+  const double* Xc = xsyn + (size_t)(r0m / 4) * QX;
+
+  auto nq_of = [&](int i) { return min(kSynKQ, nsteps - i * kSynKQ); };
+  auto issue_tables = [&](int i) {  // thread 0
+    double* st = stages + (i % kSynBS) * SD;
+    const int nq = nq_of(i);
+    mbar_expect_tx(&full[i % kSynBS], (unsigned)(nq * (2 * TQ + QX) * 8));
+    for (int q = 0; q < nq; ++q) {
+      const size_t src = (size_t)(i * kSynKQ + q) * qstride;
+      bulk_g2s(st + q * TQ, Pc + src, TQ * 8, &full[i % kSynBS]);
+      bulk_g2s(st + (kSynKQ + q) * TQ, Hc + src, TQ * 8, &full[i % kSynBS]);
+    }
+  };
+  auto issue_operand = [&](int i) {  // thread 0, after the producer grid completed
+    double* st = stages + (i % kSynBS) * SD;
+    bulk_g2s(st + 2 * kSynKQ * TQ, Xc + (size_t)i * kSynKQ * QX, (unsigned)(nq_of(i) * QX * 8),
+             &full[i % kSynBS]);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSynBS; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  // the tables are constant: start streaming them before the producer grid ends
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kSynBS && i < nstage; ++i) issue_tables(i);
+  SDCSW_PDL_WAIT();
+  if (threadIdx.x == 0) {
+    if (step_counter != nullptr && (blockIdx.x | blockIdx.y) == 0) atomicAdd(step_counter, 1);
+    for (int i = 0; i < kSynBS && i < nstage; ++i) issue_operand(i);
+  }
+
+  double aE[2][NT][2], aO[2][NT][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < NT; ++c) aE[a][c][0] = aE[a][c][1] = aO[a][c][0] = aO[a][c][1] = 0.0;
+
+  for (int i = 0; i < nstage; ++i) {
+    mbar_wait(&full[i % kSynBS], (i / kSynBS) & 1);
+    const double* st = stages + (i % kSynBS) * SD;
+    const int nq = nq_of(i);
+#pragma unroll
+    for (int q = 0; q < kSynKQ; ++q) {
+      if (q < nq) {
+        const double* pq = st + q * TQ + warp * 64 + lane;
+        const double* hq = pq + kSynKQ * TQ;
+        const double aP0 = pq[0], aP1 = pq[32], aH0 = hq[0], aH1 = hq[32];
+        const double* xq = st + 2 * kSynKQ * TQ + q * QX + gb * 16 + t * 4 + gc;
+        double bP[NT], bH[NPAIR];
+#pragma unroll
+        for (int p = 0; p < NPAIR; ++p) {
+          bP[2 * p] = xq[p * 32];
+          bP[2 * p + 1] = xq[16 * NB + p * 32];
+          bH[p] = xq[32 * NB + p * 32];
+        }
+        if (i * kSynKQ + q < se) {  // n - m even: P symmetric (E), H antisymmetric (O)
+#pragma unroll
+          for (int c = 0; c < NT; ++c) { dmma_t(aE[0][c], aP0, bP[c]); dmma_t(aE[1][c], aP1, bP[c]); }
+#pragma unroll
+          for (int p = 0; p < NPAIR; ++p) { dmma_t(aO[0][2 * p], aH0, bH[p]); dmma_t(aO[1][2 * p], aH1, bH[p]); }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NT; ++c) { dmma_t(aO[0][c], aP0, bP[c]); dmma_t(aO[1][c], aP1, bP[c]); }
+#pragma unroll
+          for (int p = 0; p < NPAIR; ++p) { dmma_t(aE[0][2 * p], aH0, bH[p]); dmma_t(aE[1][2 * p], aH1, bH[p]); }
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with this stage
+    if (threadIdx.x == 0 && i + kSynBS < nstage) {
+      issue_tables(i + kSynBS);
+      issue_operand(i + kSynBS);
+    }
+  }
+
+#pragma unroll
+  for (int c = 0; c < NT; ++c) {
+    const int be = 2 * (c >> 1) + (t >> 1);
+    const int f = (t & 1) + 2 * (c & 1);
+    if (be >= NB) continue;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int j = j0 + 8 * a + g;
+      const size_t off = ((((size_t)be * J + j) * Lp + kpos) * 4 + f) * 2;
+      const double2 vn = make_double2(aE[a][c][0] + aO[a][c][0], aE[a][c][1] + aO[a][c][1]);
+      const double2 vs = make_double2(aE[a][c][0] - aO[a][c][0], aE[a][c][1] - aO[a][c][1]);
+      if (sd.n == 0) {
+        fsyn[off] = vn;
+        fsyn[off + 1] = vs;
+      } else {  // spectral split over peer memory: every spectral peer's buffer
+        const long long par = (long long)((*sd.fseq + 1) & 1) * sd.par_stride;
+        for (int q = 0; q < sd.n; ++q) {
+          sd.dst[q][par + off] = vn;
+          sd.dst[q][par + off + 1] = vs;
+        }
+      }
+    }
+  }
+}
+
+cudaError_t configure_synthesis_bulk() {
+  cudaError_t e = cudaSuccess;
+#define SDCSW_SYNB_CFG(NBV)                                                                   \
+  if (e == cudaSuccess)                                                                       \
+    e = cudaFuncSetAttribute(k_synthesis_bulk<NBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)synb_smem(4, NBV));
+  SDCSW_SYNB_CFG(1) SDCSW_SYNB_CFG(2) SDCSW_SYNB_CFG(3) SDCSW_SYNB_CFG(4) SDCSW_SYNB_CFG(5)
+  SDCSW_SYNB_CFG(6)
+#undef SDCSW_SYNB_CFG
+  return e;
+}
+
+// one batch block of nb <= 6 states, every state in the operand record (nb = NB)
+bool synthesis_bulk_ok(const Plan& p, int nb) {
+  // automatic from T200 (T255 4 states 32.5 vs 38.6 us; one state 31.3 vs 29.9 us,
+  // kept on the same kernel so results stay bitwise independent of the batching)
+  const int on = p.syn_bulk >= 0 ? p.syn_bulk : (p.T >= 200 ? 1 : 0);
+  return on && nb >= 1 && nb <= 6 && p.J % 32 == 0;
+}
+
+cudaError_t launch_synthesis_bulk(const Plan& p, double2* fsyn, const int* mlist, int nm, int Lp,
+                                  const double* xsyn, int nb, cudaStream_t s, int* step_counter,
+                                  const SynDst& sd) {
+  const int WJ = p.J % 64 == 0 ? 4 : 2;
+  const dim3 grid(p.J / (kRowsPerWarp * WJ), nm);
+#define SDCSW_SYNB_LAUNCH(NBV)                                                                \
+  if (nb == NBV)                                                                              \
+    return launch_k(k_synthesis_bulk<NBV>, grid, dim3(32 * WJ), synb_smem(WJ, NBV), s, xsyn,  \
+                    p.J, p.ptab_s, p.htab_s, p.rowoff, p.n_even, fsyn, step_counter, mlist, Lp, \
+                    sd);
+  SDCSW_SYNB_LAUNCH(1) SDCSW_SYNB_LAUNCH(2) SDCSW_SYNB_LAUNCH(3) SDCSW_SYNB_LAUNCH(4)
+  SDCSW_SYNB_LAUNCH(5) SDCSW_SYNB_LAUNCH(6)
+#undef SDCSW_SYNB_LAUNCH
+  return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------
+// Table-streaming analysis with the B operand staged too (k_analysis_bulk).
+//
+// k_analysis_tma streams the tables by TMA but loads the analysis-data B
+// fragments per lane from global memory, prefetched one k-step ahead in
+// registers (~80 of its 168), which costs residency and ~200 instructions per
+// 20 DMMAs.  Here each stage also carries, per state, the 16 latitudes x 28
+// doubles of analysis data the chunk needs (one contiguous 3.5 KB bulk copy in
+// the fragment order the ring kernel writes), completing on the same mbarrier
+// as the table tiles; the K loop reads A and B from shared memory only.  Same
+// sums in the same order as k_analysis_tma (bitwise equal), same epilogue.
+// ---------------------------------------------------------------------------
+#ifndef SDCSW_ANAB_STAGES
+#define SDCSW_ANAB_STAGES 2
+#endif
+#ifndef SDCSW_ANAB_MINB
+#define SDCSW_ANAB_MINB 3
+#endif
+constexpr int kAnbS = SDCSW_ANAB_STAGES;
+constexpr int kAnbChunk = kTmaLat * 28;  // analysis-data doubles per state per stage
+template <int NB>
+constexpr size_t anab_smem() {
+  return (size_t)kAnbS * (2 * kTileBytes + NB * kAnbChunk * 8) + 8 * kAnbS;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(128, SDCSW_ANAB_MINB) k_analysis_bulk(
+    const __grid_constant__ CUtensorMap pmap, const __grid_constant__ CUtensorMap hmap,
+    const double2* __restrict__ gan, int nb, int T, int J, int C, const int* __restrict__ rowoff,
+    const int* __restrict__ n_even, const int* __restrict__ row_n, const int* __restrict__ moff,
+    const double* __restrict__ lam, const int* __restrict__ work, double2* __restrict__ fe) {
+  SDCSW_PDL_ENTRY();
+  constexpr int PC = 8 * NB;
+  constexpr int OS = PC + 1;
+  extern __shared__ __align__(1024) unsigned char anb_smem[];
+  double* ptile = reinterpret_cast<double*>(anb_smem);  // [kAnbS][64][16], swizzled
+  double* htile = reinterpret_cast<double*>(anb_smem + kAnbS * kTileBytes);
+  double* btile = reinterpret_cast<double*>(anb_smem + 2 * kAnbS * kTileBytes);  // [kAnbS][NB][448]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(
+      anb_smem + 2 * kAnbS * kTileBytes + (size_t)kAnbS * NB * kAnbChunk * 8);
+
+  const int wk = work[blockIdx.x];
+  const int m = wk >> 16, rb = wk & 0xffff;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int b0 = blockIdx.y * NB;
+  const int nbv = nb - b0 < NB ? nb - b0 : NB;
+  const int L = T + 1;
+  const int r0m = rowoff[m];
+  const int rows = rowoff[m + 1] - r0m;
+  const int le = n_even[m];
+  const int rblock = r0m + rb * kTmaRows;
+  const int rw = rb * kTmaRows + warp * kRowsPerWarp;
+  const bool live = rw < rows;
+  const bool ev0 = rw < le, ev1 = rw + 8 < le;
+  const int nchunks = J / kTmaLat;
+  const double* gsrc = reinterpret_cast<const double*>(gan) + ((size_t)b0 * L + m) * J * 28;
+  const size_t bstride = (size_t)L * J * 28;  // doubles per state
+
+  auto issue_tables = [&](int ch) {  // thread 0
+    const int st = ch % kAnbS;
+    mbar_expect_tx(&full[st], 2 * kTileBytes + nbv * kAnbChunk * 8);
+    tma_load_2d(ptile + st * kTmaRows * kTmaLat, &pmap, ch * kTmaLat, rblock, &full[st]);
+    tma_load_2d(htile + st * kTmaRows * kTmaLat, &hmap, ch * kTmaLat, rblock, &full[st]);
+  };
+  auto issue_data = [&](int ch) {  // thread 0, after the producer grid completed
+    const int st = ch % kAnbS;
+    for (int c = 0; c < nbv; ++c)
+      bulk_g2s(btile + (st * NB + c) * kAnbChunk, gsrc + c * bstride + (size_t)ch * kAnbChunk,
+               kAnbChunk * 8, &full[st]);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kAnbS; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int ch = 0; ch < kAnbS && ch < nchunks; ++ch) issue_tables(ch);
+  SDCSW_PDL_WAIT();
+  if (threadIdx.x == 0)
+    for (int ch = 0; ch < kAnbS && ch < nchunks; ++ch) issue_data(ch);
+
+  // lane offsets in a k-step's 112-double record: [S: P 4x8 | H 4x6][A: same]
+  const int po = t * 8 + g;
+  const int ho = 32 + t * 6 + (g < 6 ? g : 0);
+  const bool hcol = g < 6;
+  const bool any_ev = ev0 || ev1, any_od = !ev0 || !ev1;
+  double acc[2][NB][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+  const int row0 = warp * kRowsPerWarp + g;
+
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int st = ch % kAnbS;
+    mbar_wait(&full[st], (ch / kAnbS) & 1);
+    if (live) {
+      const double* pt = ptile + st * kTmaRows * kTmaLat;
+      const double* ht = htile + st * kTmaRows * kTmaLat;
+      const double* bt = btile + st * NB * kAnbChunk;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = 4 * q + t;
+        const double aP0 = swz(pt, row0, k), aP1 = swz(pt, row0 + 8, k);
+        const double aH0 = swz(ht, row0, k), aH1 = swz(ht, row0 + 8, k);
+        double ps[NB], pa[NB], hs[NB], ha[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          const double* r = bt + c * kAnbChunk + q * 112;
+          ps[c] = any_ev ? r[po] : 0.0;
+          pa[c] = any_od ? r[56 + po] : 0.0;
+          hs[c] = any_od && hcol ? r[ho] : 0.0;
+          ha[c] = any_ev && hcol ? r[56 + ho] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          dmma_t(acc[0][c], aP0, ev0 ? ps[c] : pa[c]);
+          dmma_t(acc[1][c], aP1, ev1 ? ps[c] : pa[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          dmma_t(acc[0][c], aH0, ev0 ? ha[c] : hs[c]);
+          dmma_t(acc[1][c], aH1, ev1 ? ha[c] : hs[c]);
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with stage st
+    if (threadIdx.x == 0 && ch + kAnbS < nchunks) {
+      issue_tables(ch + kAnbS);
+      issue_data(ch + kAnbS);
+    }
+  }
+  if (!live) return;
+  double* o = ptile + warp * kRowsPerWarp * OS;  // P and H stages; all copies landed and were consumed
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      o[(8 * a + g) * OS + 8 * c + 2 * t] = acc[a][c][0];
+      o[(8 * a + g) * OS + 8 * c + 2 * t + 1] = acc[a][c][1];
+    }
+  __syncwarp();
+  const int mo = moff[m];
+  for (int it = lane; it < kRowsPerWarp * NB; it += 32) {
+    const int rr = it % kRowsPerWarp, b = it / kRowsPerWarp;
+    if (rw + rr >= rows || b0 + b >= nb) continue;
+    const int n = row_n[r0m + rw + rr];
+    if (n < 0) continue;
+    const int idx = mo + n - m;
+    const double* row = o + rr * OS;
+    const double l = lam[idx];
+    double2 phi = make_double2(row[8 * b + 0], row[8 * b + 1]);
+    double2 zeta = make_double2(row[8 * b + 2], row[8 * b + 3]);
+    double2 delta = make_double2(__fma_rn(l, row[8 * b + 6], row[8 * b + 4]),
+                                 __fma_rn(l, row[8 * b + 7], row[8 * b + 5]));
+    if (m == 0) phi.y = zeta.y = delta.y = 0.0;
+    double2* dst = fe + (size_t)(b0 + b) * 3 * C;
+    dst[idx] = phi;
+    dst[C + idx] = zeta;
+    dst[2 * C + idx] = delta;
+  }
+}
+
+static_assert(kRowsPerWarp * (8 * 6 + 1) * 4 * 8 <= 2 * kAnbS * kTileBytes,
+              "bulk analysis epilogue tiles fit in the table stage buffers");
+
+cudaError_t configure_analysis_bulk() {
+  cudaError_t e = cudaSuccess;
+#define SDCSW_ANAB_CFG(NBV)                                                                   \
+  if (e == cudaSuccess)                                                                       \
+    e = cudaFuncSetAttribute(k_analysis_bulk<NBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)anab_smem<NBV>());
+  SDCSW_ANAB_CFG(1) SDCSW_ANAB_CFG(2) SDCSW_ANAB_CFG(3) SDCSW_ANAB_CFG(4) SDCSW_ANAB_CFG(5)
+  SDCSW_ANAB_CFG(6)
+#undef SDCSW_ANAB_CFG
+  return e;
+}
+
+static cudaError_t launch_analysis_bulk(const Plan& p, const Work& w, double2* fe, int nb,
+                                        int NB, const int* work, int nwork, cudaStream_t s) {
+  dim3 grid(nwork, (nb + NB - 1) / NB);
+  const CUtensorMap& pm = *reinterpret_cast<const CUtensorMap*>(&p.tmap[0]);
+  const CUtensorMap& hm = *reinterpret_cast<const CUtensorMap*>(&p.tmap[1]);
+#define SDCSW_ANAB_LAUNCH(NBV)                                                                    \
+  if (NB == NBV)                                                                                  \
+    return launch_k(k_analysis_bulk<NBV>, grid, dim3(128), anab_smem<NBV>(), s, pm, hm, w.gan, nb, \
+                    p.T, p.J, p.C, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, work, fe);
+  SDCSW_ANAB_LAUNCH(1) SDCSW_ANAB_LAUNCH(2) SDCSW_ANAB_LAUNCH(3) SDCSW_ANAB_LAUNCH(4)
+  SDCSW_ANAB_LAUNCH(5) SDCSW_ANAB_LAUNCH(6)
+#undef SDCSW_ANAB_LAUNCH
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace sdcsw

@@ -211,6 +211,10 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   // cp.async-pipelined synthesis: -1 = automatic (see synthesis_impl)
   p.syn_cp = -1;
   if (const char* env = getenv("SDCSW_SYN_CP")) p.syn_cp = atoi(env);
+  p.ana_bulk = 1;
+  if (const char* env = getenv("SDCSW_ANA_BULK")) p.ana_bulk = atoi(env);
+  p.syn_bulk = -1;
+  if (const char* env = getenv("SDCSW_SYN_BULK")) p.syn_bulk = atoi(env);
   if (const char* env = getenv("SDCSW_ANAL_WJ")) p.anal_wj = atoi(env);
   if (const char* env = getenv("SDCSW_SYNTH_WJ")) p.synth_wj = atoi(env);
   while ((J / kRowsPerWarp) % p.synth_wj) p.synth_wj /= 2;
@@ -271,6 +275,8 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
       (e = cudaMalloc(&p.coef_dev, kCoefCap * sizeof(double))) != cudaSuccess ||
       (e = configure_ring(p.ring_smem)) != cudaSuccess ||
       (e = configure_synthesis()) != cudaSuccess ||
+      (e = configure_synthesis_bulk()) != cudaSuccess ||
+      (e = configure_analysis_bulk()) != cudaSuccess ||
       (e = make_table_maps(p)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess) {
     int st = cuda_status(e, "sdcsw_plan_create");
