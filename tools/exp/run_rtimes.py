@@ -2,13 +2,14 @@ import ctypes, sys
 sys.path.insert(0, '/root/repo')
 import numpy as np
 from paper_2403_20135_b200 import _native
-_native.LIB_PATH = '/root/repo/tools/exp/libsdcsw_exp4.so'
+_native.LIB_PATH = '/root/repo/build/var/exp4.so'
 L = _native.load(_native.LIB_PATH)
 import bench, torch
 from paper_2403_20135_b200.problem import SphericalShallowWater
-for cfg, nb in (('c1', 1), ('c1', 4)):
+runs = [(a.split(':')[0], int(a.split(':')[1])) for a in sys.argv[1:]] or [('c1', 1), ('c1', 4)]
+for cfg, nb in runs:
     c = bench.CONFIGS[cfg]
-    p = SphericalShallowWater(c['trunc'], max_batch=4)
+    p = SphericalShallowWater(c['trunc'], max_batch=max(nb, 4))
     bench.time_stage(p, 0, nb, reps=3)
     u = p.empty_states(nb); out = p.empty_states(nb)
     for _ in range(3):
