@@ -464,7 +464,7 @@ def run_device(args):
             e2e = {"value": sim_steps / t_e2e, "unit": UNIT,
                    "h2d_bytes_per_step": int(u0_host.nbytes),
                    "d2h_bytes_per_step": int(traj.states[-1].nbytes),
-                   "note": "integrate() with a host numpy state per bench step (one 200-step run)"}
+                   "note": f"integrate() with a host numpy state per bench step (one {nsteps}-step run)"}
         # --- serial SDC on one GPU (the paper's sequential baseline)
         scfg = SdcConfig(table=table, n_sweeps=k_sw, mode=SweepMode.SERIAL)
         # serial SDC and the stage timings need an unsplit plan

@@ -206,7 +206,8 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   std::vector<int> work;
   // row tiles per CTA: small truncations split K over the 4 warps (more warps
   // in flight), large ones give each warp its own row tile (B reuse via L1)
-  p.anal_wj = T < 200 ? 1 : (T < 400 ? 2 : 4);
+  // (from T200 the table-streaming analysis runs, which takes 4 row tiles per CTA)
+  p.anal_wj = T < 200 ? 1 : 4;
   p.synth_wj = T < 200 ? 1 : (T < 400 ? 2 : 4);
   // cp.async-pipelined synthesis: -1 = automatic (see synthesis_impl)
   p.syn_cp = -1;

@@ -239,7 +239,7 @@ class DeviceStepper:
         _native.check(self.lib.sdcsw_stepper_set_option(self.handle, 1, int(bool(on))), "set_option")
 
     def set_fused(self, on=True):
-        """Node updates in the analysis epilogue (default where supported: T < 400, M <= 6)."""
+        """Node updates in the analysis epilogue (default where supported: T < 200, M <= 6)."""
         _native.check(self.lib.sdcsw_stepper_set_option(self.handle, 2, int(bool(on))), "set_option")
         n = ctypes.c_int()
         _native.check(self.lib.sdcsw_stepper_launches_per_step(self.handle, ctypes.byref(n)))

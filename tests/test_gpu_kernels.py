@@ -243,7 +243,7 @@ def test_node_parallel_single_rank_matches_fused_stepper():
 
 
 @pytest.mark.parametrize("trunc,m_count,k_count", [(63, 1, 1), (63, 2, 3), (63, 3, 1), (63, 4, 4),
-                                                   (63, 5, 2), (63, 6, 3), (255, 4, 3)])
+                                                   (63, 5, 2), (63, 6, 3), (127, 4, 3)])
 def test_fused_node_epilogue_bitwise(trunc, m_count, k_count):
     """Node updates fused into the analysis epilogue == separate node kernels
     (batched, chained and sequential), bitwise; launches per step 3K vs 4+4(K-1)."""
