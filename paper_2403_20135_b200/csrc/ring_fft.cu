@@ -270,6 +270,17 @@ static void build_pass_twiddles(const double2* w, std::vector<double2>& out) {
 template <int THREADS>
 constexpr int ring_min_blocks() { return THREADS <= 128 ? SDCSW_RING_MINB128 : (THREADS <= 256 ? 3 : 1); }
 
+#ifndef SDCSW_RING_L2PF
+#define SDCSW_RING_L2PF 1536  // nlon from which the ring kernel prefetches one wave ahead
+#endif
+// resident CTAs per SM of a ring kernel (shared memory bound; registers allow more)
+template <int N, int THREADS>
+constexpr int ring_resident() {
+  return (int)(232448 / (ring_smem_t<N, THREADS>() + 1024)) < ring_min_blocks<THREADS>()
+             ? (int)(232448 / (ring_smem_t<N, THREADS>() + 1024))
+             : ring_min_blocks<THREADS>();
+}
+
 template <int N, int THREADS, bool SPLIT>
 __global__ void __launch_bounds__(THREADS, ring_min_blocks<THREADS>()) k_ring(const double2* __restrict__ fsyn,
                                                   double2* __restrict__ gan, int J, int T,
@@ -313,6 +324,23 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<THREADS>()) k_ring(co
     for (int k = threadIdx.x; k < TWN; k += THREADS) sm2[5 * NP + k] = twg[k];
   const double muj = mu[j], ws = wsyn[j], wk = wke[j];
   SDCSW_PDL_WAIT();
+  if constexpr (!SPLIT && N >= SDCSW_RING_L2PF) {
+    // many waves (large nlon): pull the Fourier block of the CTA one wave ahead
+    // (linear index + resident CTAs) into L2, so its load phase hits L2 (T511, 5 states:
+    // 296.7 -> 290.0 us; neutral at nlon 768, measured)
+    if (threadIdx.x == 0) {
+      unsigned nsm;
+      asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+      const unsigned ahead = nsm * (unsigned)ring_resident<N, THREADS>();
+      const unsigned nxt = blockIdx.y * gridDim.x + blockIdx.x + ahead;
+      if (nxt < gridDim.x * gridDim.y) {
+        const double2* src = fsyn + (size_t)nxt * Lp * 8;  // [b][j] blocks are consecutive
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src),
+                     "r"((unsigned)(Lp * 8 * sizeof(double2)))
+                     : "memory");
+      }
+    }
+  }
   unsigned long long fx = 0;  // spectral split over peer memory: Fourier exchange number
   if constexpr (SPLIT) {
     if (rp.flags != nullptr) {
