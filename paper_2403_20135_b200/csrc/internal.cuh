@@ -78,6 +78,7 @@ struct Plan {
   int n_anal_work4;
   int synth_wj, anal_wj;  // row tiles per CTA (the other warps split K)
   int syn_cp;             // synthesis with the cp.async pipeline: 1 / 0 / -1 = automatic
+  int ana_nb;             // cap on states per table-streaming analysis CTA (0: all, up to 6)
   int ana_bulk;           // table-streaming analysis with the B operand staged: 1 (default) / 0
   int syn_bulk;           // CTA-staged bulk-copy synthesis (T >= 400): 1 / 0 / -1 = automatic
   FftPlan fft;

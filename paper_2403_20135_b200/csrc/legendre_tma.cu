@@ -272,7 +272,8 @@ static cudaError_t launch_analysis_bulk(const Plan& p, const Work& w, double2* f
 bool launch_analysis_tma(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s,
                          cudaError_t* err) {
   if (!tma_active(p)) return false;
-  const int NB = nb <= 6 ? nb : 4;
+  int NB = nb <= 6 ? nb : 4;
+  if (p.ana_nb > 0 && NB > p.ana_nb) NB = p.ana_nb;  // states per CTA (columns per B tile)
   const int* work = p.own_work != nullptr ? p.own_work : p.anal_work;
   const int nwork = p.own_work != nullptr ? p.n_own_work : p.n_anal_work;
   if (p.ana_bulk != 0) {  // B operand staged with the tables (default)

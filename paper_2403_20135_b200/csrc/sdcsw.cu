@@ -212,6 +212,8 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   // cp.async-pipelined synthesis: -1 = automatic (see synthesis_impl)
   p.syn_cp = -1;
   if (const char* env = getenv("SDCSW_SYN_CP")) p.syn_cp = atoi(env);
+  p.ana_nb = 0;
+  if (const char* env = getenv("SDCSW_ANA_NB")) p.ana_nb = atoi(env);
   p.ana_bulk = 1;
   if (const char* env = getenv("SDCSW_ANA_BULK")) p.ana_bulk = atoi(env);
   p.syn_bulk = -1;
