@@ -108,6 +108,22 @@ int sdcsw_sweep_nodes(sdcsw_plan* plan, int n_nodes, int node_lo, int count,
                       long long fe_stride, const double* fi, long long fi_stride, int first,
                       double* u_out, double* fi_out, void* stream);
 
+/* sdcsw_sweep_nodes with the collocation-residual norm fused into the same
+ * kernel (M <= 6, one state, unsplit plan): for every node m of the block,
+ *   resid[q][f] = || u0 + sum_j w[m][j] (fe_j + fi_j) - u_prev[q] ||_2
+ * per field f (Phi', zeta, delta) over the stored complex coefficients, where
+ * u_prev holds the previous iterate's node values u_m (count states) - the
+ * residual of the iterate whose tendencies fe/fi are.  resid is DEVICE memory
+ * [count][3]; the reduction order is fixed (deterministic).  u_out / fi_out
+ * are exactly those of sdcsw_sweep_nodes.  The reference monitors no residual
+ * (its sweeps run a fixed count, integrators.py:347-381); this is the
+ * north-star's fused quadrature + update + residual kernel. */
+int sdcsw_sweep_nodes_residual(sdcsw_plan* plan, int n_nodes, int node_lo, int count,
+                               const double* node_coef, const double* u0, const double* fe,
+                               long long fe_stride, const double* fi, long long fi_stride, int first,
+                               const double* u_prev, double* u_out, double* fi_out, double* resid,
+                               void* stream);
+
 /* Closing last-node solve of a diagonal step (integrators.py:291-311):
  *   beta = u0 + sum_j (w[j] fe_j + w[j] fi_j) - wd fi_last ; u_out = solve.
  * final_coef is HOST memory [M + 4] = (w[0..M-1], wd, alpha, alpha*phibar,

@@ -23,6 +23,7 @@ EXPORTS = (
     "sdcsw_f_impl",
     "sdcsw_implicit_solve",
     "sdcsw_sweep_nodes",
+    "sdcsw_sweep_nodes_residual",
     "sdcsw_final_node",
     "sdcsw_stepper_create",
     "sdcsw_stepper_create_ensemble",
@@ -100,6 +101,8 @@ _SIGS = {
     "sdcsw_f_impl": [_p, _p, _p, _i, _p],
     "sdcsw_implicit_solve": [_p, _dp, _p, _p, _i, _p],
     "sdcsw_sweep_nodes": [_p, _i, _i, _i, _dp, _p, _p, _ll, _p, _ll, _i, _p, _p, _p],
+    "sdcsw_sweep_nodes_residual": [_p, _i, _i, _i, _dp, _p, _p, _ll, _p, _ll, _i, _p, _p, _p, _p,
+                                   _p],
     "sdcsw_final_node": [_p, _i, _dp, _p, _p, _ll, _p, _ll, _i, _p, _p],
     "sdcsw_stepper_create": [_p, _i, _i, _i, _dp, _i, ctypes.POINTER(_p)],
     "sdcsw_stepper_create_ensemble": [_p, _i, _i, _i, _i, _dp, _i, ctypes.POINTER(_p)],

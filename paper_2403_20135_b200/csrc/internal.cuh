@@ -78,6 +78,8 @@ struct Plan {
   int n_anal_work4;
   int synth_wj, anal_wj;  // row tiles per CTA (the other warps split K)
   int syn_cp;             // synthesis with the cp.async pipeline: 1 / 0 / -1 = automatic
+  double* resid_part;     // residual partials (lazily allocated, sdcsw_sweep_nodes_residual)
+  unsigned* resid_count;
   int ana_nb;             // cap on states per table-streaming analysis CTA (0: all, up to 6)
   int ana_bulk;           // table-streaming analysis with the B operand staged: 1 (default) / 0
   int syn_bulk;           // CTA-staged bulk-copy synthesis (T >= 400): 1 / 0 / -1 = automatic
@@ -377,6 +379,13 @@ cudaError_t launch_analysis_fused(const Plan& p, const Work& w, int nb, const Fu
                                   cudaStream_t s);
 cudaError_t launch_f_impl(const Plan& p, const double2* u, double2* fi, int nb, cudaStream_t s);
 // coefficient pointers below are HOST memory; values travel as kernel parameters
+// opt-in collocation-residual norms of the sweep kernel (nodes.cu resid_block)
+struct ResidArgs {
+  const double* u_prev;  // previous iterate's node values [count][3C] complex
+  double* part;          // per-block partials [count * 3][blocks]
+  unsigned* count;       // blocks finished (0 between calls)
+  double* out;           // [count][3] norms (device)
+};
 cudaError_t launch_solve(const Plan& p, const double* coef_host, const double2* beta, double2* u,
                          int nb, cudaStream_t s);
 cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, const double* coef_host,
@@ -384,7 +393,7 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                const double2* fi, long long fi_stride, int first, double2* u_out,
                                double2* fi_out, double* xsyn_out, cudaStream_t s, int members = 1,
                                long long fe_mstride = 0, long long fi_mstride = 0, int chunk = 0,
-                               const PeerWait* pw = nullptr);
+                               const PeerWait* pw = nullptr, const ResidArgs* ra = nullptr);
 cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, const double2* u0,
                               const double2* fe, long long fe_stride, const double2* fi,
                               long long fi_stride, int first, double2* u_out, int* diverged,

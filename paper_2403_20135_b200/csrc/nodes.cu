@@ -74,6 +74,43 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
 }
 
 // ---------------------------------------------------------------------------
+// Collocation-residual norms, fused into the sweep kernel (opt-in): per node
+// and field, ||u0 + sum_j w_mj (fe_j + fi_j) - u_prev_m||_2 over the stored
+// complex coefficients.  Deterministic: a fixed-order block tree, per-block
+// partials, and the last block to finish sums the partials in block order
+// (then re-arms the counter for the next call).
+// ---------------------------------------------------------------------------
+__device__ void resid_block(const ResidArgs& ra, const double (*ss)[3], int count) {
+  __shared__ double red[256];
+  __shared__ bool last;
+  const int nv = count * 3;
+  for (int v = 0; v < nv; ++v) {
+    red[threadIdx.x] = ss != nullptr ? ss[v / 3][v % 3] : 0.0;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+      if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) ra.part[(size_t)v * gridDim.x + blockIdx.x] = red[0];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ra.count, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < nv) {
+    double acc = 0.0;
+    const volatile double* pv = ra.part + (size_t)threadIdx.x * gridDim.x;
+    for (unsigned b = 0; b < gridDim.x; ++b) acc += pv[b];
+    ra.out[threadIdx.x] = sqrt(acc);
+  }
+  if (threadIdx.x == 0) *ra.count = 0u;
+}
+
+// ---------------------------------------------------------------------------
 // The same node updates with one thread per coefficient (both components,
 // 16-byte accesses) for all nodes of the block [lo, lo + count): u0 and every
 // fe_j, fi_j are read once (instead of once per node) and the synthesis
@@ -81,6 +118,7 @@ __global__ void __launch_bounds__(256) k_sweep_nodes(
 // T.  Same rounded arithmetic as k_sweep_nodes (bit-identical).
 // M <= kFuseMaxNodes.
 // ---------------------------------------------------------------------------
+template <bool RES>  // RES: fused collocation-residual norms (resid_block)
 __global__ void __launch_bounds__(256) k_sweep_nodes_all(
     int C, int M, int lo, int count, NodeArgs cf, const double* __restrict__ u0,
     const double* __restrict__ fe, long long fe_stride, const double* __restrict__ fi,
@@ -88,22 +126,29 @@ __global__ void __launch_bounds__(256) k_sweep_nodes_all(
     double* __restrict__ u_out, double* fi_out, const double2* __restrict__ xscale,
     const int* __restrict__ idx_row, double* __restrict__ xsyn, long long fe_mstride,
     long long fi_mstride, int rows, int chunk, const int* __restrict__ idx_list, int n_list,
-    PeerWait pw) {
+    PeerWait pw, ResidArgs ra) {
   SDCSW_PDL_ENTRY();
   constexpr int MX = kFuseMaxNodes;
   const long long par = peer_wait(pw);  // node-parallel: the latest exchange's parity
   fe += par;
   fi += par;
   int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx_list != nullptr) {  // spectral split: own coefficients only
+  if (idx_list != nullptr) {  // spectral split: own coefficients only (no residual)
     if (idx >= n_list) return;
     idx = idx_list[idx];
   }
-  if (idx >= C) return;
+  if (idx >= C) {
+    if constexpr (RES) {
+      SDCSW_PDL_WAIT();
+      resid_block(ra, nullptr, count);  // the block reduction needs every thread
+    }
+    return;
+  }
   const double lam = lamv[idx];
   const double2 sc = xscale != nullptr ? xscale[idx] : make_double2(0.0, 0.0);
   const int row = xsyn != nullptr ? idx_row[idx] : 0;
   SDCSW_PDL_WAIT();
+  double ss[RES ? MX : 1][3];  // residual: squared norms per (node, field) of this coefficient
   const int z = blockIdx.z;
   const int C2 = 2 * C;
   u0 += (size_t)z * 3 * C2;
@@ -140,6 +185,16 @@ __global__ void __launch_bounds__(256) k_sweep_nodes_all(
           fmi = Ii[j];
         }
       }
+    if constexpr (RES) {  // collocation residual of the previous iterate at node m:
+      // u0 + sum_j w_mj F_j (the quadrature just formed) - u_prev_m
+      Tri pr, pi;
+      load_tri2(ra.u_prev + (size_t)q * 3 * C2, C, idx, pr, pi);
+      const double d[3][2] = {{br.phi - pr.phi, bi.phi - pi.phi},
+                              {br.zeta - pr.zeta, bi.zeta - pi.zeta},
+                              {br.delta - pr.delta, bi.delta - pi.delta}};
+#pragma unroll
+      for (int f = 0; f < 3; ++f) ss[q][f] = d[f][0] * d[f][0] + d[f][1] * d[f][1];
+    }
     br = axmy_tri(br, c[M], fmr);
     bi = axmy_tri(bi, c[M], fmi);
     const Tri ur = solve_tri(br, c[M + 1], c[M + 2], c[M + 3], lam);
@@ -153,6 +208,7 @@ __global__ void __launch_bounds__(256) k_sweep_nodes_all(
                       16 * (size_t)w, ur, ui, sc);
     }
   }
+  if constexpr (RES) resid_block(ra, ss, count);
 }
 
 // closing last-node solve, one thread per coefficient (both components)
@@ -403,15 +459,24 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                const double2* fi, long long fi_stride, int first, double2* u_out,
                                double2* fi_out, double* xsyn_out, cudaStream_t s, int members,
                                long long fe_mstride, long long fi_mstride, int chunk,
-                               const PeerWait* pw) {
+                               const PeerWait* pw, const ResidArgs* ra) {
   const long long S2 = 6LL * p.C;  // doubles per state
   const PeerWait pwv = pw != nullptr ? *pw : PeerWait{nullptr, 0, 0};
+  const ResidArgs rav = ra != nullptr ? *ra : ResidArgs{nullptr, nullptr, nullptr, nullptr};
+  if (ra != nullptr && (M > kFuseMaxNodes || members != 1 || p.own_idx != nullptr || count > 6))
+    return cudaErrorInvalidValue;
   if (M <= kFuseMaxNodes) {  // one thread per coefficient for all nodes of the block
     dim3 grid(((p.own_idx ? p.n_own_idx : p.C) + 255) / 256, 1, members);
-    launch_k(k_sweep_nodes_all, grid, 256, 0, s, p.C, M, node_lo, count,
+    if (ra != nullptr)
+      launch_k(k_sweep_nodes_all<true>, grid, 256, 0, s, p.C, M, node_lo, count,
              pack(coef_host, M * (M + 4)), D(u0), D(fe), fe_stride * S2, D(fi), fi_stride * S2,
              first, p.phibar, p.lam, W(u_out), W(fi_out), p.xscale, p.idx_row, xsyn_out,
-             fe_mstride * S2, fi_mstride * S2, p.rows, chunk, p.own_idx, p.n_own_idx, pwv);
+             fe_mstride * S2, fi_mstride * S2, p.rows, chunk, p.own_idx, p.n_own_idx, pwv, rav);
+    else
+      launch_k(k_sweep_nodes_all<false>, grid, 256, 0, s, p.C, M, node_lo, count,
+             pack(coef_host, M * (M + 4)), D(u0), D(fe), fe_stride * S2, D(fi), fi_stride * S2,
+             first, p.phibar, p.lam, W(u_out), W(fi_out), p.xscale, p.idx_row, xsyn_out,
+             fe_mstride * S2, fi_mstride * S2, p.rows, chunk, p.own_idx, p.n_own_idx, pwv, rav);
     return cudaGetLastError();
   }
   dim3 grid = grid_for(p.own_idx ? p.n_own_idx : p.C, count);

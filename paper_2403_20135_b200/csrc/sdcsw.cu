@@ -329,7 +329,7 @@ int sdcsw_plan_destroy(sdcsw_plan* h) {
   void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
                   p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev,
                   p.xscale, p.idx_row, p.xsyn, p.anal_work4, p.pkx, p.pky, p.ptw, p.pw1, p.pw2,
-                  p.ptab_a, p.htab_a, p.ptab_s, p.htab_s};
+                  p.ptab_a, p.htab_a, p.ptab_s, p.htab_s, p.resid_part, p.resid_count};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   h->alive = false;
@@ -468,6 +468,41 @@ int sdcsw_sweep_nodes(sdcsw_plan* h, int n_nodes, int node_lo, int count, const 
                                         (const double2*)fi, fi_stride, first, (double2*)u_out,
                                         (double2*)fi_out, nullptr, (cudaStream_t)stream),
                      "sdcsw_sweep_nodes");
+}
+
+int sdcsw_sweep_nodes_residual(sdcsw_plan* h, int n_nodes, int node_lo, int count,
+                               const double* node_coef, const double* u0, const double* fe,
+                               long long fe_stride, const double* fi, long long fi_stride, int first,
+                               const double* u_prev, double* u_out, double* fi_out, double* resid,
+                               void* stream) {
+  int st = check_plan(h, 1, "sdcsw_sweep_nodes_residual");
+  if (st) return st;
+  if (n_nodes < 1 || n_nodes > kFuseMaxNodes || node_lo < 0 || count < 1 ||
+      node_lo + count > n_nodes || !node_coef || !u_prev || !resid) {
+    set_error("sdcsw_sweep_nodes_residual: bad node range (M <= 6) or null argument");
+    return SDCSW_ERR_PARAM;
+  }
+  Plan& p = h->p;
+  if (p.own_idx != nullptr) {
+    set_error("sdcsw_sweep_nodes_residual: not available on a spectrally split plan");
+    return SDCSW_ERR_STATE;
+  }
+  if (p.resid_part == nullptr) {  // [6 nodes x 3 fields][blocks] partials + block counter
+    const size_t blocks = (p.C + 255) / 256;
+    if (cudaMalloc(&p.resid_part, 18 * blocks * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&p.resid_count, sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(p.resid_count, 0, sizeof(unsigned)) != cudaSuccess) {
+      set_error("sdcsw_sweep_nodes_residual: workspace allocation failed");
+      return SDCSW_ERR_CUDA;
+    }
+  }
+  const ResidArgs ra{u_prev, p.resid_part, p.resid_count, resid};
+  return cuda_status(launch_sweep_nodes(p, n_nodes, node_lo, count, node_coef,
+                                        (const double2*)u0, (const double2*)fe, fe_stride,
+                                        (const double2*)fi, fi_stride, first, (double2*)u_out,
+                                        (double2*)fi_out, nullptr, (cudaStream_t)stream, 1, 0, 0,
+                                        0, nullptr, &ra),
+                     "sdcsw_sweep_nodes_residual");
 }
 
 int sdcsw_final_node(sdcsw_plan* h, int n_nodes, const double* final_coef, const double* u0,

@@ -125,6 +125,21 @@ class CudaNodeBackend:
             "sdcsw_sweep_nodes",
         )
 
+    def sweep_nodes_residual(self, n_nodes, lo, count, coef, u0, fe, fe_stride, fi, fi_stride,
+                             first, u_prev, u_out, fi_out, resid):
+        """sweep_nodes plus the fused per-(node, field) collocation-residual norms of the
+        previous iterate (u_prev: its node values) into the device tensor resid [count, 3]."""
+        from . import _native
+
+        _native.check(
+            self.lib.sdcsw_sweep_nodes_residual(
+                self.problem.handle, n_nodes, lo, count, _native.dptr(coef), u0.data_ptr(),
+                fe.data_ptr(), fe_stride, fi.data_ptr(), fi_stride, int(first), u_prev.data_ptr(),
+                u_out.data_ptr(), fi_out.data_ptr(), resid.data_ptr(), self.problem.stream(),
+            ),
+            "sdcsw_sweep_nodes_residual",
+        )
+
     def final_node(self, n_nodes, coef, u0, fe, fe_stride, fi, fi_stride, first, u_out):
         from . import _native
 

@@ -105,6 +105,53 @@ def test_sweep_nodes_and_final_node_bit_exact():
         assert np.array_equal(u_out[q].cpu().numpy(), o.implicit_solve(dt * diag[m], slots.fi[m]))
 
 
+def test_sweep_nodes_residual_fused():
+    """sdcsw_sweep_nodes_residual: the node updates of sdcsw_sweep_nodes (bitwise) plus the
+    fused collocation-residual norms ||u0 + sum_j w_mj (fe_j + fi_j) - u_prev_m||_2 per
+    (node, field), vs numpy; deterministic across calls; node sub-blocks; first sweep."""
+    import torch
+
+    from paper_2403_20135_b200.integrators import diagonal_step_coefficients
+    from paper_2403_20135_b200.parallel_nodes import CudaNodeBackend
+
+    p = gpu(127)
+    rng = np.random.default_rng(5)
+    m_count, dt = 4, 90.0
+    S, C = p.state_size, p.n_coef
+    cfg = SdcConfig(table=CollocationTable.radau_right(m_count), n_sweeps=3,
+                    mode=SweepMode.DIAGONAL_SEQUENTIAL)
+    coef = diagonal_step_coefficients(cfg, dt, p.mean_geopotential)
+    blk = m_count * (m_count + 4)
+    c1 = np.ascontiguousarray(coef[blk : 2 * blk])
+    w = c1.reshape(m_count, m_count + 4)
+    cplx = lambda *sh: rng.standard_normal(sh) + 1j * rng.standard_normal(sh)  # noqa: E731
+    u0, fe, fi = cplx(S), cplx(m_count, S), cplx(m_count, S)
+    u_prev = cplx(m_count, S)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(p.device)  # noqa: E731
+    be = CudaNodeBackend(p)
+    for lo, cnt, first in ((0, m_count, False), (1, 2, False), (0, m_count, True)):
+        ua, fa = p.empty_states(cnt), p.empty_states(cnt)
+        be.sweep_nodes(m_count, lo, cnt, c1, dev(u0), dev(fe), 1, dev(fi), 1, first, ua, fa)
+        res = []
+        for _ in range(2):
+            ub, fb = p.empty_states(cnt), p.empty_states(cnt)
+            r = torch.zeros((cnt, 3), dtype=torch.float64, device=p.device)
+            be.sweep_nodes_residual(m_count, lo, cnt, c1, dev(u0), dev(fe), 1, dev(fi), 1, first,
+                                    dev(u_prev[lo : lo + cnt]), ub, fb, r)
+            assert torch.equal(ua, ub) and torch.equal(fa, fb)
+            res.append(r.cpu().numpy())
+        assert np.array_equal(res[0], res[1])  # fixed reduction order
+        fi_used = np.stack([p.f_impl(u0)] * m_count) if first else fi
+        for q in range(cnt):
+            m = lo + q
+            qf = u0.copy()
+            for j in range(m_count):
+                qf = qf + w[m, j] * (fe[j] + fi_used[j])
+            d = qf - u_prev[m]
+            ref = [np.linalg.norm(d[f * C : (f + 1) * C]) for f in range(3)]
+            np.testing.assert_allclose(res[0][q], ref, rtol=1e-12)
+
+
 def test_transforms_deterministic_and_batch_invariant():
     import torch
 
