@@ -348,8 +348,15 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
     const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter,
     const int* __restrict__ mlist, int Lp, const SynDst sd) {
   SDCSW_PDL_ENTRY();
-  constexpr int NPAIR = (NB + 1) / 2;
-  constexpr int NT = 2 * NPAIR;
+  // column tiles: NB / 2 state pairs x (part 0, part 1) for P plus one H tile per
+  // pair; an odd last state gets one P tile holding both its parts (columns 0-3
+  // part 0, 4-7 part 1) and one H tile (columns 0-3, the rest zero) accumulating
+  // into it, instead of a pair tile with an empty partner (NB = 5: 16 DMMAs per row
+  // quad instead of 18; per-column sums unchanged)
+  constexpr int NFULL = NB / 2;
+  constexpr bool ODD = (NB & 1) != 0;
+  constexpr int NT = 2 * NFULL + (ODD ? 1 : 0);  // P tiles
+  constexpr int NH = NFULL + (ODD ? 1 : 0);      // H tiles
   constexpr int QX = 48 * NB;  // operand doubles per row quad (3 parts x NB states x 16)
   extern __shared__ __align__(128) unsigned char synb_raw[];
   const int WJ = blockDim.x >> 5;
@@ -420,24 +427,35 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
         const double* pq = st + q * TQ + warp * 64 + lane;
         const double* hq = pq + kSynKQ * TQ;
         const double aP0 = pq[0], aP1 = pq[32], aH0 = hq[0], aH1 = hq[32];
-        const double* xq = st + 2 * kSynKQ * TQ + q * QX + gb * 16 + t * 4 + gc;
-        double bP[NT], bH[NPAIR];
+        const double* xq0 = st + 2 * kSynKQ * TQ + q * QX + t * 4 + gc;
+        const double* xq = xq0 + gb * 16;
+        double bP[NT], bH[NH];
 #pragma unroll
-        for (int p = 0; p < NPAIR; ++p) {
+        for (int p = 0; p < NFULL; ++p) {
           bP[2 * p] = xq[p * 32];
           bP[2 * p + 1] = xq[16 * NB + p * 32];
           bH[p] = xq[32 * NB + p * 32];
+        }
+        if constexpr (ODD) {  // last state: lane column group gb = part
+          bP[NT - 1] = xq0[gb * 16 * NB + (NB - 1) * 16];
+          bH[NH - 1] = gb == 0 ? xq0[32 * NB + (NB - 1) * 16] : 0.0;
         }
         if (i * kSynKQ + q < se) {  // n - m even: P symmetric (E), H antisymmetric (O)
 #pragma unroll
           for (int c = 0; c < NT; ++c) { dmma_t(aE[0][c], aP0, bP[c]); dmma_t(aE[1][c], aP1, bP[c]); }
 #pragma unroll
-          for (int p = 0; p < NPAIR; ++p) { dmma_t(aO[0][2 * p], aH0, bH[p]); dmma_t(aO[1][2 * p], aH1, bH[p]); }
+          for (int p = 0; p < NH; ++p) {
+            const int c = p < NFULL ? 2 * p : NT - 1;
+            dmma_t(aO[0][c], aH0, bH[p]); dmma_t(aO[1][c], aH1, bH[p]);
+          }
         } else {
 #pragma unroll
           for (int c = 0; c < NT; ++c) { dmma_t(aO[0][c], aP0, bP[c]); dmma_t(aO[1][c], aP1, bP[c]); }
 #pragma unroll
-          for (int p = 0; p < NPAIR; ++p) { dmma_t(aE[0][2 * p], aH0, bH[p]); dmma_t(aE[1][2 * p], aH1, bH[p]); }
+          for (int p = 0; p < NH; ++p) {
+            const int c = p < NFULL ? 2 * p : NT - 1;
+            dmma_t(aE[0][c], aH0, bH[p]); dmma_t(aE[1][c], aH1, bH[p]);
+          }
         }
       }
     }
@@ -450,9 +468,9 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
 
 #pragma unroll
   for (int c = 0; c < NT; ++c) {
-    const int be = 2 * (c >> 1) + (t >> 1);
-    const int f = (t & 1) + 2 * (c & 1);
-    if (be >= NB) continue;
+    const bool last = ODD && c == NT - 1;  // the odd state's tile: column pair t = field t
+    const int be = last ? NB - 1 : 2 * (c >> 1) + (t >> 1);
+    const int f = last ? t : (t & 1) + 2 * (c & 1);
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
       const int j = j0 + 8 * a + g;
