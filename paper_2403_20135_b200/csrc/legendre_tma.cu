@@ -610,16 +610,28 @@ __global__ void __launch_bounds__(128, SDCSW_ANAB_MINB) k_analysis_bulk(
   if (threadIdx.x == 0)
     for (int ch = 0; ch < kAnbS && ch < nchunks; ++ch) issue_data(ch);
 
-  // lane offsets in a k-step's 112-double record: [S: P 4x8 | H 4x6][A: same]
+  // lane offsets in a k-step's 112-double record: [S: P 4x8 | H 4x6][A: same].
+  // P: one 8-column tile per state.  H: the 6 H columns of all states packed
+  // into NHT = ceil(6 NB / 8) tiles (global H column 8 h + g = state s, column
+  // k; NB = 5: 9 instead of 10 DMMA pairs per k-step); H sums are kept apart
+  // and added to the P sums in the epilogue.
+  constexpr int NHT = (6 * NB + 7) / 8;
   const int po = t * 8 + g;
-  const int ho = 32 + t * 6 + (g < 6 ? g : 0);
-  const bool hcol = g < 6;
-  const bool any_ev = ev0 || ev1, any_od = !ev0 || !ev1;
-  double acc[2][NB][2];
+  int hoff[NHT];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int h = 0; h < NHT; ++h) {
+    const int col = 8 * h + g, hs_ = col / 6;
+    hoff[h] = hs_ < NB ? hs_ * kAnbChunk + 32 + t * 6 + (col - 6 * hs_) : -1;
+  }
+  const bool any_ev = ev0 || ev1, any_od = !ev0 || !ev1;
+  double acc[2][NB][2], acch[2][NHT][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
 #pragma unroll
     for (int c = 0; c < NB; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+#pragma unroll
+    for (int h = 0; h < NHT; ++h) acch[a][h][0] = acch[a][h][1] = 0.0;
+  }
   const int row0 = warp * kRowsPerWarp + g;
 
   for (int ch = 0; ch < nchunks; ++ch) {
@@ -634,14 +646,18 @@ __global__ void __launch_bounds__(128, SDCSW_ANAB_MINB) k_analysis_bulk(
         const int k = 4 * q + t;
         const double aP0 = swz(pt, row0, k), aP1 = swz(pt, row0 + 8, k);
         const double aH0 = swz(ht, row0, k), aH1 = swz(ht, row0 + 8, k);
-        double ps[NB], pa[NB], hs[NB], ha[NB];
+        double ps[NB], pa[NB], hs[NHT], ha[NHT];
 #pragma unroll
         for (int c = 0; c < NB; ++c) {
           const double* r = bt + c * kAnbChunk + q * 112;
           ps[c] = any_ev ? r[po] : 0.0;
           pa[c] = any_od ? r[56 + po] : 0.0;
-          hs[c] = any_od && hcol ? r[ho] : 0.0;
-          ha[c] = any_ev && hcol ? r[56 + ho] : 0.0;
+        }
+#pragma unroll
+        for (int h = 0; h < NHT; ++h) {
+          const double* r = bt + q * 112 + (hoff[h] < 0 ? 0 : hoff[h]);
+          hs[h] = any_od && hoff[h] >= 0 ? r[0] : 0.0;
+          ha[h] = any_ev && hoff[h] >= 0 ? r[56] : 0.0;
         }
 #pragma unroll
         for (int c = 0; c < NB; ++c) {
@@ -649,9 +665,9 @@ __global__ void __launch_bounds__(128, SDCSW_ANAB_MINB) k_analysis_bulk(
           dmma_t(acc[1][c], aP1, ev1 ? ps[c] : pa[c]);
         }
 #pragma unroll
-        for (int c = 0; c < NB; ++c) {
-          dmma_t(acc[0][c], aH0, ev0 ? ha[c] : hs[c]);
-          dmma_t(acc[1][c], aH1, ev1 ? ha[c] : hs[c]);
+        for (int h = 0; h < NHT; ++h) {
+          dmma_t(acch[0][h], aH0, ev0 ? ha[h] : hs[h]);
+          dmma_t(acch[1][h], aH1, ev1 ? ha[h] : hs[h]);
         }
       }
     }
@@ -669,6 +685,18 @@ __global__ void __launch_bounds__(128, SDCSW_ANAB_MINB) k_analysis_bulk(
     for (int c = 0; c < NB; ++c) {
       o[(8 * a + g) * OS + 8 * c + 2 * t] = acc[a][c][0];
       o[(8 * a + g) * OS + 8 * c + 2 * t + 1] = acc[a][c][1];
+    }
+  __syncwarp();
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int h = 0; h < NHT; ++h) {  // columns (2t, 2t + 1) of H tile h: one state, one slot
+      const int col = 8 * h + 2 * t, hs_ = col / 6;
+      if (hs_ < NB) {
+        double* d = o + (8 * a + g) * OS + 8 * hs_ + (col - 6 * hs_);
+        d[0] += acch[a][h][0];
+        d[1] += acch[a][h][1];
+      }
     }
   __syncwarp();
   const int mo = moff[m];
