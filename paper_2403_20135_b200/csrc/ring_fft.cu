@@ -267,8 +267,14 @@ static void build_pass_twiddles(const double2* w, std::vector<double2>& out) {
 #ifndef SDCSW_RING_MINB128
 #define SDCSW_RING_MINB128 5  // 96 registers: 5 CTAs per SM (throughput variant)
 #endif
-template <int THREADS>
-constexpr int ring_min_blocks() { return THREADS <= 128 ? SDCSW_RING_MINB128 : (THREADS <= 256 ? 3 : 1); }
+#ifndef SDCSW_RING_MINB768
+#define SDCSW_RING_MINB768 2  // shared memory allows 2 CTAs per SM anyway: up to 128 registers (T255 -2%)
+#endif
+template <int N, int THREADS>
+constexpr int ring_min_blocks() {
+  return N == 768 ? SDCSW_RING_MINB768
+                  : (THREADS <= 128 ? SDCSW_RING_MINB128 : (THREADS <= 256 ? 3 : 1));
+}
 
 #ifndef SDCSW_RING_L2PF
 #define SDCSW_RING_L2PF 1536  // nlon from which the ring kernel prefetches one wave ahead
@@ -276,13 +282,13 @@ constexpr int ring_min_blocks() { return THREADS <= 128 ? SDCSW_RING_MINB128 : (
 // resident CTAs per SM of a ring kernel (shared memory bound; registers allow more)
 template <int N, int THREADS>
 constexpr int ring_resident() {
-  return (int)(232448 / (ring_smem_t<N, THREADS>() + 1024)) < ring_min_blocks<THREADS>()
+  return (int)(232448 / (ring_smem_t<N, THREADS>() + 1024)) < ring_min_blocks<N, THREADS>()
              ? (int)(232448 / (ring_smem_t<N, THREADS>() + 1024))
-             : ring_min_blocks<THREADS>();
+             : ring_min_blocks<N, THREADS>();
 }
 
 template <int N, int THREADS, bool SPLIT>
-__global__ void __launch_bounds__(THREADS, ring_min_blocks<THREADS>()) k_ring(const double2* __restrict__ fsyn,
+__global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring(const double2* __restrict__ fsyn,
                                                   double2* __restrict__ gan, int J, int T,
                                                   const double* __restrict__ mu,
                                                   const double* __restrict__ wsyn,
