@@ -343,7 +343,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 
 template <int NB>
 __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_MINB) k_synthesis_bulk(
-    const double* __restrict__ xsyn, int J, const double* __restrict__ ptab,
+    const double* __restrict__ xsyn, int nb, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
     const int* __restrict__ n_even, double2* __restrict__ fsyn, int* step_counter,
     const int* __restrict__ mlist, int Lp, const SynDst sd) {
@@ -378,13 +378,17 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
   const size_t qstride = (size_t)(J / 8) * 32;
   const double* Pc = ptab + (size_t)(r0m / 4) * qstride + (size_t)blockIdx.x * TQ;
   const double* Hc = htab + (size_t)(r0m / 4) * qstride + (size_t)blockIdx.x * TQ;
-  const double* Xc = xsyn + (size_t)(r0m / 4) * QX;
+  // batch block blockIdx.z: states [b0, b0 + nbv) of nb; operand records are
+  // [row/4][part][nb][16], one contiguous run per quad when the block is the batch
+  const int b0 = blockIdx.z * NB, nbv = nb - b0 < NB ? nb - b0 : NB;
+  const size_t qxg = (size_t)48 * nb;  // operand doubles per row quad (all states)
+  const double* Xc = xsyn + (size_t)(r0m / 4) * qxg + (size_t)b0 * 16;
 
   auto nq_of = [&](int i) { return min(kSynKQ, nsteps - i * kSynKQ); };
   auto issue_tables = [&](int i) {  // thread 0
     double* st = stages + (i % kSynBS) * SD;
     const int nq = nq_of(i);
-    mbar_expect_tx(&full[i % kSynBS], (unsigned)(nq * (2 * TQ + QX) * 8));
+    mbar_expect_tx(&full[i % kSynBS], (unsigned)(nq * (2 * TQ + 48 * nbv) * 8));
     for (int q = 0; q < nq; ++q) {
       const size_t src = (size_t)(i * kSynKQ + q) * qstride;
       bulk_g2s(st + q * TQ, Pc + src, TQ * 8, &full[i % kSynBS]);
@@ -392,9 +396,15 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
     }
   };
   auto issue_operand = [&](int i) {  // thread 0, after the producer grid completed
-    double* st = stages + (i % kSynBS) * SD;
-    bulk_g2s(st + 2 * kSynKQ * TQ, Xc + (size_t)i * kSynKQ * QX, (unsigned)(nq_of(i) * QX * 8),
-             &full[i % kSynBS]);
+    double* st = stages + (i % kSynBS) * SD + 2 * kSynKQ * TQ;
+    if (nb == NB) {
+      bulk_g2s(st, Xc + (size_t)i * kSynKQ * QX, (unsigned)(nq_of(i) * QX * 8), &full[i % kSynBS]);
+    } else {  // one run of nbv states per (quad, part), placed at the block's [part][NB] stride
+      for (int q = 0; q < nq_of(i); ++q)
+        for (int pp = 0; pp < 3; ++pp)
+          bulk_g2s(st + q * QX + pp * 16 * NB, Xc + (size_t)(i * kSynKQ + q) * qxg + pp * 16 * nb,
+                   (unsigned)(nbv * 16 * 8), &full[i % kSynBS]);
+    }
   };
 
   if (threadIdx.x == 0) {
@@ -407,7 +417,7 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
     for (int i = 0; i < kSynBS && i < nstage; ++i) issue_tables(i);
   SDCSW_PDL_WAIT();
   if (threadIdx.x == 0) {
-    if (step_counter != nullptr && (blockIdx.x | blockIdx.y) == 0) atomicAdd(step_counter, 1);
+    if (step_counter != nullptr && (blockIdx.x | blockIdx.y | blockIdx.z) == 0) atomicAdd(step_counter, 1);
     for (int i = 0; i < kSynBS && i < nstage; ++i) issue_operand(i);
   }
 
@@ -474,7 +484,7 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
       const int j = j0 + 8 * a + g;
-      const size_t off = ((((size_t)be * J + j) * Lp + kpos) * 4 + f) * 2;
+      const size_t off = ((((size_t)(b0 + be) * J + j) * Lp + kpos) * 4 + f) * 2;
       const double2 vn = make_double2(aE[a][c][0] + aO[a][c][0], aE[a][c][1] + aO[a][c][1]);
       const double2 vs = make_double2(aE[a][c][0] - aO[a][c][0], aE[a][c][1] - aO[a][c][1]);
       if (sd.n == 0) {
@@ -505,22 +515,23 @@ cudaError_t configure_synthesis_bulk() {
 
 // one batch block of nb <= 6 states, every state in the operand record (nb = NB)
 bool synthesis_bulk_ok(const Plan& p, int nb) {
-  // automatic from T200 (T255 4 states 32.5 vs 38.6 us; one state 31.3 vs 29.9 us,
-  // kept on the same kernel so results stay bitwise independent of the batching)
-  const int on = p.syn_bulk >= 0 ? p.syn_bulk : (p.T >= 200 ? 1 : 0);
-  return on && nb >= 1 && nb <= 6 && p.J % 32 == 0;
+  // automatic from T200 (T255 4 states 32.5 vs 38.6 us; one state 24 vs 30 us), and for
+  // ensemble batches (4+ batch blocks of 6 states) at any truncation
+  const int on = p.syn_bulk >= 0 ? p.syn_bulk : (p.T >= 200 || nb >= 24 ? 1 : 0);
+  return on && nb >= 1 && p.J % 32 == 0;
 }
 
 cudaError_t launch_synthesis_bulk(const Plan& p, double2* fsyn, const int* mlist, int nm, int Lp,
                                   const double* xsyn, int nb, cudaStream_t s, int* step_counter,
                                   const SynDst& sd) {
   const int WJ = p.J % 64 == 0 ? 4 : 2;
-  const dim3 grid(p.J / (kRowsPerWarp * WJ), nm);
+  const int NB = nb <= 6 ? nb : 6;  // states per CTA (batch blocks along z)
+  const dim3 grid(p.J / (kRowsPerWarp * WJ), nm, (nb + NB - 1) / NB);
 #define SDCSW_SYNB_LAUNCH(NBV)                                                                \
-  if (nb == NBV)                                                                              \
+  if (NB == NBV)                                                                              \
     return launch_k(k_synthesis_bulk<NBV>, grid, dim3(32 * WJ), synb_smem(WJ, NBV), s, xsyn,  \
-                    p.J, p.ptab_s, p.htab_s, p.rowoff, p.n_even, fsyn, step_counter, mlist, Lp, \
-                    sd);
+                    nb, p.J, p.ptab_s, p.htab_s, p.rowoff, p.n_even, fsyn, step_counter, mlist, \
+                    Lp, sd);
   SDCSW_SYNB_LAUNCH(1) SDCSW_SYNB_LAUNCH(2) SDCSW_SYNB_LAUNCH(3) SDCSW_SYNB_LAUNCH(4)
   SDCSW_SYNB_LAUNCH(5) SDCSW_SYNB_LAUNCH(6)
 #undef SDCSW_SYNB_LAUNCH

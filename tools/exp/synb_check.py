@@ -15,12 +15,14 @@ from paper_2403_20135_b200 import random_initial_state  # noqa: E402
 from paper_2403_20135_b200.problem import SphericalShallowWater  # noqa: E402
 
 for T in [int(a) for a in sys.argv[1:]] or [127, 255, 511]:
-    nbs = (1, 4, 5) if T >= 400 else (1, 4)
+    nbs = tuple(int(x) for x in os.environ["NBS"].split()) if "NBS" in os.environ else (
+        (1, 4, 5) if T >= 400 else (1, 4))
     res = {}
     for bulk in (0, 1):
         os.environ[os.environ.get("KNOB", "SDCSW_SYN_BULK")] = str(bulk)
-        p = SphericalShallowWater(T, device=0, max_batch=6)
-        st = np.stack([random_initial_state(p.grid, s) for s in range(6)])
+        nmax = max(max(nbs), 6)
+        p = SphericalShallowWater(T, device=0, max_batch=nmax)
+        st = np.stack([random_initial_state(p.grid, s % 6) for s in range(nmax)])
         st[:, : p.n_coef] = 3e-3 * st[:, p.n_coef : 2 * p.n_coef] * 1e6
         u = torch.from_numpy(st).to(p.device)
         for nb in nbs:
