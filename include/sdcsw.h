@@ -117,7 +117,9 @@ int sdcsw_sweep_nodes(sdcsw_plan* plan, int n_nodes, int node_lo, int count,
  * [count][3]; the reduction order is fixed (deterministic).  u_out / fi_out
  * are exactly those of sdcsw_sweep_nodes.  The reference monitors no residual
  * (its sweeps run a fixed count, integrators.py:347-381); this is the
- * north-star's fused quadrature + update + residual kernel. */
+ * north-star's fused quadrature + update + residual kernel.  The reduction
+ * workspace is allocated with the plan and shared by its calls: residual sweeps
+ * on one plan must be serialised on one stream.  Graph-capturable. */
 int sdcsw_sweep_nodes_residual(sdcsw_plan* plan, int n_nodes, int node_lo, int count,
                                const double* node_coef, const double* u0, const double* fe,
                                long long fe_stride, const double* fi, long long fi_stride, int first,
@@ -279,6 +281,32 @@ int sdcsw_exchange_info(sdcsw_exchange* x, int* node_lo, int* node_count, int* l
 int sdcsw_exchange_diverged(sdcsw_exchange* x, int* step_index);
 int sdcsw_exchange_reset(sdcsw_exchange* x, void* stream);
 int sdcsw_exchange_destroy(sdcsw_exchange* x);
+
+/* NCCL transport (SURVEY 8b "sdcsw_comm_init_all" / "sdcsw_allgather_rhs";
+ * replaces the reference's per-sweep barrier over the node futures,
+ * integrators.py:278-288, when the nodes of a sweep live on different GPUs).
+ *   unique_id: rank 0 creates the NCCL unique id (SDCSW_COMM_ID_BYTES bytes);
+ *     the caller carries it to every rank (torch.distributed bootstrap only).
+ *   create: one communicator per process (ncclCommInitRank) on `device`.
+ *   split: sub-communicator of the ranks passing the same color, ordered by
+ *     key (ncclCommSplit) - node groups (same spectral part) and spectral
+ *     groups (same node group) of the node x spectral partition.
+ *   allgather_rhs: recv[world][count] <- every rank's send[count] doubles
+ *     (ncclAllGather; in rank order), stream-ordered and graph-capturable.
+ *     The node-parallel step gathers the (f_E, f_I) pairs of every rank's
+ *     node block once per sweep, and the Fourier parts once per f_E of a
+ *     spectral split.
+ *   nccl_version: the loaded library's NCCL_VERSION_CODE. */
+#define SDCSW_COMM_ID_BYTES 128
+typedef struct sdcsw_comm sdcsw_comm;
+int sdcsw_comm_unique_id(void* id, int bytes);
+int sdcsw_comm_create(const void* id, int bytes, int world, int rank, int device, sdcsw_comm** out);
+int sdcsw_comm_split(sdcsw_comm* parent, int color, int key, sdcsw_comm** out);
+int sdcsw_comm_info(sdcsw_comm* comm, int* world, int* rank);
+int sdcsw_allgather_rhs(sdcsw_comm* comm, const double* send, double* recv, long long count,
+                        void* stream);
+int sdcsw_comm_destroy(sdcsw_comm* comm);
+int sdcsw_nccl_version(void);
 
 /* out = x + w * y over n doubles, rounded as numpy's `x + w * y` (product, then
  * sum); out may alias x.  The vector update of the reference schemes

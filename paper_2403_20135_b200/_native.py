@@ -14,6 +14,7 @@ LIB_PATH = os.environ.get("SDCSW_LIB_PATH") or os.path.join(
 
 SDCSW_OK, SDCSW_ERR_PARAM, SDCSW_ERR_CUDA, SDCSW_ERR_STATE, SDCSW_ERR_DIVERGED = range(5)
 IPC_HANDLE_BYTES = 64  # SDCSW_IPC_HANDLE_BYTES
+COMM_ID_BYTES = 128  # SDCSW_COMM_ID_BYTES
 
 EXPORTS = (
     "sdcsw_plan_create",
@@ -56,6 +57,13 @@ EXPORTS = (
     "sdcsw_exchange_diverged",
     "sdcsw_exchange_reset",
     "sdcsw_exchange_destroy",
+    "sdcsw_comm_unique_id",
+    "sdcsw_comm_create",
+    "sdcsw_comm_split",
+    "sdcsw_comm_info",
+    "sdcsw_allgather_rhs",
+    "sdcsw_comm_destroy",
+    "sdcsw_nccl_version",
     "sdcsw_last_error",
     "sdcsw_version",
 )
@@ -135,6 +143,13 @@ _SIGS = {
     "sdcsw_exchange_diverged": [_p, _ip],
     "sdcsw_exchange_reset": [_p, _p],
     "sdcsw_exchange_destroy": [_p],
+    "sdcsw_comm_unique_id": [_p, _i],
+    "sdcsw_comm_create": [_p, _i, _i, _i, _i, ctypes.POINTER(_p)],
+    "sdcsw_comm_split": [_p, _i, _i, ctypes.POINTER(_p)],
+    "sdcsw_comm_info": [_p, _ip, _ip],
+    "sdcsw_allgather_rhs": [_p, _p, _p, _ll, _p],
+    "sdcsw_comm_destroy": [_p],
+    "sdcsw_nccl_version": [],
     "sdcsw_last_error": [],
     "sdcsw_version": [],
 }

@@ -197,14 +197,22 @@ __device__ __forceinline__ void write_xsyn_half(double* __restrict__ rec, size_t
   double* p1 = rec + pstride;
   double* p2 = rec + 2 * pstride;
   if (ri == 0) {
+#if SDCSW_MUTATE_UCHI  // test-only mutation (node_math.cuh write_xsyn_full)
+    rec[1] = sm * delta;
+#else
     rec[1] = -sm * delta;  // U_P im
+#endif
     rec[3] = -sm * zeta;   // V_P im
     p1[0] = zeta;
     p1[2] = phi;
     p2[0] = sa * zeta;     // U_H re
     p2[2] = -sa * delta;   // V_H re
   } else {
+#if SDCSW_MUTATE_UCHI
+    rec[0] = -sm * delta;
+#else
     rec[0] = sm * delta;   // U_P re
+#endif
     rec[2] = sm * zeta;    // V_P re
     p1[1] = zeta;
     p1[3] = phi;

@@ -481,6 +481,9 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
     const bool last = ODD && c == NT - 1;  // the odd state's tile: column pair t = field t
     const int be = last ? NB - 1 : 2 * (c >> 1) + (t >> 1);
     const int f = last ? t : (t & 1) + 2 * (c & 1);
+    // the last batch block may hold nbv < NB states: columns of the missing states
+    // were formed from stale stage memory and must not be stored
+    if (be >= nbv) continue;
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
       const int j = j0 + 8 * a + g;
@@ -513,7 +516,8 @@ cudaError_t configure_synthesis_bulk() {
   return e;
 }
 
-// one batch block of nb <= 6 states, every state in the operand record (nb = NB)
+// any nb: batch blocks of up to 6 states along grid z (the last block may be partial;
+// its missing columns are not stored)
 bool synthesis_bulk_ok(const Plan& p, int nb) {
   // automatic from T200 (T255 4 states 32.5 vs 38.6 us; one state 24 vs 30 us), and for
   // ensemble batches (4+ batch blocks of 6 states) at any truncation

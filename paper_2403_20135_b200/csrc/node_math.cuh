@@ -92,7 +92,11 @@ __device__ __forceinline__ void write_xsyn_full(double* __restrict__ rec, size_t
   double2* p0 = reinterpret_cast<double2*>(rec);
   double2* p1 = reinterpret_cast<double2*>(rec + pstride);
   double2* p2 = reinterpret_cast<double2*>(rec + 2 * pstride);
+#if SDCSW_MUTATE_UCHI  // test-only mutation: wrong sign of the i m chi term of U (KAT proof)
+  p0[0] = make_double2(-sm * im.delta, sm * re.delta);
+#else
   p0[0] = make_double2(sm * im.delta, -sm * re.delta);  // U_P re, im
+#endif
   p0[1] = make_double2(sm * im.zeta, -sm * re.zeta);    // V_P re, im
   p1[0] = make_double2(re.zeta, im.zeta);
   p1[1] = make_double2(re.phi, im.phi);

@@ -137,76 +137,79 @@ __global__ void __launch_bounds__(256) k_sweep_nodes_all(
     if (idx >= n_list) return;
     idx = idx_list[idx];
   }
-  if (idx >= C) {
-    if constexpr (RES) {
-      SDCSW_PDL_WAIT();
-      resid_block(ra, nullptr, count);  // the block reduction needs every thread
-    }
-    return;
+  // with RES every thread of the block must reach the one resid_block call (it holds
+  // block barriers), so tail threads stay converged with zero contributions
+  const bool active = idx < C;
+  if constexpr (!RES) {
+    if (!active) return;
   }
-  const double lam = lamv[idx];
-  const double2 sc = xscale != nullptr ? xscale[idx] : make_double2(0.0, 0.0);
-  const int row = xsyn != nullptr ? idx_row[idx] : 0;
-  SDCSW_PDL_WAIT();
-  double ss[RES ? MX : 1][3];  // residual: squared norms per (node, field) of this coefficient
-  const int z = blockIdx.z;
-  const int C2 = 2 * C;
-  u0 += (size_t)z * 3 * C2;
-  fe += z * fe_mstride;
-  fi += z * fi_mstride;
-  Tri a0r, a0i;
-  load_tri2(u0, C, idx, a0r, a0i);
-  const Tri f0r = f_impl_tri(a0r, phibar, lam), f0i = f_impl_tri(a0i, phibar, lam);
-  Tri Fr[MX], Fi[MX], Ir[MX], Ii[MX];
-#pragma unroll
-  for (int j = 0; j < MX; ++j)
-    if (j < M) {
-      load_tri2(fe + j * fe_stride, C, idx, Fr[j], Fi[j]);
-      if (first) {
-        Ir[j] = f0r;
-        Ii[j] = f0i;
-      } else {
-        load_tri2(fi + j * fi_stride, C, idx, Ir[j], Ii[j]);
-      }
-    }
-  const int nbt = count * gridDim.z, ch = chunk > 0 ? chunk : nbt;
-  for (int q = 0; q < count; ++q) {
-    const int m = lo + q;
-    const int ob = z * count + q;  // output batch entry
-    const double* c = cf.v + m * (M + 4);
-    Tri br = a0r, bi = a0i, fmr = f0r, fmi = f0i;
+  double ss[RES ? MX : 1][3] = {};  // residual: squared norms per (node, field) of this coefficient
+  if (active) {
+    const double lam = lamv[idx];
+    const double2 sc = xscale != nullptr ? xscale[idx] : make_double2(0.0, 0.0);
+    const int row = xsyn != nullptr ? idx_row[idx] : 0;
+    SDCSW_PDL_WAIT();
+    const int z = blockIdx.z;
+    const int C2 = 2 * C;
+    u0 += (size_t)z * 3 * C2;
+    fe += z * fe_mstride;
+    fi += z * fi_mstride;
+    Tri a0r, a0i;
+    load_tri2(u0, C, idx, a0r, a0i);
+    const Tri f0r = f_impl_tri(a0r, phibar, lam), f0i = f_impl_tri(a0i, phibar, lam);
+    Tri Fr[MX], Fi[MX], Ir[MX], Ii[MX];
 #pragma unroll
     for (int j = 0; j < MX; ++j)
       if (j < M) {
-        br = axpy_tri(br, c[j], add_tri(Fr[j], Ir[j]));
-        bi = axpy_tri(bi, c[j], add_tri(Fi[j], Ii[j]));
-        if (j == m) {
-          fmr = Ir[j];
-          fmi = Ii[j];
+        load_tri2(fe + j * fe_stride, C, idx, Fr[j], Fi[j]);
+        if (first) {
+          Ir[j] = f0r;
+          Ii[j] = f0i;
+        } else {
+          load_tri2(fi + j * fi_stride, C, idx, Ir[j], Ii[j]);
         }
       }
-    if constexpr (RES) {  // collocation residual of the previous iterate at node m:
-      // u0 + sum_j w_mj F_j (the quadrature just formed) - u_prev_m
-      Tri pr, pi;
-      load_tri2(ra.u_prev + (size_t)q * 3 * C2, C, idx, pr, pi);
-      const double d[3][2] = {{br.phi - pr.phi, bi.phi - pi.phi},
-                              {br.zeta - pr.zeta, bi.zeta - pi.zeta},
-                              {br.delta - pr.delta, bi.delta - pi.delta}};
+    const int nbt = count * gridDim.z, ch = chunk > 0 ? chunk : nbt;
+    for (int q = 0; q < count; ++q) {
+      const int m = lo + q;
+      const int ob = z * count + q;  // output batch entry
+      const double* c = cf.v + m * (M + 4);
+      Tri br = a0r, bi = a0i, fmr = f0r, fmi = f0i;
 #pragma unroll
-      for (int f = 0; f < 3; ++f) ss[q][f] = d[f][0] * d[f][0] + d[f][1] * d[f][1];
+      for (int j = 0; j < MX; ++j)
+        if (j < M) {
+          br = axpy_tri(br, c[j], add_tri(Fr[j], Ir[j]));
+          bi = axpy_tri(bi, c[j], add_tri(Fi[j], Ii[j]));
+          if (j == m) {
+            fmr = Ir[j];
+            fmi = Ii[j];
+          }
+        }
+      if constexpr (RES) {  // collocation residual of the previous iterate at node m:
+        // u0 + sum_j w_mj F_j (the quadrature just formed) - u_prev_m
+        Tri pr, pi;
+        load_tri2(ra.u_prev + (size_t)q * 3 * C2, C, idx, pr, pi);
+        const double d[3][2] = {{br.phi - pr.phi, bi.phi - pi.phi},
+                                {br.zeta - pr.zeta, bi.zeta - pi.zeta},
+                                {br.delta - pr.delta, bi.delta - pi.delta}};
+#pragma unroll
+        for (int f = 0; f < 3; ++f) ss[q][f] = d[f][0] * d[f][0] + d[f][1] * d[f][1];
+      }
+      br = axmy_tri(br, c[M], fmr);
+      bi = axmy_tri(bi, c[M], fmi);
+      const Tri ur = solve_tri(br, c[M + 1], c[M + 2], c[M + 3], lam);
+      const Tri ui = solve_tri(bi, c[M + 1], c[M + 2], c[M + 3], lam);
+      if (u_out != nullptr) store_tri2(u_out + (size_t)ob * 3 * C2, C, idx, ur, ui);
+      store_tri2(fi_out + (size_t)ob * 3 * C2, C, idx, f_impl_tri(ur, phibar, lam),
+                 f_impl_tri(ui, phibar, lam));
+      if (xsyn != nullptr) {
+        const int cb = ob / ch, w = nbt - cb * ch < ch ? nbt - cb * ch : ch;
+        write_xsyn_full(xsyn + (size_t)cb * rows * ch * kXsyn + xsyn_off(row, ob - cb * ch, w),
+                        16 * (size_t)w, ur, ui, sc);
+      }
     }
-    br = axmy_tri(br, c[M], fmr);
-    bi = axmy_tri(bi, c[M], fmi);
-    const Tri ur = solve_tri(br, c[M + 1], c[M + 2], c[M + 3], lam);
-    const Tri ui = solve_tri(bi, c[M + 1], c[M + 2], c[M + 3], lam);
-    if (u_out != nullptr) store_tri2(u_out + (size_t)ob * 3 * C2, C, idx, ur, ui);
-    store_tri2(fi_out + (size_t)ob * 3 * C2, C, idx, f_impl_tri(ur, phibar, lam),
-               f_impl_tri(ui, phibar, lam));
-    if (xsyn != nullptr) {
-      const int cb = ob / ch, w = nbt - cb * ch < ch ? nbt - cb * ch : ch;
-      write_xsyn_full(xsyn + (size_t)cb * rows * ch * kXsyn + xsyn_off(row, ob - cb * ch, w),
-                      16 * (size_t)w, ur, ui, sc);
-    }
+  } else {
+    SDCSW_PDL_WAIT();
   }
   if constexpr (RES) resid_block(ra, ss, count);
 }

@@ -276,6 +276,11 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
       (e = cudaMalloc(&p.gan, (size_t)p.max_batch * J * p.L * kNumSlots * 2 * sizeof(double2))) !=
           cudaSuccess ||
       (e = cudaMalloc(&p.coef_dev, kCoefCap * sizeof(double))) != cudaSuccess ||
+      // residual sweeps: [6 nodes x 3 fields][blocks] partials + last-block counter,
+      // allocated here so the opt-in call never allocates (or is half-built) under capture
+      (e = cudaMalloc(&p.resid_part, 18 * (size_t)((C + 255) / 256) * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&p.resid_count, sizeof(unsigned))) != cudaSuccess ||
+      (e = cudaMemset(p.resid_count, 0, sizeof(unsigned))) != cudaSuccess ||
       (e = configure_ring(p.ring_smem)) != cudaSuccess ||
       (e = configure_synthesis()) != cudaSuccess ||
       (e = configure_synthesis_bulk()) != cudaSuccess ||
@@ -286,7 +291,7 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
     void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
                     p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev,
                     p.xscale, p.idx_row, p.xsyn, p.anal_work4, p.ptab_a, p.htab_a,
-                    p.ptab_s, p.htab_s};
+                    p.ptab_s, p.htab_s, p.resid_part, p.resid_count};
     for (void* q : ptrs)
       if (q) cudaFree(q);
     delete h;
@@ -487,15 +492,8 @@ int sdcsw_sweep_nodes_residual(sdcsw_plan* h, int n_nodes, int node_lo, int coun
     set_error("sdcsw_sweep_nodes_residual: not available on a spectrally split plan");
     return SDCSW_ERR_STATE;
   }
-  if (p.resid_part == nullptr) {  // [6 nodes x 3 fields][blocks] partials + block counter
-    const size_t blocks = (p.C + 255) / 256;
-    if (cudaMalloc(&p.resid_part, 18 * blocks * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&p.resid_count, sizeof(unsigned)) != cudaSuccess ||
-        cudaMemset(p.resid_count, 0, sizeof(unsigned)) != cudaSuccess) {
-      set_error("sdcsw_sweep_nodes_residual: workspace allocation failed");
-      return SDCSW_ERR_CUDA;
-    }
-  }
+  // the partials and the block counter are per plan: residual sweeps on one plan must be
+  // serialised on one stream (include/sdcsw.h)
   const ResidArgs ra{u_prev, p.resid_part, p.resid_count, resid};
   return cuda_status(launch_sweep_nodes(p, n_nodes, node_lo, count, node_coef,
                                         (const double2*)u0, (const double2*)fe, fe_stride,

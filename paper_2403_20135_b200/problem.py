@@ -91,6 +91,22 @@ class DeviceProblem(SplitProblem):
         )
         return out
 
+    def workspace(self, which):
+        """A float64 torch view (no copy) of internal workspace ``which``
+        (``sdcsw_workspace``: 0 = Fourier coefficients, 1 = analysis data);
+        for tests and diagnostics."""
+        import torch
+
+        ptr, nbytes = ctypes.c_void_p(), ctypes.c_longlong()
+        _native.check(self._lib.sdcsw_workspace(self._plan, which, ctypes.byref(ptr), ctypes.byref(nbytes)),
+                      "sdcsw_workspace")
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (nbytes.value // 8,), "typestr": "<f8",
+                                        "data": (ptr.value, False), "version": 3, "strides": None}
+
+        return torch.as_tensor(_View(), device=self.device)
+
     def f_impl_device(self, u, out, nb=None):
         nb = u.shape[0] if nb is None else nb
         self._check_batch(u, nb)

@@ -82,3 +82,48 @@ def test_solve_contracts():
     assert_implicit_solve_contract(p, u)
     rng = np.random.default_rng(4)
     assert_implicit_linearity(p, u, random_initial_state(p.grid, 5), rng)
+
+
+# ---------------------------------------------------------------------------
+# m > 0 known-answer flows on the GPU problem (tests/sphere_kats.py): the
+# device f_E + f_I equals the analytic tendency (the oracle only builds the
+# inputs and the expected spectra from closed-form grid fields).
+# ---------------------------------------------------------------------------
+from sphere_kats import field_errors, rossby_haurwitz, tilted_potential, tilted_rotation  # noqa: E402
+
+_FLOWS = {
+    "rotation_a45": lambda o: tilted_rotation(o, np.pi / 4),
+    "rotation_a90": lambda o: tilted_rotation(o, np.pi / 2),
+    "potential_a45": lambda o: tilted_potential(o, np.pi / 4),
+    "potential_a90": lambda o: tilted_potential(o, np.pi / 2),
+    "rossby_haurwitz4": rossby_haurwitz,
+}
+
+
+@pytest.mark.parametrize("trunc", [63, 127])
+@pytest.mark.parametrize("name", sorted(_FLOWS))
+def test_known_answer_flows_m_positive(trunc, name):
+    p, o = pair(trunc)
+    x, want = _FLOWS[name](o)
+    fe, fi = p.f_expl(x), p.f_impl(x)
+    err = field_errors(o, fe + fi, want, [fe, fi])
+    assert (max(err[:2]) if name.startswith("rossby") else max(err)) <= 1e-10, err
+
+
+def test_known_answer_flows_catch_device_sign_error():
+    """A library built with the wrong sign of the i m chi term of U (in every
+    synthesis-operand writer, -DSDCSW_MUTATE_UCHI=1) fails the divergent
+    known-answer flows by O(1); the shipped library passes them."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "kat_mutation.py")],
+                       capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert max(res["default"].values()) <= 1e-10
+    assert res["mutant_u_chi_sign"]["potential_a45"] > 0.1
+    assert res["mutant_u_chi_sign"]["potential_a90"] > 0.1

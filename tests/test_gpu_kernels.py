@@ -558,3 +558,58 @@ def test_serial_divergence_reports_step():
         integrate(p, u0, 120.0, 6, SerialSdcStepper(cfg), checkpoint_interval=6)
     assert got.value.step_index == ref.value.step_index
     cfg.close()
+
+
+@pytest.mark.parametrize("nb,max_batch", [(8, 8), (8, 12), (25, 25), (13, 18)])
+def test_bulk_synthesis_partial_batch_block(nb, max_batch):
+    """Bulk-staged synthesis with nb > 6 states (batch blocks of 6 along grid z,
+    the last one partial): every state's Fourier coefficients are
+    bitwise equal to a one-state synthesis of it (per-column sums do not depend
+    on the batch), agree with the cp.async synthesis to rounding, and the
+    workspace entries of states nb..max_batch-1 keep a sentinel (no store past
+    the last state)."""
+    import torch
+
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    def plan(bulk):
+        old = os.environ.get("SDCSW_SYN_BULK")
+        os.environ["SDCSW_SYN_BULK"] = bulk
+        try:
+            return SphericalShallowWater(127, max_batch=max_batch)
+        finally:
+            if old is None:
+                del os.environ["SDCSW_SYN_BULK"]
+            else:
+                os.environ["SDCSW_SYN_BULK"] = old
+
+    def synth(p, u, nb):
+        s = p.stream()
+        _native_check(p, 0, u, nb, s)
+        _native_check(p, 3, u, nb, s)
+        torch.cuda.synchronize()
+        return p.workspace(0).view(max_batch, -1)
+
+    pb, pc = plan("1"), plan("0")
+    states = np.stack([random_initial_state(pb.grid, 70 + b) for b in range(nb)])
+    u = torch.from_numpy(states).to(pb.device).contiguous()
+    wb = pb.workspace(0).view(max_batch, -1)
+    wb.fill_(12345.0)
+    bulk = synth(pb, u, nb).clone()
+    assert torch.isfinite(bulk[:nb]).all()
+    assert (bulk[nb:] == 12345.0).all()
+    cp = synth(pc, u, nb).clone()
+    d = (bulk[:nb] - cp[:nb]).abs().max().item()
+    assert d <= 1e-13 * cp[:nb].abs().max().item()
+    for b in sorted({0, 5, 6, nb - 2, nb - 1}):
+        one = synth(pb, u[b : b + 1].contiguous(), 1)
+        assert torch.equal(one[0], bulk[b]), b
+    pb.close()
+    pc.close()
+
+
+def _native_check(p, stage, u, nb, s):
+    from paper_2403_20135_b200 import _native
+
+    out = p.empty_states(nb)
+    _native.check(p._lib.sdcsw_transform_stage(p.handle, stage, u.data_ptr(), out.data_ptr(), nb, s))

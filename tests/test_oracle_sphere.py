@@ -42,19 +42,56 @@ def test_synthesis_analysis_round_trip(small):
     assert np.max(np.abs(back - coef)) < 1e-13 * np.max(np.abs(coef))
 
 
-def test_laplacian_eigenfunction(small):
-    """lambda_n is the symbol of -laplacian: f_impl maps Phi' Y_n^m to lambda_n Y_n^m in delta."""
+# closed-form associated Legendre shapes P(mu) (any normalisation) and dP/dmu
+_LEGENDRE_SHAPES = {
+    (2, 1): (lambda x: x * np.sqrt(1 - x * x), lambda x: (1 - 2 * x * x) / np.sqrt(1 - x * x)),
+    (2, 2): (lambda x: 1 - x * x, lambda x: -2 * x),
+    (3, 2): (lambda x: x * (1 - x * x), lambda x: 1 - 3 * x * x),
+    (3, 3): (lambda x: (1 - x * x) ** 1.5, lambda x: -3 * x * np.sqrt(1 - x * x)),
+    (4, 3): (lambda x: x * (1 - x * x) ** 1.5, lambda x: np.sqrt(1 - x * x) * (1 - 4 * x * x)),
+}
+
+
+@pytest.mark.parametrize("nm", sorted(_LEGENDRE_SHAPES))
+def test_laplacian_eigenfunction(small, nm):
+    """lap Y_n^m = -n(n+1)/a^2 Y_n^m through synthesis -> grid -> analysis, m > 0.
+
+    For chi = a^2 P(mu) cos(m lam + 0.3) (and the same shape as psi) the wind is
+    known in closed form: U = (1/a) d_lam chi, V = ((1 - mu^2)/a) d_mu chi for
+    the divergent part, U = -((1 - mu^2)/a) d_mu psi, V = (1/a) d_lam psi for
+    the rotational part.  (i) The oracle's spectral wind synthesis (i m P and H
+    terms, inverse FFT) reproduces it on the grid; (ii) the divergence / curl
+    analysis of the closed-form grid wind returns -n(n+1)/a^2 times the field's
+    own coefficients (the Laplacian eigenvalue), and nothing else."""
     g, p = small
-    c = p.n_coef
-    for m, n in ((0, 3), (2, 5), (7, 7)):
-        i = np.nonzero((p.m_of == m) & (p.n_of == n))[0][0]
-        x = np.zeros(3 * c, complex)
-        x[i] = 1.0
-        fi = p.f_impl(x)
-        assert fi[2 * c + i] == n * (n + 1.0) / p.radius**2
-        # grid check: laplacian of Y via finite differences in longitude gives -m^2 part
-        grid = p.synthesize(x[:c])
-        assert abs(np.abs(grid).max()) > 0
+    n, m = nm
+    pf, dpf = _LEGENDRE_SHAPES[nm]
+    a = p.radius
+    mu = p.mu[:, None]
+    lam = 2 * np.pi * np.arange(p.nlon)[None, :] / p.nlon
+    ph = m * lam + 0.3
+    field = a * a * pf(mu) * np.cos(ph)
+    d_lam = -a * a * m * pf(mu) * np.sin(ph)
+    d_mu = a * a * dpf(mu) * np.cos(ph)
+    coef = p.analyze(field)
+    own = (p.n_of == n) & (p.m_of == m)
+    assert np.max(np.abs(coef[~own])) <= 1e-14 * np.max(np.abs(coef))  # one harmonic
+    lam_n = n * (n + 1.0) / a**2
+    cos2 = 1 - mu * mu
+    zero = np.zeros(p.n_coef, complex)
+    cases = (  # (zeta, delta) spectral, closed-form (U, V), which of (div, curl) is lap
+        (zero, -lam_n * coef, d_lam / a, cos2 * d_mu / a, 0),  # chi = field
+        (-lam_n * coef, zero, -cos2 * d_mu / a, d_lam / a, 1),  # psi = field
+    )
+    for zeta, delta, u_cf, v_cf, which in cases:
+        uf, vf = p.wind_fourier(zeta, delta)
+        scale = np.max(np.abs(u_cf)) + np.max(np.abs(v_cf))
+        assert np.max(np.abs(p.to_grid(uf) - u_cf)) <= 1e-13 * scale
+        assert np.max(np.abs(p.to_grid(vf) - v_cf)) <= 1e-13 * scale
+        div, curl = p.div_curl(p.to_fourier(u_cf), p.to_fourier(v_cf), p.w)
+        lap, other = (div, curl) if which == 0 else (curl, div)
+        assert np.linalg.norm(lap - (-lam_n) * coef) <= 1e-12 * lam_n * np.linalg.norm(coef)
+        assert np.linalg.norm(other) <= 1e-12 * lam_n * np.linalg.norm(coef)
 
 
 def test_f_expl_of_rest_is_zero(small):
@@ -171,3 +208,62 @@ def test_f_expl_vs_direct_sums():
     u[: p.n_coef] = 100.0 * rand_state(p, rng)[: p.n_coef]
     a, b = p.f_expl(u), direct_f_expl(p, u)
     assert max(relative_l2(a, b, p)) < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# m > 0 known-answer flows (tests/sphere_kats.py derives them): the discrete
+# f_E + f_I must equal the analytic tendency to rounding.
+# ---------------------------------------------------------------------------
+from sphere_kats import field_errors, rossby_haurwitz, tilted_potential, tilted_rotation  # noqa: E402
+
+_KAT_FLOWS = {
+    "rotation_a0": lambda o: tilted_rotation(o, 0.0),
+    "rotation_a45": lambda o: tilted_rotation(o, np.pi / 4),
+    "rotation_a90": lambda o: tilted_rotation(o, np.pi / 2),
+    "potential_a45": lambda o: tilted_potential(o, np.pi / 4),
+    "potential_a90": lambda o: tilted_potential(o, np.pi / 2),
+    "rossby_haurwitz4": rossby_haurwitz,
+}
+
+
+def kat_error(p, name):
+    x, want = _KAT_FLOWS[name](p)
+    fe, fi = p.f_expl(x), p.f_impl(x)
+    err = field_errors(p, fe + fi, want, [fe, fi])
+    return max(err[:2]) if name.startswith("rossby") else max(err)  # RH: delta_t not analytic
+
+
+@pytest.fixture(scope="module")
+def t42():
+    g = SphereGrid(trunc=42, nlat=64, nlon=128)
+    return SphericalShallowWaterOracle(g.trunc, g.nlat, g.nlon)
+
+
+@pytest.mark.parametrize("name", sorted(_KAT_FLOWS))
+def test_known_answer_flows(small, t42, name):
+    for p in (small[1], t42):
+        assert kat_error(p, name) <= 1e-10
+
+
+@pytest.mark.parametrize("flip", ["U_chi_P", "U_psi_H", "V_psi_P", "V_chi_H"])
+def test_known_answer_flows_catch_wind_sign_errors(small, flip):
+    """Mutation check: flipping the sign of any one term of the wind synthesis
+    (U = (i m chi P - psi H)/a, V = (i m psi P + chi H)/a) makes at least one
+    known-answer flow fail by O(1)."""
+    g, p0 = small
+    sign = {k: (-1.0 if k == flip else 1.0) for k in ("U_chi_P", "U_psi_H", "V_psi_P", "V_chi_H")}
+
+    class Mutant(SphericalShallowWaterOracle):
+        def wind_fourier(self, zeta, delta):
+            a = self.radius
+            psi, chi = -zeta * self.inv_lam, -delta * self.inv_lam
+            im = 1j * self.m_of
+            uf = (sign["U_chi_P"] * self.legendre_synthesis(im * chi, self.p)
+                  - sign["U_psi_H"] * self.legendre_synthesis(psi, self.h)) / a
+            vf = (sign["V_psi_P"] * self.legendre_synthesis(im * psi, self.p)
+                  + sign["V_chi_H"] * self.legendre_synthesis(chi, self.h)) / a
+            return uf, vf
+
+    p = Mutant(g.trunc, g.nlat, g.nlon, tables=(p0.mu, p0.w, p0.p, p0.h, p0.m_of, p0.n_of))
+    worst = max(kat_error(p, name) for name in _KAT_FLOWS if name != "rotation_a0")
+    assert worst > 0.1
