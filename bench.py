@@ -333,16 +333,10 @@ def run_device(args):
             # table-streaming regime: keep all nodes batched per GEMM (M x the
             # arithmetic intensity) and split the wavenumbers only
             groups = 1
-        xpeer, p2p_error = None, None
-        try:
-            xpeer = PeerNodeParallelDsdc(problem, cfg, dt, spectral_parts=world // groups)
-        except Exception as exc:  # noqa: BLE001 - reported in the JSON line
-            p2p_error = f"{type(exc).__name__}: {exc}"
-        ok = torch.tensor([0 if p2p_error else 1], dtype=torch.int32, device=problem.device)
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if not int(ok.item()):
-            if xpeer is not None:
-                xpeer.close()
+        # collective: peer mappings work on every rank, else every rank takes NCCL
+        xpeer, p2p_error = PeerNodeParallelDsdc.create_collective(
+            problem, cfg, dt, spectral_parts=world // groups)
+        if xpeer is None:
             problem._lib.sdcsw_plan_set_split(problem.handle, 1, 0, None, 0)
             transport = "nccl"
             print(f"[bench] peer exchange unavailable ({p2p_error}); NCCL transport", file=sys.stderr)

@@ -28,7 +28,8 @@ typedef enum {
   SDCSW_ERR_PARAM = 1,    /* -> ParameterError (errors.py:4) */
   SDCSW_ERR_CUDA = 2,     /* launch / allocation failure -> DeviceError */
   SDCSW_ERR_STATE = 3,    /* call on a destroyed or mismatched handle */
-  SDCSW_ERR_DIVERGED = 4  /* non-finite state -> DivergenceError (integrators.py:544-548) */
+  SDCSW_ERR_DIVERGED = 4, /* non-finite state -> DivergenceError (integrators.py:544-548) */
+  SDCSW_ERR_PEER = 5      /* a peer did not post an exchange within the wait bound -> DeviceError */
 } sdcsw_status;
 
 typedef struct sdcsw_plan sdcsw_plan;
@@ -257,6 +258,12 @@ int sdcsw_split_f_expl_end(sdcsw_plan* plan, double* fe, int nb, void* stream);
  *     graph of up to 8 steps.
  *   option 0: publish fused into the analysis epilogue (default 1 where the
  *     plan supports it: spherical, T < 400, unsplit).
+ *   option 1: bound, in milliseconds, of every device wait on a peer's post
+ *     (default 30000).  A wait that runs out records the peer and exchange
+ *     and returns; later waits of the exchange do not wait again (the state
+ *     is then invalid).  sdcsw_exchange_diverged reports it as
+ *     SDCSW_ERR_PEER naming the rank - a dead or stalled peer produces an
+ *     error, never a hung GPU.  reset clears it.
  *   info: own node block and kernels per step.
  *   reset: divergence is reported relative to the step count at the reset.
  * Every rank must run the same number of steps (the exchange numbers derive

@@ -12,7 +12,7 @@ from .errors import DeviceError, DivergenceError, ParameterError
 LIB_PATH = os.environ.get("SDCSW_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libsdcsw.so")  # env: experiment builds only
 
-SDCSW_OK, SDCSW_ERR_PARAM, SDCSW_ERR_CUDA, SDCSW_ERR_STATE, SDCSW_ERR_DIVERGED = range(5)
+SDCSW_OK, SDCSW_ERR_PARAM, SDCSW_ERR_CUDA, SDCSW_ERR_STATE, SDCSW_ERR_DIVERGED, SDCSW_ERR_PEER = range(6)
 IPC_HANDLE_BYTES = 64  # SDCSW_IPC_HANDLE_BYTES
 COMM_ID_BYTES = 128  # SDCSW_COMM_ID_BYTES
 

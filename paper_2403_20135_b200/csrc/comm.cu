@@ -10,10 +10,17 @@
 // collective on the data path are these calls.  All collectives are
 // stream-ordered and capturable into CUDA graphs (the node-parallel step
 // replays as one graph with the all-gathers inside).
+//
+// NCCL is bound at first use with dlopen("libnccl.so.2"), not at link time:
+// the process's NCCL is then the one PyTorch already loaded (same soname), so
+// loading libsdcsw.so can never put a second, older NCCL in front of
+// libtorch_cuda (which needs its own version's symbols).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "../../include/sdcsw.h"
@@ -28,9 +35,59 @@ struct sdcsw_comm {
 
 namespace {
 
+struct Nccl {
+  bool ok = false;
+  std::string why;
+  decltype(&::ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&::ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&::ncclCommSplit) CommSplit = nullptr;
+  decltype(&::ncclCommCount) CommCount = nullptr;
+  decltype(&::ncclCommUserRank) CommUserRank = nullptr;
+  decltype(&::ncclAllGather) AllGather = nullptr;
+  decltype(&::ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&::ncclGetErrorString) GetErrorString = nullptr;
+  decltype(&::ncclGetVersion) GetVersion = nullptr;
+};
+
+const Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) {
+      n.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+      return;
+    }
+    bool all = true;
+    auto bind = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      all = all && fn != nullptr;
+    };
+    bind(n.GetUniqueId, "ncclGetUniqueId");
+    bind(n.CommInitRank, "ncclCommInitRank");
+    bind(n.CommSplit, "ncclCommSplit");
+    bind(n.CommCount, "ncclCommCount");
+    bind(n.CommUserRank, "ncclCommUserRank");
+    bind(n.AllGather, "ncclAllGather");
+    bind(n.CommDestroy, "ncclCommDestroy");
+    bind(n.GetErrorString, "ncclGetErrorString");
+    bind(n.GetVersion, "ncclGetVersion");
+    n.ok = all;
+    if (!all) n.why = "libnccl.so.2 lacks a required symbol (NCCL >= 2.18 needed)";
+  });
+  return n;
+}
+
+int nccl_missing(const char* where) {
+  const Nccl& n = nccl();
+  if (n.ok) return SDCSW_OK;
+  sdcsw::set_error(std::string(where) + ": " + n.why);
+  return SDCSW_ERR_CUDA;
+}
+
 int nccl_status(ncclResult_t r, const char* where) {
   if (r == ncclSuccess) return SDCSW_OK;
-  sdcsw::set_error(std::string(where) + ": " + ncclGetErrorString(r) +
+  sdcsw::set_error(std::string(where) + ": " + nccl().GetErrorString(r) +
                    (r == ncclInvalidArgument || r == ncclInvalidUsage ? "" : " (NCCL)"));
   return (r == ncclInvalidArgument || r == ncclInvalidUsage) ? SDCSW_ERR_PARAM : SDCSW_ERR_CUDA;
 }
@@ -44,8 +101,9 @@ int sdcsw_comm_unique_id(void* id, int bytes) {
     sdcsw::set_error("sdcsw_comm_unique_id: need a buffer of SDCSW_COMM_ID_BYTES bytes");
     return SDCSW_ERR_PARAM;
   }
+  if (int st = nccl_missing("sdcsw_comm_unique_id")) return st;
   ncclUniqueId uid;
-  const int st = nccl_status(ncclGetUniqueId(&uid), "sdcsw_comm_unique_id");
+  const int st = nccl_status(nccl().GetUniqueId(&uid), "sdcsw_comm_unique_id");
   if (st == SDCSW_OK) memcpy(id, &uid, sizeof(uid));
   return st;
 }
@@ -58,6 +116,7 @@ int sdcsw_comm_create(const void* id, int bytes, int world, int rank, int device
     return SDCSW_ERR_PARAM;
   }
   *out = nullptr;
+  if (int st = nccl_missing("sdcsw_comm_create")) return st;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {
     sdcsw::set_error(std::string("sdcsw_comm_create: ") + cudaGetErrorString(e));
@@ -66,7 +125,7 @@ int sdcsw_comm_create(const void* id, int bytes, int world, int rank, int device
   ncclUniqueId uid;
   memcpy(&uid, id, sizeof(uid));
   sdcsw_comm* c = new sdcsw_comm;
-  const int st = nccl_status(ncclCommInitRank(&c->comm, world, uid, rank), "sdcsw_comm_create");
+  const int st = nccl_status(nccl().CommInitRank(&c->comm, world, uid, rank), "sdcsw_comm_create");
   if (st != SDCSW_OK) {
     delete c;
     return st;
@@ -85,11 +144,11 @@ int sdcsw_comm_split(sdcsw_comm* parent, int color, int key, sdcsw_comm** out) {
   }
   *out = nullptr;
   sdcsw_comm* c = new sdcsw_comm;
-  int st = nccl_status(ncclCommSplit(parent->comm, color, key, &c->comm, nullptr), "sdcsw_comm_split");
-  if (st == SDCSW_OK) st = nccl_status(ncclCommCount(c->comm, &c->world), "sdcsw_comm_split");
-  if (st == SDCSW_OK) st = nccl_status(ncclCommUserRank(c->comm, &c->rank), "sdcsw_comm_split");
+  int st = nccl_status(nccl().CommSplit(parent->comm, color, key, &c->comm, nullptr), "sdcsw_comm_split");
+  if (st == SDCSW_OK) st = nccl_status(nccl().CommCount(c->comm, &c->world), "sdcsw_comm_split");
+  if (st == SDCSW_OK) st = nccl_status(nccl().CommUserRank(c->comm, &c->rank), "sdcsw_comm_split");
   if (st != SDCSW_OK) {
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm) nccl().CommDestroy(c->comm);
     delete c;
     return st;
   }
@@ -116,7 +175,7 @@ int sdcsw_allgather_rhs(sdcsw_comm* c, const double* send, double* recv, long lo
     return SDCSW_ERR_PARAM;
   }
   if (count == 0) return SDCSW_OK;
-  return nccl_status(ncclAllGather(send, recv, (size_t)count, ncclDouble, c->comm,
+  return nccl_status(nccl().AllGather(send, recv, (size_t)count, ncclDouble, c->comm,
                                    (cudaStream_t)stream),
                      "sdcsw_allgather_rhs");
 }
@@ -124,14 +183,14 @@ int sdcsw_allgather_rhs(sdcsw_comm* c, const double* send, double* recv, long lo
 int sdcsw_comm_destroy(sdcsw_comm* c) {
   if (c == nullptr) return SDCSW_OK;
   int st = SDCSW_OK;
-  if (c->comm != nullptr) st = nccl_status(ncclCommDestroy(c->comm), "sdcsw_comm_destroy");
+  if (c->comm != nullptr) st = nccl_status(nccl().CommDestroy(c->comm), "sdcsw_comm_destroy");
   delete c;
   return st;
 }
 
-int sdcsw_nccl_version(void) {
+int sdcsw_nccl_version(void) {  // 0 if no NCCL can be loaded
   int v = 0;
-  ncclGetVersion(&v);
+  if (nccl().ok) nccl().GetVersion(&v);
   return v;
 }
 

@@ -277,6 +277,15 @@ constexpr int kMaxPeers = 16;
 struct PeerFlags {
   unsigned long long flag[kMaxPeers];  // flag[q]: last exchange rank q posted here
 };
+// Every device wait on a peer's post is bounded: after `limit_ns` (globaltimer)
+// without the post, the waiter records (peer + 1, exchange number) in the
+// exchange's error words and returns; later waits of the exchange see the
+// error and do not wait again.  The host reports it as SDCSW_ERR_PEER (a peer
+// that died or stopped stepping produces an error, not a hung GPU).
+struct PeerTimeout {
+  int* err;                      // [0] peer + 1 (0 = none), [1] channel, [2] exchange number
+  unsigned long long limit_ns;
+};
 struct PeerWait {
   const PeerFlags* flags;   // local flag block (null: no exchange, plain pointers)
   const int* epoch;         // device step counter of the exchange (incremented per step)
@@ -285,12 +294,39 @@ struct PeerWait {
   int world;
   long long par_stride;     // doubles between the two parities of X
   unsigned long long* post[kMaxPeers];  // &flags_q->flag[rank] of every rank q
+  PeerTimeout to;
 };
 #ifdef __CUDACC__
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin (acquire, system scope) until *flag >= n; false after the time limit or
+// if an earlier wait of this exchange already timed out (error recorded).
+static __device__ __noinline__ bool wait_posted(const unsigned long long* flag, unsigned long long n,
+                                         const PeerTimeout& to, int peer, int channel) {
+  if (ld_acquire_sys(flag) >= n) return true;
+  volatile int* err = to.err;
+  if (err[0] != 0) return false;
+  const unsigned long long t0 = global_ns();
+  while (ld_acquire_sys(flag) < n) {
+    __nanosleep(64);
+    if (global_ns() - t0 > to.limit_ns || err[0] != 0) {
+      if (atomicCAS(to.err, 0, peer + 1) == 0) {
+        err[1] = channel;
+        err[2] = (int)n;
+        __threadfence_system();
+      }
+      return false;
+    }
+  }
+  return true;
 }
 __device__ __forceinline__ unsigned long long exchange_number(const int* epoch, int k, int kx) {
   return (unsigned long long)(*epoch - 1) * (unsigned long long)kx + (unsigned long long)k;
@@ -311,7 +347,7 @@ __device__ __forceinline__ long long peer_wait(const PeerWait& pw) {
     if (pw.world > 1) __threadfence_system();
     for (int q = 0; q < pw.world; ++q) atomicMax_system(pw.post[q], n);
     for (int q = 0; q < pw.world; ++q)
-      while (ld_acquire_sys(&pw.flags->flag[q]) < n) __nanosleep(32);
+      if (!wait_posted(&pw.flags->flag[q], n, pw.to, q, 0)) break;
   }
   __syncthreads();
   return (long long)(n & 1) * pw.par_stride;
@@ -339,6 +375,7 @@ struct RingPeer {
   int world;
   long long par_stride;            // double2 per parity
   unsigned long long* post[kMaxPeers];  // &fourier flags of spectral peer q ->flag[sp]
+  PeerTimeout to;
 };
 
 // Sweep-fused analysis (latency regime, one state, M <= kFuseMaxNodes): the

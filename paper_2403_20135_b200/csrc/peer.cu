@@ -111,7 +111,9 @@ struct sdcsw_exchange {
   char* local;               // private buffers
   double2 *fe0, *fe_loc, *fi_loc;
   double *xsyn1, *xsynM;
-  int* flags;                // [0] first diverged epoch (INT_MAX = none), [1] epoch (never reset)
+  int* flags;                // [0] first diverged epoch (INT_MAX = none), [1] epoch (never reset),
+                             // [2..4] wait timeout: peer + 1 (0 = none), channel, exchange number
+  unsigned long long timeout_ns;  // bound of every device wait on a peer's post (option 1)
   unsigned long long* fseq;  // completed Fourier exchanges
   unsigned int* done;        // ring CTA counter
   int base_epoch;            // epoch at the last reset (divergence step = epoch - base)
@@ -166,6 +168,7 @@ PeerWait peer_wait_args(const sdcsw_exchange* x, int k) {
   pw.world = x->G;
   pw.par_stride = (long long)x->M * 2 * (long long)x->S1 * 2;
   for (int i = 0; i < x->G; ++i) pw.post[i] = &nflag_of(x, i * x->S + x->sp)->flag[x->g];
+  pw.to = PeerTimeout{x->flags + 2, x->timeout_ns};
   return pw;
 }
 
@@ -178,6 +181,7 @@ RingPeer ring_peer_args(const sdcsw_exchange* x) {
   rp.world = x->S;
   rp.par_stride = x->fpar;
   for (int q = 0; q < x->S; ++q) rp.post[q] = &fflag_of(x, x->g * x->S + q)->flag[x->sp];
+  rp.to = PeerTimeout{x->flags + 2, x->timeout_ns};
   return rp;
 }
 
@@ -405,8 +409,9 @@ int sdcsw_exchange_create_split(sdcsw_plan* h, int n_nodes, int n_sweeps, const 
   x->fseq = reinterpret_cast<unsigned long long*>(tail);
   x->done = reinterpret_cast<unsigned int*>(tail + 8);
   x->flags = reinterpret_cast<int*>(tail + 16);
-  const int init[2] = {INT_MAX, 0};
+  const int init[5] = {INT_MAX, 0, 0, 0, 0};
   cudaMemcpy(x->flags, init, sizeof(init), cudaMemcpyHostToDevice);
+  x->timeout_ns = 30ull * 1000000000ull;
   x->base[rank] = x->mem;
   x->attached = 1;
   if (S > 1) {  // the plan keeps own wavenumbers only; its Fourier buffer is F
@@ -542,6 +547,15 @@ int sdcsw_exchange_run(sdcsw_exchange* x, double* u, int n_steps, int use_graph,
 
 int sdcsw_exchange_set_option(sdcsw_exchange* x, int option, int value) {
   if (int st = check_x(x, "sdcsw_exchange_set_option")) return st;
+  if (option == 1) {  // bound of every device wait on a peer, milliseconds
+    if (value < 1) {
+      set_error("sdcsw_exchange_set_option: the wait bound must be >= 1 ms");
+      return SDCSW_ERR_PARAM;
+    }
+    x->timeout_ns = (unsigned long long)value * 1000000ull;
+    drop_graphs(x);  // the bound is a kernel argument captured in the graphs
+    return SDCSW_OK;
+  }
   if (option != 0) return SDCSW_ERR_PARAM;
   if (value && !fuse_ok(x->plan->p)) {
     set_error("sdcsw_exchange_set_option: the plan's analysis has no fused epilogue");
@@ -567,12 +581,21 @@ int sdcsw_exchange_info(sdcsw_exchange* x, int* node_lo, int* node_count, int* l
 int sdcsw_exchange_diverged(sdcsw_exchange* x, int* step_index) {
   if (int st = check_x(x, "sdcsw_exchange_diverged")) return st;
   if (!step_index) return SDCSW_ERR_PARAM;
-  int v[2];
+  int v[5];
   cudaSetDevice(x->plan->p.device);
   cudaDeviceSynchronize();
   cudaError_t e = cudaMemcpy(v, x->flags, sizeof(v), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_status(e, "sdcsw_exchange_diverged");
   *step_index = v[0] == INT_MAX ? 0 : v[0] - x->base_epoch;
+  if (v[2] != 0) {
+    const int peer = v[2] - 1;
+    const int rank = v[3] == 0 ? peer * x->S + x->sp : x->g * x->S + peer;
+    set_error("sdcsw_exchange: rank " + std::to_string(rank) + " did not post " +
+              (v[3] == 0 ? "node" : "Fourier") + " exchange " + std::to_string(v[4]) + " within " +
+              std::to_string(x->timeout_ns / 1000000ull) +
+              " ms (peer died or stopped stepping); the state is invalid");
+    return SDCSW_ERR_PEER;
+  }
   return SDCSW_OK;
 }
 
@@ -584,8 +607,9 @@ int sdcsw_exchange_reset(sdcsw_exchange* x, void* stream) {
   int epoch = 0;
   cudaError_t e = cudaStreamSynchronize(s);
   if (e == cudaSuccess) e = cudaMemcpy(&epoch, x->flags + 1, sizeof(int), cudaMemcpyDeviceToHost);
-  const int none = INT_MAX;
+  const int none = INT_MAX, clear[3] = {0, 0, 0};
   if (e == cudaSuccess) e = cudaMemcpyAsync(x->flags, &none, sizeof(int), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(x->flags + 2, clear, sizeof(clear), cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   x->base_epoch = epoch;
   return cuda_status(e, "sdcsw_exchange_reset");

@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
         if (rp.world > 1) __threadfence_system();
         for (int q = 0; q < rp.world; ++q) atomicMax_system(rp.post[q], fx);
         for (int q = 0; q < rp.world; ++q)
-          while (ld_acquire_sys(&rp.flags->flag[q]) < fx) __nanosleep(32);
+          if (!wait_posted(&rp.flags->flag[q], fx, rp.to, q, 1)) break;
       }
       __syncthreads();
       fsyn += (fx & 1) * rp.par_stride;

@@ -9,7 +9,8 @@ a group of G processes owns the contiguous node block
 1. assembles beta and solves its own nodes (``sdcsw_sweep_nodes``),
 2. evaluates f_E of its nodes (``sdcsw_f_expl``, nodes batched),
 3. all-gathers the (fe, fi) pairs of every node - the one exchange step
-   (NCCL over NVLink on the GPU; gloo in the CPU tests),
+   (``sdcsw_allgather_rhs``: NCCL over NVLink called from ``libsdcsw.so``,
+   :mod:`.comm`; torch.distributed over gloo in the CPU tests),
 
 after which every rank holds all tendencies, so the closing last-node solve
 and the next step's f_E(u0) are computed redundantly and the state stays
@@ -109,6 +110,25 @@ class CudaNodeBackend:
     def empty(self, n_states):
         return self.problem.empty_states(n_states)
 
+    def stream(self):
+        return self.problem.stream()
+
+    def make_comms(self, group, n_parts):
+        """(node-group, spectral-group) NCCL communicators of the C ABI: one
+        world communicator bootstrapped over ``group`` (unique id broadcast),
+        split by spectral part (node groups) and by node group (spectral
+        groups, only when ``n_parts`` > 1)."""
+        from .comm import NcclComm
+
+        world = NcclComm.bootstrap(self.problem.device.index, group)
+        if n_parts == 1:
+            return world, None
+        part, ng = world.rank % n_parts, world.rank // n_parts
+        node = world.split(part, ng)
+        spec = world.split(ng, part)
+        self._world_comm = world  # parent kept alive with its splits
+        return node, spec
+
     def f_expl(self, u, out, nb):
         self.problem.f_expl_device(u, out, nb)
 
@@ -160,10 +180,11 @@ class NodeParallelDsdc:
     def __init__(self, backend, cfg, dt, phibar, state_size, group=None, spectral_parts=1):
         import torch.distributed as dist
 
-        self.dist = dist
         self.backend = backend
-        world = dist.get_world_size(group)
-        rank = dist.get_rank(group)
+        if dist.is_available() and dist.is_initialized():
+            world, rank = dist.get_world_size(group), dist.get_rank(group)
+        else:
+            world, rank = 1, 0
         S = int(spectral_parts)
         if S < 1 or world % S:
             raise ParameterError(f"{world} ranks do not split into spectral groups of {S}")
@@ -171,16 +192,21 @@ class NodeParallelDsdc:
         self.part = rank % S
         node_group_index = rank // S
         n_groups = world // S
-        if S == 1:
-            self.group = group
-            self.spectral_group = None
-        else:
-            # every rank must create every group, in the same order
-            ranks = list(range(world)) if group is None else dist.get_process_group_ranks(group)
-            node_groups = [dist.new_group([ranks[g * S + q] for g in range(n_groups)]) for q in range(S)]
-            spec_groups = [dist.new_group([ranks[g * S + q] for q in range(S)]) for g in range(n_groups)]
-            self.group = node_groups[self.part]
-            self.spectral_group = spec_groups[node_group_index]
+        if hasattr(backend, "make_comms"):  # the device path: NCCL through the C ABI
+            self.node_comm, self.spec_comm = backend.make_comms(group, S)
+        else:  # CPU tests: torch.distributed collectives (gloo)
+            from .comm import DistComm
+
+            if S == 1:
+                self.node_comm, self.spec_comm = DistComm(group), None
+            else:
+                # every rank must create every group, in the same order
+                ranks = list(range(world)) if group is None else dist.get_process_group_ranks(group)
+                node_groups = [dist.new_group([ranks[g * S + q] for g in range(n_groups)]) for q in range(S)]
+                spec_groups = [dist.new_group([ranks[g * S + q] for q in range(S)]) for g in range(n_groups)]
+                self.node_comm = DistComm(node_groups[self.part])
+                self.spec_comm = DistComm(spec_groups[node_group_index])
+        self._stream = getattr(backend, "stream", lambda: None)
         self.world = n_groups
         self.rank = node_group_index
         self.m = cfg.table.n_nodes
@@ -208,9 +234,9 @@ class NodeParallelDsdc:
             self.backend.f_expl(u, out, nb)
             return
 
-        def gather(parts):  # the one Fourier exchange of a split f_E (one NCCL all-gather)
+        def gather(parts):  # the one Fourier exchange of a split f_E (one all-gather, in place)
             flat = self.backend.fourier.view(-1)[: len(parts) * parts[0].numel()]
-            self.dist.all_gather_into_tensor(flat, parts[self.part].clone(), group=self.spectral_group)
+            self.spec_comm.allgather(flat, parts[self.part], self._stream())
 
         self.backend.f_expl_split(u, out, nb, gather)
 
@@ -218,6 +244,11 @@ class NodeParallelDsdc:
         """Per-rank work: own nodes only (the redundant init/final are counted once per rank)."""
         n = 1 + (self.k - 1) * self.count
         return n, n, (self.k - 1) * self.count + 1
+
+    def close(self):
+        for c in (self.node_comm, self.spec_comm, getattr(self.backend, "_world_comm", None)):
+            if c is not None:
+                c.close()
 
     def capture(self, u, n_steps=1):
         """A CUDA graph of ``n_steps`` steps on ``u`` (kernels and NCCL all-gathers
@@ -252,8 +283,7 @@ class NodeParallelDsdc:
                 loc = self.local.view(self.per, 2, -1)
                 loc[: self.count, 0].copy_(self.fe_tmp.view(-1, self.S)[: self.count])
                 loc[: self.count, 1].copy_(self.fi_tmp.view(-1, self.S)[: self.count])
-            self.dist.all_gather_into_tensor(self.gathered.view(-1), self.local.view(-1),
-                                             group=self.group)
+            self.node_comm.allgather(self.gathered.view(-1), self.local.view(-1), self._stream())
             fe_src, fe_stride = fe_view, 2
             fi_src, fi_stride = fi_view, 2
             first = False
@@ -308,15 +338,84 @@ class PeerNodeParallelDsdc:
         if fused is not None:
             self.set_fused(fused)
         if self.world > 1 and exchange_handles:
-            import torch.distributed as dist
+            self.open_peers(group)
 
-            mine = ctypes.create_string_buffer(_native.IPC_HANDLE_BYTES)
-            _native.check(self.lib.sdcsw_exchange_ipc_handle(handle, mine, _native.IPC_HANDLE_BYTES))
-            every = [None] * self.world
-            dist.all_gather_object(every, mine.raw, group=group)
-            blob = ctypes.create_string_buffer(b"".join(every), self.world * _native.IPC_HANDLE_BYTES)
-            _native.check(self.lib.sdcsw_exchange_open_peers(handle, blob, _native.IPC_HANDLE_BYTES),
-                          "sdcsw_exchange_open_peers")
+    def ipc_handle(self):
+        """This rank's exchange-buffer IPC handle (bytes), or None if it cannot be exported."""
+        import ctypes
+
+        from . import _native
+
+        mine = ctypes.create_string_buffer(_native.IPC_HANDLE_BYTES)
+        st = self.lib.sdcsw_exchange_ipc_handle(self.handle, mine, _native.IPC_HANDLE_BYTES)
+        return mine.raw if st == _native.SDCSW_OK else None
+
+    def open_peers(self, group=None, mine=b""):
+        """All-gather the IPC handles over ``group`` and map every peer's buffer.
+
+        Collective: every rank of the group must call it, including a rank
+        whose exchange could not be created (it passes ``mine=None`` through
+        :meth:`join_failed`), so that a failure on some ranks never leaves the
+        others blocked in the all-gather; returns False on every rank if any
+        rank failed."""
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _native
+
+        if mine == b"":
+            mine = self.ipc_handle()
+        every = [None] * self.world
+        dist.all_gather_object(every, mine, group=group)
+        if any(h is None for h in every):
+            return False
+        blob = ctypes.create_string_buffer(b"".join(every), self.world * _native.IPC_HANDLE_BYTES)
+        _native.check(self.lib.sdcsw_exchange_open_peers(self.handle, blob, _native.IPC_HANDLE_BYTES),
+                      "sdcsw_exchange_open_peers")
+        return True
+
+    @classmethod
+    def create_collective(cls, problem, cfg, dt, spectral_parts=1, group=None):
+        """Create the exchange on every rank of ``group`` and map the peers, or
+        fail on ALL ranks together: returns ``(exchange, None)`` everywhere or
+        ``(None, reason)`` everywhere (reason is this rank's own error, or that
+        another rank failed).  Safe when creation or mapping fails on some ranks
+        only: the one collective (the handle all-gather) is joined by every
+        rank, and the outcome is agreed with a MIN all-reduce."""
+        import torch
+        import torch.distributed as dist
+
+        x, err = None, None
+        try:  # local part only (no collective inside)
+            x = cls(problem, cfg, dt, group=group, spectral_parts=spectral_parts, exchange_handles=False)
+        except Exception as exc:  # noqa: BLE001 - reported to the caller
+            err = f"{type(exc).__name__}: {exc}"
+        try:
+            opened = x.open_peers(group, mine=x.ipc_handle()) if x is not None else cls.join_failed(group)
+        except Exception as exc:  # noqa: BLE001 - a local mapping failure
+            opened, err = False, f"{type(exc).__name__}: {exc}"
+        dev = getattr(problem, "device", None)
+        backend = dist.get_backend(group)
+        ok = torch.tensor([1 if opened else 0], dtype=torch.int32,
+                          device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()):
+            return x, None
+        if x is not None:
+            x.close()
+        return None, err or "peer exchange unavailable on another rank"
+
+    @staticmethod
+    def join_failed(group=None):
+        """The collective part of :meth:`open_peers` for a rank whose exchange
+        could not be created: contributes no handle, so every rank sees the
+        failure and nobody opens peers."""
+        import torch.distributed as dist
+
+        every = [None] * dist.get_world_size(group)
+        dist.all_gather_object(every, None, group=group)
+        return False
 
     @classmethod
     def in_process(cls, problem, cfg, dt, world, fused=None, spectral_parts=1):
@@ -345,6 +444,14 @@ class PeerNodeParallelDsdc:
                     _native.check(x.lib.sdcsw_exchange_attach_peer(x.handle, q, b),
                                   "sdcsw_exchange_attach_peer")
         return ranks
+
+    def set_wait_bound(self, ms):
+        """Bound (milliseconds) of every device wait on a peer's post; a wait that
+        runs out makes :meth:`diverged` raise ``DeviceError`` naming the rank."""
+        from . import _native
+
+        _native.check(self.lib.sdcsw_exchange_set_option(self.handle, 1, int(ms)),
+                      "sdcsw_exchange_set_option")
 
     def set_fused(self, on=True):
         """Publish from the analysis epilogue (default where supported) or by a copy kernel."""
@@ -433,7 +540,9 @@ class PeerNodeParallelDsdc:
                       "sdcsw_exchange_reset")
 
     def diverged(self):
-        """First non-finite step index since creation / reset (0 = none); synchronises."""
+        """First non-finite step index since creation / reset (0 = none); synchronises.
+        Raises ``DeviceError`` if a peer did not post an exchange within the
+        wait bound (:meth:`set_wait_bound`)."""
         import ctypes
 
         v = ctypes.c_int()

@@ -223,12 +223,15 @@ def test_node_and_spectral_split_matches_single_process(tmp_path):
 class _FakeExchangeLib:
     """Records the exchange calls of PeerNodeParallelDsdc (host logic only)."""
 
-    def __init__(self, rank):
+    def __init__(self, rank, fail_create=False):
         self.rank = rank
         self.calls = []
+        self.fail_create = fail_create
 
     def sdcsw_exchange_create_split(self, plan, m, k, coef, n_coef, world, rank, parts, out):
         self.calls.append(("create", m, k, n_coef, world, rank, parts))
+        if self.fail_create:
+            return 2  # SDCSW_ERR_CUDA (e.g. the IPC buffer allocation failed)
         out._obj.value = 1000 + rank
         return 0
 
@@ -250,8 +253,8 @@ class _FakeProblem:
     handle = None
     mean_geopotential = 9.80616e4
 
-    def __init__(self, rank):
-        self._lib = _FakeExchangeLib(rank)
+    def __init__(self, rank, fail_create=False):
+        self._lib = _FakeExchangeLib(rank, fail_create)
 
 
 def _peer_worker(rank, world, port, out_path):
@@ -284,3 +287,37 @@ def test_peer_exchange_handles_gathered_in_rank_order(tmp_path):
     want = np.concatenate([np.full(64, q + 1, dtype=np.uint8) for q in range(world)])
     for r in range(world):
         assert np.array_equal(np.load(out + f".{r}.npy"), want)
+
+
+def _peer_fail_worker(rank, world, port, bad, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2403_20135_b200 import CollocationTable, SdcConfig, SweepMode
+    from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+
+    cfg = SdcConfig(table=CollocationTable.radau_right(4), n_sweeps=3,
+                    mode=SweepMode.DIAGONAL_PARALLEL, time_threads=1)
+    prob = _FakeProblem(rank, fail_create=rank in bad)
+    x, err = PeerNodeParallelDsdc.create_collective(prob, cfg, 90.0)
+    opened = any(c[0] == "open" for c in prob._lib.calls)
+    with open(out_path + f".{rank}", "w") as f:
+        f.write(f"{x is None} {opened} {err}")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("bad", [(1,), (0, 2), ()])
+def test_peer_exchange_failure_is_collective(tmp_path, bad):
+    """if the exchange cannot be created on some ranks, every rank
+    still joins the one collective and all of them fall back together (no
+    hang, nobody opens peers); with no failure every rank opens its peers."""
+    world = 3
+    port = 29300 + (os.getpid() % 97) + 7 * len(bad)
+    out = str(tmp_path / "f")
+    mp.spawn(_peer_fail_worker, args=(world, port, bad, out), nprocs=world, join=True)
+    for r in range(world):
+        failed, opened, err = open(out + f".{r}").read().split(" ", 2)
+        assert failed == str(bool(bad))
+        assert opened == str(not bad)
+        if bad and r not in bad:
+            assert "another rank" in err

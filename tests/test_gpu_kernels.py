@@ -255,23 +255,25 @@ def test_device_divergence_reports_step():
 
 
 def test_node_parallel_single_rank_matches_fused_stepper():
-    """The multi-GPU orchestration at world size 1 (NCCL) equals the fused stepper bitwise."""
+    """The multi-GPU orchestration at world size 1 over the C-ABI NCCL transport
+    (sdcsw_comm_create + sdcsw_allgather_rhs; no torch.distributed at all)
+    equals the fused stepper bitwise, eagerly and replayed as one CUDA graph
+    with the NCCL all-gathers inside."""
     import torch
-    import torch.distributed as dist
 
+    from paper_2403_20135_b200 import _native
+    from paper_2403_20135_b200.comm import NcclComm
     from paper_2403_20135_b200.integrators import DeviceStepper
     from paper_2403_20135_b200.parallel_nodes import CudaNodeBackend, NodeParallelDsdc
 
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29611")
-    if not dist.is_initialized():
-        dist.init_process_group("nccl", rank=0, world_size=1)
+    assert _native.lib().sdcsw_nccl_version() >= 22700
     p = gpu(63)
     table = CollocationTable.radau_right(3)
     cfg = SdcConfig(table=table, n_sweeps=3, mode=SweepMode.DIAGONAL_PARALLEL, time_threads=1)
     u0 = torch.from_numpy(random_initial_state(p.grid, 8)).to(p.device)
     a = u0.clone()
     npd = NodeParallelDsdc(CudaNodeBackend(p), cfg, 120.0, p.mean_geopotential, p.state_size)
+    assert isinstance(npd.node_comm, NcclComm) and npd.node_comm.world == 1
     for _ in range(3):
         npd.step(a)
     b = u0.clone()
@@ -286,7 +288,7 @@ def test_node_parallel_single_rank_matches_fused_stepper():
     torch.cuda.synchronize()
     assert torch.equal(c, b)
     st.close()
-    dist.destroy_process_group()
+    npd.close()
 
 
 @pytest.mark.parametrize("trunc,m_count,k_count", [(63, 1, 1), (63, 2, 3), (63, 3, 1), (63, 4, 4),

@@ -238,3 +238,44 @@ def test_exchange_spectral_split_table_streaming():
         own = torch.from_numpy(x.own_coefficients()).to(u.device)
         assert torch.equal(u.reshape(3, -1)[:, own], ref[:, own])
         x.close()
+
+
+@pytest.mark.parametrize("split", [False, True])
+def test_missing_peer_post_is_an_error_not_a_hang(split):
+    """a rank whose peer never posts (a killed or stalled
+    process) stops waiting after the wait bound and reports which rank did not
+    post, instead of spinning forever.  Rank 0 of a 2-rank exchange runs alone:
+    its node kernel of sweep 2 waits for node exchange 1 (split: its ring
+    kernel waits for the Fourier exchange of f_E(u0)), which rank 1 never
+    posts.  One kernel waits on nothing that runs concurrently, bounded to
+    250 ms.  reset() clears the error."""
+    import time
+
+    import torch
+
+    from paper_2403_20135_b200.errors import DeviceError
+    from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    cfg = _cfg(3, 3)
+    if split:
+        probs = [SphericalShallowWater(63, max_batch=8) for _ in range(2)]
+        ranks = PeerNodeParallelDsdc.in_process(probs, cfg, 120.0, 2, spectral_parts=2)
+        phases, what = range(0, 2), "Fourier exchange 1"
+    else:
+        p = gpu(63)
+        ranks = PeerNodeParallelDsdc.in_process(p, cfg, 120.0, 2)
+        phases, what = range(0, 5), "node exchange 1"
+    x = ranks[0]
+    x.set_wait_bound(250)
+    u = torch.from_numpy(random_initial_state(x.problem.grid, 3)).to(x.problem.device)
+    t0 = time.perf_counter()
+    for h in phases:
+        x.phase(u, h)
+    with pytest.raises(DeviceError, match=f"rank 1 did not post {what}"):
+        x.diverged()
+    assert time.perf_counter() - t0 < 20.0
+    x.reset()
+    assert x.diverged() == 0
+    for r in ranks:
+        r.close()

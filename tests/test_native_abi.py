@@ -71,3 +71,17 @@ def test_no_cpu_fallback():
 
     with pytest.raises(DeviceError):
         SphericalShallowWater(63)
+
+
+def test_library_loads_before_torch():
+    """libsdcsw.so has no link-time NCCL dependency (NCCL is bound at first use
+    to the process's own copy): loading it before torch must not shadow the
+    NCCL that libtorch_cuda needs."""
+    import subprocess
+    import sys
+
+    code = ("from paper_2403_20135_b200 import _native; _native.load(); import torch; "
+            "import torch.distributed; print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
