@@ -12,14 +12,26 @@ Driver contract:
 * ``value`` = simulated time steps per second (whole job), ``e2e`` = the same
   through the public API (``integrate`` with a host numpy state: H2D of the
   initial state and D2H of the final state inside the timed region).
-* ``roofline`` = the dominant kernel measured live with CUDA events.
-* ``cpu_baseline`` = the CPU oracle (bit-for-bit restatement of the reference
-  integrators over the CPU spherical problem) on a bounded sample of steps.
-* ``--impl reference`` times that CPU path alone, with every host thread.
+* ``roofline`` = the dominant kernel, timed live with CUDA events on the
+  states of a running simulation; ``roofline.traffic`` = that kernel's DRAM
+  bytes per launch from an ncu capture of the same config and batch
+  (``profiles/ncu_traffic_r02.json``), else null.
+* ``large_truncation`` = config c3 (T511, M=K=5) in the same run: steps/s and
+  the per-kernel stage times with their FP64-DMMA / HBM roofline fractions.
+* ``cpu_baseline`` = the CPU port (the reference integrators restated
+  bit-for-bit over the CPU spherical problem, batched-field transforms) in
+  the reference's three modes - dSDC parallel across nodes, dSDC sequential,
+  serial SDC - on the host's physical cores.
+* ``--impl reference`` times that CPU path alone (dSDC parallel across nodes,
+  every physical core), one simulated time step per bench step.
+* ``--plan-only`` prints, per config and N in 2/4/8, the node/spectral
+  partition and transport the multi-GPU run would use (no GPU needed).
 
 Multi-GPU (torchrun, N > 1): nodes are partitioned over ranks (contiguous
-blocks), one all-gather of (fe, fi) per sweep over NCCL; the simulation is the
-same, so ``scaling`` is "strong".
+blocks) with a spectral (m) split inside each node group when N > M; the
+exchanges run inside the kernels over peer memory (default) or as NCCL
+all-gathers called through the C ABI (``--transport nccl``); the simulation
+is the same, so ``scaling`` is "strong".
 """
 
 import argparse
@@ -46,6 +58,7 @@ CONFIGS = {
 }
 METRIC = "simulated steps/sec (fp64, dSDC)"
 UNIT = "steps/s"
+DATA = "synthetic (seeded n^-1.5 SH spectra, max wind 20 m/s)"
 
 
 def fp64_peak():
@@ -124,71 +137,164 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_oracle_rate(cfgname, sample_steps, threads=None):
-    """Time the CPU oracle (reference integrator restatement) on a bounded sample."""
-    from concurrent.futures import ThreadPoolExecutor
-
-    from oracle import sdc as osdc
-    from oracle.sphere_swe import SphericalShallowWaterOracle
-    from paper_2403_20135_b200 import CollocationTable, random_initial_state
-    from paper_2403_20135_b200.sphere import grid_for
-
-    c = CONFIGS[cfgname]
-    g = grid_for(c["trunc"])
-    prob = SphericalShallowWaterOracle(g.trunc, g.nlat, g.nlon)
-    table = CollocationTable.radau_right(c["nodes"])
-    u = random_initial_state(g, c["seed"])
-    ncpu = os.cpu_count() or 1
-    tt = threads if threads is not None else c["nodes"]
-    blas = max(1, ncpu // tt)
+def physical_cores():
+    """Physical cores this process may use (reference harness.py:98-114 records
+    psutil.cpu_count(logical=False)); affinity-limited when that is smaller."""
+    n = None
     try:
+        import psutil
+
+        n = psutil.cpu_count(logical=False)
+    except Exception:  # pragma: no cover
+        pass
+    n = n or os.cpu_count() or 1
+    try:
+        n = min(n, len(os.sched_getaffinity(0)))
+    except AttributeError:  # pragma: no cover
+        pass
+    return max(1, n)
+
+
+def workload_string(cfgname, nlon, nlat):
+    c = CONFIGS[cfgname]
+    s = (f"{cfgname}: T{c['trunc']} {nlon}x{nlat} M={c['nodes']} K={c['sweeps']} dt={c['dt']} s, "
+         f"{c['steps']} time steps per run")
+    if c.get("members", 1) > 1:
+        s += f", {c['members']} ensemble members, value = aggregate member-steps/s"
+    return s
+
+
+class CpuPort:
+    """The CPU path the reference runs (its integrators, restated bit-for-bit in
+    oracle/sdc.py) over the CPU spherical problem (oracle/sphere_swe.py,
+    batched-field transforms), in the reference's three modes:
+    dsdc_parallel (node updates on a pool of M threads, the paper's OpenMP
+    loop), dsdc_sequential and serial_sdc (one node after another, all cores
+    to BLAS / FFT)."""
+
+    MODES = ("dsdc_parallel", "dsdc_sequential", "serial_sdc")
+
+    def __init__(self, cfgname, cores=None):
+        from oracle import sdc as osdc
+        from oracle.sphere_swe import SphericalShallowWaterFast
+        from paper_2403_20135_b200 import CollocationTable, random_initial_state
+        from paper_2403_20135_b200.sphere import grid_for
+
+        self.osdc = osdc
+        self.c = c = CONFIGS[cfgname]
+        self.grid = grid_for(c["trunc"])
+        self.cores = cores or physical_cores()
+        self.m = c["nodes"]
+        self.table = CollocationTable.radau_right(self.m)
+        self.u0 = random_initial_state(self.grid, c["seed"])
+        g = self.grid
+        self.prob = SphericalShallowWaterFast(g.trunc, g.nlat, g.nlon, workers=self.cores)
+
+    def threads(self, mode):
+        """(time threads, BLAS/FFT threads per time thread)."""
+        if mode == "dsdc_parallel":
+            tt = min(self.m, self.cores)
+            return tt, max(1, self.cores // tt)
+        return 1, self.cores
+
+    def stepper(self, mode):
+        """A function u -> u advancing one time step in ``mode`` (a context
+        manager limits the BLAS threads; the pool lives as long as it)."""
+        import contextlib
+        from concurrent.futures import ThreadPoolExecutor
+
         from threadpoolctl import threadpool_limits
 
-        limiter = threadpool_limits(limits=blas)
-    except Exception:  # pragma: no cover
-        limiter = None
-    pool = ThreadPoolExecutor(max_workers=tt) if tt > 1 else None
-    try:
-        u = osdc.dsdc(prob, u, c["dt"], table, c["sweeps"], pool=pool, threads=tt)  # warm-up
-        t0 = time.perf_counter()
-        for _ in range(sample_steps):
-            u = osdc.dsdc(prob, u, c["dt"], table, c["sweeps"], pool=pool, threads=tt)
-        wall = time.perf_counter() - t0
-    finally:
-        if pool is not None:
-            pool.shutdown()
-        if limiter is not None:
-            limiter.unregister() if hasattr(limiter, "unregister") else None
-    cores = min(ncpu, tt * blas)
-    return sample_steps / wall, cores, wall
+        c, osdc = self.c, self.osdc
+        tt, blas = self.threads(mode)
+        self.prob.workers = blas
+
+        @contextlib.contextmanager
+        def ctx():
+            pool = ThreadPoolExecutor(max_workers=tt) if tt > 1 else None
+            try:
+                with threadpool_limits(limits=blas):
+                    if mode == "serial_sdc":
+                        yield lambda u: osdc.serial_sdc(self.prob, u, c["dt"], self.table, c["sweeps"])
+                    else:
+                        yield lambda u: osdc.dsdc(self.prob, u, c["dt"], self.table, c["sweeps"],
+                                                  pool=pool, threads=tt)
+            finally:
+                if pool is not None:
+                    pool.shutdown()
+        return ctx()
+
+    def rate(self, mode, warm=2, reps=3):
+        """Steps/s of ``mode``: ``warm`` untimed steps, then the minimum over
+        ``reps`` timed single steps (reference bench/harness.py:316, 427-436)."""
+        with self.stepper(mode) as step:
+            u = self.u0
+            for _ in range(warm):
+                u = step(u)
+            best = float("inf")
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                u = step(u)
+                best = min(best, time.perf_counter() - t0)
+        return 1.0 / best
+
+
+def cpu_baseline_modes(cfgname):
+    """cpu_baseline of the GPU arm: the three reference modes on the host's physical cores."""
+    port = CpuPort(cfgname)
+    t0 = time.perf_counter()
+    rates = {mode: port.rate(mode) for mode in CpuPort.MODES}
+    wall = time.perf_counter() - t0
+    c = CONFIGS[cfgname]
+    return {
+        "value": rates["dsdc_parallel"], "unit": UNIT, "cores": port.cores, "kind": "port",
+        "modes": {k: {"steps_per_s": v, "time_threads": port.threads(k)[0],
+                      "blas_threads": port.threads(k)[1]} for k, v in rates.items()},
+        "dsdc_parallel_vs_serial": rates["dsdc_parallel"] / rates["serial_sdc"],
+        "sample": (f"per mode 2 warm-up + min of 3 single {cfgname} steps (of {c['steps']}), "
+                   f"{wall:.1f} s total; oracle/sdc.py (bit-exact restatement of the reference "
+                   "integrators) over oracle/sphere_swe.py SphericalShallowWaterFast; "
+                   f"{port.cores} physical cores"),
+    }
 
 
 def run_reference(args):
+    """The reference arm: the CPU port in the reference's dSDC mode (nodes on a
+    pool of M threads, BLAS/FFT on the remaining physical cores), one simulated
+    time step of the workload per bench step; every number below is timed."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     c = CONFIGS[args.config]
-    sample = max(1, args.ref_sample)
-    rates = []
-    cores = 1
-    for _ in range(max(0, args.warmup)):
-        pass  # the oracle rate function warms itself up once
-    for _ in range(max(1, args.steps)):
-        r, cores, _ = cpu_oracle_rate(args.config, sample)
-        rates.append(r)
-    value = float(np.median(rates))
+    port = CpuPort(args.config)
+    g = port.grid
+    with port.stepper("dsdc_parallel") as step:
+        u = port.u0
+        for _ in range(max(0, args.warmup)):
+            u = step(u)
+        times = []
+        for _ in range(max(1, args.steps)):
+            t0 = time.perf_counter()
+            u = step(u)
+            times.append(time.perf_counter() - t0)
+    total = float(sum(times))
+    value = len(times) / total
+    tt, blas = port.threads("dsdc_parallel")
+    sample = (f"one simulated dSDC time step of {args.config} per bench step ({args.steps} timed after "
+              f"{args.warmup} warm-up steps, {total:.2f} s timed; a full run is {c['steps']} steps); "
+              "oracle/sdc.py (bit-exact restatement of the reference integrators) over "
+              f"oracle/sphere_swe.py SphericalShallowWaterFast; {tt} time threads x {blas} BLAS/FFT threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 / value * c["steps"], "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded n^-1.5 spectra)",
-        "config": {"workload": f"{args.config}: T{c['trunc']} M={c['nodes']} K={c['sweeps']} "
-                               f"dt={c['dt']} x{c['steps']} steps", "parallelism": "cpu"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{sample} dSDC steps per bench step (of {c['steps']}); "
-                                   "reference integrator restated bit-for-bit (oracle/sdc.py), "
-                                   "CPU spherical problem oracle/sphere_swe.py, "
-                                   f"{c['nodes']} time threads"},
+        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
+        "ms_per_step": total / len(times) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": {"workload": workload_string(args.config, g.nlon, g.nlat),
+                   "bench_step": "one simulated time step (bounded CPU sample of the run)",
+                   "parallelism": f"cpu: {tt} time threads x {blas} BLAS/FFT threads",
+                   "min_ms_per_step": min(times) * 1e3},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": port.cores, "kind": "port",
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -196,9 +302,8 @@ def run_reference(args):
 
 
 def time_stage(problem, stage, nb, reps=50):
-    """Average device duration (s) of one f_E stage launch, CUDA events on its stream."""
-    import ctypes
-
+    """Experiment tools only (tools/): device time (s) of one f_E stage launch on
+    zeroed states.  The bench's own numbers come from live_stage_times."""
     import torch
 
     from paper_2403_20135_b200 import _native
@@ -208,7 +313,7 @@ def time_stage(problem, stage, nb, reps=50):
     out = problem.empty_states(nb)
     lib = problem._lib
     s = problem.stream()
-    if stage == 3:  # synthesis alone (as in the step graph): prepare its operand once
+    if stage == 3:
         _native.check(lib.sdcsw_transform_stage(problem.handle, 0, u.data_ptr(), out.data_ptr(), nb, s))
     for _ in range(5):
         _native.check(lib.sdcsw_transform_stage(problem.handle, stage, u.data_ptr(), out.data_ptr(), nb, s))
@@ -220,52 +325,266 @@ def time_stage(problem, stage, nb, reps=50):
         lib.sdcsw_transform_stage(problem.handle, stage, u.data_ptr(), out.data_ptr(), nb, s)
     e1.record(stream)
     e1.synchronize()
-    del ctypes
     return e0.elapsed_time(e1) * 1e-3 / reps
 
 
-def stage_roofline(problem, c, members=1, fused=False):
-    """Per-stage time per simulated step; roofline of the dominant kernel.
+STAGE_NAMES = {3: "legendre_synthesis", 1: "ring_fft_products", 2: "legendre_analysis",
+               4: "legendre_analysis"}
 
-    The sweep launches carry nodes x members states, the init launch members.
-    ``fused``: the step runs the analysis with the node-update epilogue
-    (transform stage 4), so that is the kernel timed for the analysis."""
-    k = c["sweeps"]
-    m = c["nodes"] * members
-    one = members
+
+def stage_work(problem, name, nb):
+    """Algorithmic work of one launch over nb states: (amount, unit, bound).
+
+    Legendre GEMMs: 24 C J nb flop (synthesis) and 28 C J nb (analysis), C =
+    (T+1)(T+2)/2, J = nlat/2.  Ring kernel: 4 Fourier
+    fields in and 5 product fields out, 16 B per complex value, nlat (T+1)
+    values per field and state."""
     g = problem.grid
     cc, j, ll = g.n_coef, g.nlat // 2, g.trunc + 1
-    # algorithmic work per launch for a batch of nb states
-    flops = {0: lambda nb: 24.0 * cc * j * nb, 2: lambda nb: 28.0 * cc * j * nb}
-    ring_bytes = lambda nb: (8 + 14) * 16.0 * j * ll * nb  # noqa: E731  read Fourier, write analysis data
-    per_step = {}
-    detail = {}
-    for stage, name in ((3, "legendre_synthesis"), (1, "ring_fft_products"),
-                        (4 if fused else 2, "legendre_analysis")):
-        t1 = time_stage(problem, stage, one)
-        tm = time_stage(problem, stage, m)
-        per_step[name] = t1 + (k - 1) * tm
-        detail[name] = {f"us_nb{one}": t1 * 1e6, f"us_nb{m}": tm * 1e6}
-    dom = max(per_step, key=per_step.get)
-    tm = detail[dom][f"us_nb{m}"] * 1e-6
-    if dom == "ring_fft_products":
+    if name == "legendre_synthesis":
+        return 24.0 * cc * j * nb, "flop", "tensor"
+    if name == "legendre_analysis":
+        return 28.0 * cc * j * nb, "flop", "tensor"
+    return 9.0 * 16.0 * g.nlat * ll * nb, "B", "hbm"
+
+
+def live_stage_times(problem, states, fused=False, reps=30):
+    """Average device time (s) per launch of each f_E stage kernel on the live
+    states ``states`` (a running simulation's; nb = len(states)).  The whole
+    f_E runs once first so every workspace holds live data; each stage is
+    then launched ``reps`` times back to back between CUDA events on its own
+    stream.  ``fused``: the analysis timed is the step's fused node-update
+    epilogue variant (stage 4; last, since it rewrites the operand)."""
+    import torch
+
+    from paper_2403_20135_b200 import _native
+
+    nb = states.shape[0]
+    lib, s = problem._lib, problem.stream()
+    out = problem.empty_states(nb)
+    fi = problem.empty_states(nb)
+
+    def launch(stage):
+        dst = fi if stage == 4 else out
+        return lib.sdcsw_transform_stage(problem.handle, stage, states.data_ptr(), dst.data_ptr(), nb, s)
+
+    for stage in (0, 1, 2):
+        _native.check(launch(stage), "sdcsw_transform_stage")
+    if fused:
+        problem.f_impl_device(states, fi, nb)
+    stream = torch.cuda.current_stream(problem.device)
+    times = {}
+    for stage in (3, 1, 4 if fused else 2):
+        for _ in range(3):
+            _native.check(launch(stage), "sdcsw_transform_stage")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            launch(stage)
+        e1.record(stream)
+        e1.synchronize()
+        times[STAGE_NAMES[stage]] = e0.elapsed_time(e1) * 1e-3 / reps
+    return times
+
+
+def roofline_of(problem, name, nb, seconds, cfgname, fused=False):
+    work, unit, bound = stage_work(problem, name, nb)
+    if bound == "hbm":
         peak, src = hbm_peak()
-        ach = ring_bytes(m) / tm / 1e9
+        ach = work / seconds / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "peak_source": src}
+                "peak_source": src, "algorithmic_bytes": work}
     else:
-        st = 0 if dom == "legendre_synthesis" else 2
         peak, src = fp64_peak()
-        ach = flops[st](m) / tm / 1e12
-        roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                "frac": ach / peak, "peak_source": src + " (FP64 DMMA)"}
-    roof.update({"kernel": dom, "launch_nb": m, "us_per_launch": tm * 1e6, "traffic": None})
-    traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(traffic_path):
-        with open(traffic_path) as f:
-            tr = json.load(f)
-        roof["traffic"] = tr.get(dom)
+        ach = work / seconds / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "peak_source": src + " (FP64 DMMA)", "algorithmic_flop": work}
+    tname = name + ("_fused" if fused and name == "legendre_analysis" else "")
+    roof.update({"kernel": tname, "launch_nb": nb, "us_per_launch": seconds * 1e6,
+                 "traffic": measured_traffic(cfgname, tname, nb)})
+    return roof
+
+
+def measured_traffic(cfgname, name, nb):
+    """DRAM bytes (read + write) per launch of this kernel at this config and
+    batch from an ncu --set full capture (profiles/ncu_traffic_r02.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        tr = json.load(f)
+    return tr.get(cfgname, {}).get(f"{name}:nb{nb}")
+
+
+def live_states(stepper, u, n):
+    """n consecutive states of a running simulation (one step apart), starting at u."""
+    import torch
+
+    out = [u.clone()]
+    x = u.clone()
+    for _ in range(n - 1):
+        stepper.run(x, 1, use_graph=False)
+        out.append(x.clone())
+    torch.cuda.synchronize()
+    return out
+
+
+def stage_roofline(problem, c, cfgname, stepper, u, members=1, fused=False):
+    """Per-stage time per simulated step (live states) and the roofline of the
+    dominant kernel.  Sweep launches carry nodes x members states, the init
+    launch members."""
+    import torch
+
+    k = c["sweeps"]
+    m = c["nodes"] * members
+    seq = live_states(stepper, u, c["nodes"])
+    one_b = seq[0].reshape(members, -1).contiguous()
+    many = torch.cat([x.reshape(members, -1) for x in seq]).contiguous()
+    t1 = live_stage_times(problem, one_b)
+    tm = live_stage_times(problem, many, fused=fused)
+    per_step = {n: t1[n] + (k - 1) * tm[n] for n in tm}
+    detail = {n: {f"us_nb{members}": t1[n] * 1e6, f"us_nb{m}": tm[n] * 1e6} for n in tm}
+    dom = max(per_step, key=per_step.get)
+    roof = roofline_of(problem, dom, m, tm[dom], cfgname, fused)
     return roof, {n: v * 1e6 for n, v in per_step.items()}, detail
+
+
+def large_truncation_block(cfgname="c3", n_steps=20, warmup=3):
+    """Config c3 (T511, M = K = 5) in the same bench run: device-timed steps/s
+    (state resident in HBM, CUDA graphs) and every stage kernel of a live step
+    against its roofline (Legendre GEMMs: FP64 DMMA; ring, sweep-node and
+    final-node kernels: HBM)."""
+    import torch
+
+    from paper_2403_20135_b200 import CollocationTable, SdcConfig, SweepMode, random_initial_state
+    from paper_2403_20135_b200.integrators import DeviceStepper, diagonal_step_coefficients
+    from paper_2403_20135_b200.parallel_nodes import CudaNodeBackend
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    c = CONFIGS[cfgname]
+    mm, kk = c["nodes"], c["sweeps"]
+    t_setup = time.perf_counter()
+    p = SphericalShallowWater(c["trunc"], max_batch=mm)
+    cfg = SdcConfig(table=CollocationTable.radau_right(mm), n_sweeps=kk, mode=SweepMode.DIAGONAL_PARALLEL)
+    st = DeviceStepper(p, cfg, c["dt"], serial=False)
+    u = p._to_device(random_initial_state(p.grid, c["seed"])).reshape(-1).contiguous()
+    st.run(u, warmup)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t_setup
+    stream = torch.cuda.current_stream(p.device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    st.run(u, n_steps)
+    e1.record(stream)
+    e1.synchronize()
+    t_steps = e0.elapsed_time(e1) * 1e-3
+    rate = n_steps / t_steps
+    seq = live_states(st, u, mm)
+    many = torch.stack(seq).contiguous()
+    t1 = live_stage_times(p, seq[0].reshape(1, -1).contiguous())
+    tm = live_stage_times(p, many)
+    stages = {}
+    for name in tm:
+        stages[name] = {"nb1": roofline_of(p, name, 1, t1[name], cfgname),
+                        f"nb{mm}": roofline_of(p, name, mm, tm[name], cfgname)}
+    # node kernels on live tendencies: the sweep's nodes and the closing solve
+    fe, fi = p.empty_states(mm), p.empty_states(mm)
+    p.f_expl_device(many, fe, mm)
+    p.f_impl_device(many, fi, mm)
+    coef = diagonal_step_coefficients(cfg, c["dt"], p.mean_geopotential)
+    blk = mm * (mm + 4)
+    sc = np.ascontiguousarray(coef[:blk])
+    fc = np.ascontiguousarray(coef[(kk - 1) * blk:])
+    b = CudaNodeBackend(p)
+    uo, fo, one = p.empty_states(mm), p.empty_states(mm), p.empty_states(1)
+    sbytes = p.state_size * 16.0
+
+    def timed(fn, reps=20):
+        for _ in range(3):
+            fn()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(reps):
+            fn()
+        a1.record(stream)
+        a1.synchronize()
+        return a0.elapsed_time(a1) * 1e-3 / reps
+
+    peak, src = hbm_peak()
+    for name, fn, nbytes in (
+            ("sweep_nodes", lambda: b.sweep_nodes(mm, 0, mm, sc, seq[0], fe, 1, fi, 1, False, uo, fo),
+             (1 + 2 * mm) * sbytes + 2 * mm * sbytes),
+            ("final_node", lambda: b.final_node(mm, fc, seq[0], fe, 1, fi, 1, False, one),
+             (2 * mm + 2) * sbytes)):
+        t = timed(fn)
+        stages[name] = {f"nb{mm}": {"bound": "hbm", "achieved": nbytes / t / 1e9, "peak": peak,
+                                     "unit": "GB/s", "frac": nbytes / t / 1e9 / peak, "peak_source": src,
+                                     "algorithmic_bytes": nbytes, "kernel": name, "us_per_launch": t * 1e6,
+                                     "traffic": measured_traffic(cfgname, name, mm)}}
+    per_step_us = {n: (t1[n] + (kk - 1) * tm[n]) * 1e6 for n in tm}
+    per_step_us["sweep_nodes"] = (kk - 1) * stages["sweep_nodes"][f"nb{mm}"]["us_per_launch"]
+    per_step_us["final_node"] = stages["final_node"][f"nb{mm}"]["us_per_launch"]
+    st.close()
+    p.close()
+    return {
+        "workload": workload_string(cfgname, p.grid.nlon, p.grid.nlat),
+        "steps_per_s": rate, "ms_per_sim_step": t_steps / n_steps * 1e3,
+        "node_sweeps_per_s": rate * ((kk - 1) * mm + 1),
+        "timed": f"{n_steps} steps (CUDA graphs, state in HBM) after {warmup} warm-up steps",
+        "stages": stages, "stage_us_per_sim_step": per_step_us,
+        "setup_s": setup,
+        "note": "stage kernels timed on live states of this run (consecutive time steps), "
+                "CUDA events on the launching stream; fractions are algorithmic work over the "
+                "measured peaks (FP64 DMMA profiles/fp64_peak.json, HBM MEASURED_PEAKS.json)",
+    }
+
+
+def partition_plan(cfgname, world):
+    """The multi-GPU layout bench.py uses for ``cfgname`` on ``world`` GPUs (the
+    same rules as run_device): ensemble members sharded with nodes local, else
+    G node groups (the largest divisor of N that is <= M; G = 1 from T400, so
+    every GEMM keeps all nodes batched) x S = N / G spectral parts."""
+    from paper_2403_20135_b200.parallel_nodes import node_block, spectral_parts
+    from paper_2403_20135_b200.sphere import grid_for
+
+    c = CONFIGS[cfgname]
+    g = grid_for(c["trunc"])
+    mm = c["nodes"]
+    state_bytes = 3 * g.n_coef * 16
+    if c.get("members", 1) > 1:
+        per = c["members"] // world if c["members"] % world == 0 else None
+        return {"layout": "ensemble members sharded, nodes local (replicas, no collective)",
+                "members_per_gpu": per, "exchange": None}
+    groups = max(q for q in range(1, min(world, mm) + 1) if world % q == 0)
+    if c["trunc"] >= 400:
+        groups = 1
+    parts = world // groups
+    owned = spectral_parts(c["trunc"], parts)
+    coef_per_part = [int(sum(c_ for m, c_ in enumerate(range(c["trunc"] + 1, 0, -1)) if owned[m] == q))
+                     for q in range(parts)]
+    blocks = [node_block(mm, groups, q)[:2] for q in range(groups)]
+    lp = max(owned.count(q) for q in range(parts))
+    own_frac = max(coef_per_part) / g.n_coef
+    node_x = 2 * max(b[1] for b in blocks) * state_bytes * own_frac
+    four_x = 8 * 16 * (g.nlat // 2) * lp * max(b[1] for b in blocks)
+    return {
+        "node_groups": groups, "spectral_parts": parts,
+        "rank_layout": "rank r -> node group r // S, spectral part r % S",
+        "node_blocks": [{"node_lo": lo, "count": n} for lo, n in blocks],
+        "wavenumbers_per_part": [owned.count(q) for q in range(parts)],
+        "coefficients_per_part": coef_per_part,
+        "transport": "peer memory (analysis epilogue / split synthesis stores + device flags); "
+                     "NCCL through the C ABI if any rank cannot map its peers",
+        "node_exchange_bytes_per_rank_per_sweep": node_x if groups > 1 else 0,
+        "fourier_exchange_bytes_per_rank_per_fe": four_x if parts > 1 else 0,
+    }
+
+
+def plan_only():
+    out = {"plan_only": True,
+           "configs": {name: {str(n): partition_plan(name, n) for n in (2, 4, 8)} for name in CONFIGS}}
+    print(json.dumps(out), flush=True)
+    return 0
 
 
 def run_device(args):
@@ -476,33 +795,35 @@ def run_device(args):
         e1.synchronize()
         serial_rate = nsteps / (e0.elapsed_time(e1) * 1e-3)
         sst.close()
+        # --- stage kernels on live states against their rooflines
         fused = (not ensemble and world == 1
                  and launches_per_sim_step == 3 * k_sw)  # node updates in the analysis epilogue
-        roof, stage_us, stage_detail = stage_roofline(aux, c, members, fused)
+        dcfg = SdcConfig(table=table, n_sweeps=k_sw, mode=SweepMode.DIAGONAL_PARALLEL)
+        rst = DeviceStepper(aux, dcfg, dt, serial=False, members=members)
+        live = u.clone() if ensemble else us  # the state of a running simulation (unsplit)
+        roof, stage_us, stage_detail = stage_roofline(aux, c, args.config, rst, live, members, fused)
+        rst.close()
+        large = None
+        if world == 1 and not args.no_large:
+            large = large_truncation_block("c3")
         cpu = None
         if world == 1 and not args.no_cpu and not ensemble:
-            r, cores, wall = cpu_oracle_rate(args.config, args.cpu_sample)
-            cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",
-                   "sample": f"{args.cpu_sample} dSDC steps of {args.config} (of {nsteps}) after 1 "
-                             f"warm-up step, {wall:.1f} s; oracle/sdc.py (bit-exact restatement of "
-                             "the reference integrators) over oracle/sphere_swe.py"}
+            cpu = cpu_baseline_modes(args.config)
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
             "higher_is_better": True,
             "scaling": "weak" if ensemble else "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded n^-1.5 SH spectra, max wind 20 m/s)",
+            "vs_baseline": None, "dtype": "f64", "data": DATA,
             "config": {
-                "workload": f"{args.config}: T{c['trunc']} {problem.grid.nlon}x{problem.grid.nlat} "
-                            f"M={m_nodes} K={k_sw} dt={dt} s, {nsteps} time steps per bench step"
-                            + (f", {total_members} ensemble members ({members} per GPU), value = aggregate member-steps/s"
-                               if ensemble else ""),
+                "workload": workload_string(args.config, problem.grid.nlon, problem.grid.nlat)
+                            + (f" ({members} per GPU)" if ensemble else ""),
                 "bench_step": f"one full {nsteps}-step run", "l2": "flushed between bench steps (256 MiB write, untimed)",
                 "parallelism": ("1 GPU: M nodes as concurrent graph branches / batched GEMM columns" if world == 1 and not multi
                                 else f"{world} GPUs: ensemble members sharded" if ensemble
                                 else (f"{world} GPUs: node blocks x spectral (m) split; (f_E, f_I) and Fourier parts exchanged over peer memory by the analysis epilogue / split synthesis (no NCCL on the data path)"
                                       if transport == "p2p"
-                                      else f"{world} GPUs: node blocks x spectral (m) split, NCCL all-gathers per sweep / per f_E")),
+                                      else f"{world} GPUs: node blocks x spectral (m) split, NCCL all-gathers through the C ABI (sdcsw_allgather_rhs) per sweep / per f_E")),
                 "ms_per_sim_step": t_dev / sim_steps * 1e3,
                 "node_sweeps_per_s": value * node_sweeps,
                 "serial_sdc_steps_per_s_1gpu": serial_rate,
@@ -512,6 +833,7 @@ def run_device(args):
                 "multi_gpu_transport": transport if multi else None,
             },
             "roofline": roof,
+            "large_truncation": large,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches_per_sim_step * sim_steps),
@@ -532,15 +854,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-sample", type=int, default=4, help="CPU-baseline dSDC steps")
-    ap.add_argument("--ref-sample", type=int, default=4, help="reference-arm dSDC steps per bench step")
-    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--no-large", action="store_true", help="skip the c3 (T511) block")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="print the multi-GPU partition / transport per config and N (no GPU)")
     ap.add_argument("--node-parallel", action="store_true",
                     help="use the multi-GPU node/spectral orchestration even at world size 1 "
                          "(exercises the N>1 code path on one GPU)")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="multi-GPU exchanges: kernels over peer memory (default) or NCCL all-gathers")
     args = ap.parse_args()
+    if args.plan_only:
+        return plan_only()
     if args.impl == "reference":
         return run_reference(args)
     return run_device(args)

@@ -228,3 +228,127 @@ def relative_l2(a, b, problem):
         den = np.sqrt(np.sum(wgt * np.abs(y) ** 2))
         out.append(num / den if den > 0 else num)
     return out
+
+
+class SphericalShallowWaterFast(SphericalShallowWaterOracle):
+    """The same problem with the transforms organised the way a CPU spectral
+    model runs them (the timed CPU baseline of ``bench.py``; SWEET's SHTns
+    backend, ``PAPER.md:171``, is not available here):
+
+    * Legendre synthesis of all fields sharing a table in one matrix product
+      per wavenumber (P: zeta, Phi', i m chi, i m psi; H: psi, chi), analysis
+      likewise (P: A, B, C, D, KE; H: A, B, D) - 4 table passes per f_E
+      instead of 14;
+    * N/S folding: only the northern half of each table is read, the southern
+      rings follow from parity (P(-mu) = (-1)^(n-m) P(mu), H with the opposite
+      sign);
+    * stacked FFTs (``scipy.fft`` with ``workers`` threads).
+
+    Same algorithm and operators as :class:`SphericalShallowWaterOracle`; the
+    sums are ordered differently, so results agree to rounding (tested at
+    1e-13), not bit for bit."""
+
+    def __init__(self, *args, workers=1, **kw):
+        super().__init__(*args, **kw)
+        self.workers = int(workers)
+        half = self.nlat // 2
+        # coefficients permuted so that each wavenumber's even (n - m) rows and
+        # then its odd rows are contiguous; tables (northern half) in that order
+        even = (self.n_of - self.m_of) % 2 == 0
+        perm, self.esl, self.osl, pos = [], [], [], 0
+        for m in range(self.trunc + 1):
+            idx = np.arange(self.bounds[m], self.bounds[m + 1])
+            e, o = idx[even[idx]], idx[~even[idx]]
+            perm += [e, o]
+            self.esl.append(slice(pos, pos + e.size))
+            self.osl.append(slice(pos + e.size, pos + e.size + o.size))
+            pos += idx.size
+        self.perm = np.concatenate(perm)
+        self.pp = np.ascontiguousarray(self.p[self.perm, :half])
+        self.hp = np.ascontiguousarray(self.h[self.perm, :half])
+
+    def _synth(self, xp, xh):
+        """xp [C, kp], xh [C, kh] complex -> Fourier [kp + kh, nlat, nlon/2+1]
+        (rows: P fields, then H fields); real matrix products per wavenumber."""
+        half = self.nlat // 2
+        kp, kh = xp.shape[1], xh.shape[1]
+        rp = np.ascontiguousarray(xp[self.perm]).view(np.float64)  # [C, 2 kp] (re, im)
+        rh = np.ascontiguousarray(xh[self.perm]).view(np.float64)
+        fn = np.zeros((self.trunc + 1, 2, kp + kh, 2, half))  # [m][N/S][field][re/im][lat]
+        for m in range(self.trunc + 1):
+            e, o = self.esl[m], self.osl[m]
+            pe = (rp[e].T @ self.pp[e]).reshape(kp, 2, half)
+            po = (rp[o].T @ self.pp[o]).reshape(kp, 2, half)
+            he = (rh[e].T @ self.hp[e]).reshape(kh, 2, half)
+            ho = (rh[o].T @ self.hp[o]).reshape(kh, 2, half)
+            # P: even n-m symmetric about the equator; H: even n-m antisymmetric
+            fn[m, 0, :kp], fn[m, 1, :kp] = pe + po, pe - po
+            fn[m, 0, kp:], fn[m, 1, kp:] = he + ho, ho - he
+        out = np.zeros((kp + kh, self.nlat, self.nlon // 2 + 1), dtype=complex)
+        f = fn[..., 0, :] + 1j * fn[..., 1, :]  # [m][N/S][field][lat]
+        out[:, :half, : self.trunc + 1] = f[:, 0].transpose(1, 2, 0)
+        out[:, half:, : self.trunc + 1] = f[:, 1].transpose(1, 2, 0)[:, ::-1]
+        return out
+
+    def _anal(self, gp, gh):
+        """Weighted Fourier data gp [kp, nlat, T+1], gh [kh, nlat, T+1] ->
+        coefficients [C, kp] (P) and [C, kh] (H)."""
+        half = self.nlat // 2
+
+        def fold(g):  # -> symmetric / antisymmetric parts as [m][lat][2 k] real
+            s_ = g[:, :half] + g[:, half:][:, ::-1]
+            a_ = g[:, :half] - g[:, half:][:, ::-1]
+            return (np.ascontiguousarray(s_.transpose(2, 1, 0)).view(np.float64),
+                    np.ascontiguousarray(a_.transpose(2, 1, 0)).view(np.float64))
+
+        sp_, ap_ = fold(gp)
+        sh_, ah_ = fold(gh)
+        cp = np.empty((self.n_coef, 2 * gp.shape[0]))
+        ch = np.empty((self.n_coef, 2 * gh.shape[0]))
+        for m in range(self.trunc + 1):
+            e, o = self.esl[m], self.osl[m]
+            cp[e] = self.pp[e] @ sp_[m]
+            cp[o] = self.pp[o] @ ap_[m]
+            ch[e] = self.hp[e] @ ah_[m]
+            ch[o] = self.hp[o] @ sh_[m]
+        out_p = np.empty((self.n_coef, gp.shape[0]), dtype=complex)
+        out_h = np.empty((self.n_coef, gh.shape[0]), dtype=complex)
+        out_p[self.perm] = cp.view(complex)
+        out_h[self.perm] = ch.view(complex)
+        return out_p, out_h
+
+    def _f_expl(self, state):
+        import scipy.fft as sfft
+
+        phi, zeta, delta = self.views(state)
+        a = self.radius
+        psi, chi = -zeta * self.inv_lam, -delta * self.inv_lam
+        im = 1j * self.m_of
+        four = self._synth(np.stack([zeta, phi, im * chi, im * psi], axis=1),
+                           np.stack([psi, chi], axis=1))
+        zf, pf = four[0], four[1]
+        uf = (four[2] - four[4]) / a
+        vf = (four[3] + four[5]) / a
+        g = sfft.irfft(np.stack([uf, vf, zf, pf]) * self.nlon, n=self.nlon, axis=-1, workers=self.workers)
+        ug, vg, zg, pg = g
+        eta = zg + (2.0 * self.omega * self.mu)[:, None]
+        prods = np.stack([eta * ug, eta * vg, pg * ug, pg * vg,
+                          (ug * ug + vg * vg) / (2.0 * self.coslat2)[:, None]])
+        fa, fb, fc, fd, fke = sfft.rfft(prods, axis=-1, workers=self.workers)[:, :, : self.trunc + 1] / self.nlon
+        wc = (2.0 * np.pi * self.w / self.coslat2)[:, None]
+        wk = (2.0 * np.pi * self.w)[:, None]
+        cp, ch = self._anal(np.stack([fa * wc, fb * wc, fc * wc, fke * wk]),
+                            np.stack([fa * wc, fb * wc, fd * wc]))
+        div_mass = (im * cp[:, 2] - ch[:, 2]) / a
+        div_abs = (im * cp[:, 0] - ch[:, 1]) / a
+        curl_abs = (im * cp[:, 1] + ch[:, 0]) / a
+        out = np.empty(self.state_size, dtype=complex)
+        c = self.n_coef
+        out[:c] = -div_mass
+        out[c : 2 * c] = -div_abs
+        out[2 * c :] = curl_abs + self.lam * cp[:, 3]
+        real_m0 = self.m_of == 0
+        for k in range(3):
+            seg = out[k * c : (k + 1) * c]
+            seg[real_m0] = seg[real_m0].real
+        return out
