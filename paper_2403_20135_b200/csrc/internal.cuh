@@ -85,13 +85,14 @@ struct Plan {
   int syn_bulk;           // CTA-staged bulk-copy synthesis (T >= 400): 1 / 0 / -1 = automatic
   FftPlan fft;
   // workspaces
-  double2* fsyn;    // [max_batch][J][L][4][2]
+  double2* fsyn;    // [max_batch][J][4 fields][L][2 (N, S)]
   double2* gan;     // [max_batch][L][J][2 (S,A)][kNumSlots]  (GEMM-ready for the analysis)
   double* coef_dev; // small per-call coefficient staging [kCoefCap]
   double* xsyn;     // [rows][max_batch][12] synthesis B operand for API calls
   int xsyn_nb;      // record batch of the last API prep (padding rows zero for it)
   int fe_chunk;     // f_E batch chunk keeping the Fourier workspaces L2-resident (0 = no chunking)
   int ring_threads;
+  int ringp;        // persistent ring kernel: -1 automatic (many waves), 1 forced, 0 off
   size_t ring_smem;
   // TMA tensor maps (CUtensorMap, 128 B each) over the P / H tables for the
   // table-streaming analysis (T >= 400); tma_ok = maps built
@@ -109,7 +110,7 @@ struct Plan {
   int n_own_work;
   int* own_idx;     // own coefficient indices, ascending
   int n_own_idx;
-  double2* fsyn_ext;  // part-major Fourier buffer [S][nb][J][Lp][4][2] (caller-owned)
+  double2* fsyn_ext;  // part-major Fourier buffer [S][nb][J][4][Lp][2] (caller-owned)
   // planar problem (kind 1): N x N grid, spectra [N (kx)][NH = N/2 + 1 (ky)],
   // C = N * NH coefficients per field (lam = k^2 = laplacian symbol)
   int pn, pnh;
@@ -302,6 +303,42 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// mbarrier / bulk-copy helpers (TMA engine; legendre_tma.cu, ring_fft.cu)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

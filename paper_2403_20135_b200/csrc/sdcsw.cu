@@ -32,6 +32,7 @@ int cuda_status(cudaError_t e, const char* where) {
 cudaError_t configure_ring(size_t smem);
 size_t ring_smem_bytes(int nlon);
 bool ring_pass_twiddles(int nlon, const double2* w, std::vector<double2>& out);
+
 bool ring_supported(int nlon);
 
 cudaError_t f_expl_prepped(const Plan& p, const Work& w, const double* xsyn, double2* fe, int nb,
@@ -234,6 +235,8 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   }
   p.n_anal_work4 = (int)work4.size();
   p.ring_threads = 256;
+  p.ringp = -1;
+  if (const char* env = getenv("SDCSW_RINGP")) p.ringp = atoi(env);
   p.ring_smem = ring_smem_bytes(nlon);
   std::vector<double2> twp;
   ring_pass_twiddles(nlon, tw.data(), twp);
