@@ -180,6 +180,28 @@ int sdcsw_stepper_set_option(sdcsw_stepper* st, int option, int value);
  * serial SDC; n >= K + 1.  Synchronises. */
 int sdcsw_stepper_profile(sdcsw_stepper* st, double* u, double* stage_ms, int n, void* stream);
 
+/* One step stage by stage (as sdcsw_stepper_profile, one member) with a host
+ * callback after every sweep: hook(user, k) runs after sweep k (dSDC: k = 1 ..
+ * K-1, before the closing solve; serial SDC: k = 1 .. K) has completed on the
+ * device, before the next sweep is enqueued, so the callback may read the
+ * sweep's buffers (sdcsw_stepper_sweep_state).  stage_ms (optional, n >= K+1)
+ * as sdcsw_stepper_profile.  Replaces the on_sweep(k, state) callback of
+ * dsdc_step / sdc_step_serial (integrators.py:317-381).  Synchronises. */
+typedef void (*sdcsw_sweep_hook)(void* user, int sweep);
+int sdcsw_stepper_step_hooked(sdcsw_stepper* st, double* u, sdcsw_sweep_hook hook, void* user,
+                              double* stage_ms, int n, void* stream);
+/* Device buffers holding sweep k's tendencies (valid inside the hook of sweep
+ * k): fe0 = f_E(u0) (one state), fe / fi = f_E, f_I of the M nodes (M
+ * consecutive states).  The node states themselves are not retained (the
+ * reference drops them too, integrators.py:233-246); f_I(u0) is recomputed. */
+int sdcsw_stepper_sweep_state(sdcsw_stepper* st, int sweep, void** fe0, void** fe, void** fi);
+/* Sweep storage of the stepper (the analogue of the reference's storage
+ * accounting, tests/test_acceptance.py:284-305): bytes of device memory it owns
+ * and the number of state-sized buffers among them (per member: fe0 and two
+ * generations of the M nodes' fe, fi = 1 + 4M; plus node states where an f_E
+ * reads them, and the serial-SDC quadrature / correction). */
+int sdcsw_stepper_storage(sdcsw_stepper* st, long long* bytes, long long* state_buffers);
+
 /* Number of kernels one step launches (for the bench's gpu_launches). */
 int sdcsw_stepper_launches_per_step(sdcsw_stepper* st, int* n);
 

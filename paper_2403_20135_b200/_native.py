@@ -14,6 +14,7 @@ LIB_PATH = os.environ.get("SDCSW_LIB_PATH") or os.path.join(
 
 SDCSW_OK, SDCSW_ERR_PARAM, SDCSW_ERR_CUDA, SDCSW_ERR_STATE, SDCSW_ERR_DIVERGED, SDCSW_ERR_PEER = range(6)
 IPC_HANDLE_BYTES = 64  # SDCSW_IPC_HANDLE_BYTES
+SWEEP_HOOK = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int)  # sdcsw_sweep_hook
 COMM_ID_BYTES = 128  # SDCSW_COMM_ID_BYTES
 
 EXPORTS = (
@@ -35,6 +36,9 @@ EXPORTS = (
     "sdcsw_stepper_launches_per_step",
     "sdcsw_stepper_set_option",
     "sdcsw_stepper_profile",
+    "sdcsw_stepper_step_hooked",
+    "sdcsw_stepper_sweep_state",
+    "sdcsw_stepper_storage",
     "sdcsw_check_finite",
     "sdcsw_axpy",
     "sdcsw_transform_stage",
@@ -121,6 +125,9 @@ _SIGS = {
     "sdcsw_stepper_launches_per_step": [_p, _ip],
     "sdcsw_stepper_set_option": [_p, _i, _i],
     "sdcsw_stepper_profile": [_p, _p, _dp, _i, _p],
+    "sdcsw_stepper_step_hooked": [_p, _p, _p, _p, _dp, _i, _p],
+    "sdcsw_stepper_sweep_state": [_p, _i, ctypes.POINTER(_p), ctypes.POINTER(_p), ctypes.POINTER(_p)],
+    "sdcsw_stepper_storage": [_p, ctypes.POINTER(_ll), ctypes.POINTER(_ll)],
     "sdcsw_check_finite": [_p, _ll, _p, _p],
     "sdcsw_axpy": [_ll, _p, ctypes.c_double, _p, _p, _p],
     "sdcsw_transform_stage": [_p, _i, _p, _p, _i, _p],

@@ -106,6 +106,9 @@ struct sdcsw_stepper {
   int graph_steps;
   double* graph_u;
   int launches;
+  size_t nstates;  // state-sized buffers in buf
+  sdcsw_sweep_hook hook;  // per-sweep host callback of sdcsw_stepper_step_hooked (else null)
+  void* hook_user;
 };
 
 extern "C" {
@@ -876,6 +879,10 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
         }
       }
       if (marks) cudaEventRecord(marks[1 + k], s);
+      if (marks && st->hook) {  // host callback after sweep k (device idle meanwhile)
+        if ((e = cudaEventSynchronize(marks[1 + k])) != cudaSuccess) return e;
+        st->hook(st->hook_user, k);
+      }
       fi_cur = fi_new;
       fe_cur = fe_new;
     }
@@ -928,6 +935,10 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
     old_stride = 1;
     first = 0;
     if (marks) cudaEventRecord(marks[1 + k], s);
+    if (marks && st->hook) {
+      if ((e = cudaEventSynchronize(marks[1 + k])) != cudaSuccess) return e;
+      st->hook(st->hook_user, k);
+    }
   }
   return cudaSuccess;
 }
@@ -974,7 +985,14 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   }
   const Plan& p = h->p;
   s->S = (size_t)3 * p.C;
-  const size_t nstates = (size_t)E * (1 + 5 * (size_t)M) + (mode == 1 ? (size_t)M + 1 : 0);
+  // sweep storage per member: fe0, and fe / fi of the nodes twice (the sweep
+  // that is read and the one being written: the node updates of a sweep run
+  // concurrently and every one reads all old tendencies); node states only
+  // where an f_E reads them (planar dSDC; one state for serial SDC) - the
+  // spherical dSDC step keeps node states only as synthesis operands
+  const size_t ust = mode == 1 ? 1 : (p.kind == 1 ? (size_t)E * M : 0);
+  const size_t nstates = (size_t)E * (1 + 4 * (size_t)M) + ust + (mode == 1 ? (size_t)M + 1 : 0);
+  s->nstates = nstates;
   cudaError_t e = cudaSetDevice(p.device);
   if (e == cudaSuccess) e = cudaMalloc(&s->buf, nstates * s->S * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc(&s->flags, 2 * sizeof(int));
@@ -995,7 +1013,7 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   s->fe0 = q; q += E * s->S;
   s->fe = q; q += E * M * s->S;
   s->fi = q; q += E * M * s->S;
-  s->ustage = q; q += E * M * s->S;
+  s->ustage = ust ? q : nullptr; q += ust * s->S;
   s->fiB = q; q += E * M * s->S;
   s->feB = q; q += E * M * s->S;
   if (mode == 1) {
@@ -1179,6 +1197,39 @@ int sdcsw_stepper_profile(sdcsw_stepper* s, double* u, double* stage_ms, int n, 
     cudaEventElapsedTime(&ms, s->prof[i], s->prof[i + 1]);
     stage_ms[i] = ms;
   }
+  return SDCSW_OK;
+}
+
+int sdcsw_stepper_step_hooked(sdcsw_stepper* s, double* u, sdcsw_sweep_hook hook, void* user,
+                              double* stage_ms, int n, void* stream) {
+  if (!s || !u || (stage_ms && n < s->K + 1)) return SDCSW_ERR_PARAM;
+  if (s->members != 1) {
+    set_error("sdcsw_stepper_step_hooked: one member only");
+    return SDCSW_ERR_PARAM;
+  }
+  double local[42];
+  s->hook = hook;
+  s->hook_user = user;
+  const int st = sdcsw_stepper_profile(s, u, stage_ms ? stage_ms : local, s->K + 1, stream);
+  s->hook = nullptr;
+  s->hook_user = nullptr;
+  return st;
+}
+
+int sdcsw_stepper_sweep_state(sdcsw_stepper* s, int sweep, void** fe0, void** fe, void** fi) {
+  if (!s || sweep < 1 || sweep > s->K) return SDCSW_ERR_PARAM;
+  if (fe0) *fe0 = s->fe0;
+  if (fe) *fe = (sweep % 2) ? s->fe : s->feB;
+  if (fi) *fi = (sweep % 2) ? s->fi : s->fiB;
+  return SDCSW_OK;
+}
+
+int sdcsw_stepper_storage(sdcsw_stepper* s, long long* bytes, long long* state_buffers) {
+  if (!s) return SDCSW_ERR_STATE;
+  const Plan& p = s->plan->p;
+  const long long ops = p.kind == 0 ? (long long)p.rows * kXsyn * sizeof(double) * s->members * (1 + s->M) : 0;
+  if (bytes) *bytes = (long long)(s->nstates * s->S * sizeof(double2)) + ops + 2 * (long long)sizeof(int);
+  if (state_buffers) *state_buffers = (long long)s->nstates;
   return SDCSW_OK;
 }
 

@@ -255,6 +255,32 @@ class DeviceStepper:
         ms = np.zeros(n)
         _native.check(self.lib.sdcsw_stepper_profile(self.handle, u.data_ptr(), _native.dptr(ms), n,
                                                      self.problem.stream()), "sdcsw_stepper_profile")
+        return self._report_from_stages(ms)
+
+    def step_hooked(self, u, on_sweep):
+        """Advance ``u`` one step stage by stage, calling ``on_sweep(k, state)``
+        after every sweep with a :class:`DeviceSweepState` of the sweep storage
+        (``sdcsw_stepper_step_hooked``); returns a StepReport with CUDA-event
+        stage times."""
+        err = []
+
+        def hook(_user, k):
+            try:
+                on_sweep(k, DeviceSweepState(self, u, k))
+            except BaseException as exc:  # re-raised after the C call returns
+                err.append(exc)
+
+        cb = _native.SWEEP_HOOK(hook)
+        n = self.n_sweeps + 2
+        ms = np.zeros(n)
+        _native.check(self.lib.sdcsw_stepper_step_hooked(self.handle, u.data_ptr(), ctypes.cast(cb, ctypes.c_void_p),
+                                                         None, _native.dptr(ms), n, self.problem.stream()),
+                      "sdcsw_stepper_step_hooked")
+        if err:
+            raise err[0]
+        return self._report_from_stages(ms)
+
+    def _report_from_stages(self, ms):
         self.problem.add_counts(*(c * self.members for c in self.counts_per_step()))
         s = ms * 1e-3
         if self.serial:
@@ -264,6 +290,13 @@ class DeviceStepper:
         sweeps = tuple(s[1 : self.n_sweeps])
         return StepReport(float(s[: self.n_sweeps + 1].sum()), float(s[0]), sweeps,
                           float(s[self.n_sweeps]), *self.counts_per_step())
+
+    def storage(self):
+        """(bytes, state-sized buffers) of the stepper's device sweep storage
+        (``sdcsw_stepper_storage``)."""
+        b, n = ctypes.c_longlong(), ctypes.c_longlong()
+        _native.check(self.lib.sdcsw_stepper_storage(self.handle, ctypes.byref(b), ctypes.byref(n)))
+        return b.value, n.value
 
     def counts_per_step(self):
         m, k = self.n_nodes, self.n_sweeps
@@ -303,6 +336,68 @@ class DeviceStepper:
             pass
 
 
+class DeviceSweepState:
+    """What the device step retains after sweep ``k``, shown to ``on_sweep``
+    the way the reference's ``SweepState`` is (``core.py:134-162``): ``u0``,
+    ``fe0``, ``fi0`` and the node slots ``u``, ``fe``, ``fi`` (one-based node m
+    at index m - 1), as numpy arrays copied from the device on access.
+
+    The device step drops the node states once their tendencies are formed
+    (the reference drops them too, ``integrators.py:233-246``): ``u`` holds
+    ``None``.  ``f_I(u0)`` is not stored either; ``fi0`` recomputes it (not
+    counted as an evaluation).  :meth:`distinct_node_arrays` counts the arrays
+    the device actually retains between sweeps: u0, fe0 and the M nodes' fe
+    and fi, 2M + 2 (the reference's bound is 2M + 3,
+    ``pkg/tests/test_integrators.py:228-241``)."""
+
+    def __init__(self, stepper, u, k):
+        self._st, self._u, self.sweep = stepper, u, k
+        self.n_nodes = stepper.n_nodes
+        fe0, fe, fi = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _native.check(stepper.lib.sdcsw_stepper_sweep_state(stepper.handle, int(k), ctypes.byref(fe0),
+                                                            ctypes.byref(fe), ctypes.byref(fi)))
+        self._ptr = {"fe0": fe0.value, "fe": fe.value, "fi": fi.value}
+        self.u = [None] * self.n_nodes
+
+    def _states(self, which, count):
+        import torch
+
+        size = self._st.problem.state_size
+        ptr = self._ptr[which]
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (count, size), "typestr": "<c16", "data": (ptr, False),
+                                        "version": 3, "strides": None}
+
+        return torch.as_tensor(_View(), device=self._st.problem.device).cpu().numpy().copy()
+
+    @property
+    def u0(self):
+        return self._u.reshape(-1).cpu().numpy().copy()
+
+    @property
+    def fe0(self):
+        return self._states("fe0", 1)[0]
+
+    @property
+    def fi0(self):
+        p = self._st.problem
+        out = p.empty_states(1)
+        p.f_impl_device(self._u.reshape(1, -1), out, 1)
+        return out[0].cpu().numpy().copy()
+
+    @property
+    def fe(self):
+        return list(self._states("fe", self.n_nodes))
+
+    @property
+    def fi(self):
+        return list(self._states("fi", self.n_nodes))
+
+    def distinct_node_arrays(self):
+        return 2 + 2 * self.n_nodes
+
+
 def _is_device_problem(problem):
     return hasattr(problem, "handle") and hasattr(problem, "f_expl_device")
 
@@ -312,15 +407,22 @@ def _device_stepper(cfg, problem, dt, serial):
     st = cfg._steppers.get(key)
     if st is None:
         st = DeviceStepper(problem, cfg, float(dt), serial)
+        if not serial and cfg.mode is SweepMode.DIAGONAL_SEQUENTIAL:
+            # the reference's sequential mode: one node update after another
+            # (bit-identical to the batched parallel mode, as in the reference)
+            st.set_sequential(True)
         cfg._steppers[key] = st
     return st
 
 
-def _one_device_step(problem, u_n, dt, cfg, serial):
+def _one_device_step(problem, u_n, dt, cfg, serial, on_sweep=None):
     import torch
 
     st = _device_stepper(cfg, problem, dt, serial)
     u = problem._to_device(u_n).reshape(-1).contiguous()
+    if on_sweep is not None:  # stage by stage, the callback between sweeps
+        report = st.step_hooked(u, on_sweep)
+        return u.cpu().numpy().copy(), report
     before = evaluation_counters(problem)
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
@@ -341,18 +443,14 @@ def dsdc_step(problem, u_n, dt, cfg, on_sweep=None):
     """One diagonal-SDC step on the GPU; returns ``(u, report)`` (ref ``integrators.py:347-381``)."""
     if cfg.mode is SweepMode.SERIAL:
         raise ParameterError(f"diagonal step requires a diagonal mode, got {cfg.mode}")
-    if on_sweep is not None:
-        raise ParameterError("on_sweep callbacks are not supported by the fused device step")
-    return _one_device_step(problem, u_n, dt, cfg, serial=False)
+    return _one_device_step(problem, u_n, dt, cfg, serial=False, on_sweep=on_sweep)
 
 
 def sdc_step_serial(problem, u_n, dt, cfg, on_sweep=None):
     """One serial-SDC step on the GPU; returns ``(u, report)`` (ref ``integrators.py:317-344``)."""
     if cfg.mode is not SweepMode.SERIAL:
         raise ParameterError(f"serial step requires mode {SweepMode.SERIAL}, got {cfg.mode}")
-    if on_sweep is not None:
-        raise ParameterError("on_sweep callbacks are not supported by the fused device step")
-    return _one_device_step(problem, u_n, dt, cfg, serial=True)
+    return _one_device_step(problem, u_n, dt, cfg, serial=True, on_sweep=on_sweep)
 
 
 class SerialSdcStepper:
@@ -391,7 +489,8 @@ class DiagonalSdcStepper:
         return dsdc_step(problem, state, dt, self.cfg)
 
 
-def integrate(problem, initial_state, dt, n_steps, stepper, checkpoint_interval=None):
+def integrate(problem, initial_state, dt, n_steps, stepper, checkpoint_interval=None,
+              stage_timings=False):
     """March ``n_steps`` fixed steps (ref ``integrators.py:517-554``).
 
     For a device problem and an SDC stepper the state stays in HBM for the
@@ -399,6 +498,12 @@ def integrate(problem, initial_state, dt, n_steps, stepper, checkpoint_interval=
     runs on the device, and the host only sees the checkpointed states.  A
     non-finite state raises :class:`DivergenceError` with the same one-based
     step index the reference reports.
+
+    ``stage_timings`` (device path, opt-in): every step runs stage by stage
+    with CUDA events (unfused, no graph replay) so each :class:`StepReport`
+    carries ``init_s``, ``sweep_s`` and ``final_node_s`` as the reference's do
+    - the input of ``perfmodel.fit_costs``.  Results are bit-identical; the
+    default graph-replayed path reports the per-step wall time only.
     """
     if dt <= 0.0:
         raise ParameterError(f"step size must be positive, got {dt}")
@@ -439,6 +544,19 @@ def integrate(problem, initial_state, dt, n_steps, stepper, checkpoint_interval=
     done = 0
     per = st.counts_per_step()
     n_sw = stepper.cfg.n_sweeps if stepper.serial else stepper.cfg.n_sweeps - 1
+    if stage_timings:
+        for step in range(1, n_steps + 1):
+            reports.append(st.profile_step(u))
+            if step == n_steps or (checkpoint_interval and step % checkpoint_interval == 0):
+                bad = st.diverged()
+                if bad:
+                    raise DivergenceError(
+                        f"{stepper.name} diverged at step {bad} of {n_steps} (t = {bad * dt:g})",
+                        step_index=bad,
+                    ) from NumericalError("non-finite state on device")
+                times.append(step * dt)
+                states.append(u.cpu().numpy().copy())
+        return Trajectory(stepper.name, dt, n_steps, times, states, reports)
     for stop_at in stops:
         seg = stop_at - done
         start = torch.cuda.Event(enable_timing=True)

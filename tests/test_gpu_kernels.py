@@ -648,3 +648,73 @@ def test_persistent_ring_bitwise(trunc, nb):
         p.close()
     assert np.isfinite(outs[1]).all()
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_on_sweep_callback_and_storage_accounting():
+    """dsdc_step / sdc_step_serial accept the reference's on_sweep(k, state)
+    callback (integrators.py:317-381): called after every sweep with the sweep
+    storage; the step result is bitwise that of the fused step; the retained
+    arrays stay within the reference's 2M + 3 bound
+    (pkg/tests/test_integrators.py:228-241) and the counts are (13, 13, 13)
+    for M = K = 4 (criterion 7, pkg/tests/test_acceptance.py:284-305).  The
+    stepper's allocated sweep storage is 1 + 4M state buffers."""
+    from paper_2403_20135_b200 import dsdc_step, sdc_step_serial
+    from paper_2403_20135_b200.core import evaluation_counters
+    from paper_2403_20135_b200.integrators import _device_stepper
+
+    p = gpu(63)
+    u0 = random_initial_state(p.grid, 21)
+    cfg = SdcConfig(table=CollocationTable.radau_right(4), n_sweeps=4, mode=SweepMode.DIAGONAL_SEQUENTIAL)
+    plain, _ = dsdc_step(p, u0, 120.0, cfg)
+    seen = []
+
+    def cb(k, state):
+        seen.append((k, state.distinct_node_arrays(), state.fe0.copy(), state.fe, state.fi, state.u))
+
+    before = evaluation_counters(p)
+    hooked, rep = dsdc_step(p, u0, 120.0, cfg, on_sweep=cb)
+    after = evaluation_counters(p)
+    assert np.array_equal(hooked, plain)
+    assert tuple(a - b for a, b in zip(after, before)) == (13, 13, 13)
+    assert [s[0] for s in seen] == [1, 2, 3]
+    assert all(s[1] <= 2 * 4 + 3 for s in seen)
+    assert all(len(s[3]) == 4 and len(s[4]) == 4 and s[5] == [None] * 4 for s in seen)
+    # fe0 is f_E(u0); the tendencies change from sweep to sweep
+    fe0_ref = p.f_expl(u0)
+    assert max(relative_l2(seen[0][2], fe0_ref, oracle_for(p))) < 1e-14
+    assert not np.array_equal(seen[0][3][1], seen[1][3][1])
+    assert rep.init_s > 0 and len(rep.sweep_s) == 3 and rep.final_node_s > 0
+    st = _device_stepper(cfg, p, 120.0, False)
+    nbytes, nbuf = st.storage()
+    assert nbuf == 1 + 4 * 4 and nbytes >= nbuf * p.state_size * 16
+    scfg = SdcConfig(table=CollocationTable.radau_right(3), n_sweeps=2, mode=SweepMode.SERIAL)
+    ks = []
+    out_s, _ = sdc_step_serial(p, u0, 120.0, scfg, on_sweep=lambda k, s: ks.append(k))
+    assert ks == [1, 2]
+    assert np.array_equal(out_s, sdc_step_serial(p, u0, 120.0, scfg)[0])
+    cfg.close()
+    scfg.close()
+
+
+def test_integrate_stage_timings_feed_the_perf_model():
+    """integrate(..., stage_timings=True) fills init_s / sweep_s / final_node_s
+    of every StepReport from CUDA events (bitwise the same states), so the
+    reference's perfmodel.fit_costs (pkg/src/parsdc/perfmodel.py:78-111) runs on
+    a normal integrate() call."""
+    from paper_2403_20135_b200.perfmodel import fit_costs
+
+    p = gpu(63)
+    u0 = random_initial_state(p.grid, 22)
+    # sequential node updates (the reference's DIAGONAL_SEQUENTIAL): the cost
+    # model's per-node structure (the batched parallel sweep costs about one node)
+    cfg = SdcConfig(table=CollocationTable.radau_right(3), n_sweeps=3, mode=SweepMode.DIAGONAL_SEQUENTIAL)
+    fast = integrate(p, u0, 120.0, 6, DiagonalSdcStepper(cfg), checkpoint_interval=3)
+    timed = integrate(p, u0, 120.0, 6, DiagonalSdcStepper(cfg), checkpoint_interval=3, stage_timings=True)
+    for a, b in zip(fast.states, timed.states):
+        assert np.array_equal(a, b)
+    assert len(timed.reports) == 6
+    assert all(r.init_s > 0 and len(r.sweep_s) == 2 and min(r.sweep_s) > 0 and r.final_node_s > 0
+               for r in timed.reports)
+    model = fit_costs(timed.reports, 3)
+    assert model.c_e > 0
+    cfg.close()
