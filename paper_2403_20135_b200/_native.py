@@ -173,7 +173,10 @@ def load(path=LIB_PATH):
             "(the CUDA path has no CPU fallback)"
         )
     lib_ = ctypes.CDLL(path)
+    partial = os.environ.get("SDCSW_LIB_PARTIAL") == "1"  # experiment builds of older sources
     for name, args in _SIGS.items():
+        if partial and not hasattr(lib_, name):
+            continue
         fn = getattr(lib_, name)
         fn.argtypes = args
         fn.restype = ctypes.c_char_p if name == "sdcsw_last_error" else ctypes.c_int

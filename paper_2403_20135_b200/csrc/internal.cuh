@@ -85,14 +85,13 @@ struct Plan {
   int syn_bulk;           // CTA-staged bulk-copy synthesis (T >= 400): 1 / 0 / -1 = automatic
   FftPlan fft;
   // workspaces
-  double2* fsyn;    // [max_batch][J][4 fields][L][2 (N, S)]
+  double2* fsyn;    // [max_batch][J][L][4 fields][2 (N, S)]
   double2* gan;     // [max_batch][L][J][2 (S,A)][kNumSlots]  (GEMM-ready for the analysis)
   double* coef_dev; // small per-call coefficient staging [kCoefCap]
   double* xsyn;     // [rows][max_batch][12] synthesis B operand for API calls
   int xsyn_nb;      // record batch of the last API prep (padding rows zero for it)
   int fe_chunk;     // f_E batch chunk keeping the Fourier workspaces L2-resident (0 = no chunking)
   int ring_threads;
-  int ringp;        // persistent ring kernel: -1 automatic (many waves), 1 forced, 0 off
   size_t ring_smem;
   // TMA tensor maps (CUtensorMap, 128 B each) over the P / H tables for the
   // table-streaming analysis (T >= 400); tma_ok = maps built
@@ -110,7 +109,7 @@ struct Plan {
   int n_own_work;
   int* own_idx;     // own coefficient indices, ascending
   int n_own_idx;
-  double2* fsyn_ext;  // part-major Fourier buffer [S][nb][J][4][Lp][2] (caller-owned)
+  double2* fsyn_ext;  // part-major Fourier buffer [S][nb][J][Lp][4][2] (caller-owned)
   // planar problem (kind 1): N x N grid, spectra [N (kx)][NH = N/2 + 1 (ky)],
   // C = N * NH coefficients per field (lam = k^2 = laplacian symbol)
   int pn, pnh;

@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
       const int j = j0 + 8 * a + g;
-      const size_t off = ((((size_t)(b0 + be) * J + j) * 4 + f) * Lp + kpos) * 2;
+      const size_t off = ((((size_t)(b0 + be) * J + j) * Lp + kpos) * 4 + f) * 2;
       const double2 vn = make_double2(aE[a][c][0] + aO[a][c][0], aE[a][c][1] + aO[a][c][1]);
       const double2 vs = make_double2(aE[a][c][0] - aO[a][c][0], aE[a][c][1] - aO[a][c][1]);
       if (sd.n == 0) {

@@ -29,11 +29,8 @@ __device__ __forceinline__ unsigned long long gtimer_r() {  // SM cycles (phase 
   return (unsigned long long)clock64();
 }
 #define RT(i) if (threadIdx.x == 0 && cta < 8192) g_rtimes[8 * cta + (i)] = gtimer_r();
-// persistent kernel: phases of the CTA's item 2
-#define RTP(i) if (tid == 0 && k == 2) g_rtimes[8 * blockIdx.x + (i)] = gtimer_r();
 #else
 #define RT(i)
-#define RTP(i)
 #endif
 
 // Shared-memory FFT arrays are padded: element k of a transform lives at
@@ -53,7 +50,20 @@ constexpr int padded() { return N + N / 8; }  // room for the densest padding (S
 template <int N> struct RadixPlan;
 template <> struct RadixPlan<96> { static constexpr int n = 3; static constexpr int r[6] = {8, 4, 3}; };
 template <> struct RadixPlan<192> { static constexpr int n = 3; static constexpr int r[6] = {16, 4, 3}; };
+#ifndef SDCSW_PLAN384  // experiment knob; {16, 8, 3} measured best for c1 (round 2)
+#define SDCSW_PLAN384 0
+#endif
+#if SDCSW_PLAN384 == 1
+template <> struct RadixPlan<384> { static constexpr int n = 3; static constexpr int r[6] = {8, 16, 3}; };
+#elif SDCSW_PLAN384 == 2
+template <> struct RadixPlan<384> { static constexpr int n = 4; static constexpr int r[6] = {4, 4, 8, 3}; };
+#elif SDCSW_PLAN384 == 3
+template <> struct RadixPlan<384> { static constexpr int n = 4; static constexpr int r[6] = {8, 4, 4, 3}; };
+#elif SDCSW_PLAN384 == 4
+template <> struct RadixPlan<384> { static constexpr int n = 4; static constexpr int r[6] = {4, 8, 4, 3}; };
+#else
 template <> struct RadixPlan<384> { static constexpr int n = 3; static constexpr int r[6] = {16, 8, 3}; };
+#endif
 template <> struct RadixPlan<768> { static constexpr int n = 3; static constexpr int r[6] = {16, 16, 3}; };
 template <> struct RadixPlan<1536> { static constexpr int n = 4; static constexpr int r[6] = {16, 8, 4, 3}; };
 
@@ -197,26 +207,25 @@ __device__ __forceinline__ void pass(double2* Z, const double2* twp, int tid) {
   constexpr int ITEMS = NF * NR;
   constexpr int MAXIT = (ITEMS + THREADS - 1) / THREADS;
   double2 v[MAXIT][R];
-  // items past the end recompute item 0 (no divergent region around the
-  // values held across the barrier; only their stores are skipped)
 #pragma unroll
   for (int q = 0; q < MAXIT; ++q) {
-    int it = tid + q * THREADS;
-    if (ITEMS % THREADS != 0 && it >= ITEMS) it = 0;
-    const int f = it / NR, i = it - f * NR;
-    const double2* X = Z + f * padded<N>();
-    const int k = i % P;
+    const int it = tid + q * THREADS;
+    if (ITEMS % THREADS == 0 || it < ITEMS) {
+      const int f = it / NR, i = it - f * NR;
+      const double2* X = Z + f * padded<N>();
+      const int k = i % P;
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[q][r] = X[pzv(i + r * NR, SHI)];
-    if (P > 1) {
+      for (int r = 0; r < R; ++r) v[q][r] = X[pzv(i + r * NR, SHI)];
+      if (P > 1 && k) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        double2 w = k ? twp[(r - 1) * P + k] : make_double2(1.0, 0.0);
-        if (INV) w.y = -w.y;
-        v[q][r] = k ? cmul(v[q][r], w) : v[q][r];
+        for (int r = 1; r < R; ++r) {
+          double2 w = twp[(r - 1) * P + k];
+          if (INV) w.y = -w.y;
+          v[q][r] = cmul(v[q][r], w);
+        }
       }
+      dft<R, INV>(v[q]);
     }
-    dft<R, INV>(v[q]);
   }
   __syncthreads();
 #pragma unroll
@@ -251,14 +260,6 @@ __device__ __forceinline__ void forward_rest(double2* Z, const double2* tw, int 
          gen_shift<N>(n - 1 + S)>(Z, tw + tw_off_fwd<N>(S), tid);
     forward_rest<N, S + 1, THREADS>(Z, tw, tid);
   }
-}
-// threadIdx.x as an opaque value: in the persistent kernel's item loop it keeps
-// the compiler from hoisting every pass's per-thread addresses out of the loop
-// (which ran the registers out and spilled ~1 KB per thread)
-__device__ __forceinline__ int opaque_tid() {
-  int t;
-  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
-  return t;
 }
 
 // host: the per-pass twiddle tables gathered from w[k] = exp(-2 pi i k / N)
@@ -321,15 +322,15 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
   const double2* tw = TWG ? twg : sm2 + 5 * NP;
   const int L = T + 1;
   const int j = blockIdx.x, b = blockIdx.y;
-  // Fourier coefficients of (b, j): part-major [part][nbg][J][4 fields][Lp][2 (N, S)]
-  // (unsplit: one part, k = m, Lp = L); Fp(f, m) -> the (N, S) pair of field f
+  // Fourier coefficients of (b, j, m): part-major [part][nbg][J][Lp][4 fields][2 (N, S)]
+  // (unsplit: one part, k = m, Lp = L)
   const double2* F0 = fsyn + ((size_t)b * J + j) * Lp * 8;  // unsplit: part 0, k = m
-  auto Fp = [&](int f, int m) -> const double2* {
+  auto Fm = [&](int m) -> const double2* {
     if constexpr (!SPLIT) {
-      return F0 + ((size_t)f * Lp + m) * 2;
+      return F0 + (size_t)m * 8;
     } else {
       const int part = m_part[m], k = m_k[m];
-      return fsyn + (((((size_t)part * nbg + b) * J + j) * 4 + f) * Lp + k) * 2;
+      return fsyn + ((((size_t)part * nbg + b) * J + j) * Lp + k) * 8;
     }
   };
 #if SDCSW_EXP == 4
@@ -397,12 +398,10 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
     constexpr int SHO = gen_shift<N>(0);
     double2* Fs = Z;
     const int LS = L + 1;
-#pragma unroll
-    for (int f = 0; f < 4; ++f)
-      for (int e = threadIdx.x; e < 2 * L; e += THREADS) {  // coalesced: (m, hemisphere) pairs
-        const int m = e >> 1, h = e & 1;
-        Fs[(h * 4 + f) * LS + m] = Fp(f, m)[h];
-      }
+    for (int e = threadIdx.x; e < 8 * L; e += THREADS) {  // coalesced
+      const int m = e >> 3, fh = e & 7;  // fh = 2 field + hemisphere
+      Fs[((fh & 1) * 4 + (fh >> 1)) * LS + m] = Fm(m)[fh];
+    }
     __syncthreads();
     RT(7)
     double2 v[MAXIT][R];
@@ -564,209 +563,6 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
   RT(5)
 }
 
-// ---------------------------------------------------------------------------
-// Persistent ring kernel (k_ringp) for batches of many waves (T255 / T511
-// dSDC sweeps, ensembles).  One resident CTA per slot loops over (state,
-// ring pair) items; each item's Fourier block ([4 fields][L][N, S], 128 L
-// bytes, contiguous in fsyn) arrives by ONE cp.async.bulk copy into a
-// dedicated stage buffer, and the copy of the CTA's next item is issued as
-// soon as pass 0 has consumed the stage - it lands while the current item's
-// FFTs run.  The output stores of an item drain while the next item computes.
-// In the one-shot kernel (k_ring) both the load phase and the output phase
-// are exposed in every wave (each about a quarter of the CTA's time at T511,
-// SDCSW_EXP=4 phase timer).  Same arithmetic in the same order as k_ring
-// (bit-identical results).
-// ---------------------------------------------------------------------------
-template <int N>
-constexpr bool ringp_twg() { return N >= 768; }  // twiddles through L1 (shared memory holds Z + stage)
-template <int N>
-constexpr size_t ringp_smem_fixed() {
-  return (size_t)(5 * padded<N>() + (ringp_twg<N>() ? 0 : tw_total<N>())) * sizeof(double2);
-}
-template <int N, int THREADS>
-constexpr int ringp_min_blocks() { return N >= 1536 ? 1 : 2; }
-
-template <int N, int THREADS>
-__global__ void __launch_bounds__(THREADS, ringp_min_blocks<N, THREADS>()) k_ringp(
-    const double2* __restrict__ fsyn, double2* __restrict__ gan, int J, int T,
-    const double* __restrict__ mu, const double* __restrict__ wsyn, const double* __restrict__ wke,
-    const double2* __restrict__ twg, double two_omega, int nb, int frag) {
-  SDCSW_PDL_ENTRY();
-  extern __shared__ double2 sm2[];
-  constexpr int NP = padded<N>();
-  constexpr int NS = RadixPlan<N>::n;
-  constexpr int TWN = tw_total<N>();
-  constexpr bool TWG = ringp_twg<N>();
-  __shared__ __align__(8) unsigned long long bar[2];  // [0] stage full, [1] twiddles
-  double2* Z = sm2;                                    // [5][NP]
-  double2* stage = sm2 + 5 * NP + (TWG ? 0 : TWN);     // [4][L][2] of the current item
-  const double2* tw = TWG ? twg : sm2 + 5 * NP;
-  const int L = T + 1;
-  const int items = J * nb;
-  const unsigned sbytes = (unsigned)(8 * L * sizeof(double2));
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if constexpr (!TWG) {
-      mbar_expect_tx(&bar[1], (unsigned)(TWN * sizeof(double2)));
-      bulk_g2s(sm2 + 5 * NP, twg, (unsigned)(TWN * sizeof(double2)), &bar[1]);
-    }
-  }
-  __syncthreads();
-  SDCSW_PDL_WAIT();
-  int it = blockIdx.x;
-  if (threadIdx.x == 0 && it < items) {
-    mbar_expect_tx(&bar[0], sbytes);
-    bulk_g2s(stage, fsyn + (size_t)it * L * 8, sbytes, &bar[0]);
-  }
-  if constexpr (!TWG) mbar_wait(&bar[1], 0);
-#pragma unroll 1
-  for (int k = 0; it < items; ++k, it += gridDim.x) {
-    const int tid = opaque_tid();
-    const int b = it / J, j = it - b * J;  // items in fsyn block order ([b][j])
-    const double muj = mu[j], ws = wsyn[j], wk = wke[j];
-    RTP(0)
-    mbar_wait(&bar[0], k & 1);
-    RTP(6)
-    // ---- inverse pass 0 from the staged block (see k_ring)
-    {
-      constexpr int R = inv_radix<N>(0);
-      constexpr int NR = N / R;
-      constexpr int ITEMS = 4 * NR;
-      constexpr int MAXIT = (ITEMS + THREADS - 1) / THREADS;
-      constexpr int SHO = gen_shift<N>(0);
-      double2 v[MAXIT][R];
-#pragma unroll
-      for (int q = 0; q < MAXIT; ++q) {
-        int e = tid + q * THREADS;
-        if (ITEMS % THREADS != 0 && e >= ITEMS) e = 0;  // recomputed, not stored (see pass)
-        const int f = e / NR, i = e - f * NR;
-        const double2* Ff = stage + (size_t)f * L * 2;  // (N, S) pairs of field f
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int kk = i + r * NR;
-          const bool lo = kk <= T, hi = kk >= N - T;
-          const int mm = lo ? kk : (hi ? N - kk : 0);
-          double2 xn = Ff[2 * mm], xs = Ff[2 * mm + 1];
-          if (!(lo || hi)) xn = xs = make_double2(0.0, 0.0);
-          if (kk == 0) xn.y = xs.y = 0.0;
-          v[q][r] = lo ? make_double2(xn.x - xs.y, xn.y + xs.x)
-                       : make_double2(xn.x + xs.y, xs.x - xn.y);
-        }
-        dft<R, true>(v[q]);
-      }
-      __syncthreads();  // the stage is consumed (and the previous item's output phase done)
-#pragma unroll
-      for (int q = 0; q < MAXIT; ++q) {
-        const int e = tid + q * THREADS;
-        if (ITEMS % THREADS == 0 || e < ITEMS) {
-          const int f = e / NR, i = e - f * NR;
-          double2* X = Z + f * NP;
-#pragma unroll
-          for (int r = 0; r < R; ++r) X[pzv(i * R + r, SHO)] = v[q][r];
-        }
-      }
-      if (tid == 0 && it + (int)gridDim.x < items) {  // the CTA's next item lands meanwhile
-        mbar_expect_tx(&bar[0], sbytes);
-        bulk_g2s(stage, fsyn + (size_t)(it + gridDim.x) * L * 8, sbytes, &bar[0]);
-      }
-      __syncthreads();
-    }
-    RTP(7)
-    inverse_mid<N, 1, THREADS>(Z, tw, tid);
-    RTP(1)
-    // ---- fused: last inverse pass, grid products, first forward pass (see k_ring)
-    {
-      constexpr int N3 = N / 3;
-      constexpr int SHI = gen_shift<N>(NS - 2), SHO = gen_shift<N>(NS - 1);
-      const double2* twp = tw + tw_off_inv<N>(NS - 1);
-      const double cor_n = two_omega * muj, cor_s = -two_omega * muj;
-      const double ke_scale = 0.5 / ((1.0 - muj) * (1.0 + muj));
-      constexpr int MAXIT = (N3 + THREADS - 1) / THREADS;
-      double2 out[MAXIT][5][3];
-#pragma unroll
-      for (int q = 0; q < MAXIT; ++q) {
-        int i = tid + q * THREADS;
-        if (N3 % THREADS != 0 && i >= N3) i = 0;  // recomputed, not stored (see pass)
-        double2 g[4][3];
-#pragma unroll
-        for (int f = 0; f < 4; ++f) {
-          const double2* X = Z + f * NP;
-#pragma unroll
-          for (int r = 0; r < 3; ++r) g[f][r] = X[pzv(i + r * N3, SHI)];
-#pragma unroll
-          for (int r = 1; r < 3; ++r) {
-            double2 w = i ? twp[(r - 1) * N3 + i] : make_double2(1.0, 0.0);
-            w.y = -w.y;
-            g[f][r] = i ? cmul(g[f][r], w) : g[f][r];
-          }
-          dft<3, true>(g[f]);
-        }
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          const double2 U = g[0][r], V = g[1][r], Zt = g[2][r], Ph = g[3][r];
-          const double en = Zt.x + cor_n, es = Zt.y + cor_s;
-          out[q][0][r] = make_double2(en * U.x, es * U.y);
-          out[q][1][r] = make_double2(en * V.x, es * V.y);
-          out[q][2][r] = make_double2(Ph.x * U.x, Ph.y * U.y);
-          out[q][3][r] = make_double2(Ph.x * V.x, Ph.y * V.y);
-          out[q][4][r] = make_double2((U.x * U.x + V.x * V.x) * ke_scale,
-                                      (U.y * U.y + V.y * V.y) * ke_scale);
-        }
-#pragma unroll
-        for (int o = 0; o < 5; ++o) dft<3, false>(out[q][o]);
-      }
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < MAXIT; ++q) {
-        const int i = tid + q * THREADS;
-        if (N3 % THREADS == 0 || i < N3) {
-#pragma unroll
-          for (int o = 0; o < 5; ++o)
-#pragma unroll
-            for (int r = 0; r < 3; ++r) Z[o * NP + pzv(3 * i + r, SHO)] = out[q][o][r];
-        }
-      }
-      __syncthreads();
-    }
-    RTP(2)
-    forward_rest<N, 1, THREADS>(Z, tw, tid);
-    RTP(3)
-    // ---- output (see k_ring); the next item's pass 0 orders these Z reads
-    //      before its Z writes (its barrier), so no barrier here
-    const double h = 0.5 / (double)N;
-    double* outp = reinterpret_cast<double*>(gan) + (size_t)b * L * J * 28;
-    const int pofs = frag ? gan_off(j, 0, kXPhi, 0) : j * 28;
-    const int hofs = frag ? gan_off(j, 0, kYPhi, 0) : j * 28 + 2 * kYPhi;
-    const int fstride = frag ? 56 : 14;
-    constexpr int SHL = gen_shift<N>(2 * NS - 2);
-    for (int e = tid; e < 2 * L; e += THREADS) {
-      const int m = e >> 1, fold = e & 1;
-      const double dm = (double)m;
-      double2 v[5];
-#pragma unroll
-      for (int o = 0; o < 5; ++o) {
-        const double2 zm = Z[o * NP + pzv(m, SHL)], zc = Z[o * NP + pzv(m == 0 ? 0 : N - m, SHL)];
-        const double2 X = make_double2(h * (zm.x + zc.x), h * (zm.y - zc.y));
-        const double2 Y = make_double2(h * (zm.y + zc.y), -h * (zm.x - zc.x));
-        v[o] = fold ? csub(X, Y) : cadd(X, Y);
-      }
-      double* bm = outp + (size_t)m * J * 28 + fold * fstride;
-      double2* dp = reinterpret_cast<double2*>(bm + pofs);
-      double2* dh = reinterpret_cast<double2*>(bm + hofs);
-      dp[kXPhi] = make_double2(dm * v[2].y * ws, -dm * v[2].x * ws);
-      dp[kXZeta] = make_double2(dm * v[0].y * ws, -dm * v[0].x * ws);
-      dp[kXDelta] = make_double2(-dm * v[1].y * ws, dm * v[1].x * ws);
-      dp[kXKe] = make_double2(v[4].x * wk, v[4].y * wk);
-      dh[kYPhi - kYPhi] = make_double2(v[3].x * ws, v[3].y * ws);
-      dh[kYZeta - kYPhi] = make_double2(v[1].x * ws, v[1].y * ws);
-      dh[kYDelta - kYPhi] = make_double2(v[0].x * ws, v[0].y * ws);
-    }
-    RTP(4)
-  }
-}
-
 #ifndef SDCSW_RT96
 #define SDCSW_RT96 256
 #endif
@@ -796,27 +592,8 @@ size_t ring_smem_bytes(int nlon);
 
 // Each ring kernel's dynamic shared-memory limit is its own size's need (a
 // process-wide function attribute: it must not depend on which plan set it).
-#define SDCSW_RINGP_SIZES(X) X(768, 256) X(1536, 512)
-// (nlon 384 is left to the one-shot kernels: its 128-thread throughput variant
-// was faster on ensembles than k_ringp, measured)
-static int g_ringp_resident[2];  // resident CTAs per SM of k_ringp at 768 / 1536 (0 = unknown)
-
-static int ringp_slot(int nlon) { return nlon == 768 ? 0 : nlon == 1536 ? 1 : -1; }
-
 cudaError_t configure_ring(size_t /*smem*/) {
   cudaError_t e = cudaSuccess;
-#define SDCSW_RINGP_CFG(NV, TV)                                                                    \
-  if (e == cudaSuccess) {                                                                          \
-    const int mx = 232448 - 64;                                                                    \
-    e = cudaFuncSetAttribute(k_ringp<NV, TV>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);    \
-    int nres = 0;                                                                                  \
-    const size_t smem = ringp_smem_fixed<NV>() + (size_t)8 * (NV / 3) * sizeof(double2);          \
-    if (e == cudaSuccess)                                                                          \
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nres, k_ringp<NV, TV>, TV, smem);         \
-    g_ringp_resident[ringp_slot(NV)] = nres;                                                       \
-  }
-  SDCSW_RINGP_SIZES(SDCSW_RINGP_CFG)
-#undef SDCSW_RINGP_CFG
 #define SDCSW_RING_CFG(NV, TV)                                                                     \
   if (e == cudaSuccess)                                                                            \
     e = cudaFuncSetAttribute(k_ring<NV, TV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
@@ -853,43 +630,9 @@ bool ring_pass_twiddles(int nlon, const double2* w, std::vector<double2>& out) {
   return false;
 }
 
-// the persistent kernel when the batch spans at least SDCSW_RINGP_WAVES waves of
-// its resident slots (SDCSW_RINGP: 1 forces it where it fits, 0 disables)
-#ifndef SDCSW_RINGP_WAVES
-#define SDCSW_RINGP_WAVES 3  // T511 one state (2.6 waves) measured equal, five states 10% faster
-#endif
-static cudaError_t ringp_impl(const Plan& p, const double2* fsyn, double2* gan, int nb,
-                              cudaStream_t s) {
-  const int slot = ringp_slot(p.nlon);
-  if (slot < 0 || p.ringp == 0) return cudaErrorNotSupported;
-  const int L = p.T + 1;
-  const int items = p.J * nb;
-  int nsm = 0;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p.device);
-  const int res = g_ringp_resident[slot];
-  if (res < 1 || (p.ringp < 0 && items < SDCSW_RINGP_WAVES * res * nsm)) return cudaErrorNotSupported;
-  const int grid = items < res * nsm ? items : res * nsm;
-#define SDCSW_RINGP_LAUNCH(NV, TV)                                                                 \
-  if (p.nlon == NV) {                                                                              \
-    const size_t smem = ringp_smem_fixed<NV>() + (size_t)8 * L * sizeof(double2);                 \
-    if (smem > 232448 - 64) return cudaErrorNotSupported;                                          \
-    cudaError_t e = launch_k(k_ringp<NV, TV>, dim3(grid), dim3(TV), smem, s, fsyn, gan, p.J, p.T,   \
-                             p.mu, p.wsyn, p.wke, p.twiddle, 2.0 * p.omega, nb,                    \
-                             (int)tma_active(p));                                                  \
-    return e == cudaSuccess ? cudaGetLastError() : e;                                              \
-  }
-  SDCSW_RINGP_SIZES(SDCSW_RINGP_LAUNCH)
-#undef SDCSW_RINGP_LAUNCH
-  return cudaErrorNotSupported;
-}
-
 static cudaError_t ring_impl(const Plan& p, const double2* fsyn, double2* gan, const int* m_part,
                              const int* m_k, int Lp, int nb, cudaStream_t s,
                              const RingPeer& rp = RingPeer{}) {
-  if (m_part == nullptr) {
-    const cudaError_t e = ringp_impl(p, fsyn, gan, nb, s);
-    if (e != cudaErrorNotSupported) return e;
-  }
   dim3 grid(p.J, nb);
 #define SDCSW_RING_LAUNCH(NV, TV)                                                                  \
   if (p.nlon == NV) {                                                                              \

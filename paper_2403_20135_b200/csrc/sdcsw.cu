@@ -238,8 +238,6 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   }
   p.n_anal_work4 = (int)work4.size();
   p.ring_threads = 256;
-  p.ringp = -1;
-  if (const char* env = getenv("SDCSW_RINGP")) p.ringp = atoi(env);
   p.ring_smem = ring_smem_bytes(nlon);
   std::vector<double2> twp;
   ring_pass_twiddles(nlon, tw.data(), twp);

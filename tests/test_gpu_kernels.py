@@ -617,39 +617,6 @@ def _native_check(p, stage, u, nb, s):
     _native.check(p._lib.sdcsw_transform_stage(p.handle, stage, u.data_ptr(), out.data_ptr(), nb, s))
 
 
-@pytest.mark.parametrize("trunc,nb", [(255, 4), (511, 2)])
-def test_persistent_ring_bitwise(trunc, nb):
-    """The persistent ring kernel (k_ringp: bulk-prefetched Fourier blocks,
-    forced with SDCSW_RINGP=1) computes exactly the one-shot kernel's f_E."""
-    import torch
-
-    from paper_2403_20135_b200.problem import SphericalShallowWater
-
-    outs = []
-    states = None
-    for flag in ("0", "1"):
-        old = os.environ.get("SDCSW_RINGP")
-        os.environ["SDCSW_RINGP"] = flag
-        try:
-            p = SphericalShallowWater(trunc, max_batch=nb)
-        finally:
-            if old is None:
-                del os.environ["SDCSW_RINGP"]
-            else:
-                os.environ["SDCSW_RINGP"] = old
-        if states is None:
-            states = np.stack([random_initial_state(p.grid, 90 + b) for b in range(nb)])
-            states[:, : p.n_coef] = 3e-3 * states[:, p.n_coef : 2 * p.n_coef] * 1e6
-        u = torch.from_numpy(states).to(p.device).contiguous()
-        o = p.empty_states(nb)
-        p.f_expl_device(u, o, nb)
-        torch.cuda.synchronize()
-        outs.append(o.cpu().numpy())
-        p.close()
-    assert np.isfinite(outs[1]).all()
-    assert np.array_equal(outs[0], outs[1])
-
-
 def test_on_sweep_callback_and_storage_accounting():
     """dsdc_step / sdc_step_serial accept the reference's on_sweep(k, state)
     callback (integrators.py:317-381): called after every sweep with the sweep
