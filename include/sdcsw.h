@@ -131,6 +131,23 @@ int sdcsw_sweep_nodes_residual(sdcsw_plan* plan, int n_nodes, int node_lo, int c
  *   beta = u0 + sum_j (w[j] fe_j + w[j] fi_j) - wd fi_last ; u_out = solve.
  * final_coef is HOST memory [M + 4] = (w[0..M-1], wd, alpha, alpha*phibar,
  * alpha^2*phibar).  u_out may alias u0. */
+/* One serial SDC sweep (all M nodes in order) on a single state: the
+ * reference's serial_sweep (integrators.py:183-230, Alg. 1 / Eq. 5).  coef is
+ * the serial stepper's coefficient block (W = dt q [M][M], dt explicit
+ * weights [M], dt dtau [M], solve scalars [M][3]; serial_step_coefficients in
+ * integrators.py of this package).  fe_old / fi_old: the previous iterate's
+ * node tendencies (element stride fe_stride / fi_stride states; the first
+ * sweep passes f_E(u0) with stride 0, and fi_old is ignored - f_I(u0) is
+ * formed in the kernels).  Writes the new node tendencies fe_new / fi_new (M
+ * states each) and node M's state u_last; work is caller-owned scratch of
+ * M + 2 states.  The same kernels in the same order as the serial stepper
+ * (bit-identical).  Uses the plan's API operand and workspaces: serialise
+ * calls on one plan. */
+int sdcsw_serial_sweep(sdcsw_plan* plan, int n_nodes, const double* coef, const double* u0,
+                       const double* fe_old, long long fe_stride, const double* fi_old,
+                       long long fi_stride, int first, double* fe_new, double* fi_new,
+                       double* u_last, double* work, void* stream);
+
 int sdcsw_final_node(sdcsw_plan* plan, int n_nodes, const double* final_coef, const double* u0,
                      const double* fe, long long fe_stride, const double* fi, long long fi_stride,
                      int first, double* u_out, void* stream);

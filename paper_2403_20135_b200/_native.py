@@ -27,6 +27,7 @@ EXPORTS = (
     "sdcsw_sweep_nodes",
     "sdcsw_sweep_nodes_residual",
     "sdcsw_final_node",
+    "sdcsw_serial_sweep",
     "sdcsw_stepper_create",
     "sdcsw_stepper_create_ensemble",
     "sdcsw_stepper_destroy",
@@ -116,6 +117,7 @@ _SIGS = {
     "sdcsw_sweep_nodes_residual": [_p, _i, _i, _i, _dp, _p, _p, _ll, _p, _ll, _i, _p, _p, _p, _p,
                                    _p],
     "sdcsw_final_node": [_p, _i, _dp, _p, _p, _ll, _p, _ll, _i, _p, _p],
+    "sdcsw_serial_sweep": [_p, _i, _dp, _p, _p, _ll, _p, _ll, _i, _p, _p, _p, _p, _p],
     "sdcsw_stepper_create": [_p, _i, _i, _i, _dp, _i, ctypes.POINTER(_p)],
     "sdcsw_stepper_create_ensemble": [_p, _i, _i, _i, _i, _dp, _i, ctypes.POINTER(_p)],
     "sdcsw_stepper_destroy": [_p],

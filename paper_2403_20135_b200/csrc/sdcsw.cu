@@ -520,6 +520,60 @@ int sdcsw_final_node(sdcsw_plan* h, int n_nodes, const double* final_coef, const
                      "sdcsw_final_node");
 }
 
+int sdcsw_serial_sweep(sdcsw_plan* h, int n_nodes, const double* coef, const double* u0,
+                       const double* fe_old, long long fe_stride, const double* fi_old,
+                       long long fi_stride, int first, double* fe_new, double* fi_new,
+                       double* u_last, double* work, void* stream) {
+  int st = check_plan(h, 1, "sdcsw_serial_sweep");
+  if (st) return st;
+  if ((st = check_spherical(h, "sdcsw_serial_sweep"))) return st;
+  const int M = n_nodes;
+  if (M < 1 || M > 16 || !coef || !u0 || !fe_old || !fi_old || !fe_new || !fi_new || !u_last ||
+      !work) {
+    set_error("sdcsw_serial_sweep: bad node count (1..16) or null argument");
+    return SDCSW_ERR_PARAM;
+  }
+  Plan& p = h->p;
+  if (p.own_idx != nullptr) {
+    set_error("sdcsw_serial_sweep: not available on a spectrally split plan");
+    return SDCSW_ERR_STATE;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t S = (size_t)3 * p.C;
+  const double* W = coef;             // [M][M]   dt q
+  const double* we = W + M * M;       // [M]      dt explicit weights
+  const double* wi = we + M;          // [M]      dt dtau
+  const double* sc = wi + M;          // [M][3]   solve scalars
+  double2* quad = reinterpret_cast<double2*>(work);  // [M] states
+  double2* corr = quad + M * S;                      // [1]
+  double2* ustage = corr + S;                        // [1]
+  const double2* u = reinterpret_cast<const double2*>(u0);
+  const double2* ofe = reinterpret_cast<const double2*>(fe_old);
+  const double2* ofi = reinterpret_cast<const double2*>(fi_old);
+  double2* nfe = reinterpret_cast<double2*>(fe_new);
+  double2* nfi = reinterpret_cast<double2*>(fi_new);
+  cudaError_t e = cudaSuccess;
+  if (p.xsyn_nb != 1) {  // the API operand holds one state's records; padding rows zero
+    e = cudaMemsetAsync(p.xsyn, 0, (size_t)p.rows * kXsyn * sizeof(double), s);
+    p.xsyn_nb = 1;
+  }
+  // the serial branch of enqueue_step for one sweep (same kernels, same order)
+  if (e == cudaSuccess)
+    e = launch_serial_quad(p, M, W, u, ofe, fe_stride, ofi, fi_stride, first,
+                           quad, s);
+  for (int m = 0; m < M && e == cudaSuccess; ++m) {
+    const bool last = m == M - 1;
+    e = launch_serial_node(p, M, m, sc + 3 * m, quad + m * S, corr, u, ofi + fi_stride * m * S,
+                           first, ustage, last ? reinterpret_cast<double2*>(u_last) : nullptr,
+                           nfi + m * S, nullptr, nullptr, p.xsyn, s);
+    if (e == cudaSuccess) e = f_expl_prepped(p, plan_work(p), p.xsyn, nfe + m * S, 1, s, nullptr);
+    if (e == cudaSuccess && m + 1 < M)
+      e = launch_serial_update(p, m, we[m], wi[m], corr, nfe + m * S, ofe + fe_stride * m * S,
+                               nfi + m * S, ofi + fi_stride * m * S, u, first, s);
+  }
+  return cuda_status(e, "sdcsw_serial_sweep");
+}
+
 int sdcsw_transform_stage(sdcsw_plan* h, int stage, const double* in, double* out, int nb,
                           void* stream) {
   int st = check_plan(h, nb, "sdcsw_transform_stage");

@@ -160,6 +160,21 @@ class CudaNodeBackend:
             "sdcsw_sweep_nodes_residual",
         )
 
+    def serial_sweep(self, n_nodes, coef, u0, fe_old, fe_stride, fi_old, fi_stride, first,
+                     fe_new, fi_new, u_last, work):
+        """One serial SDC sweep (``sdcsw_serial_sweep``; the reference's
+        ``serial_sweep``, ``integrators.py:183-230``); ``work``: M + 2 states."""
+        from . import _native
+
+        _native.check(
+            self.lib.sdcsw_serial_sweep(
+                self.problem.handle, n_nodes, _native.dptr(coef), u0.data_ptr(), fe_old.data_ptr(),
+                fe_stride, fi_old.data_ptr(), fi_stride, int(first), fe_new.data_ptr(),
+                fi_new.data_ptr(), u_last.data_ptr(), work.data_ptr(), self.problem.stream(),
+            ),
+            "sdcsw_serial_sweep",
+        )
+
     def final_node(self, n_nodes, coef, u0, fe, fe_stride, fi, fi_stride, first, u_out):
         from . import _native
 

@@ -685,3 +685,37 @@ def test_integrate_stage_timings_feed_the_perf_model():
     model = fit_costs(timed.reports, 3)
     assert model.c_e > 0
     cfg.close()
+
+
+@pytest.mark.parametrize("trunc,m_count,k_count", [(63, 3, 3), (127, 4, 2)])
+def test_standalone_serial_sweep_matches_serial_step(trunc, m_count, k_count):
+    """sdcsw_serial_sweep (the reference's serial_sweep, integrators.py:183-230):
+    f_E(u0) followed by K standalone serial sweeps reproduces the serial SDC
+    stepper's step bitwise (SURVEY 8(b) sdcsw_serial_sweep)."""
+    import torch
+
+    from paper_2403_20135_b200 import sdc_step_serial
+    from paper_2403_20135_b200.integrators import serial_step_coefficients
+    from paper_2403_20135_b200.parallel_nodes import CudaNodeBackend
+
+    p = gpu(trunc)
+    cfg = SdcConfig(table=CollocationTable.radau_right(m_count), n_sweeps=k_count, mode=SweepMode.SERIAL)
+    u0 = random_initial_state(p.grid, 31)
+    want, _ = sdc_step_serial(p, u0, 100.0, cfg)
+    coef = np.ascontiguousarray(serial_step_coefficients(cfg, 100.0, p.mean_geopotential,
+                                                         p.solve_coefficients))
+    b = CudaNodeBackend(p)
+    u = torch.from_numpy(u0).to(p.device).reshape(1, -1).contiguous()
+    fe0 = p.empty_states(1)
+    p.f_expl_device(u, fe0, 1)
+    fe = [p.empty_states(m_count) for _ in range(2)]
+    fi = [p.empty_states(m_count) for _ in range(2)]
+    last, work = p.empty_states(1), p.empty_states(m_count + 2)
+    old_fe, old_fi, stride, first = fe0, fe0, 0, True
+    for k in range(k_count):
+        b.serial_sweep(m_count, coef, u, old_fe, stride, old_fi, stride, first, fe[k % 2], fi[k % 2],
+                       last, work)
+        old_fe, old_fi, stride, first = fe[k % 2], fi[k % 2], 1, False
+    torch.cuda.synchronize()
+    assert np.array_equal(last[0].cpu().numpy(), want)
+    cfg.close()
