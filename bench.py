@@ -595,6 +595,57 @@ def plan_only():
     return 0
 
 
+def replica_checksum(u, own=None):
+    """Sum of |u| over the entries this rank holds (own: per-field mask, spectral parts)."""
+    import torch
+
+    x = u.reshape(-1)
+    if own is not None:
+        m = torch.from_numpy(np.tile(own, 3)).to(x.device)
+        x = x[m]
+    return float(torch.sum(torch.abs(x)).item())
+
+
+def replicas_agree(xpeer, u, dist):
+    """Ranks holding the same wavenumbers must hold bitwise-equal states: compare
+    checksums of the own entries among the ranks of each spectral part."""
+    import torch
+
+    own = xpeer.own_coefficients() if xpeer.nparts > 1 else None
+    mine = torch.tensor([float(xpeer.part), replica_checksum(u, own)], dtype=torch.float64,
+                        device=u.device)
+    every = [torch.zeros_like(mine) for _ in range(dist.get_world_size())]
+    dist.all_gather(every, mine)
+    sums = {}
+    for t in every:
+        sums.setdefault(int(t[0].item()), set()).add(t[1].item())
+    return all(len(v) == 1 and np.isfinite(list(v)[0]) for v in sums.values())
+
+
+def peer_exchange_validated(xpeer, u0, dist):
+    """Three steps over the peer exchange with a 5 s wait bound before the timed
+    runs; True on every rank iff no wait ran out and the replicas agree."""
+    import torch
+
+    from paper_2403_20135_b200.errors import DeviceError
+
+    ok = True
+    try:
+        xpeer.set_wait_bound(5000)
+        v = u0.clone()
+        xpeer.run(v, 3, use_graph=False)
+        xpeer.diverged()  # DeviceError if a peer did not post within the bound
+        ok = replicas_agree(xpeer, v, dist)
+        xpeer.reset()
+        xpeer.set_wait_bound(30000)
+    except DeviceError as exc:
+        print(f"[bench] peer exchange validation: {exc}", file=sys.stderr)
+        ok = False
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=u0.device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    return bool(flag.item())
+
+
 def run_device(args):
     import torch
 
@@ -620,6 +671,7 @@ def run_device(args):
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29655")
+        os.environ.setdefault("NCCL_DEBUG", "WARN")  # stdout carries the JSON line only
         dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank,
                                 world_size=world)
     c = CONFIGS[args.config]
@@ -663,6 +715,11 @@ def run_device(args):
         # collective: peer mappings work on every rank, else every rank takes NCCL
         xpeer, p2p_error = PeerNodeParallelDsdc.create_collective(
             problem, cfg, dt, spectral_parts=world // groups)
+        if xpeer is not None and world > 1 and not peer_exchange_validated(xpeer, u0, dist):
+            # first contact of the real multi-process peer path: a wait that ran out or
+            # ranks whose replicated states disagree make every rank take NCCL
+            xpeer.close()
+            xpeer, p2p_error = None, "validation run failed (wait bound or replica mismatch)"
         if xpeer is None:
             problem._lib.sdcsw_plan_set_split(problem.handle, 1, 0, None, 0)
             transport = "nccl"
@@ -732,6 +789,9 @@ def run_device(args):
 
     # divergence check of the timed runs (device flag)
     finite = bool(torch.isfinite(torch.view_as_real(u)).all().item())
+    replicas = None
+    if multi and world > 1 and transport == "p2p":
+        replicas = replicas_agree(xpeer, u, dist)
 
     e2e_multi = None
     if multi:
@@ -839,6 +899,7 @@ def run_device(args):
                 "stage_us_per_sim_step": stage_us, "stage_us": stage_detail,
                 "finite": finite,
                 "multi_gpu_transport": transport if multi else None,
+                "replicas_bitwise_equal": replicas,
             },
             "roofline": roof,
             "large_truncation": large,
