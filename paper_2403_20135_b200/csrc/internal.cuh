@@ -92,6 +92,7 @@ struct Plan {
   int xsyn_nb;      // record batch of the last API prep (padding rows zero for it)
   int fe_chunk;     // f_E batch chunk keeping the Fourier workspaces L2-resident (0 = no chunking)
   int ring_threads;
+  bool ensemble;    // max_batch >= kEnsembleBatch: throughput-regime kernel choices
   size_t ring_smem;
   // TMA tensor maps (CUtensorMap, 128 B each) over the P / H tables for the
   // table-streaming analysis (T >= 400); tma_ok = maps built
@@ -121,6 +122,7 @@ struct Plan {
   double2* pw2;        // [max_batch][5][N][NH] row spectra of the five grid products
 };
 constexpr int kCoefCap = 4096;
+constexpr int kEnsembleBatch = 16;  // plans for at least this many states per f_E are ensemble plans
 
 // Programmatic dependent launch: every kernel is launched with programmatic
 // stream serialization and waits for its predecessor's memory

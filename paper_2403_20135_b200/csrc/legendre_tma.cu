@@ -210,7 +210,8 @@ cudaError_t make_table_maps(Plan& p) {
   const char* env = getenv("SDCSW_TMA_MIN_T");  // table-streaming analysis from this truncation
   // from T200: with the B operand staged (k_analysis_bulk) the unfused step beats the
   // fused latency-regime analysis at T255 (c2 1985 vs 1866 steps/s); not at T127/T63
-  const int tmin = env ? atoi(env) : 200;
+  // for one state, but for ensemble plans (p.ensemble) at every truncation
+  const int tmin = env ? atoi(env) : (p.ensemble ? 0 : 200);
   if (p.T < tmin || p.J % kTmaLat) return cudaSuccess;
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;

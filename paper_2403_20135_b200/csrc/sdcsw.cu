@@ -211,7 +211,11 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
   // row tiles per CTA: small truncations split K over the 4 warps (more warps
   // in flight), large ones give each warp its own row tile (B reuse via L1)
   // (from T200 the table-streaming analysis runs, which takes 4 row tiles per CTA)
-  p.anal_wj = T < 200 ? 1 : 4;
+  // ensemble plans (batches of at least kEnsembleBatch states) take the
+  // table-streaming analysis at any truncation: 64-member T127 ensemble
+  // analysis 504 -> 297 us per 256-state launch, c4 13.3k -> 15.3k member-steps/s
+  p.ensemble = p.max_batch >= kEnsembleBatch;
+  p.anal_wj = T < 200 && !p.ensemble ? 1 : 4;
   p.synth_wj = T < 200 ? 1 : (T < 400 ? 2 : 4);
   // cp.async-pipelined synthesis: -1 = automatic (see synthesis_impl)
   p.syn_cp = -1;
