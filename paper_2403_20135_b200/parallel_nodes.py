@@ -531,6 +531,41 @@ class PeerNodeParallelDsdc:
                     for h in hs:
                         x.phase(u, h)
 
+    def run_serialized(self, u, n_steps, group=None):
+        """Advance ``u`` with the ranks of ``group`` (one process each) taking turns:
+        before every half-phase each rank posts what that half-phase waits for
+        (post-only kernels), then the ranks run the half-phase one after another
+        with a host barrier in between - every wait is satisfied by completed
+        kernels of the other processes, and no kernel ever waits on a running one
+        (the B200 profiling guide forbids spinning kernels of several processes on
+        one GPU).  Same data path as :meth:`run` otherwise: real CUDA-IPC
+        mappings, stores into peer buffers, system-scope posts.  For testing the
+        multi-process protocol on one GPU."""
+        import torch
+        import torch.distributed as dist
+
+        k_sweeps = self.k
+        split = self.nparts > 1
+        groups = ([[h] for h in range(2 * k_sweeps + 1)] if split else
+                  [[2 * k, 2 * k + 1] for k in range(k_sweeps)] + [[2 * k_sweeps]])
+        world = dist.get_world_size(group)
+        me = dist.get_rank(group)
+        for _ in range(n_steps):
+            for hs in groups:
+                k = hs[0] // 2
+                if hs[0] % 2 == 0 and k >= 2:
+                    self.post(0, k - 1)
+                if hs[0] % 2 == 1 and (k == 0 or self.info()[1] > 0):
+                    self.post(1)
+                torch.cuda.synchronize()
+                dist.barrier(group)
+                for turn in range(world):
+                    if turn == me:
+                        for h in hs:
+                            self.phase(u, h)
+                        torch.cuda.synchronize()
+                    dist.barrier(group)
+
     def own_coefficients(self):
         """Boolean mask over one field's coefficients (m-major triangle): the
         entries this rank's state holds (all unless spectral parts)."""

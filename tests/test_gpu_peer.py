@@ -279,3 +279,63 @@ def test_missing_peer_post_is_an_error_not_a_hang(split):
     assert x.diverged() == 0
     for r in ranks:
         r.close()
+
+
+def _ipc_worker(rank, world, port, split, out_path):
+    import os
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2403_20135_b200.parallel_nodes import PeerNodeParallelDsdc
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    p = SphericalShallowWater(63, device=0, max_batch=8)
+    cfg = _cfg(4, 3)
+    x = PeerNodeParallelDsdc(p, cfg, 120.0, spectral_parts=world if split else 1)
+    x.set_wait_bound(10000)  # a protocol error fails the test instead of hanging it
+    u = torch.from_numpy(random_initial_state(p.grid, 23)).to(p.device)
+    x.run_serialized(u, 3)
+    bad = x.diverged()  # raises DeviceError if a wait ran out
+    own = x.own_coefficients()
+    np.save(out_path + f".{rank}.npy", u.cpu().numpy().reshape(-1))
+    np.save(out_path + f".{rank}.own.npy", own)
+    assert bad == 0
+    x.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("split", [False, True])
+def test_two_processes_over_cuda_ipc_bitwise(tmp_path, split):
+    """two processes on one GPU, each with its own plan and
+    exchange, map each other's buffers through real CUDA IPC handles; the
+    analysis epilogue (or the split synthesis) of one process stores into the
+    other's buffer and the posts are system-scope atomics into the other's flag
+    block.  The ranks take turns per half-phase (run_serialized), so every wait
+    is satisfied by completed kernels of the other process.  Both ranks end
+    bitwise equal to the single-GPU stepper (on their own wavenumbers when
+    split)."""
+    import os
+
+    import numpy as np
+    import torch
+    import torch.multiprocessing as mp
+
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    world = 2
+    port = 29400 + (os.getpid() % 97) + (50 if split else 0)
+    out = str(tmp_path / "u")
+    mp.spawn(_ipc_worker, args=(world, port, split, out), nprocs=world, join=True)
+    p = SphericalShallowWater(63, device=0, max_batch=8)
+    u0 = torch.from_numpy(random_initial_state(p.grid, 23)).to(p.device)
+    ref = _stepper_result(p, _cfg(4, 3), 120.0, u0, 3).cpu().numpy().reshape(-1)
+    p.close()
+    for r in range(world):
+        got = np.load(out + f".{r}.npy")
+        own = np.tile(np.load(out + f".{r}.own.npy"), 3)
+        assert np.array_equal(got[own], ref[own]), r
