@@ -347,6 +347,8 @@ int sdcsw_exchange_destroy(sdcsw_exchange* x);
 typedef struct sdcsw_comm sdcsw_comm;
 int sdcsw_comm_unique_id(void* id, int bytes);
 int sdcsw_comm_create(const void* id, int bytes, int world, int rank, int device, sdcsw_comm** out);
+/* single-process multi-GPU (ncclCommInitAll): out[i] is rank i on devs[i] */
+int sdcsw_comm_init_all(int ndev, const int* devs, sdcsw_comm** out);
 int sdcsw_comm_split(sdcsw_comm* parent, int color, int key, sdcsw_comm** out);
 int sdcsw_comm_info(sdcsw_comm* comm, int* world, int* rank);
 int sdcsw_allgather_rhs(sdcsw_comm* comm, const double* send, double* recv, long long count,

@@ -64,6 +64,7 @@ EXPORTS = (
     "sdcsw_exchange_destroy",
     "sdcsw_comm_unique_id",
     "sdcsw_comm_create",
+    "sdcsw_comm_init_all",
     "sdcsw_comm_split",
     "sdcsw_comm_info",
     "sdcsw_allgather_rhs",
@@ -154,6 +155,7 @@ _SIGS = {
     "sdcsw_exchange_destroy": [_p],
     "sdcsw_comm_unique_id": [_p, _i],
     "sdcsw_comm_create": [_p, _i, _i, _i, _i, ctypes.POINTER(_p)],
+    "sdcsw_comm_init_all": [_i, _ip, ctypes.POINTER(_p)],
     "sdcsw_comm_split": [_p, _i, _i, ctypes.POINTER(_p)],
     "sdcsw_comm_info": [_p, _ip, _ip],
     "sdcsw_allgather_rhs": [_p, _p, _p, _ll, _p],

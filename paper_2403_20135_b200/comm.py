@@ -44,6 +44,16 @@ class NcclComm:
         return cls(h)
 
     @classmethod
+    def init_all(cls, devices):
+        """One communicator per device of this process (``ncclCommInitAll``)."""
+        lib = _native.lib()
+        n = len(devices)
+        devs = (ctypes.c_int * n)(*devices)
+        out = (ctypes.c_void_p * n)()
+        _native.check(lib.sdcsw_comm_init_all(n, devs, out), "sdcsw_comm_init_all")
+        return [cls(ctypes.c_void_p(h)) for h in out]
+
+    @classmethod
     def bootstrap(cls, device, group=None):
         """Communicator over the ranks of the torch.distributed ``group`` (or a
         single-rank one when torch.distributed is not initialised): rank 0's

@@ -40,6 +40,7 @@ struct Nccl {
   std::string why;
   decltype(&::ncclGetUniqueId) GetUniqueId = nullptr;
   decltype(&::ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&::ncclCommInitAll) CommInitAll = nullptr;
   decltype(&::ncclCommSplit) CommSplit = nullptr;
   decltype(&::ncclCommCount) CommCount = nullptr;
   decltype(&::ncclCommUserRank) CommUserRank = nullptr;
@@ -65,6 +66,7 @@ const Nccl& nccl() {
     };
     bind(n.GetUniqueId, "ncclGetUniqueId");
     bind(n.CommInitRank, "ncclCommInitRank");
+    bind(n.CommInitAll, "ncclCommInitAll");
     bind(n.CommSplit, "ncclCommSplit");
     bind(n.CommCount, "ncclCommCount");
     bind(n.CommUserRank, "ncclCommUserRank");
@@ -134,6 +136,25 @@ int sdcsw_comm_create(const void* id, int bytes, int world, int rank, int device
   c->rank = rank;
   c->device = device;
   *out = c;
+  return SDCSW_OK;
+}
+
+int sdcsw_comm_init_all(int ndev, const int* devs, sdcsw_comm** out) {
+  if (ndev < 1 || ndev > 64 || devs == nullptr || out == nullptr) {
+    sdcsw::set_error("sdcsw_comm_init_all: bad device list");
+    return SDCSW_ERR_PARAM;
+  }
+  if (int st = nccl_missing("sdcsw_comm_init_all")) return st;
+  ncclComm_t comms[64];
+  const int st = nccl_status(nccl().CommInitAll(comms, ndev, devs), "sdcsw_comm_init_all");
+  if (st != SDCSW_OK) return st;
+  for (int i = 0; i < ndev; ++i) {
+    out[i] = new sdcsw_comm;
+    out[i]->comm = comms[i];
+    out[i]->world = ndev;
+    out[i]->rank = i;
+    out[i]->device = devs[i];
+  }
   return SDCSW_OK;
 }
 

@@ -719,3 +719,34 @@ def test_standalone_serial_sweep_matches_serial_step(trunc, m_count, k_count):
     torch.cuda.synchronize()
     assert np.array_equal(last[0].cpu().numpy(), want)
     cfg.close()
+
+
+def test_nccl_allgather_through_the_c_abi():
+    """sdcsw_comm_init_all / sdcsw_comm_create + sdcsw_allgather_rhs on one GPU:
+    the all-gather of one rank is a copy, in place and out of place."""
+    import torch
+
+    from paper_2403_20135_b200.comm import NcclComm
+
+    comms = NcclComm.init_all([0])
+    assert len(comms) == 1 and comms[0].world == 1 and comms[0].rank == 0
+    boot = NcclComm.create(NcclComm.unique_id(), 1, 0, 0)
+    x = torch.randn(1000, dtype=torch.float64, device="cuda")
+    for c in (comms[0], boot):
+        y = torch.zeros_like(x)
+        c.allgather(y, x, ctypes_stream())
+        torch.cuda.synchronize()
+        assert torch.equal(x, y)
+        z = x.clone()
+        c.allgather(z, z, ctypes_stream())  # in place
+        torch.cuda.synchronize()
+        assert torch.equal(z, x)
+        c.close()
+
+
+def ctypes_stream():
+    import ctypes
+
+    import torch
+
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
