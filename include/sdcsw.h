@@ -235,7 +235,7 @@ int sdcsw_transform_stage(sdcsw_plan* plan, int stage, const double* in, double*
                           void* stream);
 
 /* Device pointers and sizes of the internal workspaces: which 0 = Fourier
-  * coefficients [max_batch][nlat/2][4 (U,V,zeta,Phi)][T+1][2 (N,S)] complex,
+ * coefficients [max_batch][nlat/2][T+1][4 (U,V,zeta,Phi)][2 (N,S)] complex,
  * which 1 = analysis data, [max_batch][T+1] blocks of nlat/2 x 28 doubles:
  * [nlat/2][2 (N+S, N-S)][7 slots] complex when T < 400, in DMMA-fragment
  * order for the table-streaming analysis (T >= 400; gan_off in internal.cuh). */
@@ -246,7 +246,7 @@ int sdcsw_workspace(sdcsw_plan* plan, int which, void** ptr, long long* bytes);
  * (m, T-m) dealt round-robin, and this rank keeps part sp.  Afterwards
  * sdcsw_sweep_nodes / sdcsw_final_node touch only own-m coefficients, and f_E
  * runs as begin (operand prep + synthesis of own m into part sp of `fourier`,
- * a caller-owned part-major buffer [S][nb][nlat/2][4][Lp][2] complex) ->
+ * a caller-owned part-major buffer [S][nb][nlat/2][Lp][4][2] complex) ->
  * caller all-gathers the S parts of `fourier` (NCCL) -> end (ring kernel over
  * all latitudes + analysis of own m into fe).  S = 1 restores the unsplit plan.
  * The per-m and per-latitude arithmetic is unchanged, so results are

@@ -106,7 +106,7 @@ struct sdcsw_exchange {
   long long fpart;           // double2 per part of F at batch 1 (J Lp 8)
   char* mem;                 // IPC allocation: X | F | node flags | Fourier flags
   double2* X;                // [2][M][2][S1]
-  double2* F;                // [2][S][max_batch][J][4][Lp][2] (S > 1)
+  double2* F;                // [2][S][max_batch][J][Lp][4][2] (S > 1)
   PeerFlags *nflag, *fflag;
   char* local;               // private buffers
   double2 *fe0, *fe_loc, *fi_loc;
