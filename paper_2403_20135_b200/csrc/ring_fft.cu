@@ -22,6 +22,7 @@
 #ifndef SDCSW_EXP
 #define SDCSW_EXP 0
 #endif
+
 namespace sdcsw {
 #if SDCSW_EXP == 4
 __device__ unsigned long long g_rtimes[1 << 16];
@@ -202,14 +203,14 @@ constexpr size_t ring_smem_t() {
 // transforms of length N at Z[f * padded<N>()], reading generation SHI and
 // writing generation SHO; twp = this pass's twiddle table.
 template <int N, int R, int P, bool INV, int NF, int THREADS, int SHI, int SHO>
-__device__ __forceinline__ void pass(double2* Z, const double2* twp, int tid) {
+__device__ __forceinline__ void pass(double2* Z, const double2* twp) {
   constexpr int NR = N / R;
   constexpr int ITEMS = NF * NR;
   constexpr int MAXIT = (ITEMS + THREADS - 1) / THREADS;
   double2 v[MAXIT][R];
 #pragma unroll
   for (int q = 0; q < MAXIT; ++q) {
-    const int it = tid + q * THREADS;
+    const int it = threadIdx.x + q * THREADS;
     if (ITEMS % THREADS == 0 || it < ITEMS) {
       const int f = it / NR, i = it - f * NR;
       const double2* X = Z + f * padded<N>();
@@ -230,7 +231,7 @@ __device__ __forceinline__ void pass(double2* Z, const double2* twp, int tid) {
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < MAXIT; ++q) {
-    const int it = tid + q * THREADS;
+    const int it = threadIdx.x + q * THREADS;
     if (ITEMS % THREADS == 0 || it < ITEMS) {
       const int f = it / NR, i = it - f * NR;
       double2* X = Z + f * padded<N>();
@@ -245,20 +246,20 @@ __device__ __forceinline__ void pass(double2* Z, const double2* twp, int tid) {
 
 // inverse passes s in [S, n-1) and forward passes s in [S, n)
 template <int N, int S, int THREADS>
-__device__ __forceinline__ void inverse_mid(double2* Z, const double2* tw, int tid) {
+__device__ __forceinline__ void inverse_mid(double2* Z, const double2* tw) {
   if constexpr (S < RadixPlan<N>::n - 1) {
     pass<N, inv_radix<N>(S), inv_prefix<N>(S), true, 4, THREADS, gen_shift<N>(S - 1),
-         gen_shift<N>(S)>(Z, tw + tw_off_inv<N>(S), tid);
-    inverse_mid<N, S + 1, THREADS>(Z, tw, tid);
+         gen_shift<N>(S)>(Z, tw + tw_off_inv<N>(S));
+    inverse_mid<N, S + 1, THREADS>(Z, tw);
   }
 }
 template <int N, int S, int THREADS>
-__device__ __forceinline__ void forward_rest(double2* Z, const double2* tw, int tid) {
+__device__ __forceinline__ void forward_rest(double2* Z, const double2* tw) {
   constexpr int n = RadixPlan<N>::n;
   if constexpr (S < n) {
     pass<N, fwd_radix<N>(S), fwd_prefix<N>(S), false, 5, THREADS, gen_shift<N>(n - 2 + S),
-         gen_shift<N>(n - 1 + S)>(Z, tw + tw_off_fwd<N>(S), tid);
-    forward_rest<N, S + 1, THREADS>(Z, tw, tid);
+         gen_shift<N>(n - 1 + S)>(Z, tw + tw_off_fwd<N>(S));
+    forward_rest<N, S + 1, THREADS>(Z, tw);
   }
 }
 
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
   }
   RT(1)
   if constexpr (!TWG) mbar_wait(&twbar, 0);  // (the staging barrier above ordered the init)
-  inverse_mid<N, 1, THREADS>(Z, tw, threadIdx.x);
+  inverse_mid<N, 1, THREADS>(Z, tw);
   RT(2)
 
   // ---- fused: last inverse pass (radix 3, P = N/3), grid products, first
@@ -509,7 +510,7 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
     __syncthreads();
   }
   RT(3)
-  forward_rest<N, 1, THREADS>(Z, tw, threadIdx.x);
+  forward_rest<N, 1, THREADS>(Z, tw);
   if (SDCSW_TRIG_RING == 2) SDCSW_PDL_TRIGGER();
   RT(4)
 
