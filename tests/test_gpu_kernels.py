@@ -750,3 +750,41 @@ def ctypes_stream():
     import torch
 
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def test_dsdc_order_and_sweep_monotonicity_on_the_sphere():
+    """The reference's integrator oracles (pkg/tests/test_integrators.py:270-305)
+    run on the device stepper with the spherical problem: M = K = 4 dSDC
+    converges with order >= 3.5 in dt (errors against a fine-step run of the
+    same scheme over a fixed 2 h horizon), and at fixed dt the error falls
+    monotonically with the sweep count K = 1..4."""
+    import torch
+
+    from paper_2403_20135_b200.integrators import DeviceStepper
+
+    p = gpu(63)
+    u0 = torch.from_numpy(random_initial_state(p.grid, 5)).to(p.device).reshape(-1).contiguous()
+    horizon = 7200.0
+
+    def run(n_steps, k):
+        cfg = SdcConfig(table=CollocationTable.radau_right(4), n_sweeps=k,
+                        mode=SweepMode.DIAGONAL_PARALLEL)
+        st = DeviceStepper(p, cfg, horizon / n_steps, serial=False)
+        u = u0.clone()
+        st.run(u, n_steps)
+        torch.cuda.synchronize()
+        st.close()
+        return u.cpu().numpy()
+
+    ref = run(256, 4)
+    o = oracle_for(p)
+    dts, errs = [], []
+    for n in (8, 16, 32, 64):
+        dts.append(horizon / n)
+        errs.append(max(relative_l2(run(n, 4), ref, o)))
+    slope = np.polyfit(np.log(dts), np.log(errs), 1)[0]
+    print(f"dSDC M=K=4 order on the sphere: slope {slope:.2f}, errors {errs}")
+    assert slope >= 3.5, (slope, errs)
+    by_k = [max(relative_l2(run(16, k), ref, o)) for k in range(1, 5)]
+    print(f"errors by sweep count K=1..4 at 16 steps: {by_k}")
+    assert all(b < a for a, b in zip(by_k, by_k[1:])), by_k
