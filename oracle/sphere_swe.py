@@ -3,8 +3,12 @@ r"""CPU restatement of the spherical shallow-water split problem.
 TEST INFRASTRUCTURE ONLY (see ``oracle/__init__.py``).  Parity of the SH
 arithmetic is UNPINNED with respect to the reference (it has no spherical
 problem, ``SPEC.md:8``); it is pinned by analytic known-answer tests in
-``tests/test_oracle_sphere.py`` and the reference contracts
-``pkg/tests/_contracts.py:18-41``.
+``tests/test_oracle_sphere.py`` - including the m > 0 flows of
+``tests/sphere_kats.py`` (tilted solid-body rotation, tilted potential flow,
+Rossby-Haurwitz wave 4) with a sign-mutation check of every wind-synthesis
+term - and the reference contracts ``pkg/tests/_contracts.py:18-41``.
+:class:`SphericalShallowWaterFast` (end of file) is the same problem with the
+transforms organised for speed; it is the CPU baseline ``bench.py`` times.
 
 Restated from the planar template ``pkg/src/parsdc/problems/swe.py`` with
 ``k^2 -> lambda_n = n(n+1)/a^2`` and FFT2 -> spherical-harmonic transform
