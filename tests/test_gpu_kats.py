@@ -100,14 +100,19 @@ _FLOWS = {
 }
 
 
-@pytest.mark.parametrize("trunc", [63, 127])
+@pytest.mark.parametrize("trunc", [63, 127, 255])
 @pytest.mark.parametrize("name", sorted(_FLOWS))
 def test_known_answer_flows_m_positive(trunc, name):
     p, o = pair(trunc)
     x, want = _FLOWS[name](o)
     fe, fi = p.f_expl(x), p.f_impl(x)
     err = field_errors(o, fe + fi, want, [fe, fi])
-    assert (max(err[:2]) if name.startswith("rossby") else max(err)) <= 1e-10, err
+    # the delta balance is a cancellation whose rounding noise in the (zero)
+    # high-degree coefficients is amplified by lambda_n ~ n^2: 2e-12 at T63,
+    # up to 2.4e-10 at T255 (measured); Phi' and zeta stay <= 1e-11
+    tol = 1e-10 if trunc <= 127 else 1e-9
+    assert (max(err[:2]) if name.startswith("rossby") else max(err)) <= tol, err
+    assert max(err[:2]) <= 1e-10, err
 
 
 def test_known_answer_flows_catch_device_sign_error():
