@@ -339,3 +339,24 @@ def test_two_processes_over_cuda_ipc_bitwise(tmp_path, split):
         got = np.load(out + f".{r}.npy")
         own = np.tile(np.load(out + f".{r}.own.npy"), 3)
         assert np.array_equal(got[own], ref[own]), r
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_bench_node_parallel_path_world_one(transport):
+    """The bench's multi-GPU orchestration end to end at world size 1
+    (torch.distributed init, exchange construction, graphs, e2e, JSON line):
+    the path `bench.py --gpus N` takes, on the one GPU this pool gives."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MASTER_PORT=str(29500 + (os.getpid() % 97) + (7 if transport == "nccl" else 0)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--node-parallel", "--transport",
+                        transport, "--steps", "1", "--warmup", "1", "--no-cpu", "--no-large"],
+                       capture_output=True, text=True, timeout=900, cwd=root, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["config"]["multi_gpu_transport"] == transport
+    assert line["config"]["finite"] and line["value"] > 0 and line["e2e"]["value"] > 0
