@@ -348,7 +348,8 @@ class DeviceSweepState:
     counted as an evaluation).  :meth:`distinct_node_arrays` counts the arrays
     the device actually retains between sweeps: u0, fe0 and the M nodes' fe
     and fi, 2M + 2 (the reference's bound is 2M + 3,
-    ``pkg/tests/test_integrators.py:228-241``)."""
+    ``pkg/tests/test_integrators.py:228-241``).  Valid inside the callback
+    only: the next sweep overwrites the buffers the views copy from."""
 
     def __init__(self, stepper, u, k):
         self._st, self._u, self.sweep = stepper, u, k
