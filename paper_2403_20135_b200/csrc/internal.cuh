@@ -98,6 +98,12 @@ struct Plan {
   // table-streaming analysis (T >= 400); tma_ok = maps built
   alignas(64) unsigned long long tmap[2][16];
   bool tma_ok;
+  // TMA tensor maps over the analysis data for the ring kernel's output
+  // stores (ring_fft.cu): record order, fragment-order P part, H part;
+  // gmap_rows = rows (wavenumbers) per store box, 0 = plain stores
+  alignas(64) unsigned long long gmap[3][16];
+  int gmap_rows;
+  bool gmap_frag;  // the fragment-order maps were built
   // spectral split: the wavenumbers are partitioned over S ranks of a
   // spectral group (pairs (m, T-m) dealt round-robin); this rank owns part
   // split_sp.  S = 1: unsplit (m_part = 0, m_k = m, Lp = L, lists null).
@@ -500,6 +506,7 @@ cudaError_t launch_axpy(long long n, const double* x, double w, const double* y,
                         cudaStream_t s);
 
 cudaError_t make_table_maps(Plan& p);
+cudaError_t make_gan_maps(Plan& p);
 cudaError_t configure_synthesis_bulk();
 cudaError_t configure_analysis_bulk();
 bool synthesis_bulk_ok(const Plan& p, int nb);

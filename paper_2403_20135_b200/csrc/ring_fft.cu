@@ -15,7 +15,12 @@
 // Output per (b, pair, m <= T): the seven analysis data slots, pre-weighted,
 // pre-multiplied by i m where the analysis needs it and folded into symmetric
 // (N+S) / antisymmetric (N-S) parts.
+#include <cstdlib>
+#include <cstring>
 #include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "fft_math.cuh"
 
@@ -300,6 +305,35 @@ constexpr int ring_resident() {
              : ring_min_blocks<N, THREADS>();
 }
 
+// Output stores of the ring kernel: the analysis data of one latitude pair is
+// a column of the [state][m][j] layout (224 bytes per m, strided by J x 224),
+// so the CTA stages its values in shared memory (the dead FFT arrays) and one
+// thread writes them with TMA tensor stores (box rows = wavenumbers), instead
+// of 16-byte stores from every thread.
+struct alignas(64) GanMaps {
+  CUtensorMap rec;  // record order: {28 doubles, J, rows}
+  CUtensorMap fp;   // fragment order, P part: {8 doubles, j & 3, fold, j >> 2, rows}
+  CUtensorMap fh;   // fragment order, H part: {6 doubles, j & 3, fold, j >> 2, rows}
+  int rows;         // wavenumbers per store box (divides L); 0 = plain stores
+  int row0;         // first row of the launch's workspace (batch offset x L)
+};
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1,
+                                             int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<unsigned long long>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const void* src, int c0, int c1,
+                                             int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+          reinterpret_cast<unsigned long long>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(src))
+      : "memory");
+}
+
 template <int N, int THREADS, bool SPLIT>
 __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring(const double2* __restrict__ fsyn,
                                                   double2* __restrict__ gan, int J, int T,
@@ -310,10 +344,11 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
                                                   double two_omega,
                                                   const int* __restrict__ m_part,
                                                   const int* __restrict__ m_k, int Lp, int nbg,
-                                                  int frag, const RingPeer rp) {
+                                                  int frag, const RingPeer rp,
+                                                  const __grid_constant__ GanMaps gm) {
   SDCSW_PDL_ENTRY();
   if (SDCSW_TRIG_RING == 1) SDCSW_PDL_TRIGGER();
-  extern __shared__ double2 sm2[];
+  extern __shared__ __align__(128) double2 sm2[];
   constexpr int NP = padded<N>();
   constexpr int NS = RadixPlan<N>::n;
   constexpr int TWN = tw_total<N>();
@@ -515,38 +550,91 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
   RT(4)
 
   const double h = 0.5 / (double)N;
-  // analysis data (internal.cuh): record order - thread (m, fold) writes the
-  // fold's seven slots (112 contiguous bytes); fragment order (frag, TMA
-  // analysis) - the four P slots (64 bytes) and three H slots (48 bytes)
-  double* outp = reinterpret_cast<double*>(gan) + (size_t)b * L * J * 28;
-  const int pofs = frag ? gan_off(j, 0, kXPhi, 0) : j * 28;
-  const int hofs = frag ? gan_off(j, 0, kYPhi, 0) : j * 28 + 2 * kYPhi;
-  const int fstride = frag ? 56 : 14;
   constexpr int SHL = gen_shift<N>(2 * NS - 2);
-  for (int it = threadIdx.x; it < 2 * L; it += THREADS) {
+  // the seven analysis data slots (internal.cuh order) of item (m, fold)
+  auto item = [&](int it, double2 (&o)[kNumSlots]) {
     const int m = it >> 1, fold = it & 1;
     const double dm = (double)m;
     double2 v[5];
 #pragma unroll
-    for (int o = 0; o < 5; ++o) {
-      const double2 zm = Z[o * NP + pzv(m, SHL)], zc = Z[o * NP + pzv(m == 0 ? 0 : N - m, SHL)];
+    for (int q = 0; q < 5; ++q) {
+      const double2 zm = Z[q * NP + pzv(m, SHL)], zc = Z[q * NP + pzv(m == 0 ? 0 : N - m, SHL)];
       // X = FFT(north)/N, Y = FFT(south)/N; fold 0: S = X + Y, fold 1: A = X - Y
       const double2 X = make_double2(h * (zm.x + zc.x), h * (zm.y - zc.y));
       const double2 Y = make_double2(h * (zm.y + zc.y), -h * (zm.x - zc.x));
-      v[o] = fold ? csub(X, Y) : cadd(X, Y);
+      v[q] = fold ? csub(X, Y) : cadd(X, Y);
     }
-    double* bm = outp + (size_t)m * J * 28 + fold * fstride;
-    double2* dp = reinterpret_cast<double2*>(bm + pofs);  // X_phi, X_zeta, X_delta, X_ke
-    double2* dh = reinterpret_cast<double2*>(bm + hofs);  // Y_phi, Y_zeta, Y_delta
     // A = eta U: X_zeta = -(i m A) ws, Y_delta = A ws; B = eta V: X_delta = (i m B) ws,
     // Y_zeta = B ws; C = Phi U: X_phi = -(i m C) ws; D = Phi V: Y_phi = D ws; X_ke = E wk
-    dp[kXPhi] = make_double2(dm * v[2].y * ws, -dm * v[2].x * ws);
-    dp[kXZeta] = make_double2(dm * v[0].y * ws, -dm * v[0].x * ws);
-    dp[kXDelta] = make_double2(-dm * v[1].y * ws, dm * v[1].x * ws);
-    dp[kXKe] = make_double2(v[4].x * wk, v[4].y * wk);
-    dh[kYPhi - kYPhi] = make_double2(v[3].x * ws, v[3].y * ws);
-    dh[kYZeta - kYPhi] = make_double2(v[1].x * ws, v[1].y * ws);
-    dh[kYDelta - kYPhi] = make_double2(v[0].x * ws, v[0].y * ws);
+    o[kXPhi] = make_double2(dm * v[2].y * ws, -dm * v[2].x * ws);
+    o[kXZeta] = make_double2(dm * v[0].y * ws, -dm * v[0].x * ws);
+    o[kXDelta] = make_double2(-dm * v[1].y * ws, dm * v[1].x * ws);
+    o[kXKe] = make_double2(v[4].x * wk, v[4].y * wk);
+    o[kYPhi] = make_double2(v[3].x * ws, v[3].y * ws);
+    o[kYZeta] = make_double2(v[1].x * ws, v[1].y * ws);
+    o[kYDelta] = make_double2(v[0].x * ws, v[0].y * ws);
+  };
+  constexpr int MI = (2 * ((N + 2) / 3) + THREADS - 1) / THREADS;  // items per thread, L <= (N + 2) / 3
+  if (gm.rows > 0 && L <= (N + 2) / 3) {  // (then the boxes fit in the 5 FFT arrays)
+    // staged in the FFT arrays as the store boxes: record order [m][fold][7 slots];
+    // fragment order [m][fold][4 P slots] then, from L x 128 bytes, [m][fold][3 H slots]
+    double2 o[MI][kNumSlots];
+#pragma unroll
+    for (int q = 0; q < MI; ++q) {
+      const int it = threadIdx.x + q * THREADS;
+      if (it < 2 * L) item(it, o[q]);
+    }
+    __syncthreads();  // every read of the FFT arrays is done
+    double2* st = Z;
+#pragma unroll
+    for (int q = 0; q < MI; ++q) {
+      const int it = threadIdx.x + q * THREADS;
+      if (it < 2 * L) {
+        if (!frag) {
+#pragma unroll
+          for (int k = 0; k < kNumSlots; ++k) st[it * kNumSlots + k] = o[q][k];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) st[it * 4 + k] = o[q][k];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) st[8 * L + it * 3 + k] = o[q][4 + k];
+        }
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int row = gm.row0 + b * L;
+      for (int m0 = 0; m0 < L; m0 += gm.rows) {
+        if (!frag) {
+          tma_store_3d(&gm.rec, st + m0 * 2 * kNumSlots, 0, j, row + m0);
+        } else {
+          tma_store_5d(&gm.fp, st + m0 * 8, 0, j & 3, 0, j >> 2, row + m0);
+          tma_store_5d(&gm.fh, st + 8 * L + m0 * 6, 0, j & 3, 0, j >> 2, row + m0);
+        }
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // before the CTA exits
+    }
+  } else {
+    // record order - thread (m, fold) writes the fold's seven slots (112
+    // contiguous bytes); fragment order (frag, TMA analysis) - the four P
+    // slots (64 bytes) and three H slots (48 bytes)
+    double* outp = reinterpret_cast<double*>(gan) + (size_t)b * L * J * 28;
+    const int pofs = frag ? gan_off(j, 0, kXPhi, 0) : j * 28;
+    const int hofs = frag ? gan_off(j, 0, kYPhi, 0) : j * 28 + 2 * kYPhi;
+    const int fstride = frag ? 56 : 14;
+    for (int it = threadIdx.x; it < 2 * L; it += THREADS) {
+      double2 o[kNumSlots];
+      item(it, o);
+      double* bm = outp + (size_t)(it >> 1) * J * 28 + (it & 1) * fstride;
+      double2* dp = reinterpret_cast<double2*>(bm + pofs);  // X_phi, X_zeta, X_delta, X_ke
+      double2* dh = reinterpret_cast<double2*>(bm + hofs);  // Y_phi, Y_zeta, Y_delta
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dp[k] = o[k];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) dh[k] = o[4 + k];
+    }
   }
   if constexpr (SPLIT) {
     if (rp.flags != nullptr) {  // the last CTA to finish completes exchange fx for this rank
@@ -631,19 +719,68 @@ bool ring_pass_twiddles(int nlon, const double2* w, std::vector<double2>& out) {
   return false;
 }
 
+// Store maps over the whole analysis workspace (rows = max_batch x L).
+// Box rows: L up to 256, else the largest multiple of 4 dividing L up to 256
+// (box offsets in shared memory stay 128-byte aligned); none: plain stores.
+cudaError_t make_gan_maps(Plan& p) {
+  p.gmap_rows = 0;
+  p.gmap_frag = false;
+  const char* env = getenv("SDCSW_RING_TMA_STORE");
+  if (env != nullptr && atoi(env) == 0) return cudaSuccess;
+  const int L = p.L, J = p.J;
+  int rows = L <= 256 ? L : 0;
+  for (int r = 256; rows == 0 && r >= 4; r -= 4)
+    if (L % r == 0) rows = r;
+  if (rows == 0) return cudaSuccess;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || !fn || q != cudaDriverEntryPointSuccess) return cudaSuccess;
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  const cuuint64_t R = (cuuint64_t)p.max_batch * L, rs = (cuuint64_t)J * 28 * sizeof(double);
+  auto enc = [&](int i, void* base, cuuint32_t rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                 const cuuint32_t* box) {
+    const cuuint32_t elem[5] = {1, 1, 1, 1, 1};
+    return encode(reinterpret_cast<CUtensorMap*>(&p.gmap[i]), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, base,
+                  dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  {
+    const cuuint64_t dims[3] = {28, (cuuint64_t)J, R}, strides[2] = {28 * sizeof(double), rs};
+    const cuuint32_t box[3] = {28, 1, (cuuint32_t)rows};
+    if (!enc(0, p.gan, 3, dims, strides, box)) return cudaSuccess;
+  }
+  p.gmap_rows = rows;
+  if (J % 4 == 0) {  // fragment order (gan_off): [j >> 2][fold][P: j & 3 x 8 | H: j & 3 x 6]
+    const cuuint64_t dp[5] = {8, 4, 2, (cuuint64_t)J / 4, R}, dh[5] = {6, 4, 2, (cuuint64_t)J / 4, R};
+    const cuuint64_t sp[4] = {64, 448, 896, rs}, sh[4] = {48, 448, 896, rs};
+    const cuuint32_t bp[5] = {8, 1, 2, 1, (cuuint32_t)rows}, bh[5] = {6, 1, 2, 1, (cuuint32_t)rows};
+    p.gmap_frag = enc(1, p.gan, 5, dp, sp, bp) &&
+                  enc(2, reinterpret_cast<double*>(p.gan) + 32, 5, dh, sh, bh);
+  }
+  return cudaSuccess;
+}
+
 static cudaError_t ring_impl(const Plan& p, const double2* fsyn, double2* gan, const int* m_part,
                              const int* m_k, int Lp, int nb, cudaStream_t s,
                              const RingPeer& rp = RingPeer{}) {
   dim3 grid(p.J, nb);
+  const int frag = (int)tma_active(p);
+  GanMaps gm;
+  std::memcpy(&gm.rec, p.gmap[0], sizeof(CUtensorMap));
+  std::memcpy(&gm.fp, p.gmap[1], sizeof(CUtensorMap));
+  std::memcpy(&gm.fh, p.gmap[2], sizeof(CUtensorMap));
+  gm.rows = frag && !p.gmap_frag ? 0 : p.gmap_rows;
+  gm.row0 = (int)((gan - p.gan) / ((size_t)p.J * p.L * kNumSlots * 2)) * p.L;
 #define SDCSW_RING_LAUNCH(NV, TV)                                                                  \
   if (p.nlon == NV) {                                                                              \
     constexpr size_t smem = ring_smem_t<NV, TV>();                                                 \
     if (m_part != nullptr)                                                                         \
       launch_k(k_ring<NV, TV, true>, grid, TV, smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn,        \
-               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb, (int)tma_active(p), rp);   \
+               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb, frag, rp, gm);             \
     else                                                                                           \
       launch_k(k_ring<NV, TV, false>, grid, TV, smem, s, fsyn, gan, p.J, p.T, p.mu, p.wsyn,       \
-               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb, (int)tma_active(p), rp);   \
+               p.wke, p.twiddle, 2.0 * p.omega, m_part, m_k, Lp, nb, frag, rp, gm);             \
     return cudaGetLastError();                                                                     \
   }
   if (nb >= kRingTputBatch) {

@@ -294,6 +294,7 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
       (e = configure_synthesis_bulk()) != cudaSuccess ||
       (e = configure_analysis_bulk()) != cudaSuccess ||
       (e = make_table_maps(p)) != cudaSuccess ||
+      (e = make_gan_maps(p)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess) {
     int st = cuda_status(e, "sdcsw_plan_create");
     void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,

@@ -186,7 +186,7 @@ class SphericalShallowWater(DeviceProblem):
         super().__init__()
         import torch
 
-        base = grid_for(trunc)
+        base = grid_for(trunc) if not (nlat and nlon) else None
         self.grid = SphereGrid(
             trunc=trunc,
             nlat=nlat or base.nlat,

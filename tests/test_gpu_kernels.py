@@ -788,3 +788,43 @@ def test_dsdc_order_and_sweep_monotonicity_on_the_sphere():
     by_k = [max(relative_l2(run(16, k), ref, o)) for k in range(1, 5)]
     print(f"errors by sweep count K=1..4 at 16 steps: {by_k}")
     assert all(b < a for a, b in zip(by_k, by_k[1:])), by_k
+
+
+@pytest.mark.parametrize(
+    "trunc,grid,nb,max_batch",
+    [(42, (64, 192), 2, 2), (85, (128, 384), 3, 3), (127, None, 4, 4), (127, None, 20, 32),
+     (383, (576, 1536), 1, 1), (511, None, 2, 2)],
+)
+def test_ring_tma_stores_match_plain_stores(trunc, grid, nb, max_batch):
+    """The ring kernel's analysis data written by TMA tensor stores from shared
+    memory (record order; fragment order from T200 and for ensembles; one box
+    of L rows - 43 and 86 included - or 192 / 256-row boxes at T383 / T511) is bitwise the data of the
+    per-thread stores (SDCSW_RING_TMA_STORE=0): f_E agrees bit for bit."""
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    plans = []
+    for mode in ("1", "0"):
+        old = os.environ.get("SDCSW_RING_TMA_STORE")
+        os.environ["SDCSW_RING_TMA_STORE"] = mode
+        try:
+            nlat, nlon = grid or (None, None)
+            plans.append(SphericalShallowWater(trunc, nlat=nlat, nlon=nlon, max_batch=max_batch))
+        finally:
+            if old is None:
+                del os.environ["SDCSW_RING_TMA_STORE"]
+            else:
+                os.environ["SDCSW_RING_TMA_STORE"] = old
+    import torch
+
+    g, c = plans[0].grid, plans[0].n_coef
+    states = np.stack([random_initial_state(g, 3 + s) for s in range(nb)])
+    states[:, :c] = 4e-3 * states[:, c : 2 * c] * 1e6
+    outs = []
+    for p in plans:
+        u = torch.from_numpy(states).to(p.device)
+        outs.append(p.f_expl_device(u, p.empty_states(nb), nb).cpu().numpy())
+    a, b = outs
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    assert np.all(np.isfinite(a)) and np.linalg.norm(a) > 0
+    for p in plans:
+        p.close()
