@@ -241,6 +241,16 @@ int sdcsw_transform_stage(sdcsw_plan* plan, int stage, const double* in, double*
  * order for the table-streaming analysis (T >= 400; gan_off in internal.cuh). */
 int sdcsw_workspace(sdcsw_plan* plan, int which, void** ptr, long long* bytes);
 
+/* Transform family of the plan: *kind = 0 when f_E contracts with the P and H
+ * tables; 1 when it runs H-free (table-streaming plans, T >= 200 or ensembles,
+ * unless SDCSW_PONLY=0 at plan creation): P to degree T+1 and the derivative
+ * recurrence H_n = (n+1) eps_n P_{n-1} - n eps_{n+1} P_{n+1} on the coefficients,
+ * 9 instead of 13 transforms per f_E.  The analysis workspace (which 1) then
+ * holds 5 slots per (m, pair, fold): [m][nlat/2 / 4][2][4][5] complex.  Both
+ * compute the reference's f_expl (problems/swe.py:174-205 restated on the sphere)
+ * to rounding; *rows = packed table rows streamed per analysis/synthesis. */
+int sdcsw_plan_transform_kind(sdcsw_plan* plan, int* kind, int* rows);
+
 /* Spectral split (more GPUs than collocation nodes): the plan's
  * wavenumbers are partitioned over the S ranks of a spectral group, pairs
  * (m, T-m) dealt round-robin, and this rank keeps part sp.  Afterwards

@@ -44,6 +44,7 @@ EXPORTS = (
     "sdcsw_axpy",
     "sdcsw_transform_stage",
     "sdcsw_workspace",
+    "sdcsw_plan_transform_kind",
     "sdcsw_plan_set_split",
     "sdcsw_split_info",
     "sdcsw_split_f_expl_begin",
@@ -135,6 +136,7 @@ _SIGS = {
     "sdcsw_axpy": [_ll, _p, ctypes.c_double, _p, _p, _p],
     "sdcsw_transform_stage": [_p, _i, _p, _p, _i, _p],
     "sdcsw_workspace": [_p, _i, ctypes.POINTER(_p), ctypes.POINTER(_ll)],
+    "sdcsw_plan_transform_kind": [_p, _ip, _ip],
     "sdcsw_plan_set_split": [_p, _i, _i, _p, _ll],
     "sdcsw_split_info": [_p, _ip, _ip, _ip],
     "sdcsw_split_f_expl_begin": [_p, _p, _i, _p],

@@ -117,6 +117,32 @@ struct Plan {
   int* own_idx;     // own coefficient indices, ascending
   int n_own_idx;
   double2* fsyn_ext;  // part-major Fourier buffer [S][nb][J][Lp][4][2] (caller-owned)
+  // H-free transforms (legendre_ponly.cu, table-streaming path): H = (1 - mu^2) dP/dmu
+  // is replaced by the recurrence H_n = a_n P_{n-1} + b_n P_{n+1} (a_n = (n+1) eps_n,
+  // b_n = -n eps_{n+1}, eps_n = sqrt((n^2 - m^2) / (4 n^2 - 1))), applied to the
+  // coefficients: the synthesis runs 4 P transforms to degree T+1 and the analysis
+  // 5 (A, B, C, D, E) whose neighbouring degrees the assembly combines; no H table
+  int ponly;          // 1: active for unsplit plans (SDCSW_PONLY; default from T200)
+  int rowsP, CP;      // P rows (degrees m..T+1, parity-sorted, padded to 8); extended triangle
+  double* ptabP;      // [rowsP][J] (the analysis TMA map streams this)
+  double* ptabP_s;    // [rowsP/4][J/8][8][4] synthesis fragment order
+  int* rowoffP;       // [T+2]
+  int* n_evenP;       // [T+1]
+  int* rowP_n;        // [rowsP] degree k of each P row (-1: padding)
+  int* moffP;         // [T+2] offsets of the extended triangle (T+2-m entries per m)
+  int4* cvt_rows;     // [rowsP] xsyn rows of (m,k), (m,k-1), (m,k+1) (-1: none), P-triangle index
+  double2* cvt_ab;    // [rowsP] (a_{k+1}, b_{k-1}): weights of X_{k+1}, X_{k-1}
+  int2* asm_pos;      // [C] (extended-triangle index of (m,n), m)
+  double2* asm_ab;    // [C] (a_n, b_n)
+  int* anal_workP;    // [n_anal_workP] (m << 16 | 64-row block) over the P rows
+  int n_anal_workP;
+  int* own_workP;     // split plans: the work items of own m
+  int n_own_workP;
+  double* xsynP;      // [max_batch][rowsP][8] P-only synthesis operand (fragment order per batch)
+  double* ghat;       // [max_batch][CP][10] P analyses of A, B, C, D, E to degree T+1
+  alignas(64) unsigned long long tmapP[16];  // TMA map over ptabP
+  alignas(64) unsigned long long gmapP[16];  // ring store map of the 5-slot analysis data
+  int gmapP_rows;                             // rows per store box (0: plain stores)
   // planar problem (kind 1): N x N grid, spectra [N (kx)][NH = N/2 + 1 (ky)],
   // C = N * NH coefficients per field (lam = k^2 = laplacian symbol)
   int pn, pnh;
@@ -231,15 +257,44 @@ __device__ __forceinline__ void write_xsyn_half(double* __restrict__ rec, size_t
 
 #endif
 
+// P-only operand: 8 doubles per (P row, state) in two parts of four, part 0 =
+// (U', V') (re, im) with U' = i m chi / a + sum of the recurrence terms of
+// -psi / a, V' likewise of (i m psi / a, chi / a), part 1 = (zeta, Phi); same
+// fragment order as xsyn with two parts: [row quad][part][b][r % 4][4].
+constexpr int kXsynP = 8;
+// P-only analysis data per (state, m, pair j): [j >> 2][fold S, A][j & 3][5 slots
+// A, B, C, D (w_s-weighted), E (w_ke-weighted)][re, im] = 20 doubles per j
+constexpr int kSlotsP = 5;
+constexpr int kGhat = 2 * kSlotsP;  // doubles per (extended coefficient, state) of ghat
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int ganp_off(int j, int fold, int slot, int ri) {
+  return ((j >> 2) * 2 + fold) * 40 + (j & 3) * 10 + slot * 2 + ri;
+}
+
+// the H-free transforms serve this plan's f_E (every launcher routes on it, split or not)
+inline bool ponly_on(const Plan& p) { return p.kind == 0 && p.ponly && p.xsynP != nullptr; }
+
 // Transform workspaces of one f_E chain (Fourier + analysis data); concurrent
-// chains use disjoint batch slices of the plan's workspaces.
+// chains use disjoint batch slices of the plan's workspaces (the H-free path's
+// analysis data is packed at 5 slots per (pair, m, fold) instead of 7).
 struct Work {
   double2* fsyn;
   double2* gan;
+  double* xsp;   // P-only operand slice (null unless ponly)
+  double* ghat;  // P-only analysis output slice
 };
 inline Work plan_work(const Plan& p, int batch_offset = 0) {
   const size_t per = (size_t)p.J * p.L * 2;
-  return Work{p.fsyn + per * 4 * batch_offset, p.gan + per * kNumSlots * batch_offset};
+  const bool po = ponly_on(p);
+  Work w{p.fsyn + per * 4 * batch_offset, p.gan + per * (po ? kSlotsP : kNumSlots) * batch_offset,
+         nullptr, nullptr};
+  if (po) {
+    w.xsp = p.xsynP + (size_t)batch_offset * p.rowsP * kXsynP;
+    w.ghat = p.ghat + (size_t)batch_offset * p.CP * kGhat;
+  }
+  return w;
 }
 
 // launchers (return cudaError_t of the launch)
@@ -506,6 +561,16 @@ cudaError_t launch_axpy(long long n, const double* x, double w, const double* y,
                         cudaStream_t s);
 
 cudaError_t make_table_maps(Plan& p);
+// H-free path (legendre_ponly.cu): plan tables / maps, and the f_E chain stages
+cudaError_t ponly_setup(Plan& p, const double* ptab, const int* rowoff, const int* row_n,
+                        const double* mu_north);
+void ponly_free(Plan& p);
+// (the generic launchers below route to these when ponly_on(p); split plans pass
+// their own wavenumbers / work items)
+cudaError_t launch_synthesis_ponly(const Plan& p, double2* fsyn, const int* mlist, int nm, int Lp,
+                                   double* xsp, const double* xsyn, int nb, cudaStream_t s,
+                                   int* step_counter, const SynDst& sd);
+cudaError_t launch_analysis_ponly(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s);
 cudaError_t make_gan_maps(Plan& p);
 cudaError_t configure_synthesis_bulk();
 cudaError_t configure_analysis_bulk();

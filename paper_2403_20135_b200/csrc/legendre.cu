@@ -839,19 +839,29 @@ static cudaError_t synthesis_impl(const Plan& p, double2* fsyn, const int* mlist
                                   const double* xsyn, int nb, cudaStream_t s, int* step_counter,
                                   const SynDst& sd);
 
+// (H-free plans, ponly_on: operand conversion + P-only synthesis, legendre_ponly.cu)
 cudaError_t launch_synthesis(const Plan& p, const Work& w, const double* xsyn, int nb,
                              cudaStream_t s, int* step_counter) {
+  if (ponly_on(p))
+    return launch_synthesis_ponly(p, w.fsyn, nullptr, p.T + 1, p.T + 1, w.xsp, xsyn, nb, s,
+                                  step_counter, SynDst{});
   return synthesis_impl(p, w.fsyn, nullptr, p.T + 1, p.T + 1, xsyn, nb, s, step_counter, SynDst{});
 }
 
 cudaError_t launch_synthesis_split(const Plan& p, const double* xsyn, int nb, cudaStream_t s) {
   double2* part = p.fsyn_ext + (size_t)p.split_sp * nb * p.J * p.Lp * 8;
+  if (ponly_on(p))
+    return launch_synthesis_ponly(p, part, p.own_m, p.n_own_m, p.Lp, p.xsynP, xsyn, nb, s, nullptr,
+                                  SynDst{});
   return synthesis_impl(p, part, p.own_m, p.n_own_m, p.Lp, xsyn, nb, s, nullptr, SynDst{});
 }
 
 cudaError_t launch_synthesis_peer(const Plan& p, const double* xsyn, int nb, cudaStream_t s,
                                   const SynDst& d, int* step_counter) {
   if (p.split_S < 2 || d.n < 1 || d.n > kMaxPeers) return cudaErrorInvalidValue;
+  if (ponly_on(p))
+    return launch_synthesis_ponly(p, nullptr, p.own_m, p.n_own_m, p.Lp, p.xsynP, xsyn, nb, s,
+                                  step_counter, d);
   return synthesis_impl(p, nullptr, p.own_m, p.n_own_m, p.Lp, xsyn, nb, s, step_counter, d);
 }
 
@@ -915,6 +925,7 @@ static cudaError_t analysis_impl(const Plan& p, const Work& w, double2* fe, int 
 }
 
 cudaError_t launch_analysis(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s) {
+  if (ponly_on(p)) return launch_analysis_ponly(p, w, fe, nb, s);  // P analyses + assembly
   cudaError_t err;
   if (launch_analysis_tma(p, w, fe, nb, s, &err)) return err;  // table-streaming regime
   FuseArgs none{};

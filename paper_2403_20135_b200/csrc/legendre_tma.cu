@@ -300,15 +300,17 @@ bool launch_analysis_tma(const Plan& p, const Work& w, double2* fe, int nb, cuda
 constexpr int kSynKQ = SDCSW_SYNB_KQ;      // row quads (4 table rows each) per stage
 constexpr int kSynBS = SDCSW_SYNB_STAGES;  // stages in flight
 
-__host__ __device__ constexpr int synb_stage_doubles(int wj, int nbt) {
-  return kSynKQ * (2 * wj * 64 + 48 * nbt) + 16;  // + pad: odd-pair reads past the last quad
+// PO (H-free path, legendre_ponly.cu): one table (P to degree T+1) and two operand parts
+__host__ __device__ constexpr int synb_stage_doubles(int wj, int nbt, bool po = false) {
+  return po ? kSynKQ * (wj * 64 + 32 * nbt) + 16
+            : kSynKQ * (2 * wj * 64 + 48 * nbt) + 16;  // + pad: odd-pair reads past the last quad
 }
-__host__ __device__ constexpr size_t synb_smem(int wj, int nbt) {
-  return (size_t)kSynBS * synb_stage_doubles(wj, nbt) * 8 + 8 * kSynBS;
+__host__ __device__ constexpr size_t synb_smem(int wj, int nbt, bool po = false) {
+  return (size_t)kSynBS * synb_stage_doubles(wj, nbt, po) * 8 + 8 * kSynBS;
 }
 
 
-template <int NB>
+template <int NB, bool PO>
 __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_MINB) k_synthesis_bulk(
     const double* __restrict__ xsyn, int nb, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
@@ -323,11 +325,13 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
   constexpr int NFULL = NB / 2;
   constexpr bool ODD = (NB & 1) != 0;
   constexpr int NT = 2 * NFULL + (ODD ? 1 : 0);  // P tiles
-  constexpr int NH = NFULL + (ODD ? 1 : 0);      // H tiles
-  constexpr int QX = 48 * NB;  // operand doubles per row quad (3 parts x NB states x 16)
+  constexpr int NH = NFULL + (ODD ? 1 : 0);      // H tiles (none when PO)
+  constexpr int NPART = PO ? 2 : 3;              // operand parts
+  constexpr int NTAB = PO ? 1 : 2;               // tables streamed
+  constexpr int QX = 16 * NPART * NB;  // operand doubles per row quad (parts x NB states x 16)
   extern __shared__ __align__(128) unsigned char synb_raw[];
   const int WJ = blockDim.x >> 5;
-  const int SD = synb_stage_doubles(WJ, NB);
+  const int SD = synb_stage_doubles(WJ, NB, PO);
   const int TQ = WJ * 64;  // table doubles per row quad of this CTA's latitudes
   double* stages = reinterpret_cast<double*>(synb_raw);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(synb_raw + (size_t)kSynBS * SD * 8);
@@ -348,27 +352,27 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
   // batch block blockIdx.z: states [b0, b0 + nbv) of nb; operand records are
   // [row/4][part][nb][16], one contiguous run per quad when the block is the batch
   const int b0 = blockIdx.z * NB, nbv = nb - b0 < NB ? nb - b0 : NB;
-  const size_t qxg = (size_t)48 * nb;  // operand doubles per row quad (all states)
+  const size_t qxg = (size_t)16 * NPART * nb;  // operand doubles per row quad (all states)
   const double* Xc = xsyn + (size_t)(r0m / 4) * qxg + (size_t)b0 * 16;
 
   auto nq_of = [&](int i) { return min(kSynKQ, nsteps - i * kSynKQ); };
   auto issue_tables = [&](int i) {  // thread 0
     double* st = stages + (i % kSynBS) * SD;
     const int nq = nq_of(i);
-    mbar_expect_tx(&full[i % kSynBS], (unsigned)(nq * (2 * TQ + 48 * nbv) * 8));
+    mbar_expect_tx(&full[i % kSynBS], (unsigned)(nq * (NTAB * TQ + 16 * NPART * nbv) * 8));
     for (int q = 0; q < nq; ++q) {
       const size_t src = (size_t)(i * kSynKQ + q) * qstride;
       bulk_g2s(st + q * TQ, Pc + src, TQ * 8, &full[i % kSynBS]);
-      bulk_g2s(st + (kSynKQ + q) * TQ, Hc + src, TQ * 8, &full[i % kSynBS]);
+      if constexpr (!PO) bulk_g2s(st + (kSynKQ + q) * TQ, Hc + src, TQ * 8, &full[i % kSynBS]);
     }
   };
   auto issue_operand = [&](int i) {  // thread 0, after the producer grid completed
-    double* st = stages + (i % kSynBS) * SD + 2 * kSynKQ * TQ;
+    double* st = stages + (i % kSynBS) * SD + NTAB * kSynKQ * TQ;
     if (nb == NB) {
       bulk_g2s(st, Xc + (size_t)i * kSynKQ * QX, (unsigned)(nq_of(i) * QX * 8), &full[i % kSynBS]);
     } else {  // one run of nbv states per (quad, part), placed at the block's [part][NB] stride
       for (int q = 0; q < nq_of(i); ++q)
-        for (int pp = 0; pp < 3; ++pp)
+        for (int pp = 0; pp < NPART; ++pp)
           bulk_g2s(st + q * QX + pp * 16 * NB, Xc + (size_t)(i * kSynKQ + q) * qxg + pp * 16 * nb,
                    (unsigned)(nbv * 16 * 8), &full[i % kSynBS]);
     }
@@ -403,21 +407,30 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
       if (q < nq) {
         const double* pq = st + q * TQ + warp * 64 + lane;
         const double* hq = pq + kSynKQ * TQ;
-        const double aP0 = pq[0], aP1 = pq[32], aH0 = hq[0], aH1 = hq[32];
-        const double* xq0 = st + 2 * kSynKQ * TQ + q * QX + t * 4 + gc;
+        const double aP0 = pq[0], aP1 = pq[32];
+        const double aH0 = PO ? 0.0 : hq[0], aH1 = PO ? 0.0 : hq[32];
+        const double* xq0 = st + NTAB * kSynKQ * TQ + q * QX + t * 4 + gc;
         const double* xq = xq0 + gb * 16;
         double bP[NT], bH[NH];
 #pragma unroll
         for (int p = 0; p < NFULL; ++p) {
           bP[2 * p] = xq[p * 32];
           bP[2 * p + 1] = xq[16 * NB + p * 32];
-          bH[p] = xq[32 * NB + p * 32];
+          bH[p] = PO ? 0.0 : xq[32 * NB + p * 32];
         }
         if constexpr (ODD) {  // last state: lane column group gb = part
           bP[NT - 1] = xq0[gb * 16 * NB + (NB - 1) * 16];
-          bH[NH - 1] = gb == 0 ? xq0[32 * NB + (NB - 1) * 16] : 0.0;
+          bH[NH - 1] = !PO && gb == 0 ? xq0[32 * NB + (NB - 1) * 16] : 0.0;
         }
-        if (i * kSynKQ + q < se) {  // n - m even: P symmetric (E), H antisymmetric (O)
+        if constexpr (PO) {  // H-free: every operand column is a P column
+          if (i * kSynKQ + q < se) {
+#pragma unroll
+            for (int c = 0; c < NT; ++c) { dmma_t(aE[0][c], aP0, bP[c]); dmma_t(aE[1][c], aP1, bP[c]); }
+          } else {
+#pragma unroll
+            for (int c = 0; c < NT; ++c) { dmma_t(aO[0][c], aP0, bP[c]); dmma_t(aO[1][c], aP1, bP[c]); }
+          }
+        } else if (i * kSynKQ + q < se) {  // n - m even: P symmetric (E), H antisymmetric (O)
 #pragma unroll
           for (int c = 0; c < NT; ++c) { dmma_t(aE[0][c], aP0, bP[c]); dmma_t(aE[1][c], aP1, bP[c]); }
 #pragma unroll
@@ -475,8 +488,12 @@ cudaError_t configure_synthesis_bulk() {
   cudaError_t e = cudaSuccess;
 #define SDCSW_SYNB_CFG(NBV)                                                                   \
   if (e == cudaSuccess)                                                                       \
-    e = cudaFuncSetAttribute(k_synthesis_bulk<NBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             (int)synb_smem(4, NBV));
+    e = cudaFuncSetAttribute(k_synthesis_bulk<NBV, false>,                                    \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)synb_smem(4, NBV)); \
+  if (e == cudaSuccess)                                                                       \
+    e = cudaFuncSetAttribute(k_synthesis_bulk<NBV, true>,                                     \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
+                             (int)synb_smem(4, NBV, true));
   SDCSW_SYNB_CFG(1) SDCSW_SYNB_CFG(2) SDCSW_SYNB_CFG(3) SDCSW_SYNB_CFG(4) SDCSW_SYNB_CFG(5)
   SDCSW_SYNB_CFG(6)
 #undef SDCSW_SYNB_CFG
@@ -500,12 +517,30 @@ cudaError_t launch_synthesis_bulk(const Plan& p, double2* fsyn, const int* mlist
   const dim3 grid(p.J / (kRowsPerWarp * WJ), nm, (nb + NB - 1) / NB);
 #define SDCSW_SYNB_LAUNCH(NBV)                                                                \
   if (NB == NBV)                                                                              \
-    return launch_k(k_synthesis_bulk<NBV>, grid, dim3(32 * WJ), synb_smem(WJ, NBV), s, xsyn,  \
-                    nb, p.J, p.ptab_s, p.htab_s, p.rowoff, p.n_even, fsyn, step_counter, mlist, \
-                    Lp, sd);
+    return launch_k(k_synthesis_bulk<NBV, false>, grid, dim3(32 * WJ), synb_smem(WJ, NBV), s,  \
+                    xsyn, nb, p.J, p.ptab_s, p.htab_s, p.rowoff, p.n_even, fsyn, step_counter,  \
+                    mlist, Lp, sd);
   SDCSW_SYNB_LAUNCH(1) SDCSW_SYNB_LAUNCH(2) SDCSW_SYNB_LAUNCH(3) SDCSW_SYNB_LAUNCH(4)
   SDCSW_SYNB_LAUNCH(5) SDCSW_SYNB_LAUNCH(6)
 #undef SDCSW_SYNB_LAUNCH
+  return cudaErrorInvalidValue;
+}
+
+// H-free synthesis (legendre_ponly.cu): xsp = the P-only operand of the chain, P rows to T+1
+cudaError_t launch_synthesis_bulk_ponly(const Plan& p, double2* fsyn, const int* mlist, int nm,
+                                        int Lp, const double* xsp, int nb, cudaStream_t s,
+                                        int* step_counter, const SynDst& sd) {
+  const int WJ = p.J % 64 == 0 ? 4 : 2;
+  const int NB = nb <= 6 ? nb : 6;
+  const dim3 grid(p.J / (kRowsPerWarp * WJ), nm, (nb + NB - 1) / NB);
+#define SDCSW_SYNP_LAUNCH(NBV)                                                                 \
+  if (NB == NBV)                                                                               \
+    return launch_k(k_synthesis_bulk<NBV, true>, grid, dim3(32 * WJ), synb_smem(WJ, NBV, true), \
+                    s, xsp, nb, p.J, p.ptabP_s, p.ptabP_s, p.rowoffP, p.n_evenP, fsyn,          \
+                    step_counter, mlist, Lp, sd);
+  SDCSW_SYNP_LAUNCH(1) SDCSW_SYNP_LAUNCH(2) SDCSW_SYNP_LAUNCH(3) SDCSW_SYNP_LAUNCH(4)
+  SDCSW_SYNP_LAUNCH(5) SDCSW_SYNP_LAUNCH(6)
+#undef SDCSW_SYNP_LAUNCH
   return cudaErrorInvalidValue;
 }
 
@@ -730,6 +765,205 @@ static cudaError_t launch_analysis_bulk(const Plan& p, const Work& w, double2* f
   SDCSW_ANAB_LAUNCH(5) SDCSW_ANAB_LAUNCH(6)
 #undef SDCSW_ANAB_LAUNCH
   return cudaErrorInvalidValue;
+}
+
+
+// ---------------------------------------------------------------------------
+// H-free table-streaming analysis (legendre_ponly.cu): the five analysis data
+// slots (A, B, C, D, E, folded and weighted by the ring kernel) of every state
+// contracted with P only, for the degrees k = m..T+1 of the extended triangle:
+//   ghat[b][(m, k)][slot] = sum_j P_k(mu_j) D_fold(k)[j, slot]
+// (fold S for k - m even, A for odd).  Same TMA table stream and staged B
+// operand as k_analysis_bulk, one table instead of two, and the 10 columns of
+// each state packed into ceil(10 NB / 8) B tiles (NB = 5: 7 DMMA pairs per
+// k-step instead of 9).  The i m factors and the H recurrence are applied by
+// the assembly kernel (legendre_ponly.cu), which needs degrees k - 1 and k + 1.
+// ---------------------------------------------------------------------------
+constexpr int kAnpChunk = kTmaLat * 2 * kGhat;  // five-slot data doubles per state per stage
+template <int NB>
+constexpr size_t anap_smem() {
+  return (size_t)kAnbS * (kTileBytes + NB * kAnpChunk * 8) + 8 * kAnbS;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(128, SDCSW_ANAB_MINB) k_analysis_bulk_ponly(
+    const __grid_constant__ CUtensorMap pmap, const double* __restrict__ gan, int nb, int T, int J,
+    const int* __restrict__ rowoff, const int* __restrict__ n_even, const int* __restrict__ row_n,
+    const int* __restrict__ moffp, const int* __restrict__ work, double* __restrict__ ghat,
+    int CP) {
+  SDCSW_PDL_ENTRY();
+  constexpr int NC = kGhat * NB;      // B columns: 10 per state
+  constexpr int NT = (NC + 7) / 8;    // B tiles
+  constexpr int OS = NC + 1;
+  static_assert(kRowsPerWarp * OS * 4 * 8 <= kAnbS * (kTileBytes + NB * kAnpChunk * 8),
+                "the epilogue tiles fit in the consumed stage buffers");
+  extern __shared__ __align__(1024) unsigned char anp_smem[];
+  double* ptile = reinterpret_cast<double*>(anp_smem);  // [kAnbS][64][16], swizzled
+  double* btile = reinterpret_cast<double*>(anp_smem + kAnbS * kTileBytes);  // [kAnbS][NB][320]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(
+      anp_smem + kAnbS * kTileBytes + (size_t)kAnbS * NB * kAnpChunk * 8);
+
+  const int wk = work[blockIdx.x];
+  const int m = wk >> 16, rb = wk & 0xffff;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int b0 = blockIdx.y * NB;
+  const int nbv = nb - b0 < NB ? nb - b0 : NB;
+  const int L = T + 1;
+  const int r0m = rowoff[m];
+  const int rows = rowoff[m + 1] - r0m;
+  const int le = n_even[m];
+  const int rblock = r0m + rb * kTmaRows;
+  const int rw = rb * kTmaRows + warp * kRowsPerWarp;
+  const bool live = rw < rows;
+  const bool ev0 = rw < le, ev1 = rw + 8 < le;
+  const int nchunks = J / kTmaLat;
+  const double* gsrc = gan + ((size_t)b0 * L + m) * J * 2 * kGhat;
+  const size_t bstride = (size_t)L * J * 2 * kGhat;  // doubles per state
+
+  auto issue_tables = [&](int ch) {  // thread 0
+    const int st = ch % kAnbS;
+    mbar_expect_tx(&full[st], kTileBytes + nbv * kAnpChunk * 8);
+    tma_load_2d(ptile + st * kTmaRows * kTmaLat, &pmap, ch * kTmaLat, rblock, &full[st]);
+  };
+  auto issue_data = [&](int ch) {  // thread 0, after the producer grid completed
+    const int st = ch % kAnbS;
+    for (int c = 0; c < nbv; ++c)
+      bulk_g2s(btile + (st * NB + c) * kAnpChunk, gsrc + c * bstride + (size_t)ch * kAnpChunk,
+               kAnpChunk * 8, &full[st]);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kAnbS; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int ch = 0; ch < kAnbS && ch < nchunks; ++ch) issue_tables(ch);
+  SDCSW_PDL_WAIT();
+  if (threadIdx.x == 0)
+    for (int ch = 0; ch < kAnbS && ch < nchunks; ++ch) issue_data(ch);
+
+  // B column 8 h + g of tile h = state s, double d of its 10 (5 slots x re, im);
+  // per k-step (4 latitudes) a state's record is [fold][4 lat][10] = 80 doubles
+  int boff[NT];
+#pragma unroll
+  for (int h = 0; h < NT; ++h) {
+    const int col = 8 * h + g, s_ = col / kGhat;
+    boff[h] = s_ < NB ? s_ * kAnpChunk + t * kGhat + (col - kGhat * s_) : -1;
+  }
+  const bool any_ev = ev0 || ev1, any_od = !ev0 || !ev1;
+  double acc[2][NT][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int h = 0; h < NT; ++h) acc[a][h][0] = acc[a][h][1] = 0.0;
+  const int row0 = warp * kRowsPerWarp + g;
+
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int st = ch % kAnbS;
+    mbar_wait(&full[st], (ch / kAnbS) & 1);
+    if (live) {
+      const double* pt = ptile + st * kTmaRows * kTmaLat;
+      const double* bt = btile + st * NB * kAnpChunk;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = 4 * q + t;
+        const double aP0 = swz(pt, row0, k), aP1 = swz(pt, row0 + 8, k);
+        double bs[NT], ba[NT];
+#pragma unroll
+        for (int h = 0; h < NT; ++h) {
+          const double* r = bt + q * 80 + (boff[h] < 0 ? 0 : boff[h]);
+          bs[h] = any_ev && boff[h] >= 0 ? r[0] : 0.0;
+          ba[h] = any_od && boff[h] >= 0 ? r[40] : 0.0;
+        }
+#pragma unroll
+        for (int h = 0; h < NT; ++h) {
+          dmma_t(acc[0][h], aP0, ev0 ? bs[h] : ba[h]);
+          dmma_t(acc[1][h], aP1, ev1 ? bs[h] : ba[h]);
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with stage st
+    if (threadIdx.x == 0 && ch + kAnbS < nchunks) {
+      issue_tables(ch + kAnbS);
+      issue_data(ch + kAnbS);
+    }
+  }
+  if (!live) return;
+  double* o = reinterpret_cast<double*>(anp_smem) + warp * kRowsPerWarp * OS;  // stages are consumed
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      const int col = 8 * h + 2 * t;
+      if (col < NC) {
+        o[(8 * a + g) * OS + col] = acc[a][h][0];
+        o[(8 * a + g) * OS + col + 1] = acc[a][h][1];
+      }
+    }
+  __syncwarp();
+  const int mo = moffp[m];
+  for (int it = lane; it < kRowsPerWarp * NB; it += 32) {
+    const int rr = it % kRowsPerWarp, b = it / kRowsPerWarp;
+    if (rw + rr >= rows || b0 + b >= nb) continue;
+    const int k = row_n[r0m + rw + rr];
+    if (k < 0) continue;
+    const double* src = o + rr * OS + kGhat * b;
+    double2* dst = reinterpret_cast<double2*>(ghat + ((size_t)(b0 + b) * CP + mo + k - m) * kGhat);
+#pragma unroll
+    for (int q = 0; q < kSlotsP; ++q) dst[q] = make_double2(src[2 * q], src[2 * q + 1]);
+  }
+}
+
+
+cudaError_t configure_analysis_bulk_ponly() {
+  cudaError_t e = cudaSuccess;
+#define SDCSW_ANAP_CFG(NBV)                                                                   \
+  if (e == cudaSuccess)                                                                       \
+    e = cudaFuncSetAttribute(k_analysis_bulk_ponly<NBV>,                                      \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)anap_smem<NBV>());
+  SDCSW_ANAP_CFG(1) SDCSW_ANAP_CFG(2) SDCSW_ANAP_CFG(3) SDCSW_ANAP_CFG(4) SDCSW_ANAP_CFG(5)
+  SDCSW_ANAP_CFG(6)
+#undef SDCSW_ANAP_CFG
+  return e;
+}
+
+cudaError_t launch_analysis_bulk_ponly(const Plan& p, const Work& w, int nb, cudaStream_t s) {
+  const int NB = nb <= 6 ? nb : 6;
+  const bool own = p.own_idx != nullptr;  // split plan: own wavenumbers only
+  const int* work = own ? p.own_workP : p.anal_workP;
+  const int nwork = own ? p.n_own_workP : p.n_anal_workP;
+  if (nwork < 1) return cudaSuccess;
+  dim3 grid(nwork, (nb + NB - 1) / NB);
+  const CUtensorMap& pm = *reinterpret_cast<const CUtensorMap*>(p.tmapP);
+#define SDCSW_ANAP_LAUNCH(NBV)                                                                   \
+  if (NB == NBV)                                                                                 \
+    return launch_k(k_analysis_bulk_ponly<NBV>, grid, dim3(128), anap_smem<NBV>(), s, pm,         \
+                    reinterpret_cast<const double*>(w.gan), nb, p.T, p.J, p.rowoffP, p.n_evenP,  \
+                    p.rowP_n, p.moffP, work, w.ghat, p.CP);
+  SDCSW_ANAP_LAUNCH(1) SDCSW_ANAP_LAUNCH(2) SDCSW_ANAP_LAUNCH(3) SDCSW_ANAP_LAUNCH(4)
+  SDCSW_ANAP_LAUNCH(5) SDCSW_ANAP_LAUNCH(6)
+#undef SDCSW_ANAP_LAUNCH
+  return cudaErrorInvalidValue;
+}
+
+// TMA map over the H-free table [rowsP][J] (same box and swizzle as the P/H maps)
+cudaError_t make_table_map_ponly(Plan& p) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || !fn || q != cudaDriverEntryPointSuccess) return cudaErrorNotSupported;
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  const cuuint64_t dims[2] = {(cuuint64_t)p.J, (cuuint64_t)p.rowsP + 16};
+  const cuuint64_t strides[1] = {(cuuint64_t)p.J * sizeof(double)};
+  const cuuint32_t box[2] = {kTmaLat, kTmaRows};
+  const cuuint32_t elem[2] = {1, 1};
+  CUresult r = encode(reinterpret_cast<CUtensorMap*>(p.tmapP), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                      p.ptabP, dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorNotSupported;
 }
 
 }  // namespace sdcsw

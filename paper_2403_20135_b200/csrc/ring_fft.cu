@@ -70,8 +70,28 @@ template <> struct RadixPlan<384> { static constexpr int n = 4; static constexpr
 #else
 template <> struct RadixPlan<384> { static constexpr int n = 3; static constexpr int r[6] = {16, 8, 3}; };
 #endif
+#ifndef SDCSW_PLAN768  // experiment knob
+#define SDCSW_PLAN768 0
+#endif
+#if SDCSW_PLAN768 == 1
+template <> struct RadixPlan<768> { static constexpr int n = 4; static constexpr int r[6] = {8, 8, 4, 3}; };
+#elif SDCSW_PLAN768 == 2
+template <> struct RadixPlan<768> { static constexpr int n = 4; static constexpr int r[6] = {4, 8, 8, 3}; };
+#else
 template <> struct RadixPlan<768> { static constexpr int n = 3; static constexpr int r[6] = {16, 16, 3}; };
+#endif
+#ifndef SDCSW_PLAN1536  // experiment knob
+#define SDCSW_PLAN1536 0
+#endif
+#if SDCSW_PLAN1536 == 1
+template <> struct RadixPlan<1536> { static constexpr int n = 4; static constexpr int r[6] = {8, 8, 8, 3}; };
+#elif SDCSW_PLAN1536 == 2
+template <> struct RadixPlan<1536> { static constexpr int n = 4; static constexpr int r[6] = {8, 16, 4, 3}; };
+#elif SDCSW_PLAN1536 == 3
+template <> struct RadixPlan<1536> { static constexpr int n = 5; static constexpr int r[6] = {8, 4, 4, 4, 3}; };
+#else
 template <> struct RadixPlan<1536> { static constexpr int n = 4; static constexpr int r[6] = {16, 8, 4, 3}; };
+#endif
 
 template <int N>
 constexpr int inv_radix(int s) { return RadixPlan<N>::r[s]; }
@@ -314,8 +334,10 @@ struct alignas(64) GanMaps {
   CUtensorMap rec;  // record order: {28 doubles, J, rows}
   CUtensorMap fp;   // fragment order, P part: {8 doubles, j & 3, fold, j >> 2, rows}
   CUtensorMap fh;   // fragment order, H part: {6 doubles, j & 3, fold, j >> 2, rows}
+  CUtensorMap f5;   // H-free path (po): {10 doubles, j & 3, fold, j >> 2, rows}
   int rows;         // wavenumbers per store box (divides L); 0 = plain stores
   int row0;         // first row of the launch's workspace (batch offset x L)
+  int po;           // 1: write the five-slot data of the H-free analysis (ganp_off)
 };
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1,
@@ -575,7 +597,58 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
     o[kYDelta] = make_double2(v[0].x * ws, v[0].y * ws);
   };
   constexpr int MI = (2 * ((N + 2) / 3) + THREADS - 1) / THREADS;  // items per thread, L <= (N + 2) / 3
-  if (gm.rows > 0 && L <= (N + 2) / 3) {  // (then the boxes fit in the 5 FFT arrays)
+  // H-free path: the five products of item (m, fold), folded and weighted (A..D by
+  // w_s, E by w_ke); the i m factors and the recurrence act after the analysis
+  auto item5 = [&](int it, double2 (&o)[kSlotsP]) {
+    const int m = it >> 1, fold = it & 1;
+#pragma unroll
+    for (int q = 0; q < kSlotsP; ++q) {
+      const double2 zm = Z[q * NP + pzv(m, SHL)], zc = Z[q * NP + pzv(m == 0 ? 0 : N - m, SHL)];
+      const double2 X = make_double2(h * (zm.x + zc.x), h * (zm.y - zc.y));
+      const double2 Y = make_double2(h * (zm.y + zc.y), -h * (zm.x - zc.x));
+      const double2 v = fold ? csub(X, Y) : cadd(X, Y);
+      const double wq = q == 4 ? wk : ws;
+      o[q] = make_double2(v.x * wq, v.y * wq);
+    }
+  };
+  if (gm.po) {
+    if (gm.rows > 0 && L <= (N + 2) / 3) {  // staged as [m][fold][5 slots], TMA stores
+      double2 o[MI][kSlotsP];
+#pragma unroll
+      for (int q = 0; q < MI; ++q) {
+        const int it = threadIdx.x + q * THREADS;
+        if (it < 2 * L) item5(it, o[q]);
+      }
+      __syncthreads();  // every read of the FFT arrays is done
+#pragma unroll
+      for (int q = 0; q < MI; ++q) {
+        const int it = threadIdx.x + q * THREADS;
+        if (it < 2 * L) {
+#pragma unroll
+          for (int k = 0; k < kSlotsP; ++k) Z[it * kSlotsP + k] = o[q][k];
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int row = gm.row0 + b * L;
+        for (int m0 = 0; m0 < L; m0 += gm.rows)
+          tma_store_5d(&gm.f5, Z + m0 * 2 * kSlotsP, 0, j & 3, 0, j >> 2, row + m0);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+    } else {
+      double* outp = reinterpret_cast<double*>(gan) + (size_t)b * L * J * 2 * kGhat;
+      for (int it = threadIdx.x; it < 2 * L; it += THREADS) {
+        double2 o[kSlotsP];
+        item5(it, o);
+        double2* d = reinterpret_cast<double2*>(outp + (size_t)(it >> 1) * J * 2 * kGhat +
+                                                ganp_off(j, it & 1, 0, 0));
+#pragma unroll
+        for (int k = 0; k < kSlotsP; ++k) d[k] = o[k];
+      }
+    }
+  } else if (gm.rows > 0 && L <= (N + 2) / 3) {  // (then the boxes fit in the 5 FFT arrays)
     // staged in the FFT arrays as the store boxes: record order [m][fold][7 slots];
     // fragment order [m][fold][4 P slots] then, from L x 128 bytes, [m][fold][3 H slots]
     double2 o[MI][kNumSlots];
@@ -664,8 +737,11 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
 #ifndef SDCSW_RT768
 #define SDCSW_RT768 256
 #endif
+#ifndef SDCSW_RT1536
+#define SDCSW_RT1536 512
+#endif
 #define SDCSW_RING_SIZES(X) \
-  X(96, SDCSW_RT96) X(192, SDCSW_RT192) X(384, SDCSW_RT384) X(768, SDCSW_RT768) X(1536, 512)
+  X(96, SDCSW_RT96) X(192, SDCSW_RT192) X(384, SDCSW_RT384) X(768, SDCSW_RT768) X(1536, SDCSW_RT1536)
 // throughput variants (batches of at least kRingTputBatch states)
 #define SDCSW_RING_TPUT(X) X(384, 128)
 constexpr int kRingTputBatch = 16;
@@ -758,6 +834,17 @@ cudaError_t make_gan_maps(Plan& p) {
     p.gmap_frag = enc(1, p.gan, 5, dp, sp, bp) &&
                   enc(2, reinterpret_cast<double*>(p.gan) + 32, 5, dh, sh, bh);
   }
+  p.gmapP_rows = 0;
+  if (J % 4 == 0) {  // H-free five-slot data (ganp_off): [j >> 2][fold][j & 3][10]
+    const cuuint64_t d5[5] = {10, 4, 2, (cuuint64_t)J / 4, R};
+    const cuuint64_t s5[4] = {80, 320, 640, (cuuint64_t)J * 20 * sizeof(double)};
+    const cuuint32_t b5[5] = {10, 1, 2, 1, (cuuint32_t)rows};
+    const cuuint32_t elem[5] = {1, 1, 1, 1, 1};
+    if (encode(reinterpret_cast<CUtensorMap*>(p.gmapP), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, p.gan, d5,
+               s5, b5, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      p.gmapP_rows = rows;
+  }
   return cudaSuccess;
 }
 
@@ -765,13 +852,16 @@ static cudaError_t ring_impl(const Plan& p, const double2* fsyn, double2* gan, c
                              const int* m_k, int Lp, int nb, cudaStream_t s,
                              const RingPeer& rp = RingPeer{}) {
   dim3 grid(p.J, nb);
+  const int po = (int)ponly_on(p);  // five-slot output for the H-free analysis
   const int frag = (int)tma_active(p);
   GanMaps gm;
   std::memcpy(&gm.rec, p.gmap[0], sizeof(CUtensorMap));
   std::memcpy(&gm.fp, p.gmap[1], sizeof(CUtensorMap));
   std::memcpy(&gm.fh, p.gmap[2], sizeof(CUtensorMap));
-  gm.rows = frag && !p.gmap_frag ? 0 : p.gmap_rows;
-  gm.row0 = (int)((gan - p.gan) / ((size_t)p.J * p.L * kNumSlots * 2)) * p.L;
+  std::memcpy(&gm.f5, p.gmapP, sizeof(CUtensorMap));
+  gm.po = po;
+  gm.rows = po ? p.gmapP_rows : (frag && !p.gmap_frag ? 0 : p.gmap_rows);
+  gm.row0 = (int)((gan - p.gan) / ((size_t)p.J * p.L * (po ? kSlotsP : kNumSlots) * 2)) * p.L;
 #define SDCSW_RING_LAUNCH(NV, TV)                                                                  \
   if (p.nlon == NV) {                                                                              \
     constexpr size_t smem = ring_smem_t<NV, TV>();                                                 \

@@ -325,6 +325,20 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
     p.fe_chunk = 0;
     if (const char* env = getenv("SDCSW_FE_CHUNK")) p.fe_chunk = atoi(env);
   }
+  // H-free transforms (legendre_ponly.cu) for the table-streaming path (T >= 200 and
+  // ensemble plans); SDCSW_PONLY = 0 / 1 overrides the default
+  {
+    int po = 1;
+    if (const char* env = getenv("SDCSW_PONLY")) po = atoi(env);
+    if (po && tma_active(p)) {
+      if (ponly_setup(p, ptab, rowoff, row_n, mu_north) == cudaSuccess) {
+        p.ponly = 1;
+      } else {
+        cudaGetLastError();  // not built: the P/H path serves the plan
+        p.ponly = 0;
+      }
+    }
+  }
   h->alive = true;
   *out = h;
   return SDCSW_OK;
@@ -338,7 +352,9 @@ int sdcsw_plan_destroy(sdcsw_plan* h) {
   cudaSetDevice(h->p.device);
   cudaDeviceSynchronize();
   Plan& p = h->p;
-  for (void* q : {(void*)p.m_part, (void*)p.m_k, (void*)p.own_m, (void*)p.own_work, (void*)p.own_idx})
+  ponly_free(p);
+  for (void* q : {(void*)p.m_part, (void*)p.m_k, (void*)p.own_m, (void*)p.own_work, (void*)p.own_idx,
+                  (void*)p.own_workP})
     if (q) cudaFree(q);
   void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
                   p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev,
@@ -596,6 +612,7 @@ int sdcsw_transform_stage(sdcsw_plan* h, int stage, const double* in, double* ou
       e = launch_synth_prep(h->p, (const double2*)in, nb, h->p.xsyn, s);
       if (e == cudaSuccess) e = launch_synthesis(h->p, plan_work(h->p), h->p.xsyn, nb, s, nullptr);
       break;
+    // (H-free plans: stage 3 includes the operand conversion, stage 2 the assembly)
     case 3: e = launch_synthesis(h->p, plan_work(h->p), h->p.xsyn, nb, s, nullptr); break;
     case 1: e = launch_ring(h->p, plan_work(h->p), nb, s); break;
     case 2: e = launch_analysis(h->p, plan_work(h->p), (double2*)out, nb, s); break;
@@ -628,7 +645,17 @@ int sdcsw_workspace(sdcsw_plan* h, int which, void** ptr, long long* bytes) {
   const Plan& p = h->p;
   const long long per = (long long)p.max_batch * p.J * p.L * 2 * sizeof(double2);
   *ptr = which == 0 ? (void*)p.fsyn : (void*)p.gan;
-  *bytes = which == 0 ? per * 4 : per * kNumSlots;  // see sdcsw.h for the layouts
+  *bytes = which == 0 ? per * 4 : per * (ponly_on(p) ? kSlotsP : kNumSlots);  // see sdcsw.h
+  return SDCSW_OK;
+}
+
+int sdcsw_plan_transform_kind(sdcsw_plan* h, int* kind, int* rows) {
+  int st = check_plan(h, 1, "sdcsw_plan_transform_kind");
+  if (st) return st;
+  const Plan& p = h->p;
+  const bool po = ponly_on(p);
+  if (kind) *kind = po ? 1 : 0;
+  if (rows) *rows = po ? p.rowsP : p.rows;
   return SDCSW_OK;
 }
 
@@ -643,10 +670,11 @@ int sdcsw_plan_set_split(sdcsw_plan* h, int S, int sp, void* fourier, long long 
   }
   cudaSetDevice(p.device);
   cudaDeviceSynchronize();
-  for (int** q : {&p.m_part, &p.m_k, &p.own_m, &p.own_work, &p.own_idx}) {
+  for (int** q : {&p.m_part, &p.m_k, &p.own_m, &p.own_work, &p.own_idx, &p.own_workP}) {
     if (*q) cudaFree(*q);
     *q = nullptr;
   }
+  p.n_own_workP = 0;
   p.split_S = S;
   p.split_sp = sp;
   p.Lp = p.L;
@@ -678,6 +706,13 @@ int sdcsw_plan_set_split(sdcsw_plan* h, int S, int sp, void* fourier, long long 
   cudaMemcpy(work.data(), p.anal_work, work.size() * sizeof(int), cudaMemcpyDeviceToHost);
   for (int w : work)
     if (part[w >> 16] == sp) wown.push_back(w);
+  std::vector<int> wownP;  // H-free analysis work items of own m
+  if (p.anal_workP != nullptr) {
+    std::vector<int> workP(p.n_anal_workP);
+    cudaMemcpy(workP.data(), p.anal_workP, workP.size() * sizeof(int), cudaMemcpyDeviceToHost);
+    for (int w : workP)
+      if (part[w >> 16] == sp) wownP.push_back(w);
+  }
   for (int m : own) {
     const int mo = m * (T + 1) - m * (m - 1) / 2;
     for (int n = m; n <= T; ++n) idx.push_back(mo + n - m);
@@ -687,8 +722,10 @@ int sdcsw_plan_set_split(sdcsw_plan* h, int S, int sp, void* fourier, long long 
       (e = upload(&p.m_k, kpos.data(), kpos.size())) != cudaSuccess ||
       (e = upload(&p.own_m, own.data(), own.size())) != cudaSuccess ||
       (e = upload(&p.own_work, wown.data(), wown.size())) != cudaSuccess ||
-      (e = upload(&p.own_idx, idx.data(), idx.size())) != cudaSuccess)
+      (e = upload(&p.own_idx, idx.data(), idx.size())) != cudaSuccess ||
+      (!wownP.empty() && (e = upload(&p.own_workP, wownP.data(), wownP.size())) != cudaSuccess))
     return cuda_status(e, "sdcsw_plan_set_split");
+  p.n_own_workP = (int)wownP.size();
   p.Lp = Lp;
   p.n_own_m = (int)own.size();
   p.n_own_work = (int)wown.size();

@@ -58,6 +58,14 @@ class DeviceProblem(SplitProblem):
             pass
 
     @property
+    def uses_ponly(self):
+        """True when f_E runs the H-free transforms (``sdcsw_plan_transform_kind``)."""
+        kind, rows = ctypes.c_int(), ctypes.c_int()
+        _native.check(self._lib.sdcsw_plan_transform_kind(self._plan, ctypes.byref(kind), ctypes.byref(rows)),
+                      "sdcsw_plan_transform_kind")
+        return kind.value == 1
+
+    @property
     def handle(self):
         return self._plan
 

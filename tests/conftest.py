@@ -25,3 +25,4 @@ def reference():
     import parsdc
 
     return parsdc
+

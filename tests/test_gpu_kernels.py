@@ -19,6 +19,7 @@ from paper_2403_20135_b200 import (
     random_initial_state,
 )
 from paper_2403_20135_b200.errors import DivergenceError
+from plan_env import plan_env
 
 pytestmark = pytest.mark.gpu
 
@@ -438,28 +439,60 @@ def test_reference_schemes_on_gpu():
 def test_tma_analysis_matches_latency_analysis_t511():
     """T511: the table-streaming TMA analysis (fragment-order analysis data) and
     the latency-regime analysis (record order; forced with SDCSW_ANAL_WJ=2) give
-    the same f_E to summation-order rounding."""
+    the same f_E to summation-order rounding (both with the P/H tables: the H-free
+    path is compared in test_ponly_matches_ph_and_oracle)."""
     from paper_2403_20135_b200.problem import SphericalShallowWater
 
-    p = gpu(511, max_batch=5)
+    with plan_env(SDCSW_PONLY="0"):
+        p = SphericalShallowWater(511, max_batch=5)
     u = random_initial_state(p.grid, 11)
     u[: p.n_coef] = 4e-3 * u[p.n_coef : 2 * p.n_coef] * 1e6
     a = p.f_expl(u)
-    old = os.environ.get("SDCSW_ANAL_WJ")
-    os.environ["SDCSW_ANAL_WJ"] = "2"
-    try:
+    with plan_env(SDCSW_ANAL_WJ="2"):
         q = SphericalShallowWater(511, max_batch=2)
-    finally:
-        if old is None:
-            del os.environ["SDCSW_ANAL_WJ"]
-        else:
-            os.environ["SDCSW_ANAL_WJ"] = old
     b = q.f_expl(u)
     c = p.n_coef
     for f in range(3):
         x, y = a[f * c : (f + 1) * c], b[f * c : (f + 1) * c]
         assert np.linalg.norm(x - y) <= 1e-12 * np.linalg.norm(y)
     q.close()
+    p.close()
+
+
+@pytest.mark.parametrize("trunc,max_batch,nb", [(255, 4, 4), (511, 5, 5), (127, 16, 16)])
+def test_ponly_matches_ph_and_oracle(trunc, max_batch, nb):
+    """H-free transforms (legendre_ponly.cu: P tables to degree T+1, the derivative
+    recurrence for H) against the P/H path on the same plan shape and against the CPU
+    oracle with its own (independent) tables: f_E agrees with the P/H path to 3e-12
+    relative per field and state, and its error against the oracle is no larger than
+    the P/H path's (within a factor 2, floor 1e-12)."""
+    import torch
+
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    with plan_env(SDCSW_PONLY="1"):
+        po = SphericalShallowWater(trunc, max_batch=max_batch)
+    with plan_env(SDCSW_PONLY="0"):
+        ph = SphericalShallowWater(trunc, max_batch=max_batch)
+    assert po.uses_ponly and not ph.uses_ponly
+    c = po.n_coef
+    states = np.stack([random_initial_state(po.grid, 90 + b) for b in range(nb)])
+    states[:, :c] = 4e-3 * states[:, c : 2 * c] * 1e6
+    u = torch.from_numpy(states).to(po.device).contiguous()
+    a = po.f_expl_device(u, po.empty_states(nb), nb).cpu().numpy()
+    b = ph.f_expl_device(u, ph.empty_states(nb), nb).cpu().numpy()
+    for s in range(nb):
+        for f in range(3):
+            x, y = a[s, f * c : (f + 1) * c], b[s, f * c : (f + 1) * c]
+            assert np.linalg.norm(x - y) <= 3e-12 * np.linalg.norm(y), (s, f)
+    o = oracle_for(po)
+    for s in (0, nb - 1):
+        ref = o.f_expl(states[s])
+        e_po = max(relative_l2(a[s], ref, o))
+        e_ph = max(relative_l2(b[s], ref, o))
+        assert e_po <= max(2 * e_ph, 1e-12), (e_po, e_ph)
+    po.close()
+    ph.close()
 
 
 def test_plans_of_different_sizes_coexist():
@@ -575,15 +608,10 @@ def test_bulk_synthesis_partial_batch_block(nb, max_batch):
     from paper_2403_20135_b200.problem import SphericalShallowWater
 
     def plan(bulk):
-        old = os.environ.get("SDCSW_SYN_BULK")
-        os.environ["SDCSW_SYN_BULK"] = bulk
-        try:
+        # P/H tables (ensemble plans from 16 states would take the H-free path,
+        # whose synthesis is always the bulk kernel: test_ponly_partial_batch_block)
+        with plan_env(SDCSW_SYN_BULK=bulk, SDCSW_PONLY="0"):
             return SphericalShallowWater(127, max_batch=max_batch)
-        finally:
-            if old is None:
-                del os.environ["SDCSW_SYN_BULK"]
-            else:
-                os.environ["SDCSW_SYN_BULK"] = old
 
     def synth(p, u, nb):
         s = p.stream()
@@ -608,6 +636,38 @@ def test_bulk_synthesis_partial_batch_block(nb, max_batch):
         assert torch.equal(one[0], bulk[b]), b
     pb.close()
     pc.close()
+
+
+@pytest.mark.parametrize("nb,max_batch", [(25, 25), (13, 18), (8, 16)])
+def test_ponly_partial_batch_block(nb, max_batch):
+    """H-free synthesis (operand conversion + P-only bulk kernel) with batch blocks of
+    6 states, the last one partial: every state's Fourier coefficients are bitwise
+    those of a one-state synthesis, and the workspace entries of states
+    nb..max_batch-1 keep a sentinel (no store past the last state)."""
+    import torch
+
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    with plan_env(SDCSW_PONLY="1"):
+        p = SphericalShallowWater(127, max_batch=max_batch)
+    assert p.uses_ponly
+    states = np.stack([random_initial_state(p.grid, 170 + b) for b in range(nb)])
+    u = torch.from_numpy(states).to(p.device).contiguous()
+    w = p.workspace(0).view(max_batch, -1)
+    w.fill_(12345.0)
+
+    def synth(x, n):
+        _native_check(p, 0, x, n, p.stream())
+        torch.cuda.synchronize()
+        return w.clone()
+
+    full = synth(u, nb)
+    assert torch.isfinite(full[:nb]).all()
+    assert (full[nb:] == 12345.0).all()
+    for b in sorted({0, 5, 6, nb - 2, nb - 1}):
+        one = synth(u[b : b + 1].contiguous(), 1)
+        assert torch.equal(one[0], full[b]), b
+    p.close()
 
 
 def _native_check(p, stage, u, nb, s):
@@ -791,29 +851,26 @@ def test_dsdc_order_and_sweep_monotonicity_on_the_sphere():
 
 
 @pytest.mark.parametrize(
-    "trunc,grid,nb,max_batch",
-    [(42, (64, 192), 2, 2), (85, (128, 384), 3, 3), (127, None, 4, 4), (127, None, 20, 32),
-     (383, (576, 1536), 1, 1), (511, None, 2, 2)],
+    "trunc,grid,nb,max_batch,ponly",
+    [(42, (64, 192), 2, 2, None), (85, (128, 384), 3, 3, None), (127, None, 4, 4, None),
+     (127, None, 20, 32, None), (127, None, 20, 32, "0"), (383, (576, 1536), 1, 1, None),
+     (511, None, 2, 2, None), (511, None, 2, 2, "0")],
 )
-def test_ring_tma_stores_match_plain_stores(trunc, grid, nb, max_batch):
+def test_ring_tma_stores_match_plain_stores(trunc, grid, nb, max_batch, ponly):
     """The ring kernel's analysis data written by TMA tensor stores from shared
     memory (record order; fragment order from T200 and for ensembles; one box
     of L rows - 43 and 86 included - or 192 / 256-row boxes at T383 / T511) is bitwise the data of the
-    per-thread stores (SDCSW_RING_TMA_STORE=0): f_E agrees bit for bit."""
+    per-thread stores (SDCSW_RING_TMA_STORE=0): f_E agrees bit for bit.  Table-streaming
+    plans (T >= 200, ensembles) run H-free with the five-slot data; ponly = "0" forces
+    the P/H tables and the seven-slot fragment order."""
     from paper_2403_20135_b200.problem import SphericalShallowWater
 
     plans = []
+    extra = {"SDCSW_PONLY": ponly} if ponly else {}
     for mode in ("1", "0"):
-        old = os.environ.get("SDCSW_RING_TMA_STORE")
-        os.environ["SDCSW_RING_TMA_STORE"] = mode
-        try:
+        with plan_env(SDCSW_RING_TMA_STORE=mode, **extra):
             nlat, nlon = grid or (None, None)
             plans.append(SphericalShallowWater(trunc, nlat=nlat, nlon=nlon, max_batch=max_batch))
-        finally:
-            if old is None:
-                del os.environ["SDCSW_RING_TMA_STORE"]
-            else:
-                os.environ["SDCSW_RING_TMA_STORE"] = old
     import torch
 
     g, c = plans[0].grid, plans[0].n_coef

@@ -267,3 +267,90 @@ def test_known_answer_flows_catch_wind_sign_errors(small, flip):
     p = Mutant(g.trunc, g.nlat, g.nlon, tables=(p0.mu, p0.w, p0.p, p0.h, p0.m_of, p0.n_of))
     worst = max(kat_error(p, name) for name in _KAT_FLOWS if name != "rotation_a0")
     assert worst > 0.1
+
+
+# -- H-free formulation (paper_2403_20135_b200/csrc/legendre_ponly.cu) ---------
+
+
+def _eps(n, m):
+    n = np.asarray(n, dtype=float)
+    return np.where(n > m, np.sqrt(np.maximum(n * n - m * m, 0.0) / (4.0 * n * n - 1.0)), 0.0)
+
+
+def _p_extended(o):
+    """P_k^m at the oracle's nodes for k = m..T+1 (scipy), one [T+2-m, nlat] block per m."""
+    import scipy.special as sps
+
+    t = o.trunc
+    allp = sps.sph_legendre_p_all(t + 1, t + 1, np.arccos(o.mu))[0]
+    return [allp[m : t + 2, m] for m in range(t + 1)]
+
+
+def test_h_recurrence_on_oracle_tables(small):
+    """H_n = a_n P_{n-1} + b_n P_{n+1}, a_n = (n+1) eps_n, b_n = -n eps_{n+1}: the identity
+    the H-free GPU transforms rest on, checked against the oracle's own H table."""
+    _, o = small
+    t = o.trunc
+    pext = _p_extended(o)
+    for m in range(t + 1):
+        sl = slice(o.bounds[m], o.bounds[m + 1])
+        n = np.arange(m, t + 1)
+        pe = pext[m]  # rows k - m
+        lower = np.vstack([np.zeros((1, pe.shape[1])), pe[:-2]])  # P_{n-1}
+        rec = ((n + 1) * _eps(n, m))[:, None] * lower - (n * _eps(n + 1, m))[:, None] * pe[1:]
+        h = o.h[sl]
+        assert np.abs(rec - h).max() <= 1e-13 * max(1.0, np.abs(h).max()), m
+
+
+def test_h_free_f_expl_matches_oracle(small):
+    """numpy restatement of the GPU's H-free chain - operand recurrence (k_xsyn_ponly),
+    P-only synthesis to degree T+1, grid products, P analyses of A..E to T+1 and the
+    assembly (k_assemble_ponly) - equals the oracle's P/H f_E to rounding."""
+    g, o = small
+    t, a = o.trunc, o.radius
+    x = rand_state(o, np.random.default_rng(5), 1e-6)
+    phi, zeta, delta = o.views(x)
+    psi, chi = -zeta * o.inv_lam, -delta * o.inv_lam
+    pext = _p_extended(o)
+    nf = o.nlon // 2 + 1
+    four = {k: np.zeros((o.nlat, nf), complex) for k in ("u", "v", "z", "p")}
+    for m in range(t + 1):
+        sl = slice(o.bounds[m], o.bounds[m + 1])
+        k = np.arange(m, t + 2)
+        ext = lambda v: np.concatenate([v[sl], [0.0]])  # noqa: E731  degree T+1 entry = 0
+        ps, cs = ext(psi), ext(chi)
+        up1 = lambda v: np.concatenate([v[1:], [0.0]])  # noqa: E731  X_{k+1}
+        dn1 = lambda v: np.concatenate([[0.0], v[:-1]])  # noqa: E731  X_{k-1}
+        ak1 = (k + 2) * _eps(k + 1, m)  # a_{k+1}
+        bk1 = -(k - 1) * _eps(k, m)  # b_{k-1}
+        uc = (1j * m * cs - (ak1 * up1(ps) + bk1 * dn1(ps))) / a
+        vc = (1j * m * ps + (ak1 * up1(cs) + bk1 * dn1(cs))) / a
+        pe = pext[m]
+        four["u"][:, m] = uc @ pe
+        four["v"][:, m] = vc @ pe
+        four["z"][:, m] = ext(zeta) @ pe
+        four["p"][:, m] = ext(phi) @ pe
+    ug, vg, zg, pg = (o.to_grid(four[k]) for k in ("u", "v", "z", "p"))
+    eta = zg + (2.0 * o.omega * o.mu)[:, None]
+    prods = [eta * ug, eta * vg, pg * ug, pg * vg, (ug * ug + vg * vg) / (2.0 * o.coslat2)[:, None]]
+    fo = [o.to_fourier(f) for f in prods]
+    ws = 2.0 * np.pi * o.w / (a * o.coslat2)
+    wk = 2.0 * np.pi * o.w
+    out = np.empty(o.state_size, complex)
+    c = o.n_coef
+    for m in range(t + 1):
+        sl = slice(o.bounds[m], o.bounds[m + 1])
+        n = np.arange(m, t + 1)
+        pe = pext[m]
+        hat = [pe @ (ws * f[:, m]) for f in fo[:4]] + [pe @ (wk * fo[4][:, m])]
+        an, bn = (n + 1) * _eps(n, m), -n * _eps(n + 1, m)
+        rec = lambda y: an * np.concatenate([[0.0], y[: len(n) - 1]]) + bn * y[1:]  # noqa: E731
+        A, B, C, D, E = hat
+        out[sl] = -1j * m * C[:-1] + rec(D)
+        out[c + o.bounds[m] : c + o.bounds[m + 1]] = -1j * m * A[:-1] + rec(B)
+        out[2 * c + o.bounds[m] : 2 * c + o.bounds[m + 1]] = 1j * m * B[:-1] + rec(A) + o.lam[sl] * E[:-1]
+    for k in range(3):
+        seg = out[k * c : (k + 1) * c]
+        seg[o.m_of == 0] = seg[o.m_of == 0].real
+    ref = o.f_expl(x)
+    assert max(relative_l2(out, ref, o)) < 1e-12
