@@ -335,16 +335,21 @@ STAGE_NAMES = {3: "legendre_synthesis", 1: "ring_fft_products", 2: "legendre_ana
 def stage_work(problem, name, nb):
     """Algorithmic work of one launch over nb states: (amount, unit, bound).
 
-    Legendre GEMMs: 24 C J nb flop (synthesis) and 28 C J nb (analysis), C =
-    (T+1)(T+2)/2, J = nlat/2.  Ring kernel: 4 Fourier
-    fields in and 5 product fields out, 16 B per complex value, nlat (T+1)
+    Legendre GEMMs with the P and H tables: 24 C J nb flop (synthesis: P on 4
+    complex fields, H on 2) and 28 C J nb (analysis: P on 4, H on 3), C =
+    (T+1)(T+2)/2, J = nlat/2.  H-free plans
+    (problem.uses_ponly, legendre_ponly.cu): P only, to degree T+1 - C' = C + T + 1
+    coefficients - 16 C' J nb (4 complex fields) and 20 C' J nb (5); their stage
+    times include the operand conversion and the assembly kernels.  Ring kernel: 4
+    Fourier fields in and 5 product fields out, 16 B per complex value, nlat (T+1)
     values per field and state."""
     g = problem.grid
     cc, j, ll = g.n_coef, g.nlat // 2, g.trunc + 1
+    ponly = getattr(problem, "uses_ponly", False)
     if name == "legendre_synthesis":
-        return 24.0 * cc * j * nb, "flop", "tensor"
+        return (16.0 * (cc + ll) if ponly else 24.0 * cc) * j * nb, "flop", "tensor"
     if name == "legendre_analysis":
-        return 28.0 * cc * j * nb, "flop", "tensor"
+        return (20.0 * (cc + ll) if ponly else 28.0 * cc) * j * nb, "flop", "tensor"
     return 9.0 * 16.0 * g.nlat * ll * nb, "B", "hbm"
 
 
@@ -402,6 +407,10 @@ def roofline_of(problem, name, nb, seconds, cfgname, fused=False):
     tname = name + ("_fused" if fused and name == "legendre_analysis" else "")
     roof.update({"kernel": tname, "launch_nb": nb, "us_per_launch": seconds * 1e6,
                  "traffic": measured_traffic(cfgname, tname, nb)})
+    if getattr(problem, "uses_ponly", False) and bound == "tensor":
+        roof["transforms"] = ("H-free: P to degree T+1 (stage = operand conversion + P synthesis)"
+                              if name == "legendre_synthesis" else
+                              "H-free: P to degree T+1 (stage = P analysis + recurrence assembly)")
     return roof
 
 

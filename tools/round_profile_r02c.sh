@@ -1,9 +1,10 @@
 #!/bin/bash
-# ncu evidence for round 2: c1 launch list of the bench command, DRAM traffic per
-# stage kernel (c1, c3) and one --set full capture of every stage kernel.
+# ncu evidence after the H-free transforms: c1 launch list of the bench command, DRAM
+# traffic per stage (c1, c2, c3), and a --set full capture of the c3 H-free stage kernels
+# (kept under the 64 MiB gpurun_out limit: c3 only, stage kernels only).
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-tag=${TAG:-r02}
+tag=${TAG:-r02c}
 cmd="python bench.py --steps 2 --warmup 3 --no-cpu --no-large"
 $cmd > gpurun_out/plain_${tag}.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -s 600 -c 400 --csv \
@@ -13,4 +14,6 @@ ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.su
     --clock-control none --csv --log-file gpurun_out/traffic_${tag}.csv \
     python tools/traffic_capture.py c1 c2 c3 > gpurun_out/traffic_capture_${tag}.log 2>&1; echo "traffic rc=$?"
 ncu --profile-from-start off --set full --import-source on --clock-control none \
-    -o gpurun_out/prof_${tag}_stages python tools/traffic_capture.py c1 c2 c3 > gpurun_out/ncu_full_${tag}.log 2>&1; echo "full rc=$?"
+    -k regex:"k_synthesis_bulk|k_analysis_bulk_ponly|k_ring|k_xsyn_ponly|k_assemble_ponly" \
+    -o gpurun_out/prof_${tag}_c3 python tools/traffic_capture.py c3 > gpurun_out/ncu_full_${tag}.log 2>&1; echo "full rc=$?"
+ls -la gpurun_out/prof_${tag}_c3.ncu-rep

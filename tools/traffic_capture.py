@@ -51,11 +51,15 @@ def main(names):
             def stage(k):
                 dst = fi if k == 4 else out
                 _native.check(lib.sdcsw_transform_stage(p.handle, k, states.data_ptr(), dst.data_ptr(), nb, s))
-            stage(0)  # operand prep + synthesis (not labelled: two kernels)
-            print("SKIP 2", flush=True)
+            # H-free plans: stage 3 = operand conversion + synthesis, stage 2 = analysis +
+            # assembly (two kernels each, summed by traffic_to_json); stage 0 adds the prep
+            po = p.uses_ponly
+            stage(0)  # operand prep + synthesis (not labelled)
+            print(f"SKIP {3 if po else 2}", flush=True)
             for k, lab in ((3, "legendre_synthesis"), (1, "ring_fft_products"), (2, "legendre_analysis")):
                 stage(k)
-                print(f"LAUNCH {name}:{lab}:nb{nb}", flush=True)
+                for _ in range(2 if po and k != 1 else 1):
+                    print(f"LAUNCH {name}:{lab}:nb{nb}", flush=True)
             if fused and nb == mm:
                 stage(4)
                 print(f"LAUNCH {name}:legendre_analysis_fused:nb{nb}", flush=True)

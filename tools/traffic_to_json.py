@@ -43,9 +43,12 @@ def main(log, csv_path, out="profiles/ncu_traffic_r02.json"):
         if lab is None:
             continue
         cfg, kern, nb = lab.split(":")
-        res.setdefault(cfg, {})[f"{kern}:{nb}"] = d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
-        res[cfg][f"{kern}:{nb}:kernel"] = d["kernel"][:80]
-        res[cfg][f"{kern}:{nb}:ncu_us"] = d.get("gpu__time_duration.sum", 0) / 1e3
+        # a label repeated by consecutive launches (the H-free stages' two kernels) sums them
+        r = res.setdefault(cfg, {})
+        key = f"{kern}:{nb}"
+        r[key] = r.get(key, 0.0) + d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
+        r[key + ":kernel"] = (r[key + ":kernel"] + " + " if key + ":kernel" in r else "") + d["kernel"][:80]
+        r[key + ":ncu_us"] = r.get(key + ":ncu_us", 0.0) + d.get("gpu__time_duration.sum", 0) / 1e3
     with open(out, "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps(res, indent=1))
