@@ -301,16 +301,18 @@ constexpr int kSynKQ = SDCSW_SYNB_KQ;      // row quads (4 table rows each) per 
 constexpr int kSynBS = SDCSW_SYNB_STAGES;  // stages in flight
 
 // PO (H-free path, legendre_ponly.cu): one table (P to degree T+1) and two operand parts
-__host__ __device__ constexpr int synb_stage_doubles(int wj, int nbt, bool po = false) {
-  return po ? kSynKQ * (wj * 64 + 32 * nbt) + 16
-            : kSynKQ * (2 * wj * 64 + 48 * nbt) + 16;  // + pad: odd-pair reads past the last quad
+// kq: row quads per stage (the H-free kernel takes 8 from T400: T511 5 states 180 -> 168 us;
+// 4 elsewhere, where 8 measured slower)
+__host__ __device__ constexpr int synb_stage_doubles(int wj, int nbt, bool po = false, int kq = kSynKQ) {
+  return po ? kq * (wj * 64 + 32 * nbt) + 16
+            : kq * (2 * wj * 64 + 48 * nbt) + 16;  // + pad: odd-pair reads past the last quad
 }
-__host__ __device__ constexpr size_t synb_smem(int wj, int nbt, bool po = false) {
-  return (size_t)kSynBS * synb_stage_doubles(wj, nbt, po) * 8 + 8 * kSynBS;
+__host__ __device__ constexpr size_t synb_smem(int wj, int nbt, bool po = false, int kq = kSynKQ) {
+  return (size_t)kSynBS * synb_stage_doubles(wj, nbt, po, kq) * 8 + 8 * kSynBS;
 }
 
 
-template <int NB, bool PO>
+template <int NB, bool PO, int KQ = kSynKQ>
 __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_MINB) k_synthesis_bulk(
     const double* __restrict__ xsyn, int nb, int J, const double* __restrict__ ptab,
     const double* __restrict__ htab, const int* __restrict__ rowoff,
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
   constexpr int QX = 16 * NPART * NB;  // operand doubles per row quad (parts x NB states x 16)
   extern __shared__ __align__(128) unsigned char synb_raw[];
   const int WJ = blockDim.x >> 5;
-  const int SD = synb_stage_doubles(WJ, NB, PO);
+  const int SD = synb_stage_doubles(WJ, NB, PO, KQ);
   const int TQ = WJ * 64;  // table doubles per row quad of this CTA's latitudes
   double* stages = reinterpret_cast<double*>(synb_raw);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(synb_raw + (size_t)kSynBS * SD * 8);
@@ -345,7 +347,7 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
   const int r0m = rowoff[m];
   const int nsteps = (rowoff[m + 1] - r0m) >> 2;
   const int se = n_even[m] >> 2;
-  const int nstage = (nsteps + kSynKQ - 1) / kSynKQ;
+  const int nstage = (nsteps + KQ - 1) / KQ;
   const size_t qstride = (size_t)(J / 8) * 32;
   const double* Pc = ptab + (size_t)(r0m / 4) * qstride + (size_t)blockIdx.x * TQ;
   const double* Hc = htab + (size_t)(r0m / 4) * qstride + (size_t)blockIdx.x * TQ;
@@ -355,25 +357,25 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
   const size_t qxg = (size_t)16 * NPART * nb;  // operand doubles per row quad (all states)
   const double* Xc = xsyn + (size_t)(r0m / 4) * qxg + (size_t)b0 * 16;
 
-  auto nq_of = [&](int i) { return min(kSynKQ, nsteps - i * kSynKQ); };
+  auto nq_of = [&](int i) { return min(KQ, nsteps - i * KQ); };
   auto issue_tables = [&](int i) {  // thread 0
     double* st = stages + (i % kSynBS) * SD;
     const int nq = nq_of(i);
     mbar_expect_tx(&full[i % kSynBS], (unsigned)(nq * (NTAB * TQ + 16 * NPART * nbv) * 8));
     for (int q = 0; q < nq; ++q) {
-      const size_t src = (size_t)(i * kSynKQ + q) * qstride;
+      const size_t src = (size_t)(i * KQ + q) * qstride;
       bulk_g2s(st + q * TQ, Pc + src, TQ * 8, &full[i % kSynBS]);
-      if constexpr (!PO) bulk_g2s(st + (kSynKQ + q) * TQ, Hc + src, TQ * 8, &full[i % kSynBS]);
+      if constexpr (!PO) bulk_g2s(st + (KQ + q) * TQ, Hc + src, TQ * 8, &full[i % kSynBS]);
     }
   };
   auto issue_operand = [&](int i) {  // thread 0, after the producer grid completed
-    double* st = stages + (i % kSynBS) * SD + NTAB * kSynKQ * TQ;
+    double* st = stages + (i % kSynBS) * SD + NTAB * KQ * TQ;
     if (nb == NB) {
-      bulk_g2s(st, Xc + (size_t)i * kSynKQ * QX, (unsigned)(nq_of(i) * QX * 8), &full[i % kSynBS]);
+      bulk_g2s(st, Xc + (size_t)i * KQ * QX, (unsigned)(nq_of(i) * QX * 8), &full[i % kSynBS]);
     } else {  // one run of nbv states per (quad, part), placed at the block's [part][NB] stride
       for (int q = 0; q < nq_of(i); ++q)
         for (int pp = 0; pp < NPART; ++pp)
-          bulk_g2s(st + q * QX + pp * 16 * NB, Xc + (size_t)(i * kSynKQ + q) * qxg + pp * 16 * nb,
+          bulk_g2s(st + q * QX + pp * 16 * NB, Xc + (size_t)(i * KQ + q) * qxg + pp * 16 * nb,
                    (unsigned)(nbv * 16 * 8), &full[i % kSynBS]);
     }
   };
@@ -403,13 +405,13 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
     const double* st = stages + (i % kSynBS) * SD;
     const int nq = nq_of(i);
 #pragma unroll
-    for (int q = 0; q < kSynKQ; ++q) {
+    for (int q = 0; q < KQ; ++q) {
       if (q < nq) {
         const double* pq = st + q * TQ + warp * 64 + lane;
-        const double* hq = pq + kSynKQ * TQ;
+        const double* hq = pq + KQ * TQ;
         const double aP0 = pq[0], aP1 = pq[32];
         const double aH0 = PO ? 0.0 : hq[0], aH1 = PO ? 0.0 : hq[32];
-        const double* xq0 = st + NTAB * kSynKQ * TQ + q * QX + t * 4 + gc;
+        const double* xq0 = st + NTAB * KQ * TQ + q * QX + t * 4 + gc;
         const double* xq = xq0 + gb * 16;
         double bP[NT], bH[NH];
 #pragma unroll
@@ -423,14 +425,14 @@ __global__ void __launch_bounds__(128, NB <= 2 ? SDCSW_SYNB_MINB1 : SDCSW_SYNB_M
           bH[NH - 1] = !PO && gb == 0 ? xq0[32 * NB + (NB - 1) * 16] : 0.0;
         }
         if constexpr (PO) {  // H-free: every operand column is a P column
-          if (i * kSynKQ + q < se) {
+          if (i * KQ + q < se) {
 #pragma unroll
             for (int c = 0; c < NT; ++c) { dmma_t(aE[0][c], aP0, bP[c]); dmma_t(aE[1][c], aP1, bP[c]); }
           } else {
 #pragma unroll
             for (int c = 0; c < NT; ++c) { dmma_t(aO[0][c], aP0, bP[c]); dmma_t(aO[1][c], aP1, bP[c]); }
           }
-        } else if (i * kSynKQ + q < se) {  // n - m even: P symmetric (E), H antisymmetric (O)
+        } else if (i * KQ + q < se) {  // n - m even: P symmetric (E), H antisymmetric (O)
 #pragma unroll
           for (int c = 0; c < NT; ++c) { dmma_t(aE[0][c], aP0, bP[c]); dmma_t(aE[1][c], aP1, bP[c]); }
 #pragma unroll
@@ -493,7 +495,11 @@ cudaError_t configure_synthesis_bulk() {
   if (e == cudaSuccess)                                                                       \
     e = cudaFuncSetAttribute(k_synthesis_bulk<NBV, true>,                                     \
                              cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
-                             (int)synb_smem(4, NBV, true));
+                             (int)synb_smem(4, NBV, true));                                   \
+  if (e == cudaSuccess)                                                                       \
+    e = cudaFuncSetAttribute(k_synthesis_bulk<NBV, true, 8>,                                  \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
+                             (int)synb_smem(4, NBV, true, 8));
   SDCSW_SYNB_CFG(1) SDCSW_SYNB_CFG(2) SDCSW_SYNB_CFG(3) SDCSW_SYNB_CFG(4) SDCSW_SYNB_CFG(5)
   SDCSW_SYNB_CFG(6)
 #undef SDCSW_SYNB_CFG
@@ -534,10 +540,15 @@ cudaError_t launch_synthesis_bulk_ponly(const Plan& p, double2* fsyn, const int*
   const int NB = nb <= 6 ? nb : 6;
   const dim3 grid(p.J / (kRowsPerWarp * WJ), nm, (nb + NB - 1) / NB);
 #define SDCSW_SYNP_LAUNCH(NBV)                                                                 \
-  if (NB == NBV)                                                                               \
+  if (NB == NBV) {                                                                             \
+    if (p.T >= 400)                                                                            \
+      return launch_k(k_synthesis_bulk<NBV, true, 8>, grid, dim3(32 * WJ),                     \
+                      synb_smem(WJ, NBV, true, 8), s, xsp, nb, p.J, p.ptabP_s, p.ptabP_s,     \
+                      p.rowoffP, p.n_evenP, fsyn, step_counter, mlist, Lp, sd);              \
     return launch_k(k_synthesis_bulk<NBV, true>, grid, dim3(32 * WJ), synb_smem(WJ, NBV, true), \
                     s, xsp, nb, p.J, p.ptabP_s, p.ptabP_s, p.rowoffP, p.n_evenP, fsyn,          \
-                    step_counter, mlist, Lp, sd);
+                    step_counter, mlist, Lp, sd);                                               \
+  }
   SDCSW_SYNP_LAUNCH(1) SDCSW_SYNP_LAUNCH(2) SDCSW_SYNP_LAUNCH(3) SDCSW_SYNP_LAUNCH(4)
   SDCSW_SYNP_LAUNCH(5) SDCSW_SYNP_LAUNCH(6)
 #undef SDCSW_SYNP_LAUNCH
