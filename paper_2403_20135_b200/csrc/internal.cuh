@@ -132,6 +132,7 @@ struct Plan {
   int* moffP;         // [T+2] offsets of the extended triangle (T+2-m entries per m)
   int4* cvt_rows;     // [rowsP] xsyn rows of (m,k), (m,k-1), (m,k+1) (-1: none), P-triangle index
   double2* cvt_ab;    // [rowsP] (a_{k+1}, b_{k-1}): weights of X_{k+1}, X_{k-1}
+  int4* prep_idx;     // [rowsP] coefficient indices of (m,k), (m,k-1), (m,k+1) (-1: none), m
   int2* asm_pos;      // [C] (extended-triangle index of (m,n), m)
   double2* asm_ab;    // [C] (a_n, b_n)
   int* anal_workP;    // [n_anal_workP] (m << 16 | 64-row block) over the P rows
@@ -571,6 +572,10 @@ cudaError_t launch_synthesis_ponly(const Plan& p, double2* fsyn, const int* mlis
                                    double* xsp, const double* xsyn, int nb, cudaStream_t s,
                                    int* step_counter, const SynDst& sd);
 cudaError_t launch_analysis_ponly(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s);
+// H-free f_E straight from nb states u (the P-only operand built from the states, no
+// 12-double records): the dSDC stepper's path on H-free plans
+cudaError_t f_expl_states_ponly(const Plan& p, const Work& w, const double2* u, double2* fe, int nb,
+                                cudaStream_t s, int* step_counter);
 cudaError_t make_gan_maps(Plan& p);
 cudaError_t configure_synthesis_bulk();
 cudaError_t configure_analysis_bulk();

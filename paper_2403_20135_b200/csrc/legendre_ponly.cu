@@ -85,6 +85,60 @@ __global__ void __launch_bounds__(256) k_xsyn_ponly(const double* __restrict__ x
 }
 
 // ---------------------------------------------------------------------------
+// operand from the states: the same P-only records as k_xsyn_ponly, built from
+// nb states u [b][Phi', zeta, delta][C] complex with the producers' rounding
+// (write_xsyn_half: U_P = -i sm delta, V_P = -i sm zeta, U_H = sa zeta,
+// V_H = -sa delta, (sm, sa) = xscale), so both routes give the same bits.  The
+// dSDC stepper on H-free plans keeps its node states and calls this instead of
+// writing 12-double records (96 B) that the conversion re-reads.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_prep_ponly(const double2* __restrict__ u, int C, int rowsP,
+                                                    int nb, const int4* __restrict__ prep_idx,
+                                                    const double2* __restrict__ cvt_ab,
+                                                    const double2* __restrict__ xscale,
+                                                    double* __restrict__ xsp) {
+  SDCSW_PDL_ENTRY();
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)rowsP * nb;
+  if (tid >= total) return;
+  const int w = nb;
+  const int r4 = (int)(tid / (4 * w)), rem = (int)(tid - (long long)r4 * 4 * w);
+  const int b = rem >> 2, rr = rem & 3;
+  const int r = 4 * r4 + rr;
+  const int4 ix = prep_idx[r];  // constant plan data: before the dependency wait
+  const double2 ab = cvt_ab[r];
+  const double2 sc0 = ix.x >= 0 ? xscale[ix.x] : make_double2(0.0, 0.0);
+  const double sa_lo = ix.y >= 0 ? xscale[ix.y].y : 0.0, sa_hi = ix.z >= 0 ? xscale[ix.z].y : 0.0;
+  SDCSW_PDL_WAIT();
+  const double2* s = u + (size_t)b * 3 * C;
+  const size_t ps = 16 * (size_t)w;
+  double* out = xsp + ((size_t)r4 * 2 * w + b) * 16 + rr * 4;
+  double4 p0 = make_double4(0.0, 0.0, 0.0, 0.0), p1 = p0;
+  if (ix.x >= 0) {
+    const double2 phi = s[ix.x], zeta = s[C + ix.x], delta = s[2 * C + ix.x];
+    const double sm = sc0.x;
+    p0 = make_double4(sm * delta.y, -sm * delta.x, sm * zeta.y, -sm * zeta.x);  // U_P, V_P
+    p1 = make_double4(zeta.x, zeta.y, phi.x, phi.y);
+  }
+  if (ix.z >= 0) {  // a_{k+1} (U_H, V_H)(k+1)
+    const double2 z = s[C + ix.z], d = s[2 * C + ix.z];
+    p0.x = __fma_rn(ab.x, sa_hi * z.x, p0.x);
+    p0.y = __fma_rn(ab.x, sa_hi * z.y, p0.y);
+    p0.z = __fma_rn(ab.x, -sa_hi * d.x, p0.z);
+    p0.w = __fma_rn(ab.x, -sa_hi * d.y, p0.w);
+  }
+  if (ix.y >= 0) {  // b_{k-1} (U_H, V_H)(k-1)
+    const double2 z = s[C + ix.y], d = s[2 * C + ix.y];
+    p0.x = __fma_rn(ab.y, sa_lo * z.x, p0.x);
+    p0.y = __fma_rn(ab.y, sa_lo * z.y, p0.y);
+    p0.z = __fma_rn(ab.y, -sa_lo * d.x, p0.z);
+    p0.w = __fma_rn(ab.y, -sa_lo * d.y, p0.w);
+  }
+  *reinterpret_cast<double4*>(out) = p0;
+  *reinterpret_cast<double4*>(out + ps) = p1;
+}
+
+// ---------------------------------------------------------------------------
 // assembly: f_E(m, n) from the P analyses at degrees n - 1, n, n + 1
 //   Phi'_t = -i m C_n + a_n D_{n-1} + b_n D_{n+1}
 //   zeta_t = -i m A_n + a_n B_{n-1} + b_n B_{n+1}
@@ -142,6 +196,20 @@ cudaError_t launch_synthesis_ponly(const Plan& p, double2* fsyn, const int* mlis
   return launch_synthesis_bulk_ponly(p, fsyn, mlist, nm, Lp, xsp, nb, s, step_counter, sd);
 }
 
+cudaError_t f_expl_states_ponly(const Plan& p, const Work& w, const double2* u, double2* fe, int nb,
+                                cudaStream_t s, int* step_counter) {
+  if (!ponly_on(p) || p.own_idx != nullptr || w.xsp == nullptr) return cudaErrorInvalidValue;
+  const long long total = (long long)p.rowsP * nb;
+  cudaError_t e = launch_k(k_prep_ponly, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, s, u,
+                           p.C, p.rowsP, nb, p.prep_idx, p.cvt_ab, p.xscale, w.xsp);
+  if (e == cudaSuccess)
+    e = launch_synthesis_bulk_ponly(p, w.fsyn, nullptr, p.T + 1, p.T + 1, w.xsp, nb, s, step_counter,
+                                    SynDst{});
+  if (e == cudaSuccess) e = launch_ring(p, w, nb, s);
+  if (e == cudaSuccess) e = launch_analysis_ponly(p, w, fe, nb, s);
+  return e;
+}
+
 cudaError_t launch_analysis_ponly(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s) {
   cudaError_t e = launch_analysis_bulk_ponly(p, w, nb, s);
   if (e != cudaSuccess) return e;
@@ -163,13 +231,13 @@ static long double eps_l(int n, int m) {
 }
 
 void ponly_free(Plan& p) {
-  void* ptrs[] = {p.ptabP, p.ptabP_s, p.rowoffP, p.n_evenP, p.rowP_n, p.moffP, p.cvt_rows,
+  void* ptrs[] = {p.ptabP, p.ptabP_s, p.rowoffP, p.n_evenP, p.rowP_n, p.moffP, p.cvt_rows, p.prep_idx,
                   p.cvt_ab, p.asm_pos, p.asm_ab, p.anal_workP, p.own_workP, p.xsynP, p.ghat};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   p.ptabP = p.ptabP_s = nullptr;
   p.rowoffP = p.n_evenP = p.rowP_n = p.moffP = p.anal_workP = p.own_workP = nullptr;
-  p.cvt_rows = nullptr;
+  p.cvt_rows = p.prep_idx = nullptr;
   p.cvt_ab = p.asm_ab = nullptr;
   p.asm_pos = nullptr;
   p.xsynP = p.ghat = nullptr;
@@ -210,12 +278,13 @@ cudaError_t ponly_setup(Plan& p, const double* ptab, const int* rowoff, const in
   }
   const int rowsP = rowoffP[T + 1], CP = moffP[T + 1];
   std::vector<double> tabP((size_t)rowsP * J, 0.0), tabS((size_t)rowsP * J, 0.0);
-  std::vector<int4> cvt(rowsP);
+  std::vector<int4> cvt(rowsP), pidx(rowsP);
   std::vector<double2> cab(rowsP);
   for (int m = 0; m <= T; ++m)
     for (int r = rowoffP[m]; r < rowoffP[m + 1]; ++r) {
       const int k = rowP_n[r];
       cvt[r] = make_int4(-1, -1, -1, m);
+      pidx[r] = make_int4(-1, -1, -1, m);
       cab[r] = make_double2(0.0, 0.0);
       if (k < 0) continue;
       double* dst = tabP.data() + (size_t)r * J;
@@ -232,6 +301,8 @@ cudaError_t ponly_setup(Plan& p, const double* ptab, const int* rowoff, const in
         }
       }
       cvt[r] = make_int4(xr(m, k), k - 1 >= m ? xr(m, k - 1) : -1, xr(m, k + 1), m);
+      auto ci = [&](int n) { return (n < m || n > T) ? -1 : moff[m] + n - m; };
+      pidx[r] = make_int4(ci(k), ci(k - 1), ci(k + 1), m);
       // a_{k+1} = (k + 2) eps_{k+1}, b_{k-1} = -(k - 1) eps_k
       cab[r] = make_double2((double)((k + 2) * eps_l(k + 1, m)), (double)(-(k - 1) * eps_l(k, m)));
     }
@@ -260,6 +331,7 @@ cudaError_t ponly_setup(Plan& p, const double* ptab, const int* rowoff, const in
       (e = up(&p.rowoffP, rowoffP)) != cudaSuccess || (e = up(&p.n_evenP, n_evenP)) != cudaSuccess ||
       (e = up(&p.rowP_n, rowP_n, 16)) != cudaSuccess || (e = up(&p.moffP, moffP)) != cudaSuccess ||
       (e = up(&p.cvt_rows, cvt)) != cudaSuccess || (e = up(&p.cvt_ab, cab)) != cudaSuccess ||
+      (e = up(&p.prep_idx, pidx)) != cudaSuccess ||
       (e = up(&p.asm_pos, apos)) != cudaSuccess || (e = up(&p.asm_ab, aab)) != cudaSuccess ||
       (e = up(&p.anal_workP, work)) != cudaSuccess ||
       (e = cudaMalloc(&p.xsynP, (size_t)p.max_batch * rowsP * kXsynP * sizeof(double))) != cudaSuccess ||

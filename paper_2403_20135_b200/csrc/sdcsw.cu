@@ -107,6 +107,7 @@ struct sdcsw_stepper {
   double* graph_u;
   int launches;
   size_t nstates;  // state-sized buffers in buf
+  int sprep;       // H-free dSDC: f_E builds its P-only operand from the node states (ustage)
   sdcsw_sweep_hook hook;  // per-sweep host callback of sdcsw_stepper_step_hooked (else null)
   void* hook_user;
 };
@@ -921,9 +922,11 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
   const int E = st->members;
   if (marks) cudaEventRecord(marks[0], s);
   const bool planar = p.kind == 1;  // planar: f_E reads the node states, no operand records
-  cudaError_t e = planar ? planar_f_expl(p, u, st->fe0, E, s, counter)
-                         : f_expl_prepped(p, plan_work(p), st->xsyn1, st->fe0, E, s, counter,
-                                          p.fe_chunk);
+  const bool sprep = st->sprep && st->mode == 0;  // H-free: f_E from the node states too
+  cudaError_t e = planar  ? planar_f_expl(p, u, st->fe0, E, s, counter)
+                  : sprep ? f_expl_states_ponly(p, plan_work(p), u, st->fe0, E, s, counter)
+                          : f_expl_prepped(p, plan_work(p), st->xsyn1, st->fe0, E, s, counter,
+                                           p.fe_chunk);
   if (e != cudaSuccess) return e;
   if (marks) cudaEventRecord(marks[1], s);
   if (st->mode == 0) {
@@ -954,16 +957,19 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
       for (int g = 0; g < G; ++g) {
         const int lo = g * M / G, hi = (g + 1) * M / G, cnt = hi - lo;
         cudaStream_t sg = (G > 1 && !seq) ? st->side[g] : s;
-        double* xs = planar ? nullptr : st->xsynM + (size_t)lo * E * p.rows * kXsyn;
-        // spherical: the node states reach the f_E only as synthesis operands (xs),
-        // so they are not stored; the planar f_E reads them from ustage
+        const bool keep = planar || sprep;  // node states stored for an f_E that reads them
+        double* xs = keep ? nullptr : st->xsynM + (size_t)lo * E * p.rows * kXsyn;
+        // spherical P/H: the node states reach the f_E only as synthesis operands (xs),
+        // so they are not stored; the planar and H-free f_E read them from ustage
         e = launch_sweep_nodes(p, M, lo, cnt, coef, u, fe_cur, first ? 0 : 1,
-                               fi_cur, first ? 0 : 1, first, planar ? st->ustage + lo * S : nullptr,
+                               fi_cur, first ? 0 : 1, first, keep ? st->ustage + lo * S : nullptr,
                                fi_new + lo * S, xs, sg, E, first ? 1 : mS, mS, p.fe_chunk);
         if (e != cudaSuccess) return e;
-        e = planar ? planar_f_expl(p, st->ustage + lo * S, fe_new + lo * S, cnt * E, sg, nullptr)
-                   : f_expl_prepped(p, plan_work(p, lo), xs, fe_new + lo * S, cnt * E, sg,
-                                    nullptr, p.fe_chunk);
+        e = planar  ? planar_f_expl(p, st->ustage + lo * S, fe_new + lo * S, cnt * E, sg, nullptr)
+            : sprep ? f_expl_states_ponly(p, plan_work(p, lo), st->ustage + lo * S, fe_new + lo * S,
+                                          cnt * E, sg, nullptr)
+                    : f_expl_prepped(p, plan_work(p, lo), xs, fe_new + lo * S, cnt * E, sg,
+                                     nullptr, p.fe_chunk);
         if (e != cudaSuccess) return e;
       }
       if (G > 1 && !seq) {
@@ -981,7 +987,7 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
       fe_cur = fe_new;
     }
     const bool first = K == 1;
-    double* xs1 = planar ? nullptr : st->xsyn1;
+    double* xs1 = planar || sprep ? nullptr : st->xsyn1;
     if (marks) {
       e = launch_final_node(p, M, st->coef.data() + (size_t)(K - 1) * cstride, u,
                             fe_cur, first ? 0 : 1, fi_cur, first ? 0 : 1,
@@ -1084,7 +1090,11 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   // concurrently and every one reads all old tendencies); node states only
   // where an f_E reads them (planar dSDC; one state for serial SDC) - the
   // spherical dSDC step keeps node states only as synthesis operands
-  const size_t ust = mode == 1 ? 1 : (p.kind == 1 ? (size_t)E * M : 0);
+  // H-free plans (legendre_ponly.cu): the dSDC step keeps its node states and builds the
+  // P-only synthesis operand from them (k_prep_ponly), instead of writing 12-double
+  // operand records that a conversion kernel re-reads (c4: -100 MB per f_E of 256 states)
+  const int sprep = mode == 0 && p.kind == 0 && ponly_on(p) && p.own_idx == nullptr ? 1 : 0;
+  const size_t ust = mode == 1 ? 1 : (p.kind == 1 || sprep ? (size_t)E * M : 0);
   const size_t nstates = (size_t)E * (1 + 4 * (size_t)M) + ust + (mode == 1 ? (size_t)M + 1 : 0);
   s->nstates = nstates;
   cudaError_t e = cudaSetDevice(p.device);
@@ -1108,6 +1118,7 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   s->fe = q; q += E * M * s->S;
   s->fi = q; q += E * M * s->S;
   s->ustage = ust ? q : nullptr; q += ust * s->S;
+  s->sprep = sprep;
   s->fiB = q; q += E * M * s->S;
   s->feB = q; q += E * M * s->S;
   if (mode == 1) {
@@ -1188,6 +1199,9 @@ int sdcsw_stepper_launches_per_step(sdcsw_stepper* s, int* n) {
   s->launches = s->mode == 0 ? (fused_active(s) ? 3 * s->K : 4 + 4 * G * (s->K - 1))
                              : (serial_fused_active(s) ? 3 + s->K * (2 + 3 * s->M)
                                                        : 3 + s->K * 5 * s->M);
+  // H-free plans: every f_E adds its operand kernel (prep or conversion) and the assembly
+  if (ponly_on(s->plan->p) && !fused_active(s) && !serial_fused_active(s))
+    s->launches += 2 * (s->mode == 0 ? 1 + G * (s->K - 1) : 1 + s->K * s->M);
   *n = s->launches;
   return SDCSW_OK;
 }
@@ -1203,7 +1217,8 @@ int sdcsw_stepper_run(sdcsw_stepper* s, double* u, int n_steps, int use_graph, v
   if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
   if (n_steps == 0) return SDCSW_OK;
   // the caller may have changed u since the last step: rebuild its synthesis operand
-  if (s->plan->p.kind == 0) {
+  // (H-free dSDC builds it from u inside every step)
+  if (s->plan->p.kind == 0 && !s->sprep) {
     e = launch_synth_prep(s->plan->p, (const double2*)u, s->members, s->xsyn1, cs,
                           s->plan->p.fe_chunk);
     if (e != cudaSuccess) return cuda_status(e, "sdcsw_stepper_run prep");
@@ -1277,7 +1292,7 @@ int sdcsw_stepper_profile(sdcsw_stepper* s, double* u, double* stage_ms, int n, 
     for (int i = 0; i < s->K + 2; ++i) cudaEventCreate(&s->prof[i]);
     s->prof_ready = true;
   }
-  if (s->plan->p.kind == 0)
+  if (s->plan->p.kind == 0 && !s->sprep)
     e = launch_synth_prep(s->plan->p, (const double2*)u, s->members, s->xsyn1, cs,
                           s->plan->p.fe_chunk);
   if (e == cudaSuccess) e = enqueue_step(s, (double2*)u, cs, s->prof);

@@ -18,7 +18,7 @@ for cfg, nb in runs:
         L.sdcsw_transform_stage(p.handle, 1, u.data_ptr(), out.data_ptr(), nb, p.stream())
     os.environ.get('X')
     torch.cuda.synchronize()
-    n = p.grid.nlat // 2 * nb
+    n = min(p.grid.nlat // 2 * nb, 8192)
     buf = (ctypes.c_ulonglong * (8 * n))()
     L.sdcsw_debug_rtimes.argtypes = [ctypes.c_void_p, ctypes.c_int]
     L.sdcsw_debug_rtimes(buf, 8 * n)
