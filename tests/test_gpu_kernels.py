@@ -374,7 +374,7 @@ def test_ensemble_members_match_single_runs():
     single.close()
 
 
-@pytest.mark.parametrize("trunc,nparts", [(127, 2), (127, 4), (255, 2)])
+@pytest.mark.parametrize("trunc,nparts", [(127, 2), (127, 4), (255, 2), (255, 3)])
 def test_spectral_split_f_expl_bitwise(trunc, nparts):
     """Spectral split kernels on one device: the parts are run one
     after another into a shared part-major Fourier buffer (no inter-rank
@@ -885,3 +885,79 @@ def test_ring_tma_stores_match_plain_stores(trunc, grid, nb, max_batch, ponly):
     assert np.all(np.isfinite(a)) and np.linalg.norm(a) > 0
     for p in plans:
         p.close()
+
+
+def test_ponly_stepper_ensemble_matches_single_runs():
+    """H-free dSDC stepper (operand built from the node states, k_prep_ponly) at T255:
+    an ensemble of 2 members gives, per member, exactly the single-member result, and
+    both agree with the P/H stepper to rounding."""
+    import torch
+
+    from paper_2403_20135_b200.integrators import DeviceStepper
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    with plan_env(SDCSW_PONLY="1"):
+        p = SphericalShallowWater(255, max_batch=6)
+    with plan_env(SDCSW_PONLY="0"):
+        q = SphericalShallowWater(255, max_batch=3)
+    assert p.uses_ponly and not q.uses_ponly
+    cfg = SdcConfig(table=CollocationTable.radau_right(3), n_sweeps=2,
+                    mode=SweepMode.DIAGONAL_PARALLEL, time_threads=3)
+    states = np.stack([random_initial_state(p.grid, 60 + e) for e in range(2)])
+    ens = torch.from_numpy(states).to(p.device).contiguous()
+    st = DeviceStepper(p, cfg, 60.0, serial=False, members=2)
+    st.run(ens, 2)
+    single = DeviceStepper(p, cfg, 60.0, serial=False)
+    ref = DeviceStepper(q, cfg, 60.0, serial=False)
+    o = oracle_for(p)
+    for e in range(2):
+        u = torch.from_numpy(states[e]).to(p.device).contiguous()
+        single.run(u, 2)
+        assert torch.equal(u, ens[e])
+        v = torch.from_numpy(states[e]).to(q.device).contiguous()
+        ref.run(v, 2)
+        assert max(relative_l2(u.cpu().numpy(), v.cpu().numpy(), o)) < 1e-12
+    for s in (st, single, ref):
+        s.close()
+    p.close()
+    q.close()
+
+
+def test_ponly_serial_sdc_matches_ph():
+    """Serial SDC on an H-free plan (operand records + conversion route) against the
+    P/H tables at T255: two steps agree to rounding."""
+    import torch
+
+    from paper_2403_20135_b200.integrators import DeviceStepper
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    with plan_env(SDCSW_PONLY="1"):
+        p = SphericalShallowWater(255, max_batch=4)
+    with plan_env(SDCSW_PONLY="0"):
+        q = SphericalShallowWater(255, max_batch=4)
+    cfg = SdcConfig(table=CollocationTable.radau_right(3), n_sweeps=2, mode=SweepMode.SERIAL)
+    u0 = random_initial_state(p.grid, 66)
+    out = []
+    for prob in (p, q):
+        st = DeviceStepper(prob, cfg, 60.0, serial=True)
+        u = torch.from_numpy(u0).to(prob.device).contiguous()
+        st.run(u, 2)
+        out.append(u.cpu().numpy())
+        st.close()
+    assert max(relative_l2(out[0], out[1], oracle_for(p))) < 1e-12
+    p.close()
+    q.close()
+
+
+def test_ponly_t383_f_expl_vs_oracle():
+    """H-free f_E on a non-power-of-two grid (T383, 576 x 1536: L = 384, 192-row TMA store
+    boxes) against the CPU oracle with its own tables."""
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    p = SphericalShallowWater(383, nlat=576, nlon=1536, max_batch=2)
+    assert p.uses_ponly
+    u = random_initial_state(p.grid, 77)
+    u[: p.n_coef] = 4e-3 * u[p.n_coef : 2 * p.n_coef] * 1e6
+    o = SphericalShallowWaterOracle(p.grid.trunc, p.grid.nlat, p.grid.nlon)
+    assert max(relative_l2(p.f_expl(u), o.f_expl(u), o)) < 1e-10
+    p.close()
