@@ -26,28 +26,33 @@ def main(names):
     jobs = []
     for name in names:
         c = bench.CONFIGS[name]
-        mm, kk = c["nodes"], c["sweeps"]
-        p = SphericalShallowWater(c["trunc"], max_batch=mm)
+        mm, kk, me = c["nodes"], c["sweeps"], c.get("members", 1)
+        # ensembles (c4): the init f_E carries the members, the sweeps nodes x members
+        # states - the launches bench.py's stage roofline times
+        p = SphericalShallowWater(c["trunc"], max_batch=mm * me)
         cfg = SdcConfig(table=CollocationTable.radau_right(mm), n_sweeps=kk, mode=SweepMode.DIAGONAL_PARALLEL)
-        st = DeviceStepper(p, cfg, c["dt"], serial=False)
-        u = p._to_device(random_initial_state(p.grid, c["seed"])).reshape(-1).contiguous()
+        st = DeviceStepper(p, cfg, c["dt"], serial=False, members=me)
+        u0 = np.stack([random_initial_state(p.grid, c["seed"] + e) for e in range(me)])
+        u = torch.from_numpy(u0).to(p.device).reshape(-1).contiguous()
         st.run(u, 3)
         seq = bench.live_states(st, u, mm)
-        many = torch.stack(seq).contiguous()
+        many = torch.cat([x.reshape(me, -1) for x in seq]).contiguous()
+        one = seq[0].reshape(me, -1).contiguous()
+        nbm = mm * me
         fused = st.launches_per_step == 3 * kk
-        out, fi = p.empty_states(mm), p.empty_states(mm)
-        fe = p.empty_states(mm)
-        p.f_expl_device(many, fe, mm)
-        p.f_impl_device(many, fi, mm)
+        out, fi = p.empty_states(nbm), p.empty_states(nbm)
+        fe = p.empty_states(nbm)
+        p.f_expl_device(many, fe, nbm)
+        p.f_impl_device(many, fi, nbm)
         coef = diagonal_step_coefficients(cfg, c["dt"], p.mean_geopotential)
         blk = mm * (mm + 4)
         b = CudaNodeBackend(p)
-        jobs.append((name, p, st, seq, many, fused, out, fi, fe, coef, blk, b, mm, kk))
+        jobs.append((name, p, st, seq, many, one, me, fused, out, fi, fe, coef, blk, b, mm, kk))
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
-    for name, p, st, seq, many, fused, out, fi, fe, coef, blk, b, mm, kk in jobs:
+    for name, p, st, seq, many, one, me, fused, out, fi, fe, coef, blk, b, mm, kk in jobs:
         lib, s = p._lib, p.stream()
-        for nb, states in ((1, seq[0].reshape(1, -1).contiguous()), (mm, many)):
+        for nb, states in ((me, one), (mm * me, many)):
             def stage(k):
                 dst = fi if k == 4 else out
                 _native.check(lib.sdcsw_transform_stage(p.handle, k, states.data_ptr(), dst.data_ptr(), nb, s))
@@ -60,13 +65,15 @@ def main(names):
                 stage(k)
                 for _ in range(2 if po and k != 1 else 1):
                     print(f"LAUNCH {name}:{lab}:nb{nb}", flush=True)
-            if fused and nb == mm:
+            if fused and nb == mm * me:
                 stage(4)
                 print(f"LAUNCH {name}:legendre_analysis_fused:nb{nb}", flush=True)
-        uo, fo, one = p.empty_states(mm), p.empty_states(mm), p.empty_states(1)
+        if me > 1:
+            continue  # (the node kernels' roofline is reported for c3 only)
+        uo, fo, one1 = p.empty_states(mm), p.empty_states(mm), p.empty_states(1)
         b.sweep_nodes(mm, 0, mm, np.ascontiguousarray(coef[:blk]), seq[0], fe, 1, fi, 1, False, uo, fo)
         print(f"LAUNCH {name}:sweep_nodes:nb{mm}", flush=True)
-        b.final_node(mm, np.ascontiguousarray(coef[(kk - 1) * blk:]), seq[0], fe, 1, fi, 1, False, one)
+        b.final_node(mm, np.ascontiguousarray(coef[(kk - 1) * blk:]), seq[0], fe, 1, fi, 1, False, one1)
         print(f"LAUNCH {name}:final_node:nb{mm}", flush=True)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
