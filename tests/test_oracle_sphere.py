@@ -286,10 +286,12 @@ def _p_extended(o):
     return [allp[m : t + 2, m] for m in range(t + 1)]
 
 
-def test_h_recurrence_on_oracle_tables(small):
+@pytest.mark.parametrize("which", ["small", "t42"])
+def test_h_recurrence_on_oracle_tables(which, request):
     """H_n = a_n P_{n-1} + b_n P_{n+1}, a_n = (n+1) eps_n, b_n = -n eps_{n+1}: the identity
     the H-free GPU transforms rest on, checked against the oracle's own H table."""
-    _, o = small
+    fx = request.getfixturevalue(which)
+    o = fx[1] if isinstance(fx, tuple) else fx
     t = o.trunc
     pext = _p_extended(o)
     for m in range(t + 1):
@@ -302,11 +304,13 @@ def test_h_recurrence_on_oracle_tables(small):
         assert np.abs(rec - h).max() <= 1e-13 * max(1.0, np.abs(h).max()), m
 
 
-def test_h_free_f_expl_matches_oracle(small):
+@pytest.mark.parametrize("which", ["small", "t42"])
+def test_h_free_f_expl_matches_oracle(which, request):
     """numpy restatement of the GPU's H-free chain - operand recurrence (k_xsyn_ponly),
     P-only synthesis to degree T+1, grid products, P analyses of A..E to T+1 and the
     assembly (k_assemble_ponly) - equals the oracle's P/H f_E to rounding."""
-    g, o = small
+    fx = request.getfixturevalue(which)
+    o = fx[1] if isinstance(fx, tuple) else fx
     t, a = o.trunc, o.radius
     x = rand_state(o, np.random.default_rng(5), 1e-6)
     phi, zeta, delta = o.views(x)
