@@ -133,6 +133,7 @@ struct Plan {
   int4* cvt_rows;     // [rowsP] xsyn rows of (m,k), (m,k-1), (m,k+1) (-1: none), P-triangle index
   double2* cvt_ab;    // [rowsP] (a_{k+1}, b_{k-1}): weights of X_{k+1}, X_{k-1}
   int4* prep_idx;     // [rowsP] coefficient indices of (m,k), (m,k-1), (m,k+1) (-1: none), m
+  int4* coef_prow;    // [C] P row of (m,n), P row of (m,T+1) when n = T (else -1), n > m, n < T
   int2* asm_pos;      // [C] (extended-triangle index of (m,n), m)
   double2* asm_ab;    // [C] (a_n, b_n)
   int* anal_workP;    // [n_anal_workP] (m << 16 | 64-row block) over the P rows
@@ -576,6 +577,15 @@ cudaError_t launch_analysis_ponly(const Plan& p, const Work& w, double2* fe, int
 // 12-double records): the dSDC stepper's path on H-free plans
 cudaError_t f_expl_states_ponly(const Plan& p, const Work& w, const double2* u, double2* fe, int nb,
                                 cudaStream_t s, int* step_counter);
+// H-free f_E from the P-only operand a node kernel already wrote into w.xsp
+cudaError_t f_expl_operand_ponly(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s);
+// the dSDC sweep's node updates writing f_I and the P-only synthesis operand of the new node
+// states (nodes.cu k_sweep_nodes_po; no node states stored, no operand kernel)
+cudaError_t launch_sweep_nodes_po(const Plan& p, int M, int node_lo, int count, const double* coef_host,
+                                  const double2* u0, const double2* fe, long long fe_stride,
+                                  const double2* fi, long long fi_stride, int first, double2* fi_out,
+                                  double* xsp, cudaStream_t s, int members, long long fe_mstride,
+                                  long long fi_mstride);
 cudaError_t make_gan_maps(Plan& p);
 cudaError_t configure_synthesis_bulk();
 cudaError_t configure_analysis_bulk();

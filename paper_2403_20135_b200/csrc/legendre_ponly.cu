@@ -210,6 +210,15 @@ cudaError_t f_expl_states_ponly(const Plan& p, const Work& w, const double2* u, 
   return e;
 }
 
+cudaError_t f_expl_operand_ponly(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s) {
+  if (!ponly_on(p) || p.own_idx != nullptr || w.xsp == nullptr) return cudaErrorInvalidValue;
+  cudaError_t e = launch_synthesis_bulk_ponly(p, w.fsyn, nullptr, p.T + 1, p.T + 1, w.xsp, nb, s,
+                                              nullptr, SynDst{});
+  if (e == cudaSuccess) e = launch_ring(p, w, nb, s);
+  if (e == cudaSuccess) e = launch_analysis_ponly(p, w, fe, nb, s);
+  return e;
+}
+
 cudaError_t launch_analysis_ponly(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s) {
   cudaError_t e = launch_analysis_bulk_ponly(p, w, nb, s);
   if (e != cudaSuccess) return e;
@@ -232,12 +241,13 @@ static long double eps_l(int n, int m) {
 
 void ponly_free(Plan& p) {
   void* ptrs[] = {p.ptabP, p.ptabP_s, p.rowoffP, p.n_evenP, p.rowP_n, p.moffP, p.cvt_rows, p.prep_idx,
+                  p.coef_prow,
                   p.cvt_ab, p.asm_pos, p.asm_ab, p.anal_workP, p.own_workP, p.xsynP, p.ghat};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   p.ptabP = p.ptabP_s = nullptr;
   p.rowoffP = p.n_evenP = p.rowP_n = p.moffP = p.anal_workP = p.own_workP = nullptr;
-  p.cvt_rows = p.prep_idx = nullptr;
+  p.cvt_rows = p.prep_idx = p.coef_prow = nullptr;
   p.cvt_ab = p.asm_ab = nullptr;
   p.asm_pos = nullptr;
   p.xsynP = p.ghat = nullptr;
@@ -311,6 +321,21 @@ cudaError_t ponly_setup(Plan& p, const double* ptab, const int* rowoff, const in
       tabS[(((size_t)(r / 4) * (J / 8) + j / 8) * 8 + j % 8) * 4 + r % 4] = tabP[(size_t)r * J + j];
   std::vector<int2> apos(C);
   std::vector<double2> aab(C);
+  std::vector<int4> cprow(C);
+  for (int m = 0; m <= T; ++m)
+    for (int r = rowoffP[m]; r < rowoffP[m + 1]; ++r) {
+      const int k = rowP_n[r];
+      if (k < 0) continue;
+      if (k <= T) {
+        int4& c = cprow[moff[m] + k - m];
+        c.x = r;
+        c.z = k > m ? 1 : 0;
+        c.w = k < T ? 1 : 0;
+        if (k < T) c.y = -1;
+      } else {
+        cprow[moff[m] + T - m].y = r;  // the extra degree-(T+1) row, written by (m, T)
+      }
+    }
   for (int m = 0; m <= T; ++m)
     for (int n = m; n <= T; ++n) {
       const int idx = moff[m] + n - m;
@@ -331,10 +356,12 @@ cudaError_t ponly_setup(Plan& p, const double* ptab, const int* rowoff, const in
       (e = up(&p.rowoffP, rowoffP)) != cudaSuccess || (e = up(&p.n_evenP, n_evenP)) != cudaSuccess ||
       (e = up(&p.rowP_n, rowP_n, 16)) != cudaSuccess || (e = up(&p.moffP, moffP)) != cudaSuccess ||
       (e = up(&p.cvt_rows, cvt)) != cudaSuccess || (e = up(&p.cvt_ab, cab)) != cudaSuccess ||
-      (e = up(&p.prep_idx, pidx)) != cudaSuccess ||
+      (e = up(&p.prep_idx, pidx)) != cudaSuccess || (e = up(&p.coef_prow, cprow)) != cudaSuccess ||
       (e = up(&p.asm_pos, apos)) != cudaSuccess || (e = up(&p.asm_ab, aab)) != cudaSuccess ||
       (e = up(&p.anal_workP, work)) != cudaSuccess ||
       (e = cudaMalloc(&p.xsynP, (size_t)p.max_batch * rowsP * kXsynP * sizeof(double))) != cudaSuccess ||
+      // padding rows must read as zero (k_sweep_nodes_po writes valid rows only)
+      (e = cudaMemset(p.xsynP, 0, (size_t)p.max_batch * rowsP * kXsynP * sizeof(double))) != cudaSuccess ||
       (e = cudaMalloc(&p.ghat, (size_t)p.max_batch * CP * kGhat * sizeof(double))) != cudaSuccess ||
       (e = configure_analysis_bulk_ponly()) != cudaSuccess || (e = make_table_map_ponly(p)) != cudaSuccess) {
     ponly_free(p);

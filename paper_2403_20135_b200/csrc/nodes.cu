@@ -214,6 +214,116 @@ __global__ void __launch_bounds__(256) k_sweep_nodes_all(
   if constexpr (RES) resid_block(ra, ss, count);
 }
 
+// ---------------------------------------------------------------------------
+// H-free dSDC sweep (legendre_ponly.cu): the node updates of k_sweep_nodes_all
+// (same rounded arithmetic, bit-identical f_I) writing, instead of the node
+// states, the P-only synthesis operand of the new states - the records
+// k_prep_ponly would build from them, bit for bit.  The record of degree n needs
+// U_H, V_H of degrees n -+ 1, which adjacent threads hold (coefficients of one m
+// are consecutive): each warp owns 30 coefficients and its lanes 0 and 31 are a
+// halo (they update the neighbouring warps' first / last coefficient, store
+// nothing), and the neighbours' values arrive by warp shuffles.  M <= kFuseMaxNodes.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sweep_nodes_po(
+    int C, int M, int lo, int count, NodeArgs cf, const double* __restrict__ u0,
+    const double* __restrict__ fe, long long fe_stride, const double* __restrict__ fi,
+    long long fi_stride, int first, double phibar, const double* __restrict__ lamv,
+    double* fi_out, const double2* __restrict__ xscale, const int4* __restrict__ coef_prow,
+    const double2* __restrict__ cvt_ab, double* __restrict__ xsp, long long fe_mstride,
+    long long fi_mstride) {
+  SDCSW_PDL_ENTRY();
+  constexpr int MX = kFuseMaxNodes;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int idx = gw * 30 + lane - 1;
+  const bool own = lane >= 1 && lane <= 30 && idx < C;
+  const int ic = idx < 0 ? 0 : (idx >= C ? C - 1 : idx);  // halo / tail lanes compute a clamped one
+  // constant plan data before the dependency wait
+  const double lam = lamv[ic];
+  const double2 sc = xscale[ic];
+  const int4 pr = coef_prow[ic];
+  const double2 ab = cvt_ab[pr.x];
+  const double bx = pr.y >= 0 ? cvt_ab[pr.y].y : 0.0;  // b_T of the degree-(T+1) row
+  SDCSW_PDL_WAIT();
+  const int z = blockIdx.z;
+  const int C2 = 2 * C;
+  u0 += (size_t)z * 3 * C2;
+  fe += z * fe_mstride;
+  fi += z * fi_mstride;
+  Tri a0r, a0i;
+  load_tri2(u0, C, ic, a0r, a0i);
+  const Tri f0r = f_impl_tri(a0r, phibar, lam), f0i = f_impl_tri(a0i, phibar, lam);
+  Tri Fr[MX], Fi[MX], Ir[MX], Ii[MX];
+#pragma unroll
+  for (int j = 0; j < MX; ++j)
+    if (j < M) {
+      load_tri2(fe + j * fe_stride, C, ic, Fr[j], Fi[j]);
+      if (first) {
+        Ir[j] = f0r;
+        Ii[j] = f0i;
+      } else {
+        load_tri2(fi + j * fi_stride, C, ic, Ir[j], Ii[j]);
+      }
+    }
+  const int nbt = count * gridDim.z;       // operand batch of the chain
+  const size_t ps = 16 * (size_t)nbt;      // part stride of the P-only records
+  auto rec_of = [&](int r, int b) { return xsp + ((size_t)(r >> 2) * 2 * nbt + b) * 16 + (r & 3) * 4; };
+  for (int q = 0; q < count; ++q) {
+    const int m = lo + q;
+    const int ob = z * count + q;  // output batch entry
+    const double* c = cf.v + m * (M + 4);
+    Tri br = a0r, bi = a0i, fmr = f0r, fmi = f0i;
+#pragma unroll
+    for (int j = 0; j < MX; ++j)
+      if (j < M) {
+        br = axpy_tri(br, c[j], add_tri(Fr[j], Ir[j]));
+        bi = axpy_tri(bi, c[j], add_tri(Fi[j], Ii[j]));
+        if (j == m) {
+          fmr = Ir[j];
+          fmi = Ii[j];
+        }
+      }
+    br = axmy_tri(br, c[M], fmr);
+    bi = axmy_tri(bi, c[M], fmi);
+    const Tri ur = solve_tri(br, c[M + 1], c[M + 2], c[M + 3], lam);
+    const Tri ui = solve_tri(bi, c[M + 1], c[M + 2], c[M + 3], lam);
+    if (own)
+      store_tri2(fi_out + (size_t)ob * 3 * C2, C, idx, f_impl_tri(ur, phibar, lam),
+                 f_impl_tri(ui, phibar, lam));
+    // U_H = sa zeta, V_H = -sa delta (the producers' rounded products); neighbours by shuffle
+    const double sa = sc.y, sm = sc.x;
+    const double uhr = sa * ur.zeta, uhi = sa * ui.zeta, vhr = -sa * ur.delta, vhi = -sa * ui.delta;
+    const double hur = __shfl_down_sync(0xffffffffu, uhr, 1), hui = __shfl_down_sync(0xffffffffu, uhi, 1);
+    const double hvr = __shfl_down_sync(0xffffffffu, vhr, 1), hvi = __shfl_down_sync(0xffffffffu, vhi, 1);
+    const double lur = __shfl_up_sync(0xffffffffu, uhr, 1), lui = __shfl_up_sync(0xffffffffu, uhi, 1);
+    const double lvr = __shfl_up_sync(0xffffffffu, vhr, 1), lvi = __shfl_up_sync(0xffffffffu, vhi, 1);
+    if (own) {
+      double4 p0 = make_double4(sm * ui.delta, -sm * ur.delta, sm * ui.zeta, -sm * ur.zeta);  // U_P, V_P
+      if (pr.w) {  // a_{n+1} (U_H, V_H)(n+1)
+        p0.x = __fma_rn(ab.x, hur, p0.x);
+        p0.y = __fma_rn(ab.x, hui, p0.y);
+        p0.z = __fma_rn(ab.x, hvr, p0.z);
+        p0.w = __fma_rn(ab.x, hvi, p0.w);
+      }
+      if (pr.z) {  // b_{n-1} (U_H, V_H)(n-1)
+        p0.x = __fma_rn(ab.y, lur, p0.x);
+        p0.y = __fma_rn(ab.y, lui, p0.y);
+        p0.z = __fma_rn(ab.y, lvr, p0.z);
+        p0.w = __fma_rn(ab.y, lvi, p0.w);
+      }
+      double* r0 = rec_of(pr.x, ob);
+      *reinterpret_cast<double4*>(r0) = p0;
+      *reinterpret_cast<double4*>(r0 + ps) = make_double4(ur.zeta, ui.zeta, ur.phi, ui.phi);
+      if (pr.y >= 0) {  // n = T: the record of degree T+1 is b_T (U_H, V_H)(T)
+        double* r1 = rec_of(pr.y, ob);
+        *reinterpret_cast<double4*>(r1) = make_double4(__fma_rn(bx, uhr, 0.0), __fma_rn(bx, uhi, 0.0),
+                                                       __fma_rn(bx, vhr, 0.0), __fma_rn(bx, vhi, 0.0));
+        *reinterpret_cast<double4*>(r1 + ps) = make_double4(0.0, 0.0, 0.0, 0.0);
+      }
+    }
+  }
+}
+
 // closing last-node solve, one thread per coefficient (both components)
 __global__ void __launch_bounds__(256) k_final_node_c(
     int C, int M, NodeArgs cf, const double* __restrict__ u0, const double* __restrict__ fe,
@@ -490,6 +600,22 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
                                                      W(u_out), W(fi_out), p.xscale, p.idx_row,
                                                      xsyn_out, fe_mstride * S2, fi_mstride * S2,
                                                      p.rows, chunk, p.own_idx, p.n_own_idx, pwv);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_nodes_po(const Plan& p, int M, int node_lo, int count, const double* coef_host,
+                                  const double2* u0, const double2* fe, long long fe_stride,
+                                  const double2* fi, long long fi_stride, int first, double2* fi_out,
+                                  double* xsp, cudaStream_t s, int members, long long fe_mstride,
+                                  long long fi_mstride) {
+  if (M > kFuseMaxNodes || p.coef_prow == nullptr || xsp == nullptr || p.own_idx != nullptr)
+    return cudaErrorInvalidValue;
+  const long long S2 = 6LL * p.C;
+  const int warps = (p.C + 29) / 30;  // 30 coefficients per warp (+ 2 halo lanes)
+  dim3 grid((warps + 7) / 8, 1, members);
+  launch_k(k_sweep_nodes_po, grid, 256, 0, s, p.C, M, node_lo, count, pack(coef_host, M * (M + 4)),
+           D(u0), D(fe), fe_stride * S2, D(fi), fi_stride * S2, first, p.phibar, p.lam, W(fi_out),
+           p.xscale, p.coef_prow, p.cvt_ab, xsp, fe_mstride * S2, fi_mstride * S2);
   return cudaGetLastError();
 }
 

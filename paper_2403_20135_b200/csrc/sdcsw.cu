@@ -108,6 +108,7 @@ struct sdcsw_stepper {
   int launches;
   size_t nstates;  // state-sized buffers in buf
   int sprep;       // H-free dSDC: f_E builds its P-only operand from the node states (ustage)
+  int nodes_po;    // H-free dSDC: the sweep's node kernel writes the P-only operand itself
   sdcsw_sweep_hook hook;  // per-sweep host callback of sdcsw_stepper_step_hooked (else null)
   void* hook_user;
 };
@@ -957,6 +958,16 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
       for (int g = 0; g < G; ++g) {
         const int lo = g * M / G, hi = (g + 1) * M / G, cnt = hi - lo;
         cudaStream_t sg = (G > 1 && !seq) ? st->side[g] : s;
+        if (sprep && st->nodes_po) {  // H-free: the node kernel writes the P-only operand
+          const Work wk = plan_work(p, lo);
+          e = launch_sweep_nodes_po(p, M, lo, cnt, coef, u, fe_cur, first ? 0 : 1, fi_cur,
+                                    first ? 0 : 1, first, fi_new + lo * S, wk.xsp, sg, E,
+                                    first ? 1 : mS, mS);
+          if (e != cudaSuccess) return e;
+          e = f_expl_operand_ponly(p, wk, fe_new + lo * S, cnt * E, sg);
+          if (e != cudaSuccess) return e;
+          continue;
+        }
         const bool keep = planar || sprep;  // node states stored for an f_E that reads them
         double* xs = keep ? nullptr : st->xsynM + (size_t)lo * E * p.rows * kXsyn;
         // spherical P/H: the node states reach the f_E only as synthesis operands (xs),
@@ -1094,7 +1105,11 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   // P-only synthesis operand from them (k_prep_ponly), instead of writing 12-double
   // operand records that a conversion kernel re-reads (c4: -100 MB per f_E of 256 states)
   const int sprep = mode == 0 && p.kind == 0 && ponly_on(p) && p.own_idx == nullptr ? 1 : 0;
-  const size_t ust = mode == 1 ? 1 : (p.kind == 1 || sprep ? (size_t)E * M : 0);
+  // and with M <= kFuseMaxNodes the sweep's node kernel writes that operand directly
+  // (k_sweep_nodes_po: no node states, no operand kernel; SDCSW_NODES_PO=0 turns it off)
+  int nodes_po = sprep && M <= kFuseMaxNodes ? 1 : 0;
+  if (const char* env = getenv("SDCSW_NODES_PO")) nodes_po = nodes_po && atoi(env) != 0;
+  const size_t ust = mode == 1 ? 1 : (p.kind == 1 || (sprep && !nodes_po) ? (size_t)E * M : 0);
   const size_t nstates = (size_t)E * (1 + 4 * (size_t)M) + ust + (mode == 1 ? (size_t)M + 1 : 0);
   s->nstates = nstates;
   cudaError_t e = cudaSetDevice(p.device);
@@ -1119,6 +1134,7 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   s->fi = q; q += E * M * s->S;
   s->ustage = ust ? q : nullptr; q += ust * s->S;
   s->sprep = sprep;
+  s->nodes_po = nodes_po;
   s->fiB = q; q += E * M * s->S;
   s->feB = q; q += E * M * s->S;
   if (mode == 1) {
@@ -1199,9 +1215,10 @@ int sdcsw_stepper_launches_per_step(sdcsw_stepper* s, int* n) {
   s->launches = s->mode == 0 ? (fused_active(s) ? 3 * s->K : 4 + 4 * G * (s->K - 1))
                              : (serial_fused_active(s) ? 3 + s->K * (2 + 3 * s->M)
                                                        : 3 + s->K * 5 * s->M);
-  // H-free plans: every f_E adds its operand kernel (prep or conversion) and the assembly
+  // H-free plans: every f_E adds its operand kernel (prep or conversion) and the assembly;
+  // with nodes_po the sweeps' operand comes from the node kernel (assembly only)
   if (ponly_on(s->plan->p) && !fused_active(s) && !serial_fused_active(s))
-    s->launches += 2 * (s->mode == 0 ? 1 + G * (s->K - 1) : 1 + s->K * s->M);
+    s->launches += s->mode == 0 ? 2 + (s->nodes_po ? 1 : 2) * G * (s->K - 1) : 2 * (1 + s->K * s->M);
   *n = s->launches;
   return SDCSW_OK;
 }

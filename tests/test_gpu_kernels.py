@@ -961,3 +961,32 @@ def test_ponly_t383_f_expl_vs_oracle():
     o = SphericalShallowWaterOracle(p.grid.trunc, p.grid.nlat, p.grid.nlon)
     assert max(relative_l2(p.f_expl(u), o.f_expl(u), o)) < 1e-10
     p.close()
+
+
+@pytest.mark.parametrize("trunc,m_count,k_count,members", [(255, 4, 3, 1), (127, 4, 2, 6)])
+def test_ponly_node_kernel_operand_bitwise(trunc, m_count, k_count, members):
+    """H-free dSDC: the sweep's node kernel writing the P-only synthesis operand itself
+    (k_sweep_nodes_po, neighbour degrees by warp shuffles across a 30 + 2 halo lane
+    layout) gives bit for bit the result of storing the node states and building the
+    operand from them (k_prep_ponly; SDCSW_NODES_PO=0)."""
+    import torch
+
+    from paper_2403_20135_b200.integrators import DeviceStepper
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    outs = []
+    for po in ("1", "0"):
+        with plan_env(SDCSW_NODES_PO=po, SDCSW_PONLY="1"):
+            p = SphericalShallowWater(trunc, max_batch=m_count * members)
+            cfg = SdcConfig(table=CollocationTable.radau_right(m_count), n_sweeps=k_count,
+                            mode=SweepMode.DIAGONAL_PARALLEL)
+            st = DeviceStepper(p, cfg, 60.0, serial=False, members=members)
+        assert p.uses_ponly
+        u0 = np.stack([random_initial_state(p.grid, 15 + e) for e in range(members)])
+        u = torch.from_numpy(u0).to(p.device).reshape(-1).contiguous()
+        st.run(u, 3)
+        torch.cuda.synchronize()
+        outs.append(u.cpu().numpy())
+        st.close()
+        p.close()
+    assert np.array_equal(outs[0].view(np.uint64), outs[1].view(np.uint64))
