@@ -990,3 +990,32 @@ def test_ponly_node_kernel_operand_bitwise(trunc, m_count, k_count, members):
         st.close()
         p.close()
     assert np.array_equal(outs[0].view(np.uint64), outs[1].view(np.uint64))
+
+
+def test_ponly_stepper_chains_and_sequential_bitwise():
+    """H-free dSDC at T255 (the node kernel writing the P-only operand into each chain's
+    workspace slice): concurrent node chains (2 and 4 graph branches) and sequential node
+    updates give the batched result bit for bit."""
+    import torch
+
+    from paper_2403_20135_b200.integrators import DeviceStepper
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    with plan_env(SDCSW_PONLY="1"):
+        p = SphericalShallowWater(255, max_batch=4)
+    cfg = SdcConfig(table=CollocationTable.radau_right(4), n_sweeps=3,
+                    mode=SweepMode.DIAGONAL_PARALLEL)
+    u0 = torch.from_numpy(random_initial_state(p.grid, 88)).to(p.device).contiguous()
+    outs = []
+    for chains, seq in ((1, False), (2, False), (4, False), (1, True)):
+        st = DeviceStepper(p, cfg, 60.0, serial=False)
+        st.set_chains(chains)
+        st.set_sequential(seq)
+        u = u0.clone()
+        st.run(u, 3)
+        torch.cuda.synchronize()
+        outs.append(u)
+        st.close()
+    for o in outs[1:]:
+        assert torch.equal(outs[0], o)
+    p.close()
