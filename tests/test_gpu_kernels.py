@@ -1019,3 +1019,25 @@ def test_ponly_stepper_chains_and_sequential_bitwise():
     for o in outs[1:]:
         assert torch.equal(outs[0], o)
     p.close()
+
+
+@pytest.mark.parametrize("trunc,nlat,nlon,max_batch", [(210, 320, 768, 3), (301, 448, 768, 2)])
+def test_ponly_odd_sizes_vs_oracle(trunc, nlat, nlon, max_batch):
+    """H-free plans of unusual shape - odd L = T + 1 (211-row TMA store boxes), nlat/2 not a
+    multiple of 64 (two-warp synthesis CTAs), degree-(T+1) rows of odd and even parity -
+    against the CPU oracle with its own tables, for a batch of states."""
+    import torch
+
+    from paper_2403_20135_b200.problem import SphericalShallowWater
+
+    p = SphericalShallowWater(trunc, nlat=nlat, nlon=nlon, max_batch=max_batch)
+    assert p.uses_ponly
+    c = p.n_coef
+    states = np.stack([random_initial_state(p.grid, 120 + b) for b in range(max_batch)])
+    states[:, :c] = 4e-3 * states[:, c : 2 * c] * 1e6
+    u = torch.from_numpy(states).to(p.device).contiguous()
+    out = p.f_expl_device(u, p.empty_states(max_batch), max_batch).cpu().numpy()
+    o = SphericalShallowWaterOracle(p.grid.trunc, p.grid.nlat, p.grid.nlon)
+    for b in (0, max_batch - 1):
+        assert max(relative_l2(out[b], o.f_expl(states[b]), o)) < 1e-10
+    p.close()
