@@ -577,8 +577,9 @@ cudaError_t launch_analysis_ponly(const Plan& p, const Work& w, double2* fe, int
 // 12-double records): the dSDC stepper's path on H-free plans
 cudaError_t f_expl_states_ponly(const Plan& p, const Work& w, const double2* u, double2* fe, int nb,
                                 cudaStream_t s, int* step_counter);
-// H-free f_E from the P-only operand a node kernel already wrote into w.xsp
-cudaError_t f_expl_operand_ponly(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s);
+// H-free f_E from the P-only operand xsp a node kernel already wrote (padding rows zero)
+cudaError_t f_expl_operand_ponly(const Plan& p, const Work& w, const double* xsp, double2* fe, int nb,
+                                 cudaStream_t s);
 // the dSDC sweep's node updates writing f_I and the P-only synthesis operand of the new node
 // states (nodes.cu k_sweep_nodes_po; no node states stored, no operand kernel)
 cudaError_t launch_sweep_nodes_po(const Plan& p, int M, int node_lo, int count, const double* coef_host,

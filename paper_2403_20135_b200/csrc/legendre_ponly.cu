@@ -210,9 +210,10 @@ cudaError_t f_expl_states_ponly(const Plan& p, const Work& w, const double2* u, 
   return e;
 }
 
-cudaError_t f_expl_operand_ponly(const Plan& p, const Work& w, double2* fe, int nb, cudaStream_t s) {
-  if (!ponly_on(p) || p.own_idx != nullptr || w.xsp == nullptr) return cudaErrorInvalidValue;
-  cudaError_t e = launch_synthesis_bulk_ponly(p, w.fsyn, nullptr, p.T + 1, p.T + 1, w.xsp, nb, s,
+cudaError_t f_expl_operand_ponly(const Plan& p, const Work& w, const double* xsp, double2* fe, int nb,
+                                 cudaStream_t s) {
+  if (!ponly_on(p) || p.own_idx != nullptr || xsp == nullptr) return cudaErrorInvalidValue;
+  cudaError_t e = launch_synthesis_bulk_ponly(p, w.fsyn, nullptr, p.T + 1, p.T + 1, xsp, nb, s,
                                               nullptr, SynDst{});
   if (e == cudaSuccess) e = launch_ring(p, w, nb, s);
   if (e == cudaSuccess) e = launch_analysis_ponly(p, w, fe, nb, s);

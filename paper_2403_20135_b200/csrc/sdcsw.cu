@@ -4,6 +4,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cmath>
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <string>
@@ -959,12 +960,14 @@ static cudaError_t enqueue_step(sdcsw_stepper* st, double2* u, cudaStream_t s,
         const int lo = g * M / G, hi = (g + 1) * M / G, cnt = hi - lo;
         cudaStream_t sg = (G > 1 && !seq) ? st->side[g] : s;
         if (sprep && st->nodes_po) {  // H-free: the node kernel writes the P-only operand
-          const Work wk = plan_work(p, lo);
+          // into the stepper's own operand storage (zeroed at creation, written only here,
+          // always with this group's layout: its padding rows stay zero)
+          double* xo = st->xsynM + (size_t)lo * E * p.rowsP * kXsynP;
           e = launch_sweep_nodes_po(p, M, lo, cnt, coef, u, fe_cur, first ? 0 : 1, fi_cur,
-                                    first ? 0 : 1, first, fi_new + lo * S, wk.xsp, sg, E,
+                                    first ? 0 : 1, first, fi_new + lo * S, xo, sg, E,
                                     first ? 1 : mS, mS);
           if (e != cudaSuccess) return e;
-          e = f_expl_operand_ponly(p, wk, fe_new + lo * S, cnt * E, sg);
+          e = f_expl_operand_ponly(p, plan_work(p, lo), xo, fe_new + lo * S, cnt * E, sg);
           if (e != cudaSuccess) return e;
           continue;
         }
@@ -1115,10 +1118,11 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   cudaError_t e = cudaSetDevice(p.device);
   if (e == cudaSuccess) e = cudaMalloc(&s->buf, nstates * s->S * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc(&s->flags, 2 * sizeof(int));
-  const size_t xs = (size_t)p.rows * kXsyn * sizeof(double);
+  // operand records per state: 12-double rows, or (H-free sweeps) 8-double P-only rows
+  const size_t xs = std::max((size_t)p.rows * kXsyn, (size_t)p.rowsP * kXsynP) * sizeof(double);
   if (e == cudaSuccess) e = cudaMalloc(&s->xsyn1, xs * E * (1 + M));
   if (e == cudaSuccess) e = cudaMemset(s->xsyn1, 0, xs * E * (1 + M));
-  s->xsynM = s->xsyn1 ? s->xsyn1 + (size_t)E * p.rows * kXsyn : nullptr;
+  s->xsynM = s->xsyn1 ? s->xsyn1 + xs / sizeof(double) * E : nullptr;
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     if (s->buf) cudaFree(s->buf);
@@ -1353,7 +1357,8 @@ int sdcsw_stepper_sweep_state(sdcsw_stepper* s, int sweep, void** fe0, void** fe
 int sdcsw_stepper_storage(sdcsw_stepper* s, long long* bytes, long long* state_buffers) {
   if (!s) return SDCSW_ERR_STATE;
   const Plan& p = s->plan->p;
-  const long long ops = p.kind == 0 ? (long long)p.rows * kXsyn * sizeof(double) * s->members * (1 + s->M) : 0;
+  const long long rec = (long long)std::max((size_t)p.rows * kXsyn, (size_t)p.rowsP * kXsynP) * sizeof(double);
+  const long long ops = p.kind == 0 ? rec * s->members * (1 + s->M) : 0;
   if (bytes) *bytes = (long long)(s->nstates * s->S * sizeof(double2)) + ops + 2 * (long long)sizeof(int);
   if (state_buffers) *state_buffers = (long long)s->nstates;
   return SDCSW_OK;
