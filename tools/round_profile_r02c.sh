@@ -14,6 +14,6 @@ ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.su
     --clock-control none --csv --log-file gpurun_out/traffic_${tag}.csv \
     python tools/traffic_capture.py c1 c2 c3 > gpurun_out/traffic_capture_${tag}.log 2>&1; echo "traffic rc=$?"
 ncu --profile-from-start off --set full --import-source on --clock-control none \
-    -k regex:"k_synthesis_bulk|k_analysis_bulk_ponly|k_ring|k_xsyn_ponly|k_assemble_ponly" \
+    -k regex:"k_synthesis_bulk|k_analysis_bulk_ponly|k_ring|k_xsyn_ponly|k_prep_ponly|k_assemble_ponly|k_sweep_nodes_po" \
     -o gpurun_out/prof_${tag}_c3 python tools/traffic_capture.py c3 > gpurun_out/ncu_full_${tag}.log 2>&1; echo "full rc=$?"
 ls -la gpurun_out/prof_${tag}_c3.ncu-rep
