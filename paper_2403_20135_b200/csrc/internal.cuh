@@ -268,6 +268,7 @@ constexpr int kXsynP = 8;
 // A, B, C, D (w_s-weighted), E (w_ke-weighted)][re, im] = 20 doubles per j
 constexpr int kSlotsP = 5;
 constexpr int kGhat = 2 * kSlotsP;  // doubles per (extended coefficient, state) of ghat
+constexpr int kGanP = 4 * kSlotsP;  // doubles per (state, m, pair j) of the H-free analysis data
 #if defined(__CUDACC__)
 __host__ __device__
 #endif

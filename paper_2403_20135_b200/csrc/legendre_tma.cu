@@ -790,7 +790,7 @@ static cudaError_t launch_analysis_bulk(const Plan& p, const Work& w, double2* f
 // k-step instead of 9).  The i m factors and the H recurrence are applied by
 // the assembly kernel (legendre_ponly.cu), which needs degrees k - 1 and k + 1.
 // ---------------------------------------------------------------------------
-constexpr int kAnpChunk = kTmaLat * 2 * kGhat;  // five-slot data doubles per state per stage
+constexpr int kAnpChunk = kTmaLat * kGanP;  // five-slot data doubles per state per stage
 template <int NB>
 constexpr size_t anap_smem() {
   return (size_t)kAnbS * (kTileBytes + NB * kAnpChunk * 8) + 8 * kAnbS;
@@ -829,8 +829,8 @@ __global__ void __launch_bounds__(128, SDCSW_ANAB_MINB) k_analysis_bulk_ponly(
   const bool live = rw < rows;
   const bool ev0 = rw < le, ev1 = rw + 8 < le;
   const int nchunks = J / kTmaLat;
-  const double* gsrc = gan + ((size_t)b0 * L + m) * J * 2 * kGhat;
-  const size_t bstride = (size_t)L * J * 2 * kGhat;  // doubles per state
+  const double* gsrc = gan + ((size_t)b0 * L + m) * J * kGanP;
+  const size_t bstride = (size_t)L * J * kGanP;  // doubles per state
 
   auto issue_tables = [&](int ch) {  // thread 0
     const int st = ch % kAnbS;

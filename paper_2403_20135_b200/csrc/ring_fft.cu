@@ -648,11 +648,11 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       }
     } else {
-      double* outp = reinterpret_cast<double*>(gan) + (size_t)b * L * J * 2 * kGhat;
+      double* outp = reinterpret_cast<double*>(gan) + (size_t)b * L * J * kGanP;
       for (int it = threadIdx.x; it < 2 * L; it += THREADS) {
         double2 o[kSlotsP];
         item5(it, o);
-        double2* d = reinterpret_cast<double2*>(outp + (size_t)(it >> 1) * J * 2 * kGhat +
+        double2* d = reinterpret_cast<double2*>(outp + (size_t)(it >> 1) * J * kGanP +
                                                 ganp_off(j, it & 1, 0, 0));
 #pragma unroll
         for (int k = 0; k < kSlotsP; ++k) d[k] = o[k];
