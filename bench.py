@@ -407,6 +407,14 @@ def roofline_of(problem, name, nb, seconds, cfgname, fused=False):
     tname = name + ("_fused" if fused and name == "legendre_analysis" else "")
     roof.update({"kernel": tname, "launch_nb": nb, "us_per_launch": seconds * 1e6,
                  "traffic": measured_traffic(cfgname, tname, nb)})
+    wf = measured_traffic(cfgname, tname, nb, ":smem_wavefronts")
+    if bound == "hbm" and wf:
+        # the ring kernel's own bound is on chip: its shared-memory traffic (ncu wavefronts of
+        # this launch, 128 B each) over the same measured launch time, against 128 B/clk/SM
+        ach_s = wf * 128.0 / seconds / 1e9
+        roof["smem"] = {"achieved": ach_s, "peak": SMEM_PEAK_GBS, "unit": "GB/s",
+                        "frac": ach_s / SMEM_PEAK_GBS, "wavefronts": wf,
+                        "peak_source": "1 wavefront (128 B)/clk/SM (ncu's peak) x 148 SMs x 1965 MHz, nominal"}
     if getattr(problem, "uses_ponly", False) and bound == "tensor":
         roof["transforms"] = ("H-free: P to degree T+1 (stage = operand conversion + P synthesis)"
                               if name == "legendre_synthesis" else
@@ -414,15 +422,22 @@ def roofline_of(problem, name, nb, seconds, cfgname, fused=False):
     return roof
 
 
-def measured_traffic(cfgname, name, nb):
+def measured_traffic(cfgname, name, nb, what=""):
     """DRAM bytes (read + write) per launch of this kernel at this config and
-    batch from an ncu --set full capture (profiles/ncu_traffic_r02.json), or None."""
+    batch from an ncu capture (profiles/ncu_traffic_r02.json), or None; what =
+    ":smem_wavefronts": its shared-memory wavefronts instead."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")
     if not os.path.exists(path):
         return None
     with open(path) as f:
         tr = json.load(f)
-    return tr.get(cfgname, {}).get(f"{name}:nb{nb}")
+    return tr.get(cfgname, {}).get(f"{name}:nb{nb}{what}")
+
+
+# shared-memory bandwidth of the B200: one 128 B wavefront per SM per clock (ncu's peak for
+# l1tex__data_pipe_lsu_wavefronts_mem_shared), 148 SMs at the 1965 MHz clock of this pool
+# (B200_PROFILING.md); MEASURED_PEAKS.json has no shared-memory figure
+SMEM_PEAK_GBS = 148 * 128 * 1.965e9 / 1e9
 
 
 def live_states(stepper, u, n):

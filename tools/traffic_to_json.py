@@ -37,7 +37,7 @@ def main(log, csv_path, out="profiles/ncu_traffic_r02.json"):
     launches = rows(csv_path)
     if len(launches) != len(labels):
         raise SystemExit(f"{len(launches)} profiled launches vs {len(labels)} labels")
-    res = {"source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum of tools/traffic_capture.py "
+    res = {"source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum(,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum) of tools/traffic_capture.py "
                      f"(live states, one launch per label; cold L2 per ncu replay); {csv_path}"}
     for lab, d in zip(labels, launches):
         if lab is None:
@@ -47,6 +47,9 @@ def main(log, csv_path, out="profiles/ncu_traffic_r02.json"):
         r = res.setdefault(cfg, {})
         key = f"{kern}:{nb}"
         r[key] = r.get(key, 0.0) + d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
+        wf = d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")
+        if wf is not None:  # shared-memory wavefronts (128 B each): the on-chip traffic
+            r[key + ":smem_wavefronts"] = r.get(key + ":smem_wavefronts", 0.0) + wf
         r[key + ":kernel"] = (r[key + ":kernel"] + " + " if key + ":kernel" in r else "") + d["kernel"][:80]
         r[key + ":ncu_us"] = r.get(key + ":ncu_us", 0.0) + d.get("gpu__time_duration.sum", 0) / 1e3
     with open(out, "w") as f:
