@@ -274,6 +274,9 @@ __device__ __forceinline__ void pass(double2* Z, const double2* twp, int keep = 
   __syncthreads();
 }
 
+#ifndef SDCSW_RING_P0PAD
+#define SDCSW_RING_P0PAD 1  // zero-padded coefficient staging for the first inverse pass
+#endif
 #ifndef SDCSW_RING_PRUNE
 #define SDCSW_RING_PRUNE 1  // skip the last forward pass's stores of bins the output never reads
                             // (from nlon 768: T255 ring -1.5%, T511 -0.6%; +0.5% at nlon 384)
@@ -465,11 +468,19 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
     constexpr int MAXIT = (ITEMS + THREADS - 1) / THREADS;
     constexpr int SHO = gen_shift<N>(0);
     double2* Fs = Z;
-    const int LS = L + 1;
+    // zero-padded rows (m = L..N/2 hold zeros): the pass reads bin min(k, N - k) for every
+    // k without a branch on the truncation (SDCSW_RING_P0PAD=0: rows of L, masked reads)
+    constexpr int LP = SDCSW_RING_P0PAD ? N / 2 + 1 : 0;
+    const int LS = SDCSW_RING_P0PAD ? LP : L + 1;
     for (int e = threadIdx.x; e < 8 * L; e += THREADS) {  // coalesced
       const int m = e >> 3, fh = e & 7;  // fh = 2 field + hemisphere
       Fs[((fh & 1) * 4 + (fh >> 1)) * LS + m] = Fm(m)[fh];
     }
+    if (SDCSW_RING_P0PAD)
+      for (int e = threadIdx.x; e < 8 * (LP - L); e += THREADS) {
+        const int row = e / (LP - L), m = L + (e - row * (LP - L));
+        Fs[row * LS + m] = make_double2(0.0, 0.0);
+      }
     __syncthreads();
     RT(7)
     double2 v[MAXIT][R];
@@ -483,12 +494,23 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int k = i + r * NR;
-          const bool lo = k <= T, hi = k >= N - T;
-          double2 xn = make_double2(0.0, 0.0), xs = xn;
-          if (lo || hi) {
+          bool lo;
+          double2 xn, xs;
+          if constexpr (SDCSW_RING_P0PAD) {
+            lo = k <= N / 2;
             const int mm = lo ? k : N - k;
             xn = FN[mm];
             xs = FS[mm];
+          } else {
+            lo = k <= T;
+            const bool hi = k >= N - T;
+            xn = make_double2(0.0, 0.0);
+            xs = xn;
+            if (lo || hi) {
+              const int mm = lo ? k : N - k;
+              xn = FN[mm];
+              xs = FS[mm];
+            }
           }
           if (k == 0) xn.y = xs.y = 0.0;
           v[q][r] = lo ? make_double2(xn.x - xs.y, xn.y + xs.x)
