@@ -28,6 +28,9 @@
 #define SDCSW_EXP 0
 #endif
 
+#ifndef SDCSW_TW_ALL
+#define SDCSW_TW_ALL 1  // multiply by the twiddle at k = 0 too (w^0 = 1): no divergent branch
+#endif
 namespace sdcsw {
 #if SDCSW_EXP == 4
 __device__ unsigned long long g_rtimes[1 << 16];
@@ -244,7 +247,7 @@ __device__ __forceinline__ void pass(double2* Z, const double2* twp, int keep = 
       const int k = i % P;
 #pragma unroll
       for (int r = 0; r < R; ++r) v[q][r] = X[pzv(i + r * NR, SHI)];
-      if (P > 1 && k) {
+      if (P > 1 && (SDCSW_TW_ALL || k)) {  // (k = 0: the table holds w^0 = 1)
 #pragma unroll
         for (int r = 1; r < R; ++r) {
           double2 w = twp[(r - 1) * P + k];
@@ -559,7 +562,7 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
           const double2* X = Z + f * NP;
 #pragma unroll
           for (int r = 0; r < 3; ++r) g[f][r] = X[pzv(i + r * N3, SHI)];
-          if (i) {  // twiddles exp(+2 pi i r i / N)
+          if (SDCSW_TW_ALL || i) {  // twiddles exp(+2 pi i r i / N) (i = 0: 1)
 #pragma unroll
             for (int r = 1; r < 3; ++r) {
               double2 w = twp[(r - 1) * N3 + i];
