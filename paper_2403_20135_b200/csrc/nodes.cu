@@ -14,6 +14,7 @@
 // One thread owns one (m, n) coefficient index and its three fields; memory
 // traffic is (1 + 2M) state reads and 2M state writes per sweep.
 #include <climits>
+#include <cstdlib>
 
 #include "node_math.cuh"
 
@@ -567,6 +568,17 @@ cudaError_t launch_solve(const Plan& p, const double* coef_host, const double2* 
   return cudaSuccess;
 }
 
+// threads per CTA of the one-thread-per-coefficient node kernels (experiment knob
+// SDCSW_NODE_THREADS in {64, 128, 256}; the residual variant keeps 256)
+static int node_threads() {
+  static const int t = [] {
+    const char* e = getenv("SDCSW_NODE_THREADS");
+    const int v = e != nullptr ? atoi(e) : 256;
+    return v == 64 || v == 128 || v == 256 ? v : 256;
+  }();
+  return t;
+}
+
 cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, const double* coef_host,
                                const double2* u0, const double2* fe, long long fe_stride,
                                const double2* fi, long long fi_stride, int first, double2* u_out,
@@ -585,11 +597,14 @@ cudaError_t launch_sweep_nodes(const Plan& p, int M, int node_lo, int count, con
              pack(coef_host, M * (M + 4)), D(u0), D(fe), fe_stride * S2, D(fi), fi_stride * S2,
              first, p.phibar, p.lam, W(u_out), W(fi_out), p.xscale, p.idx_row, xsyn_out,
              fe_mstride * S2, fi_mstride * S2, p.rows, chunk, p.own_idx, p.n_own_idx, pwv, rav);
-    else
-      launch_k(k_sweep_nodes_all<false>, grid, 256, 0, s, p.C, M, node_lo, count,
+    else {
+      const int nt = node_threads();
+      grid.x = ((p.own_idx ? p.n_own_idx : p.C) + nt - 1) / nt;
+      launch_k(k_sweep_nodes_all<false>, grid, nt, 0, s, p.C, M, node_lo, count,
              pack(coef_host, M * (M + 4)), D(u0), D(fe), fe_stride * S2, D(fi), fi_stride * S2,
              first, p.phibar, p.lam, W(u_out), W(fi_out), p.xscale, p.idx_row, xsyn_out,
              fe_mstride * S2, fi_mstride * S2, p.rows, chunk, p.own_idx, p.n_own_idx, pwv, rav);
+    }
     return cudaGetLastError();
   }
   dim3 grid = grid_for(p.own_idx ? p.n_own_idx : p.C, count);
@@ -627,8 +642,9 @@ cudaError_t launch_final_node(const Plan& p, int M, const double* coef_host, con
                               const PeerWait* pw) {
   const long long S2 = 6LL * p.C;
   const PeerWait pwv = pw != nullptr ? *pw : PeerWait{nullptr, 0, 0};
-  dim3 grid(((p.own_idx ? p.n_own_idx : p.C) + 255) / 256, 1, members);
-  launch_k(k_final_node_c, grid, 256, 0, s, p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
+  const int nt = node_threads();
+  dim3 grid(((p.own_idx ? p.n_own_idx : p.C) + nt - 1) / nt, 1, members);
+  launch_k(k_final_node_c, grid, nt, 0, s, p.C, M, pack(coef_host, M + 4), D(u0), D(fe),
                                              fe_stride * S2, D(fi), fi_stride * S2, first, p.phibar,
                                              p.lam, W(u_out), diverged, step_counter, p.xscale,
                                              p.idx_row, xsyn_out, fe_mstride * S2, fi_mstride * S2,

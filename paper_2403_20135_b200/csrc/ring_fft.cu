@@ -280,6 +280,10 @@ __device__ __forceinline__ void pass(double2* Z, const double2* twp, int keep = 
 #ifndef SDCSW_RING_P0PAD
 #define SDCSW_RING_P0PAD 1  // zero-padded coefficient staging for the first inverse pass
 #endif
+#ifndef SDCSW_RING_P0DIRECT
+#define SDCSW_RING_P0DIRECT 0  // first inverse pass loads its butterfly inputs straight from the
+                               // Fourier workspace (no shared-memory staging, two barriers fewer)
+#endif
 #ifndef SDCSW_RING_PRUNE
 #define SDCSW_RING_PRUNE 1  // skip the last forward pass's stores of bins the output never reads
                             // (from nlon 768: T255 ring -1.5%, T511 -0.6%; +0.5% at nlon 384)
@@ -475,16 +479,18 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
     // k without a branch on the truncation (SDCSW_RING_P0PAD=0: rows of L, masked reads)
     constexpr int LP = SDCSW_RING_P0PAD ? N / 2 + 1 : 0;
     const int LS = SDCSW_RING_P0PAD ? LP : L + 1;
-    for (int e = threadIdx.x; e < 8 * L; e += THREADS) {  // coalesced
-      const int m = e >> 3, fh = e & 7;  // fh = 2 field + hemisphere
-      Fs[((fh & 1) * 4 + (fh >> 1)) * LS + m] = Fm(m)[fh];
-    }
-    if (SDCSW_RING_P0PAD)
-      for (int e = threadIdx.x; e < 8 * (LP - L); e += THREADS) {
-        const int row = e / (LP - L), m = L + (e - row * (LP - L));
-        Fs[row * LS + m] = make_double2(0.0, 0.0);
+    if constexpr (!SDCSW_RING_P0DIRECT) {
+      for (int e = threadIdx.x; e < 8 * L; e += THREADS) {  // coalesced
+        const int m = e >> 3, fh = e & 7;  // fh = 2 field + hemisphere
+        Fs[((fh & 1) * 4 + (fh >> 1)) * LS + m] = Fm(m)[fh];
       }
-    __syncthreads();
+      if (SDCSW_RING_P0PAD)
+        for (int e = threadIdx.x; e < 8 * (LP - L); e += THREADS) {
+          const int row = e / (LP - L), m = L + (e - row * (LP - L));
+          Fs[row * LS + m] = make_double2(0.0, 0.0);
+        }
+      __syncthreads();
+    }
     RT(7)
     double2 v[MAXIT][R];
 #pragma unroll
@@ -499,7 +505,18 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
           const int k = i + r * NR;
           bool lo;
           double2 xn, xs;
-          if constexpr (SDCSW_RING_P0PAD) {
+          if constexpr (SDCSW_RING_P0DIRECT) {
+            // (field f, m): the N and S values are one 32-byte record of the workspace
+            lo = k <= N / 2;
+            const int mm = lo ? k : N - k;
+            xn = make_double2(0.0, 0.0);
+            xs = xn;
+            if (mm <= T) {
+              const double2* src = Fm(mm) + 2 * f;
+              xn = src[0];
+              xs = src[1];
+            }
+          } else if constexpr (SDCSW_RING_P0PAD) {
             lo = k <= N / 2;
             const int mm = lo ? k : N - k;
             xn = FN[mm];
@@ -522,7 +539,7 @@ __global__ void __launch_bounds__(THREADS, ring_min_blocks<N, THREADS>()) k_ring
         dft<R, true>(v[q]);
       }
     }
-    __syncthreads();
+    if constexpr (!SDCSW_RING_P0DIRECT) __syncthreads();  // (staged inputs read in place)
 #pragma unroll
     for (int q = 0; q < MAXIT; ++q) {
       const int it = threadIdx.x + q * THREADS;
