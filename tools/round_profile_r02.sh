@@ -13,4 +13,4 @@ ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.su
     --clock-control none --csv --log-file gpurun_out/traffic_${tag}.csv \
     python tools/traffic_capture.py c1 c2 c3 > gpurun_out/traffic_capture_${tag}.log 2>&1; echo "traffic rc=$?"
 ncu --profile-from-start off --set full --import-source on --clock-control none \
-    -o gpurun_out/prof_${tag}_stages python tools/traffic_capture.py c1 c2 c3 > gpurun_out/ncu_full_${tag}.log 2>&1; echo "full rc=$?"
+    -o gpurun_out/prof_${tag}_stages python tools/traffic_capture.py ${FULL_CFGS:-c1 c2 c3} > gpurun_out/ncu_full_${tag}.log 2>&1; echo "full rc=$?"
