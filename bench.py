@@ -224,34 +224,39 @@ class CpuPort:
                     pool.shutdown()
         return ctx()
 
-    def rate(self, mode, warm=2, reps=3):
+    def rate(self, mode, warm=2, reps=3, budget_s=3.5):
         """Steps/s of ``mode``: ``warm`` untimed steps, then the minimum over
-        ``reps`` timed single steps (reference bench/harness.py:316, 427-436)."""
+        at least ``reps`` timed single steps, repeated until ``budget_s`` seconds
+        of timed work (reference bench/harness.py:316, 427-436).  Returns
+        (steps/s, timed steps)."""
         with self.stepper(mode) as step:
             u = self.u0
             for _ in range(warm):
                 u = step(u)
-            best = float("inf")
-            for _ in range(reps):
+            best, spent, n = float("inf"), 0.0, 0
+            while n < reps or spent < budget_s:
                 t0 = time.perf_counter()
                 u = step(u)
-                best = min(best, time.perf_counter() - t0)
-        return 1.0 / best
+                dt = time.perf_counter() - t0
+                best, spent, n = min(best, dt), spent + dt, n + 1
+        return 1.0 / best, n
 
 
 def cpu_baseline_modes(cfgname):
     """cpu_baseline of the GPU arm: the three reference modes on the host's physical cores."""
     port = CpuPort(cfgname)
     t0 = time.perf_counter()
-    rates = {mode: port.rate(mode) for mode in CpuPort.MODES}
+    timed = {mode: port.rate(mode) for mode in CpuPort.MODES}
+    rates = {k: v[0] for k, v in timed.items()}
     wall = time.perf_counter() - t0
     c = CONFIGS[cfgname]
     return {
         "value": rates["dsdc_parallel"], "unit": UNIT, "cores": port.cores, "kind": "port",
-        "modes": {k: {"steps_per_s": v, "time_threads": port.threads(k)[0],
+        "modes": {k: {"steps_per_s": v, "timed_steps": timed[k][1], "time_threads": port.threads(k)[0],
                       "blas_threads": port.threads(k)[1]} for k, v in rates.items()},
         "dsdc_parallel_vs_serial": rates["dsdc_parallel"] / rates["serial_sdc"],
-        "sample": (f"per mode 2 warm-up + min of 3 single {cfgname} steps (of {c['steps']}), "
+        "sample": (f"per mode 2 warm-up + min over {min(v[1] for v in timed.values())}-"
+                   f"{max(v[1] for v in timed.values())} single {cfgname} steps (of {c['steps']}; 3.5 s of timed steps per mode), "
                    f"{wall:.1f} s total; oracle/sdc.py (bit-exact restatement of the reference "
                    "integrators) over oracle/sphere_swe.py SphericalShallowWaterFast; "
                    f"{port.cores} physical cores"),
