@@ -375,6 +375,20 @@ int sdcsw_axpy(long long n, const double* x, double w, const double* y, double* 
  * Replaces check_finite (core.py:42-50) without a host round trip. */
 int sdcsw_check_finite(const double* x, long long n, int* flag, void* stream);
 
+/* Bounds check of the library's own device allocations.  With SDCSW_GUARD=1 in
+ * the environment when the library is loaded, every plan / stepper allocation
+ * carries a 64 KiB canary in front and behind; this call synchronises the
+ * device and returns the number of canary bytes any kernel has overwritten
+ * (live allocations now, plus those found when allocations were freed) and the
+ * number of live guarded allocations (-1: guards are off).  The reference has
+ * no counterpart (numpy bounds-checks every index); it stands in for
+ * compute-sanitizer memcheck in the tests (tests/test_gpu_guard.py). */
+int sdcsw_guard_check(long long* corrupted_bytes, int* live_allocations);
+/* Writes one byte past a 256-byte guarded allocation and frees it: with guards
+ * on, the next sdcsw_guard_check reports one more corrupted byte (the proof
+ * that the canaries see an overrun). */
+int sdcsw_guard_selftest(void);
+
 const char* sdcsw_last_error(void);
 int sdcsw_version(void);
 

@@ -71,6 +71,8 @@ EXPORTS = (
     "sdcsw_allgather_rhs",
     "sdcsw_comm_destroy",
     "sdcsw_nccl_version",
+    "sdcsw_guard_check",
+    "sdcsw_guard_selftest",
     "sdcsw_last_error",
     "sdcsw_version",
 )
@@ -163,6 +165,8 @@ _SIGS = {
     "sdcsw_allgather_rhs": [_p, _p, _p, _ll, _p],
     "sdcsw_comm_destroy": [_p],
     "sdcsw_nccl_version": [],
+    "sdcsw_guard_check": [ctypes.POINTER(ctypes.c_longlong), _ip],
+    "sdcsw_guard_selftest": [],
     "sdcsw_last_error": [],
     "sdcsw_version": [],
 }

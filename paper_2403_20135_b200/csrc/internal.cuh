@@ -206,6 +206,17 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 
 // error plumbing
 void set_error(const std::string& msg);
+
+// Device allocations of plans and steppers.  With SDCSW_GUARD=1 in the
+// environment every allocation carries a 64 KiB canary in front and behind,
+// checked when it is freed and by sdcsw_guard_check(): the in-library bounds
+// check for out-of-range stores of the kernels (padding reads stay legal).
+cudaError_t dev_alloc(void** p, size_t bytes);
+cudaError_t dev_free(void* p);
+template <typename T>
+inline cudaError_t dev_alloc(T** p, size_t bytes) {
+  return dev_alloc(reinterpret_cast<void**>(p), bytes);
+}
 int cuda_status(cudaError_t e, const char* where);
 
 // Synthesis B operand ("xsyn"), 12 doubles per (packed table row r, batch

@@ -245,7 +245,7 @@ void ponly_free(Plan& p) {
                   p.coef_prow,
                   p.cvt_ab, p.asm_pos, p.asm_ab, p.anal_workP, p.own_workP, p.xsynP, p.ghat};
   for (void* q : ptrs)
-    if (q) cudaFree(q);
+    if (q) dev_free(q);
   p.ptabP = p.ptabP_s = nullptr;
   p.rowoffP = p.n_evenP = p.rowP_n = p.moffP = p.anal_workP = p.own_workP = nullptr;
   p.cvt_rows = p.prep_idx = p.coef_prow = nullptr;
@@ -256,7 +256,7 @@ void ponly_free(Plan& p) {
 
 template <typename T>
 static cudaError_t up(T** dst, const std::vector<T>& v, size_t pad = 0) {
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), (v.size() + pad) * sizeof(T));
+  cudaError_t e = dev_alloc(dst, (v.size() + pad) * sizeof(T));
   if (e != cudaSuccess) return e;
   if (pad) e = cudaMemset(*dst + v.size(), 0, pad * sizeof(T));
   if (e == cudaSuccess && !v.empty())
@@ -360,10 +360,10 @@ cudaError_t ponly_setup(Plan& p, const double* ptab, const int* rowoff, const in
       (e = up(&p.prep_idx, pidx)) != cudaSuccess || (e = up(&p.coef_prow, cprow)) != cudaSuccess ||
       (e = up(&p.asm_pos, apos)) != cudaSuccess || (e = up(&p.asm_ab, aab)) != cudaSuccess ||
       (e = up(&p.anal_workP, work)) != cudaSuccess ||
-      (e = cudaMalloc(&p.xsynP, (size_t)p.max_batch * rowsP * kXsynP * sizeof(double))) != cudaSuccess ||
+      (e = dev_alloc(&p.xsynP, (size_t)p.max_batch * rowsP * kXsynP * sizeof(double))) != cudaSuccess ||
       // padding rows must read as zero (k_sweep_nodes_po writes valid rows only)
       (e = cudaMemset(p.xsynP, 0, (size_t)p.max_batch * rowsP * kXsynP * sizeof(double))) != cudaSuccess ||
-      (e = cudaMalloc(&p.ghat, (size_t)p.max_batch * CP * kGhat * sizeof(double))) != cudaSuccess ||
+      (e = dev_alloc(&p.ghat, (size_t)p.max_batch * CP * kGhat * sizeof(double))) != cudaSuccess ||
       (e = configure_analysis_bulk_ponly()) != cudaSuccess || (e = make_table_map_ponly(p)) != cudaSuccess) {
     ponly_free(p);
     return e;

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -23,6 +24,69 @@ static bool pdl_default() {
 bool g_pdl = pdl_default();
 
 void set_error(const std::string& msg) { g_error = msg; }
+
+// ---- guarded allocations (SDCSW_GUARD=1) ----------------------------------------
+namespace {
+constexpr size_t kGuardBytes = 64 << 10;
+constexpr unsigned char kGuardFill = 0xA5;
+struct GuardRec {
+  char* base;
+  size_t bytes;
+};
+std::mutex g_guard_mu;
+std::vector<GuardRec> g_guards;
+long long g_guard_bad = 0;  // corrupted canary bytes of allocations already freed
+
+bool guard_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("SDCSW_GUARD");
+    return e != nullptr && e[0] == '1';
+  }();
+  return on;
+}
+
+long long guard_scan(const GuardRec& r) {
+  std::vector<unsigned char> h(2 * kGuardBytes);
+  if (cudaMemcpy(h.data(), r.base, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(h.data() + kGuardBytes, r.base + kGuardBytes + r.bytes, kGuardBytes,
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 2 * (long long)kGuardBytes;
+  long long bad = 0;
+  for (unsigned char c : h) bad += c != kGuardFill;
+  return bad;
+}
+}  // namespace
+
+cudaError_t dev_alloc(void** p, size_t bytes) {
+  if (!guard_on()) return cudaMalloc(p, bytes);
+  char* base = nullptr;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&base), bytes + 2 * kGuardBytes);
+  if (e != cudaSuccess) return e;
+  e = cudaMemset(base, kGuardFill, kGuardBytes);
+  if (e == cudaSuccess) e = cudaMemset(base + kGuardBytes + bytes, kGuardFill, kGuardBytes);
+  if (e != cudaSuccess) {
+    cudaFree(base);
+    return e;
+  }
+  std::lock_guard<std::mutex> lock(g_guard_mu);
+  g_guards.push_back({base, bytes});
+  *p = base + kGuardBytes;
+  return cudaSuccess;
+}
+
+cudaError_t dev_free(void* p) {
+  if (!guard_on() || p == nullptr) return cudaFree(p);
+  std::lock_guard<std::mutex> lock(g_guard_mu);
+  for (size_t i = 0; i < g_guards.size(); ++i) {
+    if (g_guards[i].base + kGuardBytes != p) continue;
+    cudaDeviceSynchronize();
+    g_guard_bad += guard_scan(g_guards[i]);
+    char* base = g_guards[i].base;
+    g_guards.erase(g_guards.begin() + i);
+    return cudaFree(base);
+  }
+  return cudaFree(p);
+}
 
 int cuda_status(cudaError_t e, const char* where) {
   if (e == cudaSuccess) return SDCSW_OK;
@@ -70,7 +134,7 @@ cudaError_t f_expl(Plan& p, const double2* u, double2* fe, int nb, cudaStream_t 
 
 template <typename T>
 static cudaError_t upload(T** dst, const T* src, size_t n, size_t pad = 0) {
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), (n + pad) * sizeof(T));
+  cudaError_t e = dev_alloc(dst, (n + pad) * sizeof(T));
   if (e != cudaSuccess) return e;
   if (pad) cudaMemset(*dst + n, 0, pad * sizeof(T));
   if (n) e = cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice);
@@ -118,6 +182,34 @@ extern "C" {
 
 const char* sdcsw_last_error(void) { return g_error.c_str(); }
 int sdcsw_version(void) { return 1; }
+
+int sdcsw_guard_check(long long* corrupted_bytes, int* live_allocations) {
+  if (!corrupted_bytes || !live_allocations) {
+    set_error("sdcsw_guard_check: null argument");
+    return SDCSW_ERR_PARAM;
+  }
+  if (!guard_on()) {
+    *corrupted_bytes = 0;
+    *live_allocations = -1;
+    return SDCSW_OK;
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_status(e, "sdcsw_guard_check");
+  std::lock_guard<std::mutex> lock(g_guard_mu);
+  long long bad = g_guard_bad;
+  for (const GuardRec& r : g_guards) bad += guard_scan(r);
+  *corrupted_bytes = bad;
+  *live_allocations = (int)g_guards.size();
+  return SDCSW_OK;
+}
+
+int sdcsw_guard_selftest(void) {
+  unsigned char* q = nullptr;
+  cudaError_t e = dev_alloc(&q, 256);
+  if (e == cudaSuccess) e = cudaMemset(q + 255, 0, 2);  // the second byte is out of bounds
+  if (e == cudaSuccess) e = dev_free(q);
+  return cuda_status(e, "sdcsw_guard_selftest");
+}
 
 int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_north,
                       const double* w_north, const double* ptab, const double* htab,
@@ -276,21 +368,21 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
       (e = upload(&p.inv_nn, inv_nn.data(), inv_nn.size())) != cudaSuccess ||
       (e = upload(&p.xscale, xscale.data(), xscale.size())) != cudaSuccess ||
       (e = upload(&p.idx_row, idx_row.data(), idx_row.size())) != cudaSuccess ||
-      (e = cudaMalloc(&p.xsyn, (size_t)p.rows * p.max_batch * kXsyn * sizeof(double))) != cudaSuccess ||
+      (e = dev_alloc(&p.xsyn, (size_t)p.rows * p.max_batch * kXsyn * sizeof(double))) != cudaSuccess ||
       (e = upload(&p.mu, mu_north, (size_t)J)) != cudaSuccess ||
       (e = upload(&p.wsyn, wsyn.data(), wsyn.size())) != cudaSuccess ||
       (e = upload(&p.wke, wke.data(), wke.size())) != cudaSuccess ||
       (e = upload(&p.twiddle, twp.data(), twp.size())) != cudaSuccess ||
       (e = upload(&p.anal_work, work.data(), work.size())) != cudaSuccess ||
       (e = upload(&p.anal_work4, work4.data(), work4.size())) != cudaSuccess ||
-      (e = cudaMalloc(&p.fsyn, (size_t)p.max_batch * J * p.L * 8 * sizeof(double2))) != cudaSuccess ||
-      (e = cudaMalloc(&p.gan, (size_t)p.max_batch * J * p.L * kNumSlots * 2 * sizeof(double2))) !=
+      (e = dev_alloc(&p.fsyn, (size_t)p.max_batch * J * p.L * 8 * sizeof(double2))) != cudaSuccess ||
+      (e = dev_alloc(&p.gan, (size_t)p.max_batch * J * p.L * kNumSlots * 2 * sizeof(double2))) !=
           cudaSuccess ||
-      (e = cudaMalloc(&p.coef_dev, kCoefCap * sizeof(double))) != cudaSuccess ||
+      (e = dev_alloc(&p.coef_dev, kCoefCap * sizeof(double))) != cudaSuccess ||
       // residual sweeps: [6 nodes x 3 fields][blocks] partials + last-block counter,
       // allocated here so the opt-in call never allocates (or is half-built) under capture
-      (e = cudaMalloc(&p.resid_part, 18 * (size_t)((C + 255) / 256) * sizeof(double))) != cudaSuccess ||
-      (e = cudaMalloc(&p.resid_count, sizeof(unsigned))) != cudaSuccess ||
+      (e = dev_alloc(&p.resid_part, 18 * (size_t)((C + 255) / 256) * sizeof(double))) != cudaSuccess ||
+      (e = dev_alloc(&p.resid_count, sizeof(unsigned))) != cudaSuccess ||
       (e = cudaMemset(p.resid_count, 0, sizeof(unsigned))) != cudaSuccess ||
       (e = configure_ring(p.ring_smem)) != cudaSuccess ||
       (e = configure_synthesis()) != cudaSuccess ||
@@ -305,7 +397,7 @@ int sdcsw_plan_create(int device, const sdcsw_config* cfg, const double* mu_nort
                     p.xscale, p.idx_row, p.xsyn, p.anal_work4, p.ptab_a, p.htab_a,
                     p.ptab_s, p.htab_s, p.resid_part, p.resid_count};
     for (void* q : ptrs)
-      if (q) cudaFree(q);
+      if (q) dev_free(q);
     delete h;
     return st;
   }
@@ -358,13 +450,13 @@ int sdcsw_plan_destroy(sdcsw_plan* h) {
   ponly_free(p);
   for (void* q : {(void*)p.m_part, (void*)p.m_k, (void*)p.own_m, (void*)p.own_work, (void*)p.own_idx,
                   (void*)p.own_workP})
-    if (q) cudaFree(q);
+    if (q) dev_free(q);
   void* ptrs[] = {p.ptab, p.htab, p.rowoff, p.n_even, p.row_n, p.moff, p.lam, p.inv_nn, p.mu,
                   p.wsyn, p.wke, p.twiddle, p.anal_work, p.fsyn, p.gan, p.coef_dev,
                   p.xscale, p.idx_row, p.xsyn, p.anal_work4, p.pkx, p.pky, p.ptw, p.pw1, p.pw2,
                   p.ptab_a, p.htab_a, p.ptab_s, p.htab_s, p.resid_part, p.resid_count};
   for (void* q : ptrs)
-    if (q) cudaFree(q);
+    if (q) dev_free(q);
   h->alive = false;
   delete h;
   return SDCSW_OK;
@@ -413,14 +505,14 @@ int sdcsw_plan_create_planar(int device, const sdcsw_planar_config* cfg, const d
       (e = upload(&p.pky, ky, (size_t)p.pnh)) != cudaSuccess ||
       (e = upload(&p.lam, lam, (size_t)p.C)) != cudaSuccess ||
       (e = upload(&p.ptw, tw.data(), tw.size())) != cudaSuccess ||
-      (e = cudaMalloc(&p.pw1, 4 * wbytes)) != cudaSuccess ||
-      (e = cudaMalloc(&p.pw2, 5 * wbytes)) != cudaSuccess ||
-      (e = cudaMalloc(&p.coef_dev, kCoefCap * sizeof(double))) != cudaSuccess ||
+      (e = dev_alloc(&p.pw1, 4 * wbytes)) != cudaSuccess ||
+      (e = dev_alloc(&p.pw2, 5 * wbytes)) != cudaSuccess ||
+      (e = dev_alloc(&p.coef_dev, kCoefCap * sizeof(double))) != cudaSuccess ||
       (e = configure_planar(n)) != cudaSuccess) {
     const int st = cuda_status(e, "sdcsw_plan_create_planar");
     for (void* q : {(void*)p.pkx, (void*)p.pky, (void*)p.lam, (void*)p.ptw, (void*)p.pw1,
                     (void*)p.pw2, (void*)p.coef_dev})
-      if (q) cudaFree(q);
+      if (q) dev_free(q);
     delete h;
     return st;
   }
@@ -674,7 +766,7 @@ int sdcsw_plan_set_split(sdcsw_plan* h, int S, int sp, void* fourier, long long 
   cudaSetDevice(p.device);
   cudaDeviceSynchronize();
   for (int** q : {&p.m_part, &p.m_k, &p.own_m, &p.own_work, &p.own_idx, &p.own_workP}) {
-    if (*q) cudaFree(*q);
+    if (*q) dev_free(*q);
     *q = nullptr;
   }
   p.n_own_workP = 0;
@@ -1116,18 +1208,18 @@ int sdcsw_stepper_create_ensemble(sdcsw_plan* h, int mode, int n_nodes, int n_sw
   const size_t nstates = (size_t)E * (1 + 4 * (size_t)M) + ust + (mode == 1 ? (size_t)M + 1 : 0);
   s->nstates = nstates;
   cudaError_t e = cudaSetDevice(p.device);
-  if (e == cudaSuccess) e = cudaMalloc(&s->buf, nstates * s->S * sizeof(double2));
-  if (e == cudaSuccess) e = cudaMalloc(&s->flags, 2 * sizeof(int));
+  if (e == cudaSuccess) e = dev_alloc(&s->buf, nstates * s->S * sizeof(double2));
+  if (e == cudaSuccess) e = dev_alloc(&s->flags, 2 * sizeof(int));
   // operand records per state: 12-double rows, or (H-free sweeps) 8-double P-only rows
   const size_t xs = std::max((size_t)p.rows * kXsyn, (size_t)p.rowsP * kXsynP) * sizeof(double);
-  if (e == cudaSuccess) e = cudaMalloc(&s->xsyn1, xs * E * (1 + M));
+  if (e == cudaSuccess) e = dev_alloc(&s->xsyn1, xs * E * (1 + M));
   if (e == cudaSuccess) e = cudaMemset(s->xsyn1, 0, xs * E * (1 + M));
   s->xsynM = s->xsyn1 ? s->xsyn1 + xs / sizeof(double) * E : nullptr;
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
-    if (s->buf) cudaFree(s->buf);
-    if (s->flags) cudaFree(s->flags);
-    if (s->xsyn1) cudaFree(s->xsyn1);
+    if (s->buf) dev_free(s->buf);
+    if (s->flags) dev_free(s->flags);
+    if (s->xsyn1) dev_free(s->xsyn1);
     delete s;
     return cuda_status(e, "sdcsw_stepper_create");
   }
@@ -1198,9 +1290,9 @@ int sdcsw_stepper_destroy(sdcsw_stepper* s) {
   if (s->prof_ready)
     for (int i = 0; i < s->K + 2; ++i) cudaEventDestroy(s->prof[i]);
   cudaStreamDestroy(s->cap);
-  cudaFree(s->buf);
-  cudaFree(s->flags);
-  cudaFree(s->xsyn1);
+  dev_free(s->buf);
+  dev_free(s->flags);
+  dev_free(s->xsyn1);
   delete s;
   return SDCSW_OK;
 }

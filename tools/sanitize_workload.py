@@ -10,8 +10,8 @@ round-1 advisor asked for), planar.  Default: all.
 
 compute-sanitizer is closed on this round's GPU pool (every tool exits at once with "closed on
 this pool"; gpurun of 2026-10-21), so this script has only run plain there (all parts finite);
-the out-of-bounds cases the advisor named are covered by the bitwise GPU tests with
-max_batch == nb (tests/test_gpu_kernels.py)."""
+its stand-in is the library's own canary check: SDCSW_GUARD=1 python tools/sanitize_workload.py
+prints the canary bytes overwritten after every part (tests/test_gpu_guard.py asserts 0)."""
 import os
 import sys
 
@@ -72,10 +72,13 @@ def latency():
 
 def hfree():
     # ensemble-sized T127 plans: bulk synthesis in batch blocks with partial tails
-    for nb in (16, 25):
+    base = None
+    for nb in (16, 25, 256):  # 256 = the c4 batch (64 members x 4 nodes), 256 % 6 = 4
         p = SphericalShallowWater(127, max_batch=nb)
         assert p.uses_ponly
-        st = np.stack([random_initial_state(p.grid, b) for b in range(nb)])
+        if base is None:
+            base = [random_initial_state(p.grid, b) for b in range(25)]
+        st = np.stack([base[b % 25] for b in range(nb)])
         u = torch.from_numpy(st).to(p.device)
         o = p.empty_states(nb)
         for n in (nb, nb - 3, 1):
@@ -124,8 +127,26 @@ def planar():
     st.close()
 
 
+def guard_report():
+    """Canary bytes overwritten so far (SDCSW_GUARD=1; include/sdcsw.h sdcsw_guard_check)."""
+    import ctypes
+
+    from paper_2403_20135_b200 import _native
+
+    bad, live = ctypes.c_longlong(), ctypes.c_int()
+    _native.check(_native.lib().sdcsw_guard_check(ctypes.byref(bad), ctypes.byref(live)), "guard")
+    return bad.value, live.value
+
+
 if __name__ == "__main__":
     parts = sys.argv[1:] or ["latency", "hfree", "planar"]
     for name in parts:
         {"latency": latency, "hfree": hfree, "planar": planar}[name]()
+        print(f"guard after {name}: corrupted_bytes={guard_report()[0]}", flush=True)
+    if os.environ.get("SDCSW_GUARD") == "1":
+        from paper_2403_20135_b200 import _native
+
+        before = guard_report()[0]
+        _native.check(_native.lib().sdcsw_guard_selftest(), "selftest")
+        print(f"guard selftest: +{guard_report()[0] - before} corrupted byte(s)", flush=True)
     print("sanitize workload done", flush=True)
