@@ -3,7 +3,8 @@
 Builds libsdcsw.so with -DSDCSW_MUTATE_UCHI=1 (the i m chi term of U gets the
 wrong sign in every synthesis-operand writer) into a scratch directory and
 prints, as one JSON line, the worst known-answer-flow error of that library
-and of the default one.  ``python tools/kat_mutation.py [--eval LIB]``
+and of the default one, plus each library's energy / potential-enstrophy drift
+over 6 dSDC steps at T63 (tests/sphere_invariants.py).  ``python tools/kat_mutation.py [--eval LIB]``
 (GPU; --eval is the per-library child process)."""
 
 import json
@@ -35,6 +36,23 @@ def evaluate():
         fe, fi = p.f_expl(x), p.f_impl(x)
         e = field_errors(o, fe + fi, want, [fe, fi])
         out[name] = float(max(e[:2]) if name.startswith("rossby") else max(e))
+    # conservation over a short run on the device stepper (tests/sphere_invariants.py)
+    import torch
+
+    from paper_2403_20135_b200 import CollocationTable, SdcConfig, SweepMode, random_initial_state
+    from paper_2403_20135_b200.integrators import DeviceStepper
+    from sphere_invariants import drifts
+
+    u0 = random_initial_state(p.grid, seed=1)
+    cfg = SdcConfig(table=CollocationTable.radau_right(3), n_sweeps=3, mode=SweepMode.DIAGONAL_PARALLEL)
+    st = DeviceStepper(p, cfg, 120.0, serial=False)
+    u = torch.from_numpy(u0).to(p.device).reshape(-1).contiguous()
+    st.run(u, 6, use_graph=False)
+    torch.cuda.synchronize()
+    d = drifts(o, u0, u.cpu().numpy())
+    out["energy_drift_6_steps"] = float(d["energy"])
+    out["enstrophy_drift_6_steps"] = float(d["potential_enstrophy"])
+    st.close()
     p.close()
     print(json.dumps(out))
 
