@@ -25,7 +25,7 @@ def evaluate():
     from paper_2403_20135_b200.problem import SphericalShallowWater
     from sphere_kats import field_errors, rossby_haurwitz, tilted_potential, tilted_rotation
 
-    p = SphericalShallowWater(63, max_batch=2)
+    p = SphericalShallowWater(63, max_batch=3)
     o = SphericalShallowWaterOracle(63, p.grid.nlat, p.grid.nlon)
     out = {}
     for name, fn in (("rotation_a45", lambda o: tilted_rotation(o, np.pi / 4)),
