@@ -574,11 +574,12 @@ def integrate(problem, initial_state, dt, n_steps, stepper, checkpoint_interval=
                 f"{stepper.name} diverged at step {bad} of {n_steps} (t = {bad * dt:g})",
                 step_index=bad,
             ) from NumericalError("non-finite state on device", component=comp)
-        for _ in range(seg):
-            reports.append(StepReport(wall, 0.0, (0.0,) * n_sw, 0.0, *per))
+        # one (immutable) report shared by the segment's steps: they replayed as graphs and
+        # carry the same averaged wall time
+        reports.extend([StepReport(wall, 0.0, (0.0,) * n_sw, 0.0, *per)] * seg)
         done = stop_at
         times.append(done * dt)
-        states.append(u.cpu().numpy().copy())
+        states.append(u.cpu().numpy())  # (a fresh host buffer, owned by the checkpoint)
     return Trajectory(stepper.name, dt, n_steps, times, states, reports)
 
 
