@@ -6,7 +6,10 @@ problem, ``SPEC.md:8``); it is pinned by analytic known-answer tests in
 ``tests/test_oracle_sphere.py`` - including the m > 0 flows of
 ``tests/sphere_kats.py`` (tilted solid-body rotation, tilted potential flow,
 Rossby-Haurwitz wave 4) with a sign-mutation check of every wind-synthesis
-term - and the reference contracts ``pkg/tests/_contracts.py:18-41``.
+term - by the conservation laws of the continuous equations over whole runs
+(``tests/sphere_invariants.py``: energy, angular momentum, potential
+enstrophy; eight single-term sign mutants fail them) and by the reference
+contracts ``pkg/tests/_contracts.py:18-41``.
 :class:`SphericalShallowWaterFast` (end of file) is the same problem with the
 transforms organised for speed; it is the CPU baseline ``bench.py`` times.
 
