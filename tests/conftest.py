@@ -26,3 +26,22 @@ def reference():
 
     return parsdc
 
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """SDCSW_GUARD=1 python -m pytest tests -m gpu: the whole suite runs with canaries around
+    every device allocation of the library (include/sdcsw.h sdcsw_guard_check); any canary
+    byte a kernel overwrote fails the session."""
+    if os.environ.get("SDCSW_GUARD") != "1":
+        return
+    import ctypes
+
+    from paper_2403_20135_b200 import _native
+
+    if _native._LIB is None:
+        return
+    bad, live = ctypes.c_longlong(), ctypes.c_int()
+    rc = _native._LIB.sdcsw_guard_check(ctypes.byref(bad), ctypes.byref(live))
+    print(f"\n[sdcsw guard] rc={rc} corrupted_bytes={bad.value} live_allocations={live.value}")
+    if rc != 0 or bad.value != 0:
+        session.exitstatus = 1
